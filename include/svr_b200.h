@@ -1,0 +1,240 @@
+/*
+ * svr_b200.h — C ABI of the B200-native sparse-voxel rasterizer.
+ *
+ * This is the drop-in boundary for the render and gradient path of the
+ * reference C++ toolkit (`proj/include/svr/raster.hpp:52-141`,
+ * `proj/src/raster.cpp`). Every entry point takes plain pointers and sizes;
+ * no C++ or torch types cross it. The C++ API of the reference
+ * (`svr::render`, `svr::render_with_pools`, `svr::render_backward`,
+ * `svr::project_voxel`, `svr::tile_sign_patterns`, `svr::build_sort_entries`,
+ * `svr::sort_entries`) is re-implemented on top of this ABI in
+ * `paper_2412_04459_b200/cpp/raster_dropin.cpp`; see INTEGRATION.md.
+ *
+ * Errors: every function returns an svr_status. On failure a thread-local
+ * message is available from svr_last_error(). The status codes map 1:1 onto
+ * the exception types the reference throws:
+ *   SVR_ERR_INVALID_ARGUMENT -> std::invalid_argument (raster.cpp:207-211,
+ *                               octree.hpp:47-49/54-55/71-72)
+ *   SVR_ERR_LENGTH           -> std::length_error     (raster.cpp:146-150)
+ *   SVR_ERR_RUNTIME          -> std::runtime_error    (raster.cpp:329-332)
+ * SVR_ERR_CUDA / SVR_ERR_NO_DEVICE have no reference counterpart (the
+ * reference never touches a GPU); there is no CPU fallback.
+ */
+#ifndef SVR_B200_H
+#define SVR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SVR_ABI_VERSION 1
+
+typedef enum svr_status {
+    SVR_OK = 0,
+    SVR_ERR_INVALID_ARGUMENT = 1,
+    SVR_ERR_LENGTH = 2,
+    SVR_ERR_RUNTIME = 3,
+    SVR_ERR_CUDA = 4,
+    SVR_ERR_NO_DEVICE = 5
+} svr_status;
+
+/* Limits of the reference (raster.hpp:18-20, scene.hpp:19, octree.hpp:16). */
+#define SVR_TILE_SIZE 16
+#define SVR_TILE_ID_BITS 16
+#define SVR_VOXEL_ID_BITS 29
+#define SVR_MAX_LEVEL 16
+
+typedef struct svr_ctx svr_ctx;     /* one per (host thread, device): stream + arenas */
+typedef struct svr_scene svr_scene; /* device-resident SparseScene                     */
+typedef struct svr_frame svr_frame; /* device-resident per-view state (ForwardRecords) */
+
+/* svr::Camera (camera.hpp:13-49). rot is the row-major camera-to-world
+ * rotation, pos the camera centre. */
+typedef struct svr_camera {
+    int32_t width, height;
+    double fx, fy, cx, cy;
+    double rot[9];
+    double pos[3];
+} svr_camera;
+
+/* svr::RenderOptions (raster.hpp:22-31). */
+typedef struct svr_render_options {
+    int32_t K;              /* samples per voxel, 1..3            */
+    double t_threshold;     /* early-termination transmittance    */
+    double supersample;     /* >= 1                               */
+    double background[3];
+    double near_plane;
+    double far_sentinel;
+    int32_t record_stats;   /* per-voxel max blending weight      */
+    int32_t training;       /* keep forward records for backward  */
+} svr_render_options;
+
+/* svr::SparseScene (scene.hpp:21-46), host arrays. */
+typedef struct svr_scene_desc {
+    uint64_t n_voxels;
+    uint64_t n_pool;
+    int32_t sh_degree;               /* 0..3                              */
+    double bounds_center[3];
+    double bounds_size;
+    const uint64_t* codes;           /* OctPath.code, 48-bit left aligned */
+    const uint8_t* levels;           /* OctPath.level, 1..16              */
+    const uint32_t* corner_index;    /* [n_voxels][8]                     */
+    const float* density;            /* [n_pool]                          */
+    const float* sh;                 /* [n_voxels][3*(deg+1)^2]           */
+} svr_scene_desc;
+
+/* Per-view summary (one device->host read). */
+typedef struct svr_frame_info {
+    int32_t width, height;        /* target resolution            */
+    int32_t ss_width, ss_height;  /* supersampled render grid     */
+    int32_t tiles_x, tiles_y;
+    uint64_t n_visible;           /* |pre| (raster.cpp:217)       */
+    uint64_t n_entries;           /* E   (raster.cpp:218)         */
+    uint64_t n_contribs;          /* training only                */
+    int32_t sort_passes;          /* radix passes the sort ran    */
+    int32_t training;
+} svr_frame_info;
+
+/* Buffers a frame exposes (svr_frame_download / svr_frame_device_ptr).
+ * Images are row-major with interleaved channels, float32, exactly the
+ * svr::Image layout (image.hpp:10-26) narrowed to f32. */
+typedef enum svr_buffer {
+    SVR_BUF_COLOR = 0,         /* W*H*3   f32                            */
+    SVR_BUF_DEPTH = 1,         /* W*H     f32                            */
+    SVR_BUF_MEDIAN_DEPTH = 2,  /* W*H     f32                            */
+    SVR_BUF_NORMAL = 3,        /* W*H*3   f32                            */
+    SVR_BUF_TRANSMITTANCE = 4, /* W*H     f32                            */
+    SVR_BUF_MAX_BLEND = 5,     /* n_voxels f32 (record_stats)           */
+    SVR_BUF_SS_COLOR = 6,      /* sw*sh*3 f32                            */
+    SVR_BUF_SS_DEPTH = 7,      /* sw*sh   f32                            */
+    SVR_BUF_SS_TFIN = 8,       /* sw*sh   f32                            */
+    SVR_BUF_SORT_KEYS = 9,     /* E u64, sorted SortEntry::key           */
+    SVR_BUF_SORT_VALUES = 10,  /* E u32, sorted SortEntry::value         */
+    SVR_BUF_TILE_RANGES = 11,  /* tiles*2 u32, [lo,hi) per tile          */
+    SVR_BUF_TILE_MASKS = 12,   /* tiles u8, bit s set iff pattern s used */
+    SVR_BUF_VOXEL_RECTS = 13,  /* n_voxels*4 i32 (tx0,tx1,ty0,ty1); tx1<tx0 => culled */
+    SVR_BUF_VOXEL_AABB = 14,   /* n_voxels*4 f64 (x0,x1,y0,y1), exact    */
+    SVR_BUF_ENTRIES_KEYS = 15,   /* E u64 in emission order (debug mode) */
+    SVR_BUF_ENTRIES_VALUES = 16, /* E u32 in emission order (debug mode) */
+    SVR_BUF_PIX_COUNT = 17,    /* sw*sh u32 (training)                   */
+    SVR_BUF_PIX_BEGIN = 18,    /* sw*sh u32 (training)                   */
+    SVR_BUF_VOXEL_COLOR = 19,  /* n_voxels*3 f32 (visible voxels only)   */
+    SVR_BUF_VOXEL_NORMAL = 20  /* n_voxels*3 f32 (visible voxels only)   */
+} svr_buffer;
+
+/* ---- context ---------------------------------------------------------- */
+const char* svr_last_error(void);
+int svr_abi_version(void);
+int svr_ctx_create(int device, svr_ctx** out);
+int svr_ctx_destroy(svr_ctx* ctx);
+/* cudaStream_t the context launches on (for event timing by the caller). */
+void* svr_ctx_stream(svr_ctx* ctx);
+int svr_ctx_synchronize(svr_ctx* ctx);
+/* debug != 0 keeps the pre-sort entry list so it can be dumped bit-exactly. */
+int svr_ctx_set_debug(svr_ctx* ctx, int debug);
+
+/* ---- scene ------------------------------------------------------------ */
+/* Validates levels/paths like to_voxel_index (octree.hpp:68-82) and uploads. */
+int svr_scene_upload(svr_ctx* ctx, const svr_scene_desc* desc, svr_scene** out);
+/* Refresh the parameter pools (PoolsD, raster.hpp:47-52) without touching
+ * the geometry. on_device != 0: pointers are device pointers. Either may be
+ * NULL to keep the current values. */
+int svr_scene_set_params(svr_ctx* ctx, svr_scene* scene, const float* density, const float* sh,
+                         int on_device);
+int svr_scene_destroy(svr_scene* scene);
+/* Device pointers of the parameter pools (for optimisers living on device). */
+int svr_scene_param_ptrs(svr_scene* scene, float** density, float** sh, uint64_t* n_pool,
+                         uint64_t* n_sh);
+
+/* ---- forward (raster.cpp:205-301) ------------------------------------- */
+int svr_frame_create(svr_ctx* ctx, svr_frame** out);
+int svr_frame_destroy(svr_frame* frame);
+/* Renders `cam` into `frame` (buffers are reused across calls). Throws the
+ * reference's invalid_argument / length_error conditions as status codes. */
+int svr_render(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam,
+               const svr_render_options* opts, svr_frame* frame);
+int svr_frame_get_info(svr_frame* frame, svr_frame_info* out);
+/* Copies a buffer to host memory (synchronous). bytes must match. */
+int svr_frame_download(svr_frame* frame, svr_buffer which, void* dst, size_t bytes);
+/* Device pointer + size of a buffer (no copy, valid until the next render). */
+int svr_frame_device_ptr(svr_frame* frame, svr_buffer which, void** ptr, size_t* bytes);
+
+/* ForwardRecords materialisation (raster.hpp:72-82): visible voxel ids in
+ * `pre` order, and per contribution the pre index plus the ray segment. */
+int svr_frame_records(svr_frame* frame, uint32_t* pre_vids, uint64_t n_pre,
+                      uint32_t* contrib_pre, double* contrib_a, double* contrib_b,
+                      uint64_t n_contribs);
+
+/* ---- backward (raster.cpp:303-423) ------------------------------------ */
+typedef struct svr_upstream {
+    const float* d_color;        /* W*H*3 or NULL   */
+    const float* d_depth;        /* W*H   or NULL   */
+    const float* d_normal;       /* W*H*3 or NULL   */
+    const float* d_tfin_ss;      /* sw*sh or NULL   */
+    const float* d_weight;       /* n_contribs or NULL  */
+    const float* d_voxel_color;  /* n_contribs*3 or NULL */
+    uint64_t n_d_weight;         /* element counts for the size checks */
+    uint64_t n_d_voxel_color;    /* (in Vec3 units)                     */
+    int32_t on_device;           /* pointers are device pointers        */
+} svr_upstream;
+
+typedef struct svr_gradients {
+    float* density;   /* n_pool                */
+    float* sh;        /* n_voxels*stride       */
+    float* priority;  /* n_voxels              */
+    int32_t on_device;
+} svr_gradients;
+
+int svr_render_backward(svr_ctx* ctx, const svr_scene* scene, svr_frame* frame,
+                        const svr_upstream* up, svr_gradients* out);
+
+/* L1 photometric loss on the rendered colour (new; pattern of mse_loss,
+ * losses.cpp:121-131): L = mean|C-gt|, dL/dC = sign(C-gt)/(3WH). gt is a
+ * device pointer (W*H*3 f32); d_color (device, W*H*3) receives the gradient;
+ * loss (device, 1 f32) may be NULL. */
+int svr_l1_loss(svr_ctx* ctx, svr_frame* frame, const float* gt, float* d_color, float* loss);
+
+/* One view of the training step: forward(training) -> L1 -> backward,
+ * accumulating into device gradient buffers (not cleared when accumulate). */
+int svr_train_step_l1(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam,
+                      const svr_render_options* opts, const float* gt_device, svr_frame* frame,
+                      svr_gradients* grads, int accumulate, float* loss_device);
+
+/* ---- pipeline pieces (raster.hpp:115-127), batch form, host buffers ---- */
+/* project_voxel (raster.cpp:72-118) for n voxels. visible[i] is 0/1; aabb is
+ * (x0,x1,y0,y1) and rect (tx0,tx1,ty0,ty1) per voxel. */
+int svr_project_voxels(svr_ctx* ctx, const svr_camera* cam, uint64_t n, const double* centers,
+                       const double* sizes, double near_plane, uint8_t* visible, double* aabb,
+                       int32_t* rect);
+/* tile_sign_patterns (raster.cpp:120-142) for every tile: bitmask per tile. */
+int svr_tile_sign_masks(svr_ctx* ctx, const svr_camera* cam, uint8_t* masks, uint64_t n_tiles);
+/* build_sort_entries (raster.cpp:144-172): `pre` given as voxel ids, their
+ * paths and tile rects. Two-phase: call with keys==NULL to get *n_out. */
+int svr_build_sort_entries(svr_ctx* ctx, const svr_camera* cam, uint64_t scene_voxel_count,
+                           uint64_t n_pre, const uint32_t* vids, const uint64_t* codes,
+                           const int32_t* rects, uint64_t* keys, uint32_t* values,
+                           uint64_t capacity, uint64_t* n_out);
+/* sort_entries (raster.cpp:174-178): ascending (key, value), in place. */
+int svr_sort_entries(svr_ctx* ctx, uint64_t n, uint64_t* keys, uint32_t* values);
+
+/* ---- synthetic fixtures (host utility, not on the render path) -------- */
+/* Generator G of SURVEY §8(d): level-3 dense grid, random subdivision to
+ * <= max_level until the next split would exceed target, densities
+ * U(-4,2.5), SH from the pattern of tests/test_raster.cpp:15-37. Writes
+ * host arrays allocated by the library (free with svr_free). */
+int svr_synth_random_scene(uint64_t seed, uint64_t target, int max_level, int sh_degree,
+                           uint64_t* n_voxels, uint64_t* n_pool, uint64_t** codes,
+                           uint8_t** levels, uint32_t** corner_index, float** density,
+                           float** sh);
+/* ring_cameras (synth.cpp:89-118), camera i of n. */
+int svr_ring_camera(int n_views, int index, int width, int height, double distance,
+                    double fov_x_deg, svr_camera* out);
+void svr_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SVR_B200_H */

@@ -1,0 +1,285 @@
+"""TEST INFRASTRUCTURE — NOT PART OF THE PRODUCT.
+
+ctypes front end of the CPU checkers:
+  * `oracle/_ref/libsvr_ref.so`: the UNMODIFIED reference C++ sources
+    (/root/reference/proj/src/{scene,image,raster,losses,synth}.cpp) behind
+    the extern "C" shim `oracle/ref_shim.cpp` (built by `make -C oracle ref`).
+  * `oracle/_ref/libsvr_oracle.so`: the plain-C restatement `svr_oracle.c`
+    (built by `make -C oracle oracle`), pinned against the former.
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline leg may
+import this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_SO = os.path.join(HERE, "_ref", "libsvr_ref.so")
+PORT_SO = os.path.join(HERE, "_ref", "libsvr_oracle.so")
+
+_ref = None
+_port = None
+
+
+def _svr():
+    import paper_2412_04459_b200 as svr  # structs only; no compute
+    return svr
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO) or os.path.isdir("/root/reference/proj")
+
+
+def load_ref() -> C.CDLL:
+    global _ref
+    if _ref is not None:
+        return _ref
+    if not os.path.exists(REF_SO):
+        if os.path.isdir("/root/reference/proj"):
+            subprocess.run(["make", "-C", HERE, "ref"], check=True, capture_output=True)
+        else:
+            raise FileNotFoundError(f"{REF_SO} missing and /root/reference absent")
+    lib = C.CDLL(REF_SO)
+    svr = _svr()
+    P = C.c_void_p
+    cam = C.POINTER(svr.svr_camera)
+    opt = C.POINTER(svr.svr_render_options)
+    sig = {
+        "ref_last_error": (C.c_char_p, []),
+        "ref_scene_gen": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.POINTER(P)]),
+        "ref_scene_make": (C.c_int, [C.POINTER(svr.svr_scene_desc), C.POINTER(P)]),
+        "ref_scene_from_paths": (C.c_int, [P, P, C.c_uint64, C.c_float, C.c_int, C.POINTER(P)]),
+        "ref_scene_free": (None, [P]),
+        "ref_scene_sizes": (None, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                   C.POINTER(C.c_int)]),
+        "ref_scene_export": (None, [P, P, P, P, P, P]),
+        "ref_scene_set_params": (None, [P, P, P]),
+        "ref_ring_camera": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                      cam]),
+        "ref_scaled_camera": (C.c_int, [cam, C.c_double, cam]),
+        "ref_render": (C.c_int, [P, cam, opt, C.c_int, P, P, P, P, P, P]),
+        "ref_project": (C.c_int, [P, cam, C.c_double, P, P, P]),
+        "ref_project_one": (C.c_int, [cam, P, C.c_double, C.c_double, P, P, C.POINTER(C.c_int)]),
+        "ref_tile_masks": (C.c_int, [cam, P]),
+        "ref_entries": (C.c_int, [P, cam, C.c_double, C.c_int, C.POINTER(C.c_uint64), P, P]),
+        "ref_sort_entries": (C.c_int, [C.c_uint64, P, P]),
+        "ref_forward_train": (C.c_int, [P, cam, opt, C.POINTER(P), C.POINTER(C.c_uint64),
+                                        C.POINTER(C.c_uint64), P, P, P, P]),
+        "ref_frame_free": (None, [P]),
+        "ref_frame_records": (None, [P, P, P, P, P, P, P, P]),
+        "ref_backward": (C.c_int, [P, P, P, P, P, P, P, C.c_uint64, P, C.c_uint64, P, P, P]),
+        "ref_train_step_l1": (C.c_int, [P, cam, opt, P, C.POINTER(C.c_double), P, P, P, P]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _ref = lib
+    return lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _chk(st):
+    if st != 0:
+        svr = _svr()
+        msg = load_ref().ref_last_error().decode()
+        raise svr._EXC.get(st, svr.SvrError)(msg)
+
+
+class RefScene:
+    """A reference svr::SparseScene living in the oracle library."""
+
+    def __init__(self, handle):
+        self.h = handle
+
+    @staticmethod
+    def generate(seed: int, target: int, max_level: int, sh_degree: int = 3) -> "RefScene":
+        h = C.c_void_p()
+        _chk(load_ref().ref_scene_gen(seed, target, max_level, sh_degree, C.byref(h)))
+        return RefScene(h)
+
+    @staticmethod
+    def from_arrays(a) -> "RefScene":
+        svr = _svr()
+        keep = [np.ascontiguousarray(a.codes, np.uint64), np.ascontiguousarray(a.levels, np.uint8),
+                np.ascontiguousarray(a.corner_index, np.uint32).reshape(-1),
+                np.ascontiguousarray(a.density, np.float32),
+                np.ascontiguousarray(a.sh, np.float32).reshape(-1)]
+        d = svr.svr_scene_desc()
+        d.n_voxels, d.n_pool, d.sh_degree = a.n_voxels, a.n_pool, int(a.sh_degree)
+        for i in range(3):
+            d.bounds_center[i] = float(a.bounds_center[i])
+        d.bounds_size = float(a.bounds_size)
+        d.codes, d.levels, d.corner_index, d.density, d.sh = [_p(x) for x in keep]
+        h = C.c_void_p()
+        _chk(load_ref().ref_scene_make(C.byref(d), C.byref(h)))
+        return RefScene(h)
+
+    @staticmethod
+    def from_paths(codes, levels, fill: float, sh_degree: int) -> "RefScene":
+        codes = np.ascontiguousarray(codes, np.uint64)
+        levels = np.ascontiguousarray(levels, np.uint8)
+        h = C.c_void_p()
+        _chk(load_ref().ref_scene_from_paths(_p(codes), _p(levels), codes.size, fill, sh_degree,
+                                             C.byref(h)))
+        return RefScene(h)
+
+    def arrays(self):
+        svr = _svr()
+        n, p, deg = C.c_uint64(), C.c_uint64(), C.c_int()
+        lib = load_ref()
+        lib.ref_scene_sizes(self.h, C.byref(n), C.byref(p), C.byref(deg))
+        N, P, D = n.value, p.value, deg.value
+        stride = 3 * (D + 1) ** 2
+        codes = np.empty(N, np.uint64)
+        levels = np.empty(N, np.uint8)
+        ci = np.empty((N, 8), np.uint32)
+        dens = np.empty(P, np.float32)
+        sh = np.empty((N, stride), np.float32)
+        lib.ref_scene_export(self.h, _p(codes), _p(levels), _p(ci), _p(dens), _p(sh))
+        return svr.SceneArrays(codes, levels, ci, dens, sh, D)
+
+    def set_params(self, density=None, sh=None):
+        d = None if density is None else np.ascontiguousarray(density, np.float32)
+        s = None if sh is None else np.ascontiguousarray(sh, np.float32)
+        load_ref().ref_scene_set_params(self.h, _p(d), _p(s))
+
+    def __del__(self):
+        try:
+            if self.h:
+                load_ref().ref_scene_free(self.h)
+        except Exception:
+            pass
+
+
+def ref_ring_camera(n, i, w, h, dist=1.3, fov=55.0):
+    svr = _svr()
+    c = svr.svr_camera()
+    _chk(load_ref().ref_ring_camera(n, i, w, h, dist, fov, C.byref(c)))
+    return svr.Camera.from_c(c)
+
+
+def ref_scaled_camera(cam, ss):
+    svr = _svr()
+    c, o = cam.to_c(), svr.svr_camera()
+    _chk(load_ref().ref_scaled_camera(C.byref(c), ss, C.byref(o)))
+    return svr.Camera.from_c(o)
+
+
+def ref_render(scene: RefScene, cam, opts, oracle: bool = False, n_voxels: int = 0):
+    """svr::render (or render_oracle): dict of double images at target res."""
+    W, H = cam.width, cam.height
+    out = {"color": np.empty((H, W, 3)), "depth": np.empty((H, W)),
+           "median_depth": np.empty((H, W)), "normal": np.empty((H, W, 3)),
+           "transmittance": np.empty((H, W))}
+    mb = np.empty(n_voxels) if opts.record_stats else None
+    c, o = cam.to_c(), opts.to_c()
+    _chk(load_ref().ref_render(scene.h, C.byref(c), C.byref(o), int(oracle), _p(out["color"]),
+                               _p(out["depth"]), _p(out["median_depth"]), _p(out["normal"]),
+                               _p(out["transmittance"]), _p(mb)))
+    out["max_blend_weight"] = mb
+    return out
+
+
+def ref_project(scene: RefScene, cam, n_voxels: int, near: float = 1e-6):
+    vis = np.empty(n_voxels, np.uint8)
+    aabb = np.empty((n_voxels, 4))
+    rect = np.empty((n_voxels, 4), np.int32)
+    c = cam.to_c()
+    _chk(load_ref().ref_project(scene.h, C.byref(c), near, _p(vis), _p(aabb), _p(rect)))
+    return vis.astype(bool), aabb, rect
+
+
+def ref_tile_masks(cam):
+    ntx, nty = (cam.width + 15) // 16, (cam.height + 15) // 16
+    out = np.empty(ntx * nty, np.uint8)
+    c = cam.to_c()
+    _chk(load_ref().ref_tile_masks(C.byref(c), _p(out)))
+    return out
+
+
+def ref_entries(scene: RefScene, cam, sorted_: bool, near: float = 1e-6):
+    lib = load_ref()
+    c = cam.to_c()
+    n = C.c_uint64()
+    _chk(lib.ref_entries(scene.h, C.byref(c), near, int(sorted_), C.byref(n), None, None))
+    keys = np.empty(n.value, np.uint64)
+    vals = np.empty(n.value, np.uint32)
+    _chk(lib.ref_entries(scene.h, C.byref(c), near, int(sorted_), C.byref(n), _p(keys), _p(vals)))
+    return keys, vals
+
+
+def ref_sort_entries(keys, vals):
+    k = np.ascontiguousarray(keys, np.uint64).copy()
+    v = np.ascontiguousarray(vals, np.uint32).copy()
+    _chk(load_ref().ref_sort_entries(k.size, _p(k), _p(v)))
+    return k, v
+
+
+class RefFrame:
+    def __init__(self, scene: RefScene, cam, opts):
+        self.scene = scene
+        lib = load_ref()
+        W, H = cam.width, cam.height
+        self.color = np.empty((H, W, 3))
+        self.depth = np.empty((H, W))
+        self.normal = np.empty((H, W, 3))
+        self.transmittance = np.empty((H, W))
+        h = C.c_void_p()
+        npre, nc = C.c_uint64(), C.c_uint64()
+        c, o = cam.to_c(), opts.to_c()
+        _chk(lib.ref_forward_train(scene.h, C.byref(c), C.byref(o), C.byref(h), C.byref(npre),
+                                   C.byref(nc), _p(self.color), _p(self.depth), _p(self.normal),
+                                   _p(self.transmittance)))
+        self.h = h
+        self.n_pre, self.n_contribs = npre.value, nc.value
+        ss = ref_scaled_camera(cam, opts.supersample)
+        self.sw, self.sh = ss.width, ss.height
+
+    def records(self):
+        pre = np.empty(self.n_pre, np.uint32)
+        cp = np.empty(self.n_contribs, np.uint32)
+        ca = np.empty(self.n_contribs)
+        cb = np.empty(self.n_contribs)
+        pb = np.empty(self.sw * self.sh, np.uint32)
+        pc = np.empty(self.sw * self.sh, np.uint32)
+        tf = np.empty(self.sw * self.sh)
+        load_ref().ref_frame_records(self.h, _p(pre), _p(cp), _p(ca), _p(cb), _p(pb), _p(pc), _p(tf))
+        return pre, cp, ca, cb, pb, pc, tf
+
+    def backward(self, n_pool, n_sh, n_vox, d_color=None, d_depth=None, d_normal=None,
+                 d_tfin_ss=None, d_weight=None, d_voxel_color=None):
+        keep = [None if x is None else np.ascontiguousarray(x, np.float64).reshape(-1)
+                for x in (d_color, d_depth, d_normal, d_tfin_ss, d_weight, d_voxel_color)]
+        gd, gs, gp = np.empty(n_pool), np.empty(n_sh), np.empty(n_vox)
+        nw = 0 if keep[4] is None else keep[4].size
+        nvc = 0 if keep[5] is None else keep[5].size // 3
+        _chk(load_ref().ref_backward(self.scene.h, self.h, _p(keep[0]), _p(keep[1]), _p(keep[2]),
+                                     _p(keep[3]), _p(keep[4]), nw, _p(keep[5]), nvc, _p(gd),
+                                     _p(gs), _p(gp)))
+        return gd, gs, gp
+
+    def __del__(self):
+        try:
+            load_ref().ref_frame_free(self.h)
+        except Exception:
+            pass
+
+
+def ref_train_step_l1(scene: RefScene, cam, opts, gt, n_pool, n_sh, n_vox):
+    c, o = cam.to_c(), opts.to_c()
+    gt = np.ascontiguousarray(gt, np.float64)
+    loss = C.c_double()
+    dcol = np.empty_like(gt)
+    gd, gs, gp = np.empty(n_pool), np.empty(n_sh), np.empty(n_vox)
+    _chk(load_ref().ref_train_step_l1(scene.h, C.byref(c), C.byref(o), _p(gt), C.byref(loss),
+                                      _p(dcol), _p(gd), _p(gs), _p(gp)))
+    return loss.value, dcol, gd, gs, gp

@@ -1,0 +1,989 @@
+// capi.cu — the C ABI (include/svr_b200.h): contexts, device-resident scenes,
+// per-view frames, and the orchestration of the sm_100a kernels that
+// replaces render_with_pools / render_backward (raster.cpp:205-423).
+//
+// There is no CPU fallback: every compute entry point launches CUDA kernels
+// and fails with SVR_ERR_NO_DEVICE / SVR_ERR_CUDA when it cannot.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "svr_internal.h"
+#include "svr_kernels.h"
+
+namespace svrb {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver)
+        throw Error(SVR_ERR_NO_DEVICE, std::string(what) + ": " + cudaGetErrorString(e));
+    throw Error(SVR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void DevBuf::reserve(size_t n) {
+    if (n <= bytes) return;
+    release();
+    size_t alloc = std::max<size_t>(n + n / 8, 256);
+    SVR_CUDA(cudaMalloc(&p, alloc));
+    bytes = alloc;
+}
+
+void DevBuf::release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+}
+
+void HostBuf::reserve(size_t n) {
+    if (n <= bytes) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    SVR_CUDA(cudaMallocHost(&p, n));
+    bytes = n;
+}
+
+HostBuf::~HostBuf() {
+    if (p) cudaFreeHost(p);
+}
+
+namespace {
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return SVR_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.status;
+    } catch (const std::bad_alloc& e) {
+        g_last_error = e.what();
+        return SVR_ERR_RUNTIME;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return SVR_ERR_RUNTIME;
+    }
+}
+
+void require(bool ok, int status, const char* msg) {
+    if (!ok) throw Error(status, msg);
+}
+
+int tiles_along(int px) { return (px + kTile - 1) / kTile; }
+
+// Camera::scaled (camera.hpp:38-48).
+svr_camera scaled_camera(const svr_camera& c, int nw, int nh) {
+    svr_camera s = c;
+    double rx = double(nw) / c.width, ry = double(nh) / c.height;
+    s.width = nw;
+    s.height = nh;
+    s.fx = c.fx * rx;
+    s.cx = c.cx * rx;
+    s.fy = c.fy * ry;
+    s.cy = c.cy * ry;
+    return s;
+}
+
+DevCamera dev_camera(const svr_camera& c) {
+    DevCamera d{};
+    d.W = c.width;
+    d.H = c.height;
+    d.ntx = tiles_along(c.width);
+    d.nty = tiles_along(c.height);
+    d.fx = c.fx;
+    d.fy = c.fy;
+    d.cx = c.cx;
+    d.cy = c.cy;
+    for (int i = 0; i < 9; ++i) d.rot[i] = c.rot[i];
+    for (int i = 0; i < 3; ++i) d.pos[i] = c.pos[i];
+    return d;
+}
+
+int bit_width(uint64_t x) {
+    int b = 0;
+    while (x) {
+        ++b;
+        x >>= 1;
+    }
+    return b;
+}
+
+void set_device(svr_ctx* ctx) { SVR_CUDA(cudaSetDevice(ctx->device)); }
+
+template <class T>
+T* grow(DevBuf& b, uint64_t count) {
+    b.reserve(std::max<uint64_t>(count, 1) * sizeof(T));
+    return b.as<T>();
+}
+
+// axis_taps (image.cpp:9-23) as CSR, plus the transposed table for the adjoint.
+void axis_taps(int src, int dst, std::vector<int>& ptr, std::vector<int>& idx,
+               std::vector<float>& w, std::vector<int>& tptr, std::vector<int>& tidx,
+               std::vector<float>& tw) {
+    double scale = double(src) / dst;
+    ptr.assign(1, 0);
+    idx.clear();
+    w.clear();
+    std::vector<std::vector<std::pair<int, float>>> tr(src);
+    for (int d = 0; d < dst; ++d) {
+        double lo = d * scale, hi = (d + 1) * scale;
+        int s0 = int(lo), s1 = std::min(src - 1, int(std::ceil(hi)) - 1);
+        for (int s = s0; s <= s1; ++s) {
+            double overlap = std::min(hi, double(s + 1)) - std::max(lo, double(s));
+            if (overlap > 0) {
+                idx.push_back(s);
+                w.push_back(float(overlap / scale));
+                tr[s].push_back({d, float(overlap / scale)});
+            }
+        }
+        ptr.push_back(int(idx.size()));
+    }
+    tptr.assign(1, 0);
+    tidx.clear();
+    tw.clear();
+    for (int s = 0; s < src; ++s) {
+        for (auto& pr : tr[s]) {
+            tidx.push_back(pr.first);
+            tw.push_back(pr.second);
+        }
+        tptr.push_back(int(tidx.size()));
+    }
+}
+
+struct TapSet {
+    TapTable fwd, adj;
+};
+
+TapSet ensure_taps(svr_frame* f) {
+    // Layout inside f->taps: [ptr_x idx_x w_x ptr_y idx_y w_y tptr_x tidx_x tw_x tptr_y tidx_y tw_y]
+    std::vector<int> px, ix, py, iy, tpx, tix, tpy, tiy;
+    std::vector<float> wx, wy, twx, twy;
+    axis_taps(f->sw, f->W, px, ix, wx, tpx, tix, twx);
+    axis_taps(f->sh, f->H, py, iy, wy, tpy, tiy, twy);
+    std::vector<std::pair<const void*, size_t>> parts = {
+        {px.data(), px.size() * 4},   {ix.data(), ix.size() * 4},   {wx.data(), wx.size() * 4},
+        {py.data(), py.size() * 4},   {iy.data(), iy.size() * 4},   {wy.data(), wy.size() * 4},
+        {tpx.data(), tpx.size() * 4}, {tix.data(), tix.size() * 4}, {twx.data(), twx.size() * 4},
+        {tpy.data(), tpy.size() * 4}, {tiy.data(), tiy.size() * 4}, {twy.data(), twy.size() * 4}};
+    std::vector<size_t> off;
+    size_t total = 0;
+    for (auto& p : parts) {
+        off.push_back(total);
+        total += (p.second + 15) & ~size_t(15);
+    }
+    bool fresh = !(f->tap_src_w == f->sw && f->tap_src_h == f->sh && f->tap_dst_w == f->W &&
+                   f->tap_dst_h == f->H);
+    if (fresh) {
+        f->taps.reserve(total);
+        std::vector<char> host(total, 0);
+        for (size_t i = 0; i < parts.size(); ++i)
+            if (parts[i].second) std::memcpy(host.data() + off[i], parts[i].first, parts[i].second);
+        SVR_CUDA(cudaMemcpy(f->taps.p, host.data(), total, cudaMemcpyHostToDevice));
+        f->tap_src_w = f->sw;
+        f->tap_src_h = f->sh;
+        f->tap_dst_w = f->W;
+        f->tap_dst_h = f->H;
+    }
+    char* b = f->taps.as<char>();
+    TapSet t;
+    t.fwd = {reinterpret_cast<int*>(b + off[0]),  reinterpret_cast<int*>(b + off[1]),
+             reinterpret_cast<float*>(b + off[2]), reinterpret_cast<int*>(b + off[3]),
+             reinterpret_cast<int*>(b + off[4]),  reinterpret_cast<float*>(b + off[5])};
+    t.adj = {reinterpret_cast<int*>(b + off[6]),  reinterpret_cast<int*>(b + off[7]),
+             reinterpret_cast<float*>(b + off[8]), reinterpret_cast<int*>(b + off[9]),
+             reinterpret_cast<int*>(b + off[10]), reinterpret_cast<float*>(b + off[11])};
+    return t;
+}
+
+// Validation of RenderOptions, in raster.cpp:207-211 order.
+void validate_options(const svr_render_options& o) {
+    require(o.supersample >= 1.0, SVR_ERR_INVALID_ARGUMENT, "supersample factor must be >= 1");
+    require(o.K >= 1 && o.K <= 3, SVR_ERR_INVALID_ARGUMENT,
+            "rasterizer sample count K must be in {1,2,3}");
+    require(o.t_threshold > 0.0 && o.t_threshold < 1.0, SVR_ERR_INVALID_ARGUMENT,
+            "transmittance threshold must be in (0,1)");
+}
+
+// Radix digits that can differ between entries (see sort.cu): the sign
+// pattern (value bits 29..31) when more than one pattern exists, then the
+// key bits from the finest occupied octree level up to the top tile-id bit.
+int plan_sort(int max_level, int ntiles, uint32_t pattern_or, RadixPass* passes) {
+    int np = 0;
+    if (__builtin_popcount(pattern_or) > 1) passes[np++] = {1, 29, 3};
+    int lo = 48 - 3 * max_level;
+    int hi = 48 + bit_width(uint64_t(ntiles - 1));
+    for (int b = lo; b < hi; b += 8) passes[np++] = {0, b, std::min(8, hi - b)};
+    return np;
+}
+
+void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
+                 const svr_render_options* opts, svr_frame* f) {
+    require(ctx && scene && cam_in && opts && f, SVR_ERR_INVALID_ARGUMENT, "null argument");
+    set_device(ctx);
+    validate_options(*opts);
+    require(cam_in->width > 0 && cam_in->height > 0, SVR_ERR_INVALID_ARGUMENT,
+            "camera resolution must be positive");
+    cudaStream_t st = ctx->stream;
+    const int W = cam_in->width, H = cam_in->height;
+    const int sw = int(std::ceil(opts->supersample * W));
+    const int sh = int(std::ceil(opts->supersample * H));
+    const svr_camera ss_cam = scaled_camera(*cam_in, sw, sh);
+    const DevCamera cam = dev_camera(ss_cam);
+    const int ntiles = cam.ntx * cam.nty;
+    // build_sort_entries capacity checks (raster.cpp:146-150)
+    require(scene->n_voxels < (uint64_t(1) << 29), SVR_ERR_LENGTH,
+            "voxel count exceeds the 29-bit id capacity");
+    require(uint64_t(cam.ntx) * cam.nty < (uint64_t(1) << 16), SVR_ERR_LENGTH,
+            "tile count exceeds the 16-bit id capacity");
+
+    f->ctx = ctx;
+    f->scene = scene;
+    f->opts = *opts;
+    f->cam = cam;
+    f->ss_cam = ss_cam;
+    f->W = W;
+    f->H = H;
+    f->sw = sw;
+    f->sh = sh;
+    f->ntx = cam.ntx;
+    f->nty = cam.nty;
+    f->n_voxels = scene->n_voxels;
+    f->training = opts->training != 0;
+    f->has_records = false;
+    f->n_contribs = 0;
+    const uint64_t N = scene->n_voxels;
+    const bool ss1 = (sw == W && sh == H);
+
+    // K2: tile sign masks + SAT
+    uint8_t* masks = grow<uint8_t>(f->tile_masks, ntiles);
+    uint32_t* sat = grow<uint32_t>(f->tile_sat, uint64_t(cam.ntx + 1) * (cam.nty + 1));
+    FrameStatus* status = grow<FrameStatus>(f->status, 1);
+    SVR_CUDA(cudaMemsetAsync(status, 0, sizeof(FrameStatus), st));
+    launch_tile_setup(cam, masks, sat, status, st);
+
+    // K1: preprocess
+    PreprocessArgs pa{};
+    pa.n = N;
+    pa.paths = scene->paths.as<uint64_t>();
+    pa.corner_index = scene->corner_index.as<uint32_t>();
+    pa.density = scene->density.as<float>();
+    pa.sh = scene->sh.as<float>();
+    pa.sh_degree = scene->sh_degree;
+    pa.sh_stride = scene->sh_stride;
+    for (int i = 0; i < 3; ++i) pa.bc[i] = scene->bounds_center[i];
+    pa.bsize = scene->bounds_size;
+    pa.near_plane = opts->near_plane;
+    pa.tile_sat = sat;
+    pa.rects = grow<int4>(f->rects, N);
+    pa.aabb = ctx->debug ? grow<double4>(f->aabb, N) : nullptr;
+    pa.records = grow<float4>(f->records, N * kRecordF4);
+    pa.counts = grow<uint32_t>(f->counts, N);
+    launch_preprocess(cam, pa, st);
+
+    // K3: scan of the per-voxel entry counts -> emission offsets, E
+    uint32_t* offsets = grow<uint32_t>(f->offsets, N);
+    ctx->scratch.reserve(scan_scratch_bytes(std::max<uint64_t>(N, uint64_t(ntiles) * 256)));
+    exclusive_scan_u32(pa.counts, offsets, N, &status->n_entries, ctx->scratch.p, st);
+    ctx->pinned.reserve(sizeof(FrameStatus));
+    FrameStatus* hs = static_cast<FrameStatus*>(ctx->pinned.p);
+    SVR_CUDA(cudaMemcpyAsync(hs, status, sizeof(FrameStatus), cudaMemcpyDeviceToHost, st));
+    SVR_CUDA(cudaStreamSynchronize(st));
+    const uint64_t E = hs->n_entries;
+    const uint32_t pattern_or = hs->pattern_or;
+    require(E < (uint64_t(1) << 30), SVR_ERR_LENGTH, "entry count exceeds 2^30");
+    f->n_entries = E;
+
+    // K4: duplicate (reference emission order: vid, ty, tx, s)
+    for (int b = 0; b < 2; ++b) {
+        grow<uint64_t>(f->keys[b], E);
+        grow<uint32_t>(f->vals[b], E);
+    }
+    launch_duplicate(cam, N, pa.paths, pa.rects, masks, pa.counts, offsets, f->keys[0].as<uint64_t>(),
+                     f->vals[0].as<uint32_t>(), st);
+    if (ctx->debug) {
+        grow<uint64_t>(f->dbg_keys, E);
+        grow<uint32_t>(f->dbg_vals, E);
+        SVR_CUDA(cudaMemcpyAsync(f->dbg_keys.p, f->keys[0].p, E * 8, cudaMemcpyDeviceToDevice, st));
+        SVR_CUDA(cudaMemcpyAsync(f->dbg_vals.p, f->vals[0].p, E * 4, cudaMemcpyDeviceToDevice, st));
+    }
+
+    // K5: onesweep radix sort over the digits that can differ
+    RadixPass passes[kMaxRadixPasses];
+    const int np = plan_sort(scene->max_level, ntiles, pattern_or, passes);
+    f->sort_passes = np;
+    ctx->scratch2.reserve(sort_scratch_bytes(E, np));
+    f->sorted_buf = radix_sort_pairs(f->keys[0].as<uint64_t>(), f->vals[0].as<uint32_t>(),
+                                     f->keys[1].as<uint64_t>(), f->vals[1].as<uint32_t>(), E,
+                                     passes, np, ctx->scratch2.p, st);
+    const uint64_t* skeys = f->keys[f->sorted_buf].as<uint64_t>();
+    const uint32_t* svals = f->vals[f->sorted_buf].as<uint32_t>();
+
+    // K6: tile ranges
+    uint2* ranges = grow<uint2>(f->ranges, ntiles);
+    launch_tile_ranges(skeys, E, ranges, ntiles, st);
+
+    // output buffers
+    const uint64_t npx = uint64_t(W) * H, nss = uint64_t(sw) * sh;
+    float* oc = grow<float>(f->out_color, npx * 3);
+    float* od = grow<float>(f->out_depth, npx);
+    float* om = grow<float>(f->out_median, npx);
+    float* on = grow<float>(f->out_normal, npx * 3);
+    float* ot = grow<float>(f->out_tfin, npx);
+    CompositeArgs ca{};
+    ca.ranges = ranges;
+    ca.vals = svals;
+    ca.records = pa.records;
+    ca.K = opts->K;
+    ca.t_threshold = float(opts->t_threshold);
+    for (int i = 0; i < 3; ++i) ca.bg[i] = float(opts->background[i]);
+    ca.far_sentinel = float(opts->far_sentinel);
+    if (ss1) {
+        ca.color = oc, ca.depth = od, ca.median = om, ca.normal = on, ca.tfin = ot;
+    } else {
+        ca.color = grow<float>(f->ss_color, nss * 3);
+        ca.depth = grow<float>(f->ss_depth, nss);
+        ca.median = grow<float>(f->ss_median, nss);
+        ca.normal = grow<float>(f->ss_normal, nss * 3);
+        ca.tfin = grow<float>(f->ss_tfin, nss);
+    }
+    if (opts->record_stats) {
+        ca.max_blend = grow<unsigned int>(f->max_blend, N);
+        SVR_CUDA(cudaMemsetAsync(ca.max_blend, 0, N * 4, st));
+    }
+    if (f->training) ca.pix_count = grow<uint32_t>(f->pix_count, uint64_t(ntiles) * 256);
+    if (f->training) SVR_CUDA(cudaMemsetAsync(ca.pix_count, 0, uint64_t(ntiles) * 256 * 4, st));
+
+    // K7: composite
+    launch_composite(cam, ca, false, st);
+
+    if (f->training) {
+        // ForwardRecords: per-pixel contribution lists in the reference's
+        // order (tile-major, pixel row-major inside the tile).
+        uint32_t* pb = grow<uint32_t>(f->pix_begin, uint64_t(ntiles) * 256);
+        exclusive_scan_u32(ca.pix_count, pb, uint64_t(ntiles) * 256, &status->n_contribs,
+                           ctx->scratch.p, st);
+        SVR_CUDA(cudaMemcpyAsync(hs, status, sizeof(FrameStatus), cudaMemcpyDeviceToHost, st));
+        SVR_CUDA(cudaStreamSynchronize(st));
+        const uint64_t C = hs->n_contribs;
+        require(C < (uint64_t(1) << 32), SVR_ERR_LENGTH, "contribution count exceeds 2^32");
+        f->n_contribs = C;
+        CompositeArgs cr = ca;
+        cr.pix_begin = pb;
+        cr.contrib_entry = grow<uint32_t>(f->contrib_entry, C);
+        cr.contrib_T = grow<float>(f->contrib_T, C);
+        cr.max_blend = nullptr;
+        launch_composite(cam, cr, true, st);
+        f->has_records = true;
+    }
+
+    // K8: area downsampling of the five outputs (identity when ss == 1)
+    if (!ss1) {
+        TapSet taps = ensure_taps(f);
+        launch_downsample(taps.fwd, ca.color, 3, sw, oc, W, H, st);
+        launch_downsample(taps.fwd, ca.depth, 1, sw, od, W, H, st);
+        launch_downsample(taps.fwd, ca.median, 1, sw, om, W, H, st);
+        launch_downsample(taps.fwd, ca.normal, 3, sw, on, W, H, st);
+        launch_downsample(taps.fwd, ca.tfin, 1, sw, ot, W, H, st);
+    }
+    (void)nss;
+    f->n_visible = ~uint64_t(0);  // computed lazily
+}
+
+uint64_t count_visible(svr_frame* f) {
+    if (f->n_visible != ~uint64_t(0)) return f->n_visible;
+    svr_ctx* ctx = f->ctx;
+    cudaStream_t st = ctx->stream;
+    const uint64_t N = f->n_voxels;
+    uint32_t* flags = grow<uint32_t>(f->visible_rank, N);
+    launch_visible_flags(f->rects.as<int4>(), N, flags, st);
+    DevBuf tot;
+    tot.reserve(8);
+    ctx->scratch.reserve(scan_scratch_bytes(N));
+    exclusive_scan_u32(flags, flags, N, tot.as<unsigned long long>(), ctx->scratch.p, st);
+    unsigned long long h = 0;
+    SVR_CUDA(cudaMemcpyAsync(&h, tot.p, 8, cudaMemcpyDeviceToHost, st));
+    SVR_CUDA(cudaStreamSynchronize(st));
+    f->n_visible = h;
+    return h;
+}
+
+struct BufView {
+    const void* p;
+    size_t bytes;
+};
+
+BufView frame_buffer(svr_frame* f, svr_buffer which) {
+    require(f && f->ctx, SVR_ERR_INVALID_ARGUMENT, "frame has not been rendered");
+    const uint64_t npx = uint64_t(f->W) * f->H, nss = uint64_t(f->sw) * f->sh;
+    const bool ss1 = (f->sw == f->W && f->sh == f->H);
+    const uint64_t ntiles = uint64_t(f->ntx) * f->nty;
+    switch (which) {
+        case SVR_BUF_COLOR: return {f->out_color.p, npx * 12};
+        case SVR_BUF_DEPTH: return {f->out_depth.p, npx * 4};
+        case SVR_BUF_MEDIAN_DEPTH: return {f->out_median.p, npx * 4};
+        case SVR_BUF_NORMAL: return {f->out_normal.p, npx * 12};
+        case SVR_BUF_TRANSMITTANCE: return {f->out_tfin.p, npx * 4};
+        case SVR_BUF_MAX_BLEND:
+            require(f->opts.record_stats, SVR_ERR_INVALID_ARGUMENT, "render without record_stats");
+            return {f->max_blend.p, f->n_voxels * 4};
+        case SVR_BUF_SS_COLOR: return {ss1 ? f->out_color.p : f->ss_color.p, nss * 12};
+        case SVR_BUF_SS_DEPTH: return {ss1 ? f->out_depth.p : f->ss_depth.p, nss * 4};
+        case SVR_BUF_SS_TFIN: return {ss1 ? f->out_tfin.p : f->ss_tfin.p, nss * 4};
+        case SVR_BUF_SORT_KEYS: return {f->keys[f->sorted_buf].p, f->n_entries * 8};
+        case SVR_BUF_SORT_VALUES: return {f->vals[f->sorted_buf].p, f->n_entries * 4};
+        case SVR_BUF_TILE_RANGES: return {f->ranges.p, ntiles * 8};
+        case SVR_BUF_TILE_MASKS: return {f->tile_masks.p, ntiles};
+        case SVR_BUF_VOXEL_RECTS: return {f->rects.p, f->n_voxels * 16};
+        case SVR_BUF_VOXEL_AABB:
+            require(f->ctx->debug, SVR_ERR_INVALID_ARGUMENT, "AABB dump needs svr_ctx_set_debug");
+            return {f->aabb.p, f->n_voxels * 32};
+        case SVR_BUF_ENTRIES_KEYS:
+            require(f->ctx->debug, SVR_ERR_INVALID_ARGUMENT, "entry dump needs svr_ctx_set_debug");
+            return {f->dbg_keys.p, f->n_entries * 8};
+        case SVR_BUF_ENTRIES_VALUES:
+            require(f->ctx->debug, SVR_ERR_INVALID_ARGUMENT, "entry dump needs svr_ctx_set_debug");
+            return {f->dbg_vals.p, f->n_entries * 4};
+        case SVR_BUF_PIX_COUNT:
+        case SVR_BUF_PIX_BEGIN: {
+            require(f->has_records, SVR_ERR_RUNTIME, "frame has no forward records");
+            uint32_t* img = grow<uint32_t>(f->bwd_dcolor, nss);
+            launch_tile_to_image_u32(which == SVR_BUF_PIX_COUNT ? f->pix_count.as<uint32_t>()
+                                                                : f->pix_begin.as<uint32_t>(),
+                                     img, f->sw, f->sh, f->ntx, f->ctx->stream);
+            return {img, nss * 4};
+        }
+        default: break;
+    }
+    throw Error(SVR_ERR_INVALID_ARGUMENT, "unknown buffer id");
+}
+
+void backward_impl(svr_ctx* ctx, const svr_scene* scene, svr_frame* f, const svr_upstream* up,
+                   svr_gradients* out, bool accumulate) {
+    require(ctx && scene && f && up && out, SVR_ERR_INVALID_ARGUMENT, "null argument");
+    set_device(ctx);
+    require(f->has_records, SVR_ERR_RUNTIME,
+            "frame has no forward records (render with training = true)");
+    require(f->scene == scene, SVR_ERR_RUNTIME, "frame was rendered from another scene");
+    // raster.cpp:327-332
+    require(!up->d_weight || up->n_d_weight == f->n_contribs, SVR_ERR_RUNTIME,
+            "per-contribution weight gradients do not match the records");
+    require(!up->d_voxel_color || up->n_d_voxel_color == f->n_contribs, SVR_ERR_RUNTIME,
+            "per-contribution color gradients do not match the records");
+    cudaStream_t st = ctx->stream;
+    const uint64_t N = scene->n_voxels, P = scene->n_pool;
+    const uint64_t shn = N * uint64_t(scene->sh_stride);
+    const uint64_t npx = uint64_t(f->W) * f->H, nss = uint64_t(f->sw) * f->sh;
+    const bool ss1 = (f->sw == f->W && f->sh == f->H);
+
+    // Stage upstream buffers on the device.
+    struct Up {
+        const float* p;
+        uint64_t n;
+    };
+    Up ins[6] = {{up->d_color, npx * 3},        {up->d_depth, npx},
+                 {up->d_normal, npx * 3},       {up->d_tfin_ss, nss},
+                 {up->d_weight, f->n_contribs}, {up->d_voxel_color, f->n_contribs * 3}};
+    const float* dev_in[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    uint64_t total = 0;
+    for (auto& u : ins)
+        if (u.p && !up->on_device) total += (u.n + 3) & ~uint64_t(3);
+    float* stage = total ? grow<float>(f->bwd_dcolor, total + 16) : nullptr;
+    uint64_t off = 0;
+    for (int i = 0; i < 6; ++i) {
+        if (!ins[i].p) continue;
+        if (up->on_device) {
+            dev_in[i] = ins[i].p;
+        } else {
+            SVR_CUDA(cudaMemcpyAsync(stage + off, ins[i].p, ins[i].n * 4, cudaMemcpyHostToDevice, st));
+            dev_in[i] = stage + off;
+            off += (ins[i].n + 3) & ~uint64_t(3);
+        }
+    }
+    // Lift image-level grads to the supersampled grid (raster.cpp:317-324).
+    const float* gC = dev_in[0];
+    const float* gD = dev_in[1];
+    const float* gN = dev_in[2];
+    if (!ss1 && (gC || gD || gN)) {
+        TapSet taps = ensure_taps(f);
+        float* lift = grow<float>(f->bwd_lift, nss * 7);
+        if (gC) {
+            launch_lift(taps.adj, gC, 3, f->W, lift, f->sw, f->sh, st);
+            gC = lift;
+        }
+        if (gD) {
+            launch_lift(taps.adj, gD, 1, f->W, lift + nss * 3, f->sw, f->sh, st);
+            gD = lift + nss * 3;
+        }
+        if (gN) {
+            launch_lift(taps.adj, gN, 3, f->W, lift + nss * 4, f->sw, f->sh, st);
+            gN = lift + nss * 4;
+        }
+    }
+
+    // Gradient outputs on device.
+    float *gd = out->density, *gs = out->sh, *gp = out->priority;
+    DevBuf tmp_d, tmp_s, tmp_p;
+    if (!out->on_device) {
+        gd = grow<float>(tmp_d, P);
+        gs = grow<float>(tmp_s, shn);
+        gp = grow<float>(tmp_p, N);
+    }
+    require(gd && gs && gp, SVR_ERR_INVALID_ARGUMENT, "gradient buffers must not be null");
+    if (!accumulate) {
+        SVR_CUDA(cudaMemsetAsync(gd, 0, P * 4, st));
+        SVR_CUDA(cudaMemsetAsync(gp, 0, N * 4, st));
+    }
+    float* gcol = grow<float>(f->bwd_gc, N * 3);
+    float* gnor = grow<float>(f->bwd_gn, N * 3);
+    SVR_CUDA(cudaMemsetAsync(gcol, 0, N * 12, st));
+    SVR_CUDA(cudaMemsetAsync(gnor, 0, N * 12, st));
+
+    BackwardArgs ba{};
+    ba.ranges = f->ranges.as<uint2>();
+    ba.vals = f->vals[f->sorted_buf].as<uint32_t>();
+    ba.records = f->records.as<float4>();
+    ba.corner_index = scene->corner_index.as<uint32_t>();
+    ba.K = f->opts.K;
+    for (int i = 0; i < 3; ++i) ba.bg[i] = float(f->opts.background[i]);
+    ba.gC = gC;
+    ba.gD = gD;
+    ba.gN = gN;
+    ba.gT = dev_in[3];
+    ba.d_weight = dev_in[4];
+    ba.d_voxel_color = dev_in[5];
+    ba.pix_count = f->pix_count.as<uint32_t>();
+    ba.pix_begin = f->pix_begin.as<uint32_t>();
+    ba.contrib_entry = f->contrib_entry.as<uint32_t>();
+    ba.contrib_T = f->contrib_T.as<float>();
+    ba.g_density = gd;
+    ba.g_color = gcol;
+    ba.g_normal = gnor;
+    ba.g_priority = gp;
+    launch_composite_backward(f->cam, ba, st);
+
+    EpilogueArgs ea{};
+    ea.n = N;
+    ea.paths = scene->paths.as<uint64_t>();
+    ea.rects = f->rects.as<int4>();
+    ea.records = f->records.as<float4>();
+    ea.corner_index = scene->corner_index.as<uint32_t>();
+    ea.sh = scene->sh.as<float>();
+    ea.sh_degree = scene->sh_degree;
+    ea.sh_stride = scene->sh_stride;
+    for (int i = 0; i < 3; ++i) ea.bc[i] = scene->bounds_center[i];
+    ea.bsize = scene->bounds_size;
+    ea.g_color = gcol;
+    ea.g_normal = gnor;
+    ea.g_sh = gs;
+    ea.g_density = gd;
+    ea.accumulate = accumulate ? 1 : 0;
+    launch_voxel_epilogue(f->cam, ea, st);
+
+    if (!out->on_device) {
+        if (out->density) SVR_CUDA(cudaMemcpyAsync(out->density, gd, P * 4, cudaMemcpyDeviceToHost, st));
+        if (out->sh) SVR_CUDA(cudaMemcpyAsync(out->sh, gs, shn * 4, cudaMemcpyDeviceToHost, st));
+        if (out->priority) SVR_CUDA(cudaMemcpyAsync(out->priority, gp, N * 4, cudaMemcpyDeviceToHost, st));
+        SVR_CUDA(cudaStreamSynchronize(st));
+    }
+}
+
+}  // namespace
+}  // namespace svrb
+
+using namespace svrb;
+
+extern "C" {
+
+const char* svr_last_error(void) { return g_last_error.c_str(); }
+int svr_abi_version(void) { return SVR_ABI_VERSION; }
+
+int svr_ctx_create(int device, svr_ctx** out) {
+    return guard([&] {
+        require(out != nullptr, SVR_ERR_INVALID_ARGUMENT, "null output");
+        int n = 0;
+        cudaError_t e = cudaGetDeviceCount(&n);
+        if (e != cudaSuccess || n == 0)
+            throw Error(SVR_ERR_NO_DEVICE, "no CUDA device: the rasterizer has no CPU fallback");
+        require(device >= 0 && device < n, SVR_ERR_INVALID_ARGUMENT, "device index out of range");
+        auto* c = new svr_ctx;
+        c->device = device;
+        SVR_CUDA(cudaSetDevice(device));
+        SVR_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        SVR_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+        *out = c;
+    });
+}
+
+int svr_ctx_destroy(svr_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+void* svr_ctx_stream(svr_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int svr_ctx_synchronize(svr_ctx* ctx) {
+    return guard([&] { SVR_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+int svr_ctx_set_debug(svr_ctx* ctx, int debug) {
+    return guard([&] { ctx->debug = debug != 0; });
+}
+
+int svr_scene_upload(svr_ctx* ctx, const svr_scene_desc* d, svr_scene** out) {
+    return guard([&] {
+        require(ctx && d && out, SVR_ERR_INVALID_ARGUMENT, "null argument");
+        require(d->sh_degree >= 0 && d->sh_degree <= 3, SVR_ERR_INVALID_ARGUMENT,
+                "SH degree out of [0,3]");
+        set_device(ctx);
+        const uint64_t N = d->n_voxels;
+        const int stride = 3 * (d->sh_degree + 1) * (d->sh_degree + 1);
+        std::vector<uint64_t> paths(N);
+        int max_level = 1;
+        for (uint64_t i = 0; i < N; ++i) {
+            int lv = d->levels[i];
+            // check_level / to_voxel_index (octree.hpp:47-49, 68-73)
+            require(lv >= 1 && lv <= kMaxLevel, SVR_ERR_INVALID_ARGUMENT,
+                    "octree level out of [1,16]");
+            int shift = 3 * (kMaxLevel - lv);
+            require(shift >= 64 || (d->codes[i] & ((uint64_t(1) << shift) - 1)) == 0,
+                    SVR_ERR_INVALID_ARGUMENT, "octpath has nonzero bits below its level");
+            require((d->codes[i] >> 48) == 0, SVR_ERR_INVALID_ARGUMENT,
+                    "octpath code exceeds 48 bits");
+            paths[i] = d->codes[i] | (uint64_t(lv) << 48);
+            max_level = std::max(max_level, lv);
+        }
+        for (uint64_t i = 0; i < N * 8; ++i)
+            require(d->corner_index[i] < d->n_pool, SVR_ERR_INVALID_ARGUMENT,
+                    "corner index out of the density pool");
+        auto* s = new svr_scene;
+        try {
+            s->n_voxels = N;
+            s->n_pool = d->n_pool;
+            s->sh_degree = d->sh_degree;
+            s->sh_stride = stride;
+            s->max_level = max_level;
+            for (int i = 0; i < 3; ++i) s->bounds_center[i] = d->bounds_center[i];
+            s->bounds_size = d->bounds_size;
+            s->paths.reserve(std::max<uint64_t>(N, 1) * 8);
+            s->corner_index.reserve(std::max<uint64_t>(N, 1) * 32);
+            s->density.reserve(std::max<uint64_t>(d->n_pool, 1) * 4);
+            s->sh.reserve(std::max<uint64_t>(N * stride, 1) * 4);
+            if (N) {
+                SVR_CUDA(cudaMemcpy(s->paths.p, paths.data(), N * 8, cudaMemcpyHostToDevice));
+                SVR_CUDA(cudaMemcpy(s->corner_index.p, d->corner_index, N * 32,
+                                    cudaMemcpyHostToDevice));
+                SVR_CUDA(cudaMemcpy(s->sh.p, d->sh, N * stride * 4, cudaMemcpyHostToDevice));
+            }
+            if (d->n_pool)
+                SVR_CUDA(cudaMemcpy(s->density.p, d->density, d->n_pool * 4, cudaMemcpyHostToDevice));
+        } catch (...) {
+            delete s;
+            throw;
+        }
+        *out = s;
+    });
+}
+
+int svr_scene_set_params(svr_ctx* ctx, svr_scene* s, const float* density, const float* sh,
+                         int on_device) {
+    return guard([&] {
+        require(ctx && s, SVR_ERR_INVALID_ARGUMENT, "null argument");
+        set_device(ctx);
+        cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        if (density && s->n_pool)
+            SVR_CUDA(cudaMemcpyAsync(s->density.p, density, s->n_pool * 4, k, ctx->stream));
+        if (sh && s->n_voxels)
+            SVR_CUDA(cudaMemcpyAsync(s->sh.p, sh, s->n_voxels * s->sh_stride * 4, k, ctx->stream));
+        if (!on_device) SVR_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int svr_scene_destroy(svr_scene* s) {
+    return guard([&] { delete s; });
+}
+
+int svr_scene_param_ptrs(svr_scene* s, float** density, float** sh, uint64_t* n_pool,
+                         uint64_t* n_sh) {
+    return guard([&] {
+        require(s != nullptr, SVR_ERR_INVALID_ARGUMENT, "null scene");
+        if (density) *density = s->density.as<float>();
+        if (sh) *sh = s->sh.as<float>();
+        if (n_pool) *n_pool = s->n_pool;
+        if (n_sh) *n_sh = s->n_voxels * s->sh_stride;
+    });
+}
+
+int svr_frame_create(svr_ctx* ctx, svr_frame** out) {
+    return guard([&] {
+        require(ctx && out, SVR_ERR_INVALID_ARGUMENT, "null argument");
+        auto* f = new svr_frame;
+        f->ctx = ctx;
+        *out = f;
+    });
+}
+
+int svr_frame_destroy(svr_frame* f) {
+    return guard([&] {
+        if (!f) return;
+        if (f->ctx) cudaSetDevice(f->ctx->device);
+        delete f;
+    });
+}
+
+int svr_render(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam,
+               const svr_render_options* opts, svr_frame* frame) {
+    return guard([&] { render_impl(ctx, scene, cam, opts, frame); });
+}
+
+int svr_frame_get_info(svr_frame* f, svr_frame_info* out) {
+    return guard([&] {
+        require(f && out && f->scene, SVR_ERR_INVALID_ARGUMENT, "frame has not been rendered");
+        set_device(f->ctx);
+        out->width = f->W;
+        out->height = f->H;
+        out->ss_width = f->sw;
+        out->ss_height = f->sh;
+        out->tiles_x = f->ntx;
+        out->tiles_y = f->nty;
+        out->n_visible = count_visible(f);
+        out->n_entries = f->n_entries;
+        out->n_contribs = f->n_contribs;
+        out->sort_passes = f->sort_passes;
+        out->training = f->training;
+    });
+}
+
+int svr_frame_download(svr_frame* f, svr_buffer which, void* dst, size_t bytes) {
+    return guard([&] {
+        set_device(f->ctx);
+        BufView b = frame_buffer(f, which);
+        require(bytes == b.bytes, SVR_ERR_INVALID_ARGUMENT, "download size mismatch");
+        if (bytes)
+            SVR_CUDA(cudaMemcpyAsync(dst, b.p, bytes, cudaMemcpyDeviceToHost, f->ctx->stream));
+        SVR_CUDA(cudaStreamSynchronize(f->ctx->stream));
+    });
+}
+
+int svr_frame_device_ptr(svr_frame* f, svr_buffer which, void** ptr, size_t* bytes) {
+    return guard([&] {
+        set_device(f->ctx);
+        BufView b = frame_buffer(f, which);
+        *ptr = const_cast<void*>(b.p);
+        *bytes = b.bytes;
+    });
+}
+
+int svr_frame_records(svr_frame* f, uint32_t* pre_vids, uint64_t n_pre, uint32_t* contrib_pre,
+                      double* contrib_a, double* contrib_b, uint64_t n_contribs) {
+    return guard([&] {
+        require(f && f->has_records, SVR_ERR_RUNTIME, "frame has no forward records");
+        set_device(f->ctx);
+        cudaStream_t st = f->ctx->stream;
+        uint64_t nv = count_visible(f);
+        require(n_pre == nv, SVR_ERR_INVALID_ARGUMENT, "pre size mismatch");
+        require(n_contribs == f->n_contribs, SVR_ERR_INVALID_ARGUMENT, "contrib size mismatch");
+        const uint64_t N = f->n_voxels;
+        if (pre_vids && nv) {
+            std::vector<int4> rects(N);
+            SVR_CUDA(cudaMemcpy(rects.data(), f->rects.p, N * 16, cudaMemcpyDeviceToHost));
+            uint64_t k = 0;
+            for (uint64_t v = 0; v < N; ++v)
+                if (rects[v].y >= rects[v].x) pre_vids[k++] = uint32_t(v);
+        }
+        if (n_contribs && (contrib_pre || contrib_a || contrib_b)) {
+            DevBuf dp, da, db;
+            uint32_t* p = grow<uint32_t>(dp, n_contribs);
+            double* a = grow<double>(da, n_contribs);
+            double* b = grow<double>(db, n_contribs);
+            launch_contrib_segments(f->cam, f->ranges.as<uint2>(), f->vals[f->sorted_buf].as<uint32_t>(),
+                                    f->records.as<float4>(), f->pix_count.as<uint32_t>(),
+                                    f->pix_begin.as<uint32_t>(), f->contrib_entry.as<uint32_t>(),
+                                    f->visible_rank.as<uint32_t>(), p, a, b, f->ntx * f->nty, st);
+            if (contrib_pre) SVR_CUDA(cudaMemcpyAsync(contrib_pre, p, n_contribs * 4, cudaMemcpyDeviceToHost, st));
+            if (contrib_a) SVR_CUDA(cudaMemcpyAsync(contrib_a, a, n_contribs * 8, cudaMemcpyDeviceToHost, st));
+            if (contrib_b) SVR_CUDA(cudaMemcpyAsync(contrib_b, b, n_contribs * 8, cudaMemcpyDeviceToHost, st));
+            SVR_CUDA(cudaStreamSynchronize(st));
+        }
+    });
+}
+
+int svr_render_backward(svr_ctx* ctx, const svr_scene* scene, svr_frame* frame,
+                        const svr_upstream* up, svr_gradients* out) {
+    return guard([&] { backward_impl(ctx, scene, frame, up, out, false); });
+}
+
+int svr_l1_loss(svr_ctx* ctx, svr_frame* f, const float* gt, float* d_color, float* loss) {
+    return guard([&] {
+        require(ctx && f && gt && d_color, SVR_ERR_INVALID_ARGUMENT, "null argument");
+        set_device(ctx);
+        launch_l1_loss(f->out_color.as<float>(), gt, uint64_t(f->W) * f->H * 3, d_color, loss,
+                       ctx->stream);
+    });
+}
+
+int svr_train_step_l1(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam,
+                      const svr_render_options* opts, const float* gt_device, svr_frame* f,
+                      svr_gradients* grads, int accumulate, float* loss_device) {
+    return guard([&] {
+        require(opts && grads && grads->on_device, SVR_ERR_INVALID_ARGUMENT,
+                "train step needs device gradient buffers");
+        svr_render_options o = *opts;
+        o.training = 1;
+        render_impl(ctx, scene, cam, &o, f);
+        const uint64_t n = uint64_t(f->W) * f->H * 3;
+        float* dcol = grow<float>(f->l1_grad, n);
+        launch_l1_loss(f->out_color.as<float>(), gt_device, n, dcol, loss_device, ctx->stream);
+        svr_upstream up{};
+        up.d_color = dcol;
+        up.on_device = 1;
+        backward_impl(ctx, scene, f, &up, grads, accumulate != 0);
+    });
+}
+
+int svr_project_voxels(svr_ctx* ctx, const svr_camera* cam, uint64_t n, const double* centers,
+                       const double* sizes, double near_plane, uint8_t* visible, double* aabb,
+                       int32_t* rect) {
+    return guard([&] {
+        require(ctx && cam, SVR_ERR_INVALID_ARGUMENT, "null argument");
+        set_device(ctx);
+        if (n == 0) return;
+        cudaStream_t st = ctx->stream;
+        DevCamera dc = dev_camera(*cam);
+        DevBuf b;
+        b.reserve(n * (24 + 8 + 1 + 32 + 16) + 64);
+        char* p = b.as<char>();
+        double* dcen = reinterpret_cast<double*>(p);
+        double* dsz = dcen + 3 * n;
+        double* dab = dsz + n;
+        int* drc = reinterpret_cast<int*>(dab + 4 * n);
+        uint8_t* dvis = reinterpret_cast<uint8_t*>(drc + 4 * n);
+        SVR_CUDA(cudaMemcpyAsync(dcen, centers, n * 24, cudaMemcpyHostToDevice, st));
+        SVR_CUDA(cudaMemcpyAsync(dsz, sizes, n * 8, cudaMemcpyHostToDevice, st));
+        launch_project_batch(dc, n, dcen, dsz, near_plane, dvis, dab, drc, st);
+        SVR_CUDA(cudaMemcpyAsync(visible, dvis, n, cudaMemcpyDeviceToHost, st));
+        SVR_CUDA(cudaMemcpyAsync(aabb, dab, n * 32, cudaMemcpyDeviceToHost, st));
+        SVR_CUDA(cudaMemcpyAsync(rect, drc, n * 16, cudaMemcpyDeviceToHost, st));
+        SVR_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int svr_tile_sign_masks(svr_ctx* ctx, const svr_camera* cam, uint8_t* masks, uint64_t n_tiles) {
+    return guard([&] {
+        require(ctx && cam && masks, SVR_ERR_INVALID_ARGUMENT, "null argument");
+        set_device(ctx);
+        DevCamera dc = dev_camera(*cam);
+        require(n_tiles == uint64_t(dc.ntx) * dc.nty, SVR_ERR_INVALID_ARGUMENT,
+                "tile count mismatch");
+        if (!n_tiles) return;
+        DevBuf b;
+        b.reserve(n_tiles);
+        launch_tile_masks_only(dc, b.as<uint8_t>(), ctx->stream);
+        SVR_CUDA(cudaMemcpyAsync(masks, b.p, n_tiles, cudaMemcpyDeviceToHost, ctx->stream));
+        SVR_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int svr_build_sort_entries(svr_ctx* ctx, const svr_camera* cam, uint64_t scene_voxel_count,
+                           uint64_t n_pre, const uint32_t* vids, const uint64_t* codes,
+                           const int32_t* rects, uint64_t* keys, uint32_t* values,
+                           uint64_t capacity, uint64_t* n_out) {
+    return guard([&] {
+        require(ctx && cam && n_out, SVR_ERR_INVALID_ARGUMENT, "null argument");
+        set_device(ctx);
+        require(scene_voxel_count < (uint64_t(1) << 29), SVR_ERR_LENGTH,
+                "voxel count exceeds the 29-bit id capacity");
+        DevCamera dc = dev_camera(*cam);
+        require(uint64_t(dc.ntx) * dc.nty < (uint64_t(1) << 16), SVR_ERR_LENGTH,
+                "tile count exceeds the 16-bit id capacity");
+        cudaStream_t st = ctx->stream;
+        const int ntiles = dc.ntx * dc.nty;
+        const uint64_t n = n_pre;
+        DevBuf bm, bsat, bst, bv, bc, br, bcnt, boff, bk, bvals;
+        uint8_t* masks = grow<uint8_t>(bm, ntiles);
+        uint32_t* sat = grow<uint32_t>(bsat, uint64_t(dc.ntx + 1) * (dc.nty + 1));
+        FrameStatus* status = grow<FrameStatus>(bst, 1);
+        SVR_CUDA(cudaMemsetAsync(status, 0, sizeof(FrameStatus), st));
+        launch_tile_setup(dc, masks, sat, status, st);
+        uint32_t* dv = grow<uint32_t>(bv, n);
+        uint64_t* dcode = grow<uint64_t>(bc, n);
+        int4* drect = grow<int4>(br, n);
+        uint32_t* cnt = grow<uint32_t>(bcnt, n);
+        uint32_t* off = grow<uint32_t>(boff, n);
+        if (n) {
+            SVR_CUDA(cudaMemcpyAsync(dv, vids, n * 4, cudaMemcpyHostToDevice, st));
+            SVR_CUDA(cudaMemcpyAsync(dcode, codes, n * 8, cudaMemcpyHostToDevice, st));
+            SVR_CUDA(cudaMemcpyAsync(drect, rects, n * 16, cudaMemcpyHostToDevice, st));
+        }
+        launch_entry_counts(dc, n, drect, sat, cnt, st);
+        ctx->scratch.reserve(scan_scratch_bytes(n));
+        exclusive_scan_u32(cnt, off, n, &status->n_entries, ctx->scratch.p, st);
+        unsigned long long E = 0;
+        SVR_CUDA(cudaMemcpyAsync(&E, &status->n_entries, 8, cudaMemcpyDeviceToHost, st));
+        SVR_CUDA(cudaStreamSynchronize(st));
+        *n_out = E;
+        if (!keys) return;
+        require(capacity >= E, SVR_ERR_INVALID_ARGUMENT, "entry buffer too small");
+        uint64_t* dk = grow<uint64_t>(bk, E);
+        uint32_t* dvv = grow<uint32_t>(bvals, E);
+        launch_duplicate_list(dc, n, dv, dcode, drect, masks, off, dk, dvv, st);
+        if (E) {
+            SVR_CUDA(cudaMemcpyAsync(keys, dk, E * 8, cudaMemcpyDeviceToHost, st));
+            SVR_CUDA(cudaMemcpyAsync(values, dvv, E * 4, cudaMemcpyDeviceToHost, st));
+        }
+        SVR_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int svr_sort_entries(svr_ctx* ctx, uint64_t n, uint64_t* keys, uint32_t* values) {
+    return guard([&] {
+        require(ctx, SVR_ERR_INVALID_ARGUMENT, "null context");
+        set_device(ctx);
+        if (n <= 1) return;
+        // Only digits where some pair differs need a pass (stable LSD).
+        uint64_t kx = 0;
+        uint32_t vx = 0;
+        for (uint64_t i = 1; i < n; ++i) {
+            kx |= keys[i] ^ keys[0];
+            vx |= values[i] ^ values[0];
+        }
+        RadixPass passes[kMaxRadixPasses];
+        int np = 0;
+        auto add_range = [&](int src, uint64_t diff) {
+            if (!diff) return;
+            int lo = __builtin_ctzll(diff), hi = 64 - __builtin_clzll(diff);
+            for (int b = lo; b < hi; b += 8) passes[np++] = {src, b, std::min(8, hi - b)};
+        };
+        add_range(1, vx);
+        add_range(0, kx);
+        cudaStream_t st = ctx->stream;
+        DevBuf k0, v0, k1, v1;
+        uint64_t* dk0 = grow<uint64_t>(k0, n);
+        uint32_t* dv0 = grow<uint32_t>(v0, n);
+        uint64_t* dk1 = grow<uint64_t>(k1, n);
+        uint32_t* dv1 = grow<uint32_t>(v1, n);
+        SVR_CUDA(cudaMemcpyAsync(dk0, keys, n * 8, cudaMemcpyHostToDevice, st));
+        SVR_CUDA(cudaMemcpyAsync(dv0, values, n * 4, cudaMemcpyHostToDevice, st));
+        ctx->scratch2.reserve(sort_scratch_bytes(n, np));
+        int r = radix_sort_pairs(dk0, dv0, dk1, dv1, n, passes, np, ctx->scratch2.p, st);
+        SVR_CUDA(cudaMemcpyAsync(keys, r ? dk1 : dk0, n * 8, cudaMemcpyDeviceToHost, st));
+        SVR_CUDA(cudaMemcpyAsync(values, r ? dv1 : dv0, n * 4, cudaMemcpyDeviceToHost, st));
+        SVR_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+void svr_free(void* p) { std::free(p); }
+
+}  // extern "C"

@@ -1,0 +1,252 @@
+// sort.cu — hand-written onesweep LSD radix sort of (u64 key, u32 value).
+//
+// Replaces sort_entries (raster.cpp:174-178, std::sort by (key, value)).
+// Design (Adinets & Merrill, "Onesweep", 2022):
+//   1. one upsweep kernel builds the digit histograms of ALL passes in a
+//      single read of the keys;
+//   2. one kernel per pass: each CTA claims a partition via an atomic
+//      ticket (forward-progress order), ranks its keys with warp-level
+//      match.any multi-split, publishes its per-digit count and resolves its
+//      global offset by decoupled look-back over earlier partitions, then
+//      scatters through shared memory so global writes are digit-contiguous.
+// Each pass reads and writes every pair once (12 B + 12 B). The sort is
+// stable, so sorting only the key bits that can differ (the caller decides,
+// see capi.cu) reproduces the full (key, value) order exactly.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "svr_internal.h"
+#include "svr_kernels.h"
+
+namespace svrb {
+
+namespace {
+
+constexpr int kRadix = 256;
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kItems = 12;
+constexpr int kTileKeys = kThreads * kItems;  // 3072 pairs per partition
+constexpr uint32_t kFlagAgg = 1u << 30;
+constexpr uint32_t kFlagInc = 2u << 30;
+constexpr uint32_t kValMask = (1u << 30) - 1;
+
+struct PassSpec {
+    int n;
+    RadixPass p[kMaxRadixPasses];
+};
+
+__device__ __forceinline__ uint32_t digit_of(uint64_t k, uint32_t v, RadixPass p) {
+    uint64_t w = p.src == 0 ? k : uint64_t(v);
+    return uint32_t(w >> p.shift) & ((1u << p.bits) - 1u);
+}
+
+__global__ void __launch_bounds__(kThreads) hist_kernel(const uint64_t* keys, const uint32_t* vals,
+                                                        uint64_t n, PassSpec spec,
+                                                        uint32_t* hist) {
+    __shared__ uint32_t s_hist[kMaxRadixPasses][kRadix];
+    for (int i = threadIdx.x; i < spec.n * kRadix; i += kThreads) (&s_hist[0][0])[i] = 0;
+    __syncthreads();
+    for (uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * kThreads) {
+        uint64_t k = keys[i];
+        uint32_t v = vals[i];
+        for (int p = 0; p < spec.n; ++p) atomicAdd(&s_hist[p][digit_of(k, v, spec.p[p])], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < spec.n * kRadix; i += kThreads) {
+        uint32_t c = (&s_hist[0][0])[i];
+        if (c) atomicAdd(&hist[i], c);
+    }
+}
+
+// One block per pass: exclusive scan of the 256 digit counts.
+__global__ void __launch_bounds__(kRadix) bin_scan_kernel(uint32_t* hist) {
+    __shared__ uint32_t s[kRadix];
+    uint32_t* h = hist + blockIdx.x * kRadix;
+    uint32_t v = h[threadIdx.x];
+    s[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < kRadix; o <<= 1) {
+        uint32_t t = threadIdx.x >= o ? s[threadIdx.x - o] : 0;
+        __syncthreads();
+        s[threadIdx.x] += t;
+        __syncthreads();
+    }
+    h[threadIdx.x] = s[threadIdx.x] - v;
+}
+
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
+    asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(p), "r"(v));
+}
+
+__global__ void __launch_bounds__(kThreads) onesweep_kernel(
+    const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+    uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint64_t n, RadixPass pass,
+    const uint32_t* __restrict__ bin_base, uint32_t* status, uint32_t* ticket) {
+    __shared__ uint32_t s_warp_hist[kWarps][kRadix + 1];
+    __shared__ uint32_t s_block_excl[kRadix];
+    __shared__ uint32_t s_global[kRadix];
+    __shared__ uint64_t s_keys[kTileKeys];
+    __shared__ uint32_t s_vals[kTileKeys];
+    __shared__ uint32_t s_part;
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_part = atomicAdd(ticket, 1u);
+    for (int i = threadIdx.x; i < kWarps * (kRadix + 1); i += kThreads)
+        (&s_warp_hist[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t part = s_part;
+    const uint64_t base = uint64_t(part) * kTileKeys;
+    const uint64_t wbase = base + uint64_t(warp) * 32 * kItems;
+
+    uint64_t k[kItems];
+    uint32_t v[kItems], d[kItems], r[kItems];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+        uint64_t idx = wbase + uint64_t(i) * 32 + lane;
+        if (idx < n) {
+            k[i] = keys_in[idx];
+            v[i] = vals_in[idx];
+            d[i] = digit_of(k[i], v[i], pass);
+        } else {
+            k[i] = 0;
+            v[i] = 0;
+            d[i] = kRadix;  // out of range: ranked into a discarded bin
+        }
+    }
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    uint32_t* wh = s_warp_hist[warp];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+        uint32_t peers = __match_any_sync(0xffffffffu, d[i]);
+        uint32_t below = __popc(peers & lt_mask);
+        uint32_t prev = wh[d[i]];
+        r[i] = prev + below;
+        __syncwarp();
+        if (below == 0) wh[d[i]] = prev + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+
+    // Per digit: exclusive offsets across warps, block total, block-wide
+    // exclusive scan over digits, decoupled look-back for the global base.
+    const int dg = threadIdx.x;  // kThreads == kRadix
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+        uint32_t t = s_warp_hist[w][dg];
+        s_warp_hist[w][dg] = cnt;
+        cnt += t;
+    }
+    uint32_t* my_status = status + uint64_t(part) * kRadix + dg;
+    if (part == 0)
+        st_volatile(my_status, kFlagInc | cnt);
+    else
+        st_volatile(my_status, kFlagAgg | cnt);
+
+    // block-wide exclusive scan of cnt over digits
+    s_block_excl[dg] = cnt;
+    __syncthreads();
+    for (int o = 1; o < kRadix; o <<= 1) {
+        uint32_t t = dg >= o ? s_block_excl[dg - o] : 0;
+        __syncthreads();
+        s_block_excl[dg] += t;
+        __syncthreads();
+    }
+    const uint32_t block_excl = s_block_excl[dg] - cnt;
+    __syncthreads();
+    s_block_excl[dg] = block_excl;
+
+    uint32_t excl = 0;
+    if (part > 0) {
+        int64_t p = int64_t(part) - 1;
+        while (p >= 0) {
+            uint32_t s = ld_volatile(status + uint64_t(p) * kRadix + dg);
+            if ((s & ~kValMask) == 0) continue;  // not published yet
+            excl += s & kValMask;
+            if (s & kFlagInc) break;
+            --p;
+        }
+        st_volatile(my_status, kFlagInc | (excl + cnt));
+    }
+    s_global[dg] = bin_base[dg] + excl - block_excl;
+    __syncthreads();
+
+    // Scatter to shared memory in digit order, then out to global.
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+        if (d[i] < kRadix) {
+            uint32_t pos = s_block_excl[d[i]] + s_warp_hist[warp][d[i]] + r[i];
+            s_keys[pos] = k[i];
+            s_vals[pos] = v[i];
+        }
+    }
+    __syncthreads();
+    const uint32_t tile_n = uint32_t(min(uint64_t(kTileKeys), n - base));
+    for (uint32_t pos = threadIdx.x; pos < tile_n; pos += kThreads) {
+        uint64_t kk = s_keys[pos];
+        uint32_t vv = s_vals[pos];
+        uint32_t dd = digit_of(kk, vv, pass);
+        uint64_t o = uint64_t(s_global[dd]) + pos;
+        keys_out[o] = kk;
+        vals_out[o] = vv;
+    }
+}
+
+}  // namespace
+
+size_t sort_scratch_bytes(uint64_t n, int npasses) {
+    uint64_t nparts = (n + kTileKeys - 1) / kTileKeys;
+    return size_t(npasses) * kRadix * 4          // histograms / bin bases
+           + size_t(npasses) * 4 + 64            // tickets
+           + size_t(nparts + 1) * kRadix * 4;    // look-back status
+}
+
+int radix_sort_pairs(uint64_t* keys0, uint32_t* vals0, uint64_t* keys1, uint32_t* vals1,
+                     uint64_t n, const RadixPass* passes, int npasses, void* scratch,
+                     cudaStream_t st) {
+    if (n <= 1 || npasses == 0) return 0;
+    if (npasses > kMaxRadixPasses) throw Error(SVR_ERR_RUNTIME, "too many radix passes");
+    if (n >= (uint64_t(1) << 30))
+        throw Error(SVR_ERR_LENGTH, "sort supports fewer than 2^30 entries");
+    PassSpec spec{};
+    spec.n = npasses;
+    for (int i = 0; i < npasses; ++i) spec.p[i] = passes[i];
+    uint64_t nparts = (n + kTileKeys - 1) / kTileKeys;
+    char* s = static_cast<char*>(scratch);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(s);
+    uint32_t* tickets = reinterpret_cast<uint32_t*>(s + size_t(npasses) * kRadix * 4);
+    uint32_t* status =
+        reinterpret_cast<uint32_t*>(s + size_t(npasses) * kRadix * 4 + size_t(npasses) * 4 + 64);
+    SVR_CUDA(cudaMemsetAsync(hist, 0, size_t(npasses) * kRadix * 4 + size_t(npasses) * 4 + 64, st));
+    int hist_blocks = int(std::min<uint64_t>((n + kThreads - 1) / kThreads, 148 * 4));
+    hist_kernel<<<hist_blocks, kThreads, 0, st>>>(keys0, vals0, n, spec, hist);
+    SVR_LAUNCH("hist_kernel");
+    bin_scan_kernel<<<npasses, kRadix, 0, st>>>(hist);
+    SVR_LAUNCH("bin_scan_kernel");
+    uint64_t* kin = keys0;
+    uint32_t* vin = vals0;
+    uint64_t* kout = keys1;
+    uint32_t* vout = vals1;
+    int cur = 0;
+    for (int p = 0; p < npasses; ++p) {
+        SVR_CUDA(cudaMemsetAsync(status, 0, size_t(nparts) * kRadix * 4, st));
+        onesweep_kernel<<<unsigned(nparts), kThreads, 0, st>>>(kin, vin, kout, vout, n, passes[p],
+                                                              hist + p * kRadix, status,
+                                                              tickets + p);
+        SVR_LAUNCH("onesweep_kernel");
+        std::swap(kin, kout);
+        std::swap(vin, vout);
+        cur ^= 1;
+    }
+    return cur;
+}
+
+}  // namespace svrb

@@ -1,0 +1,97 @@
+// svr_internal.h — host-side objects behind the C ABI (include/svr_b200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "svr_b200.h"
+#include "svr_math.cuh"
+
+namespace svrb {
+
+// Errors carry the svr_status they map to (and thereby the reference
+// exception type the C++ drop-in rethrows).
+struct Error : std::runtime_error {
+    int status;
+    Error(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+void cuda_check(cudaError_t e, const char* what);
+#define SVR_CUDA(x) ::svrb::cuda_check((x), #x)
+#define SVR_LAUNCH(what) ::svrb::cuda_check(cudaGetLastError(), what)
+
+// Grow-only device allocation; contents are not preserved across growth.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void reserve(size_t n);
+    void release();
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+    ~DevBuf() { release(); }
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+};
+
+// Pinned host staging buffer, grow-only.
+struct HostBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void reserve(size_t n);
+    ~HostBuf();
+};
+
+}  // namespace svrb
+
+struct svr_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+    bool debug = false;
+    svrb::DevBuf scratch;   // sort/scan temporaries
+    svrb::DevBuf scratch2;
+    svrb::HostBuf pinned;   // small readbacks
+};
+
+struct svr_scene {
+    uint64_t n_voxels = 0, n_pool = 0;
+    int sh_degree = 3, sh_stride = 48;
+    int max_level = 1;
+    double bounds_center[3] = {0, 0, 0};
+    double bounds_size = 1.0;
+    svrb::DevBuf paths;         // u64: code | level << 48
+    svrb::DevBuf corner_index;  // u32 [n][8]
+    svrb::DevBuf density;       // f32 [n_pool]
+    svrb::DevBuf sh;            // f32 [n][stride]
+};
+
+// Per-view state. Also the device half of svr::ForwardRecords.
+struct svr_frame {
+    svr_ctx* ctx = nullptr;
+    const svr_scene* scene = nullptr;
+    svr_render_options opts{};
+    svrb::DevCamera cam{};     // supersampled camera actually rendered with
+    svr_camera ss_cam{};       // same, ABI form
+    int W = 0, H = 0, sw = 0, sh = 0, ntx = 0, nty = 0;
+    uint64_t n_voxels = 0;
+    uint64_t n_visible = 0, n_entries = 0, n_contribs = 0;
+    int sort_passes = 0;
+    bool training = false;
+    bool has_records = false;
+
+    svrb::DevBuf tile_masks, tile_sat, rects, aabb, records, counts, offsets, visible_rank;
+    svrb::DevBuf keys[2], vals[2], dbg_keys, dbg_vals, ranges;
+    svrb::DevBuf out_color, out_depth, out_median, out_normal, out_tfin, max_blend;
+    svrb::DevBuf ss_color, ss_depth, ss_median, ss_normal, ss_tfin;
+    svrb::DevBuf pix_count, pix_begin, contrib_entry, contrib_T;
+    svrb::DevBuf taps;  // resampler tables
+    svrb::DevBuf bwd_gc, bwd_gn, bwd_lift, bwd_dcolor, status, l1_grad;
+    int sorted_buf = 0;  // which of keys[]/vals[] holds the sorted list
+    int tap_src_w = -1, tap_src_h = -1, tap_dst_w = -1, tap_dst_h = -1;
+    int n_taps_x = 0, n_taps_y = 0;
+};

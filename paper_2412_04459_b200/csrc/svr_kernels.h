@@ -1,0 +1,184 @@
+// svr_kernels.h — host launchers for the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "svr_math.cuh"
+
+namespace svrb {
+
+// ---- scan.cu ---------------------------------------------------------------
+// Exclusive prefix sum of n u32 values; writes the u64 grand total to
+// *total (device). `scratch` must hold scan_scratch_bytes(n).
+size_t scan_scratch_bytes(uint64_t n);
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, unsigned long long* total,
+                        void* scratch, cudaStream_t st);
+
+// ---- sort.cu ---------------------------------------------------------------
+// One LSD digit: bits [shift, shift+bits) of the key (src 0) or value (src 1).
+struct RadixPass {
+    int src;
+    int shift;
+    int bits;  // 1..8
+};
+constexpr int kMaxRadixPasses = 16;
+size_t sort_scratch_bytes(uint64_t n, int npasses);
+// Stable LSD onesweep sort of (key, value) pairs over the given digits.
+// Ping-pongs between buffer 0 and 1; returns the index holding the result.
+int radix_sort_pairs(uint64_t* keys0, uint32_t* vals0, uint64_t* keys1, uint32_t* vals1,
+                     uint64_t n, const RadixPass* passes, int npasses, void* scratch,
+                     cudaStream_t st);
+
+// ---- raster.cu -------------------------------------------------------------
+struct FrameStatus {          // device -> host summary, one read per frame
+    unsigned long long n_entries;
+    unsigned int pattern_or;  // OR of all tile sign masks
+    unsigned int pad;
+    unsigned long long n_contribs;
+};
+
+void launch_tile_setup(const DevCamera& cam, uint8_t* masks, uint32_t* sat, FrameStatus* status,
+                       cudaStream_t st);
+
+struct PreprocessArgs {
+    uint64_t n;
+    const uint64_t* paths;
+    const uint32_t* corner_index;
+    const float* density;
+    const float* sh;
+    int sh_degree, sh_stride;
+    double bc[3];
+    double bsize;
+    double near_plane;
+    const uint32_t* tile_sat;
+    int4* rects;
+    double4* aabb;  // optional
+    float4* records;
+    uint32_t* counts;
+};
+void launch_preprocess(const DevCamera& cam, const PreprocessArgs& a, cudaStream_t st);
+
+void launch_duplicate(const DevCamera& cam, uint64_t n, const uint64_t* paths, const int4* rects,
+                      const uint8_t* masks, const uint32_t* counts, const uint32_t* offsets,
+                      uint64_t* keys, uint32_t* vals, cudaStream_t st);
+
+void launch_tile_ranges(const uint64_t* keys, uint64_t n, uint2* ranges, int ntiles,
+                        cudaStream_t st);
+
+struct CompositeArgs {
+    const uint2* ranges;
+    const uint32_t* vals;
+    const float4* records;
+    int K;
+    float t_threshold;
+    float bg[3];
+    float far_sentinel;
+    float* color;   // sw*sh*3
+    float* depth;
+    float* median;
+    float* normal;
+    float* tfin;
+    uint32_t* pix_count;        // tile-major [ntiles*256], optional
+    unsigned int* max_blend;    // per voxel, optional (float bits)
+    // record pass
+    const uint32_t* pix_begin;  // tile-major
+    uint32_t* contrib_entry;
+    float* contrib_T;
+};
+void launch_composite(const DevCamera& cam, const CompositeArgs& a, bool record_pass,
+                      cudaStream_t st);
+
+// Area resampler (image.cpp:9-45): CSR taps per destination index.
+struct TapTable {
+    const int* ptr_x;  // dst_w+1
+    const int* idx_x;
+    const float* w_x;
+    const int* ptr_y;  // dst_h+1
+    const int* idx_y;
+    const float* w_y;
+};
+// Downsamples `nch` interleaved channel images src (sw x sh) -> dst (W x H).
+void launch_downsample(const TapTable& t, const float* src, int channels, int sw, float* dst,
+                       int W, int H, cudaStream_t st);
+
+// Gathers tile-major per-pixel values into row-major image order.
+void launch_tile_to_image_u32(const uint32_t* tm, uint32_t* img, int sw, int sh, int ntx,
+                              cudaStream_t st);
+
+// Visible rank (pre index) per voxel: 1 where rect is non-empty.
+void launch_visible_flags(const int4* rects, uint64_t n, uint32_t* flags, cudaStream_t st);
+
+// Contribution segments (a, b) in double for ForwardRecords materialisation.
+void launch_contrib_segments(const DevCamera& cam, const uint2* ranges, const uint32_t* vals,
+                             const float4* records, const uint32_t* pix_count,
+                             const uint32_t* pix_begin, const uint32_t* contrib_entry,
+                             const uint32_t* pre_rank, uint32_t* contrib_pre, double* a,
+                             double* b, int ntiles, cudaStream_t st);
+
+// ---- backward.cu -----------------------------------------------------------
+// Adjoint of the area resampler (image.cpp:47-60); transposed CSR taps.
+void launch_lift(const TapTable& transposed, const float* g, int channels, int W, float* out,
+                 int sw, int sh, cudaStream_t st);
+
+void launch_l1_loss(const float* color, const float* gt, uint64_t n, float* d_color, float* loss,
+                    cudaStream_t st);
+
+struct BackwardArgs {
+    const uint2* ranges;
+    const uint32_t* vals;
+    const float4* records;
+    const uint32_t* corner_index;
+    int K;
+    float bg[3];
+    const float* gC;  // ss res, optional
+    const float* gD;
+    const float* gN;
+    const float* gT;
+    const float* d_weight;       // per contrib, optional
+    const float* d_voxel_color;  // per contrib x3, optional
+    const uint32_t* pix_count;   // tile-major
+    const uint32_t* pix_begin;
+    const uint32_t* contrib_entry;
+    const float* contrib_T;
+    float* g_density;
+    float* g_color;   // per voxel x3 (scratch)
+    float* g_normal;  // per voxel x3 (scratch)
+    float* g_priority;
+};
+void launch_composite_backward(const DevCamera& cam, const BackwardArgs& a, cudaStream_t st);
+
+struct EpilogueArgs {
+    uint64_t n;
+    const uint64_t* paths;
+    const int4* rects;
+    const float4* records;
+    const uint32_t* corner_index;
+    const float* sh;
+    int sh_degree, sh_stride;
+    double bc[3];
+    double bsize;
+    const float* g_color;
+    const float* g_normal;
+    float* g_sh;
+    float* g_density;
+    int accumulate;
+};
+void launch_voxel_epilogue(const DevCamera& cam, const EpilogueArgs& a, cudaStream_t st);
+
+// ---- pieces (batch utilities for the drop-in's pipeline functions) ---------
+void launch_project_batch(const DevCamera& cam, uint64_t n, const double* centers,
+                          const double* sizes, double near_plane, uint8_t* visible,
+                          double* aabb, int* rect, cudaStream_t st);
+void launch_tile_masks_only(const DevCamera& cam, uint8_t* masks, cudaStream_t st);
+void launch_entry_counts(const DevCamera& cam, uint64_t n, const int4* rects,
+                         const uint32_t* sat, uint32_t* counts, cudaStream_t st);
+void launch_duplicate_list(const DevCamera& cam, uint64_t n, const uint32_t* vids,
+                           const uint64_t* codes, const int4* rects, const uint8_t* masks,
+                           const uint32_t* offsets, uint64_t* keys, uint32_t* vals,
+                           cudaStream_t st);
+
+constexpr int kRecordF4 = 7;  // float4 slots per voxel record (112 B)
+
+}  // namespace svrb

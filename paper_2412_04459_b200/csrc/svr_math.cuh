@@ -1,0 +1,295 @@
+// svr_math.cuh — per-voxel math shared by the sm_100a kernels.
+//
+// Two precision regimes, as the parity contract demands (SURVEY §7 hard
+// part 1, §8(a)):
+//   * fp64, bit-exact with the reference's double arithmetic: voxel geometry
+//     (octree.hpp:68-90), corner projection + padded AABB + tile rect
+//     (raster.cpp:72-118), per-pixel ray direction and sign bits
+//     (camera.hpp:24-27, octree.hpp:93-95), tile sign patterns
+//     (raster.cpp:120-142). Every operation goes through an explicitly
+//     rounded intrinsic (__dadd_rn, __dmul_rn, ...) in the same evaluation
+//     order the reference's C++ uses, so no FMA contraction can occur
+//     regardless of compiler flags. The host copy (used only by the C++
+//     drop-in's camera scaling) compiles the same expressions with
+//     -ffp-contract=off.
+//   * fp32, tolerance-checked: ray/box slab test, K-point alpha quadrature,
+//     depth, SH colour, normals (field.hpp:23-201, sh.hpp:18-83).
+#pragma once
+
+#include <cstdint>
+
+#if defined(__CUDACC__)
+#define SVR_HD __host__ __device__ __forceinline__
+#else
+#define SVR_HD inline
+#endif
+
+namespace svrb {
+
+constexpr int kTile = 16;
+constexpr int kMaxLevel = 16;
+constexpr uint64_t kGroupOnes = 0x249249249249ull;  // octree.hpp:19
+constexpr double kAabbPad = 1e-6;                     // raster.cpp:11
+constexpr float kExplinKnee = 1.1f;                   // field.hpp:19
+
+// ---------------------------------------------------------------- fp64 exact
+#if defined(__CUDA_ARCH__)
+SVR_HD double dadd(double a, double b) { return __dadd_rn(a, b); }
+SVR_HD double dsub(double a, double b) { return __dsub_rn(a, b); }
+SVR_HD double dmul(double a, double b) { return __dmul_rn(a, b); }
+SVR_HD double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+#else
+SVR_HD double dadd(double a, double b) { return a + b; }
+SVR_HD double dsub(double a, double b) { return a - b; }
+SVR_HD double dmul(double a, double b) { return a * b; }
+SVR_HD double ddiv(double a, double b) { return a / b; }
+#endif
+
+// Camera as the kernels see it (svr::Camera, camera.hpp:13-49).
+struct DevCamera {
+    int W, H, ntx, nty;
+    double fx, fy, cx, cy;
+    double rot[9];  // camera-to-world, row-major
+    double pos[3];
+};
+
+// Mat3 * Vec3 in geom.hpp:73-76 order: (m0*x + m1*y) + m2*z per row.
+SVR_HD void mat_vec(const double* m, double x, double y, double z, double* o) {
+    o[0] = dadd(dadd(dmul(m[0], x), dmul(m[1], y)), dmul(m[2], z));
+    o[1] = dadd(dadd(dmul(m[3], x), dmul(m[4], y)), dmul(m[5], z));
+    o[2] = dadd(dadd(dmul(m[6], x), dmul(m[7], y)), dmul(m[8], z));
+}
+
+// rot.transposed() * v (camera.hpp:29): row r of the transpose = column r.
+SVR_HD void mat_t_vec(const double* m, double x, double y, double z, double* o) {
+    o[0] = dadd(dadd(dmul(m[0], x), dmul(m[3], y)), dmul(m[6], z));
+    o[1] = dadd(dadd(dmul(m[1], x), dmul(m[4], y)), dmul(m[7], z));
+    o[2] = dadd(dadd(dmul(m[2], x), dmul(m[5], y)), dmul(m[8], z));
+}
+
+// Camera::pixel_ray direction (camera.hpp:24-27), unnormalised.
+SVR_HD void pixel_ray_dir(const DevCamera& c, double px, double py, double* d) {
+    double cxd = ddiv(dsub(dadd(px, 0.5), c.cx), c.fx);
+    double cyd = ddiv(dsub(dadd(py, 0.5), c.cy), c.fy);
+    mat_vec(c.rot, cxd, cyd, 1.0, d);
+}
+
+// ray_sign_bits (octree.hpp:93-95): bit2 = x<0, bit1 = y<0, bit0 = z<0.
+SVR_HD uint32_t sign_bits(const double* d) {
+    return 4u * (d[0] < 0.0) + 2u * (d[1] < 0.0) + 1u * (d[2] < 0.0);
+}
+
+// int(double) as the reference's x86-64 build executes it (cvttsd2si):
+// truncation, and INT_MIN for anything outside the int32 range.
+SVR_HD int x86_double_to_int(double f) {
+    return (f > -2147483649.0 && f < 2147483648.0) ? int(f) : int(0x80000000u);
+}
+
+SVR_HD int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// to_voxel_index (octree.hpp:68-82) + voxel_geometry (octree.hpp:85-90).
+// Levels/paths are validated once at upload, so no checks here.
+SVR_HD void voxel_geometry(uint64_t code, int level, const double* bc, double bsize,
+                           double* center, double* size) {
+    uint64_t c = code >> (3 * (kMaxLevel - level));
+    uint32_t i = 0, j = 0, k = 0;
+    for (int n = 0; n < level; ++n) {
+        i |= uint32_t((c >> 2) & 1) << n;
+        j |= uint32_t((c >> 1) & 1) << n;
+        k |= uint32_t(c & 1) << n;
+        c >>= 3;
+    }
+    double s = ldexp(bsize, -level);
+    double half_root = dmul(0.5, bsize);
+    center[0] = dadd(dsub(bc[0], half_root), dmul(s, dadd(double(i), 0.5)));
+    center[1] = dadd(dsub(bc[1], half_root), dmul(s, dadd(double(j), 0.5)));
+    center[2] = dadd(dsub(bc[2], half_root), dmul(s, dadd(double(k), 0.5)));
+    *size = s;
+}
+
+struct Projection {
+    double x0, x1, y0, y1;
+    int tx0, tx1, ty0, ty1;
+};
+
+// project_voxel (raster.cpp:72-118), bit-exact. Returns false when culled;
+// then tx0=0, tx1=-1, ty0=0, ty1=-1 exactly like a fresh PreVoxel.
+SVR_HD bool project_voxel(const DevCamera& cam, const double* center, double size, double near,
+                          Projection& out) {
+    out.tx0 = 0;
+    out.tx1 = -1;
+    out.ty0 = 0;
+    out.ty1 = -1;
+    out.x0 = out.x1 = out.y0 = out.y1 = 0.0;
+    bool any_front = false, any_behind = false;
+    const double inf = __builtin_huge_val();
+    double x0 = inf, x1 = -inf, y0 = inf, y1 = -inf;
+    double h = dmul(0.5, size);
+    for (int c = 0; c < 8; ++c) {
+        double px = dadd(center[0], ((c >> 2) & 1) ? h : -h);
+        double py = dadd(center[1], ((c >> 1) & 1) ? h : -h);
+        double pz = dadd(center[2], (c & 1) ? h : -h);
+        double pc[3];
+        mat_t_vec(cam.rot, dsub(px, cam.pos[0]), dsub(py, cam.pos[1]), dsub(pz, cam.pos[2]), pc);
+        if (pc[2] <= near) {
+            any_behind = true;
+            continue;
+        }
+        any_front = true;
+        double u = dadd(ddiv(dmul(cam.fx, pc[0]), pc[2]), cam.cx);
+        double v = dadd(ddiv(dmul(cam.fy, pc[1]), pc[2]), cam.cy);
+        x0 = (u < x0) ? u : x0;  // std::min(x0, u)
+        x1 = (x1 < u) ? u : x1;  // std::max(x1, u)
+        y0 = (v < y0) ? v : y0;
+        y1 = (y1 < v) ? v : y1;
+    }
+    if (!any_front) return false;
+    if (any_behind) {
+        x0 = 0;
+        x1 = cam.W;
+        y0 = 0;
+        y1 = cam.H;
+    }
+    x0 = dsub(x0, kAabbPad);
+    x1 = dadd(x1, kAabbPad);
+    y0 = dsub(y0, kAabbPad);
+    y1 = dadd(y1, kAabbPad);
+    if (x1 < 0 || y1 < 0 || x0 > cam.W || y0 > cam.H) return false;
+    out.x0 = x0;
+    out.x1 = x1;
+    out.y0 = y0;
+    out.y1 = y1;
+    out.tx0 = clampi(x86_double_to_int(floor(ddiv(x0, double(kTile)))), 0, cam.ntx - 1);
+    out.tx1 = clampi(x86_double_to_int(floor(ddiv(x1, double(kTile)))), 0, cam.ntx - 1);
+    out.ty0 = clampi(x86_double_to_int(floor(ddiv(y0, double(kTile)))), 0, cam.nty - 1);
+    out.ty1 = clampi(x86_double_to_int(floor(ddiv(y1, double(kTile)))), 0, cam.nty - 1);
+    return true;
+}
+
+// tile_sign_patterns (raster.cpp:120-142) as a bitmask over s in [0,8).
+SVR_HD uint32_t tile_sign_mask(const DevCamera& cam, int tx, int ty) {
+    int px0 = tx * kTile, py0 = ty * kTile;
+    int px1 = px0 + kTile - 1 < cam.W - 1 ? px0 + kTile - 1 : cam.W - 1;
+    int py1 = py0 + kTile - 1 < cam.H - 1 ? py0 + kTile - 1 : cam.H - 1;
+    bool neg[3] = {false, false, false}, nonneg[3] = {false, false, false};
+    for (int yi = 0; yi < 2; ++yi)
+        for (int xi = 0; xi < 2; ++xi) {
+            double d[3];
+            pixel_ray_dir(cam, double(xi ? px1 : px0), double(yi ? py1 : py0), d);
+            for (int ax = 0; ax < 3; ++ax) (d[ax] < 0.0 ? neg[ax] : nonneg[ax]) = true;
+        }
+    uint32_t mask = 0;
+    for (uint32_t s = 0; s < 8; ++s) {
+        bool ok = true;
+        for (int ax = 0; ax < 3; ++ax) {
+            bool want_neg = (s >> (2 - ax)) & 1;
+            if (want_neg ? !neg[ax] : !nonneg[ax]) ok = false;
+        }
+        if (ok) mask |= 1u << s;
+    }
+    return mask;
+}
+
+// ---------------------------------------------------------------- fp32 field
+// explin (field.hpp:23-26) and its derivative (field.hpp:28-31).
+#if defined(__CUDA_ARCH__)
+__device__ __forceinline__ float fexp(float x) { return __expf(x); }
+#else
+inline float fexp(float x) { return expf(x); }
+#endif
+// exp(x/1.1 - 1 + ln 1.1) = exp(x/1.1) * (1.1/e)
+constexpr float kExplinScale = 0.40467196f;  // 1.1 / e
+SVR_HD float explin(float x) { return x > kExplinKnee ? x : fexp(x * (1.0f / 1.1f)) * kExplinScale; }
+SVR_HD float explin_deriv(float x) {
+    return x > kExplinKnee ? 1.0f : fexp(x * (1.0f / 1.1f)) * (kExplinScale / 1.1f);
+}
+
+// trilinear (field.hpp:33-47), corner order (i<<2)|(j<<1)|k.
+SVR_HD float trilinear(const float* V, float qx, float qy, float qz) {
+    float wx0 = 1.0f - qx, wy0 = 1.0f - qy, wz0 = 1.0f - qz;
+    float a00 = V[0] * wz0 + V[1] * qz;
+    float a01 = V[2] * wz0 + V[3] * qz;
+    float a10 = V[4] * wz0 + V[5] * qz;
+    float a11 = V[6] * wz0 + V[7] * qz;
+    float b0 = a00 * wy0 + a01 * qy;
+    float b1 = a10 * wy0 + a11 * qy;
+    return b0 * wx0 + b1 * qx;
+}
+
+SVR_HD void trilinear_weights(float qx, float qy, float qz, float* w) {
+    float wx[2] = {1.0f - qx, qx}, wy[2] = {1.0f - qy, qy}, wz[2] = {1.0f - qz, qz};
+#pragma unroll
+    for (int c = 0; c < 8; ++c) w[c] = wx[(c >> 2) & 1] * wy[(c >> 1) & 1] * wz[c & 1];
+}
+
+// density_gradient + voxel_normal (field.hpp:132-154).
+SVR_HD void density_gradient(const float* V, float* g) {
+    g[0] = 0.25f * ((V[4] + V[5] + V[6] + V[7]) - (V[0] + V[1] + V[2] + V[3]));
+    g[1] = 0.25f * ((V[2] + V[3] + V[6] + V[7]) - (V[0] + V[1] + V[4] + V[5]));
+    g[2] = 0.25f * ((V[1] + V[3] + V[5] + V[7]) - (V[0] + V[2] + V[4] + V[6]));
+}
+
+SVR_HD void voxel_normal(const float* V, float* n) {
+    float g[3];
+    density_gradient(V, g);
+    float len = sqrtf(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+    if (len == 0.0f) {
+        n[0] = n[1] = n[2] = 0.0f;
+        return;
+    }
+    float inv = 1.0f / len;
+    n[0] = g[0] * inv;
+    n[1] = g[1] * inv;
+    n[2] = g[2] * inv;
+}
+
+// voxel_normal_backward (field.hpp:158-170).
+SVR_HD void voxel_normal_backward(const float* V, const float* dn, float* gV) {
+    float g[3];
+    density_gradient(V, g);
+    float len = sqrtf(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+    if (len == 0.0f) {
+        for (int c = 0; c < 8; ++c) gV[c] = 0.0f;
+        return;
+    }
+    float inv = 1.0f / len;
+    float n[3] = {g[0] * inv, g[1] * inv, g[2] * inv};
+    float dot = dn[0] * n[0] + dn[1] * n[1] + dn[2] * n[2];
+    float gx = (dn[0] - n[0] * dot) * inv, gy = (dn[1] - n[1] * dot) * inv,
+          gz = (dn[2] - n[2] * dot) * inv;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        float si = ((c >> 2) & 1) ? 1.0f : -1.0f;
+        float sj = ((c >> 1) & 1) ? 1.0f : -1.0f;
+        float sk = (c & 1) ? 1.0f : -1.0f;
+        gV[c] = 0.25f * (gx * si + gy * sj + gz * sk);
+    }
+}
+
+// sh_basis (sh.hpp:18-45), 3DGS ordering and constants.
+SVR_HD int sh_basis(int degree, float x, float y, float z, float* b) {
+    b[0] = 0.28209479177387814f;
+    if (degree < 1) return 1;
+    const float C1 = 0.4886025119029199f;
+    b[1] = -C1 * y;
+    b[2] = C1 * z;
+    b[3] = -C1 * x;
+    if (degree < 2) return 4;
+    float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    b[4] = 1.0925484305920792f * xy;
+    b[5] = -1.0925484305920792f * yz;
+    b[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
+    b[7] = -1.0925484305920792f * xz;
+    b[8] = 0.5462742152960396f * (xx - yy);
+    if (degree < 3) return 9;
+    b[9] = -0.5900435899266435f * y * (3.0f * xx - yy);
+    b[10] = 2.890611442640554f * xy * z;
+    b[11] = -0.4570457994644658f * y * (4.0f * zz - xx - yy);
+    b[12] = 0.3731763325901154f * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+    b[13] = -0.4570457994644658f * x * (4.0f * zz - xx - yy);
+    b[14] = 1.445305721320277f * z * (xx - yy);
+    b[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
+    return 16;
+}
+
+}  // namespace svrb

@@ -1,0 +1,66 @@
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
+
+
+@pytest.fixture(scope="session")
+def svr():
+    import paper_2412_04459_b200 as m
+    m.load_library()
+    return m
+
+
+@pytest.fixture(scope="session")
+def ctx(svr):
+    return svr.Context(0, debug=True)
+
+
+@pytest.fixture(scope="session")
+def ref():
+    from oracle import ref as r
+    r.load_ref()
+    return r
+
+
+def look_at_origin(svr, w, h, dist, theta, elev=0.25):
+    """Camera of tests/test_raster.cpp:41-60 (numpy restatement)."""
+    pos = dist * np.array([np.cos(elev) * np.cos(theta), np.sin(elev), np.cos(elev) * np.sin(theta)])
+    fwd = -pos / np.sqrt((pos * pos).sum())
+    right = np.cross(fwd, [0.0, 1.0, 0.0])
+    right = right / np.sqrt((right * right).sum())
+    down = np.cross(fwd, right)
+    rot = np.stack([right, down, fwd], axis=1)
+    return svr.Camera(w, h, 0.9 * w, 0.9 * w, 0.5 * w, 0.5 * h, rot, pos)
+
+
+def max_abs(a, b):
+    return float(np.max(np.abs(np.asarray(a, np.float64) - np.asarray(b, np.float64)))) if np.size(a) else 0.0
+
+
+def sentinel_aware_depth(ours, theirs, far=1e30):
+    """Sentinel masks exactly; values only where neither side saw the sentinel."""
+    mo = np.asarray(ours) > 1e20
+    mt = np.asarray(theirs) > 1e20
+    assert np.array_equal(mo, mt), f"sentinel mask differs at {int((mo != mt).sum())} pixels"
+    keep = ~mo
+    return max_abs(np.asarray(ours)[keep], np.asarray(theirs)[keep])
+
+
+def grad_close(g, gref, rel=1e-3):
+    """|g-g_ref| <= rel*(max(|g|,|g_ref|) + s), s = rel*max|g_ref|."""
+    g = np.asarray(g, np.float64).reshape(-1)
+    gref = np.asarray(gref, np.float64).reshape(-1)
+    s = rel * float(np.max(np.abs(gref))) if gref.size else 0.0
+    tol = rel * (np.maximum(np.abs(g), np.abs(gref)) + s)
+    bad = np.abs(g - gref) > tol
+    return int(bad.sum()), float(np.max(np.abs(g - gref) - tol)) if g.size else 0.0

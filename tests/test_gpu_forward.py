@@ -1,0 +1,252 @@
+"""GPU parity of the forward path against the unmodified reference (oracle/_ref).
+
+Bit-exact: tile sign masks, per-voxel projection (culling, padded AABB, tile
+rect), the emitted entry list in reference emission order, the sorted
+(key, value) list and the tile ranges. Tolerance: colour, transmittance,
+normal, depth and median depth max-abs 1e-4 (sentinel-aware for depths).
+Mirrors proj/tests/test_raster.cpp and acceptance.cpp:166-186.
+"""
+import numpy as np
+import pytest
+
+from conftest import look_at_origin, max_abs, sentinel_aware_depth
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def cfg1(svr, ctx, ref):
+    arrays = svr.synth_random_scene(2024, 65536, 7, 3)
+    return arrays, svr.Scene(ctx, arrays), ref.RefScene.generate(2024, 65536, 7, 3)
+
+
+def small_scene(svr, ctx, ref, seed, subdiv=40, deg=2, maxlv=8):
+    arrays = svr.synth_random_scene(seed, 512 + 7 * subdiv, maxlv, deg)
+    return arrays, svr.Scene(ctx, arrays), ref.RefScene.from_arrays(arrays)
+
+
+def test_tile_masks_bit_exact(svr, ctx, ref):
+    cams = [svr.ring_camera(4, i, 200 + 37 * i, 130 + 11 * i) for i in range(4)]
+    wide = svr.Camera(32, 32, 16, 16, 20, 20, np.eye(3), np.zeros(3))  # test_raster.cpp:171-174
+    narrow = look_at_origin(svr, 64, 64, 2.0, 0.8, 0.6)
+    narrow.fx = narrow.fy = 3.0 * 64
+    for cam in cams + [wide, narrow]:
+        assert np.array_equal(svr.tile_sign_masks(ctx, cam), ref.ref_tile_masks(cam))
+    m = svr.tile_sign_masks(ctx, wide)
+    assert any(bin(int(x)).count("1") >= 2 for x in m)
+
+
+def test_projection_bit_exact(svr, ctx, ref, cfg1):
+    arrays, scene, rscene = cfg1
+    for i, ss in [(0, 1.0), (1, 1.5), (2, 1.0)]:
+        cam = svr.ring_camera(3, i, 256, 256)
+        opts = svr.RenderOptions(supersample=ss)
+        f = svr.Frame(ctx)
+        svr.render_into(f, scene, cam, opts)
+        ss_cam = ref.ref_scaled_camera(cam, ss)
+        vis, aabb, rect = ref.ref_project(rscene, ss_cam, arrays.n_voxels)
+        ours_rect = f.download("VOXEL_RECTS", np.int32, (-1, 4))
+        ours_aabb = f.download("VOXEL_AABB", np.float64, (-1, 4))
+        assert np.array_equal(ours_rect, rect)
+        assert np.array_equal(ours_aabb[vis], aabb[vis])  # bit-exact doubles
+        assert np.array_equal(ours_rect[:, 1] >= ours_rect[:, 0], vis)
+
+
+def test_project_voxels_api_matches_reference(svr, ctx, ref):
+    rng = np.random.default_rng(404)
+    for trial in range(20):  # test_raster.cpp:129-147 setup
+        cam = look_at_origin(svr, 48, 48, 1.8, 2 * np.pi * trial / 20.0)
+        centers = rng.uniform(-0.5, 0.5, (64, 3))
+        sizes = 0.05 + 0.2 * np.abs(rng.uniform(-0.5, 0.5, 64))
+        centers[0] = cam.pos + 1.0 * cam.rot[:, 2] * -1.0  # behind the camera
+        vis, aabb, rect = svr.project_voxels(ctx, cam, centers, sizes)
+        import ctypes as C
+        lib = ref.load_ref()
+        for i in range(64):
+            ra, rr, rv = np.empty(4), np.empty(4, np.int32), C.c_int()
+            c = cam.to_c()
+            lib.ref_project_one(C.byref(c), ref._p(np.ascontiguousarray(centers[i])), sizes[i], 1e-6,
+                                ref._p(ra), ref._p(rr), C.byref(rv))
+            assert bool(rv.value) == bool(vis[i])
+            assert np.array_equal(rr, rect[i])
+            if vis[i]:
+                assert np.array_equal(ra, aabb[i])
+        assert not vis[0]
+
+
+@pytest.mark.parametrize("ss", [1.0, 1.5])
+def test_entries_sort_ranges_bit_exact(svr, ctx, ref, cfg1, ss):
+    arrays, scene, rscene = cfg1
+    cam = svr.ring_camera(1, 0, 256, 256)
+    f = svr.Frame(ctx)
+    svr.render_into(f, scene, cam, svr.RenderOptions(supersample=ss))
+    ss_cam = ref.ref_scaled_camera(cam, ss)
+    k_ref, v_ref = ref.ref_entries(rscene, ss_cam, sorted_=False)
+    k, v = f.download("ENTRIES_KEYS", np.uint64), f.download("ENTRIES_VALUES", np.uint32)
+    assert k.size == k_ref.size > 0
+    assert np.array_equal(k, k_ref) and np.array_equal(v, v_ref)
+    ks_ref, vs_ref = ref.ref_entries(rscene, ss_cam, sorted_=True)
+    ks, vs = f.download("SORT_KEYS", np.uint64), f.download("SORT_VALUES", np.uint32)
+    assert np.array_equal(ks, ks_ref) and np.array_equal(vs, vs_ref)
+    ranges = f.download("TILE_RANGES", np.uint32, (-1, 2))
+    ntiles = ranges.shape[0]
+    tiles = (ks_ref >> np.uint64(48)).astype(np.int64)
+    lo = np.searchsorted(tiles, np.arange(ntiles), "left")
+    hi = np.searchsorted(tiles, np.arange(ntiles), "right")
+    nonempty = hi > lo
+    assert np.array_equal(ranges[nonempty, 0], lo[nonempty])
+    assert np.array_equal(ranges[nonempty, 1], hi[nonempty])
+    assert np.all(ranges[~nonempty, 0] == ranges[~nonempty, 1])
+
+
+def test_multi_pattern_entries_bit_exact(svr, ctx, ref):
+    """A camera inside the scene: straddlers get the whole image, tiles carry
+    several sign patterns (raster.cpp:96-103, 120-142)."""
+    arrays, scene, rscene = small_scene(svr, ctx, ref, 77, subdiv=60)
+    rot = np.eye(3)
+    cam = svr.Camera(64, 48, 30.0, 30.0, 31.3, 22.7, rot, np.array([0.01, -0.02, -0.03]))
+    f = svr.Frame(ctx)
+    svr.render_into(f, scene, cam, svr.RenderOptions(supersample=1.0))
+    k_ref, v_ref = ref.ref_entries(rscene, cam, sorted_=False)
+    assert np.array_equal(f.download("ENTRIES_KEYS", np.uint64), k_ref)
+    assert np.array_equal(f.download("ENTRIES_VALUES", np.uint32), v_ref)
+    ks_ref, vs_ref = ref.ref_entries(rscene, cam, sorted_=True)
+    assert np.array_equal(f.download("SORT_KEYS", np.uint64), ks_ref)
+    assert np.array_equal(f.download("SORT_VALUES", np.uint32), vs_ref)
+    assert f.info().sort_passes >= 2
+
+
+def compare_outputs(out, r, tol=TOL):
+    errs = {
+        "color": max_abs(out.color, r["color"]),
+        "transmittance": max_abs(out.transmittance, r["transmittance"]),
+        "normal": max_abs(out.normal, r["normal"]),
+        "depth": sentinel_aware_depth(out.depth, r["depth"]),
+        "median_depth": sentinel_aware_depth(out.median_depth, r["median_depth"]),
+    }
+    for k, e in errs.items():
+        assert e <= tol, f"{k}: max abs err {e:.3e} > {tol}"
+    return errs
+
+
+@pytest.mark.parametrize("K", [1, 2, 3])
+def test_render_matches_reference_cfg1(svr, ctx, ref, cfg1, K):
+    arrays, scene, rscene = cfg1
+    cam = svr.ring_camera(1, 0, 256, 256)
+    opts = svr.RenderOptions(K=K, supersample=1.0, background=(0.1, 0.2, 0.3))
+    out = svr.render(scene, cam, opts)
+    compare_outputs(out, ref.ref_render(rscene, cam, opts))
+
+
+def test_render_supersampled_matches_reference(svr, ctx, ref, cfg1):
+    arrays, scene, rscene = cfg1
+    cam = svr.ring_camera(2, 1, 200, 150)
+    opts = svr.RenderOptions(K=1, supersample=1.5)
+    compare_outputs(svr.render(scene, cam, opts), ref.ref_render(rscene, cam, opts))
+
+
+@pytest.mark.parametrize("trial", range(8))
+def test_rasterizer_matches_reference_small_scenes(svr, ctx, ref, trial):
+    """test_raster.cpp:242-257 pattern: K = 1 + trial % 3, 64^2, background."""
+    arrays, scene, rscene = small_scene(svr, ctx, ref, 2024 + trial)
+    cam = look_at_origin(svr, 64, 64, 1.6 + 0.1 * trial, 0.8 * trial, 0.3 - 0.05 * trial)
+    opts = svr.RenderOptions(K=1 + trial % 3, supersample=1.0, background=(0.1, 0.2, 0.3))
+    compare_outputs(svr.render(scene, cam, opts), ref.ref_render(rscene, cam, opts))
+    # and the brute-force oracle within the same tolerance
+    r_or = ref.ref_render(rscene, cam, opts, oracle=True)
+    out = svr.render(scene, cam, opts)
+    assert max_abs(out.color, r_or["color"]) <= TOL
+
+
+def test_record_stats_max_blend(svr, ctx, ref, cfg1):
+    arrays, scene, rscene = cfg1
+    cam = svr.ring_camera(1, 0, 128, 128)
+    opts = svr.RenderOptions(supersample=1.0, record_stats=True)
+    out = svr.render(scene, cam, opts)
+    r = ref.ref_render(rscene, cam, opts, n_voxels=arrays.n_voxels)
+    assert max_abs(out.max_blend_weight, r["max_blend_weight"]) <= TOL
+
+
+def test_empty_scene_renders_background(svr, ctx):
+    """test_raster.cpp:101-115."""
+    arrays = svr.SceneArrays(np.zeros(0, np.uint64), np.zeros(0, np.uint8),
+                             np.zeros((0, 8), np.uint32), np.zeros(0, np.float32),
+                             np.zeros((0, 48), np.float32), 3)
+    scene = svr.Scene(ctx, arrays)
+    cam = look_at_origin(svr, 32, 24, 1.5, 0.7)
+    out = svr.render(scene, cam, svr.RenderOptions(background=(0.25, 0.5, 0.75)))
+    assert np.allclose(out.color[..., 0], 0.25, atol=1e-7)
+    assert np.allclose(out.color[..., 2], 0.75, atol=1e-7)
+    assert np.all(out.transmittance == 1.0)
+    assert np.all(out.depth == np.float32(1e30))
+
+
+def test_option_validation_and_capacity(svr, ctx, cfg1):
+    """test_raster.cpp:86-99 and :207-210."""
+    _, scene, _ = cfg1
+    cam = look_at_origin(svr, 16, 16, 1.5, 0.3)
+    with pytest.raises(svr.InvalidArgument):
+        svr.render(scene, cam, svr.RenderOptions(K=4))
+    with pytest.raises(svr.InvalidArgument):
+        svr.render(scene, cam, svr.RenderOptions(supersample=0.5))
+    with pytest.raises(svr.InvalidArgument):
+        svr.render(scene, cam, svr.RenderOptions(supersample=1.0, t_threshold=0.0))
+    huge = look_at_origin(svr, 1 << 20, 16, 1.5, 0.3)
+    with pytest.raises(svr.LengthError):
+        svr.render(scene, huge, svr.RenderOptions(supersample=1.0))
+
+
+def test_opaque_voxel_saturates(svr, ctx, ref):
+    """test_raster.cpp:284-309: one level-1 voxel with density 800."""
+    rs = ref.RefScene.from_paths(np.array([0], np.uint64), np.array([1], np.uint8), 800.0, 0)
+    a = rs.arrays()
+    a.sh[0, :] = np.array([0.8, 0.3, 0.6]) / 0.28209479177387814
+    rs.set_params(sh=a.sh)
+    scene = svr.Scene(ctx, a)
+    cam = look_at_origin(svr, 32, 32, 2.0, np.pi + 0.78, -0.3)
+    opts = svr.RenderOptions(supersample=1.0)
+    out = svr.render(scene, cam, opts)
+    compare_outputs(out, ref.ref_render(rs, cam, opts))
+    c = out.color[16, 16]
+    assert abs(c[0] - 0.8) < 1e-5 and abs(c[1] - 0.3) < 1e-5 and abs(c[2] - 0.6) < 1e-5
+
+
+def test_sort_entries_api(svr, ctx, ref):
+    rng = np.random.default_rng(5)
+    for n, kbits in [(1, 10), (17, 64), (5000, 20), (100_000, 64), (300_000, 40)]:
+        k = rng.integers(0, 2 ** 63, n, dtype=np.uint64) >> np.uint64(64 - kbits) if kbits < 64 \
+            else rng.integers(0, 2 ** 63, n, dtype=np.uint64) * np.uint64(2)
+        k[: n // 3] = k[0]  # many equal keys: value decides
+        v = rng.integers(0, 2 ** 32, n, dtype=np.uint64).astype(np.uint32)
+        ks, vs = svr.sort_entries(ctx, k, v)
+        kr, vr = ref.ref_sort_entries(k, v)
+        assert np.array_equal(ks, kr) and np.array_equal(vs, vr)
+
+
+def test_build_sort_entries_api(svr, ctx, ref, cfg1):
+    arrays, scene, rscene = cfg1
+    cam = svr.ring_camera(1, 0, 96, 80)
+    vis, aabb, rect = ref.ref_project(rscene, cam, arrays.n_voxels)
+    vids = np.nonzero(vis)[0].astype(np.uint32)
+    k, v = svr.build_sort_entries(ctx, cam, arrays.n_voxels, vids, arrays.codes[vids], rect[vids])
+    kr, vr = ref.ref_entries(rscene, cam, sorted_=False)
+    assert np.array_equal(k, kr) and np.array_equal(v, vr)
+
+
+@pytest.mark.slow
+def test_cfg2_bit_exact_and_images(svr, ctx, ref):
+    """Config 2 at full size: 1,048,573 voxels, 1024^2."""
+    arrays = svr.synth_random_scene(7, 1 << 20, 9, 3)
+    assert arrays.n_voxels == 1048573
+    scene = svr.Scene(ctx, arrays)
+    rscene = ref.RefScene.from_arrays(arrays)
+    cam = svr.ring_camera(1, 0, 1024, 1024)
+    f = svr.Frame(ctx)
+    opts = svr.RenderOptions(supersample=1.0)
+    svr.render_into(f, scene, cam, opts)
+    ks_ref, vs_ref = ref.ref_entries(rscene, cam, sorted_=True)
+    assert ks_ref.size == 1763171
+    assert np.array_equal(f.download("SORT_KEYS", np.uint64), ks_ref)
+    assert np.array_equal(f.download("SORT_VALUES", np.uint32), vs_ref)
