@@ -234,6 +234,15 @@ int svr_ring_camera(int n_views, int index, int width, int height, double distan
                     double fov_x_deg, svr_camera* out);
 void svr_free(void* p);
 
+/* ---- instrumentation ---------------------------------------------------- */
+/* Number of kernels this library has launched (process-wide). */
+unsigned long long svr_launch_count(void);
+/* Per-stage CUDA-event timing on the context stream. Stage order:
+ * tile_setup, preprocess, scan, duplicate, sort, ranges, composite,
+ * record, downsample, backward, epilogue, other. */
+int svr_ctx_enable_timing(svr_ctx* ctx, int enable);
+int svr_ctx_stage_times(svr_ctx* ctx, double* ms, int n, int reset);
+
 #ifdef __cplusplus
 }
 #endif

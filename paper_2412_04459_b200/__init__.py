@@ -111,8 +111,11 @@ EXPORTS = [
     "svr_render", "svr_frame_get_info", "svr_frame_download", "svr_frame_device_ptr",
     "svr_frame_records", "svr_render_backward", "svr_l1_loss", "svr_train_step_l1",
     "svr_project_voxels", "svr_tile_sign_masks", "svr_build_sort_entries", "svr_sort_entries",
-    "svr_synth_random_scene", "svr_ring_camera", "svr_free",
+    "svr_synth_random_scene", "svr_ring_camera", "svr_free", "svr_launch_count",
+    "svr_ctx_enable_timing", "svr_ctx_stage_times",
 ]
+STAGES = ["tile_setup", "preprocess", "scan", "duplicate", "sort", "ranges", "composite",
+          "record", "downsample", "backward", "epilogue", "other"]
 
 _lib = None
 
@@ -167,6 +170,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "svr_ring_camera": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
                                       C.c_double, C.POINTER(svr_camera)]),
         "svr_free": (None, [P]),
+        "svr_launch_count": (C.c_ulonglong, []),
+        "svr_ctx_enable_timing": (C.c_int, [P, C.c_int]),
+        "svr_ctx_stage_times": (C.c_int, [P, C.POINTER(C.c_double), C.c_int, C.c_int]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -319,6 +325,19 @@ class Context:
 
     def synchronize(self) -> None:
         _check(self._lib.svr_ctx_synchronize(self.h))
+
+    def enable_timing(self, on: bool = True) -> None:
+        _check(self._lib.svr_ctx_enable_timing(self.h, int(on)))
+
+    def stage_times(self, reset: bool = True) -> dict:
+        buf = (C.c_double * len(STAGES))()
+        _check(self._lib.svr_ctx_stage_times(self.h, buf, len(STAGES), int(reset)))
+        return {k: buf[i] for i, k in enumerate(STAGES)}
+
+
+def launch_count() -> int:
+    """Kernels launched by libsvr_b200.so so far (process-wide)."""
+    return int(load_library().svr_launch_count())
 
     def close(self) -> None:
         if getattr(self, "h", None):

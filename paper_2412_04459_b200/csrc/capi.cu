@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -19,6 +20,38 @@ namespace svrb {
 
 namespace {
 thread_local std::string g_last_error;
+std::atomic<unsigned long long> g_launches{0};
+}
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// Records a stage boundary on the context stream (no-op unless timing).
+void mark(svr_ctx* ctx, int stage) {
+    if (!ctx->timing) return;
+    cudaEvent_t e;
+    if (!ctx->event_pool.empty()) {
+        e = ctx->event_pool.back();
+        ctx->event_pool.pop_back();
+    } else {
+        SVR_CUDA(cudaEventCreate(&e));
+    }
+    SVR_CUDA(cudaEventRecord(e, ctx->stream));
+    ctx->marks.push_back({stage, e});
+}
+
+// Folds recorded marks into stage_ms (synchronises the stream).
+void collect_marks(svr_ctx* ctx) {
+    if (ctx->marks.empty()) return;
+    SVR_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (size_t i = 0; i + 1 < ctx->marks.size(); ++i) {
+        int st = ctx->marks[i].first;
+        if (st < 0) continue;
+        float ms = 0.f;
+        SVR_CUDA(cudaEventElapsedTime(&ms, ctx->marks[i].second, ctx->marks[i + 1].second));
+        ctx->stage_ms[st] += ms;
+    }
+    for (auto& m : ctx->marks) ctx->event_pool.push_back(m.second);
+    ctx->marks.clear();
 }
 
 void cuda_check(cudaError_t e, const char* what) {
@@ -267,6 +300,7 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     uint32_t* sat = grow<uint32_t>(f->tile_sat, uint64_t(cam.ntx + 1) * (cam.nty + 1));
     FrameStatus* status = grow<FrameStatus>(f->status, 1);
     SVR_CUDA(cudaMemsetAsync(status, 0, sizeof(FrameStatus), st));
+    mark(ctx, kStageTileSetup);
     launch_tile_setup(cam, masks, sat, status, st);
 
     // K1: preprocess
@@ -286,12 +320,15 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     pa.aabb = ctx->debug ? grow<double4>(f->aabb, N) : nullptr;
     pa.records = grow<float4>(f->records, N * kRecordF4);
     pa.counts = grow<uint32_t>(f->counts, N);
+    mark(ctx, kStagePreprocess);
     launch_preprocess(cam, pa, st);
 
     // K3: scan of the per-voxel entry counts -> emission offsets, E
     uint32_t* offsets = grow<uint32_t>(f->offsets, N);
     ctx->scratch.reserve(scan_scratch_bytes(std::max<uint64_t>(N, uint64_t(ntiles) * 256)));
+    mark(ctx, kStageScan);
     exclusive_scan_u32(pa.counts, offsets, N, &status->n_entries, ctx->scratch.p, st);
+    mark(ctx, -1);
     ctx->pinned.reserve(sizeof(FrameStatus));
     FrameStatus* hs = static_cast<FrameStatus*>(ctx->pinned.p);
     SVR_CUDA(cudaMemcpyAsync(hs, status, sizeof(FrameStatus), cudaMemcpyDeviceToHost, st));
@@ -306,6 +343,7 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
         grow<uint64_t>(f->keys[b], E);
         grow<uint32_t>(f->vals[b], E);
     }
+    mark(ctx, kStageDuplicate);
     launch_duplicate(cam, N, pa.paths, pa.rects, masks, pa.counts, offsets, f->keys[0].as<uint64_t>(),
                      f->vals[0].as<uint32_t>(), st);
     if (ctx->debug) {
@@ -319,6 +357,7 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     RadixPass passes[kMaxRadixPasses];
     const int np = plan_sort(scene->max_level, ntiles, pattern_or, passes);
     f->sort_passes = np;
+    mark(ctx, kStageSort);
     ctx->scratch2.reserve(sort_scratch_bytes(E, np));
     f->sorted_buf = radix_sort_pairs(f->keys[0].as<uint64_t>(), f->vals[0].as<uint32_t>(),
                                      f->keys[1].as<uint64_t>(), f->vals[1].as<uint32_t>(), E,
@@ -328,7 +367,9 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
 
     // K6: tile ranges
     uint2* ranges = grow<uint2>(f->ranges, ntiles);
+    mark(ctx, kStageRanges);
     launch_tile_ranges(skeys, E, ranges, ntiles, st);
+    mark(ctx, -1);
 
     // output buffers
     const uint64_t npx = uint64_t(W) * H, nss = uint64_t(sw) * sh;
@@ -362,7 +403,9 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     if (f->training) SVR_CUDA(cudaMemsetAsync(ca.pix_count, 0, uint64_t(ntiles) * 256 * 4, st));
 
     // K7: composite
+    mark(ctx, kStageComposite);
     launch_composite(cam, ca, false, st);
+    mark(ctx, kStageOther);
 
     if (f->training) {
         // ForwardRecords: per-pixel contribution lists in the reference's
@@ -380,13 +423,16 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
         cr.contrib_entry = grow<uint32_t>(f->contrib_entry, C);
         cr.contrib_T = grow<float>(f->contrib_T, C);
         cr.max_blend = nullptr;
+        mark(ctx, kStageRecord);
         launch_composite(cam, cr, true, st);
+        mark(ctx, -1);
         f->has_records = true;
     }
 
     // K8: area downsampling of the five outputs (identity when ss == 1)
     if (!ss1) {
         TapSet taps = ensure_taps(f);
+        mark(ctx, kStageDownsample);
         launch_downsample(taps.fwd, ca.color, 3, sw, oc, W, H, st);
         launch_downsample(taps.fwd, ca.depth, 1, sw, od, W, H, st);
         launch_downsample(taps.fwd, ca.median, 1, sw, om, W, H, st);
@@ -394,6 +440,7 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
         launch_downsample(taps.fwd, ca.tfin, 1, sw, ot, W, H, st);
     }
     (void)nss;
+    mark(ctx, -1);
     f->n_visible = ~uint64_t(0);  // computed lazily
 }
 
@@ -567,6 +614,7 @@ void backward_impl(svr_ctx* ctx, const svr_scene* scene, svr_frame* f, const svr
     ba.g_color = gcol;
     ba.g_normal = gnor;
     ba.g_priority = gp;
+    mark(ctx, kStageBackward);
     launch_composite_backward(f->cam, ba, st);
 
     EpilogueArgs ea{};
@@ -585,7 +633,9 @@ void backward_impl(svr_ctx* ctx, const svr_scene* scene, svr_frame* f, const svr
     ea.g_sh = gs;
     ea.g_density = gd;
     ea.accumulate = accumulate ? 1 : 0;
+    mark(ctx, kStageEpilogue);
     launch_voxel_epilogue(f->cam, ea, st);
+    mark(ctx, -1);
 
     if (!out->on_device) {
         if (out->density) SVR_CUDA(cudaMemcpyAsync(out->density, gd, P * 4, cudaMemcpyDeviceToHost, st));
@@ -627,6 +677,8 @@ int svr_ctx_destroy(svr_ctx* ctx) {
         if (!ctx) return;
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
+        for (auto& m : ctx->marks) cudaEventDestroy(m.second);
+        for (auto& e : ctx->event_pool) cudaEventDestroy(e);
         cudaStreamDestroy(ctx->stream);
         delete ctx;
     });
@@ -985,5 +1037,26 @@ int svr_sort_entries(svr_ctx* ctx, uint64_t n, uint64_t* keys, uint32_t* values)
 }
 
 void svr_free(void* p) { std::free(p); }
+
+unsigned long long svr_launch_count(void) { return g_launches.load(); }
+
+int svr_ctx_enable_timing(svr_ctx* ctx, int enable) {
+    return guard([&] {
+        require(ctx != nullptr, SVR_ERR_INVALID_ARGUMENT, "null context");
+        collect_marks(ctx);
+        ctx->timing = enable != 0;
+    });
+}
+
+int svr_ctx_stage_times(svr_ctx* ctx, double* ms, int n, int reset) {
+    return guard([&] {
+        require(ctx != nullptr, SVR_ERR_INVALID_ARGUMENT, "null context");
+        set_device(ctx);
+        collect_marks(ctx);
+        for (int i = 0; i < n && i < kNumStages; ++i) ms[i] = ctx->stage_ms[i];
+        if (reset)
+            for (double& v : ctx->stage_ms) v = 0.0;
+    });
+}
 
 }  // extern "C"

@@ -22,40 +22,61 @@ namespace {
 constexpr uint64_t kCodeMask48 = (uint64_t(1) << 48) - 1;
 
 // ------------------------------------------------------------------- K2
+// Single CTA: per-tile sign-pattern masks (fp64, bit-exact) and the
+// summed-area table of their popcounts, built in shared memory (one
+// warp-parallel row scan, then column sums), so a voxel's entry count is
+// four table reads whatever its tile rectangle (near-plane straddlers cover
+// the whole image).
+constexpr int kSatSmemMax = 48 * 1024;  // u32 entries that fit the dynamic smem budget
+
 __global__ void __launch_bounds__(1024) tile_setup_kernel(DevCamera cam, uint8_t* masks,
-                                                          uint32_t* sat, FrameStatus* status) {
+                                                          uint32_t* sat, FrameStatus* status,
+                                                          int use_smem) {
+    extern __shared__ uint32_t s_sat[];
     const int ntx = cam.ntx, nty = cam.nty, ntiles = ntx * nty;
-    const int sw = ntx + 1;
+    const int sw = ntx + 1, ncell = sw * (nty + 1);
+    uint32_t* t = use_smem ? s_sat : sat;
     __shared__ unsigned int s_or;
     if (threadIdx.x == 0) s_or = 0;
+    for (int i = threadIdx.x; i < ncell; i += blockDim.x) t[i] = 0;
     __syncthreads();
     unsigned int local_or = 0;
-    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
-        int tx = t % ntx, ty = t / ntx;
-        uint32_t m = tile_sign_mask(cam, tx, ty);
-        masks[t] = uint8_t(m);
+    for (int k = threadIdx.x; k < ntiles; k += blockDim.x) {
+        const int tx = k % ntx, ty = k / ntx;
+        const uint32_t m = tile_sign_mask(cam, tx, ty);
+        masks[k] = uint8_t(m);
         local_or |= m;
-        sat[(ty + 1) * sw + tx + 1] = __popc(m);
+        t[(ty + 1) * sw + tx + 1] = __popc(m);
     }
-    for (int i = threadIdx.x; i < sw; i += blockDim.x) sat[i] = 0;
-    for (int i = threadIdx.x; i <= nty; i += blockDim.x) sat[i * sw] = 0;
     atomicOr(&s_or, local_or);
     __syncthreads();
-    for (int r = threadIdx.x + 1; r <= nty; r += blockDim.x) {
-        uint32_t run = 0;
-        for (int c = 1; c <= ntx; ++c) {
-            run += sat[r * sw + c];
-            sat[r * sw + c] = run;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    // row prefix sums: one warp per row, 32 columns at a time
+    for (int r = warp + 1; r <= nty; r += nwarps) {
+        uint32_t carry = 0;
+        for (int c0 = 1; c0 <= ntx; c0 += 32) {
+            const int c = c0 + lane;
+            uint32_t v = c <= ntx ? t[r * sw + c] : 0u;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t n = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += n;
+            }
+            if (c <= ntx) t[r * sw + c] = v + carry;
+            carry += __shfl_sync(0xffffffffu, v, 31);
         }
     }
     __syncthreads();
     for (int c = threadIdx.x + 1; c <= ntx; c += blockDim.x) {
         uint32_t run = 0;
         for (int r = 1; r <= nty; ++r) {
-            run += sat[r * sw + c];
-            sat[r * sw + c] = run;
+            run += t[r * sw + c];
+            t[r * sw + c] = run;
         }
     }
+    __syncthreads();
+    if (use_smem)
+        for (int i = threadIdx.x; i < ncell; i += blockDim.x) sat[i] = t[i];
     if (threadIdx.x == 0 && status) status->pattern_or = s_or;
 }
 
@@ -73,73 +94,120 @@ __device__ __forceinline__ uint32_t sat_rect(const uint32_t* sat, int ntx, int t
 }
 
 // ------------------------------------------------------------------- K1
-__global__ void __launch_bounds__(256) preprocess_kernel(DevCamera cam, PreprocessArgs a) {
-    uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (v >= a.n) return;
-    const uint64_t path = a.paths[v];
-    double center[3], size;
-    voxel_geometry(path & kCodeMask48, int(path >> 48), a.bc, a.bsize, center, &size);
-    Projection pr;
-    bool vis = project_voxel(cam, center, size, a.near_plane, pr);
-    a.rects[v] = make_int4(pr.tx0, pr.tx1, pr.ty0, pr.ty1);
-    if (a.aabb) a.aabb[v] = make_double4(pr.x0, pr.x1, pr.y0, pr.y1);
-    if (!vis) {
-        a.counts[v] = 0;
-        return;
-    }
-    a.counts[v] = sat_rect(a.tile_sat, cam.ntx, pr.tx0, pr.tx1, pr.ty0, pr.ty1);
+// 128 threads = 4 warps, one voxel per thread. The SH coefficients of a
+// warp's 32 voxels (32 x 192 B, contiguous) are fetched with coalesced
+// 16-B loads into a bank-conflict-free padded tile (odd row pitch), and the
+// 112-B records of the whole CTA are staged in shared memory and written
+// back as one contiguous, coalesced block.
+constexpr int kPreThreads = 128;
 
-    // Geometry relative to the camera, rounded once from the exact doubles.
-    const double h = dmul(0.5, size);
-    float4 r0, r1, r2, r3, r4, r5, r6;
-    r0.x = float(dsub(dsub(center[0], h), cam.pos[0]));
-    r0.y = float(dsub(dsub(center[1], h), cam.pos[1]));
-    r0.z = float(dsub(dsub(center[2], h), cam.pos[2]));
-    r0.w = float(1.0 / size);
-    r1.x = float(dsub(dadd(center[0], h), cam.pos[0]));
-    r1.y = float(dsub(dadd(center[1], h), cam.pos[1]));
-    r1.z = float(dsub(dadd(center[2], h), cam.pos[2]));
-    r1.w = __uint_as_float(uint32_t(v));
-    // Screen AABB, rounded outward so the fp32 test is a superset.
-    r2 = make_float4(__double2float_rd(pr.x0), __double2float_ru(pr.x1),
-                     __double2float_rd(pr.y0), __double2float_ru(pr.y1));
-    const uint4* ci4 = reinterpret_cast<const uint4*>(a.corner_index + 8 * v);
-    uint4 c0 = ci4[0], c1 = ci4[1];
-    float V[8] = {a.density[c0.x], a.density[c0.y], a.density[c0.z], a.density[c0.w],
-                  a.density[c1.x], a.density[c1.y], a.density[c1.z], a.density[c1.w]};
-    r3 = make_float4(V[0], V[1], V[2], V[3]);
-    r4 = make_float4(V[4], V[5], V[6], V[7]);
-    // sh_eval(normalized(center - cam.pos)) (raster.cpp:195-196, sh.hpp:48-58)
-    double dx = dsub(center[0], cam.pos[0]), dy = dsub(center[1], cam.pos[1]),
-           dz = dsub(center[2], cam.pos[2]);
-    double nrm = sqrt(dx * dx + dy * dy + dz * dz);
-    float ux = 0.f, uy = 0.f, uz = 0.f;
-    if (nrm > 0.0) {
-        ux = float(dx / nrm);
-        uy = float(dy / nrm);
-        uz = float(dz / nrm);
+__global__ void __launch_bounds__(kPreThreads, 8) preprocess_kernel(DevCamera cam, PreprocessArgs a) {
+    extern __shared__ float4 smem4[];
+    float* smem = reinterpret_cast<float*>(smem4);
+    const int pad = a.sh_stride | 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float* s_sh = smem + warp * 32 * pad;
+    float4* s_rec = smem4 + ((kPreThreads * pad + 3) / 4);
+    const uint64_t v0 = uint64_t(blockIdx.x) * kPreThreads;
+    const uint64_t v = v0 + threadIdx.x;
+    const bool valid = v < a.n;
+
+    // 1. coalesced SH staging for this warp's voxels
+    const uint64_t wv0 = v0 + uint64_t(warp) * 32;
+    const int nvw = wv0 < a.n ? int(min(uint64_t(32), a.n - wv0)) : 0;
+    const int total = nvw * a.sh_stride;
+    const float* src = a.sh + wv0 * uint64_t(a.sh_stride);
+    if ((a.sh_stride & 3) == 0) {
+        const float4* src4 = reinterpret_cast<const float4*>(src);
+        for (int e4 = lane; e4 < total / 4; e4 += 32) {
+            float4 f = __ldg(src4 + e4);
+            int e = 4 * e4;
+            int r = e / a.sh_stride, c = e - r * a.sh_stride;
+            float* d = s_sh + r * pad + c;  // stride % 4 == 0: the 4 floats share a row
+            d[0] = f.x;
+            d[1] = f.y;
+            d[2] = f.z;
+            d[3] = f.w;
+        }
+    } else {
+        for (int e = lane; e < total; e += 32) {
+            int r = e / a.sh_stride;
+            s_sh[r * pad + (e - r * a.sh_stride)] = __ldg(src + e);
+        }
     }
-    float b[16];
-    int nb = sh_basis(a.sh_degree, ux, uy, uz, b);
-    const float* co = a.sh + v * uint64_t(a.sh_stride);
-    float cr = 0.f, cg = 0.f, cb = 0.f;
-    for (int m = 0; m < nb; ++m) {
-        cr += b[m] * co[3 * m + 0];
-        cg += b[m] * co[3 * m + 1];
-        cb += b[m] * co[3 * m + 2];
+    __syncwarp();
+
+    float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0, r3 = r0, r4 = r0, r5 = r0, r6 = r0;
+    if (valid) {
+        const uint64_t path = a.paths[v];
+        double center[3], size;
+        voxel_geometry(path & kCodeMask48, int(path >> 48), a.bc, a.bsize, center, &size);
+        Projection pr;
+        const bool vis = project_voxel(cam, center, size, a.near_plane, pr);
+        a.rects[v] = make_int4(pr.tx0, pr.tx1, pr.ty0, pr.ty1);
+        if (a.aabb) a.aabb[v] = make_double4(pr.x0, pr.x1, pr.y0, pr.y1);
+        a.counts[v] = vis ? sat_rect(a.tile_sat, cam.ntx, pr.tx0, pr.tx1, pr.ty0, pr.ty1) : 0u;
+        if (vis) {
+            // Geometry relative to the camera, rounded once from the exact doubles.
+            const double h = dmul(0.5, size);
+            r0.x = float(dsub(dsub(center[0], h), cam.pos[0]));
+            r0.y = float(dsub(dsub(center[1], h), cam.pos[1]));
+            r0.z = float(dsub(dsub(center[2], h), cam.pos[2]));
+            r0.w = float(1.0 / size);
+            r1.x = float(dsub(dadd(center[0], h), cam.pos[0]));
+            r1.y = float(dsub(dadd(center[1], h), cam.pos[1]));
+            r1.z = float(dsub(dadd(center[2], h), cam.pos[2]));
+            r1.w = __uint_as_float(uint32_t(v));
+            // Screen AABB, rounded outward so the fp32 test is a superset.
+            r2 = make_float4(__double2float_rd(pr.x0), __double2float_ru(pr.x1),
+                             __double2float_rd(pr.y0), __double2float_ru(pr.y1));
+            const uint4* ci4 = reinterpret_cast<const uint4*>(a.corner_index + 8 * v);
+            const uint4 c0 = __ldg(ci4), c1 = __ldg(ci4 + 1);
+            float V[8] = {__ldg(a.density + c0.x), __ldg(a.density + c0.y), __ldg(a.density + c0.z),
+                          __ldg(a.density + c0.w), __ldg(a.density + c1.x), __ldg(a.density + c1.y),
+                          __ldg(a.density + c1.z), __ldg(a.density + c1.w)};
+            r3 = make_float4(V[0], V[1], V[2], V[3]);
+            r4 = make_float4(V[4], V[5], V[6], V[7]);
+            // sh_eval(normalized(center - cam.pos)) (raster.cpp:195-196, sh.hpp:48-58)
+            const double dx = dsub(center[0], cam.pos[0]), dy = dsub(center[1], cam.pos[1]),
+                         dz = dsub(center[2], cam.pos[2]);
+            const double nrm = sqrt(dx * dx + dy * dy + dz * dz);
+            float ux = 0.f, uy = 0.f, uz = 0.f;
+            if (nrm > 0.0) {
+                ux = float(dx / nrm);
+                uy = float(dy / nrm);
+                uz = float(dz / nrm);
+            }
+            float b[16];
+            const int nb = sh_basis(a.sh_degree, ux, uy, uz, b);
+            const float* co = s_sh + lane * pad;
+            float cr = 0.f, cg = 0.f, cb = 0.f;
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                if (m < nb) {
+                    cr += b[m] * co[3 * m + 0];
+                    cg += b[m] * co[3 * m + 1];
+                    cb += b[m] * co[3 * m + 2];
+                }
+            }
+            r5 = make_float4(fmaxf(0.f, cr), fmaxf(0.f, cg), fmaxf(0.f, cb), 0.f);
+            float n[3];
+            voxel_normal(V, n);
+            r6 = make_float4(n[0], n[1], n[2], 0.f);
+        }
     }
-    r5 = make_float4(fmaxf(0.f, cr), fmaxf(0.f, cg), fmaxf(0.f, cb), 0.f);
-    float n[3];
-    voxel_normal(V, n);
-    r6 = make_float4(n[0], n[1], n[2], 0.f);
-    float4* rec = a.records + v * kRecordF4;
-    rec[0] = r0;
-    rec[1] = r1;
-    rec[2] = r2;
-    rec[3] = r3;
-    rec[4] = r4;
-    rec[5] = r5;
-    rec[6] = r6;
+    float4* sr = s_rec + threadIdx.x * kRecordF4;
+    sr[0] = r0;
+    sr[1] = r1;
+    sr[2] = r2;
+    sr[3] = r3;
+    sr[4] = r4;
+    sr[5] = r5;
+    sr[6] = r6;
+    __syncthreads();
+    const int nblk = v0 < a.n ? int(min(uint64_t(kPreThreads), a.n - v0)) : 0;
+    float4* dst = a.records + v0 * kRecordF4;
+    for (int i = threadIdx.x; i < nblk * kRecordF4; i += kPreThreads) dst[i] = s_rec[i];
 }
 
 // ------------------------------------------------------------------- K4
@@ -210,25 +278,48 @@ __global__ void tile_ranges_kernel(const uint64_t* keys, uint64_t n, uint2* rang
 }
 
 // ------------------------------------------------------------------- K7
-// One CTA per 16x16 tile, one thread per pixel. Voxel records of a batch of
-// 256 entries are staged in shared memory (one 112-B record per thread,
-// SoA by float4 slot so every read in the inner loop is a broadcast), the
-// batch is walked front to back with exactly CompositeCtx::add's arithmetic
-// in fp32, and the CTA exits as soon as every pixel terminated
-// (__syncthreads_count as the block-wide vote).
+// One CTA per 16x16 tile, one thread per pixel; each warp owns an 8x4 pixel
+// block. Voxel records of a batch of 256 entries are staged in shared
+// memory (one 112-B record per thread, SoA by float4 slot). Each warp then
+// culls the batch 32 entries at a time against its own 8x4 footprint and
+// the sign patterns its pixels carry (one lane per entry, __ballot_sync),
+// and walks only the surviving entries front to back with exactly
+// CompositeCtx::add's arithmetic in fp32 (the per-pixel sign and AABB tests
+// are kept, so the set and order of composited voxels is the reference's).
+// The CTA exits once every pixel terminated (__syncthreads_count vote).
+__device__ __forceinline__ void pixel_of(const DevCamera& cam, int tile, int tid, int& px, int& py) {
+    const int tx = tile % cam.ntx, ty = tile / cam.ntx;
+    const int warp = tid >> 5, lane = tid & 31;
+    px = tx * kTile + (warp & 1) * 8 + (lane & 7);
+    py = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+}
+
+// Warp-autonomous compositing: no CTA-wide barrier inside the entry loop, so
+// a warp whose 8x4 block sees few voxels never waits for a busy neighbour.
+// Per chunk of 32 entries: lane i holds entry i's value and screen AABB
+// (prefetched one chunk ahead, values two chunks ahead), the warp ballots the
+// entries that overlap its block, gathers those records (112 B each,
+// coalesced 16-B pieces) into warp-private shared memory, and walks them in
+// order.
 template <int K, bool RECORD>
 __global__ void __launch_bounds__(256) composite_kernel(DevCamera cam, CompositeArgs a) {
-    __shared__ float4 s_rec[kRecordF4][256];
-    __shared__ uint32_t s_sign[256];
+    __shared__ float4 s_rec[8][32][kRecordF4];
+    __shared__ uint32_t s_vid[8][32];
 
     const int tile = blockIdx.x;
-    const int tx = tile % cam.ntx, ty = tile / cam.ntx;
-    const int px = tx * kTile + (threadIdx.x & 15), py = ty * kTile + (threadIdx.x >> 4);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int px, py;
+    pixel_of(cam, tile, threadIdx.x, px, py);
     const bool inside = px < cam.W && py < cam.H;
+    // this warp's 8x4 footprint in pixel-centre coordinates
+    const int wx0 = px - (lane & 7), wy0 = py - (lane >> 3);
+    const float fx0 = float(wx0) + 0.5f, fx1 = float(wx0) + 7.5f;
+    const float fy0 = float(wy0) + 0.5f, fy1 = float(wy0) + 3.5f;
 
     double dd[3];
     pixel_ray_dir(cam, double(px), double(py), dd);
     const uint32_t my_sign = sign_bits(dd);
+    const uint32_t warp_signs = __reduce_or_sync(0xffffffffu, inside ? (1u << my_sign) : 0u);
     const float dx = float(dd[0]), dy = float(dd[1]), dz = float(dd[2]);
     const float ix = 1.0f / dx, iy = 1.0f / dy, iz = 1.0f / dz;
     const float dnorm = float(sqrt(dd[0] * dd[0] + dd[1] * dd[1] + dd[2] * dd[2]));
@@ -238,60 +329,83 @@ __global__ void __launch_bounds__(256) composite_kernel(DevCamera cam, Composite
     float median = -1.0f;
     uint32_t cnt = 0;
     bool done = !inside;
-    const uint32_t slot = uint32_t(tile) * 256u + threadIdx.x;
+    const uint32_t slot = uint32_t(tile) * 256u + uint32_t((py % kTile) * kTile + (px % kTile));
     uint32_t rec_base = 0;
     if (RECORD) rec_base = inside ? a.pix_begin[slot] : 0u;
 
     const uint2 range = a.ranges[tile];
     const float thr = a.t_threshold;
-    for (uint32_t start = range.x; start < range.y; start += 256) {
-        if (__syncthreads_count(!done) == 0) break;
-        const uint32_t idx = start + threadIdx.x;
-        if (idx < range.y) {
-            uint32_t val = a.vals[idx];
-            uint32_t vid = val & ((1u << 29) - 1u);
-            s_sign[threadIdx.x] = val >> 29;
-            const float4* rec = a.records + uint64_t(vid) * kRecordF4;
-#pragma unroll
-            for (int k = 0; k < kRecordF4; ++k) s_rec[k][threadIdx.x] = __ldg(rec + k);
+    constexpr uint32_t kVidMask = (1u << 29) - 1u;
+    float4 (*wrec)[kRecordF4] = s_rec[warp];
+    uint32_t* wvid = s_vid[warp];
+
+    // software pipeline: v0/b0 = current chunk, v1 = next chunk's values
+    uint32_t v0 = 0, v1 = 0;
+    float4 b0 = make_float4(0.f, -1.f, 0.f, -1.f);
+    if (range.x + lane < range.y) {
+        v0 = __ldg(a.vals + range.x + lane);
+        b0 = __ldg(a.records + uint64_t(v0 & kVidMask) * kRecordF4 + 2);
+    }
+    if (range.x + 32 + lane < range.y) v1 = __ldg(a.vals + range.x + 32 + lane);
+
+    for (uint32_t c = range.x; c < range.y; c += 32) {
+        if (__all_sync(0xffffffffu, done)) break;
+        float4 b1 = make_float4(0.f, -1.f, 0.f, -1.f);
+        uint32_t v2 = 0;
+        if (c + 32 + lane < range.y) b1 = __ldg(a.records + uint64_t(v1 & kVidMask) * kRecordF4 + 2);
+        if (c + 64 + lane < range.y) v2 = __ldg(a.vals + c + 64 + lane);
+
+        const bool valid = c + lane < range.y;
+        const bool rel = valid && ((warp_signs >> (v0 >> 29)) & 1u) &&
+                         !(fx1 < b0.x || fx0 > b0.y || fy1 < b0.z || fy0 > b0.w);
+        const uint32_t m = __ballot_sync(0xffffffffu, rel);
+        const int nrel = __popc(m);
+        if (rel) wvid[__popc(m & ((1u << lane) - 1u))] = v0;
+        __syncwarp();
+        for (int i = lane; i < nrel * kRecordF4; i += 32) {
+            const int sl = i / kRecordF4, k = i - sl * kRecordF4;
+            wrec[sl][k] = __ldg(a.records + uint64_t(wvid[sl] & kVidMask) * kRecordF4 + k);
         }
-        __syncthreads();
-        const int nb = int(min(256u, range.y - start));
-        if (!done) {
-            for (int j = 0; j < nb; ++j) {
-                if (s_sign[j] != my_sign) continue;
-                const float4 bb = s_rec[2][j];
-                if (pcx < bb.x || pcx > bb.y || pcy < bb.z || pcy > bb.w) continue;
-                const float4 lo = s_rec[0][j], hi = s_rec[1][j];
-                float t0 = lo.x * ix, t1 = hi.x * ix;
-                float ta = fminf(t0, t1), tb = fmaxf(t0, t1);
-                t0 = lo.y * iy;
-                t1 = hi.y * iy;
-                ta = fmaxf(ta, fminf(t0, t1));
-                tb = fminf(tb, fmaxf(t0, t1));
-                t0 = lo.z * iz;
-                t1 = hi.z * iz;
-                ta = fmaxf(ta, fminf(t0, t1));
-                tb = fminf(tb, fmaxf(t0, t1));
-                if (!(ta <= tb && ta > 0.0f)) continue;
-                // voxel_alpha (field.hpp:92-116), K-point midpoint quadrature
-                const float4 va = s_rec[3][j], vb = s_rec[4][j];
-                const float V[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
-                const float seg = tb - ta;
-                const float lk = seg * dnorm * (1.0f / K);
-                float sa[K], tk[K];
-                float sum = 0.f;
+        __syncwarp();
+        uint32_t mm = m;
+        for (int sl = 0; sl < nrel; ++sl) {
+            const int j = __ffs(mm) - 1;  // chunk-local entry index (for the record pass)
+            mm &= mm - 1;
+            if (done || (wvid[sl] >> 29) != my_sign) continue;
+            const float4 bb = wrec[sl][2];
+            if (pcx < bb.x || pcx > bb.y || pcy < bb.z || pcy > bb.w) continue;
+            const float4 lo = wrec[sl][0], hi = wrec[sl][1];
+            float t0 = lo.x * ix, t1 = hi.x * ix;
+            float ta = fminf(t0, t1), tb = fmaxf(t0, t1);
+            t0 = lo.y * iy;
+            t1 = hi.y * iy;
+            ta = fmaxf(ta, fminf(t0, t1));
+            tb = fminf(tb, fmaxf(t0, t1));
+            t0 = lo.z * iz;
+            t1 = hi.z * iz;
+            ta = fmaxf(ta, fminf(t0, t1));
+            tb = fminf(tb, fmaxf(t0, t1));
+            if (!(ta <= tb && ta > 0.0f)) continue;
+            // voxel_alpha (field.hpp:92-116), K-point midpoint quadrature
+            const float4 va = wrec[sl][3], vb = wrec[sl][4];
+            const float V[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
+            const float seg = tb - ta;
+            const float lk = seg * dnorm * (1.0f / K);
+            float sa[K], tk[K];
+            float sum = 0.f;
 #pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    tk[k] = ta + ((k + 0.5f) / K) * seg;
-                    const float qx = (tk[k] * dx - lo.x) * lo.w;
-                    const float qy = (tk[k] * dy - lo.y) * lo.w;
-                    const float qz = (tk[k] * dz - lo.z) * lo.w;
-                    const float act = explin(trilinear(V, qx, qy, qz));
-                    sum += act;
-                    sa[k] = 1.0f - fexp(-lk * act);
-                }
-                const float alpha = (K == 1) ? sa[0] : 1.0f - fexp(-lk * sum);
+            for (int k = 0; k < K; ++k) {
+                tk[k] = ta + ((k + 0.5f) / K) * seg;
+                const float qx = (tk[k] * dx - lo.x) * lo.w;
+                const float qy = (tk[k] * dy - lo.y) * lo.w;
+                const float qz = (tk[k] * dz - lo.z) * lo.w;
+                const float act = explin(trilinear(V, qx, qy, qz));
+                sum += act;
+                sa[k] = 1.0f - fexp(-lk * act);
+            }
+            const float alpha = (K == 1) ? sa[0] : 1.0f - fexp(-lk * sum);
+            const float w = T * alpha;
+            if (!RECORD) {
                 // voxel_depth (field.hpp:173-181)
                 float dvox = 0.f, Tk = 1.f;
 #pragma unroll
@@ -310,29 +424,27 @@ __global__ void __launch_bounds__(256) composite_kernel(DevCamera cam, Composite
                         }
                     }
                 }
-                const float w = T * alpha;
-                if (!RECORD) {
-                    const float4 col = s_rec[5][j], nor = s_rec[6][j];
-                    cr += w * col.x;
-                    cg += w * col.y;
-                    cb += w * col.z;
-                    nx += w * nor.x;
-                    ny += w * nor.y;
-                    nz += w * nor.z;
-                    depth += T * dvox;
-                    if (a.max_blend) atomicMax(a.max_blend + __float_as_uint(hi.w), __float_as_uint(w));
-                } else {
-                    a.contrib_entry[rec_base + cnt] = start + j;
-                    a.contrib_T[rec_base + cnt] = T;
-                }
-                T *= 1.0f - alpha;
-                ++cnt;
-                if (T < thr) {
-                    done = true;
-                    break;
-                }
+                const float4 col = wrec[sl][5], nor = wrec[sl][6];
+                cr += w * col.x;
+                cg += w * col.y;
+                cb += w * col.z;
+                nx += w * nor.x;
+                ny += w * nor.y;
+                nz += w * nor.z;
+                depth += T * dvox;
+                if (a.max_blend) atomicMax(a.max_blend + __float_as_uint(hi.w), __float_as_uint(w));
+            } else {
+                a.contrib_entry[rec_base + cnt] = c + j;
+                a.contrib_T[rec_base + cnt] = T;
             }
+            T *= 1.0f - alpha;
+            ++cnt;
+            if (T < thr) done = true;
         }
+        __syncwarp();
+        v0 = v1;
+        b0 = b1;
+        v1 = v2;
     }
     if (RECORD || !inside) return;
     // CompositeCtx::finish (raster.cpp:56-60)
@@ -449,7 +561,16 @@ inline unsigned blocks_for(uint64_t n, int threads) { return unsigned((n + threa
 
 void launch_tile_setup(const DevCamera& cam, uint8_t* masks, uint32_t* sat, FrameStatus* status,
                        cudaStream_t st) {
-    tile_setup_kernel<<<1, 1024, 0, st>>>(cam, masks, sat, status);
+    const int ncell = (cam.ntx + 1) * (cam.nty + 1);
+    const int use_smem = ncell <= kSatSmemMax;
+    const size_t smem = use_smem ? size_t(ncell) * 4 : 0;
+    static bool attr_set = false;
+    if (!attr_set) {
+        SVR_CUDA(cudaFuncSetAttribute(tile_setup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kSatSmemMax * 4));
+        attr_set = true;
+    }
+    tile_setup_kernel<<<1, 1024, smem, st>>>(cam, masks, sat, status, use_smem);
     SVR_LAUNCH("tile_setup_kernel");
 }
 
@@ -461,7 +582,9 @@ void launch_tile_masks_only(const DevCamera& cam, uint8_t* masks, cudaStream_t s
 
 void launch_preprocess(const DevCamera& cam, const PreprocessArgs& a, cudaStream_t st) {
     if (a.n == 0) return;
-    preprocess_kernel<<<blocks_for(a.n, 256), 256, 0, st>>>(cam, a);
+    const int pad = a.sh_stride | 1;
+    const size_t smem = size_t((kPreThreads * pad + 3) / 4) * 16 + size_t(kPreThreads) * kRecordF4 * 16;
+    preprocess_kernel<<<blocks_for(a.n, kPreThreads), kPreThreads, smem, st>>>(cam, a);
     SVR_LAUNCH("preprocess_kernel");
 }
 

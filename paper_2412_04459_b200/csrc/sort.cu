@@ -26,8 +26,8 @@ namespace {
 constexpr int kRadix = 256;
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 12;
-constexpr int kTileKeys = kThreads * kItems;  // 3072 pairs per partition
+constexpr int kItems = 8;
+constexpr int kTileKeys = kThreads * kItems;  // 2048 pairs per partition
 constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagInc = 2u << 30;
 constexpr uint32_t kValMask = (1u << 30) - 1;
@@ -86,7 +86,7 @@ __device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
     asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(p), "r"(v));
 }
 
-__global__ void __launch_bounds__(kThreads) onesweep_kernel(
+__global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
     const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint64_t n, RadixPass pass,
     const uint32_t* __restrict__ bin_base, uint32_t* status, uint32_t* ticket) {
@@ -164,15 +164,28 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
     __syncthreads();
     s_block_excl[dg] = block_excl;
 
+    // Decoupled look-back, four predecessors per round so the dependent
+    // L2 round trips overlap; stops at the first inclusive prefix.
     uint32_t excl = 0;
     if (part > 0) {
         int64_t p = int64_t(part) - 1;
         while (p >= 0) {
-            uint32_t s = ld_volatile(status + uint64_t(p) * kRadix + dg);
-            if ((s & ~kValMask) == 0) continue;  // not published yet
-            excl += s & kValMask;
-            if (s & kFlagInc) break;
-            --p;
+            uint32_t s[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                s[q] = (p - q >= 0) ? ld_volatile(status + uint64_t(p - q) * kRadix + dg) : kFlagInc;
+            int q = 0;
+            bool stop = false;
+            for (; q < 4; ++q) {
+                if ((s[q] & ~kValMask) == 0) break;  // not published yet: re-poll from here
+                excl += s[q] & kValMask;
+                if (s[q] & kFlagInc) {
+                    stop = true;
+                    break;
+                }
+            }
+            if (stop) break;
+            p -= q;
         }
         st_volatile(my_status, kFlagInc | (excl + cnt));
     }
@@ -204,9 +217,9 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(
 
 size_t sort_scratch_bytes(uint64_t n, int npasses) {
     uint64_t nparts = (n + kTileKeys - 1) / kTileKeys;
-    return size_t(npasses) * kRadix * 4          // histograms / bin bases
-           + size_t(npasses) * 4 + 64            // tickets
-           + size_t(nparts + 1) * kRadix * 4;    // look-back status
+    return size_t(npasses) * kRadix * 4                     // histograms / bin bases
+           + size_t(npasses) * 4 + 64                       // tickets
+           + size_t(npasses) * (nparts + 1) * kRadix * 4;   // look-back status per pass
 }
 
 int radix_sort_pairs(uint64_t* keys0, uint32_t* vals0, uint64_t* keys1, uint32_t* vals1,
@@ -225,7 +238,8 @@ int radix_sort_pairs(uint64_t* keys0, uint32_t* vals0, uint64_t* keys1, uint32_t
     uint32_t* tickets = reinterpret_cast<uint32_t*>(s + size_t(npasses) * kRadix * 4);
     uint32_t* status =
         reinterpret_cast<uint32_t*>(s + size_t(npasses) * kRadix * 4 + size_t(npasses) * 4 + 64);
-    SVR_CUDA(cudaMemsetAsync(hist, 0, size_t(npasses) * kRadix * 4 + size_t(npasses) * 4 + 64, st));
+    // one memset clears histograms, tickets and every pass's look-back status
+    SVR_CUDA(cudaMemsetAsync(hist, 0, sort_scratch_bytes(n, npasses), st));
     int hist_blocks = int(std::min<uint64_t>((n + kThreads - 1) / kThreads, 148 * 4));
     hist_kernel<<<hist_blocks, kThreads, 0, st>>>(keys0, vals0, n, spec, hist);
     SVR_LAUNCH("hist_kernel");
@@ -237,10 +251,9 @@ int radix_sort_pairs(uint64_t* keys0, uint32_t* vals0, uint64_t* keys1, uint32_t
     uint32_t* vout = vals1;
     int cur = 0;
     for (int p = 0; p < npasses; ++p) {
-        SVR_CUDA(cudaMemsetAsync(status, 0, size_t(nparts) * kRadix * 4, st));
-        onesweep_kernel<<<unsigned(nparts), kThreads, 0, st>>>(kin, vin, kout, vout, n, passes[p],
-                                                              hist + p * kRadix, status,
-                                                              tickets + p);
+        onesweep_kernel<<<unsigned(nparts), kThreads, 0, st>>>(
+            kin, vin, kout, vout, n, passes[p], hist + p * kRadix,
+            status + size_t(p) * (nparts + 1) * kRadix, tickets + p);
         SVR_LAUNCH("onesweep_kernel");
         std::swap(kin, kout);
         std::swap(vin, vout);

@@ -21,8 +21,26 @@ struct Error : std::runtime_error {
 };
 
 void cuda_check(cudaError_t e, const char* what);
+void count_launch();
 #define SVR_CUDA(x) ::svrb::cuda_check((x), #x)
-#define SVR_LAUNCH(what) ::svrb::cuda_check(cudaGetLastError(), what)
+#define SVR_LAUNCH(what) (::svrb::count_launch(), ::svrb::cuda_check(cudaGetLastError(), what))
+
+// Stages timed by svr_ctx_stage_times (CUDA events on the context stream).
+enum Stage {
+    kStageTileSetup = 0,
+    kStagePreprocess,
+    kStageScan,
+    kStageDuplicate,
+    kStageSort,
+    kStageRanges,
+    kStageComposite,
+    kStageRecord,
+    kStageDownsample,
+    kStageBackward,
+    kStageEpilogue,
+    kStageOther,
+    kNumStages
+};
 
 // Grow-only device allocation; contents are not preserved across growth.
 struct DevBuf {
@@ -50,6 +68,10 @@ struct HostBuf {
 
 struct svr_ctx {
     int device = 0;
+    bool timing = false;
+    std::vector<std::pair<int, cudaEvent_t>> marks;  // stage starting at each event
+    std::vector<cudaEvent_t> event_pool;
+    double stage_ms[svrb::kNumStages] = {};
     cudaStream_t stream = nullptr;
     int num_sms = 148;
     bool debug = false;

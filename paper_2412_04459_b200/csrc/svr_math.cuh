@@ -193,13 +193,22 @@ SVR_HD uint32_t tile_sign_mask(const DevCamera& cam, int tx, int ty) {
 // ---------------------------------------------------------------- fp32 field
 // explin (field.hpp:23-26) and its derivative (field.hpp:28-31).
 #if defined(__CUDA_ARCH__)
-__device__ __forceinline__ float fexp(float x) { return __expf(x); }
+// exp(x) as one MUFU.EX2 (flush-to-zero; results are < 1e-38 only where they
+// are irrelevant to alpha = 1 - exp(-x) and explin's exponential branch).
+__device__ __forceinline__ float fexp(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x * 1.4426950408889634f));
+    return y;
+}
 #else
 inline float fexp(float x) { return expf(x); }
 #endif
-// exp(x/1.1 - 1 + ln 1.1) = exp(x/1.1) * (1.1/e)
+// exp(x/1.1 - 1 + ln 1.1) = exp(x/1.1) * (1.1/e); branch-free select
 constexpr float kExplinScale = 0.40467196f;  // 1.1 / e
-SVR_HD float explin(float x) { return x > kExplinKnee ? x : fexp(x * (1.0f / 1.1f)) * kExplinScale; }
+SVR_HD float explin(float x) {
+    const float e = fexp(x * (1.0f / 1.1f)) * kExplinScale;
+    return x > kExplinKnee ? x : e;
+}
 SVR_HD float explin_deriv(float x) {
     return x > kExplinKnee ? 1.0f : fexp(x * (1.0f / 1.1f)) * (kExplinScale / 1.1f);
 }
