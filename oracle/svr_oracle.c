@@ -656,3 +656,50 @@ int orc_backward(const svr_scene_desc* s, const svr_camera* cam, const svr_rende
     free_fwd(&f);
     return SVR_OK;
 }
+
+/* ------------------------------------------------------------ primitive hooks
+ * Exported only so tests/test_oracle_cpu.py can pin the restatement against
+ * the known-answer vectors of the reference's unit tests
+ * (test_octree.cpp, test_field.cpp, test_sh.cpp, test_camera.cpp,
+ * test_image.cpp). */
+uint64_t orc_t_octpath(uint32_t i, uint32_t j, uint32_t k, int level) {  /* octree.hpp:51-66 */
+    uint64_t code = 0;
+    for (int n = 0; n < level; ++n) {
+        uint64_t bits = 4 * (i & 1) + 2 * (j & 1) + (k & 1);
+        code |= bits << (3 * n);
+        i >>= 1; j >>= 1; k >>= 1;
+    }
+    return code << (3 * (MAX_LEVEL - level));
+}
+uint32_t orc_t_sign_bits(double x, double y, double z) { return sign_bits(V3(x, y, z)); }
+uint64_t orc_t_dir_dep_order(uint64_t code, uint32_t s) { return code ^ ((uint64_t)s * GROUP_ONES); }
+double orc_t_explin(double x) { return explin(x); }
+double orc_t_explin_deriv(double x) { return explin_deriv(x); }
+int orc_t_ray_aabb(const double* c, double size, const double* o, const double* d, double* ab) {
+    return ray_aabb(V3(c[0], c[1], c[2]), size, V3(o[0], o[1], o[2]), V3(d[0], d[1], d[2]), &ab[0], &ab[1]);
+}
+double orc_t_voxel_alpha(const double* V, const double* c, double size, const double* o,
+                         const double* d, int K) {
+    double a, b;
+    ray_aabb(V3(c[0], c[1], c[2]), size, V3(o[0], o[1], o[2]), V3(d[0], d[1], d[2]), &a, &b);
+    acache ca;
+    return voxel_alpha(V, V3(c[0], c[1], c[2]), size, a, b, V3(o[0], o[1], o[2]), V3(d[0], d[1], d[2]), K, &ca);
+}
+double orc_t_voxel_depth(const double* sa, const double* t, int K) {
+    acache c;
+    memset(&c, 0, sizeof c);
+    c.K = K;
+    for (int k = 0; k < K; ++k) { c.sa[k] = sa[k]; c.t[k] = t[k]; }
+    return voxel_depth(&c);
+}
+void orc_t_sh_basis(int deg, double x, double y, double z, double* b) { sh_basis(deg, V3(x, y, z), b); }
+void orc_t_pixel_ray(const svr_camera* cam, double px, double py, double* d) {
+    v3 r = pixel_dir(cam, px, py);
+    d[0] = r.x; d[1] = r.y; d[2] = r.z;
+}
+void orc_t_downsample(const double* src, int sw, int sh, int ch, double* dst, int W, int H) {
+    downsample(src, sw, sh, ch, dst, W, H);
+}
+void orc_t_adjoint(const double* g, int W, int H, int ch, double* src, int sw, int sh) {
+    adjoint(g, W, H, ch, src, sw, sh);
+}

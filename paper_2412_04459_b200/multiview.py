@@ -1,0 +1,103 @@
+"""Multi-GPU paths of the rasterizer: the two partitioned workloads of
+SURVEY §8(e).
+
+* View-sharded rendering (config 4): every rank holds a replica of the scene
+  and renders its own subset of the views; no collective on the data path.
+* View-batch training step (config 5): every rank runs forward -> L1 ->
+  backward for its views into ONE flat gradient buffer
+  [density (P) | SH (N*stride)] and the ranks sum it with a single in-place
+  all-reduce (NCCL over NVLink on B200s; gloo in the CPU tests).
+
+One process per GPU (torch.distributed for the plumbing). The reference has
+no distributed code; the sum of per-view `render_backward` gradients is the
+oracle (tests/test_multiview_cpu.py, tests/test_gpu_multiview.py).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+
+def shard_views(n_views: int, rank: int, world: int) -> List[int]:
+    """Views owned by `rank`: rank, rank+world, ... (balanced to within one)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("rank must be in [0, world)")
+    return list(range(rank, n_views, world))
+
+
+def flat_layout(n_pool: int, n_sh: int, align: int = 64):
+    """Offsets (in floats) of the density and SH gradients in the flat buffer."""
+    sh_off = (n_pool + align - 1) // align * align
+    return 0, sh_off, sh_off + n_sh
+
+
+def allreduce_flat(buf, group=None) -> None:
+    """Sums the flat gradient buffer over all ranks, in place (one collective)."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+
+
+class ShardedTrainer:
+    """Config-5 training step on this rank's GPU.
+
+    `step(view_ids)` renders each view with training records, applies the L1
+    loss against its ground truth and accumulates render_backward into the
+    flat device gradient buffer, then all-reduces it across ranks.
+    """
+
+    def __init__(self, ctx, scene, cameras: Sequence, gts: Sequence, opts, group=None):
+        import torch
+
+        import paper_2412_04459_b200 as svr
+        self.svr = svr
+        self.ctx, self.scene, self.cams, self.opts, self.group = ctx, scene, cameras, opts, group
+        dev = torch.device("cuda", ctx.device)
+        self.gts = [g if isinstance(g, torch.Tensor) else
+                    torch.tensor(np.asarray(g), dtype=torch.float32, device=dev) for g in gts]
+        a = scene.arrays
+        self.n_pool, self.n_sh = a.n_pool, a.n_voxels * a.sh_stride
+        d0, s0, total = flat_layout(self.n_pool, self.n_sh)
+        self.flat = torch.zeros(total, dtype=torch.float32, device=dev)
+        self.priority = torch.zeros(a.n_voxels, dtype=torch.float32, device=dev)
+        self.loss = torch.zeros(1, dtype=torch.float32, device=dev)
+        self.density_grad = self.flat[d0:d0 + self.n_pool]
+        self.sh_grad = self.flat[s0:s0 + self.n_sh]
+        self.frame = svr.Frame(ctx)
+        self.stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+
+    def step(self, view_ids: Sequence[int], reduce: bool = True) -> float:
+        import torch
+        svr = self.svr
+        lib = svr.load_library()
+        g = svr.svr_gradients()
+        g.density, g.sh = self.density_grad.data_ptr(), self.sh_grad.data_ptr()
+        g.priority, g.on_device = self.priority.data_ptr(), 1
+        torch.cuda.current_stream().synchronize()
+        with torch.cuda.stream(self.stream):
+            self.flat.zero_()
+            self.priority.zero_()
+        total = 0.0
+        for n, v in enumerate(view_ids):
+            c, o = self.cams[v].to_c(), self.opts.to_c()
+            svr._check(lib.svr_train_step_l1(self.ctx.h, self.scene.h, C.byref(c), C.byref(o),
+                                             C.c_void_p(self.gts[v].data_ptr()), self.frame.h,
+                                             C.byref(g), 1, C.c_void_p(self.loss.data_ptr())))
+            with torch.cuda.stream(self.stream):
+                total += self.loss  # device scalar, read once below
+        with torch.cuda.stream(self.stream):
+            loss_t = total if isinstance(total, torch.Tensor) else torch.zeros(1, device=self.flat.device)
+        torch.cuda.current_stream().wait_stream(self.stream)
+        if reduce:
+            allreduce_flat(self.flat, self.group)
+        return float(loss_t.item())
+
+
+def sum_gradients_reference(per_view_grads: Sequence[dict]) -> dict:
+    """Oracle for the all-reduce: element-wise sum of per-view gradients."""
+    out = {}
+    for k in ("density", "sh", "priority"):
+        out[k] = np.sum([np.asarray(g[k], np.float64).reshape(-1) for g in per_view_grads], axis=0)
+    return out

@@ -1,0 +1,96 @@
+"""CPU checks of the C-ABI boundary (no GPU): the library loads, exports every
+function include/svr_b200.h declares, its structs match the ctypes mirror,
+host-only utilities match the reference, and compute entry points fail
+loudly (no CPU fallback) when no device exists."""
+import ctypes as C
+import os
+import re
+import subprocess
+import tempfile
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "svr_b200.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"^[A-Za-z_][\w \*]*?\b(svr_\w+)\s*\(", src, flags=re.M)
+    return sorted(set(names))
+
+
+def test_library_exports_every_declared_symbol(svr):
+    lib = svr.load_library()
+    names = declared_functions()
+    assert len(names) >= 30
+    for n in names:
+        assert hasattr(lib, n), f"{n} declared in svr_b200.h but not exported"
+    assert sorted(svr.EXPORTS) == names
+    assert lib.svr_abi_version() == 1
+
+
+def test_struct_layouts_match_header(svr):
+    structs = {"svr_camera": svr.svr_camera, "svr_render_options": svr.svr_render_options,
+               "svr_scene_desc": svr.svr_scene_desc, "svr_frame_info": svr.svr_frame_info,
+               "svr_upstream": svr.svr_upstream, "svr_gradients": svr.svr_gradients}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void){"]
+    for name, cls in structs.items():
+        lines.append(f'printf("{name} %zu\\n", sizeof({name}));')
+        for f, _ in cls._fields_:
+            lines.append(f'printf("{name}.{f} %zu\\n", offsetof({name}, {f}));')
+    lines.append("return 0;}")
+    with tempfile.TemporaryDirectory() as d:
+        c = os.path.join(d, "layout.c")
+        open(c, "w").write("\n".join(lines))
+        exe = os.path.join(d, "layout")
+        subprocess.run(["gcc", c, "-o", exe], check=True)
+        out = subprocess.run([exe], check=True, capture_output=True, text=True).stdout
+    got = dict(line.split() for line in out.strip().splitlines())
+    for name, cls in structs.items():
+        assert int(got[name]) == C.sizeof(cls), name
+        for f, _ in cls._fields_:
+            assert int(got[f"{name}.{f}"]) == getattr(cls, f).offset, f"{name}.{f}"
+
+
+def test_no_cpu_fallback_without_device(svr):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a CUDA device is present")
+    with pytest.raises(svr.NoDeviceError):
+        svr.Context(0)
+
+
+def test_ring_cameras_match_reference(svr):
+    from oracle import ref
+    if not os.path.exists(ref.REF_SO) and not os.path.isdir("/root/reference/proj"):
+        pytest.skip("compiled reference unavailable")
+    for n, i, w, h, dist, fov in [(1, 0, 1024, 1024, 1.3, 55.0), (256, 77, 1024, 1024, 1.0, 55.0),
+                                  (5, 4, 96, 64, 1.5, 60.0)]:
+        a, b = svr.ring_camera(n, i, w, h, dist, fov), ref.ref_ring_camera(n, i, w, h, dist, fov)
+        assert (a.fx, a.fy, a.cx, a.cy) == (b.fx, b.fy, b.cx, b.cy)
+        assert np.array_equal(a.rot, b.rot) and np.array_equal(a.pos, b.pos)
+
+
+@pytest.mark.parametrize("seed,target,maxlv,deg", [(2024, 65536, 7, 3), (7, 20000, 9, 1),
+                                                   (3, 513, 4, 0)])
+def test_generator_matches_reference(svr, seed, target, maxlv, deg):
+    from oracle import ref
+    if not os.path.exists(ref.REF_SO) and not os.path.isdir("/root/reference/proj"):
+        pytest.skip("compiled reference unavailable")
+    a = svr.synth_random_scene(seed, target, maxlv, deg)
+    r = ref.RefScene.generate(seed, target, maxlv, deg).arrays()
+    for f in ("codes", "levels", "corner_index", "density", "sh"):
+        assert np.array_equal(getattr(a, f), getattr(r, f)), f
+
+
+def test_option_objects_roundtrip(svr):
+    o = svr.RenderOptions(K=3, t_threshold=1e-3, supersample=1.5, background=(1, 2, 3),
+                          record_stats=True, training=True).to_c()
+    assert (o.K, o.t_threshold, o.supersample, list(o.background), o.record_stats, o.training) == \
+        (3, 1e-3, 1.5, [1.0, 2.0, 3.0], 1, 1)
+    cam = svr.Camera(10, 20, 1.0, 2.0, 3.0, 4.0, np.arange(9.0).reshape(3, 3), np.array([5., 6, 7]))
+    back = svr.Camera.from_c(cam.to_c())
+    assert np.array_equal(back.rot, cam.rot) and np.array_equal(back.pos, cam.pos)

@@ -1,0 +1,203 @@
+"""CPU tests of the oracle (test infrastructure) — no GPU.
+
+1. The plain-C restatement (oracle/svr_oracle.c) reproduces the known-answer
+   vectors of the reference's own unit tests.
+2. It reproduces the committed golden fixtures (generated from the
+   unmodified reference by tests/golden/make_golden.py) bit for bit on the
+   integer/fp64-exact arrays and to 1e-12 on the images and gradients.
+3. Where the compiled reference (oracle/_ref/libsvr_ref.so) is present, it
+   matches it on a fresh configuration.
+"""
+import ctypes as C
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import port
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "ref_small.npz")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    l = port.load()
+    P = C.c_void_p
+    for name, res, args in [
+        ("orc_t_octpath", C.c_uint64, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_int]),
+        ("orc_t_sign_bits", C.c_uint32, [C.c_double] * 3),
+        ("orc_t_dir_dep_order", C.c_uint64, [C.c_uint64, C.c_uint32]),
+        ("orc_t_explin", C.c_double, [C.c_double]),
+        ("orc_t_explin_deriv", C.c_double, [C.c_double]),
+        ("orc_t_ray_aabb", C.c_int, [P, C.c_double, P, P, P]),
+        ("orc_t_voxel_alpha", C.c_double, [P, P, C.c_double, P, P, C.c_int]),
+        ("orc_t_voxel_depth", C.c_double, [P, P, C.c_int]),
+        ("orc_t_sh_basis", None, [C.c_int, C.c_double, C.c_double, C.c_double, P]),
+        ("orc_t_pixel_ray", None, [P, C.c_double, C.c_double, P]),
+        ("orc_t_downsample", None, [P, C.c_int, C.c_int, C.c_int, P, C.c_int, C.c_int]),
+        ("orc_t_adjoint", None, [P, C.c_int, C.c_int, C.c_int, P, C.c_int, C.c_int]),
+    ]:
+        f = getattr(l, name)
+        f.restype, f.argtypes = res, args
+    return l
+
+
+def _p(a):
+    return np.ascontiguousarray(a).ctypes.data_as(C.c_void_p)
+
+
+def test_known_morton_codes(lib):  # test_octree.cpp:45-53
+    assert lib.orc_t_octpath(0, 0, 0, 5) == 0
+    assert lib.orc_t_octpath(1, 0, 0, 1) == 140737488355328
+    assert lib.orc_t_octpath(0, 1, 0, 1) == 0b010 << 45
+    assert lib.orc_t_octpath(0, 0, 1, 1) == 0b001 << 45
+
+
+def test_known_sign_bits_and_order(lib):  # test_octree.cpp:133-158
+    assert lib.orc_t_sign_bits(1, 1, 1) == 0
+    assert lib.orc_t_sign_bits(-1, 2, -3) == 5
+    assert lib.orc_t_sign_bits(0, -1, 0) == 2
+    assert lib.orc_t_sign_bits(-1, -1, -1) == 7
+    all2 = sum(0b010 << (3 * g) for g in range(16))
+    all4 = sum(0b100 << (3 * g) for g in range(16))
+    assert lib.orc_t_dir_dep_order(all2, 0b110) == all4
+    rng = np.random.default_rng(7)
+    for _ in range(50):
+        code = int(lib.orc_t_octpath(*[int(x) for x in rng.integers(0, 1 << 16, 3)], 16))
+        for s in range(8):
+            assert lib.orc_t_dir_dep_order(lib.orc_t_dir_dep_order(code, s), s) == code
+
+
+def test_known_explin(lib):  # test_field.cpp:35-53
+    assert lib.orc_t_explin(2.0) == 2.0 and lib.orc_t_explin(5.5) == 5.5
+    assert math.isclose(lib.orc_t_explin(1.1), 1.1, rel_tol=1e-14)
+    assert math.isclose(lib.orc_t_explin(0.0), 1.1 / math.e, rel_tol=1e-12)
+    assert lib.orc_t_explin_deriv(2.0) == 1.0
+    h = 1e-7
+    assert math.isclose(lib.orc_t_explin(1.1 + h) - lib.orc_t_explin(1.1 - h), 2 * h, rel_tol=1e-4)
+
+
+def test_known_slab_and_alpha(lib):  # test_field.cpp:76-114
+    ab = np.zeros(2)
+    assert lib.orc_t_ray_aabb(_p([0., 0, 0]), 2.0, _p([-5., 0, 0]), _p([1., 0, 0]), ab.ctypes.data_as(C.c_void_p))
+    assert math.isclose(ab[0], 4.0) and math.isclose(ab[1], 6.0)
+    assert not lib.orc_t_ray_aabb(_p([0., 0, 0]), 2.0, _p([-5., 3, 0]), _p([1., 0, 0]), ab.ctypes.data_as(C.c_void_p))
+    assert not lib.orc_t_ray_aabb(_p([0., 0, 0]), 2.0, _p([0.2, 0.1, 0]), _p([1., 0, 0]), ab.ctypes.data_as(C.c_void_p))
+    assert lib.orc_t_ray_aabb(_p([0., 0, 0]), 2.0, _p([-5., 0, 0]), _p([2., 0, 0]), ab.ctypes.data_as(C.c_void_p))
+    assert math.isclose(ab[0], 2.0) and math.isclose(ab[1], 3.0)
+    V = np.full(8, 2.5)
+    o, d = np.array([-3., 0.1, 0.2]), np.array([2., 0.1, -0.05])
+    lib.orc_t_ray_aabb(_p([0., 0, 0]), 1.0, _p(o), _p(d), ab.ctypes.data_as(C.c_void_p))
+    l = (ab[1] - ab[0]) * np.linalg.norm(d)
+    for K in range(1, 9):
+        a = lib.orc_t_voxel_alpha(_p(V), _p([0., 0, 0]), 1.0, _p(o), _p(d), K)
+        assert math.isclose(a, 1 - math.exp(-2.5 * l), rel_tol=1e-13)
+    V = np.full(8, -10.0)
+    a = lib.orc_t_voxel_alpha(_p(V), _p([0., 0, 0]), 1.0, _p([-2., 0.01, -0.02]), _p([1., 0, 0]), 1)
+    assert a < 1e-4 and math.isclose(a, 1 - math.exp(-1.0 * lib.orc_t_explin(-10.0)), rel_tol=1e-12)
+
+
+def test_known_depth_sh_ray(lib):  # test_field.cpp:259-270, test_sh.cpp:65-77, test_camera.cpp:11-22
+    assert math.isclose(lib.orc_t_voxel_depth(_p([0.3]), _p([2.0]), 1), 0.6)
+    assert math.isclose(lib.orc_t_voxel_depth(_p([1.0, 0.7]), _p([2.0, 3.0]), 2), 2.0)
+    assert math.isclose(lib.orc_t_voxel_depth(_p([0.2, 0.7]), _p([2.0, 3.0]), 2), 0.4 + 0.8 * 0.7 * 3.0)
+    b = np.zeros(16)
+    lib.orc_t_sh_basis(3, 1 / 3, 2 / 3, 2 / 3, b.ctypes.data_as(C.c_void_p))
+    C1 = 0.4886025119029199
+    expect = {0: 0.28209479177387814, 1: -C1 * 2 / 3, 2: C1 * 2 / 3, 3: -C1 / 3,
+              4: 1.0925484305920792 * 2 / 9, 6: 0.31539156525252005 * (8 / 9 - 1 / 9 - 4 / 9),
+              8: 0.5462742152960396 * (1 / 9 - 4 / 9),
+              12: 0.3731763325901154 * (2 / 3) * (8 / 9 - 3 / 9 - 12 / 9)}
+    for i, v in expect.items():
+        assert math.isclose(b[i], v, rel_tol=1e-12, abs_tol=1e-15)
+    import paper_2412_04459_b200 as svr
+    cam = svr.Camera(1, 1, 1.0, 1.0, 0.5, 0.5).to_c()
+    d = np.zeros(3)
+    lib.orc_t_pixel_ray(C.byref(cam), 0.0, 0.0, d.ctypes.data_as(C.c_void_p))
+    assert list(d) == [0.0, 0.0, 1.0]
+
+
+def test_known_resampler(lib):  # test_image.cpp:28-86
+    src = np.array([[x + 10 * y for x in range(4)] for y in range(4)], float)
+    dst = np.zeros((2, 2))
+    lib.orc_t_downsample(_p(src), 4, 4, 1, dst.ctypes.data_as(C.c_void_p), 2, 2)
+    assert math.isclose(dst[0, 0], (0 + 1 + 10 + 11) / 4) and math.isclose(dst[1, 1], (22 + 23 + 32 + 33) / 4)
+    rng = np.random.default_rng(3)
+    for sw, sh, dw, dh in [(9, 6, 4, 3), (15, 11, 10, 7), (6, 6, 6, 6)]:
+        x = rng.uniform(size=(sh, sw, 3))
+        y = rng.uniform(size=(dh, dw, 3))
+        ax = np.zeros((dh, dw, 3))
+        aty = np.zeros((sh, sw, 3))
+        lib.orc_t_downsample(_p(x), sw, sh, 3, ax.ctypes.data_as(C.c_void_p), dw, dh)
+        lib.orc_t_adjoint(_p(y), dw, dh, 3, aty.ctypes.data_as(C.c_void_p), sw, sh)
+        assert math.isclose((ax * y).sum(), (x * aty).sum(), rel_tol=1e-12)
+
+
+@pytest.fixture(scope="module")
+def golden():
+    return np.load(GOLDEN)
+
+
+@pytest.fixture(scope="module")
+def gscene(golden):
+    import paper_2412_04459_b200 as svr
+    seed, target, maxlv, deg = [int(x) for x in golden["scene_params"]]
+    a = svr.synth_random_scene(seed, target, maxlv, deg)
+    from golden.make_golden import scene_digest
+    assert scene_digest(a) == str(golden["scene_digest"]), "generator G drifted from the golden scene"
+    return a
+
+
+def _case(golden, name):
+    import paper_2412_04459_b200 as svr
+    c = golden[f"{name}/camera"]
+    cam = svr.Camera(int(c[0]), int(c[1]), c[2], c[3], c[4], c[5], c[6:15].reshape(3, 3), c[15:18])
+    o = golden[f"{name}/opts"]
+    return cam, int(o[0]), float(o[1]), tuple(o[2:5])
+
+
+@pytest.mark.parametrize("name", ["ss1_K2", "ss15_K1"])
+def test_port_matches_golden(golden, gscene, name):
+    import paper_2412_04459_b200 as svr
+    cam, K, ss, bg = _case(golden, name)
+    import oracle.ref as _r  # noqa: F401  (only for the scaled-camera helper below)
+    sw, sh = int(math.ceil(ss * cam.width)), int(math.ceil(ss * cam.height))
+    rx, ry = sw / cam.width, sh / cam.height
+    scam = svr.Camera(sw, sh, cam.fx * rx, cam.fy * ry, cam.cx * rx, cam.cy * ry, cam.rot, cam.pos)
+    assert np.array_equal(port.tile_masks(scam), golden[f"{name}/tile_masks"])
+    vis, aabb, rect = port.project(gscene, scam)
+    assert np.array_equal(vis, golden[f"{name}/visible"].astype(bool))
+    assert np.array_equal(aabb, golden[f"{name}/aabb"])
+    assert np.array_equal(rect, golden[f"{name}/rect"])
+    for sorted_, tag in [(False, "entry"), (True, "sorted")]:
+        k, v = port.entries(gscene, scam, sorted_)
+        assert np.array_equal(k, golden[f"{name}/{tag}_keys"])
+        assert np.array_equal(v, golden[f"{name}/{tag}_values"])
+    opts = svr.RenderOptions(K=K, supersample=ss, background=bg)
+    r = port.render(gscene, cam, opts)
+    for k in ("color", "depth", "median_depth", "normal", "transmittance"):
+        assert np.allclose(r[k], golden[f"{name}/{k}"], rtol=1e-12, atol=1e-12), k
+    g = port.backward(gscene, cam, svr.RenderOptions(K=K, supersample=ss, background=bg, training=True),
+                      d_color=golden[f"{name}/d_color"])
+    for k, gk in [("density", "g_density"), ("sh", "g_sh"), ("priority", "g_priority")]:
+        assert np.allclose(np.asarray(g[k]).reshape(-1), golden[f"{name}/{gk}"], rtol=1e-10, atol=1e-14), k
+
+
+def test_port_matches_compiled_reference():
+    from oracle import ref
+    if not os.path.exists(ref.REF_SO) and not os.path.isdir("/root/reference/proj"):
+        pytest.skip("compiled reference unavailable on this host")
+    import paper_2412_04459_b200 as svr
+    a = svr.synth_random_scene(99, 3000, 7, 3)
+    rs = ref.RefScene.from_arrays(a)
+    cam = svr.ring_camera(5, 3, 72, 56, 1.2, 60.0)
+    opts = svr.RenderOptions(K=3, supersample=1.25, background=(0.3, 0.1, 0.2), record_stats=True)
+    r1 = port.render(a, cam, opts)
+    r2 = ref.ref_render(rs, cam, opts, n_voxels=a.n_voxels)
+    for k in ("color", "depth", "median_depth", "normal", "transmittance", "max_blend_weight"):
+        assert np.array_equal(r1[k], r2[k]), k
+    scam = ref.ref_scaled_camera(cam, 1.25)
+    k1, v1 = port.entries(a, scam, True)
+    k2, v2 = ref.ref_entries(rs, scam, True)
+    assert np.array_equal(k1, k2) and np.array_equal(v1, v2)
