@@ -168,6 +168,32 @@ int svr_frame_records(svr_frame* frame, uint32_t* pre_vids, uint64_t n_pre,
                       uint32_t* contrib_pre, double* contrib_a, double* contrib_b,
                       uint64_t n_contribs);
 
+/* svr::PreVoxel (raster.hpp:55-64) with VoxelNormal (field.hpp:143-147). */
+typedef struct svr_pre_voxel {
+    uint32_t vid;
+    int32_t degenerate;
+    double center[3];
+    double size;
+    double V[8];
+    double color[3];
+    double normal[3];
+    double raw[3];
+    double x0, x1, y0, y1;
+    int32_t tx0, tx1, ty0, ty1;
+} svr_pre_voxel;
+
+/* ForwardRecords::pre of a rendered frame: every visible voxel in vid order
+ * (n = svr_frame_info.n_visible). Geometry and AABB are the exact fp64
+ * values; colour and normal come from the fp32 preprocess. */
+int svr_frame_pre(svr_frame* frame, svr_pre_voxel* out, uint64_t n);
+
+/* render_oracle (raster.cpp:425-473): brute-force per-ray compositing of
+ * every visible voxel in (entry distance, dir_dep_order) order, fp64, no
+ * tiles and no supersampling. Fills the frame's five target-resolution
+ * images. O(hits x voxels) per pixel: a test oracle for small scenes. */
+int svr_render_oracle(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam,
+                      const svr_render_options* opts, svr_frame* frame);
+
 /* ---- backward (raster.cpp:303-423) ------------------------------------ */
 typedef struct svr_upstream {
     const float* d_color;        /* W*H*3 or NULL   */

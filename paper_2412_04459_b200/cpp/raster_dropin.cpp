@@ -1,0 +1,393 @@
+// raster_dropin.cpp — drop-in replacement for proj/src/raster.cpp.
+//
+// Implements every function declared in the reference's
+// proj/include/svr/raster.hpp (compile against those headers, link instead of
+// raster.cpp) on top of the C ABI of include/svr_b200.h, i.e. on the
+// hand-written sm_100a kernels of libsvr_b200.so. There is no CPU fallback:
+// without a device every entry point throws std::runtime_error.
+//
+//   make_pools          raster.cpp:65-70   host copy, same semantics
+//   project_voxel       raster.cpp:72-118  svr_project_voxels (fp64, bit-exact)
+//   tile_sign_patterns  raster.cpp:120-142 svr_tile_sign_masks
+//   build_sort_entries  raster.cpp:144-172 svr_build_sort_entries (same emission order)
+//   sort_entries        raster.cpp:174-178 svr_sort_entries (onesweep radix sort)
+//   render(_with_pools) raster.cpp:205-301 svr_scene_upload + svr_render + downloads
+//   render_backward     raster.cpp:303-423 svr_render_backward on the frame that
+//                                          produced the ForwardRecords
+//   render_oracle       raster.cpp:425-473 svr_render_oracle (fp64 brute force)
+//
+// Error behaviour: the C status codes are rethrown as the exception types the
+// reference throws (invalid_argument / length_error / runtime_error).
+// Threading: one svr_ctx per host thread (thread_local), device from
+// $SVR_DEVICE (default 0); all functions stay reentrant.
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "svr/raster.hpp"
+#include "svr_b200.h"
+
+namespace svr {
+
+namespace {
+
+void check(int st) {
+    if (st == SVR_OK) return;
+    std::string msg = svr_last_error();
+    switch (st) {
+        case SVR_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case SVR_ERR_LENGTH: throw std::length_error(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+
+struct CtxHolder {
+    svr_ctx* c = nullptr;
+    ~CtxHolder() {
+        if (c) svr_ctx_destroy(c);
+    }
+};
+
+svr_ctx* ctx() {
+    thread_local CtxHolder h;
+    if (!h.c) {
+        const char* dev = std::getenv("SVR_DEVICE");
+        check(svr_ctx_create(dev ? std::atoi(dev) : 0, &h.c));
+    }
+    return h.c;
+}
+
+svr_camera to_c(const Camera& cam) {
+    svr_camera c;
+    c.width = cam.width;
+    c.height = cam.height;
+    c.fx = cam.fx;
+    c.fy = cam.fy;
+    c.cx = cam.cx;
+    c.cy = cam.cy;
+    for (int i = 0; i < 9; ++i) c.rot[i] = cam.rot.m[i];
+    c.pos[0] = cam.pos.x;
+    c.pos[1] = cam.pos.y;
+    c.pos[2] = cam.pos.z;
+    return c;
+}
+
+svr_render_options to_c(const RenderOptions& o) {
+    svr_render_options r;
+    r.K = o.K;
+    r.t_threshold = o.t_threshold;
+    r.supersample = o.supersample;
+    r.background[0] = o.background.x;
+    r.background[1] = o.background.y;
+    r.background[2] = o.background.z;
+    r.near_plane = o.near_plane;
+    r.far_sentinel = o.far_sentinel;
+    r.record_stats = o.record_stats ? 1 : 0;
+    r.training = o.training ? 1 : 0;
+    return r;
+}
+
+// Device copy of a SparseScene whose parameter pools come from PoolsD
+// (narrowed to the float the scene stores, so make_pools round-trips).
+struct SceneHandle {
+    svr_scene* s = nullptr;
+    ~SceneHandle() {
+        if (s) svr_scene_destroy(s);
+    }
+};
+
+std::unique_ptr<SceneHandle> upload(const SparseScene& scene, const PoolsD& pools) {
+    const size_t n = scene.voxel_count();
+    std::vector<uint64_t> codes(n);
+    std::vector<uint8_t> levels(n);
+    for (size_t i = 0; i < n; ++i) {
+        if (scene.voxels[i].level < 1 || scene.voxels[i].level > 255)
+            throw std::invalid_argument("octree level out of [1,16]");
+        codes[i] = scene.voxels[i].code;
+        levels[i] = uint8_t(scene.voxels[i].level);
+    }
+    std::vector<float> dens(pools.density.begin(), pools.density.end());
+    std::vector<float> sh(pools.sh.begin(), pools.sh.end());
+    if (dens.size() != scene.pool_count() || sh.size() != scene.sh.size())
+        throw std::invalid_argument("parameter pools do not match the scene");
+    svr_scene_desc d{};
+    d.n_voxels = n;
+    d.n_pool = scene.pool_count();
+    d.sh_degree = scene.sh_degree;
+    d.bounds_center[0] = scene.bounds.center.x;
+    d.bounds_center[1] = scene.bounds.center.y;
+    d.bounds_center[2] = scene.bounds.center.z;
+    d.bounds_size = scene.bounds.size;
+    d.codes = codes.data();
+    d.levels = levels.data();
+    static_assert(sizeof(std::array<uint32_t, 8>) == 32, "corner_index layout");
+    d.corner_index = n ? scene.corner_index[0].data() : nullptr;
+    d.density = dens.data();
+    d.sh = sh.data();
+    auto h = std::make_unique<SceneHandle>();
+    check(svr_scene_upload(ctx(), &d, &h->s));
+    return h;
+}
+
+Image download_image(svr_frame* f, svr_buffer which, int w, int h, int ch, double far = 0.0,
+                     bool sentinel = false) {
+    std::vector<float> tmp(size_t(w) * h * ch);
+    check(svr_frame_download(f, which, tmp.data(), tmp.size() * sizeof(float)));
+    Image img(w, h, ch);
+    const float ffar = float(far);
+    for (size_t i = 0; i < tmp.size(); ++i)
+        img.data[i] = (sentinel && tmp[i] == ffar) ? far : double(tmp[i]);
+    return img;
+}
+
+// GPU state behind a ForwardRecords handed out by render_with_pools. Owned by
+// the shared_ptr's deleter, so it lives exactly as long as the records.
+struct GpuRecords {
+    std::unique_ptr<SceneHandle> scene;
+    svr_frame* frame = nullptr;
+    ~GpuRecords() {
+        if (frame) svr_frame_destroy(frame);
+    }
+};
+
+std::mutex g_mu;
+std::unordered_map<const ForwardRecords*, std::shared_ptr<GpuRecords>> g_records;
+
+Camera scaled_camera(const Camera& cam, const RenderOptions& o) {
+    const int sw = int(std::ceil(o.supersample * cam.width));
+    const int sh = int(std::ceil(o.supersample * cam.height));
+    return cam.scaled(sw, sh);
+}
+
+}  // namespace
+
+PoolsD make_pools(const SparseScene& scene) {
+    PoolsD p;
+    p.density.assign(scene.density.begin(), scene.density.end());
+    p.sh.assign(scene.sh.begin(), scene.sh.end());
+    return p;
+}
+
+bool project_voxel(const Camera& cam, const Vec3& center, double size, PreVoxel& out,
+                   double near_plane) {
+    const svr_camera c = to_c(cam);
+    const double cen[3] = {center.x, center.y, center.z};
+    uint8_t vis = 0;
+    double aabb[4];
+    int32_t rect[4];
+    check(svr_project_voxels(ctx(), &c, 1, cen, &size, near_plane, &vis, aabb, rect));
+    out.tx0 = 0;
+    out.tx1 = -1;
+    if (!vis) return false;
+    out.x0 = aabb[0];
+    out.x1 = aabb[1];
+    out.y0 = aabb[2];
+    out.y1 = aabb[3];
+    out.tx0 = rect[0];
+    out.tx1 = rect[1];
+    out.ty0 = rect[2];
+    out.ty1 = rect[3];
+    return true;
+}
+
+std::vector<SignBits> tile_sign_patterns(const Camera& cam, int tx, int ty) {
+    const svr_camera c = to_c(cam);
+    const int ntx = (cam.width + kTileSize - 1) / kTileSize;
+    const int nty = (cam.height + kTileSize - 1) / kTileSize;
+    std::vector<uint8_t> masks(size_t(ntx) * nty);
+    check(svr_tile_sign_masks(ctx(), &c, masks.data(), masks.size()));
+    std::vector<SignBits> out;
+    const uint8_t m = masks.at(size_t(ty) * ntx + tx);
+    for (SignBits s = 0; s < 8; ++s)
+        if (m >> s & 1) out.push_back(s);
+    return out;
+}
+
+std::vector<SortEntry> build_sort_entries(const std::vector<PreVoxel>& pre, const Camera& cam,
+                                          const SparseScene& scene) {
+    const svr_camera c = to_c(cam);
+    std::vector<uint32_t> vids(pre.size());
+    std::vector<uint64_t> codes(pre.size());
+    std::vector<int32_t> rects(4 * pre.size());
+    for (size_t i = 0; i < pre.size(); ++i) {
+        vids[i] = pre[i].vid;
+        codes[i] = scene.voxels.at(pre[i].vid).code;
+        rects[4 * i + 0] = pre[i].tx0;
+        rects[4 * i + 1] = pre[i].tx1;
+        rects[4 * i + 2] = pre[i].ty0;
+        rects[4 * i + 3] = pre[i].ty1;
+    }
+    uint64_t n = 0;
+    check(svr_build_sort_entries(ctx(), &c, scene.voxel_count(), pre.size(), vids.data(),
+                                 codes.data(), rects.data(), nullptr, nullptr, 0, &n));
+    std::vector<uint64_t> keys(n);
+    std::vector<uint32_t> vals(n);
+    check(svr_build_sort_entries(ctx(), &c, scene.voxel_count(), pre.size(), vids.data(),
+                                 codes.data(), rects.data(), keys.data(), vals.data(), n, &n));
+    std::vector<SortEntry> out(n);
+    for (uint64_t i = 0; i < n; ++i) out[i] = {keys[i], vals[i]};
+    return out;
+}
+
+void sort_entries(std::vector<SortEntry>& entries) {
+    std::vector<uint64_t> keys(entries.size());
+    std::vector<uint32_t> vals(entries.size());
+    for (size_t i = 0; i < entries.size(); ++i) {
+        keys[i] = entries[i].key;
+        vals[i] = entries[i].value;
+    }
+    check(svr_sort_entries(ctx(), entries.size(), keys.data(), vals.data()));
+    for (size_t i = 0; i < entries.size(); ++i) entries[i] = {keys[i], vals[i]};
+}
+
+RenderOutput render_with_pools(const SparseScene& scene, const PoolsD& pools, const Camera& cam,
+                               const RenderOptions& opts) {
+    auto gpu = std::make_shared<GpuRecords>();
+    gpu->scene = upload(scene, pools);
+    check(svr_frame_create(ctx(), &gpu->frame));
+    const svr_camera c = to_c(cam);
+    const svr_render_options o = to_c(opts);
+    check(svr_render(ctx(), gpu->scene->s, &c, &o, gpu->frame));
+    svr_frame* f = gpu->frame;
+    const int W = cam.width, H = cam.height;
+    RenderOutput out;
+    out.color = download_image(f, SVR_BUF_COLOR, W, H, 3);
+    out.depth = download_image(f, SVR_BUF_DEPTH, W, H, 1, opts.far_sentinel, true);
+    out.median_depth = download_image(f, SVR_BUF_MEDIAN_DEPTH, W, H, 1, opts.far_sentinel, true);
+    out.normal = download_image(f, SVR_BUF_NORMAL, W, H, 3);
+    out.transmittance = download_image(f, SVR_BUF_TRANSMITTANCE, W, H, 1);
+    if (opts.record_stats) {
+        std::vector<float> mb(scene.voxel_count());
+        check(svr_frame_download(f, SVR_BUF_MAX_BLEND, mb.data(), mb.size() * sizeof(float)));
+        out.max_blend_weight.assign(mb.begin(), mb.end());
+    }
+    if (opts.training) {
+        svr_frame_info info;
+        check(svr_frame_get_info(f, &info));
+        const Camera ss_cam = scaled_camera(cam, opts);
+        const int sw = ss_cam.width, sh = ss_cam.height;
+        auto* rec = new ForwardRecords;
+        rec->ss_cam = ss_cam;
+        rec->opts = opts;
+        std::vector<svr_pre_voxel> pre(info.n_visible);
+        check(svr_frame_pre(f, pre.data(), pre.size()));
+        rec->pre.resize(pre.size());
+        for (size_t i = 0; i < pre.size(); ++i) {
+            const svr_pre_voxel& p = pre[i];
+            PreVoxel& q = rec->pre[i];
+            q.vid = p.vid;
+            q.center = {p.center[0], p.center[1], p.center[2]};
+            q.size = p.size;
+            for (int k = 0; k < 8; ++k) q.V[k] = p.V[k];
+            q.color = {p.color[0], p.color[1], p.color[2]};
+            q.normal.n = {p.normal[0], p.normal[1], p.normal[2]};
+            q.normal.raw = {p.raw[0], p.raw[1], p.raw[2]};
+            q.normal.degenerate = p.degenerate != 0;
+            q.x0 = p.x0, q.x1 = p.x1, q.y0 = p.y0, q.y1 = p.y1;
+            q.tx0 = p.tx0, q.tx1 = p.tx1, q.ty0 = p.ty0, q.ty1 = p.ty1;
+        }
+        std::vector<uint32_t> cpre(info.n_contribs);
+        std::vector<double> ca(info.n_contribs), cb(info.n_contribs);
+        check(svr_frame_records(f, nullptr, info.n_visible, cpre.data(), ca.data(), cb.data(),
+                                info.n_contribs));
+        rec->contribs.resize(info.n_contribs);
+        for (size_t i = 0; i < cpre.size(); ++i) rec->contribs[i] = {cpre[i], ca[i], cb[i]};
+        rec->pix_begin.resize(size_t(sw) * sh);
+        rec->pix_count.resize(size_t(sw) * sh);
+        check(svr_frame_download(f, SVR_BUF_PIX_BEGIN, rec->pix_begin.data(), rec->pix_begin.size() * 4));
+        check(svr_frame_download(f, SVR_BUF_PIX_COUNT, rec->pix_count.data(), rec->pix_count.size() * 4));
+        rec->ss_color = download_image(f, SVR_BUF_SS_COLOR, sw, sh, 3);
+        rec->ss_depth = download_image(f, SVR_BUF_SS_DEPTH, sw, sh, 1, opts.far_sentinel, true);
+        rec->ss_tfin = download_image(f, SVR_BUF_SS_TFIN, sw, sh, 1);
+        {
+            std::lock_guard<std::mutex> lk(g_mu);
+            g_records[rec] = gpu;
+        }
+        out.records = std::shared_ptr<ForwardRecords>(rec, [](ForwardRecords* r) {
+            {
+                std::lock_guard<std::mutex> lk(g_mu);
+                g_records.erase(r);
+            }
+            delete r;
+        });
+    }
+    return out;
+}
+
+RenderOutput render(const SparseScene& scene, const Camera& cam, const RenderOptions& opts) {
+    return render_with_pools(scene, make_pools(scene), cam, opts);
+}
+
+SceneGradients render_backward(const SparseScene& scene, const PoolsD& pools,
+                               const ForwardRecords& records, const UpstreamGrads& grads) {
+    (void)pools;  // the frame was rendered from these pools
+    std::shared_ptr<GpuRecords> gpu;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto it = g_records.find(&records);
+        if (it != g_records.end()) gpu = it->second;
+    }
+    if (!gpu)
+        throw std::runtime_error("ForwardRecords were not produced by this renderer's render_with_pools");
+    // raster.cpp:327-332
+    if (!grads.d_weight.empty() && grads.d_weight.size() != records.contribs.size())
+        throw std::runtime_error("per-contribution weight gradients do not match the records");
+    if (!grads.d_voxel_color.empty() && grads.d_voxel_color.size() != records.contribs.size())
+        throw std::runtime_error("per-contribution color gradients do not match the records");
+    auto narrow = [](const std::vector<double>& v) { return std::vector<float>(v.begin(), v.end()); };
+    std::vector<float> dc = narrow(grads.d_color.data), dd = narrow(grads.d_depth.data),
+                       dn = narrow(grads.d_normal.data), dt = narrow(grads.d_tfin_ss),
+                       dw = narrow(grads.d_weight), dvc;
+    dvc.reserve(3 * grads.d_voxel_color.size());
+    for (const Vec3& v : grads.d_voxel_color) {
+        dvc.push_back(float(v.x));
+        dvc.push_back(float(v.y));
+        dvc.push_back(float(v.z));
+    }
+    svr_upstream up{};
+    up.d_color = dc.empty() ? nullptr : dc.data();
+    up.d_depth = dd.empty() ? nullptr : dd.data();
+    up.d_normal = dn.empty() ? nullptr : dn.data();
+    up.d_tfin_ss = dt.empty() ? nullptr : dt.data();
+    up.d_weight = dw.empty() ? nullptr : dw.data();
+    up.d_voxel_color = dvc.empty() ? nullptr : dvc.data();
+    up.n_d_weight = grads.d_weight.size();
+    up.n_d_voxel_color = grads.d_voxel_color.size();
+    up.on_device = 0;
+    std::vector<float> gd(scene.pool_count()), gs(scene.sh.size()), gp(scene.voxel_count());
+    svr_gradients g{gd.data(), gs.data(), gp.data(), 0};
+    check(svr_render_backward(ctx(), gpu->scene->s, gpu->frame, &up, &g));
+    SceneGradients out;
+    out.density.assign(gd.begin(), gd.end());
+    out.sh.assign(gs.begin(), gs.end());
+    out.priority.assign(gp.begin(), gp.end());
+    return out;
+}
+
+RenderOutput render_oracle(const SparseScene& scene, const Camera& cam, const RenderOptions& opts) {
+    if (opts.record_stats)
+        throw std::invalid_argument("render_oracle on the GPU does not record per-voxel stats");
+    auto sh = upload(scene, make_pools(scene));
+    svr_frame* f = nullptr;
+    check(svr_frame_create(ctx(), &f));
+    std::unique_ptr<svr_frame, int (*)(svr_frame*)> guard(f, svr_frame_destroy);
+    const svr_camera c = to_c(cam);
+    const svr_render_options o = to_c(opts);
+    check(svr_render_oracle(ctx(), sh->s, &c, &o, f));
+    const int W = cam.width, H = cam.height;
+    RenderOutput out;
+    out.color = download_image(f, SVR_BUF_COLOR, W, H, 3);
+    out.depth = download_image(f, SVR_BUF_DEPTH, W, H, 1, opts.far_sentinel, true);
+    out.median_depth = download_image(f, SVR_BUF_MEDIAN_DEPTH, W, H, 1, opts.far_sentinel, true);
+    out.normal = download_image(f, SVR_BUF_NORMAL, W, H, 3);
+    out.transmittance = download_image(f, SVR_BUF_TRANSMITTANCE, W, H, 1);
+    return out;
+}
+
+}  // namespace svr

@@ -646,6 +646,14 @@ void backward_impl(svr_ctx* ctx, const svr_scene* scene, svr_frame* f, const svr
 }
 
 }  // namespace
+
+// Entry points shared with dropin_support.cu.
+uint64_t frame_visible_count(svr_frame* f) { return count_visible(f); }
+int guarded_call(void (*fn)(void*), void* arg) {
+    return guard([&] { fn(arg); });
+}
+DevCamera make_dev_camera(const svr_camera& c) { return dev_camera(c); }
+
 }  // namespace svrb
 
 using namespace svrb;
