@@ -369,6 +369,8 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     uint2* ranges = grow<uint2>(f->ranges, ntiles);
     mark(ctx, kStageRanges);
     launch_tile_ranges(skeys, E, ranges, ntiles, st);
+    uint32_t* torder = grow<uint32_t>(f->tile_order, ntiles);
+    launch_tile_order(ranges, ntiles, torder, st);
     mark(ctx, -1);
 
     // output buffers
@@ -380,6 +382,7 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     float* ot = grow<float>(f->out_tfin, npx);
     CompositeArgs ca{};
     ca.ranges = ranges;
+    ca.tile_order = torder;
     ca.vals = svals;
     ca.records = pa.records;
     ca.K = opts->K;

@@ -277,6 +277,34 @@ __global__ void tile_ranges_kernel(const uint64_t* keys, uint64_t n, uint2* rang
     if (i == n - 1 || uint32_t(keys[i + 1] >> 48) != t) ranges[t].y = uint32_t(i + 1);
 }
 
+// Longest-processing-time-first tile order for K7: tiles bucketed by
+// floor(log2(entries+1)), heaviest bucket first, so the long tiles start in
+// the first wave and the kernel tail is made of short ones.
+__global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* ranges, int ntiles,
+                                                          uint32_t* order) {
+    __shared__ uint32_t s_cnt[33];
+    if (threadIdx.x < 33) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
+        const uint2 r = ranges[t];
+        atomicAdd(&s_cnt[31 - __clz(r.y - r.x + 1)], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int b = 31; b >= 0; --b) {
+            const uint32_t c = s_cnt[b];
+            s_cnt[b] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
+        const uint2 r = ranges[t];
+        order[atomicAdd(&s_cnt[31 - __clz(r.y - r.x + 1)], 1u)] = uint32_t(t);
+    }
+}
+
 // ------------------------------------------------------------------- K7
 // One CTA per 16x16 tile, one thread per pixel; each warp owns an 8x4 pixel
 // block. Voxel records of a batch of 256 entries are staged in shared
@@ -306,7 +334,7 @@ __global__ void __launch_bounds__(256) composite_kernel(DevCamera cam, Composite
     __shared__ float4 s_rec[8][32][kRecordF4];
     __shared__ uint32_t s_vid[8][32];
 
-    const int tile = blockIdx.x;
+    const int tile = a.tile_order ? int(a.tile_order[blockIdx.x]) : int(blockIdx.x);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int px, py;
     pixel_of(cam, tile, threadIdx.x, px, py);
@@ -620,6 +648,11 @@ void launch_tile_ranges(const uint64_t* keys, uint64_t n, uint2* ranges, int nti
     if (n == 0) return;
     tile_ranges_kernel<<<blocks_for(n, 256), 256, 0, st>>>(keys, n, ranges);
     SVR_LAUNCH("tile_ranges_kernel");
+}
+
+void launch_tile_order(const uint2* ranges, int ntiles, uint32_t* order, cudaStream_t st) {
+    tile_order_kernel<<<1, 1024, 0, st>>>(ranges, ntiles, order);
+    SVR_LAUNCH("tile_order_kernel");
 }
 
 void launch_composite(const DevCamera& cam, const CompositeArgs& a, bool record_pass,

@@ -107,7 +107,7 @@ struct svr_frame {
     bool has_records = false;
 
     svrb::DevBuf tile_masks, tile_sat, rects, aabb, records, counts, offsets, visible_rank;
-    svrb::DevBuf keys[2], vals[2], dbg_keys, dbg_vals, ranges;
+    svrb::DevBuf keys[2], vals[2], dbg_keys, dbg_vals, ranges, tile_order;
     svrb::DevBuf out_color, out_depth, out_median, out_normal, out_tfin, max_blend;
     svrb::DevBuf ss_color, ss_depth, ss_median, ss_normal, ss_tfin;
     svrb::DevBuf pix_count, pix_begin, contrib_entry, contrib_T;

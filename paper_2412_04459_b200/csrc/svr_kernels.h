@@ -69,6 +69,7 @@ void launch_tile_ranges(const uint64_t* keys, uint64_t n, uint2* ranges, int nti
 
 struct CompositeArgs {
     const uint2* ranges;
+    const uint32_t* tile_order;  // optional LPT tile schedule
     const uint32_t* vals;
     const float4* records;
     int K;
@@ -89,6 +90,7 @@ struct CompositeArgs {
 };
 void launch_composite(const DevCamera& cam, const CompositeArgs& a, bool record_pass,
                       cudaStream_t st);
+void launch_tile_order(const uint2* ranges, int ntiles, uint32_t* order, cudaStream_t st);
 
 // Area resampler (image.cpp:9-45): CSR taps per destination index.
 struct TapTable {
