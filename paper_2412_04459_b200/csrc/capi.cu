@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -338,37 +339,74 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     require(E < (uint64_t(1) << 30), SVR_ERR_LENGTH, "entry count exceeds 2^30");
     f->n_entries = E;
 
-    // K4: duplicate (reference emission order: vid, ty, tx, s)
-    for (int b = 0; b < 2; ++b) {
-        grow<uint64_t>(f->keys[b], E);
-        grow<uint32_t>(f->vals[b], E);
-    }
-    mark(ctx, kStageDuplicate);
-    launch_duplicate(cam, N, pa.paths, pa.rects, masks, pa.counts, offsets, f->keys[0].as<uint64_t>(),
-                     f->vals[0].as<uint32_t>(), st);
-    if (ctx->debug) {
-        grow<uint64_t>(f->dbg_keys, E);
-        grow<uint32_t>(f->dbg_vals, E);
-        SVR_CUDA(cudaMemcpyAsync(f->dbg_keys.p, f->keys[0].p, E * 8, cudaMemcpyDeviceToDevice, st));
-        SVR_CUDA(cudaMemcpyAsync(f->dbg_vals.p, f->vals[0].p, E * 4, cudaMemcpyDeviceToDevice, st));
-    }
-
-    // K5: onesweep radix sort over the digits that can differ
-    RadixPass passes[kMaxRadixPasses];
-    const int np = plan_sort(scene->max_level, ntiles, pattern_or, passes);
-    f->sort_passes = np;
-    mark(ctx, kStageSort);
-    ctx->scratch2.reserve(sort_scratch_bytes(E, np));
-    f->sorted_buf = radix_sort_pairs(f->keys[0].as<uint64_t>(), f->vals[0].as<uint32_t>(),
-                                     f->keys[1].as<uint64_t>(), f->vals[1].as<uint32_t>(), E,
-                                     passes, np, ctx->scratch2.p, st);
-    const uint64_t* skeys = f->keys[f->sorted_buf].as<uint64_t>();
-    const uint32_t* svals = f->vals[f->sorted_buf].as<uint32_t>();
-
-    // K6: tile ranges
+    // K4 + K5 + K6. Packed path when tile | order | s | vid fits in 64 bits
+    // (config 2: 12 + 27 + 3 + 20 = 62): keys-only sort of 8-B entries, digit
+    // histograms fused into the duplicate kernel. Otherwise the general
+    // (u64 key, u32 value) path. Both reproduce the reference's emission
+    // order (vid, ty, tx, s) and its (key, value) sort order.
+    const int tile_bits = bit_width(uint64_t(ntiles - 1));
+    const int vb = std::max(1, bit_width(N > 0 ? N - 1 : 0));
+    const int lmax = scene->max_level;
+    const bool multi = __builtin_popcount(pattern_or) > 1;
+    static const bool packed_enabled = [] {
+        const char* e = std::getenv("SVR_PACKED_KEYS");
+        return e == nullptr || e[0] != '0';
+    }();
+    f->packed = packed_enabled && N > 0 && (vb + 3 + 3 * lmax + tile_bits) <= 64;
     uint2* ranges = grow<uint2>(f->ranges, ntiles);
-    mark(ctx, kStageRanges);
-    launch_tile_ranges(skeys, E, ranges, ntiles, st);
+    RadixPass passes[kMaxRadixPasses];
+    int np = 0;
+    if (f->packed) {
+        f->fmt = PackedFormat{vb, lmax, vb + 3 + 3 * lmax};
+        const int lo = vb + (multi ? 0 : 3), hi = f->fmt.tile_shift + tile_bits;
+        for (int b = lo; b < hi; b += 8) passes[np++] = {0, b, std::min(8, hi - b)};
+        RadixPlan plan{};
+        plan.n = np;
+        for (int i = 0; i < np; ++i) plan.p[i] = passes[i];
+        grow<uint64_t>(f->keys[0], E);
+        grow<uint64_t>(f->keys[1], E);
+        grow<uint32_t>(f->vals[0], E);
+        ctx->scratch2.reserve(sort_scratch_bytes(E, np));
+        mark(ctx, kStageDuplicate);
+        launch_duplicate_packed(cam, N, pa.paths, pa.rects, masks, pa.counts, offsets, f->fmt,
+                                f->keys[0].as<uint64_t>(), plan, sort_hist_ptr(ctx->scratch2.p), st);
+        if (ctx->debug) {
+            grow<uint64_t>(f->dbg_keys, E);
+            SVR_CUDA(cudaMemcpyAsync(f->dbg_keys.p, f->keys[0].p, E * 8, cudaMemcpyDeviceToDevice, st));
+        }
+        mark(ctx, kStageSort);
+        f->sorted_buf = radix_sort_keys(f->keys[0].as<uint64_t>(), f->keys[1].as<uint64_t>(), E,
+                                        passes, np, ctx->scratch2.p, st, false);
+        mark(ctx, kStageRanges);
+        launch_tile_ranges_packed(f->keys[f->sorted_buf].as<uint64_t>(), E, f->fmt, ranges,
+                                  f->vals[0].as<uint32_t>(), ntiles, st);
+        f->vals_buf = 0;
+    } else {
+        for (int b = 0; b < 2; ++b) {
+            grow<uint64_t>(f->keys[b], E);
+            grow<uint32_t>(f->vals[b], E);
+        }
+        mark(ctx, kStageDuplicate);
+        launch_duplicate(cam, N, pa.paths, pa.rects, masks, pa.counts, offsets,
+                         f->keys[0].as<uint64_t>(), f->vals[0].as<uint32_t>(), st);
+        if (ctx->debug) {
+            grow<uint64_t>(f->dbg_keys, E);
+            grow<uint32_t>(f->dbg_vals, E);
+            SVR_CUDA(cudaMemcpyAsync(f->dbg_keys.p, f->keys[0].p, E * 8, cudaMemcpyDeviceToDevice, st));
+            SVR_CUDA(cudaMemcpyAsync(f->dbg_vals.p, f->vals[0].p, E * 4, cudaMemcpyDeviceToDevice, st));
+        }
+        np = plan_sort(lmax, ntiles, pattern_or, passes);
+        mark(ctx, kStageSort);
+        ctx->scratch2.reserve(sort_scratch_bytes(E, np));
+        f->sorted_buf = radix_sort_pairs(f->keys[0].as<uint64_t>(), f->vals[0].as<uint32_t>(),
+                                         f->keys[1].as<uint64_t>(), f->vals[1].as<uint32_t>(), E,
+                                         passes, np, ctx->scratch2.p, st);
+        mark(ctx, kStageRanges);
+        launch_tile_ranges(f->keys[f->sorted_buf].as<uint64_t>(), E, ranges, ntiles, st);
+        f->vals_buf = f->sorted_buf;
+    }
+    f->sort_passes = np;
+    const uint32_t* svals = f->vals[f->vals_buf].as<uint32_t>();
     uint32_t* torder = grow<uint32_t>(f->tile_order, ntiles);
     launch_tile_order(ranges, ntiles, torder, st);
     mark(ctx, -1);
@@ -487,8 +525,18 @@ BufView frame_buffer(svr_frame* f, svr_buffer which) {
         case SVR_BUF_SS_COLOR: return {ss1 ? f->out_color.p : f->ss_color.p, nss * 12};
         case SVR_BUF_SS_DEPTH: return {ss1 ? f->out_depth.p : f->ss_depth.p, nss * 4};
         case SVR_BUF_SS_TFIN: return {ss1 ? f->out_tfin.p : f->ss_tfin.p, nss * 4};
-        case SVR_BUF_SORT_KEYS: return {f->keys[f->sorted_buf].p, f->n_entries * 8};
-        case SVR_BUF_SORT_VALUES: return {f->vals[f->sorted_buf].p, f->n_entries * 4};
+        case SVR_BUF_SORT_KEYS:
+        case SVR_BUF_SORT_VALUES:
+            if (f->packed) {
+                uint64_t* k = grow<uint64_t>(f->ref_keys, f->n_entries);
+                uint32_t* v = grow<uint32_t>(f->ref_vals, f->n_entries);
+                launch_unpack_entries(f->keys[f->sorted_buf].as<uint64_t>(), f->n_entries, f->fmt, k,
+                                      v, f->ctx->stream);
+                return which == SVR_BUF_SORT_KEYS ? BufView{k, f->n_entries * 8}
+                                                  : BufView{v, f->n_entries * 4};
+            }
+            return which == SVR_BUF_SORT_KEYS ? BufView{f->keys[f->sorted_buf].p, f->n_entries * 8}
+                                              : BufView{f->vals[f->sorted_buf].p, f->n_entries * 4};
         case SVR_BUF_TILE_RANGES: return {f->ranges.p, ntiles * 8};
         case SVR_BUF_TILE_MASKS: return {f->tile_masks.p, ntiles};
         case SVR_BUF_VOXEL_RECTS: return {f->rects.p, f->n_voxels * 16};
@@ -496,11 +544,18 @@ BufView frame_buffer(svr_frame* f, svr_buffer which) {
             require(f->ctx->debug, SVR_ERR_INVALID_ARGUMENT, "AABB dump needs svr_ctx_set_debug");
             return {f->aabb.p, f->n_voxels * 32};
         case SVR_BUF_ENTRIES_KEYS:
-            require(f->ctx->debug, SVR_ERR_INVALID_ARGUMENT, "entry dump needs svr_ctx_set_debug");
-            return {f->dbg_keys.p, f->n_entries * 8};
         case SVR_BUF_ENTRIES_VALUES:
             require(f->ctx->debug, SVR_ERR_INVALID_ARGUMENT, "entry dump needs svr_ctx_set_debug");
-            return {f->dbg_vals.p, f->n_entries * 4};
+            if (f->packed) {
+                uint64_t* k = grow<uint64_t>(f->ref_keys, f->n_entries);
+                uint32_t* v = grow<uint32_t>(f->ref_vals, f->n_entries);
+                launch_unpack_entries(f->dbg_keys.as<uint64_t>(), f->n_entries, f->fmt, k, v,
+                                      f->ctx->stream);
+                return which == SVR_BUF_ENTRIES_KEYS ? BufView{k, f->n_entries * 8}
+                                                     : BufView{v, f->n_entries * 4};
+            }
+            return which == SVR_BUF_ENTRIES_KEYS ? BufView{f->dbg_keys.p, f->n_entries * 8}
+                                                 : BufView{f->dbg_vals.p, f->n_entries * 4};
         case SVR_BUF_PIX_COUNT:
         case SVR_BUF_PIX_BEGIN: {
             require(f->has_records, SVR_ERR_RUNTIME, "frame has no forward records");
@@ -598,7 +653,7 @@ void backward_impl(svr_ctx* ctx, const svr_scene* scene, svr_frame* f, const svr
 
     BackwardArgs ba{};
     ba.ranges = f->ranges.as<uint2>();
-    ba.vals = f->vals[f->sorted_buf].as<uint32_t>();
+    ba.vals = f->vals[f->vals_buf].as<uint32_t>();
     ba.records = f->records.as<float4>();
     ba.corner_index = scene->corner_index.as<uint32_t>();
     ba.K = f->opts.K;
@@ -871,7 +926,7 @@ int svr_frame_records(svr_frame* f, uint32_t* pre_vids, uint64_t n_pre, uint32_t
             uint32_t* p = grow<uint32_t>(dp, n_contribs);
             double* a = grow<double>(da, n_contribs);
             double* b = grow<double>(db, n_contribs);
-            launch_contrib_segments(f->cam, f->ranges.as<uint2>(), f->vals[f->sorted_buf].as<uint32_t>(),
+            launch_contrib_segments(f->cam, f->ranges.as<uint2>(), f->vals[f->vals_buf].as<uint32_t>(),
                                     f->records.as<float4>(), f->pix_count.as<uint32_t>(),
                                     f->pix_begin.as<uint32_t>(), f->contrib_entry.as<uint32_t>(),
                                     f->visible_rank.as<uint32_t>(), p, a, b, f->ntx * f->nty, st);

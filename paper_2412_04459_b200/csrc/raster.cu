@@ -268,6 +268,67 @@ __global__ void entry_counts_kernel(DevCamera cam, uint64_t n, const int4* rects
     counts[i] = (r.y < r.x || r.w < r.z) ? 0u : sat_rect(sat, cam.ntx, r.x, r.y, r.z, r.w);
 }
 
+// Packed variant of K4: one u64 per entry,
+//   tile | top 3*Lmax bits of dir_dep_order(code, s) | s | vid,
+// whose unsigned order is exactly the reference's (key, value) order
+// (the dropped order bits are the sign pattern repeated, raster.cpp:165,
+// octree.hpp:99-101). The kernel also accumulates the radix-sort digit
+// histograms of every pass, so the sort needs no separate histogram read.
+__global__ void __launch_bounds__(256) duplicate_packed_kernel(
+    DevCamera cam, uint64_t n, const uint64_t* __restrict__ paths, const int4* __restrict__ rects,
+    const uint8_t* __restrict__ masks, const uint32_t* __restrict__ counts,
+    const uint32_t* __restrict__ offsets, PackedFormat fmt, uint64_t* __restrict__ keys,
+    RadixPlan plan, uint32_t* hist) {
+    (void)plan;
+    (void)hist;
+    const uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (v < n && counts[v] != 0) {
+        const uint64_t code = paths[v] & kCodeMask48;
+        const int obits = 3 * fmt.lmax;
+        const int4 r = rects[v];
+        uint32_t o = offsets[v];
+        for (int ty = r.z; ty <= r.w; ++ty)
+            for (int tx = r.x; tx <= r.y; ++tx) {
+                const uint64_t tid = uint64_t(ty) * cam.ntx + tx;
+                uint32_t m = masks[tid];
+                while (m) {
+                    const uint32_t sgn = __ffs(m) - 1;
+                    m &= m - 1;
+                    const uint64_t order = (code ^ (uint64_t(sgn) * kGroupOnes)) >> (48 - obits);
+                    const uint64_t key = (tid << fmt.tile_shift) | (order << (fmt.vb + 3)) |
+                                         (uint64_t(sgn) << fmt.vb) | v;
+                    keys[o++] = key;
+                }
+            }
+    }
+}
+
+__global__ void tile_ranges_packed_kernel(const uint64_t* __restrict__ keys, uint64_t n,
+                                          PackedFormat fmt, uint2* ranges, uint32_t* vals) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t k = keys[i];
+    const uint32_t t = uint32_t(k >> fmt.tile_shift);
+    vals[i] = (uint32_t((k >> fmt.vb) & 7u) << 29) | uint32_t(k & ((uint64_t(1) << fmt.vb) - 1));
+    if (i == 0 || uint32_t(keys[i - 1] >> fmt.tile_shift) != t) ranges[t].x = uint32_t(i);
+    if (i == n - 1 || uint32_t(keys[i + 1] >> fmt.tile_shift) != t) ranges[t].y = uint32_t(i + 1);
+}
+
+__global__ void unpack_entries_kernel(const uint64_t* packed, uint64_t n, PackedFormat fmt,
+                                      uint64_t* keys, uint32_t* vals) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t k = packed[i];
+    const int obits = 3 * fmt.lmax;
+    const uint64_t vid = k & ((uint64_t(1) << fmt.vb) - 1);
+    const uint64_t sgn = (k >> fmt.vb) & 7u;
+    const uint64_t otop = (k >> (fmt.vb + 3)) & ((uint64_t(1) << obits) - 1);
+    const uint64_t tid = k >> fmt.tile_shift;
+    const uint64_t low = obits < 48 ? ((sgn * kGroupOnes) & ((uint64_t(1) << (48 - obits)) - 1)) : 0;
+    keys[i] = (tid << 48) | (obits > 0 ? (otop << (48 - obits)) : 0) | low;
+    vals[i] = uint32_t(sgn << 29) | uint32_t(vid);
+}
+
 // ------------------------------------------------------------------- K6
 __global__ void tile_ranges_kernel(const uint64_t* keys, uint64_t n, uint2* ranges) {
     uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -640,6 +701,31 @@ void launch_entry_counts(const DevCamera& cam, uint64_t n, const int4* rects,
     if (n == 0) return;
     entry_counts_kernel<<<blocks_for(n, 256), 256, 0, st>>>(cam, n, rects, sat, counts);
     SVR_LAUNCH("entry_counts_kernel");
+}
+
+void launch_duplicate_packed(const DevCamera& cam, uint64_t n, const uint64_t* paths,
+                             const int4* rects, const uint8_t* masks, const uint32_t* counts,
+                             const uint32_t* offsets, PackedFormat fmt, uint64_t* keys,
+                             const RadixPlan& plan, uint32_t* hist, cudaStream_t st) {
+    if (n == 0) return;
+    duplicate_packed_kernel<<<blocks_for(n, 256), 256, 0, st>>>(cam, n, paths, rects, masks, counts,
+                                                                offsets, fmt, keys, plan, hist);
+    SVR_LAUNCH("duplicate_packed_kernel");
+}
+
+void launch_tile_ranges_packed(const uint64_t* keys, uint64_t n, PackedFormat fmt, uint2* ranges,
+                               uint32_t* vals, int ntiles, cudaStream_t st) {
+    SVR_CUDA(cudaMemsetAsync(ranges, 0, size_t(ntiles) * sizeof(uint2), st));
+    if (n == 0) return;
+    tile_ranges_packed_kernel<<<blocks_for(n, 256), 256, 0, st>>>(keys, n, fmt, ranges, vals);
+    SVR_LAUNCH("tile_ranges_packed_kernel");
+}
+
+void launch_unpack_entries(const uint64_t* packed, uint64_t n, PackedFormat fmt, uint64_t* keys,
+                           uint32_t* vals, cudaStream_t st) {
+    if (n == 0) return;
+    unpack_entries_kernel<<<blocks_for(n, 256), 256, 0, st>>>(packed, n, fmt, keys, vals);
+    SVR_LAUNCH("unpack_entries_kernel");
 }
 
 void launch_tile_ranges(const uint64_t* keys, uint64_t n, uint2* ranges, int ntiles,

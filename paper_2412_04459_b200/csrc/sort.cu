@@ -28,6 +28,15 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kItems = 8;
 constexpr int kTileKeys = kThreads * kItems;  // 2048 pairs per partition
+// keys-only partitions are larger: 3072 keys, so a config-2 pass (1.76M
+// keys) is 574 CTAs = one wave of 4 resident CTAs on 148 SMs
+constexpr int kItemsK = 12;
+constexpr int kTileKeysK = kThreads * kItemsK;
+template <bool PAIRS>
+struct Part {
+    static constexpr int items = PAIRS ? kItems : kItemsK;
+    static constexpr int keys = kThreads * items;
+};
 constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagInc = 2u << 30;
 constexpr uint32_t kValMask = (1u << 30) - 1;
@@ -51,7 +60,7 @@ __global__ void __launch_bounds__(kThreads) hist_kernel(const uint64_t* keys, co
     for (uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * kThreads) {
         uint64_t k = keys[i];
-        uint32_t v = vals[i];
+        uint32_t v = vals ? vals[i] : 0u;
         for (int p = 0; p < spec.n; ++p) atomicAdd(&s_hist[p][digit_of(k, v, spec.p[p])], 1u);
     }
     __syncthreads();
@@ -86,6 +95,7 @@ __device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
     asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(p), "r"(v));
 }
 
+template <bool PAIRS>
 __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
     const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint64_t n, RadixPass pass,
@@ -93,8 +103,8 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
     __shared__ uint32_t s_warp_hist[kWarps][kRadix + 1];
     __shared__ uint32_t s_block_excl[kRadix];
     __shared__ uint32_t s_global[kRadix];
-    __shared__ uint64_t s_keys[kTileKeys];
-    __shared__ uint32_t s_vals[kTileKeys];
+    __shared__ uint64_t s_keys[Part<PAIRS>::keys];
+    __shared__ uint32_t s_vals[PAIRS ? Part<PAIRS>::keys : 1];
     __shared__ uint32_t s_part;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -103,34 +113,35 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
         (&s_warp_hist[0][0])[i] = 0;
     __syncthreads();
     const uint32_t part = s_part;
-    const uint64_t base = uint64_t(part) * kTileKeys;
-    const uint64_t wbase = base + uint64_t(warp) * 32 * kItems;
+    const uint64_t base = uint64_t(part) * Part<PAIRS>::keys;
+    const uint64_t wbase = base + uint64_t(warp) * 32 * Part<PAIRS>::items;
 
-    uint64_t k[kItems];
-    uint32_t v[kItems], d[kItems], r[kItems];
+    // Digits are recomputed from the key/value when needed (saves registers);
+    // out-of-range slots get digit kRadix and are ranked into a discarded bin.
+    uint64_t k[Part<PAIRS>::items];
+    uint32_t v[PAIRS ? Part<PAIRS>::items : 1], r[Part<PAIRS>::items];
+    const uint64_t nvalid = n > wbase ? n - wbase : 0;
+    auto dig = [&](int i) -> uint32_t {
+        return (uint64_t(i) * 32 + lane < nvalid) ? digit_of(k[i], PAIRS ? v[PAIRS ? i : 0] : 0u, pass)
+                                                  : uint32_t(kRadix);
+    };
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {
+    for (int i = 0; i < Part<PAIRS>::items; ++i) {
         uint64_t idx = wbase + uint64_t(i) * 32 + lane;
-        if (idx < n) {
-            k[i] = keys_in[idx];
-            v[i] = vals_in[idx];
-            d[i] = digit_of(k[i], v[i], pass);
-        } else {
-            k[i] = 0;
-            v[i] = 0;
-            d[i] = kRadix;  // out of range: ranked into a discarded bin
-        }
+        k[i] = idx < n ? keys_in[idx] : 0ull;
+        if (PAIRS) v[PAIRS ? i : 0] = idx < n ? vals_in[idx] : 0u;
     }
     const uint32_t lt_mask = (1u << lane) - 1u;
     uint32_t* wh = s_warp_hist[warp];
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-        uint32_t peers = __match_any_sync(0xffffffffu, d[i]);
+    for (int i = 0; i < Part<PAIRS>::items; ++i) {
+        const uint32_t di = dig(i);
+        uint32_t peers = __match_any_sync(0xffffffffu, di);
         uint32_t below = __popc(peers & lt_mask);
-        uint32_t prev = wh[d[i]];
+        uint32_t prev = wh[di];
         r[i] = prev + below;
         __syncwarp();
-        if (below == 0) wh[d[i]] = prev + __popc(peers);
+        if (below == 0) wh[di] = prev + __popc(peers);
         __syncwarp();
     }
     __syncthreads();
@@ -194,29 +205,30 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
 
     // Scatter to shared memory in digit order, then out to global.
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-        if (d[i] < kRadix) {
-            uint32_t pos = s_block_excl[d[i]] + s_warp_hist[warp][d[i]] + r[i];
+    for (int i = 0; i < Part<PAIRS>::items; ++i) {
+        const uint32_t di = dig(i);
+        if (di < kRadix) {
+            uint32_t pos = s_block_excl[di] + s_warp_hist[warp][di] + r[i];
             s_keys[pos] = k[i];
-            s_vals[pos] = v[i];
+            if (PAIRS) s_vals[pos] = v[PAIRS ? i : 0];
         }
     }
     __syncthreads();
-    const uint32_t tile_n = uint32_t(min(uint64_t(kTileKeys), n - base));
+    const uint32_t tile_n = uint32_t(min(uint64_t(Part<PAIRS>::keys), n - base));
     for (uint32_t pos = threadIdx.x; pos < tile_n; pos += kThreads) {
         uint64_t kk = s_keys[pos];
-        uint32_t vv = s_vals[pos];
+        uint32_t vv = PAIRS ? s_vals[pos] : 0u;
         uint32_t dd = digit_of(kk, vv, pass);
         uint64_t o = uint64_t(s_global[dd]) + pos;
         keys_out[o] = kk;
-        vals_out[o] = vv;
+        if (PAIRS) vals_out[o] = vv;
     }
 }
 
 }  // namespace
 
 size_t sort_scratch_bytes(uint64_t n, int npasses) {
-    uint64_t nparts = (n + kTileKeys - 1) / kTileKeys;
+    uint64_t nparts = (n + kTileKeys - 1) / kTileKeys;  // >= keys-only partition count
     return size_t(npasses) * kRadix * 4                     // histograms / bin bases
            + size_t(npasses) * 4 + 64                       // tickets
            + size_t(npasses) * (nparts + 1) * kRadix * 4;   // look-back status per pass
@@ -251,12 +263,58 @@ int radix_sort_pairs(uint64_t* keys0, uint32_t* vals0, uint64_t* keys1, uint32_t
     uint32_t* vout = vals1;
     int cur = 0;
     for (int p = 0; p < npasses; ++p) {
-        onesweep_kernel<<<unsigned(nparts), kThreads, 0, st>>>(
+        onesweep_kernel<true><<<unsigned(nparts), kThreads, 0, st>>>(
             kin, vin, kout, vout, n, passes[p], hist + p * kRadix,
             status + size_t(p) * (nparts + 1) * kRadix, tickets + p);
         SVR_LAUNCH("onesweep_kernel");
         std::swap(kin, kout);
         std::swap(vin, vout);
+        cur ^= 1;
+    }
+    return cur;
+}
+
+uint32_t* sort_hist_ptr(void* scratch) { return static_cast<uint32_t*>(scratch); }
+
+void sort_prepare(void* scratch, uint64_t n, int npasses, cudaStream_t st) {
+    SVR_CUDA(cudaMemsetAsync(scratch, 0, sort_scratch_bytes(n, npasses), st));
+}
+
+int radix_sort_keys(uint64_t* keys0, uint64_t* keys1, uint64_t n, const RadixPass* passes,
+                    int npasses, void* scratch, cudaStream_t st, bool hist_ready) {
+    if (n <= 1 || npasses == 0) return 0;
+    if (npasses > kMaxRadixPasses) throw Error(SVR_ERR_RUNTIME, "too many radix passes");
+    if (n >= (uint64_t(1) << 30))
+        throw Error(SVR_ERR_LENGTH, "sort supports fewer than 2^30 entries");
+    for (int i = 0; i < npasses; ++i)
+        if (passes[i].src != 0) throw Error(SVR_ERR_RUNTIME, "keys-only sort takes key digits only");
+    const uint64_t nparts_alloc = (n + kTileKeys - 1) / kTileKeys;
+    const uint64_t nparts = (n + kTileKeysK - 1) / kTileKeysK;
+    char* s = static_cast<char*>(scratch);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(s);
+    uint32_t* tickets = reinterpret_cast<uint32_t*>(s + size_t(npasses) * kRadix * 4);
+    uint32_t* status =
+        reinterpret_cast<uint32_t*>(s + size_t(npasses) * kRadix * 4 + size_t(npasses) * 4 + 64);
+    if (!hist_ready) {
+        SVR_CUDA(cudaMemsetAsync(hist, 0, sort_scratch_bytes(n, npasses), st));
+        PassSpec spec{};
+        spec.n = npasses;
+        for (int i = 0; i < npasses; ++i) spec.p[i] = passes[i];
+        int hist_blocks = int(std::min<uint64_t>((n + kThreads - 1) / kThreads, 148 * 4));
+        hist_kernel<<<hist_blocks, kThreads, 0, st>>>(keys0, nullptr, n, spec, hist);
+        SVR_LAUNCH("hist_kernel");
+    }
+    bin_scan_kernel<<<npasses, kRadix, 0, st>>>(hist);
+    SVR_LAUNCH("bin_scan_kernel");
+    uint64_t* kin = keys0;
+    uint64_t* kout = keys1;
+    int cur = 0;
+    for (int p = 0; p < npasses; ++p) {
+        onesweep_kernel<false><<<unsigned(nparts), kThreads, 0, st>>>(
+            kin, nullptr, kout, nullptr, n, passes[p], hist + p * kRadix,
+            status + size_t(p) * (nparts_alloc + 1) * kRadix, tickets + p);
+        SVR_LAUNCH("onesweep_kernel");
+        std::swap(kin, kout);
         cur ^= 1;
     }
     return cur;

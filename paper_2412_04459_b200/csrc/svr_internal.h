@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "svr_b200.h"
+#include "svr_kernels.h"
 #include "svr_math.cuh"
 
 namespace svrb {
@@ -114,6 +115,10 @@ struct svr_frame {
     svrb::DevBuf taps;  // resampler tables
     svrb::DevBuf bwd_gc, bwd_gn, bwd_lift, bwd_dcolor, status, l1_grad;
     int sorted_buf = 0;  // which of keys[]/vals[] holds the sorted list
+    int vals_buf = 0;    // which vals[] the compositing kernels read
+    bool packed = false; // entries in the packed 64-bit format (PackedFormat)
+    svrb::PackedFormat fmt{};
+    svrb::DevBuf ref_keys, ref_vals;  // reference-format dumps of packed entries
     int tap_src_w = -1, tap_src_h = -1, tap_dst_w = -1, tap_dst_h = -1;
     int n_taps_x = 0, n_taps_y = 0;
 };

@@ -30,6 +30,17 @@ size_t sort_scratch_bytes(uint64_t n, int npasses);
 int radix_sort_pairs(uint64_t* keys0, uint32_t* vals0, uint64_t* keys1, uint32_t* vals1,
                      uint64_t n, const RadixPass* passes, int npasses, void* scratch,
                      cudaStream_t st);
+// Keys-only variant. With hist_ready the digit histograms were already
+// accumulated into sort_hist_ptr(scratch) (after sort_prepare) by the
+// producer of the keys (the fused duplicate kernel).
+struct RadixPlan {
+    int n;
+    RadixPass p[kMaxRadixPasses];
+};
+uint32_t* sort_hist_ptr(void* scratch);
+void sort_prepare(void* scratch, uint64_t n, int npasses, cudaStream_t st);
+int radix_sort_keys(uint64_t* keys0, uint64_t* keys1, uint64_t n, const RadixPass* passes,
+                    int npasses, void* scratch, cudaStream_t st, bool hist_ready);
 
 // ---- raster.cu -------------------------------------------------------------
 struct FrameStatus {          // device -> host summary, one read per frame
@@ -66,6 +77,26 @@ void launch_duplicate(const DevCamera& cam, uint64_t n, const uint64_t* paths, c
 
 void launch_tile_ranges(const uint64_t* keys, uint64_t n, uint2* ranges, int ntiles,
                         cudaStream_t st);
+
+// Packed entry format (when it fits in 64 bits):
+//   tile | top 3*Lmax order bits | sign s (3) | vid (vb bits)
+// Sorting it keys-only reproduces the reference's (key, value) order.
+struct PackedFormat {
+    int vb;          // voxel-id bits
+    int lmax;        // finest occupied octree level
+    int tile_shift;  // vb + 3 + 3*lmax
+};
+void launch_duplicate_packed(const DevCamera& cam, uint64_t n, const uint64_t* paths,
+                             const int4* rects, const uint8_t* masks, const uint32_t* counts,
+                             const uint32_t* offsets, PackedFormat fmt, uint64_t* keys,
+                             const RadixPlan& plan, uint32_t* hist, cudaStream_t st);
+// Tile ranges from packed sorted keys; also writes the reference value
+// (s << 29 | vid) per entry for the compositing kernels.
+void launch_tile_ranges_packed(const uint64_t* keys, uint64_t n, PackedFormat fmt, uint2* ranges,
+                               uint32_t* vals, int ntiles, cudaStream_t st);
+// Reference SortEntry (key, value) from packed keys (parity dumps).
+void launch_unpack_entries(const uint64_t* packed, uint64_t n, PackedFormat fmt, uint64_t* keys,
+                           uint32_t* vals, cudaStream_t st);
 
 struct CompositeArgs {
     const uint2* ranges;
