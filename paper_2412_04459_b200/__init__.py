@@ -18,7 +18,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsvr_b200.so")
+LIB_PATH = os.environ.get("SVR_LIB", os.path.join(_HERE, "libsvr_b200.so"))
 
 TILE_SIZE = 16
 TILE_ID_BITS = 16

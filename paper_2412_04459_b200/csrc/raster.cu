@@ -100,18 +100,29 @@ __device__ __forceinline__ uint32_t sat_rect(const uint32_t* sat, int ntx, int t
 // 112-B records of the whole CTA are staged in shared memory and written
 // back as one contiguous, coalesced block.
 constexpr int kPreThreads = 128;
+#ifndef SVR_PRE_SMEM_SH
+#define SVR_PRE_SMEM_SH 0
+#endif
+#ifndef SVR_PRE_MINB
+#define SVR_PRE_MINB 6
+#endif
 
-__global__ void __launch_bounds__(kPreThreads, 8) preprocess_kernel(DevCamera cam, PreprocessArgs a) {
+__global__ void __launch_bounds__(kPreThreads, SVR_PRE_MINB) preprocess_kernel(DevCamera cam, PreprocessArgs a) {
     extern __shared__ float4 smem4[];
+#if SVR_PRE_SMEM_SH
     float* smem = reinterpret_cast<float*>(smem4);
     const int pad = a.sh_stride | 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     float* s_sh = smem + warp * 32 * pad;
     float4* s_rec = smem4 + ((kPreThreads * pad + 3) / 4);
+#else
+    float4* s_rec = smem4;
+#endif
     const uint64_t v0 = uint64_t(blockIdx.x) * kPreThreads;
     const uint64_t v = v0 + threadIdx.x;
     const bool valid = v < a.n;
 
+#if SVR_PRE_SMEM_SH
     // 1. coalesced SH staging for this warp's voxels
     const uint64_t wv0 = v0 + uint64_t(warp) * 32;
     const int nvw = wv0 < a.n ? int(min(uint64_t(32), a.n - wv0)) : 0;
@@ -136,6 +147,7 @@ __global__ void __launch_bounds__(kPreThreads, 8) preprocess_kernel(DevCamera ca
         }
     }
     __syncwarp();
+#endif
 
     float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0, r3 = r0, r4 = r0, r5 = r0, r6 = r0;
     if (valid) {
@@ -180,8 +192,9 @@ __global__ void __launch_bounds__(kPreThreads, 8) preprocess_kernel(DevCamera ca
             }
             float b[16];
             const int nb = sh_basis(a.sh_degree, ux, uy, uz, b);
-            const float* co = s_sh + lane * pad;
             float cr = 0.f, cg = 0.f, cb = 0.f;
+#if SVR_PRE_SMEM_SH
+            const float* co = s_sh + lane * pad;
 #pragma unroll
             for (int m = 0; m < 16; ++m) {
                 if (m < nb) {
@@ -190,6 +203,32 @@ __global__ void __launch_bounds__(kPreThreads, 8) preprocess_kernel(DevCamera ca
                     cb += b[m] * co[3 * m + 2];
                 }
             }
+#else
+            const float* co = a.sh + v * uint64_t(a.sh_stride);
+            if (a.sh_stride == 48) {
+                // degree 3: 12 aligned 16-B loads of this voxel's 192 B
+                const float4* c4 = reinterpret_cast<const float4*>(co);
+#pragma unroll
+                for (int q = 0; q < 12; ++q) {
+                    const float4 t = __ldg(c4 + q);
+                    const float e4[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int e = 4 * q + j, m = e / 3, ch = e - 3 * (e / 3);
+                        const float c = b[m] * e4[j];
+                        if (ch == 0) cr += c;
+                        else if (ch == 1) cg += c;
+                        else cb += c;
+                    }
+                }
+            } else {
+                for (int m = 0; m < nb; ++m) {
+                    cr += b[m] * __ldg(co + 3 * m + 0);
+                    cg += b[m] * __ldg(co + 3 * m + 1);
+                    cb += b[m] * __ldg(co + 3 * m + 2);
+                }
+            }
+#endif
             r5 = make_float4(fmaxf(0.f, cr), fmaxf(0.f, cg), fmaxf(0.f, cb), 0.f);
             float n[3];
             voxel_normal(V, n);
@@ -671,8 +710,12 @@ void launch_tile_masks_only(const DevCamera& cam, uint8_t* masks, cudaStream_t s
 
 void launch_preprocess(const DevCamera& cam, const PreprocessArgs& a, cudaStream_t st) {
     if (a.n == 0) return;
+#if SVR_PRE_SMEM_SH
     const int pad = a.sh_stride | 1;
     const size_t smem = size_t((kPreThreads * pad + 3) / 4) * 16 + size_t(kPreThreads) * kRecordF4 * 16;
+#else
+    const size_t smem = size_t(kPreThreads) * kRecordF4 * 16;
+#endif
     preprocess_kernel<<<blocks_for(a.n, kPreThreads), kPreThreads, smem, st>>>(cam, a);
     SVR_LAUNCH("preprocess_kernel");
 }
