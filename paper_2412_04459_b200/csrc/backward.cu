@@ -127,18 +127,19 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
 #pragma unroll
             for (int q = 0; q < kAcc; ++q) acc[q] = 0.f;
             if (hit) {
-                const float4 lo = s_rec[0][j], hi = s_rec[1][j];
-                float t0 = lo.x * ix, t1 = hi.x * ix;
+                const float4 lo = s_rec[0][j];
+                const float inv = s_rec[5][j].w;
+                float t0 = lo.x * ix, t1 = (lo.x + lo.w) * ix;
                 float ta = fminf(t0, t1), tb = fmaxf(t0, t1);
                 t0 = lo.y * iy;
-                t1 = hi.y * iy;
+                t1 = (lo.y + lo.w) * iy;
                 ta = fmaxf(ta, fminf(t0, t1));
                 tb = fminf(tb, fmaxf(t0, t1));
                 t0 = lo.z * iz;
-                t1 = hi.z * iz;
+                t1 = (lo.z + lo.w) * iz;
                 ta = fmaxf(ta, fminf(t0, t1));
                 tb = fminf(tb, fmaxf(t0, t1));
-                const float4 va = s_rec[3][j], vb = s_rec[4][j];
+                const float4 va = s_rec[2][j], vb = s_rec[3][j];
                 const float V[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
                 const float seg = tb - ta;
                 const float lk = seg * dnorm * (1.0f / K);
@@ -147,9 +148,9 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     tk[k] = ta + ((k + 0.5f) / K) * seg;
-                    qk[k][0] = (tk[k] * dx - lo.x) * lo.w;
-                    qk[k][1] = (tk[k] * dy - lo.y) * lo.w;
-                    qk[k][2] = (tk[k] * dz - lo.z) * lo.w;
+                    qk[k][0] = (tk[k] * dx - lo.x) * inv;
+                    qk[k][1] = (tk[k] * dy - lo.y) * inv;
+                    qk[k][2] = (tk[k] * dz - lo.z) * inv;
                     vk[k] = trilinear(V, qk[k][0], qk[k][1], qk[k][2]);
                     const float act = explin(vk[k]);
                     sum += act;
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
                     Tk *= 1.0f - sa[k];
                 }
                 const float Ti = a.contrib_T[base + kidx];
-                const float4 col = s_rec[5][j], nor = s_rec[6][j];
+                const float4 col = s_rec[4][j], nor = s_rec[5][j];
                 const float gw = a.d_weight ? a.d_weight[base + kidx] : 0.f;
                 const float phi = gC[0] * col.x + gC[1] * col.y + gC[2] * col.z + gN[0] * nor.x +
                                   gN[1] * nor.y + gN[2] * nor.z + gw;
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
         // one set of global atomics per touched entry of this batch
         if (threadIdx.x < nb && s_touch[threadIdx.x]) {
             const int j = threadIdx.x;
-            const uint32_t vid = __float_as_uint(s_rec[1][j].w);
+            const uint32_t vid = __float_as_uint(s_rec[4][j].w);
             const uint4* ci4 = reinterpret_cast<const uint4*>(a.corner_index + 8ull * vid);
             const uint4 c0 = ci4[0], c1 = ci4[1];
             const uint32_t ci[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
@@ -296,7 +297,7 @@ __global__ void __launch_bounds__(256) voxel_epilogue_kernel(DevCamera cam, Epil
         }
     }
     const float4* rec = a.records + v * kRecordF4;
-    const float4 va = rec[3], vb = rec[4];
+    const float4 va = rec[2], vb = rec[3];
     const float V[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
     const float dn[3] = {a.g_normal[3 * v], a.g_normal[3 * v + 1], a.g_normal[3 * v + 2]};
     if (dn[0] == 0.f && dn[1] == 0.f && dn[2] == 0.f) return;

@@ -40,7 +40,7 @@ __global__ void frame_pre_kernel(DevCamera cam, uint64_t n, const uint64_t* path
     p.size = size;
     for (int c = 0; c < 8; ++c) p.V[c] = density[corner_index[8 * v + c]];
     const float4* rec = records + v * kRecordF4;
-    p.color[0] = rec[5].x, p.color[1] = rec[5].y, p.color[2] = rec[5].z;
+    p.color[0] = rec[4].x, p.color[1] = rec[4].y, p.color[2] = rec[4].z;
     // density_gradient in double from the exact corner values (field.hpp:132-154)
     double g[3] = {0, 0, 0};
     for (int c = 0; c < 8; ++c) {

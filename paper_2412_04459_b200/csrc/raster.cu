@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(kPreThreads, SVR_PRE_MINB) preprocess_kernel(D
     __syncwarp();
 #endif
 
-    float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0, r3 = r0, r4 = r0, r5 = r0, r6 = r0;
+    float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0, r3 = r0, r4 = r0, r5 = r0;
     if (valid) {
         const uint64_t path = a.paths[v];
         double center[3], size;
@@ -165,21 +165,17 @@ __global__ void __launch_bounds__(kPreThreads, SVR_PRE_MINB) preprocess_kernel(D
             r0.x = float(dsub(dsub(center[0], h), cam.pos[0]));
             r0.y = float(dsub(dsub(center[1], h), cam.pos[1]));
             r0.z = float(dsub(dsub(center[2], h), cam.pos[2]));
-            r0.w = float(1.0 / size);
-            r1.x = float(dsub(dadd(center[0], h), cam.pos[0]));
-            r1.y = float(dsub(dadd(center[1], h), cam.pos[1]));
-            r1.z = float(dsub(dadd(center[2], h), cam.pos[2]));
-            r1.w = __uint_as_float(uint32_t(v));
+            r0.w = float(size);
             // Screen AABB, rounded outward so the fp32 test is a superset.
-            r2 = make_float4(__double2float_rd(pr.x0), __double2float_ru(pr.x1),
+            r1 = make_float4(__double2float_rd(pr.x0), __double2float_ru(pr.x1),
                              __double2float_rd(pr.y0), __double2float_ru(pr.y1));
             const uint4* ci4 = reinterpret_cast<const uint4*>(a.corner_index + 8 * v);
             const uint4 c0 = __ldg(ci4), c1 = __ldg(ci4 + 1);
             float V[8] = {__ldg(a.density + c0.x), __ldg(a.density + c0.y), __ldg(a.density + c0.z),
                           __ldg(a.density + c0.w), __ldg(a.density + c1.x), __ldg(a.density + c1.y),
                           __ldg(a.density + c1.z), __ldg(a.density + c1.w)};
-            r3 = make_float4(V[0], V[1], V[2], V[3]);
-            r4 = make_float4(V[4], V[5], V[6], V[7]);
+            r2 = make_float4(V[0], V[1], V[2], V[3]);
+            r3 = make_float4(V[4], V[5], V[6], V[7]);
             // sh_eval(normalized(center - cam.pos)) (raster.cpp:195-196, sh.hpp:48-58)
             const double dx = dsub(center[0], cam.pos[0]), dy = dsub(center[1], cam.pos[1]),
                          dz = dsub(center[2], cam.pos[2]);
@@ -229,10 +225,10 @@ __global__ void __launch_bounds__(kPreThreads, SVR_PRE_MINB) preprocess_kernel(D
                 }
             }
 #endif
-            r5 = make_float4(fmaxf(0.f, cr), fmaxf(0.f, cg), fmaxf(0.f, cb), 0.f);
+            r4 = make_float4(fmaxf(0.f, cr), fmaxf(0.f, cg), fmaxf(0.f, cb), __uint_as_float(uint32_t(v)));
             float n[3];
             voxel_normal(V, n);
-            r6 = make_float4(n[0], n[1], n[2], 0.f);
+            r5 = make_float4(n[0], n[1], n[2], float(1.0 / size));
         }
     }
     float4* sr = s_rec + threadIdx.x * kRecordF4;
@@ -242,7 +238,6 @@ __global__ void __launch_bounds__(kPreThreads, SVR_PRE_MINB) preprocess_kernel(D
     sr[3] = r3;
     sr[4] = r4;
     sr[5] = r5;
-    sr[6] = r6;
     __syncthreads();
     const int nblk = v0 < a.n ? int(min(uint64_t(kPreThreads), a.n - v0)) : 0;
     float4* dst = a.records + v0 * kRecordF4;
@@ -448,6 +443,7 @@ __global__ void __launch_bounds__(256) composite_kernel(DevCamera cam, Composite
     pixel_ray_dir(cam, double(px), double(py), dd);
     const uint32_t my_sign = sign_bits(dd);
     const uint32_t warp_signs = __reduce_or_sync(0xffffffffu, inside ? (1u << my_sign) : 0u);
+    const bool one_sign = __popc(warp_signs) <= 1;
     const float dx = float(dd[0]), dy = float(dd[1]), dz = float(dd[2]);
     const float ix = 1.0f / dx, iy = 1.0f / dy, iz = 1.0f / dz;
     const float dnorm = float(sqrt(dd[0] * dd[0] + dd[1] * dd[1] + dd[2] * dd[2]));
@@ -472,7 +468,7 @@ __global__ void __launch_bounds__(256) composite_kernel(DevCamera cam, Composite
     float4 b0 = make_float4(0.f, -1.f, 0.f, -1.f);
     if (range.x + lane < range.y) {
         v0 = __ldg(a.vals + range.x + lane);
-        b0 = __ldg(a.records + uint64_t(v0 & kVidMask) * kRecordF4 + 2);
+        b0 = __ldg(a.records + uint64_t(v0 & kVidMask) * kRecordF4 + 1);
     }
     if (range.x + 32 + lane < range.y) v1 = __ldg(a.vals + range.x + 32 + lane);
 
@@ -480,7 +476,7 @@ __global__ void __launch_bounds__(256) composite_kernel(DevCamera cam, Composite
         if (__all_sync(0xffffffffu, done)) break;
         float4 b1 = make_float4(0.f, -1.f, 0.f, -1.f);
         uint32_t v2 = 0;
-        if (c + 32 + lane < range.y) b1 = __ldg(a.records + uint64_t(v1 & kVidMask) * kRecordF4 + 2);
+        if (c + 32 + lane < range.y) b1 = __ldg(a.records + uint64_t(v1 & kVidMask) * kRecordF4 + 1);
         if (c + 64 + lane < range.y) v2 = __ldg(a.vals + c + 64 + lane);
 
         const bool valid = c + lane < range.y;
@@ -495,79 +491,98 @@ __global__ void __launch_bounds__(256) composite_kernel(DevCamera cam, Composite
             wrec[sl][k] = __ldg(a.records + uint64_t(wvid[sl] & kVidMask) * kRecordF4 + k);
         }
         __syncwarp();
+        // Slots are evaluated two at a time, branch-free (slab + quadrature of
+        // both are independent of the pixel state, so their latencies
+        // overlap), then folded into the pixel state in entry order.
         uint32_t mm = m;
-        for (int sl = 0; sl < nrel; ++sl) {
-            const int j = __ffs(mm) - 1;  // chunk-local entry index (for the record pass)
+        for (int sl = 0; sl < nrel; sl += 2) {
+            const bool has_b = sl + 1 < nrel;
+            const int ja = __ffs(mm) - 1;  // chunk-local entry index (record pass)
             mm &= mm - 1;
-            if (done || (wvid[sl] >> 29) != my_sign) continue;
-            const float4 bb = wrec[sl][2];
-            if (pcx < bb.x || pcx > bb.y || pcy < bb.z || pcy > bb.w) continue;
-            const float4 lo = wrec[sl][0], hi = wrec[sl][1];
-            float t0 = lo.x * ix, t1 = hi.x * ix;
-            float ta = fminf(t0, t1), tb = fmaxf(t0, t1);
-            t0 = lo.y * iy;
-            t1 = hi.y * iy;
-            ta = fmaxf(ta, fminf(t0, t1));
-            tb = fminf(tb, fmaxf(t0, t1));
-            t0 = lo.z * iz;
-            t1 = hi.z * iz;
-            ta = fmaxf(ta, fminf(t0, t1));
-            tb = fminf(tb, fmaxf(t0, t1));
-            if (!(ta <= tb && ta > 0.0f)) continue;
-            // voxel_alpha (field.hpp:92-116), K-point midpoint quadrature
-            const float4 va = wrec[sl][3], vb = wrec[sl][4];
-            const float V[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
-            const float seg = tb - ta;
-            const float lk = seg * dnorm * (1.0f / K);
-            float sa[K], tk[K];
-            float sum = 0.f;
+            const int jb = has_b ? __ffs(mm) - 1 : 0;
+            if (has_b) mm &= mm - 1;
+            float alpha[2], dvox[2], sa[2][K], tk[2][K];
+            bool ok[2];
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                tk[k] = ta + ((k + 0.5f) / K) * seg;
-                const float qx = (tk[k] * dx - lo.x) * lo.w;
-                const float qy = (tk[k] * dy - lo.y) * lo.w;
-                const float qz = (tk[k] * dz - lo.z) * lo.w;
-                const float act = explin(trilinear(V, qx, qy, qz));
-                sum += act;
-                sa[k] = 1.0f - fexp(-lk * act);
-            }
-            const float alpha = (K == 1) ? sa[0] : 1.0f - fexp(-lk * sum);
-            const float w = T * alpha;
-            if (!RECORD) {
-                // voxel_depth (field.hpp:173-181)
-                float dvox = 0.f, Tk = 1.f;
+            for (int u = 0; u < 2; ++u) {
+                const int s_ = (u == 0) ? sl : (has_b ? sl + 1 : sl);
+                const float4 bb = wrec[s_][1];
+                const float4 lo = wrec[s_][0];
+                const float4 va = wrec[s_][2], vb = wrec[s_][3];
+                const float inv = wrec[s_][5].w;
+                const bool pass = (u == 0 || has_b) && !done &&
+                                  (one_sign || (wvid[s_] >> 29) == my_sign) &&
+                                  !(pcx < bb.x || pcx > bb.y || pcy < bb.z || pcy > bb.w);
+                float t0 = lo.x * ix, t1 = (lo.x + lo.w) * ix;
+                float ta = fminf(t0, t1), tb = fmaxf(t0, t1);
+                t0 = lo.y * iy;
+                t1 = (lo.y + lo.w) * iy;
+                ta = fmaxf(ta, fminf(t0, t1));
+                tb = fminf(tb, fmaxf(t0, t1));
+                t0 = lo.z * iz;
+                t1 = (lo.z + lo.w) * iz;
+                ta = fmaxf(ta, fminf(t0, t1));
+                tb = fminf(tb, fmaxf(t0, t1));
+                ok[u] = pass && (ta <= tb && ta > 0.0f);
+                // voxel_alpha (field.hpp:92-116), K-point midpoint quadrature
+                const float V[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
+                const float seg = tb - ta;
+                const float lk = seg * dnorm * (1.0f / K);
+                float sum = 0.f;
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
-                    dvox += Tk * sa[k] * tk[k];
-                    Tk *= 1.0f - sa[k];
+                    tk[u][k] = ta + ((k + 0.5f) / K) * seg;
+                    const float qx = (tk[u][k] * dx - lo.x) * inv;
+                    const float qy = (tk[u][k] * dy - lo.y) * inv;
+                    const float qz = (tk[u][k] * dz - lo.z) * inv;
+                    const float act = explin(trilinear(V, qx, qy, qz));
+                    sum += act;
+                    sa[u][k] = 1.0f - fexp(-lk * act);
                 }
-                if (median < 0.0f) {
-                    float Tf = T;
+                alpha[u] = (K == 1) ? sa[u][0] : 1.0f - fexp(-lk * sum);
+                // voxel_depth (field.hpp:173-181)
+                float dv = 0.f, Tk = 1.f;
 #pragma unroll
-                    for (int k = 0; k < K; ++k) {
-                        Tf *= 1.0f - sa[k];
-                        if (Tf < 0.5f) {
-                            median = tk[k];
-                            break;
+                for (int k = 0; k < K; ++k) {
+                    dv += Tk * sa[u][k] * tk[u][k];
+                    Tk *= 1.0f - sa[u][k];
+                }
+                dvox[u] = dv;
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                if (!ok[u] || done) continue;
+                const int s_ = sl + u;
+                const float w = T * alpha[u];
+                if (!RECORD) {
+                    if (median < 0.0f) {
+                        float Tf = T;
+#pragma unroll
+                        for (int k = 0; k < K; ++k) {
+                            Tf *= 1.0f - sa[u][k];
+                            if (Tf < 0.5f) {
+                                median = tk[u][k];
+                                break;
+                            }
                         }
                     }
+                    const float4 col = wrec[s_][4], nor = wrec[s_][5];
+                    cr += w * col.x;
+                    cg += w * col.y;
+                    cb += w * col.z;
+                    nx += w * nor.x;
+                    ny += w * nor.y;
+                    nz += w * nor.z;
+                    depth += T * dvox[u];
+                    if (a.max_blend) atomicMax(a.max_blend + __float_as_uint(col.w), __float_as_uint(w));
+                } else {
+                    a.contrib_entry[rec_base + cnt] = c + uint32_t(u == 0 ? ja : jb);
+                    a.contrib_T[rec_base + cnt] = T;
                 }
-                const float4 col = wrec[sl][5], nor = wrec[sl][6];
-                cr += w * col.x;
-                cg += w * col.y;
-                cb += w * col.z;
-                nx += w * nor.x;
-                ny += w * nor.y;
-                nz += w * nor.z;
-                depth += T * dvox;
-                if (a.max_blend) atomicMax(a.max_blend + __float_as_uint(hi.w), __float_as_uint(w));
-            } else {
-                a.contrib_entry[rec_base + cnt] = c + j;
-                a.contrib_T[rec_base + cnt] = T;
+                T *= 1.0f - alpha[u];
+                ++cnt;
+                if (T < thr) done = true;
             }
-            T *= 1.0f - alpha;
-            ++cnt;
-            if (T < thr) done = true;
         }
         __syncwarp();
         v0 = v1;
@@ -648,15 +663,14 @@ __global__ void __launch_bounds__(256) contrib_segments_kernel(
         uint32_t e = contrib_entry[base + c];
         uint32_t vid = vals[e] & ((1u << 29) - 1u);
         const float4 lo = records[uint64_t(vid) * kRecordF4 + 0];
-        const float4 hi = records[uint64_t(vid) * kRecordF4 + 1];
-        float t0 = lo.x * ix, t1 = hi.x * ix;
+        float t0 = lo.x * ix, t1 = (lo.x + lo.w) * ix;
         float ta = fminf(t0, t1), tb = fmaxf(t0, t1);
         t0 = lo.y * iy;
-        t1 = hi.y * iy;
+        t1 = (lo.y + lo.w) * iy;
         ta = fmaxf(ta, fminf(t0, t1));
         tb = fminf(tb, fmaxf(t0, t1));
         t0 = lo.z * iz;
-        t1 = hi.z * iz;
+        t1 = (lo.z + lo.w) * iz;
         ta = fmaxf(ta, fminf(t0, t1));
         tb = fminf(tb, fmaxf(t0, t1));
         contrib_pre[base + c] = pre_rank[vid];

@@ -212,6 +212,9 @@ void launch_duplicate_list(const DevCamera& cam, uint64_t n, const uint32_t* vid
                            const uint32_t* offsets, uint64_t* keys, uint32_t* vals,
                            cudaStream_t st);
 
-constexpr int kRecordF4 = 7;  // float4 slots per voxel record (112 B)
+// Voxel record (96 B = 6 float4), written by K1, read by K7/K9/K10:
+//   [0] lo.xyz (camera-relative min corner), size   [1] screen AABB x0,x1,y0,y1
+//   [2] V0..V3   [3] V4..V7   [4] rgb, vid (bits)   [5] unit normal, 1/size
+constexpr int kRecordF4 = 6;
 
 }  // namespace svrb
