@@ -255,6 +255,17 @@ int svr_synth_random_scene(uint64_t seed, uint64_t target, int max_level, int sh
                            uint64_t* n_voxels, uint64_t* n_pool, uint64_t** codes,
                            uint8_t** levels, uint32_t** corner_index, float** density,
                            float** sh);
+/* init_unbounded (optim.cpp:96-184) for cameras cams[0..n_cams): observed
+ * main block at level shell_levels+init_level, coarser shells refined by
+ * max sampling rate until bg/fg >= bg_ratio; then the pool is built as
+ * rebuild_corner_indexing and parameters drawn as generator G from a fresh
+ * mt19937_64(seed) (densities U(-4,2.5), SH as tests/test_raster.cpp:29-37).
+ * Also returns the scene bounds (centre, size). Same ownership as above. */
+int svr_synth_unbounded_scene(const svr_camera* cams, int n_cams, int init_level,
+                              int shell_levels, double bg_ratio, uint64_t seed, int sh_degree,
+                              uint64_t* n_voxels, uint64_t* n_pool, uint64_t** codes,
+                              uint8_t** levels, uint32_t** corner_index, float** density,
+                              float** sh, double* bounds_center, double* bounds_size);
 /* ring_cameras (synth.cpp:89-118), camera i of n. */
 int svr_ring_camera(int n_views, int index, int width, int height, double distance,
                     double fov_x_deg, svr_camera* out);

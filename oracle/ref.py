@@ -52,6 +52,9 @@ def load_ref() -> C.CDLL:
     sig = {
         "ref_last_error": (C.c_char_p, []),
         "ref_scene_gen": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.POINTER(P)]),
+        "ref_scene_unbounded": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64,
+                                          C.c_int, C.POINTER(P)]),
+        "ref_scene_bounds": (None, [P, P, C.POINTER(C.c_double)]),
         "ref_scene_make": (C.c_int, [C.POINTER(svr.svr_scene_desc), C.POINTER(P)]),
         "ref_scene_from_paths": (C.c_int, [P, P, C.c_uint64, C.c_float, C.c_int, C.POINTER(P)]),
         "ref_scene_free": (None, [P]),
@@ -105,6 +108,23 @@ class RefScene:
         h = C.c_void_p()
         _chk(load_ref().ref_scene_gen(seed, target, max_level, sh_degree, C.byref(h)))
         return RefScene(h)
+
+    @staticmethod
+    def unbounded(cameras, init_level: int, shell_levels: int, bg_ratio: float, seed: int,
+                  sh_degree: int = 3) -> "RefScene":
+        """init_unbounded (optim.cpp:96-184) + G-style parameters."""
+        svr = _svr()
+        arr = (svr.svr_camera * len(cameras))(*[c.to_c() for c in cameras])
+        h = C.c_void_p()
+        _chk(load_ref().ref_scene_unbounded(arr, len(cameras), init_level, shell_levels,
+                                            bg_ratio, seed, sh_degree, C.byref(h)))
+        return RefScene(h)
+
+    def bounds(self):
+        c = (C.c_double * 3)()
+        s = C.c_double()
+        load_ref().ref_scene_bounds(self.h, c, C.byref(s))
+        return tuple(c), s.value
 
     @staticmethod
     def from_arrays(a) -> "RefScene":

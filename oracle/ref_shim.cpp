@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "svr/losses.hpp"
+#include "svr/optim.hpp"
 #include "svr/raster.hpp"
 #include "svr/synth.hpp"
 #include "svr_b200.h"
@@ -150,6 +151,40 @@ int ref_scene_gen(uint64_t seed, uint64_t target, int max_level, int sh_degree, 
         }
         *out = s;
     });
+}
+
+// Config-4/5 scene: the reference's own init_unbounded
+// (optim.cpp:96-184), then parameters drawn as generator G from a fresh
+// mt19937_64(seed) (density per pool entry, then SH per voxel).
+int ref_scene_unbounded(const svr_camera* cams, int n_cams, int init_level, int shell_levels,
+                        double bg_ratio, uint64_t seed, int sh_degree, void** out) {
+    return guarded([&] {
+        std::vector<Camera> cv;
+        for (int i = 0; i < n_cams; ++i) cv.push_back(to_cam(&cams[i]));
+        TrainConfig cfg;
+        cfg.init_level = init_level;
+        cfg.shell_levels = shell_levels;
+        cfg.bg_ratio = bg_ratio;
+        cfg.sh_degree = sh_degree;
+        auto* s = new SparseScene(init_unbounded(cv, cfg));
+        std::mt19937_64 rng(seed);
+        std::uniform_real_distribution<double> ud(-4.0, 2.5), uc(0.05, 0.8);
+        for (auto& d : s->density) d = float(ud(rng));
+        for (size_t vi = 0; vi < s->voxel_count(); ++vi) {
+            float* sh = s->sh_of(vi);
+            for (int ch = 0; ch < 3; ++ch) sh[ch] = float(sh_dc_for_intensity(uc(rng)));
+            for (int m = 3; m < s->sh_stride(); ++m) sh[m] = float(0.1 * (uc(rng) - 0.4));
+        }
+        *out = s;
+    });
+}
+
+void ref_scene_bounds(void* h, double* center, double* size) {
+    auto* s = static_cast<SparseScene*>(h);
+    center[0] = s->bounds.center.x;
+    center[1] = s->bounds.center.y;
+    center[2] = s->bounds.center.z;
+    *size = s->bounds.size;
 }
 
 // Scene from explicit arrays (fixtures built elsewhere).

@@ -112,7 +112,8 @@ EXPORTS = [
     "svr_frame_records", "svr_render_backward", "svr_l1_loss", "svr_train_step_l1",
     "svr_project_voxels", "svr_tile_sign_masks", "svr_build_sort_entries", "svr_sort_entries",
     "svr_synth_random_scene", "svr_ring_camera", "svr_free", "svr_launch_count",
-    "svr_ctx_enable_timing", "svr_ctx_stage_times",
+    "svr_ctx_enable_timing", "svr_ctx_stage_times", "svr_frame_pre", "svr_render_oracle",
+    "svr_synth_unbounded_scene",
 ]
 STAGES = ["tile_setup", "preprocess", "scan", "duplicate", "sort", "ranges", "composite",
           "record", "downsample", "backward", "epilogue", "other"]
@@ -167,12 +168,19 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                              C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                              C.POINTER(P), C.POINTER(P), C.POINTER(P),
                                              C.POINTER(P), C.POINTER(P)]),
+        "svr_synth_unbounded_scene": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_double,
+                                                C.c_uint64, C.c_int, C.POINTER(C.c_uint64),
+                                                C.POINTER(C.c_uint64)] + [C.POINTER(P)] * 5
+                                      + [P, C.POINTER(C.c_double)]),
         "svr_ring_camera": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
                                       C.c_double, C.POINTER(svr_camera)]),
         "svr_free": (None, [P]),
         "svr_launch_count": (C.c_ulonglong, []),
         "svr_ctx_enable_timing": (C.c_int, [P, C.c_int]),
         "svr_ctx_stage_times": (C.c_int, [P, C.POINTER(C.c_double), C.c_int, C.c_int]),
+        "svr_frame_pre": (C.c_int, [P, P, C.c_uint64]),
+        "svr_render_oracle": (C.c_int, [P, P, C.POINTER(svr_camera),
+                                        C.POINTER(svr_render_options), P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -284,13 +292,7 @@ class SceneArrays:
         return 3 * (self.sh_degree + 1) ** 2
 
 
-def synth_random_scene(seed: int, target: int, max_level: int, sh_degree: int = 3) -> SceneArrays:
-    """Generator G of SURVEY §8(d) (same RNG stream as the oracle's)."""
-    lib = load_library()
-    n, p = C.c_uint64(), C.c_uint64()
-    ptrs = [C.c_void_p() for _ in range(5)]
-    _check(lib.svr_synth_random_scene(seed, target, max_level, sh_degree, C.byref(n), C.byref(p),
-                                      *[C.byref(x) for x in ptrs]))
+def _take_scene(lib, n, p, ptrs, sh_degree, **kw) -> SceneArrays:
     N, P = n.value, p.value
     stride = 3 * (sh_degree + 1) ** 2
 
@@ -303,7 +305,35 @@ def synth_random_scene(seed: int, target: int, max_level: int, sh_degree: int = 
     return SceneArrays(take(ptrs[0], np.uint64, N), take(ptrs[1], np.uint8, N),
                        take(ptrs[2], np.uint32, N * 8).reshape(N, 8),
                        take(ptrs[3], np.float32, P), take(ptrs[4], np.float32, N * stride)
-                       .reshape(N, stride), sh_degree)
+                       .reshape(N, stride), sh_degree, **kw)
+
+
+def synth_random_scene(seed: int, target: int, max_level: int, sh_degree: int = 3) -> SceneArrays:
+    """Generator G of SURVEY §8(d) (same RNG stream as the oracle's)."""
+    lib = load_library()
+    n, p = C.c_uint64(), C.c_uint64()
+    ptrs = [C.c_void_p() for _ in range(5)]
+    _check(lib.svr_synth_random_scene(seed, target, max_level, sh_degree, C.byref(n), C.byref(p),
+                                      *[C.byref(x) for x in ptrs]))
+    return _take_scene(lib, n, p, ptrs, sh_degree)
+
+
+def synth_unbounded_scene(cameras: Sequence["Camera"], init_level: int = 7, shell_levels: int = 5,
+                          bg_ratio: float = 2.8, seed: int = 7,
+                          sh_degree: int = 3) -> SceneArrays:
+    """init_unbounded (optim.cpp:96-184) over `cameras`, parameters randomised
+    as generator G from mt19937_64(seed): the config-4/5 scene of SURVEY §8(d)
+    is synth_unbounded_scene([ring_camera(8, i, 1024, 1024) for i in range(8)])."""
+    lib = load_library()
+    arr = (svr_camera * len(cameras))(*[c.to_c() for c in cameras])
+    n, p = C.c_uint64(), C.c_uint64()
+    ptrs = [C.c_void_p() for _ in range(5)]
+    bc = (C.c_double * 3)()
+    bs = C.c_double()
+    _check(lib.svr_synth_unbounded_scene(arr, len(cameras), init_level, shell_levels, bg_ratio,
+                                         seed, sh_degree, C.byref(n), C.byref(p),
+                                         *[C.byref(x) for x in ptrs], bc, C.byref(bs)))
+    return _take_scene(lib, n, p, ptrs, sh_degree, bounds_center=tuple(bc), bounds_size=bs.value)
 
 
 # ---------------------------------------------------------------- handles
