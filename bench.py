@@ -1,23 +1,35 @@
 #!/usr/bin/env python
 """Benchmark of the B200 sparse-voxel rasterizer (BASELINE.json metric).
 
-metric : FPS @1024x1024 on the 1M-voxel scene (config 2), reported as
-         frames/s (whole job, all ranks) plus Mrays/s and HBM roofline.
+Default workload (the driver's bench line) is config 2:
+metric : FPS @1024x1024 on the 1M-voxel scene, reported as frames/s (whole
+         job, all ranks) plus Mrays/s and the HBM roofline of the dominant
+         kernel.
 step   : one forward render (svr::render path: preprocess -> duplicate ->
-         onesweep sort -> tile ranges -> composite) of one 1024x1024 view of
-         the config-2 scene per GPU. Views come from ring_cameras(256, ...)
-         (view 0 is exactly config 2's camera); rank r renders views
-         r, r+N, r+2N, ... so the work is view-sharded (weak scaling, no
-         collective on the data path).
+         onesweep sort -> tile ranges -> composite) of one 1024x1024 view per
+         GPU. Views come from ring_cameras(256, ...) (view 0 is exactly
+         config 2's camera); rank r renders views r, r+N, r+2N, ... (weak
+         scaling, no collective on the data path).
 value  : device time, CUDA events on the library's stream around each step,
          L2 flushed (256 MiB write) before every timed step, max over ranks.
-e2e    : the same render through the C ABI with the camera passed from the
-         host and all five output images (37.7 MB) copied back to pinned
-         host memory every step, wall clock, max over ranks.
+e2e    : the same step through the C ABI with host buffers: camera in, all
+         five output images (37.7 MB) copied back to pinned host memory every
+         step, wall clock, max over ranks.
+
+Other SURVEY §8(d) workloads (--workload; bench lines for profiles/, the
+driver runs the default):
+  cfg3  training step at 800x800 on the 1M scene: forward (with records) ->
+        L1 against a U(0,1) image -> render_backward to density/SH.
+  cfg4  8M-voxel init_unbounded scene, 1024^2 views of ring_cameras(256, ...,
+        radius 1.0) sharded by view.
+  cfg5  cfg4 scene, training step on a batch of 4 views per GPU with one
+        in-place all-reduce of the flat [density | SH] gradient (NCCL).
+
 --impl reference : the reference's own CPU implementation (oracle/_ref,
          compiled unmodified) on this host's cores, same metric/config.
 
-Run: python bench.py [--gpus N --steps K --warmup W]; N>1 under torchrun.
+Run: python bench.py [--gpus N --steps K --warmup W --workload cfgX]; N>1
+under torchrun.
 """
 from __future__ import annotations
 
@@ -36,14 +48,38 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "FPS @1024x1024 (1M voxels)"
-UNIT = "frames/s"
 N_VIEWS = 256
-RES = 1024
-SCENE = dict(seed=7, target=1 << 20, max_level=9, sh_degree=3)
-WORKLOAD = ("cfg2: generator G(seed 7, 2^20, max level 9) -> 1,048,573 leaf voxels (L3-9), "
-            "SH degree 3; 1024x1024, supersample 1.0, K=1, t_threshold 1e-4, bg 0; views "
-            "ring_cameras(256, 1024, 1024, 1.3, 55 deg), rank r renders views r, r+N, ...")
+G_SCENE = dict(seed=7, target=1 << 20, max_level=9, sh_degree=3)
+U_SCENE = dict(init_level=7, shell_levels=5, bg_ratio=2.8, seed=7, sh_degree=3)
+WORKLOADS = {
+    "cfg2": dict(kind="render", scene="G", res=1024, dist=1.3, batch=1,
+                 metric="FPS @1024x1024 (1M voxels)", unit="frames/s",
+                 desc="cfg2: generator G(seed 7, 2^20, max level 9) -> 1,048,573 leaf voxels "
+                      "(L3-9), SH degree 3; 1024x1024, supersample 1.0, K=1, t_threshold 1e-4, "
+                      "bg 0; views ring_cameras(256, 1024, 1024, 1.3, 55 deg), rank r renders "
+                      "views r, r+N, ..."),
+    "cfg3": dict(kind="train", scene="G", res=800, dist=1.3, batch=1,
+                 metric="training steps/s @800x800 (1M voxels)", unit="steps/s",
+                 desc="cfg3: cfg2 scene, ring_cameras(1, 800, 800, 1.3, 55 deg)[0], gt U(0,1) "
+                      "seed 17; forward with records -> L1 -> render_backward to density, SH "
+                      "(and priority), K=1, supersample 1.0"),
+    "cfg4": dict(kind="render", scene="U", res=1024, dist=1.0, batch=1,
+                 metric="FPS @1024x1024 (8M voxels, 256 views)", unit="frames/s",
+                 desc="cfg4: init_unbounded(ring_cameras(8, 1024, 1024, 1.3, 55 deg), init_level "
+                      "7, shell_levels 5, bg_ratio 2.8) -> 7,824,544 voxels (L2-16), parameters "
+                      "as G (seed 7); 1024x1024 views of ring_cameras(256, 1024, 1024, 1.0, 55 "
+                      "deg), rank r renders views r, r+N, ..."),
+    "cfg5": dict(kind="train", scene="U", res=1024, dist=1.0, batch=4,
+                 metric="training views/s @1024x1024 (8M voxels)", unit="views/s",
+                 desc="cfg5: cfg4 scene; per GPU a batch of 4 views of ring_cameras(256, 1024, "
+                      "1024, 1.0, 55 deg) (rank r: views 4(r + N i) .. +3), gt U(0,1) seed "
+                      "17+view; forward -> L1 -> backward into one flat [density | SH] buffer, "
+                      "in-place all-reduce (NCCL) across ranks"),
+}
+# the driver's metric/config (BASELINE.json) is config 2's
+METRIC = WORKLOADS["cfg2"]["metric"]
+UNIT = WORKLOADS["cfg2"]["unit"]
+WORKLOAD = WORKLOADS["cfg2"]["desc"]
 
 
 def parse():
@@ -55,6 +91,7 @@ def parse():
     p.add_argument("--supersample", type=float, default=1.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=20)
+    p.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
     return p.parse_args()
 
 
@@ -136,45 +173,118 @@ def measured_peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def stage_bytes(stage, n_vox, n_pool, n_vis, E, R, ntiles, stride, npass):
-    """Algorithmic bytes per launch."""
+def stage_bytes(stage, d):
+    """Algorithmic bytes per launch. d: n_vox, n_pool, n_vis,
+    E, R, ntiles, stride, npass, contribs."""
     if stage == "composite":
-        return E * (4 + 112) + ntiles * 8 + R * 36
+        return d["E"] * (4 + 96) + d["ntiles"] * 8 + d["R"] * 36
     if stage == "preprocess":
-        return n_vox * (8 + 16 + 4) + 4 * n_pool + n_vis * (32 + 4 * stride + 112)
+        return d["n_vox"] * (8 + 16 + 4) + 4 * d["n_pool"] + d["n_vis"] * (32 + 4 * d["stride"] + 96)
     if stage == "sort":
-        return E * 12 + npass * E * 24
+        return d["npass"] * d["E"] * 16
     if stage == "duplicate":
-        return n_vis * (8 + 16 + 8) + E * 12
+        return d["n_vis"] * (8 + 16 + 8) + d["E"] * 8
     if stage == "scan":
-        return n_vox * 12
+        return d["n_vox"] * 12
+    if stage == "backward":
+        return (d["E"] * 4 + d["n_vis"] * (96 + 32 + 28) + d["contribs"] * 8 + d["R"] * 20
+                + 4 * d["n_pool"])
+    if stage == "epilogue":
+        return d["n_vox"] * 16 + d["n_vis"] * (8 + 8 * d["stride"] + 24 + 32 + 32)
     return None
 
 
-def traffic_from_profiles(stage):
+def traffic_from_profiles(stage, workload):
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as fh:
-            return json.load(fh).get(stage)
+            t = json.load(fh)
+        return t.get(workload, {}).get(stage) if isinstance(t.get(workload), dict) else t.get(stage)
     except (OSError, ValueError):
         return None
 
 
+# ------------------------------------------------------------------ scenes / views
+def make_scene_arrays(svr, w):
+    if w["scene"] == "G":
+        return svr.synth_random_scene(**G_SCENE)
+    cams = [svr.ring_camera(8, i, 1024, 1024) for i in range(8)]
+    return svr.synth_unbounded_scene(cams, **U_SCENE)
+
+
+def view_ids(w, rank, world, i):
+    """Views of step i on `rank` (view-sharded, `batch` views per step).
+    cfg3 trains on its single view; cfg5 cycles through 4 batches per rank
+    (16 ground-truth images resident per GPU)."""
+    if w["kind"] == "train" and w["scene"] == "G":
+        return [0] * w["batch"]
+    b = w["batch"]
+    first = b * (rank + world * (i % 4 if w["kind"] == "train" else i))
+    return [(first + k) % N_VIEWS for k in range(b)]
+
+
+def make_camera(svr, w, v):
+    if w["kind"] == "train" and w["scene"] == "G":
+        return svr.ring_camera(1, 0, w["res"], w["res"], w["dist"])  # cfg3's single view
+    return svr.ring_camera(N_VIEWS, v, w["res"], w["res"], w["dist"])
+
+
+def make_gt(w, v):
+    seed = 17 if w["scene"] == "G" else 17 + v
+    return np.random.default_rng(seed).uniform(0, 1, (w["res"], w["res"], 3)).astype(np.float32)
+
+
 # ------------------------------------------------------------------ reference (CPU)
-def reference_frame_time(ref, rscene, cam, opts, threads: int) -> float:
-    """One full frame through the reference's own svr::render, split into
-    `threads` horizontal bands rendered concurrently (the reference API is
-    reentrant; ctypes releases the GIL). Returns seconds."""
-    import paper_2412_04459_b200 as svr
-    rows = max(16, ((cam.height + threads - 1) // threads + 15) // 16 * 16)
-    bands = []
+def band_cameras(svr, cam, threads, rows=None):
+    """Horizontal bands of `cam` (each a full camera with shifted cy)."""
+    rows = rows or max(16, ((cam.height + threads - 1) // threads + 15) // 16 * 16)
+    out = []
     for y0 in range(0, cam.height, rows):
         h = min(rows, cam.height - y0)
-        bands.append(svr.Camera(cam.width, h, cam.fx, cam.fy, cam.cx, cam.cy - y0, cam.rot, cam.pos))
+        out.append(svr.Camera(cam.width, h, cam.fx, cam.fy, cam.cx, cam.cy - y0, cam.rot, cam.pos))
+    return out
+
+
+def reference_step_time(ref, rscene, arrays, w, cam, opts, threads, gt=None, frac=1.0):
+    """One step of workload w through the reference's own svr::render (and,
+    for training, its L1 + render_backward) split into row bands rendered
+    concurrently (the reference API is reentrant; ctypes releases the GIL).
+    frac < 1 renders only that fraction of the bands (evenly spread) and
+    scales the time. Returns seconds per full step."""
+    import paper_2412_04459_b200 as svr
+    bands = band_cameras(svr, cam, threads)
+    if frac < 1.0:
+        keep = max(1, int(round(len(bands) * frac)))
+        idx = np.linspace(0, len(bands) - 1, keep).round().astype(int)
+        scale = len(bands) / keep
+        bands = [bands[i] for i in sorted(set(idx))]
+    else:
+        scale = 1.0
+
+    def one(c):
+        if w["kind"] == "render":
+            ref.ref_render(rscene, c, opts)
+        else:
+            y0 = int(round(cam.cy - c.cy))
+            g = gt[y0:y0 + c.height]
+            ref.ref_train_step_l1(rscene, c, opts, g, arrays.n_pool, arrays.n_voxels * arrays.sh_stride,
+                                  arrays.n_voxels)
+
     t0 = time.perf_counter()
-    with cf.ThreadPoolExecutor(max_workers=len(bands)) as ex:
-        list(ex.map(lambda c: ref.ref_render(rscene, c, opts), bands))
-    return time.perf_counter() - t0
+    with cf.ThreadPoolExecutor(max_workers=min(threads, len(bands))) as ex:
+        list(ex.map(one, bands))
+    return (time.perf_counter() - t0) * scale
+
+
+CPU_FRACTION = {"cfg2": 1.0, "cfg3": 1.0, "cfg4": 1.0 / 16, "cfg5": 1.0 / 16}
+
+
+def cpu_sample_text(w, name, cores):
+    frac = CPU_FRACTION[name]
+    what = "render" if w["kind"] == "render" else "train step (render + L1 + render_backward)"
+    part = "the full view" if frac >= 1.0 else f"{frac:.4g} of the view's row bands (evenly spread), time scaled up"
+    return (f"one {w['res']}x{w['res']} {name} {what} through the unmodified reference "
+            f"(oracle/_ref) split into row bands on {cores} threads; {part}")
 
 
 def run_reference(args, rank):
@@ -182,56 +292,111 @@ def run_reference(args, rank):
         return
     import paper_2412_04459_b200 as svr
     from oracle import ref
+    w = WORKLOADS[args.workload]
     cores = host_cores()
-    rscene = ref.RefScene.generate(**SCENE)
-    opts = svr.RenderOptions(K=1, supersample=args.supersample)
-    cams = [svr.ring_camera(N_VIEWS, i, RES, RES) for i in range(N_VIEWS)]
+    arrays = make_scene_arrays(svr, w)
+    rscene = ref.RefScene.from_arrays(arrays)
+    opts = svr.RenderOptions(K=1, supersample=args.supersample, training=w["kind"] == "train")
+    frac = CPU_FRACTION[args.workload]
+
+    def step(i):
+        t = 0.0
+        for v in view_ids(w, 0, 1, i):
+            cam = make_camera(svr, w, v)
+            t += reference_step_time(ref, rscene, arrays, w, cam, opts, cores,
+                                     make_gt(w, v) if w["kind"] == "train" else None, frac)
+        return t
+
     for i in range(args.warmup):
-        reference_frame_time(ref, rscene, cams[i % N_VIEWS], opts, cores)
-    total = 0.0
-    for i in range(args.steps):
-        total += reference_frame_time(ref, rscene, cams[i % N_VIEWS], opts, cores)
-    fps = args.steps / total
-    sw = int(np.ceil(args.supersample * RES))
+        step(i)
+    total = sum(step(i) for i in range(args.steps))
+    units = args.steps * w["batch"]
+    val = units / total
+    sw = int(np.ceil(args.supersample * w["res"]))
     line = {
-        "impl": "reference", "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "mrays_per_s": fps * sw * sw / 1e6,
-        "config": {"workload": WORKLOAD, "voxels": 1048573, "resolution": f"{RES}x{RES}",
+        "impl": "reference", "metric": w["metric"], "value": val, "unit": w["unit"],
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "mrays_per_s": val * sw * sw / 1e6,
+        "config": {"workload": w["desc"], "voxels": arrays.n_voxels, "resolution": f"{w['res']}x{w['res']}",
                    "supersample": args.supersample, "K": 1, "parallelism": "cpu threads"},
-        "cpu_baseline": {"value": fps, "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": f"each step = one full 1024x1024 view rendered by the unmodified "
-                                   f"reference svr::render, split into {cores} row bands on "
-                                   f"{cores} threads"},
-        "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": val, "unit": w["unit"], "cores": cores, "kind": "reference",
+                         "sample": cpu_sample_text(w, args.workload, cores)},
+        "e2e": {"value": val, "unit": w["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ ours
+class RenderStep:
+    """cfg2/cfg4 step: one view rendered into a resident frame."""
+
+    def __init__(self, svr, ctx, scene, w, rank, world):
+        self.svr, self.scene, self.w, self.rank, self.world = svr, scene, w, rank, world
+        self.frame = svr.Frame(ctx)
+        self.opts = svr.RenderOptions(K=1, supersample=1.0)
+        self.cams = {}
+
+    def cam(self, v):
+        if v not in self.cams:
+            self.cams[v] = make_camera(self.svr, self.w, v)
+        return self.cams[v]
+
+    def __call__(self, i):
+        for v in view_ids(self.w, self.rank, self.world, i):
+            self.svr.render_into(self.frame, self.scene, self.cam(v), self.opts)
+
+
+class TrainStep:
+    """cfg3/cfg5 step: ShardedTrainer over this rank's batch of views."""
+
+    def __init__(self, svr, ctx, scene, w, rank, world):
+        import torch
+        from paper_2412_04459_b200.multiview import ShardedTrainer
+        self.w, self.rank, self.world = w, rank, world
+        self.views = sorted({v for i in range(4) for v in view_ids(w, rank, world, i)})
+        dev = torch.device("cuda", ctx.device)
+        cams, gts = {}, {}
+        for v in self.views:
+            cams[v] = make_camera(svr, w, v)
+            gts[v] = torch.tensor(make_gt(w, v), device=dev)
+        # ShardedTrainer indexes cameras/gts by view id
+        idx = {v: k for k, v in enumerate(self.views)}
+        self.idx = idx
+        self.trainer = ShardedTrainer(ctx, scene, [cams[v] for v in self.views],
+                                      [gts[v] for v in self.views],
+                                      svr.RenderOptions(K=1, supersample=1.0, training=True))
+        self.loss = None
+
+    def ids(self, i):
+        return [self.idx[v] for v in view_ids(self.w, self.rank, self.world, i) if v in self.idx]
+
+    def __call__(self, i):
+        self.loss = self.trainer.step(self.ids(i))
+
+
 def run_ours(args, rank, world, local_rank):
+    import ctypes as C
+
     import torch
     import torch.distributed as dist
+
     import paper_2412_04459_b200 as svr
 
+    w = WORKLOADS[args.workload]
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     ctx = svr.Context(local_rank)
-    arrays = svr.synth_random_scene(**SCENE)
+    arrays = make_scene_arrays(svr, w)
     scene = svr.Scene(ctx, arrays)
-    cams = [svr.ring_camera(N_VIEWS, i, RES, RES) for i in range(N_VIEWS)]
-    opts = svr.RenderOptions(K=1, supersample=args.supersample)
-    frame = svr.Frame(ctx)
+    step = (RenderStep if w["kind"] == "render" else TrainStep)(svr, ctx, scene, w, rank, world)
     st = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local_rank))
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > 126 MB L2
 
-    def view(i):
-        return cams[(rank + world * i) % N_VIEWS]
-
     for i in range(max(3, args.warmup)):
-        svr.render_into(frame, scene, view(i), opts)
+        step(i)
     ctx.synchronize()
     torch.cuda.synchronize()
     if world > 1:
@@ -246,15 +411,16 @@ def run_ours(args, rank, world, local_rank):
     ctx.stage_times(reset=True)
     launches0 = svr.launch_count()
     stats = []
+    frame = step.frame if w["kind"] == "render" else step.trainer.frame
     for i in range(args.steps):
         with torch.cuda.stream(st):
             flush.zero_()
         ev[i][0].record(st)
-        svr.render_into(frame, scene, view(i), opts)
+        step(i)
         ev[i][1].record(st)
         if i < 4:
             inf = frame.info()
-            stats.append((inf.n_entries, inf.n_visible, inf.sort_passes))
+            stats.append((inf.n_entries, inf.n_visible, inf.sort_passes, inf.n_contribs))
     ctx.synchronize()
     torch.cuda.synchronize()
     launches = svr.launch_count() - launches0
@@ -266,36 +432,56 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dev_ms_max = float(t.item())
-    fps = world * args.steps / (dev_ms_max / 1e3)
+    units_per_step = w["batch"]
+    value = world * units_per_step * args.steps / (dev_ms_max / 1e3)
 
     # ---- e2e through the C ABI with host buffers ------------------------
-    H = W = RES
-    pinned = {k: torch.empty(n, dtype=torch.float32, pin_memory=True)
-              for k, n in [("COLOR", H * W * 3), ("DEPTH", H * W), ("MEDIAN_DEPTH", H * W),
-                           ("NORMAL", H * W * 3), ("TRANSMITTANCE", H * W)]}
+    H = W = w["res"]
     lib = svr.load_library()
-    import ctypes as C
+    if w["kind"] == "render":
+        pinned = {k: torch.empty(n, dtype=torch.float32, pin_memory=True)
+                  for k, n in [("COLOR", H * W * 3), ("DEPTH", H * W), ("MEDIAN_DEPTH", H * W),
+                               ("NORMAL", H * W * 3), ("TRANSMITTANCE", H * W)]}
 
-    def e2e_step(i):
-        svr.render_into(frame, scene, view(i), opts)
-        for k, buf in pinned.items():
-            svr._check(lib.svr_frame_download(frame.h, svr.BUF[k], C.c_void_p(buf.data_ptr()),
-                                              C.c_size_t(buf.numel() * 4)))
+        def e2e_step(i):
+            step(i)
+            for k, buf in pinned.items():
+                svr._check(lib.svr_frame_download(frame.h, svr.BUF[k], C.c_void_p(buf.data_ptr()),
+                                                  C.c_size_t(buf.numel() * 4)))
 
+        d2h = sum(b.numel() * 4 for b in pinned.values())
+        h2d = C.sizeof(svr.svr_camera) + C.sizeof(svr.svr_render_options)
+        e2e_note = ("scene resident on device (uploaded once); per step camera in, "
+                    "color+depth+median+normal+transmittance out to pinned host memory")
+    else:
+        host_gt = {v: torch.tensor(make_gt(w, v)).pin_memory() for v in step.views}
+        tr = step.trainer
+
+        def e2e_step(i):
+            ids = step.ids(i)
+            with torch.cuda.stream(tr.stream):
+                for k in ids:
+                    tr.gts[k].copy_(host_gt[step.views[k]], non_blocking=True)
+            step(i)  # reads the loss back to the host
+
+        d2h = 4
+        h2d = units_per_step * (H * W * 12 + C.sizeof(svr.svr_camera))
+        e2e_note = ("scene and gradient buffers resident on device; per step each view's ground "
+                    "truth (pinned host) and camera in, the loss out")
     for i in range(2):
         e2e_step(i)
+    ctx.synchronize()
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for i in range(args.e2e_steps):
         e2e_step(i)
+    ctx.synchronize()
     e2e_s = time.perf_counter() - t0
     te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_fps = world * args.e2e_steps / float(te.item())
-    d2h = sum(b.numel() * 4 for b in pinned.values())
-    h2d = C.sizeof(svr.svr_camera) + C.sizeof(svr.svr_render_options)
+    e2e_val = world * units_per_step * args.e2e_steps / float(te.item())
 
     if rank != 0:
         if world > 1:
@@ -303,18 +489,23 @@ def run_ours(args, rank, world, local_rank):
         return
 
     # ---- roofline of the dominant kernel --------------------------------
-    E, n_vis, npass = stats[0]
-    sw = int(np.ceil(args.supersample * RES))
+    E, n_vis, npass, contribs = stats[0]
+    sw = int(np.ceil(args.supersample * w["res"]))
     ntiles = ((sw + 15) // 16) ** 2
-    per_launch = {k: v / args.steps for k, v in stage.items()}
-    dom = max(["preprocess", "sort", "composite", "duplicate", "scan"], key=lambda k: per_launch[k])
-    byt = stage_bytes(dom, arrays.n_voxels, arrays.n_pool, n_vis, E, sw * sw, ntiles,
-                      arrays.sh_stride, npass)
+    launches_per_step = {k: v / (args.steps * units_per_step) for k, v in stage.items()}
+    per_step = {k: v / args.steps for k, v in stage.items()}
+    cand = ["preprocess", "sort", "composite", "duplicate", "scan", "backward", "epilogue"]
+    dom = max(cand, key=lambda k: per_step.get(k, 0.0))
+    dd = dict(n_vox=arrays.n_voxels, n_pool=arrays.n_pool, n_vis=n_vis, E=E, R=sw * sw,
+              ntiles=ntiles, stride=arrays.sh_stride, npass=npass, contribs=contribs)
+    byt = stage_bytes(dom, dd)
     peak, peak_src = measured_peak_hbm()
-    achieved = byt / (per_launch[dom] * 1e-3) / 1e9
+    kernel_ms = launches_per_step[dom]  # one launch per view
+    achieved = byt / (kernel_ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic_from_profiles(dom),
-                "algorithmic_bytes": byt, "kernel_ms": per_launch[dom], "peak_source": peak_src}
+                "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic_from_profiles(dom, args.workload),
+                "algorithmic_bytes": byt, "kernel_ms": kernel_ms, "peak_source": peak_src}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -322,34 +513,42 @@ def run_ours(args, rank, world, local_rank):
             from oracle import ref
             rscene = ref.RefScene.from_arrays(arrays)
             cores = host_cores()
-            secs = reference_frame_time(ref, rscene, cams[0], opts, cores)
-            cpu = {"value": 1.0 / secs, "unit": UNIT, "cores": cores, "kind": "reference",
-                   "sample": f"one full 1024x1024 config-2 view through the unmodified reference "
-                             f"svr::render (oracle/_ref), split into row bands on {cores} threads"}
+            v = view_ids(w, 0, 1, 0)[0]
+            opts = svr.RenderOptions(K=1, supersample=1.0, training=w["kind"] == "train")
+            secs = reference_step_time(ref, rscene, arrays, w, make_camera(svr, w, v), opts, cores,
+                                       make_gt(w, v) if w["kind"] == "train" else None,
+                                       CPU_FRACTION[args.workload])
+            cpu = {"value": 1.0 / secs, "unit": w["unit"], "cores": cores, "kind": "reference",
+                   "sample": cpu_sample_text(w, args.workload, cores)}
         except Exception as e:  # the reference library may be absent on a fresh box
-            cpu = {"value": None, "unit": UNIT, "cores": host_cores(), "kind": "reference",
+            cpu = {"value": None, "unit": w["unit"], "cores": host_cores(), "kind": "reference",
                    "sample": f"unavailable: {type(e).__name__}: {e}"}
 
+    config = {"workload": w["desc"], "voxels": arrays.n_voxels, "pool": arrays.n_pool,
+              "resolution": f"{w['res']}x{w['res']}", "supersample": args.supersample, "K": 1,
+              "entries_per_view": int(E), "visible_voxels": int(n_vis), "sort_passes": npass,
+              "l2": "flushed (256 MiB write) before every timed step",
+              "parallelism": (f"view-sharded over {world} GPU(s), no data-path collective"
+                              if w["kind"] == "render" else
+                              f"view-batch sharded over {world} GPU(s), one in-place all-reduce "
+                              f"of the flat gradient per step"),
+              "precision": "projection/tile binning fp64 (bit-exact), compositing fp32"}
+    if w["kind"] == "train":
+        config["contribs_per_view"] = int(contribs)
+        config["views_per_gpu_step"] = units_per_step
     line = {
-        "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (generator G, random-init parameters)",
-        "mrays_per_s": fps * sw * sw / 1e6,
-        "config": {"workload": WORKLOAD, "voxels": arrays.n_voxels, "pool": arrays.n_pool,
-                   "resolution": f"{RES}x{RES}", "supersample": args.supersample, "K": 1,
-                   "entries_per_view": int(E), "visible_voxels": int(n_vis), "sort_passes": npass,
-                   "l2": "flushed (256 MiB write) before every timed step",
-                   "parallelism": f"view-sharded over {world} GPU(s), no data-path collective",
-                   "precision": "projection/tile binning fp64 (bit-exact), compositing fp32"},
+        "metric": w["metric"], "value": value, "unit": w["unit"], "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (random-init parameters)",
+        "mrays_per_s": value * sw * sw / 1e6,
+        "config": config,
         "roofline": roofline,
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e_fps, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h,
-                "note": "scene resident on device (uploaded once); per step camera in, "
-                        "color+depth+median+normal+transmittance out to pinned host memory"},
+        "e2e": {"value": e2e_val, "unit": w["unit"], "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "note": e2e_note},
         "gpu_launches": launches,
-        "stage_ms_per_step": per_launch,
+        "stage_ms_per_step": per_step,
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)

@@ -22,7 +22,6 @@ namespace svrb {
 
 namespace {
 
-constexpr int kAcc = 15;  // 8 corner densities + 3 colour + 3 normal + priority
 
 __global__ void lift_kernel(TapTable t, const float* g, int ch, int W, float* out, int sw,
                             int sh) {
@@ -64,30 +63,67 @@ __global__ void l1_kernel(const float* c, const float* gt, uint64_t n, float inv
     }
 }
 
+// Sum of v[0..15] over the 32 lanes by recursive halving: each step sends
+// half of the remaining values to the partner lane, so 16 values cost 16
+// shuffles instead of 80. On return lanes 2q and 2q+1 hold the total of
+// component q.
+__device__ __forceinline__ float warp_transpose_sum16(float (&v)[16], int lane) {
+#pragma unroll
+    for (int h = 8, bit = 16; h >= 1; h >>= 1, bit >>= 1) {
+        const bool upper = (lane & bit) != 0;
+#pragma unroll
+        for (int i = 0; i < h; ++i) {
+            const float send = upper ? v[i] : v[i + h];
+            const float keep = upper ? v[i + h] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
+        }
+    }
+    return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+
+// K9: warp-autonomous reverse walk. Each warp owns the same 8x4 pixel block
+// as the forward composite and walks the tile's entry list backwards in
+// chunks of 32, visiting only chunks that hold one of its pending
+// contributions. Per chunk, the entries that can matter for the block
+// (sign pattern, screen AABB, frustum: the forward's own filters) are
+// gathered into warp-private shared memory; then the warp repeatedly takes
+// the largest pending entry id over its lanes (every lane's contribution
+// list is descending) and the lanes whose next contribution it is apply the
+// division-free recursion of raster.cpp:374-407. The 15 per-entry sums
+// (8 corner densities, colour, normal, priority) are reduced across the warp
+// by recursive halving and issued as one vector of global atomics.
 template <int K>
 __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, BackwardArgs a) {
-    __shared__ float4 s_rec[kRecordF4][256];
-    __shared__ float s_acc[kAcc][256];
-    __shared__ uint32_t s_touch[256];
-    __shared__ int s_max_last;
+    __shared__ float4 s_rec[8][32][kRecordF4];
+    __shared__ float s_cone[8][4][3];
 
-    const int tile = blockIdx.x;
+    const int tile = a.tile_order ? int(a.tile_order[blockIdx.x]) : int(blockIdx.x);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tx = tile % cam.ntx, ty = tile / cam.ntx;
-    const int px = tx * kTile + (threadIdx.x & 15), py = ty * kTile + (threadIdx.x >> 4);
+    const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
+    const int py = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
     const bool inside = px < cam.W && py < cam.H;
-    const uint32_t slot = uint32_t(tile) * 256u + threadIdx.x;
-    const int lane = threadIdx.x & 31;
+    const uint32_t slot = uint32_t(tile) * 256u + uint32_t((py % kTile) * kTile + (px % kTile));
+    const int wx0 = px - (lane & 7), wy0 = py - (lane >> 3);
+    const float fx0 = float(wx0) + 0.5f, fx1 = float(wx0) + 7.5f;
+    const float fy0 = float(wy0) + 0.5f, fy1 = float(wy0) + 3.5f;
 
     double dd[3];
     pixel_ray_dir(cam, double(px), double(py), dd);
+    const uint32_t my_sign = sign_bits(dd);
+    const uint32_t warp_signs = __reduce_or_sync(0xffffffffu, inside ? (1u << my_sign) : 0u);
     const float dx = float(dd[0]), dy = float(dd[1]), dz = float(dd[2]);
     const float ix = 1.0f / dx, iy = 1.0f / dy, iz = 1.0f / dz;
     const float dnorm = float(sqrt(dd[0] * dd[0] + dd[1] * dd[1] + dd[2] * dd[2]));
+    float (*cone)[3] = s_cone[warp];
+    if (lane == 0) warp_cone_planes(cam, wx0, wy0, cone);
+    __syncwarp();
 
-    uint32_t n = 0, base = 0;
+    int n = 0;
+    uint32_t base = 0;
     float gC[3] = {0.f, 0.f, 0.f}, gN[3] = {0.f, 0.f, 0.f}, gD = 0.f, gT = 0.f;
     if (inside) {
-        n = a.pix_count[slot];
+        n = int(a.pix_count[slot]);
         base = a.pix_begin[slot];
         const uint64_t p = uint64_t(py) * cam.W + px;
         if (a.gC) gC[0] = a.gC[3 * p], gC[1] = a.gC[3 * p + 1], gC[2] = a.gC[3 * p + 2];
@@ -95,40 +131,57 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
         if (a.gD) gD = a.gD[p];
         if (a.gT) gT = a.gT[p];
     }
-    int kidx = int(n) - 1;  // next contribution to match, walking backwards
-    int next_e = kidx >= 0 ? int(a.contrib_entry[base + kidx]) : -1;
+    // pending contributions: (e1, T1) next, (e2, T2) the one after (prefetched)
+    // record k of this pixel: compact base + k, or staged k * stride + slot
+    const uint64_t rb = a.stage_stride ? slot : base;
+    const uint64_t rs = a.stage_stride ? a.stage_stride : 1u;
+    int kidx = n - 1;
+    int e1 = -1, e2 = -1;
+    float T1 = 0.f, T2 = 0.f;
+    if (kidx >= 0) e1 = int(a.contrib_entry[rb + kidx * rs]), T1 = a.contrib_T[rb + kidx * rs];
+    if (kidx >= 1)
+        e2 = int(a.contrib_entry[rb + (kidx - 1) * rs]), T2 = a.contrib_T[rb + (kidx - 1) * rs];
     float Ra = gC[0] * a.bg[0] + gC[1] * a.bg[1] + gC[2] * a.bg[2] + gT;
     float Rd = 0.f;
 
-    if (threadIdx.x == 0) s_max_last = -1;
-    for (int i = threadIdx.x; i < kAcc * 256; i += 256) (&s_acc[0][0])[i] = 0.f;
-    __syncthreads();
-    atomicMax(&s_max_last, next_e);
-    __syncthreads();
-    const int last = s_max_last;
     const uint2 range = a.ranges[tile];
-    if (last < 0) return;
+    constexpr uint32_t kVidMask = (1u << 29) - 1u;
+    float4 (*wrec)[kRecordF4] = s_rec[warp];
 
-    for (int end = last + 1; end > int(range.x); end -= 256) {
-        const int start = max(int(range.x), end - 256);
-        const int nb = end - start;
-        if (threadIdx.x < nb) {
-            const uint32_t vid = a.vals[start + threadIdx.x] & ((1u << 29) - 1u);
-            const float4* rec = a.records + uint64_t(vid) * kRecordF4;
-#pragma unroll
-            for (int k = 0; k < kRecordF4; ++k) s_rec[k][threadIdx.x] = __ldg(rec + k);
+    int cur = __reduce_max_sync(0xffffffffu, unsigned(e1 + 1)) - 1;
+    while (cur >= 0) {
+        // chunk holding `cur`, aligned to the tile's range start
+        const uint32_t c0 = range.x + (uint32_t(cur) - range.x) / 32u * 32u;
+        const uint32_t e = c0 + lane;
+        bool rel = false;
+        uint32_t v = 0;
+        if (e < range.y && e <= uint32_t(cur)) {
+            v = __ldg(a.vals + e);
+            const float4 b = __ldg(a.records + uint64_t(v & kVidMask) * kRecordF4 + 1);
+            rel = ((warp_signs >> (v >> 29)) & 1u) &&
+                  !(fx1 < b.x || fx0 > b.y || fy1 < b.z || fy0 > b.w);
+            if (rel && (b.y - b.x) * (b.w - b.z) > kConeMinArea) {
+                const float4 lo = __ldg(a.records + uint64_t(v & kVidMask) * kRecordF4);
+                rel = box_in_cone(cone, lo);
+            }
         }
-        s_touch[threadIdx.x] = 0;
-        __syncthreads();
-        for (int j = nb - 1; j >= 0; --j) {
-            const bool hit = (next_e == start + j);
-            if (!__any_sync(0xffffffffu, hit)) continue;
-            float acc[kAcc];
+        const uint32_t m = __ballot_sync(0xffffffffu, rel);
+        if (rel) {
+            const int sl = __popc(m & ((1u << lane) - 1u));
+            const float4* src = a.records + uint64_t(v & kVidMask) * kRecordF4;
 #pragma unroll
-            for (int q = 0; q < kAcc; ++q) acc[q] = 0.f;
+            for (int k = 0; k < kRecordF4; ++k) wrec[sl][k] = __ldg(src + k);
+        }
+        __syncwarp();
+        while (cur >= int(c0)) {
+            const int sl = __popc(m & ((1u << (uint32_t(cur) - c0)) - 1u));
+            const bool hit = (e1 == cur);
+            float acc[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) acc[q] = 0.f;
             if (hit) {
-                const float4 lo = s_rec[0][j];
-                const float inv = s_rec[5][j].w;
+                const float4 lo = wrec[sl][0];
+                const float inv = wrec[sl][5].w;
                 float t0 = lo.x * ix, t1 = (lo.x + lo.w) * ix;
                 float ta = fminf(t0, t1), tb = fmaxf(t0, t1);
                 t0 = lo.y * iy;
@@ -139,7 +192,7 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
                 t1 = (lo.z + lo.w) * iz;
                 ta = fmaxf(ta, fminf(t0, t1));
                 tb = fminf(tb, fmaxf(t0, t1));
-                const float4 va = s_rec[2][j], vb = s_rec[3][j];
+                const float4 va = wrec[sl][2], vb = wrec[sl][3];
                 const float V[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
                 const float seg = tb - ta;
                 const float lk = seg * dnorm * (1.0f / K);
@@ -154,17 +207,17 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
                     vk[k] = trilinear(V, qk[k][0], qk[k][1], qk[k][2]);
                     const float act = explin(vk[k]);
                     sum += act;
-                    sa[k] = 1.0f - fexp(-lk * act);
+                    sa[k] = one_minus_exp_neg(lk * act);
                 }
-                const float alpha = (K == 1) ? sa[0] : 1.0f - fexp(-lk * sum);
+                const float alpha = (K == 1) ? sa[0] : one_minus_exp_neg(lk * sum);
                 float dvox = 0.f, Tk = 1.f;
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     dvox += Tk * sa[k] * tk[k];
                     Tk *= 1.0f - sa[k];
                 }
-                const float Ti = a.contrib_T[base + kidx];
-                const float4 col = s_rec[4][j], nor = s_rec[5][j];
+                const float Ti = T1;
+                const float4 col = wrec[sl][4], nor = wrec[sl][5];
                 const float gw = a.d_weight ? a.d_weight[base + kidx] : 0.f;
                 const float phi = gC[0] * col.x + gC[1] * col.y + gC[2] * col.z + gN[0] * nor.x +
                                   gN[1] * nor.y + gN[2] * nor.z + gw;
@@ -186,8 +239,8 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
                 for (int k = 0; k < K; ++k) {
                     float others = 1.f;
 #pragma unroll
-                    for (int m = 0; m < K; ++m)
-                        if (m != k) others *= 1.0f - sa[m];
+                    for (int mm = 0; mm < K; ++mm)
+                        if (mm != k) others *= 1.0f - sa[mm];
                     const float dAk = A * others + Ti * gD * ddk[k];
                     const float dv = dAk * (1.0f - sa[k]) * lk * explin_deriv(vk[k]);
                     float w[8];
@@ -210,102 +263,115 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
                 acc[13] = wgt * gN[2];
                 Ra = alpha * phi + (1.0f - alpha) * Ra;
                 Rd = dvox * gD + (1.0f - alpha) * Rd;
+                // advance this pixel's list; prefetch the one after
                 --kidx;
-                next_e = kidx >= 0 ? int(a.contrib_entry[base + kidx]) : -1;
+                e1 = e2;
+                T1 = T2;
+                if (kidx >= 1) {
+                    e2 = int(a.contrib_entry[rb + (kidx - 1) * rs]);
+                    T2 = a.contrib_T[rb + (kidx - 1) * rs];
+                } else {
+                    e2 = -1;
+                }
             }
-#pragma unroll
-            for (int q = 0; q < kAcc; ++q) {
-                float v = acc[q];
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                acc[q] = v;
+            const float tot = warp_transpose_sum16(acc, lane);
+            const int q = lane >> 1;
+            if ((lane & 1) == 0 && q < 15) {
+                const uint32_t vid = __float_as_uint(wrec[sl][4].w);
+                float* dst;
+                if (q < 8) dst = a.g_density + __ldg(a.corner_index + 8ull * vid + q);
+                else if (q < 11) dst = a.g_color + 3ull * vid + (q - 8);
+                else if (q < 14) dst = a.g_normal + 3ull * vid + (q - 11);
+                else dst = a.g_priority + vid;
+                atomicAdd(dst, tot);
             }
-            if (lane == 0) {
-#pragma unroll
-                for (int q = 0; q < kAcc; ++q) atomicAdd(&s_acc[q][j], acc[q]);
-                s_touch[j] = 1;
-            }
+            cur = __reduce_max_sync(0xffffffffu, unsigned(e1 + 1)) - 1;
         }
-        __syncthreads();
-        // one set of global atomics per touched entry of this batch
-        if (threadIdx.x < nb && s_touch[threadIdx.x]) {
-            const int j = threadIdx.x;
-            const uint32_t vid = __float_as_uint(s_rec[4][j].w);
-            const uint4* ci4 = reinterpret_cast<const uint4*>(a.corner_index + 8ull * vid);
-            const uint4 c0 = ci4[0], c1 = ci4[1];
-            const uint32_t ci[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-#pragma unroll
-            for (int c = 0; c < 8; ++c) atomicAdd(a.g_density + ci[c], s_acc[c][j]);
-            atomicAdd(a.g_color + 3ull * vid + 0, s_acc[8][j]);
-            atomicAdd(a.g_color + 3ull * vid + 1, s_acc[9][j]);
-            atomicAdd(a.g_color + 3ull * vid + 2, s_acc[10][j]);
-            atomicAdd(a.g_normal + 3ull * vid + 0, s_acc[11][j]);
-            atomicAdd(a.g_normal + 3ull * vid + 1, s_acc[12][j]);
-            atomicAdd(a.g_normal + 3ull * vid + 2, s_acc[13][j]);
-            atomicAdd(a.g_priority + vid, s_acc[14][j]);
-#pragma unroll
-            for (int q = 0; q < kAcc; ++q) s_acc[q][j] = 0.f;
-        }
-        if (__syncthreads_count(kidx >= 0) == 0) break;
+        __syncwarp();
     }
 }
 
+// K10: 16 lanes per voxel, lane m owns SH basis function m, so the SH rows
+// (3(d+1)^2 floats per voxel) are read and written as contiguous runs. The
+// raw colour for the clamp mask (sh.hpp:66-74) is reduced over the 16 lanes;
+// the normal chain (field.hpp:158-170) runs on the first lane.
 __global__ void __launch_bounds__(256) voxel_epilogue_kernel(DevCamera cam, EpilogueArgs a) {
-    const uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (v >= a.n) return;
+    const uint64_t v = uint64_t(blockIdx.x) * 16u + (threadIdx.x >> 4);
+    const int m = threadIdx.x & 15;
+    const bool live = v < a.n;
+    const int4 r = live ? a.rects[v] : make_int4(0, -1, 0, -1);
+    const bool vis = r.y >= r.x;  // in `pre`
+    const int nb = (a.sh_degree + 1) * (a.sh_degree + 1);
     float* gsh = a.g_sh + v * uint64_t(a.sh_stride);
-    const int4 r = a.rects[v];
-    if (r.y < r.x) {  // not in `pre`: no gradient
-        if (!a.accumulate)
-            for (int m = 0; m < a.sh_stride; ++m) gsh[m] = 0.f;
-        return;
-    }
-    const uint64_t path = a.paths[v];
-    double center[3], size;
-    voxel_geometry(path & ((uint64_t(1) << 48) - 1), int(path >> 48), a.bc, a.bsize, center, &size);
-    double dx = dsub(center[0], cam.pos[0]), dy = dsub(center[1], cam.pos[1]),
-           dz = dsub(center[2], cam.pos[2]);
-    double nrm = sqrt(dx * dx + dy * dy + dz * dz);
     float ux = 0.f, uy = 0.f, uz = 0.f;
-    if (nrm > 0.0) {
-        ux = float(dx / nrm);
-        uy = float(dy / nrm);
-        uz = float(dz / nrm);
-    }
-    float b[16];
-    const int nb = sh_basis(a.sh_degree, ux, uy, uz, b);
-    const float* co = a.sh + v * uint64_t(a.sh_stride);
-    float raw[3] = {0.f, 0.f, 0.f};
-    for (int m = 0; m < nb; ++m) {
-        raw[0] += b[m] * co[3 * m + 0];
-        raw[1] += b[m] * co[3 * m + 1];
-        raw[2] += b[m] * co[3 * m + 2];
-    }
-    const float g0 = raw[0] > 0.f ? a.g_color[3 * v + 0] : 0.f;
-    const float g1 = raw[1] > 0.f ? a.g_color[3 * v + 1] : 0.f;
-    const float g2 = raw[2] > 0.f ? a.g_color[3 * v + 2] : 0.f;
-    for (int m = 0; m < nb; ++m) {
-        float o0 = b[m] * g0, o1 = b[m] * g1, o2 = b[m] * g2;
-        if (a.accumulate) {
-            gsh[3 * m + 0] += o0;
-            gsh[3 * m + 1] += o1;
-            gsh[3 * m + 2] += o2;
-        } else {
-            gsh[3 * m + 0] = o0;
-            gsh[3 * m + 1] = o1;
-            gsh[3 * m + 2] = o2;
+    if (vis && m == 0) {
+        const uint64_t path = a.paths[v];
+        double center[3], size;
+        voxel_geometry(path & ((uint64_t(1) << 48) - 1), int(path >> 48), a.bc, a.bsize, center,
+                       &size);
+        const double dx = dsub(center[0], cam.pos[0]), dy = dsub(center[1], cam.pos[1]),
+                     dz = dsub(center[2], cam.pos[2]);
+        const double nrm = sqrt(dx * dx + dy * dy + dz * dz);
+        if (nrm > 0.0) {
+            ux = float(dx / nrm);
+            uy = float(dy / nrm);
+            uz = float(dz / nrm);
         }
     }
+    const int leader = threadIdx.x & 16;  // lane of m == 0 within the warp
+    ux = __shfl_sync(0xffffffffu, ux, leader);
+    uy = __shfl_sync(0xffffffffu, uy, leader);
+    uz = __shfl_sync(0xffffffffu, uz, leader);
+    float b[16];
+    sh_basis(a.sh_degree, ux, uy, uz, b);
+    float bm = 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) bm = (m == i) ? b[i] : bm;
+    const bool mine = vis && m < nb;
+    float c0 = 0.f, c1 = 0.f, c2 = 0.f;
+    if (mine) {
+        const float* co = a.sh + v * uint64_t(a.sh_stride) + 3 * m;
+        c0 = co[0], c1 = co[1], c2 = co[2];
+    }
+    float r0 = bm * c0, r1 = bm * c1, r2 = bm * c2;
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+        r0 += __shfl_xor_sync(0xffffffffu, r0, o);
+        r1 += __shfl_xor_sync(0xffffffffu, r1, o);
+        r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+    }
+    if (!live) return;
+    if (!vis) {  // not in `pre`: no gradient
+        if (!a.accumulate)
+            for (int i = m; i < a.sh_stride; i += 16) gsh[i] = 0.f;
+        return;
+    }
+    const float g0 = r0 > 0.f ? a.g_color[3 * v + 0] : 0.f;
+    const float g1 = r1 > 0.f ? a.g_color[3 * v + 1] : 0.f;
+    const float g2 = r2 > 0.f ? a.g_color[3 * v + 2] : 0.f;
+    if (m < nb) {
+        float* o = gsh + 3 * m;
+        if (a.accumulate) {
+            o[0] += bm * g0;
+            o[1] += bm * g1;
+            o[2] += bm * g2;
+        } else {
+            o[0] = bm * g0;
+            o[1] = bm * g1;
+            o[2] = bm * g2;
+        }
+    }
+    if (m != 0) return;
+    const float dn[3] = {a.g_normal[3 * v], a.g_normal[3 * v + 1], a.g_normal[3 * v + 2]};
+    if (dn[0] == 0.f && dn[1] == 0.f && dn[2] == 0.f) return;
     const float4* rec = a.records + v * kRecordF4;
     const float4 va = rec[2], vb = rec[3];
     const float V[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
-    const float dn[3] = {a.g_normal[3 * v], a.g_normal[3 * v + 1], a.g_normal[3 * v + 2]};
-    if (dn[0] == 0.f && dn[1] == 0.f && dn[2] == 0.f) return;
     float gV[8];
     voxel_normal_backward(V, dn, gV);
     const uint4* ci4 = reinterpret_cast<const uint4*>(a.corner_index + 8 * v);
-    const uint4 c0 = ci4[0], c1 = ci4[1];
-    const uint32_t ci[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    const uint4 q0 = ci4[0], q1 = ci4[1];
+    const uint32_t ci[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
 #pragma unroll
     for (int c = 0; c < 8; ++c) atomicAdd(a.g_density + ci[c], gV[c]);
 }
@@ -349,7 +415,7 @@ void launch_composite_backward(const DevCamera& cam, const BackwardArgs& a, cuda
 
 void launch_voxel_epilogue(const DevCamera& cam, const EpilogueArgs& a, cudaStream_t st) {
     if (a.n == 0) return;
-    voxel_epilogue_kernel<<<blocks_for(a.n, 256), 256, 0, st>>>(cam, a);
+    voxel_epilogue_kernel<<<blocks_for(a.n, 16), 256, 0, st>>>(cam, a);
     SVR_LAUNCH("voxel_epilogue_kernel");
 }
 

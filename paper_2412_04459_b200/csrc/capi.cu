@@ -352,13 +352,21 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
         const char* e = std::getenv("SVR_PACKED_KEYS");
         return e == nullptr || e[0] != '0';
     }();
-    f->packed = packed_enabled && N > 0 && (vb + 3 + 3 * lmax + tile_bits) <= 64;
+    static const bool rank_enabled = [] {
+        const char* e = std::getenv("SVR_RANK_KEYS");
+        return e == nullptr || e[0] != '0';
+    }();
+    // Morton-rank keys: tile | rank(s, vid) | s | vid, sorted on tile|rank only.
+    const int rb = scene->rank_bits;
+    const bool use_rank = rank_enabled && N > 0 && rb > 0 && (vb + 3 + rb + tile_bits) <= 64;
+    f->packed = packed_enabled && N > 0 && (use_rank || (vb + 3 + 3 * lmax + tile_bits) <= 64);
     uint2* ranges = grow<uint2>(f->ranges, ntiles);
     RadixPass passes[kMaxRadixPasses];
     int np = 0;
     if (f->packed) {
-        f->fmt = PackedFormat{vb, lmax, vb + 3 + 3 * lmax};
-        const int lo = vb + (multi ? 0 : 3), hi = f->fmt.tile_shift + tile_bits;
+        f->fmt = use_rank ? PackedFormat{vb, lmax, vb + 3 + rb, rb}
+                          : PackedFormat{vb, lmax, vb + 3 + 3 * lmax, 0};
+        const int lo = vb + ((multi && !use_rank) ? 0 : 3), hi = f->fmt.tile_shift + tile_bits;
         for (int b = lo; b < hi; b += 8) passes[np++] = {0, b, std::min(8, hi - b)};
         RadixPlan plan{};
         plan.n = np;
@@ -369,7 +377,9 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
         ctx->scratch2.reserve(sort_scratch_bytes(E, np));
         mark(ctx, kStageDuplicate);
         launch_duplicate_packed(cam, N, pa.paths, pa.rects, masks, pa.counts, offsets, f->fmt,
-                                f->keys[0].as<uint64_t>(), plan, sort_hist_ptr(ctx->scratch2.p), st);
+                                use_rank ? scene->morton_rank.as<uint32_t>() : nullptr,
+                                f->keys[0].as<uint64_t>(), sat, grow<uint32_t>(f->big, N),
+                                &status->n_big, st);
         if (ctx->debug) {
             grow<uint64_t>(f->dbg_keys, E);
             SVR_CUDA(cudaMemcpyAsync(f->dbg_keys.p, f->keys[0].p, E * 8, cudaMemcpyDeviceToDevice, st));
@@ -440,8 +450,25 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
         ca.max_blend = grow<unsigned int>(f->max_blend, N);
         SVR_CUDA(cudaMemsetAsync(ca.max_blend, 0, N * 4, st));
     }
-    if (f->training) ca.pix_count = grow<uint32_t>(f->pix_count, uint64_t(ntiles) * 256);
-    if (f->training) SVR_CUDA(cudaMemsetAsync(ca.pix_count, 0, uint64_t(ntiles) * 256 * 4, st));
+    const uint64_t nslots = uint64_t(ntiles) * 256;
+    f->staged = false;
+    f->compact_valid = false;
+    if (f->training) {
+        ca.pix_count = grow<uint32_t>(f->pix_count, nslots);
+        SVR_CUDA(cudaMemsetAsync(ca.pix_count, 0, nslots * 4, st));
+        static const bool stage_enabled = [] {
+            const char* e = std::getenv("SVR_STAGED_RECORDS");
+            return e == nullptr || e[0] != '0';
+        }();
+        if (stage_enabled && nslots < (uint64_t(1) << 32) &&
+            uint64_t(f->stage_cap) * nslots < (uint64_t(1) << 32)) {
+            ca.stage_entry = grow<uint32_t>(f->stage_entry, uint64_t(f->stage_cap) * nslots);
+            ca.stage_T = grow<float>(f->stage_T, uint64_t(f->stage_cap) * nslots);
+            ca.stage_cap = f->stage_cap;
+            ca.stage_stride = uint32_t(nslots);
+            ca.overflow = &status->overflow;
+        }
+    }
 
     // K7: composite
     mark(ctx, kStageComposite);
@@ -459,14 +486,23 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
         const uint64_t C = hs->n_contribs;
         require(C < (uint64_t(1) << 32), SVR_ERR_LENGTH, "contribution count exceeds 2^32");
         f->n_contribs = C;
-        CompositeArgs cr = ca;
-        cr.pix_begin = pb;
-        cr.contrib_entry = grow<uint32_t>(f->contrib_entry, C);
-        cr.contrib_T = grow<float>(f->contrib_T, C);
-        cr.max_blend = nullptr;
-        mark(ctx, kStageRecord);
-        launch_composite(cam, cr, true, st);
-        mark(ctx, -1);
+        if (ca.stage_entry && !hs->overflow) {
+            f->staged = true;  // one pass did it; compact lists are built on demand
+        } else {
+            // second pass writes the compact lists directly; a staged frame
+            // that overflowed doubles its capacity for the next render
+            if (ca.stage_entry) f->stage_cap = std::min<uint32_t>(f->stage_cap * 2, 4096);
+            CompositeArgs cr = ca;
+            cr.pix_begin = pb;
+            cr.contrib_entry = grow<uint32_t>(f->contrib_entry, C);
+            cr.contrib_T = grow<float>(f->contrib_T, C);
+            cr.max_blend = nullptr;
+            cr.stage_entry = nullptr;
+            mark(ctx, kStageRecord);
+            launch_composite(cam, cr, true, st);
+            mark(ctx, -1);
+            f->compact_valid = true;
+        }
         f->has_records = true;
     }
 
@@ -483,6 +519,17 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     (void)nss;
     mark(ctx, -1);
     f->n_visible = ~uint64_t(0);  // computed lazily
+}
+
+// Compact (reference-order) contribution lists for the host-facing records.
+void ensure_compact(svr_frame* f) {
+    if (!f->has_records || f->compact_valid) return;
+    const uint64_t nslots = uint64_t(f->ntx) * f->nty * 256;
+    launch_compact_contribs(f->pix_count.as<uint32_t>(), f->pix_begin.as<uint32_t>(),
+                            f->stage_entry.as<uint32_t>(), f->stage_T.as<float>(),
+                            uint32_t(nslots), grow<uint32_t>(f->contrib_entry, f->n_contribs),
+                            grow<float>(f->contrib_T, f->n_contribs), f->ctx->stream);
+    f->compact_valid = true;
 }
 
 uint64_t count_visible(svr_frame* f) {
@@ -530,8 +577,8 @@ BufView frame_buffer(svr_frame* f, svr_buffer which) {
             if (f->packed) {
                 uint64_t* k = grow<uint64_t>(f->ref_keys, f->n_entries);
                 uint32_t* v = grow<uint32_t>(f->ref_vals, f->n_entries);
-                launch_unpack_entries(f->keys[f->sorted_buf].as<uint64_t>(), f->n_entries, f->fmt, k,
-                                      v, f->ctx->stream);
+                launch_unpack_entries(f->keys[f->sorted_buf].as<uint64_t>(), f->n_entries, f->fmt,
+                                      f->scene->paths.as<uint64_t>(), k, v, f->ctx->stream);
                 return which == SVR_BUF_SORT_KEYS ? BufView{k, f->n_entries * 8}
                                                   : BufView{v, f->n_entries * 4};
             }
@@ -549,8 +596,8 @@ BufView frame_buffer(svr_frame* f, svr_buffer which) {
             if (f->packed) {
                 uint64_t* k = grow<uint64_t>(f->ref_keys, f->n_entries);
                 uint32_t* v = grow<uint32_t>(f->ref_vals, f->n_entries);
-                launch_unpack_entries(f->dbg_keys.as<uint64_t>(), f->n_entries, f->fmt, k, v,
-                                      f->ctx->stream);
+                launch_unpack_entries(f->dbg_keys.as<uint64_t>(), f->n_entries, f->fmt,
+                                      f->scene->paths.as<uint64_t>(), k, v, f->ctx->stream);
                 return which == SVR_BUF_ENTRIES_KEYS ? BufView{k, f->n_entries * 8}
                                                      : BufView{v, f->n_entries * 4};
             }
@@ -653,6 +700,7 @@ void backward_impl(svr_ctx* ctx, const svr_scene* scene, svr_frame* f, const svr
 
     BackwardArgs ba{};
     ba.ranges = f->ranges.as<uint2>();
+    ba.tile_order = f->tile_order.as<uint32_t>();
     ba.vals = f->vals[f->vals_buf].as<uint32_t>();
     ba.records = f->records.as<float4>();
     ba.corner_index = scene->corner_index.as<uint32_t>();
@@ -666,8 +714,9 @@ void backward_impl(svr_ctx* ctx, const svr_scene* scene, svr_frame* f, const svr
     ba.d_voxel_color = dev_in[5];
     ba.pix_count = f->pix_count.as<uint32_t>();
     ba.pix_begin = f->pix_begin.as<uint32_t>();
-    ba.contrib_entry = f->contrib_entry.as<uint32_t>();
-    ba.contrib_T = f->contrib_T.as<float>();
+    ba.contrib_entry = f->staged ? f->stage_entry.as<uint32_t>() : f->contrib_entry.as<uint32_t>();
+    ba.contrib_T = f->staged ? f->stage_T.as<float>() : f->contrib_T.as<float>();
+    ba.stage_stride = f->staged ? uint32_t(uint64_t(f->ntx) * f->nty * 256) : 0u;
     ba.g_density = gd;
     ba.g_color = gcol;
     ba.g_normal = gnor;
@@ -807,6 +856,16 @@ int svr_scene_upload(svr_ctx* ctx, const svr_scene_desc* d, svr_scene** out) {
             }
             if (d->n_pool)
                 SVR_CUDA(cudaMemcpy(s->density.p, d->density, d->n_pool * 4, cudaMemcpyHostToDevice));
+            // Morton rank table for the sort keys (needs 8N < 2^32).
+            if (N > 0 && N < (uint64_t(1) << 28)) {
+                s->morton_rank.reserve(N * 8 * 4);
+                DevBuf tmp;
+                tmp.reserve(morton_rank_scratch_bytes(N, max_level));
+                build_morton_rank(s->paths.as<uint64_t>(), N, max_level,
+                                  s->morton_rank.as<uint32_t>(), tmp.p, ctx->stream);
+                SVR_CUDA(cudaStreamSynchronize(ctx->stream));
+                s->rank_bits = bit_width(8 * N - 1);
+            }
         } catch (...) {
             delete s;
             throw;
@@ -910,6 +969,7 @@ int svr_frame_records(svr_frame* f, uint32_t* pre_vids, uint64_t n_pre, uint32_t
         require(f && f->has_records, SVR_ERR_RUNTIME, "frame has no forward records");
         set_device(f->ctx);
         cudaStream_t st = f->ctx->stream;
+        ensure_compact(f);
         uint64_t nv = count_visible(f);
         require(n_pre == nv, SVR_ERR_INVALID_ARGUMENT, "pre size mismatch");
         require(n_contribs == f->n_contribs, SVR_ERR_INVALID_ARGUMENT, "contrib size mismatch");

@@ -308,33 +308,104 @@ __global__ void entry_counts_kernel(DevCamera cam, uint64_t n, const int4* rects
 // (the dropped order bits are the sign pattern repeated, raster.cpp:165,
 // octree.hpp:99-101). The kernel also accumulates the radix-sort digit
 // histograms of every pass, so the sort needs no separate histogram read.
+__device__ __forceinline__ uint64_t packed_key(PackedFormat fmt, const uint32_t* __restrict__ rank,
+                                               uint64_t n, uint64_t v, uint64_t code, uint64_t tid,
+                                               uint32_t sgn) {
+    const uint64_t order = fmt.rank_bits
+                               ? uint64_t(__ldg(rank + sgn * n + v))
+                               : (code ^ (uint64_t(sgn) * kGroupOnes)) >> (48 - 3 * fmt.lmax);
+    return (tid << fmt.tile_shift) | (order << (fmt.vb + 3)) | (uint64_t(sgn) << fmt.vb) | v;
+}
+
+// Voxels with more than this many entries (large or near-plane footprints,
+// which get the whole screen) are emitted by duplicate_big_kernel.
+constexpr uint32_t kBigEntries = 128;
+
 __global__ void __launch_bounds__(256) duplicate_packed_kernel(
     DevCamera cam, uint64_t n, const uint64_t* __restrict__ paths, const int4* __restrict__ rects,
     const uint8_t* __restrict__ masks, const uint32_t* __restrict__ counts,
-    const uint32_t* __restrict__ offsets, PackedFormat fmt, uint64_t* __restrict__ keys,
-    RadixPlan plan, uint32_t* hist) {
-    (void)plan;
-    (void)hist;
+    const uint32_t* __restrict__ offsets, PackedFormat fmt, const uint32_t* __restrict__ rank,
+    uint64_t* __restrict__ keys, uint32_t* big, unsigned int* n_big) {
     const uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (v < n && counts[v] != 0) {
+    if (v >= n) return;
+    const uint32_t cnt = counts[v];
+    if (cnt == 0) return;
+    if (cnt > kBigEntries) {
+        big[atomicAdd(n_big, 1u)] = uint32_t(v);
+        return;
+    }
+    const uint64_t code = paths[v] & kCodeMask48;
+    const int4 r = rects[v];
+    uint32_t o = offsets[v];
+    for (int ty = r.z; ty <= r.w; ++ty)
+        for (int tx = r.x; tx <= r.y; ++tx) {
+            const uint64_t tid = uint64_t(ty) * cam.ntx + tx;
+            uint32_t m = masks[tid];
+            while (m) {
+                const uint32_t sgn = __ffs(m) - 1;
+                m &= m - 1;
+                keys[o++] = packed_key(fmt, rank, n, v, code, tid, sgn);
+            }
+        }
+}
+
+// One CTA per large voxel (grid-stride over the list): warp w emits rows
+// ty0 + w, ty0 + w + 8, ...; a row starts at the voxel's offset plus the
+// SAT count of the rect rows above it, and lanes place their tile's
+// patterns by a warp prefix sum, so the reference emission order
+// (vid, ty, tx, s) is kept exactly.
+__global__ void __launch_bounds__(256) duplicate_big_kernel(
+    DevCamera cam, uint64_t n, const uint64_t* __restrict__ paths, const int4* __restrict__ rects,
+    const uint8_t* __restrict__ masks, const uint32_t* __restrict__ offsets,
+    const uint32_t* __restrict__ tile_sat, PackedFormat fmt, const uint32_t* __restrict__ rank,
+    uint64_t* __restrict__ keys, const uint32_t* __restrict__ big,
+    const unsigned int* __restrict__ n_big) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t nb = *n_big;
+    for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
+        const uint64_t v = big[b];
         const uint64_t code = paths[v] & kCodeMask48;
-        const int obits = 3 * fmt.lmax;
         const int4 r = rects[v];
-        uint32_t o = offsets[v];
-        for (int ty = r.z; ty <= r.w; ++ty)
-            for (int tx = r.x; tx <= r.y; ++tx) {
+        const uint32_t o0 = offsets[v];
+        for (int ty = r.z + warp; ty <= r.w; ty += 8) {
+            uint32_t o = o0 + (ty > r.z ? sat_rect(tile_sat, cam.ntx, r.x, r.y, r.z, ty - 1) : 0u);
+            for (int tx0 = r.x; tx0 <= r.y; tx0 += 32) {
+                const int tx = tx0 + lane;
                 const uint64_t tid = uint64_t(ty) * cam.ntx + tx;
-                uint32_t m = masks[tid];
+                uint32_t m = tx <= r.y ? uint32_t(masks[tid]) : 0u;
+                const uint32_t c = __popc(m);
+                uint32_t incl = c;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+                    if (lane >= d) incl += y;
+                }
+                uint32_t at = o + incl - c;
                 while (m) {
                     const uint32_t sgn = __ffs(m) - 1;
                     m &= m - 1;
-                    const uint64_t order = (code ^ (uint64_t(sgn) * kGroupOnes)) >> (48 - obits);
-                    const uint64_t key = (tid << fmt.tile_shift) | (order << (fmt.vb + 3)) |
-                                         (uint64_t(sgn) << fmt.vb) | v;
-                    keys[o++] = key;
+                    keys[at++] = packed_key(fmt, rank, n, v, code, tid, sgn);
                 }
+                o += __shfl_sync(0xffffffffu, incl, 31);
             }
+        }
     }
+}
+
+__global__ void rank_keys_kernel(const uint64_t* __restrict__ paths, uint64_t n, uint64_t* keys,
+                                 uint32_t* vals) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= 8 * n) return;
+    const uint64_t s = i / n, v = i - s * n;
+    keys[i] = (paths[v] & kCodeMask48) ^ (s * kGroupOnes);
+    vals[i] = uint32_t(s << 29) | uint32_t(v);
+}
+
+__global__ void rank_scatter_kernel(const uint32_t* __restrict__ vals, uint64_t n, uint32_t* rank) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= 8 * n) return;
+    const uint32_t val = vals[i];
+    rank[uint64_t(val >> 29) * n + (val & ((1u << 29) - 1u))] = uint32_t(i);
 }
 
 __global__ void tile_ranges_packed_kernel(const uint64_t* __restrict__ keys, uint64_t n,
@@ -349,18 +420,22 @@ __global__ void tile_ranges_packed_kernel(const uint64_t* __restrict__ keys, uin
 }
 
 __global__ void unpack_entries_kernel(const uint64_t* packed, uint64_t n, PackedFormat fmt,
-                                      uint64_t* keys, uint32_t* vals) {
+                                      const uint64_t* paths, uint64_t* keys, uint32_t* vals) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint64_t k = packed[i];
-    const int obits = 3 * fmt.lmax;
     const uint64_t vid = k & ((uint64_t(1) << fmt.vb) - 1);
     const uint64_t sgn = (k >> fmt.vb) & 7u;
-    const uint64_t otop = (k >> (fmt.vb + 3)) & ((uint64_t(1) << obits) - 1);
     const uint64_t tid = k >> fmt.tile_shift;
+    vals[i] = uint32_t(sgn << 29) | uint32_t(vid);
+    if (fmt.rank_bits) {
+        keys[i] = (tid << 48) | ((paths[vid] & kCodeMask48) ^ (sgn * kGroupOnes));
+        return;
+    }
+    const int obits = 3 * fmt.lmax;
+    const uint64_t otop = (k >> (fmt.vb + 3)) & ((uint64_t(1) << obits) - 1);
     const uint64_t low = obits < 48 ? ((sgn * kGroupOnes) & ((uint64_t(1) << (48 - obits)) - 1)) : 0;
     keys[i] = (tid << 48) | (obits > 0 ? (otop << (48 - obits)) : 0) | low;
-    vals[i] = uint32_t(sgn << 29) | uint32_t(vid);
 }
 
 // ------------------------------------------------------------------- K6
@@ -448,6 +523,13 @@ __global__ void __launch_bounds__(256) composite_kernel(DevCamera cam, Composite
     const float ix = 1.0f / dx, iy = 1.0f / dy, iz = 1.0f / dz;
     const float dnorm = float(sqrt(dd[0] * dd[0] + dd[1] * dd[1] + dd[2] * dd[2]));
     const float pcx = float(px) + 0.5f, pcy = float(py) + 0.5f;
+    // Frustum of this warp's 8x4 block (warp_cone_planes): skips boxes whose
+    // screen AABB is loose, e.g. near-plane voxels, which get the full screen
+    // (raster.cpp:95-101), without changing the composited set.
+    __shared__ float s_cone[8][4][3];
+    float (*cone)[3] = s_cone[warp];
+    if (lane == 0) warp_cone_planes(cam, wx0, wy0, cone);
+    __syncwarp();
 
     float T = 1.0f, cr = 0.f, cg = 0.f, cb = 0.f, nx = 0.f, ny = 0.f, nz = 0.f, depth = 0.f;
     float median = -1.0f;
@@ -480,8 +562,12 @@ __global__ void __launch_bounds__(256) composite_kernel(DevCamera cam, Composite
         if (c + 64 + lane < range.y) v2 = __ldg(a.vals + c + 64 + lane);
 
         const bool valid = c + lane < range.y;
-        const bool rel = valid && ((warp_signs >> (v0 >> 29)) & 1u) &&
-                         !(fx1 < b0.x || fx0 > b0.y || fy1 < b0.z || fy0 > b0.w);
+        bool rel = valid && ((warp_signs >> (v0 >> 29)) & 1u) &&
+                   !(fx1 < b0.x || fx0 > b0.y || fy1 < b0.z || fy0 > b0.w);
+        // frustum test only for entries with a large screen AABB
+        const bool wide = rel && (b0.y - b0.x) * (b0.w - b0.z) > kConeMinArea;
+        if (__any_sync(0xffffffffu, wide) && wide)
+            rel = box_in_cone(cone, __ldg(a.records + uint64_t(v0 & kVidMask) * kRecordF4));
         const uint32_t m = __ballot_sync(0xffffffffu, rel);
         const int nrel = __popc(m);
         if (rel) wvid[__popc(m & ((1u << lane) - 1u))] = v0;
@@ -537,9 +623,9 @@ __global__ void __launch_bounds__(256) composite_kernel(DevCamera cam, Composite
                     const float qz = (tk[u][k] * dz - lo.z) * inv;
                     const float act = explin(trilinear(V, qx, qy, qz));
                     sum += act;
-                    sa[u][k] = 1.0f - fexp(-lk * act);
+                    sa[u][k] = one_minus_exp_neg(lk * act);
                 }
-                alpha[u] = (K == 1) ? sa[u][0] : 1.0f - fexp(-lk * sum);
+                alpha[u] = (K == 1) ? sa[u][0] : one_minus_exp_neg(lk * sum);
                 // voxel_depth (field.hpp:173-181)
                 float dv = 0.f, Tk = 1.f;
 #pragma unroll
@@ -575,6 +661,15 @@ __global__ void __launch_bounds__(256) composite_kernel(DevCamera cam, Composite
                     nz += w * nor.z;
                     depth += T * dvox[u];
                     if (a.max_blend) atomicMax(a.max_blend + __float_as_uint(col.w), __float_as_uint(w));
+                    if (a.stage_entry) {
+                        if (cnt < a.stage_cap) {
+                            const uint32_t at = cnt * a.stage_stride + slot;
+                            a.stage_entry[at] = c + uint32_t(u == 0 ? ja : jb);
+                            a.stage_T[at] = T;
+                        } else {
+                            *a.overflow = 1u;
+                        }
+                    }
                 } else {
                     a.contrib_entry[rec_base + cnt] = c + uint32_t(u == 0 ? ja : jb);
                     a.contrib_T[rec_base + cnt] = T;
@@ -607,6 +702,20 @@ __global__ void __launch_bounds__(256) composite_kernel(DevCamera cam, Composite
     a.median[p] = median;
     a.tfin[p] = T;
     if (a.pix_count) a.pix_count[slot] = cnt;
+}
+
+__global__ void compact_contribs_kernel(const uint32_t* __restrict__ pix_count,
+                                        const uint32_t* __restrict__ pix_begin,
+                                        const uint32_t* __restrict__ stage_entry,
+                                        const float* __restrict__ stage_T, uint32_t stride,
+                                        uint32_t* contrib_entry, float* contrib_T) {
+    const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
+    if (slot >= stride) return;
+    const uint32_t n = pix_count[slot], b = pix_begin[slot];
+    for (uint32_t k = 0; k < n; ++k) {
+        contrib_entry[b + k] = stage_entry[uint64_t(k) * stride + slot];
+        contrib_T[b + k] = stage_T[uint64_t(k) * stride + slot];
+    }
 }
 
 // ------------------------------------------------------------------- K8
@@ -762,12 +871,47 @@ void launch_entry_counts(const DevCamera& cam, uint64_t n, const int4* rects,
 
 void launch_duplicate_packed(const DevCamera& cam, uint64_t n, const uint64_t* paths,
                              const int4* rects, const uint8_t* masks, const uint32_t* counts,
-                             const uint32_t* offsets, PackedFormat fmt, uint64_t* keys,
-                             const RadixPlan& plan, uint32_t* hist, cudaStream_t st) {
+                             const uint32_t* offsets, PackedFormat fmt, const uint32_t* rank,
+                             uint64_t* keys, const uint32_t* tile_sat, uint32_t* big,
+                             unsigned int* n_big, cudaStream_t st) {
     if (n == 0) return;
     duplicate_packed_kernel<<<blocks_for(n, 256), 256, 0, st>>>(cam, n, paths, rects, masks, counts,
-                                                                offsets, fmt, keys, plan, hist);
+                                                                offsets, fmt, rank, keys, big, n_big);
     SVR_LAUNCH("duplicate_packed_kernel");
+    duplicate_big_kernel<<<148 * 4, 256, 0, st>>>(cam, n, paths, rects, masks, offsets, tile_sat,
+                                                   fmt, rank, keys, big, n_big);
+    SVR_LAUNCH("duplicate_big_kernel");
+}
+
+size_t morton_rank_scratch_bytes(uint64_t n, int lmax) {
+    const uint64_t m = 8 * n;
+    const int npass = (3 * lmax + 7) / 8;
+    return 2 * m * 8 + 2 * m * 4 + 256 + sort_scratch_bytes(m, npass);
+}
+
+void build_morton_rank(const uint64_t* paths, uint64_t n, int lmax, uint32_t* rank, void* scratch,
+                       cudaStream_t st) {
+    if (n == 0) return;
+    const uint64_t m = 8 * n;
+    char* p = static_cast<char*>(scratch);
+    uint64_t* k0 = reinterpret_cast<uint64_t*>(p);
+    uint64_t* k1 = k0 + m;
+    uint32_t* v0 = reinterpret_cast<uint32_t*>(k1 + m);
+    uint32_t* v1 = v0 + m;
+    void* sort_scratch = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(v1 + m) + 255) &
+                                                 ~uintptr_t(255));
+    rank_keys_kernel<<<blocks_for(m, 256), 256, 0, st>>>(paths, n, k0, v0);
+    SVR_LAUNCH("rank_keys_kernel");
+    // (code ^ s*G) differs only in bits [48 - 3*lmax, 48); the pairs are
+    // generated in ascending value order, so the stable sort breaks key ties
+    // by value exactly as std::sort on (key, value) does.
+    RadixPass passes[kMaxRadixPasses];
+    int np = 0;
+    for (int b = 48 - 3 * lmax; b < 48; b += 8) passes[np++] = {0, b, std::min(8, 48 - b)};
+    int out = 0;
+    if (np > 0) out = radix_sort_pairs(k0, v0, k1, v1, m, passes, np, sort_scratch, st);
+    rank_scatter_kernel<<<blocks_for(m, 256), 256, 0, st>>>(out ? v1 : v0, n, rank);
+    SVR_LAUNCH("rank_scatter_kernel");
 }
 
 void launch_tile_ranges_packed(const uint64_t* keys, uint64_t n, PackedFormat fmt, uint2* ranges,
@@ -778,10 +922,10 @@ void launch_tile_ranges_packed(const uint64_t* keys, uint64_t n, PackedFormat fm
     SVR_LAUNCH("tile_ranges_packed_kernel");
 }
 
-void launch_unpack_entries(const uint64_t* packed, uint64_t n, PackedFormat fmt, uint64_t* keys,
-                           uint32_t* vals, cudaStream_t st) {
+void launch_unpack_entries(const uint64_t* packed, uint64_t n, PackedFormat fmt,
+                           const uint64_t* paths, uint64_t* keys, uint32_t* vals, cudaStream_t st) {
     if (n == 0) return;
-    unpack_entries_kernel<<<blocks_for(n, 256), 256, 0, st>>>(packed, n, fmt, keys, vals);
+    unpack_entries_kernel<<<blocks_for(n, 256), 256, 0, st>>>(packed, n, fmt, paths, keys, vals);
     SVR_LAUNCH("unpack_entries_kernel");
 }
 
@@ -791,6 +935,15 @@ void launch_tile_ranges(const uint64_t* keys, uint64_t n, uint2* ranges, int nti
     if (n == 0) return;
     tile_ranges_kernel<<<blocks_for(n, 256), 256, 0, st>>>(keys, n, ranges);
     SVR_LAUNCH("tile_ranges_kernel");
+}
+
+void launch_compact_contribs(const uint32_t* pix_count, const uint32_t* pix_begin,
+                             const uint32_t* stage_entry, const float* stage_T, uint32_t stride,
+                             uint32_t* contrib_entry, float* contrib_T, cudaStream_t st) {
+    if (stride == 0) return;
+    compact_contribs_kernel<<<blocks_for(stride, 256), 256, 0, st>>>(
+        pix_count, pix_begin, stage_entry, stage_T, stride, contrib_entry, contrib_T);
+    SVR_LAUNCH("compact_contribs_kernel");
 }
 
 void launch_tile_order(const uint2* ranges, int ntiles, uint32_t* order, cudaStream_t st) {

@@ -91,6 +91,8 @@ struct svr_scene {
     svrb::DevBuf corner_index;  // u32 [n][8]
     svrb::DevBuf density;       // f32 [n_pool]
     svrb::DevBuf sh;            // f32 [n][stride]
+    svrb::DevBuf morton_rank;   // u32 [8][n]: build_morton_rank (sort keys)
+    int rank_bits = 0;          // bit width of 8n-1; 0 = no table
 };
 
 // Per-view state. Also the device half of svr::ForwardRecords.
@@ -108,10 +110,14 @@ struct svr_frame {
     bool has_records = false;
 
     svrb::DevBuf tile_masks, tile_sat, rects, aabb, records, counts, offsets, visible_rank;
-    svrb::DevBuf keys[2], vals[2], dbg_keys, dbg_vals, ranges, tile_order;
+    svrb::DevBuf keys[2], vals[2], dbg_keys, dbg_vals, ranges, tile_order, big;
     svrb::DevBuf out_color, out_depth, out_median, out_normal, out_tfin, max_blend;
     svrb::DevBuf ss_color, ss_depth, ss_median, ss_normal, ss_tfin;
     svrb::DevBuf pix_count, pix_begin, contrib_entry, contrib_T;
+    svrb::DevBuf stage_entry, stage_T;  // single-pass training records
+    uint32_t stage_cap = 64;            // per-pixel capacity, doubles on overflow
+    bool staged = false;                // records live in stage_* ...
+    bool compact_valid = false;         // ... and contrib_* is (not yet) built
     svrb::DevBuf taps;  // resampler tables
     svrb::DevBuf bwd_gc, bwd_gn, bwd_lift, bwd_dcolor, status, l1_grad;
     int sorted_buf = 0;  // which of keys[]/vals[] holds the sorted list

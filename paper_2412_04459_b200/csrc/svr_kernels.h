@@ -46,8 +46,10 @@ int radix_sort_keys(uint64_t* keys0, uint64_t* keys1, uint64_t n, const RadixPas
 struct FrameStatus {          // device -> host summary, one read per frame
     unsigned long long n_entries;
     unsigned int pattern_or;  // OR of all tile sign masks
-    unsigned int pad;
+    unsigned int overflow;    // a pixel exceeded the staged-record capacity
     unsigned long long n_contribs;
+    unsigned int n_big;       // voxels handed to the cooperative duplicate
+    unsigned int pad;
 };
 
 void launch_tile_setup(const DevCamera& cam, uint8_t* masks, uint32_t* sat, FrameStatus* status,
@@ -84,19 +86,28 @@ void launch_tile_ranges(const uint64_t* keys, uint64_t n, uint2* ranges, int nti
 struct PackedFormat {
     int vb;          // voxel-id bits
     int lmax;        // finest occupied octree level
-    int tile_shift;  // vb + 3 + 3*lmax
+    int tile_shift;  // vb + 3 + order bits
+    int rank_bits;   // >0: order = Morton rank of (s, vid) (scene table); 0: code ^ s*G bits
 };
 void launch_duplicate_packed(const DevCamera& cam, uint64_t n, const uint64_t* paths,
                              const int4* rects, const uint8_t* masks, const uint32_t* counts,
-                             const uint32_t* offsets, PackedFormat fmt, uint64_t* keys,
-                             const RadixPlan& plan, uint32_t* hist, cudaStream_t st);
+                             const uint32_t* offsets, PackedFormat fmt, const uint32_t* rank,
+                             uint64_t* keys, const uint32_t* tile_sat, uint32_t* big,
+                             unsigned int* n_big, cudaStream_t st);
+// Direction-aware Morton rank table of a scene: rank[s*n + vid] = position of
+// (code_vid ^ s*kGroupOnes, s << 29 | vid) in the ascending order of all 8n
+// such pairs, i.e. the reference's within-tile (key, value) order
+// (raster.cpp:163-177) as one dense integer. Camera independent.
+size_t morton_rank_scratch_bytes(uint64_t n, int lmax);
+void build_morton_rank(const uint64_t* paths, uint64_t n, int lmax, uint32_t* rank, void* scratch,
+                       cudaStream_t st);
 // Tile ranges from packed sorted keys; also writes the reference value
 // (s << 29 | vid) per entry for the compositing kernels.
 void launch_tile_ranges_packed(const uint64_t* keys, uint64_t n, PackedFormat fmt, uint2* ranges,
                                uint32_t* vals, int ntiles, cudaStream_t st);
 // Reference SortEntry (key, value) from packed keys (parity dumps).
-void launch_unpack_entries(const uint64_t* packed, uint64_t n, PackedFormat fmt, uint64_t* keys,
-                           uint32_t* vals, cudaStream_t st);
+void launch_unpack_entries(const uint64_t* packed, uint64_t n, PackedFormat fmt,
+                           const uint64_t* paths, uint64_t* keys, uint32_t* vals, cudaStream_t st);
 
 struct CompositeArgs {
     const uint2* ranges;
@@ -118,7 +129,17 @@ struct CompositeArgs {
     const uint32_t* pix_begin;  // tile-major
     uint32_t* contrib_entry;
     float* contrib_T;
+    // single-pass training records: contribution k of pixel slot s goes to
+    // stage_*[k * stage_stride + s] while k < stage_cap, else *overflow = 1
+    uint32_t* stage_entry;
+    float* stage_T;
+    uint32_t stage_cap, stage_stride;
+    unsigned int* overflow;
 };
+// Staged -> compact (reference order) contribution records.
+void launch_compact_contribs(const uint32_t* pix_count, const uint32_t* pix_begin,
+                             const uint32_t* stage_entry, const float* stage_T, uint32_t stride,
+                             uint32_t* contrib_entry, float* contrib_T, cudaStream_t st);
 void launch_composite(const DevCamera& cam, const CompositeArgs& a, bool record_pass,
                       cudaStream_t st);
 void launch_tile_order(const uint2* ranges, int ntiles, uint32_t* order, cudaStream_t st);
@@ -160,6 +181,7 @@ void launch_l1_loss(const float* color, const float* gt, uint64_t n, float* d_co
 
 struct BackwardArgs {
     const uint2* ranges;
+    const uint32_t* tile_order;  // optional LPT tile schedule (forward's)
     const uint32_t* vals;
     const float4* records;
     const uint32_t* corner_index;
@@ -173,8 +195,9 @@ struct BackwardArgs {
     const float* d_voxel_color;  // per contrib x3, optional
     const uint32_t* pix_count;   // tile-major
     const uint32_t* pix_begin;
-    const uint32_t* contrib_entry;
+    const uint32_t* contrib_entry;  // compact, or staged when stage_stride > 0
     const float* contrib_T;
+    uint32_t stage_stride;
     float* g_density;
     float* g_color;   // per voxel x3 (scratch)
     float* g_normal;  // per voxel x3 (scratch)

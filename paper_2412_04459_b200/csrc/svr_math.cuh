@@ -74,6 +74,39 @@ SVR_HD void pixel_ray_dir(const DevCamera& c, double px, double py, double* d) {
     mat_vec(c.rot, cxd, cyd, 1.0, d);
 }
 
+// Side planes of the view frustum through an 8x4 pixel block whose first
+// pixel is (wx0, wy0), widened by one pixel on every side: camera-frame
+// half-spaces x/z >= a, x/z <= b, y/z >= c, y/z <= d with inward normals
+// (1,0,-a), (-1,0,b), (0,1,-c), (0,-1,d), rotated to world (n_w = rot n_c).
+SVR_HD void warp_cone_planes(const DevCamera& cam, int wx0, int wy0, float (*cone)[3]) {
+    const double a_ = (double(wx0) - 0.5 - cam.cx) / cam.fx, b_ = (double(wx0) + 8.5 - cam.cx) / cam.fx;
+    const double c_ = (double(wy0) - 0.5 - cam.cy) / cam.fy, d_ = (double(wy0) + 4.5 - cam.cy) / cam.fy;
+    const double nc[4][3] = {{1.0, 0.0, -a_}, {-1.0, 0.0, b_}, {0.0, 1.0, -c_}, {0.0, -1.0, d_}};
+    for (int q = 0; q < 4; ++q)
+        for (int r = 0; r < 3; ++r)
+            cone[q][r] = float(cam.rot[3 * r + 0] * nc[q][0] + cam.rot[3 * r + 1] * nc[q][1] +
+                               cam.rot[3 * r + 2] * nc[q][2]);
+}
+
+// False iff the camera-relative box [lo.xyz, lo.xyz + lo.w] lies strictly
+// outside one of the planes: then no pixel ray of the block can hit it and
+// the per-pixel slab test would reject it, so skipping it changes nothing.
+// The one-pixel widening dwarfs the fp32 rounding of this test.
+SVR_HD bool box_in_cone(const float (*cone)[3], float4 lo) {
+    const float eps = 1e-5f * (fabsf(lo.x) + fabsf(lo.y) + fabsf(lo.z) + lo.w);
+    bool in = true;
+    for (int q = 0; q < 4; ++q) {
+        const float vmax = cone[q][0] * lo.x + cone[q][1] * lo.y + cone[q][2] * lo.z +
+                           lo.w * (fmaxf(cone[q][0], 0.f) + fmaxf(cone[q][1], 0.f) +
+                                   fmaxf(cone[q][2], 0.f));
+        if (vmax < -eps) in = false;
+    }
+    return in;
+}
+
+// Frustum culling pays only for entries whose screen AABB is loose.
+constexpr float kConeMinArea = 64.0f * 64.0f;  // px^2
+
 // ray_sign_bits (octree.hpp:93-95): bit2 = x<0, bit1 = y<0, bit0 = z<0.
 SVR_HD uint32_t sign_bits(const double* d) {
     return 4u * (d[0] < 0.0) + 2u * (d[1] < 0.0) + 1u * (d[2] < 0.0);
@@ -203,6 +236,18 @@ __device__ __forceinline__ float fexp(float x) {
 #else
 inline float fexp(float x) { return expf(x); }
 #endif
+// alpha = 1 - exp(-x) for x >= 0 (voxel_alpha, field.hpp:92-116). For
+// x < 1/32 the difference 1 - exp(-x) would keep only the absolute accuracy
+// of exp near 1 (~1e-7), i.e. a large relative error in a small alpha, and
+// that error adds up over the hundreds of faint voxels a ray can cross
+// (depth = sum T alpha t grows with t). There the series
+// x - x^2/2 + x^3/6 - x^4/24 is used (truncation < x^5/120).
+SVR_HD float one_minus_exp_neg(float x) {
+    const float big = 1.0f - fexp(-x);
+    const float small = x * (1.0f - x * (0.5f - x * (1.0f / 6.0f - x * (1.0f / 24.0f))));
+    return x < 0.03125f ? small : big;
+}
+
 // exp(x/1.1 - 1 + ln 1.1) = exp(x/1.1) * (1.1/e); branch-free select
 constexpr float kExplinScale = 0.40467196f;  // 1.1 / e
 SVR_HD float explin(float x) {
