@@ -159,6 +159,15 @@ int svr_render(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam,
 int svr_frame_get_info(svr_frame* frame, svr_frame_info* out);
 /* Copies a buffer to host memory (synchronous). bytes must match. */
 int svr_frame_download(svr_frame* frame, svr_buffer which, void* dst, size_t bytes);
+/* Pipelined variant for serving loops: enqueues the copy on the context's
+ * copy stream behind the frame's pending work and returns at once. dst
+ * (pinned host memory for a truly asynchronous copy) is complete after
+ * svr_frame_wait(frame). A later render, backward or download through the
+ * same frame waits for the copy on the device, so a caller alternating two
+ * frames overlaps frame i's read-back with frame i+1's rendering. */
+int svr_frame_download_async(svr_frame* frame, svr_buffer which, void* dst, size_t bytes);
+/* Blocks until the frame's asynchronous downloads have landed. */
+int svr_frame_wait(svr_frame* frame);
 /* Device pointer + size of a buffer (no copy, valid until the next render). */
 int svr_frame_device_ptr(svr_frame* frame, svr_buffer which, void** ptr, size_t* bytes);
 

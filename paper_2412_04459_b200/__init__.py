@@ -109,7 +109,8 @@ EXPORTS = [
     "svr_ctx_synchronize", "svr_ctx_set_debug", "svr_scene_upload", "svr_scene_set_params",
     "svr_scene_destroy", "svr_scene_param_ptrs", "svr_frame_create", "svr_frame_destroy",
     "svr_render", "svr_frame_get_info", "svr_frame_download", "svr_frame_device_ptr",
-    "svr_frame_records", "svr_render_backward", "svr_l1_loss", "svr_train_step_l1",
+    "svr_frame_download_async", "svr_frame_wait", "svr_frame_records", "svr_render_backward",
+    "svr_l1_loss", "svr_train_step_l1",
     "svr_project_voxels", "svr_tile_sign_masks", "svr_build_sort_entries", "svr_sort_entries",
     "svr_synth_random_scene", "svr_ring_camera", "svr_free", "svr_launch_count",
     "svr_ctx_enable_timing", "svr_ctx_stage_times", "svr_frame_pre", "svr_render_oracle",
@@ -145,6 +146,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "svr_scene_param_ptrs": (C.c_int, [P, C.POINTER(P), C.POINTER(P),
                                            C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         "svr_frame_create": (C.c_int, [P, C.POINTER(P)]),
+        "svr_frame_download_async": (C.c_int, [P, C.c_int, P, C.c_size_t]),
+        "svr_frame_wait": (C.c_int, [P]),
         "svr_frame_destroy": (C.c_int, [P]),
         "svr_render": (C.c_int, [P, P, C.POINTER(svr_camera), C.POINTER(svr_render_options), P]),
         "svr_frame_get_info": (C.c_int, [P, C.POINTER(svr_frame_info)]),
@@ -461,6 +464,19 @@ class Frame:
         out = np.empty(nbytes // np.dtype(dtype).itemsize, dtype=dtype)
         _check(self.ctx._lib.svr_frame_download(self.h, BUF[which], _ptr(out), C.c_size_t(nbytes)))
         return out if shape is None else out.reshape(shape)
+
+    def download_async(self, which: str, out) -> None:
+        """Enqueues the read-back of buffer `which` into `out` (a contiguous
+        numpy array or CPU tensor of the buffer's size, pinned for overlap);
+        `out` is complete after wait()."""
+        ptr = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
+        nbytes = out.numel() * out.element_size() if hasattr(out, "numel") else out.nbytes
+        _check(self.ctx._lib.svr_frame_download_async(self.h, BUF[which], C.c_void_p(ptr),
+                                                      C.c_size_t(nbytes)))
+
+    def wait(self) -> None:
+        """Blocks until this frame's asynchronous downloads have landed."""
+        _check(self.ctx._lib.svr_frame_wait(self.h))
 
     def records(self):
         """(pre_vids, contrib_pre, contrib_a, contrib_b, pix_begin, pix_count)."""

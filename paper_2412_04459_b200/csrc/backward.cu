@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(256) voxel_epilogue_kernel(DevCamera cam, Epil
     ux = __shfl_sync(0xffffffffu, ux, leader);
     uy = __shfl_sync(0xffffffffu, uy, leader);
     uz = __shfl_sync(0xffffffffu, uz, leader);
-    float b[16];
+    float b[16] = {};  // lanes m >= (d+1)^2 read zeros, not stale registers
     sh_basis(a.sh_degree, ux, uy, uz, b);
     float bm = 0.f;
 #pragma unroll

@@ -237,6 +237,15 @@ TapSet ensure_taps(svr_frame* f) {
     return t;
 }
 
+// Device-side ordering against a frame's in-flight asynchronous downloads:
+// anything that rewrites frame buffers first makes the main stream wait.
+void wait_copies(svr_frame* f) {
+    if (f && f->copy_pending) {
+        SVR_CUDA(cudaStreamWaitEvent(f->ctx->stream, f->copied, 0));
+        f->copy_pending = false;
+    }
+}
+
 // Validation of RenderOptions, in raster.cpp:207-211 order.
 void validate_options(const svr_render_options& o) {
     require(o.supersample >= 1.0, SVR_ERR_INVALID_ARGUMENT, "supersample factor must be >= 1");
@@ -278,6 +287,10 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     require(uint64_t(cam.ntx) * cam.nty < (uint64_t(1) << 16), SVR_ERR_LENGTH,
             "tile count exceeds the 16-bit id capacity");
 
+    if (f->copy_pending) {  // rendering rewrites the outputs an async copy reads
+        SVR_CUDA(cudaStreamWaitEvent(ctx->stream, f->copied, 0));
+        f->copy_pending = false;
+    }
     f->ctx = ctx;
     f->scene = scene;
     f->opts = *opts;
@@ -332,7 +345,7 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     mark(ctx, -1);
     ctx->pinned.reserve(sizeof(FrameStatus));
     FrameStatus* hs = static_cast<FrameStatus*>(ctx->pinned.p);
-    SVR_CUDA(cudaMemcpyAsync(hs, status, sizeof(FrameStatus), cudaMemcpyDeviceToHost, st));
+    launch_status_to_host(status, hs, st);
     SVR_CUDA(cudaStreamSynchronize(st));
     const uint64_t E = hs->n_entries;
     const uint32_t pattern_or = hs->pattern_or;
@@ -481,7 +494,7 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
         uint32_t* pb = grow<uint32_t>(f->pix_begin, uint64_t(ntiles) * 256);
         exclusive_scan_u32(ca.pix_count, pb, uint64_t(ntiles) * 256, &status->n_contribs,
                            ctx->scratch.p, st);
-        SVR_CUDA(cudaMemcpyAsync(hs, status, sizeof(FrameStatus), cudaMemcpyDeviceToHost, st));
+        launch_status_to_host(status, hs, st);
         SVR_CUDA(cudaStreamSynchronize(st));
         const uint64_t C = hs->n_contribs;
         require(C < (uint64_t(1) << 32), SVR_ERR_LENGTH, "contribution count exceeds 2^32");
@@ -560,6 +573,13 @@ BufView frame_buffer(svr_frame* f, svr_buffer which) {
     const uint64_t npx = uint64_t(f->W) * f->H, nss = uint64_t(f->sw) * f->sh;
     const bool ss1 = (f->sw == f->W && f->sh == f->H);
     const uint64_t ntiles = uint64_t(f->ntx) * f->nty;
+    switch (which) {  // materialised buffers reuse scratch an async copy may still read
+        case SVR_BUF_COLOR: case SVR_BUF_DEPTH: case SVR_BUF_MEDIAN_DEPTH: case SVR_BUF_NORMAL:
+        case SVR_BUF_TRANSMITTANCE: case SVR_BUF_MAX_BLEND: case SVR_BUF_SS_COLOR:
+        case SVR_BUF_SS_DEPTH: case SVR_BUF_SS_TFIN: case SVR_BUF_TILE_RANGES:
+        case SVR_BUF_TILE_MASKS: case SVR_BUF_VOXEL_RECTS: break;
+        default: wait_copies(f);
+    }
     switch (which) {
         case SVR_BUF_COLOR: return {f->out_color.p, npx * 12};
         case SVR_BUF_DEPTH: return {f->out_depth.p, npx * 4};
@@ -629,6 +649,7 @@ void backward_impl(svr_ctx* ctx, const svr_scene* scene, svr_frame* f, const svr
             "per-contribution weight gradients do not match the records");
     require(!up->d_voxel_color || up->n_d_voxel_color == f->n_contribs, SVR_ERR_RUNTIME,
             "per-contribution color gradients do not match the records");
+    wait_copies(f);
     cudaStream_t st = ctx->stream;
     const uint64_t N = scene->n_voxels, P = scene->n_pool;
     const uint64_t shn = N * uint64_t(scene->sh_stride);
@@ -782,6 +803,7 @@ int svr_ctx_create(int device, svr_ctx** out) {
         c->device = device;
         SVR_CUDA(cudaSetDevice(device));
         SVR_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        SVR_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         SVR_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
         *out = c;
     });
@@ -792,9 +814,11 @@ int svr_ctx_destroy(svr_ctx* ctx) {
         if (!ctx) return;
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
+        cudaStreamSynchronize(ctx->copy_stream);
         for (auto& m : ctx->marks) cudaEventDestroy(m.second);
         for (auto& e : ctx->event_pool) cudaEventDestroy(e);
         cudaStreamDestroy(ctx->stream);
+        cudaStreamDestroy(ctx->copy_stream);
         delete ctx;
     });
 }
@@ -916,6 +940,11 @@ int svr_frame_destroy(svr_frame* f) {
     return guard([&] {
         if (!f) return;
         if (f->ctx) cudaSetDevice(f->ctx->device);
+        if (f->copied) {
+            cudaEventSynchronize(f->copied);
+            cudaEventDestroy(f->copied);
+        }
+        if (f->ready) cudaEventDestroy(f->ready);
         delete f;
     });
 }
@@ -951,6 +980,30 @@ int svr_frame_download(svr_frame* f, svr_buffer which, void* dst, size_t bytes) 
         if (bytes)
             SVR_CUDA(cudaMemcpyAsync(dst, b.p, bytes, cudaMemcpyDeviceToHost, f->ctx->stream));
         SVR_CUDA(cudaStreamSynchronize(f->ctx->stream));
+    });
+}
+
+int svr_frame_download_async(svr_frame* f, svr_buffer which, void* dst, size_t bytes) {
+    return guard([&] {
+        require(f && f->ctx && dst, SVR_ERR_INVALID_ARGUMENT, "null argument");
+        set_device(f->ctx);
+        BufView b = frame_buffer(f, which);
+        require(bytes == b.bytes, SVR_ERR_INVALID_ARGUMENT, "download size mismatch");
+        if (!f->ready) SVR_CUDA(cudaEventCreateWithFlags(&f->ready, cudaEventDisableTiming));
+        if (!f->copied) SVR_CUDA(cudaEventCreateWithFlags(&f->copied, cudaEventDisableTiming));
+        SVR_CUDA(cudaEventRecord(f->ready, f->ctx->stream));
+        SVR_CUDA(cudaStreamWaitEvent(f->ctx->copy_stream, f->ready, 0));
+        if (bytes)
+            SVR_CUDA(cudaMemcpyAsync(dst, b.p, bytes, cudaMemcpyDeviceToHost, f->ctx->copy_stream));
+        SVR_CUDA(cudaEventRecord(f->copied, f->ctx->copy_stream));
+        f->copy_pending = true;
+    });
+}
+
+int svr_frame_wait(svr_frame* f) {
+    return guard([&] {
+        require(f != nullptr, SVR_ERR_INVALID_ARGUMENT, "null argument");
+        if (f->copied) SVR_CUDA(cudaEventSynchronize(f->copied));
     });
 }
 

@@ -806,9 +806,19 @@ __global__ void project_batch_kernel(DevCamera cam, uint64_t n, const double* ce
     rect[4 * i + 3] = pr.ty1;
 }
 
+// Frame summary -> mapped pinned host memory, written by the SM over PCIe:
+// no copy-engine transfer, so this read-back never queues behind a large
+// asynchronous image download on the copy stream.
+__global__ void status_to_host_kernel(const FrameStatus* d, FrameStatus* h) { *h = *d; }
+
 inline unsigned blocks_for(uint64_t n, int threads) { return unsigned((n + threads - 1) / threads); }
 
 }  // namespace
+
+void launch_status_to_host(const FrameStatus* d, FrameStatus* h, cudaStream_t st) {
+    status_to_host_kernel<<<1, 1, 0, st>>>(d, h);
+    SVR_LAUNCH("status_to_host_kernel");
+}
 
 void launch_tile_setup(const DevCamera& cam, uint8_t* masks, uint32_t* sat, FrameStatus* status,
                        cudaStream_t st) {

@@ -74,6 +74,7 @@ struct svr_ctx {
     std::vector<cudaEvent_t> event_pool;
     double stage_ms[svrb::kNumStages] = {};
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;  // svr_frame_download_async
     int num_sms = 148;
     bool debug = false;
     svrb::DevBuf scratch;   // sort/scan temporaries
@@ -127,4 +128,8 @@ struct svr_frame {
     svrb::DevBuf ref_keys, ref_vals;  // reference-format dumps of packed entries
     int tap_src_w = -1, tap_src_h = -1, tap_dst_w = -1, tap_dst_h = -1;
     int n_taps_x = 0, n_taps_y = 0;
+    // asynchronous read-back (svr_frame_download_async)
+    cudaEvent_t ready = nullptr;   // main stream reached the copy point
+    cudaEvent_t copied = nullptr;  // copy stream finished the downloads
+    bool copy_pending = false;
 };

@@ -54,6 +54,8 @@ struct FrameStatus {          // device -> host summary, one read per frame
 
 void launch_tile_setup(const DevCamera& cam, uint8_t* masks, uint32_t* sat, FrameStatus* status,
                        cudaStream_t st);
+// Copies the device FrameStatus into host-mapped pinned memory with a kernel.
+void launch_status_to_host(const FrameStatus* d, FrameStatus* h, cudaStream_t st);
 
 struct PreprocessArgs {
     uint64_t n;

@@ -248,14 +248,28 @@ SVR_HD float one_minus_exp_neg(float x) {
     return x < 0.03125f ? small : big;
 }
 
-// exp(x/1.1 - 1 + ln 1.1) = exp(x/1.1) * (1.1/e); branch-free select
-constexpr float kExplinScale = 0.40467196f;  // 1.1 / e
+// explin below the knee (field.hpp:23-26): exp(x/1.1 - 1 + ln 1.1)
+// = 2^(x * log2(e)/1.1 + log2(1.1/e)), one FFMA + one MUFU.EX2; branch-free
+// select. (The constants carry the reference's 1.1/e exactly to fp32: an
+// error in them is a uniform relative bias on every optical depth, which
+// compounds through T over hundreds of voxels per ray.)
+#if defined(__CUDA_ARCH__)
+__device__ __forceinline__ float fexp2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+#else
+inline float fexp2(float x) { return exp2f(x); }
+#endif
+constexpr float kExplinA = 1.31154096f;   // log2(e) / 1.1
+constexpr float kExplinB = -1.30519152f;  // log2(1.1 / e)
 SVR_HD float explin(float x) {
-    const float e = fexp(x * (1.0f / 1.1f)) * kExplinScale;
+    const float e = fexp2(fmaf(x, kExplinA, kExplinB));
     return x > kExplinKnee ? x : e;
 }
 SVR_HD float explin_deriv(float x) {
-    return x > kExplinKnee ? 1.0f : fexp(x * (1.0f / 1.1f)) * (kExplinScale / 1.1f);
+    return x > kExplinKnee ? 1.0f : fexp2(fmaf(x, kExplinA, kExplinB)) * (1.0f / 1.1f);
 }
 
 // trilinear (field.hpp:33-47), corner order (i<<2)|(j<<1)|k.
