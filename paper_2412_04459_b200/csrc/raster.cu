@@ -476,15 +476,28 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* ranges, i
 }
 
 // ------------------------------------------------------------------- K7
-// One CTA per 16x16 tile, one thread per pixel; each warp owns an 8x4 pixel
-// block. Voxel records of a batch of 256 entries are staged in shared
-// memory (one 112-B record per thread, SoA by float4 slot). Each warp then
-// culls the batch 32 entries at a time against its own 8x4 footprint and
-// the sign patterns its pixels carry (one lane per entry, __ballot_sync),
-// and walks only the surviving entries front to back with exactly
-// CompositeCtx::add's arithmetic in fp32 (the per-pixel sign and AABB tests
-// are kept, so the set and order of composited voxels is the reference's).
-// The CTA exits once every pixel terminated (__syncthreads_count vote).
+// One CTA per 16x16 tile (LPT order), eight warps; each warp owns an 8x4
+// pixel block and runs autonomously (no CTA barrier inside the entry loop,
+// so a warp whose block sees few voxels never waits for a busy neighbour).
+//
+// The tile's sorted entry list is consumed in chunks of 32 (one entry per
+// lane). Per chunk the warp culls with the reference's own filters lifted to
+// its block (sign patterns, screen AABB; a frustum test for loose AABBs) and
+// ballots the survivors ("slots"). Their 96-B records are copied into
+// warp-private shared memory with cp.async one chunk AHEAD of use (double
+// buffer), so the L2 latency of the gather overlaps the compositing of the
+// previous chunk.
+//
+// Compositing a chunk is two-phase:
+//   A. every lane tests every slot (sign, AABB, fp32 slab): a bit per slot;
+//   B. every lane walks ITS OWN hit bits in entry order and runs the K-point
+//      quadrature + CompositeCtx::add only there. All lanes execute the same
+//      instructions (they differ in which slot they read), so lane
+//      utilisation is set by the busiest pixel of the block, not by how
+//      many pixels each voxel covers (~1/3 of the block on config 2).
+// The per-pixel set and order of composited voxels is the reference's
+// (raster.cpp:17-61, 238-281), and a pixel stops after the voxel that took
+// T below the threshold.
 __device__ __forceinline__ void pixel_of(const DevCamera& cam, int tile, int tid, int& px, int& py) {
     const int tx = tile % cam.ntx, ty = tile / cam.ntx;
     const int warp = tid >> 5, lane = tid & 31;
@@ -492,17 +505,41 @@ __device__ __forceinline__ void pixel_of(const DevCamera& cam, int tile, int tid
     py = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
 }
 
-// Warp-autonomous compositing: no CTA-wide barrier inside the entry loop, so
-// a warp whose 8x4 block sees few voxels never waits for a busy neighbour.
-// Per chunk of 32 entries: lane i holds entry i's value and screen AABB
-// (prefetched one chunk ahead, values two chunks ahead), the warp ballots the
-// entries that overlap its block, gathers those records (112 B each,
-// coalesced 16-B pieces) into warp-private shared memory, and walks them in
-// order.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// fp32 slab test of ray_aabb (field.hpp:58-69) against the camera-relative
+// box [lo.xyz, lo.xyz + lo.w].
+__device__ __forceinline__ void slab(float4 lo, float ix, float iy, float iz, float& ta, float& tb) {
+    float t0 = lo.x * ix, t1 = (lo.x + lo.w) * ix;
+    ta = fminf(t0, t1);
+    tb = fmaxf(t0, t1);
+    t0 = lo.y * iy;
+    t1 = (lo.y + lo.w) * iy;
+    ta = fmaxf(ta, fminf(t0, t1));
+    tb = fminf(tb, fmaxf(t0, t1));
+    t0 = lo.z * iz;
+    t1 = (lo.z + lo.w) * iz;
+    ta = fmaxf(ta, fminf(t0, t1));
+    tb = fminf(tb, fmaxf(t0, t1));
+}
+
+constexpr int kCompWarps = 8;
+constexpr size_t kCompSmem = size_t(2) * kCompWarps * 32 * kRecordF4 * sizeof(float4);
+
 template <int K, bool RECORD>
-__global__ void __launch_bounds__(256) composite_kernel(DevCamera cam, CompositeArgs a) {
-    __shared__ float4 s_rec[8][32][kRecordF4];
-    __shared__ uint32_t s_vid[8][32];
+__global__ void __launch_bounds__(256, 4) composite_kernel(DevCamera cam, CompositeArgs a) {
+    extern __shared__ float4 s_rec_dyn[];  // [2][8 warps][32 slots][kRecordF4]
+    __shared__ uint32_t s_vid[2][kCompWarps][32];
+    __shared__ uint8_t s_j[2][kCompWarps][32];  // chunk-local entry index of each slot
+    __shared__ float s_cone[kCompWarps][4][3];
 
     const int tile = a.tile_order ? int(a.tile_order[blockIdx.x]) : int(blockIdx.x);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -526,7 +563,6 @@ __global__ void __launch_bounds__(256) composite_kernel(DevCamera cam, Composite
     // Frustum of this warp's 8x4 block (warp_cone_planes): skips boxes whose
     // screen AABB is loose, e.g. near-plane voxels, which get the full screen
     // (raster.cpp:95-101), without changing the composited set.
-    __shared__ float s_cone[8][4][3];
     float (*cone)[3] = s_cone[warp];
     if (lane == 0) warp_cone_planes(cam, wx0, wy0, cone);
     __syncwarp();
@@ -542,148 +578,170 @@ __global__ void __launch_bounds__(256) composite_kernel(DevCamera cam, Composite
     const uint2 range = a.ranges[tile];
     const float thr = a.t_threshold;
     constexpr uint32_t kVidMask = (1u << 29) - 1u;
-    float4 (*wrec)[kRecordF4] = s_rec[warp];
-    uint32_t* wvid = s_vid[warp];
+    float4 (*wrec0)[kRecordF4] =
+        reinterpret_cast<float4 (*)[kRecordF4]>(s_rec_dyn + size_t(warp) * 32 * kRecordF4);
+    float4 (*wrec1)[kRecordF4] = wrec0 + kCompWarps * 32;
 
-    // software pipeline: v0/b0 = current chunk, v1 = next chunk's values
-    uint32_t v0 = 0, v1 = 0;
-    float4 b0 = make_float4(0.f, -1.f, 0.f, -1.f);
+    // Cull one chunk (entries c .. c+31, lane = entry) and start the copy of
+    // its surviving records into buffer `buf`. Returns the survivor mask.
+    auto stage = [&](uint32_t c, uint32_t v, float4 b, int buf) -> uint32_t {
+        bool rel = c + lane < range.y && ((warp_signs >> (v >> 29)) & 1u) &&
+                   !(fx1 < b.x || fx0 > b.y || fy1 < b.z || fy0 > b.w);
+        // frustum test only for entries with a large screen AABB
+        const bool wide = rel && (b.y - b.x) * (b.w - b.z) > kConeMinArea;
+        if (__any_sync(0xffffffffu, wide) && wide)
+            rel = box_in_cone(cone, __ldg(a.records + uint64_t(v & kVidMask) * kRecordF4));
+        const uint32_t m = __ballot_sync(0xffffffffu, rel);
+        const int nrel = __popc(m);
+        uint32_t* wvid = s_vid[buf][warp];
+        if (rel) {
+            const int at = __popc(m & ((1u << lane) - 1u));
+            wvid[at] = v;
+            s_j[buf][warp][at] = uint8_t(lane);
+        }
+        __syncwarp();
+        float4(*wrec)[kRecordF4] = buf ? wrec1 : wrec0;
+        for (int i = lane; i < nrel * kRecordF4; i += 32) {
+            const int sl = i / kRecordF4, k = i - sl * kRecordF4;
+            cp_async16(&wrec[sl][k], a.records + uint64_t(wvid[sl] & kVidMask) * kRecordF4 + k);
+        }
+        cp_async_commit();
+        return m;
+    };
+
+    // software pipeline: chunk c's records are in flight while chunk c-1 is
+    // composited; (v1, b1) describe chunk c+1, v2 chunk c+2.
+    uint32_t v0 = 0, v1 = 0, v2 = 0;
+    float4 b0 = make_float4(0.f, -1.f, 0.f, -1.f), b1 = b0;
     if (range.x + lane < range.y) {
         v0 = __ldg(a.vals + range.x + lane);
         b0 = __ldg(a.records + uint64_t(v0 & kVidMask) * kRecordF4 + 1);
     }
-    if (range.x + 32 + lane < range.y) v1 = __ldg(a.vals + range.x + 32 + lane);
+    if (range.x + 32 + lane < range.y) {
+        v1 = __ldg(a.vals + range.x + 32 + lane);
+        b1 = __ldg(a.records + uint64_t(v1 & kVidMask) * kRecordF4 + 1);
+    }
+    if (range.x + 64 + lane < range.y) v2 = __ldg(a.vals + range.x + 64 + lane);
+    uint32_t m_cur = range.x < range.y ? stage(range.x, v0, b0, 0) : 0u;
+    int buf = 0;
 
-    for (uint32_t c = range.x; c < range.y; c += 32) {
+    for (uint32_t c = range.x; c < range.y; c += 32, buf ^= 1) {
         if (__all_sync(0xffffffffu, done)) break;
-        float4 b1 = make_float4(0.f, -1.f, 0.f, -1.f);
-        uint32_t v2 = 0;
-        if (c + 32 + lane < range.y) b1 = __ldg(a.records + uint64_t(v1 & kVidMask) * kRecordF4 + 1);
-        if (c + 64 + lane < range.y) v2 = __ldg(a.vals + c + 64 + lane);
-
-        const bool valid = c + lane < range.y;
-        bool rel = valid && ((warp_signs >> (v0 >> 29)) & 1u) &&
-                   !(fx1 < b0.x || fx0 > b0.y || fy1 < b0.z || fy0 > b0.w);
-        // frustum test only for entries with a large screen AABB
-        const bool wide = rel && (b0.y - b0.x) * (b0.w - b0.z) > kConeMinArea;
-        if (__any_sync(0xffffffffu, wide) && wide)
-            rel = box_in_cone(cone, __ldg(a.records + uint64_t(v0 & kVidMask) * kRecordF4));
-        const uint32_t m = __ballot_sync(0xffffffffu, rel);
-        const int nrel = __popc(m);
-        if (rel) wvid[__popc(m & ((1u << lane) - 1u))] = v0;
-        __syncwarp();
-        for (int i = lane; i < nrel * kRecordF4; i += 32) {
-            const int sl = i / kRecordF4, k = i - sl * kRecordF4;
-            wrec[sl][k] = __ldg(a.records + uint64_t(wvid[sl] & kVidMask) * kRecordF4 + k);
+        // prefetch: AABB of chunk c+2, values of chunk c+3
+        float4 b2 = make_float4(0.f, -1.f, 0.f, -1.f);
+        uint32_t v3 = 0;
+        if (c + 64 + lane < range.y) b2 = __ldg(a.records + uint64_t(v2 & kVidMask) * kRecordF4 + 1);
+        if (c + 96 + lane < range.y) v3 = __ldg(a.vals + c + 96 + lane);
+        // stage chunk c+1 into the other buffer, then wait for chunk c
+        uint32_t m_next = 0;
+        if (c + 32 < range.y) {
+            m_next = stage(c + 32, v1, b1, buf ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
         __syncwarp();
-        // Slots are evaluated two at a time, branch-free (slab + quadrature of
-        // both are independent of the pixel state, so their latencies
-        // overlap), then folded into the pixel state in entry order.
-        uint32_t mm = m;
-        for (int sl = 0; sl < nrel; sl += 2) {
-            const bool has_b = sl + 1 < nrel;
-            const int ja = __ffs(mm) - 1;  // chunk-local entry index (record pass)
-            mm &= mm - 1;
-            const int jb = has_b ? __ffs(mm) - 1 : 0;
-            if (has_b) mm &= mm - 1;
-            float alpha[2], dvox[2], sa[2][K], tk[2][K];
-            bool ok[2];
+
+        const int nrel = __popc(m_cur);
+        float4(*wrec)[kRecordF4] = buf ? wrec1 : wrec0;
+        const uint32_t* wvid = s_vid[buf][warp];
+        const uint8_t* wj = s_j[buf][warp];
+        // Phase A: this lane's hit set among the slots.
+        uint32_t hits = 0;
+        if (!done) {
+#pragma unroll 2
+            for (int sl = 0; sl < nrel; ++sl) {
+                const float4 bb = wrec[sl][1];
+                float ta, tb;
+                slab(wrec[sl][0], ix, iy, iz, ta, tb);
+                const bool ok = (one_sign || (wvid[sl] >> 29) == my_sign) &&
+                                !(pcx < bb.x || pcx > bb.y || pcy < bb.z || pcy > bb.w) &&
+                                ta <= tb && ta > 0.0f;
+                hits |= uint32_t(ok) << sl;
+            }
+        }
+        // Phase B: this lane's hits, in entry order.
+        while (hits) {
+            const int s_ = __ffs(hits) - 1;
+            hits &= hits - 1;
+            const float4 lo = wrec[s_][0];
+            float ta, tb;
+            slab(lo, ix, iy, iz, ta, tb);
+            const float4 va = wrec[s_][2], vb = wrec[s_][3];
+            const float inv = wrec[s_][5].w;
+            const float V[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
+            const float seg = tb - ta;
+            const float lk = seg * dnorm * (1.0f / K);
+            // voxel_alpha (field.hpp:92-116), K-point midpoint quadrature
+            float sa[K], tk[K], sum = 0.f;
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int s_ = (u == 0) ? sl : (has_b ? sl + 1 : sl);
-                const float4 bb = wrec[s_][1];
-                const float4 lo = wrec[s_][0];
-                const float4 va = wrec[s_][2], vb = wrec[s_][3];
-                const float inv = wrec[s_][5].w;
-                const bool pass = (u == 0 || has_b) && !done &&
-                                  (one_sign || (wvid[s_] >> 29) == my_sign) &&
-                                  !(pcx < bb.x || pcx > bb.y || pcy < bb.z || pcy > bb.w);
-                float t0 = lo.x * ix, t1 = (lo.x + lo.w) * ix;
-                float ta = fminf(t0, t1), tb = fmaxf(t0, t1);
-                t0 = lo.y * iy;
-                t1 = (lo.y + lo.w) * iy;
-                ta = fmaxf(ta, fminf(t0, t1));
-                tb = fminf(tb, fmaxf(t0, t1));
-                t0 = lo.z * iz;
-                t1 = (lo.z + lo.w) * iz;
-                ta = fmaxf(ta, fminf(t0, t1));
-                tb = fminf(tb, fmaxf(t0, t1));
-                ok[u] = pass && (ta <= tb && ta > 0.0f);
-                // voxel_alpha (field.hpp:92-116), K-point midpoint quadrature
-                const float V[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
-                const float seg = tb - ta;
-                const float lk = seg * dnorm * (1.0f / K);
-                float sum = 0.f;
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    tk[u][k] = ta + ((k + 0.5f) / K) * seg;
-                    const float qx = (tk[u][k] * dx - lo.x) * inv;
-                    const float qy = (tk[u][k] * dy - lo.y) * inv;
-                    const float qz = (tk[u][k] * dz - lo.z) * inv;
-                    const float act = explin(trilinear(V, qx, qy, qz));
-                    sum += act;
-                    sa[u][k] = one_minus_exp_neg(lk * act);
-                }
-                alpha[u] = (K == 1) ? sa[u][0] : one_minus_exp_neg(lk * sum);
-                // voxel_depth (field.hpp:173-181)
+            for (int k = 0; k < K; ++k) {
+                tk[k] = ta + ((k + 0.5f) / K) * seg;
+                const float qx = (tk[k] * dx - lo.x) * inv;
+                const float qy = (tk[k] * dy - lo.y) * inv;
+                const float qz = (tk[k] * dz - lo.z) * inv;
+                const float act = explin(trilinear(V, qx, qy, qz));
+                sum += act;
+                sa[k] = one_minus_exp_neg(lk * act);
+            }
+            const float alpha = (K == 1) ? sa[0] : one_minus_exp_neg(lk * sum);
+            const uint32_t entry = c + wj[s_];
+            if (!RECORD) {
+                // voxel_depth (field.hpp:173-181) and the median crossing
                 float dv = 0.f, Tk = 1.f;
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
-                    dv += Tk * sa[u][k] * tk[u][k];
-                    Tk *= 1.0f - sa[u][k];
+                    dv += Tk * sa[k] * tk[k];
+                    Tk *= 1.0f - sa[k];
                 }
-                dvox[u] = dv;
+                if (median < 0.0f) {
+                    float Tf = T;
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        Tf *= 1.0f - sa[k];
+                        if (Tf < 0.5f) {
+                            median = tk[k];
+                            break;
+                        }
+                    }
+                }
+                const float w = T * alpha;
+                const float4 col = wrec[s_][4], nor = wrec[s_][5];
+                cr += w * col.x;
+                cg += w * col.y;
+                cb += w * col.z;
+                nx += w * nor.x;
+                ny += w * nor.y;
+                nz += w * nor.z;
+                depth += T * dv;
+                if (a.max_blend) atomicMax(a.max_blend + __float_as_uint(col.w), __float_as_uint(w));
+                if (a.stage_entry) {
+                    if (cnt < a.stage_cap) {
+                        const uint32_t at = cnt * a.stage_stride + slot;
+                        a.stage_entry[at] = entry;
+                        a.stage_T[at] = T;
+                    } else {
+                        *a.overflow = 1u;
+                    }
+                }
+            } else {
+                a.contrib_entry[rec_base + cnt] = entry;
+                a.contrib_T[rec_base + cnt] = T;
             }
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                if (!ok[u] || done) continue;
-                const int s_ = sl + u;
-                const float w = T * alpha[u];
-                if (!RECORD) {
-                    if (median < 0.0f) {
-                        float Tf = T;
-#pragma unroll
-                        for (int k = 0; k < K; ++k) {
-                            Tf *= 1.0f - sa[u][k];
-                            if (Tf < 0.5f) {
-                                median = tk[u][k];
-                                break;
-                            }
-                        }
-                    }
-                    const float4 col = wrec[s_][4], nor = wrec[s_][5];
-                    cr += w * col.x;
-                    cg += w * col.y;
-                    cb += w * col.z;
-                    nx += w * nor.x;
-                    ny += w * nor.y;
-                    nz += w * nor.z;
-                    depth += T * dvox[u];
-                    if (a.max_blend) atomicMax(a.max_blend + __float_as_uint(col.w), __float_as_uint(w));
-                    if (a.stage_entry) {
-                        if (cnt < a.stage_cap) {
-                            const uint32_t at = cnt * a.stage_stride + slot;
-                            a.stage_entry[at] = c + uint32_t(u == 0 ? ja : jb);
-                            a.stage_T[at] = T;
-                        } else {
-                            *a.overflow = 1u;
-                        }
-                    }
-                } else {
-                    a.contrib_entry[rec_base + cnt] = c + uint32_t(u == 0 ? ja : jb);
-                    a.contrib_T[rec_base + cnt] = T;
-                }
-                T *= 1.0f - alpha[u];
-                ++cnt;
-                if (T < thr) done = true;
+            T *= 1.0f - alpha;
+            ++cnt;
+            if (T < thr) {
+                done = true;
+                hits = 0;
             }
         }
-        __syncwarp();
-        v0 = v1;
-        b0 = b1;
+        __syncwarp();  // buffer `buf` is restaged two chunks later
+        m_cur = m_next;
         v1 = v2;
+        b1 = b2;
+        v2 = v3;
     }
+    cp_async_wait<0>();  // no copy may outlive the CTA's shared memory
     if (RECORD || !inside) return;
     // CompositeCtx::finish (raster.cpp:56-60)
     cr += T * a.bg[0];
@@ -964,12 +1022,19 @@ void launch_tile_order(const uint2* ranges, int ntiles, uint32_t* order, cudaStr
 void launch_composite(const DevCamera& cam, const CompositeArgs& a, bool record_pass,
                       cudaStream_t st) {
     const unsigned ntiles = unsigned(cam.ntx * cam.nty);
+    static bool attr_set = false;
+    if (!attr_set) {
+        for (auto fn : {composite_kernel<1, false>, composite_kernel<1, true>, composite_kernel<2, false>,
+                        composite_kernel<2, true>, composite_kernel<3, false>, composite_kernel<3, true>})
+            SVR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCompSmem)));
+        attr_set = true;
+    }
 #define SVR_COMPOSITE_CASE(KK)                                                        \
     case KK:                                                                          \
         if (record_pass)                                                              \
-            composite_kernel<KK, true><<<ntiles, 256, 0, st>>>(cam, a);              \
+            composite_kernel<KK, true><<<ntiles, 256, kCompSmem, st>>>(cam, a);      \
         else                                                                          \
-            composite_kernel<KK, false><<<ntiles, 256, 0, st>>>(cam, a);             \
+            composite_kernel<KK, false><<<ntiles, 256, kCompSmem, st>>>(cam, a);     \
         break;
     switch (a.K) {
         SVR_COMPOSITE_CASE(1)
