@@ -367,11 +367,6 @@ class Context:
         _check(self._lib.svr_ctx_stage_times(self.h, buf, len(STAGES), int(reset)))
         return {k: buf[i] for i, k in enumerate(STAGES)}
 
-
-def launch_count() -> int:
-    """Kernels launched by libsvr_b200.so so far (process-wide)."""
-    return int(load_library().svr_launch_count())
-
     def close(self) -> None:
         if getattr(self, "h", None):
             self._lib.svr_ctx_destroy(self.h)
@@ -382,6 +377,11 @@ def launch_count() -> int:
             self.close()
         except Exception:
             pass
+
+
+def launch_count() -> int:
+    """Kernels launched by libsvr_b200.so so far (process-wide)."""
+    return int(load_library().svr_launch_count())
 
 
 class Scene:

@@ -1,6 +1,4 @@
 mkdir -p gpurun_out; rm -f gpurun_out/variants.log
-for v in laneq cpasync; do
-  echo "== $v" >> gpurun_out/variants.log
-  SVR_LIB=variants/libsvr_$v.so timeout 120 python tools/quick_time.py >> gpurun_out/variants.log 2>&1
-done
-timeout 900 python -m pytest tests/ -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_gpu.log
+timeout 120 python tools/stage_time.py >> gpurun_out/variants.log 2>&1
+SVR_RANK_ORDER=0 timeout 120 python tools/stage_time.py >> gpurun_out/variants.log 2>&1
+SVR_FRAMES=2 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_rank.csv python tools/profile_step.py > /dev/null 2>&1
