@@ -166,9 +166,13 @@ __global__ void __launch_bounds__(kPreThreads, SVR_PRE_MINB) preprocess_kernel(D
             r0.y = float(dsub(dsub(center[1], h), cam.pos[1]));
             r0.z = float(dsub(dsub(center[2], h), cam.pos[2]));
             r0.w = float(size);
-            // Screen AABB, rounded outward so the fp32 test is a superset.
+            // Screen AABB, rounded outward so the fp32 test is a superset;
+            // empty for near-plane voxels no image ray can reach (their
+            // entries stay; the compositing warps skip them at the AABB test).
             r1 = make_float4(__double2float_rd(pr.x0), __double2float_ru(pr.x1),
                              __double2float_rd(pr.y0), __double2float_ru(pr.y1));
+            if (pr.straddles && box_outside_image_frustum(cam, center, size))
+                r1 = make_float4(1.f, 0.f, 1.f, 0.f);
             const uint4* ci4 = reinterpret_cast<const uint4*>(a.corner_index + 8 * v);
             const uint4 c0 = __ldg(ci4), c1 = __ldg(ci4 + 1);
             float V[8] = {__ldg(a.density + c0.x), __ldg(a.density + c0.y), __ldg(a.density + c0.z),

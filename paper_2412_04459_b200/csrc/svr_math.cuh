@@ -143,6 +143,7 @@ SVR_HD void voxel_geometry(uint64_t code, int level, const double* bc, double bs
 struct Projection {
     double x0, x1, y0, y1;
     int tx0, tx1, ty0, ty1;
+    bool straddles;  // a corner is at or behind the near plane: AABB = whole image
 };
 
 // project_voxel (raster.cpp:72-118), bit-exact. Returns false when culled;
@@ -154,6 +155,7 @@ SVR_HD bool project_voxel(const DevCamera& cam, const double* center, double siz
     out.ty0 = 0;
     out.ty1 = -1;
     out.x0 = out.x1 = out.y0 = out.y1 = 0.0;
+    out.straddles = false;
     bool any_front = false, any_behind = false;
     const double inf = __builtin_huge_val();
     double x0 = inf, x1 = -inf, y0 = inf, y1 = -inf;
@@ -177,6 +179,7 @@ SVR_HD bool project_voxel(const DevCamera& cam, const double* center, double siz
         y1 = (y1 < v) ? v : y1;
     }
     if (!any_front) return false;
+    out.straddles = any_behind;
     if (any_behind) {
         x0 = 0;
         x1 = cam.W;
@@ -197,6 +200,33 @@ SVR_HD bool project_voxel(const DevCamera& cam, const double* center, double siz
     out.ty0 = clampi(x86_double_to_int(floor(ddiv(y0, double(kTile)))), 0, cam.nty - 1);
     out.ty1 = clampi(x86_double_to_int(floor(ddiv(y1, double(kTile)))), 0, cam.nty - 1);
     return true;
+}
+
+// True iff no pixel ray of the image can enter the box at t > 0: all eight
+// corners lie strictly outside one side plane of the image frustum (planes
+// through the camera centre along the image border widened by one pixel;
+// a ray point has camera z = t > 0, and the outside of a plane through the
+// centre is convex, so the whole box is outside too). Used only to give
+// near-plane voxels, whose reference AABB is the whole image
+// (raster.cpp:95-101), an empty compositing footprint; their entries are
+// still emitted exactly as the reference does.
+SVR_HD bool box_outside_image_frustum(const DevCamera& cam, const double* center, double size) {
+    const double u0 = (-1.0 - cam.cx) / cam.fx, u1 = (cam.W + 1.0 - cam.cx) / cam.fx;
+    const double v0 = (-1.0 - cam.cy) / cam.fy, v1 = (cam.H + 1.0 - cam.cy) / cam.fy;
+    const double h = 0.5 * size;
+    bool out[4] = {true, true, true, true};
+    for (int c = 0; c < 8; ++c) {
+        double pc[3];
+        mat_t_vec(cam.rot, center[0] + (((c >> 2) & 1) ? h : -h) - cam.pos[0],
+                  center[1] + (((c >> 1) & 1) ? h : -h) - cam.pos[1],
+                  center[2] + ((c & 1) ? h : -h) - cam.pos[2], pc);
+        const double tol = 1e-9 * (fabs(pc[0]) + fabs(pc[1]) + fabs(pc[2]));
+        if (pc[0] - u0 * pc[2] >= -tol) out[0] = false;
+        if (u1 * pc[2] - pc[0] >= -tol) out[1] = false;
+        if (pc[1] - v0 * pc[2] >= -tol) out[2] = false;
+        if (v1 * pc[2] - pc[1] >= -tol) out[3] = false;
+    }
+    return out[0] || out[1] || out[2] || out[3];
 }
 
 // tile_sign_patterns (raster.cpp:120-142) as a bitmask over s in [0,8).
