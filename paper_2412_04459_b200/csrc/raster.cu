@@ -596,18 +596,17 @@ __global__ void __launch_bounds__(256, 4) composite_kernel(DevCamera cam, Compos
         if (__any_sync(0xffffffffu, wide) && wide)
             rel = box_in_cone(cone, __ldg(a.records + uint64_t(v & kVidMask) * kRecordF4));
         const uint32_t m = __ballot_sync(0xffffffffu, rel);
-        const int nrel = __popc(m);
         uint32_t* wvid = s_vid[buf][warp];
+        const int at = __popc(m & ((1u << lane) - 1u));
         if (rel) {
-            const int at = __popc(m & ((1u << lane) - 1u));
             wvid[at] = v;
             s_j[buf][warp][at] = uint8_t(lane);
         }
-        __syncwarp();
         float4(*wrec)[kRecordF4] = buf ? wrec1 : wrec0;
-        for (int i = lane; i < nrel * kRecordF4; i += 32) {
-            const int sl = i / kRecordF4, k = i - sl * kRecordF4;
-            cp_async16(&wrec[sl][k], a.records + uint64_t(wvid[sl] & kVidMask) * kRecordF4 + k);
+        if (rel) {  // the lane of each surviving entry copies its record
+            const float4* src = a.records + uint64_t(v & kVidMask) * kRecordF4;
+#pragma unroll
+            for (int k = 0; k < kRecordF4; ++k) cp_async16(&wrec[at][k], src + k);
         }
         cp_async_commit();
         return m;
@@ -650,24 +649,25 @@ __global__ void __launch_bounds__(256, 4) composite_kernel(DevCamera cam, Compos
         float4(*wrec)[kRecordF4] = buf ? wrec1 : wrec0;
         const uint32_t* wvid = s_vid[buf][warp];
         const uint8_t* wj = s_j[buf][warp];
-        // Phase A: this lane's hit set among the slots.
+        // Phase A: this lane's slab hits among the slots (the sign-pattern
+        // and AABB filters, which rarely reject a slab hit, run in phase B).
         uint32_t hits = 0;
         if (!done) {
 #pragma unroll 2
             for (int sl = 0; sl < nrel; ++sl) {
-                const float4 bb = wrec[sl][1];
                 float ta, tb;
                 slab(wrec[sl][0], ix, iy, iz, ta, tb);
-                const bool ok = (one_sign || (wvid[sl] >> 29) == my_sign) &&
-                                !(pcx < bb.x || pcx > bb.y || pcy < bb.z || pcy > bb.w) &&
-                                ta <= tb && ta > 0.0f;
-                hits |= uint32_t(ok) << sl;
+                hits |= uint32_t(ta <= tb && ta > 0.0f) << sl;
             }
         }
         // Phase B: this lane's hits, in entry order.
         while (hits) {
             const int s_ = __ffs(hits) - 1;
             hits &= hits - 1;
+            const float4 bb = wrec[s_][1];
+            if (!((one_sign || (wvid[s_] >> 29) == my_sign) &&
+                  !(pcx < bb.x || pcx > bb.y || pcy < bb.z || pcy > bb.w)))
+                continue;
             const float4 lo = wrec[s_][0];
             float ta, tb;
             slab(lo, ix, iy, iz, ta, tb);
