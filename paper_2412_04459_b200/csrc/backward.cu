@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
 // (3(d+1)^2 floats per voxel) are read and written as contiguous runs. The
 // raw colour for the clamp mask (sh.hpp:66-74) is reduced over the 16 lanes;
 // the normal chain (field.hpp:158-170) runs on the first lane.
-__global__ void __launch_bounds__(256) voxel_epilogue_kernel(DevCamera cam, EpilogueArgs a) {
+__global__ void __launch_bounds__(256) voxel_epilogue_kernel(EpilogueArgs a) {
     const uint64_t v = uint64_t(blockIdx.x) * 16u + (threadIdx.x >> 4);
     const int m = threadIdx.x & 15;
     const bool live = v < a.n;
@@ -303,25 +303,13 @@ __global__ void __launch_bounds__(256) voxel_epilogue_kernel(DevCamera cam, Epil
     const bool vis = r.y >= r.x;  // in `pre`
     const int nb = (a.sh_degree + 1) * (a.sh_degree + 1);
     float* gsh = a.g_sh + v * uint64_t(a.sh_stride);
+    // sh_eval direction exactly as K1 used it (raster.cpp:195-196): the
+    // forward colour and this clamp mask see identical floats
     float ux = 0.f, uy = 0.f, uz = 0.f;
-    if (vis && m == 0) {
-        const uint64_t path = a.paths[v];
-        double center[3], size;
-        voxel_geometry(path & ((uint64_t(1) << 48) - 1), int(path >> 48), a.bc, a.bsize, center,
-                       &size);
-        const double dx = dsub(center[0], cam.pos[0]), dy = dsub(center[1], cam.pos[1]),
-                     dz = dsub(center[2], cam.pos[2]);
-        const double nrm = sqrt(dx * dx + dy * dy + dz * dz);
-        if (nrm > 0.0) {
-            ux = float(dx / nrm);
-            uy = float(dy / nrm);
-            uz = float(dz / nrm);
-        }
+    if (vis) {
+        const float4 d = __ldg(a.view_dir + v);
+        ux = d.x, uy = d.y, uz = d.z;
     }
-    const int leader = threadIdx.x & 16;  // lane of m == 0 within the warp
-    ux = __shfl_sync(0xffffffffu, ux, leader);
-    uy = __shfl_sync(0xffffffffu, uy, leader);
-    uz = __shfl_sync(0xffffffffu, uz, leader);
     float b[16] = {};  // lanes m >= (d+1)^2 read zeros, not stale registers
     sh_basis(a.sh_degree, ux, uy, uz, b);
     float bm = 0.f;
@@ -415,7 +403,8 @@ void launch_composite_backward(const DevCamera& cam, const BackwardArgs& a, cuda
 
 void launch_voxel_epilogue(const DevCamera& cam, const EpilogueArgs& a, cudaStream_t st) {
     if (a.n == 0) return;
-    voxel_epilogue_kernel<<<blocks_for(a.n, 16), 256, 0, st>>>(cam, a);
+    voxel_epilogue_kernel<<<blocks_for(a.n, 16), 256, 0, st>>>(a);
+    (void)cam;
     SVR_LAUNCH("voxel_epilogue_kernel");
 }
 

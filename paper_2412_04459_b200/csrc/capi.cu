@@ -334,6 +334,7 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     pa.aabb = ctx->debug ? grow<double4>(f->aabb, N) : nullptr;
     pa.records = grow<float4>(f->records, N * kRecordF4);
     pa.counts = grow<uint32_t>(f->counts, N);
+    pa.view_dir = f->training ? grow<float4>(f->view_dir, N) : nullptr;
     mark(ctx, kStagePreprocess);
     launch_preprocess(cam, pa, st);
 
@@ -750,6 +751,7 @@ void backward_impl(svr_ctx* ctx, const svr_scene* scene, svr_frame* f, const svr
     ea.paths = scene->paths.as<uint64_t>();
     ea.rects = f->rects.as<int4>();
     ea.records = f->records.as<float4>();
+    ea.view_dir = f->view_dir.as<float4>();
     ea.corner_index = scene->corner_index.as<uint32_t>();
     ea.sh = scene->sh.as<float>();
     ea.sh_degree = scene->sh_degree;

@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(kPreThreads, SVR_PRE_MINB) preprocess_kernel(D
                 uy = float(dy / nrm);
                 uz = float(dz / nrm);
             }
+            if (a.view_dir) a.view_dir[v] = make_float4(ux, uy, uz, 0.f);
             float b[16];
             const int nb = sh_basis(a.sh_degree, ux, uy, uz, b);
             float cr = 0.f, cg = 0.f, cb = 0.f;

@@ -72,6 +72,7 @@ struct PreprocessArgs {
     double4* aabb;  // optional
     float4* records;
     uint32_t* counts;
+    float4* view_dir;  // optional (training): unit sh_eval direction per visible voxel
 };
 void launch_preprocess(const DevCamera& cam, const PreprocessArgs& a, cudaStream_t st);
 
@@ -212,6 +213,7 @@ struct EpilogueArgs {
     const uint64_t* paths;
     const int4* rects;
     const float4* records;
+    const float4* view_dir;  // K1's sh_eval directions (same floats as the forward)
     const uint32_t* corner_index;
     const float* sh;
     int sh_degree, sh_stride;

@@ -76,15 +76,17 @@ class ShardedTrainer:
         g.density, g.sh = self.density_grad.data_ptr(), self.sh_grad.data_ptr()
         g.priority, g.on_device = self.priority.data_ptr(), 1
         torch.cuda.current_stream().synchronize()
-        with torch.cuda.stream(self.stream):
-            self.flat.zero_()
-            self.priority.zero_()
+        if not view_ids:  # no view on this rank: contribute zeros to the sum
+            with torch.cuda.stream(self.stream):
+                self.flat.zero_()
+                self.priority.zero_()
         total = 0.0
         for n, v in enumerate(view_ids):
             c, o = self.cams[v].to_c(), self.opts.to_c()
             svr._check(lib.svr_train_step_l1(self.ctx.h, self.scene.h, C.byref(c), C.byref(o),
                                              C.c_void_p(self.gts[v].data_ptr()), self.frame.h,
-                                             C.byref(g), 1, C.c_void_p(self.loss.data_ptr())))
+                                             C.byref(g), int(n > 0),  # first view overwrites
+                                             C.c_void_p(self.loss.data_ptr())))
             with torch.cuda.stream(self.stream):
                 total += self.loss  # device scalar, read once below
         with torch.cuda.stream(self.stream):
