@@ -194,17 +194,21 @@ def stage_bytes(stage, d):
     return None
 
 
-def traffic_from_profiles(stage, workload):
+def traffic_from_profiles(stage, workload, npass=1):
+    """Measured DRAM bytes per launch of `stage` for this workload, from the
+    committed ncu summary (profiles/ncu_traffic.json, tools/summarize_ncu.py);
+    None when that workload was not captured."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as fh:
-            t = json.load(fh)
-        return t.get(workload, {}).get(stage) if isinstance(t.get(workload), dict) else t.get(stage)
-    except (OSError, ValueError):
+            t = json.load(fh).get(workload, {})
+    except (OSError, ValueError, AttributeError):
         return None
+    if stage == "sort":
+        return t["sort_pass"] * npass if "sort_pass" in t else None
+    return t.get(stage)
 
 
-# ------------------------------------------------------------------ scenes / views
 def make_scene_arrays(svr, w):
     if w["scene"] == "G":
         return svr.synth_random_scene(**G_SCENE)
@@ -483,7 +487,8 @@ def run_ours(args, rank, world, local_rank):
         h2d = units_per_step * (H * W * 12 + C.sizeof(svr.svr_camera))
         e2e_note = ("scene and gradient buffers resident on device; per step each view's ground "
                     "truth (pinned host) and camera in, the loss out")
-    for i in range(max(6, args.warmup)):  # every rotating frame allocates its buffers
+    # every rotating frame sizes its buffers for every view of the timed loop
+    for i in range(max(args.e2e_steps, 6, args.warmup)):
         e2e_step(i)
     e2e_drain()
     ctx.synchronize()
@@ -521,7 +526,7 @@ def run_ours(args, rank, world, local_rank):
     achieved = byt / (kernel_ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic_from_profiles(dom, args.workload),
+                "traffic": traffic_from_profiles(dom, args.workload, npass),
                 "algorithmic_bytes": byt, "kernel_ms": kernel_ms, "peak_source": peak_src}
 
     cpu = None

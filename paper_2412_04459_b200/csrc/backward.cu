@@ -193,7 +193,6 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
                 ta = fmaxf(ta, fminf(t0, t1));
                 tb = fminf(tb, fmaxf(t0, t1));
                 const float4 va = wrec[sl][2], vb = wrec[sl][3];
-                const float V[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
                 const float seg = tb - ta;
                 const float lk = seg * dnorm * (1.0f / K);
                 float sa[K], tk[K], vk[K], qk[K][3];
@@ -204,7 +203,7 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
                     qk[k][0] = (tk[k] * dx - lo.x) * inv;
                     qk[k][1] = (tk[k] * dy - lo.y) * inv;
                     qk[k][2] = (tk[k] * dz - lo.z) * inv;
-                    vk[k] = trilinear(V, qk[k][0], qk[k][1], qk[k][2]);
+                    vk[k] = trilinear_poly(va, vb, qk[k][0], qk[k][1], qk[k][2]);
                     const float act = explin(vk[k]);
                     sum += act;
                     sa[k] = one_minus_exp_neg(lk * act);
@@ -353,8 +352,8 @@ __global__ void __launch_bounds__(256) voxel_epilogue_kernel(EpilogueArgs a) {
     const float dn[3] = {a.g_normal[3 * v], a.g_normal[3 * v + 1], a.g_normal[3 * v + 2]};
     if (dn[0] == 0.f && dn[1] == 0.f && dn[2] == 0.f) return;
     const float4* rec = a.records + v * kRecordF4;
-    const float4 va = rec[2], vb = rec[3];
-    const float V[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
+    float V[8];
+    trilinear_corners(rec[2], rec[3], V);
     float gV[8];
     voxel_normal_backward(V, dn, gV);
     const uint4* ci4 = reinterpret_cast<const uint4*>(a.corner_index + 8 * v);

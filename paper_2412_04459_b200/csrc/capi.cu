@@ -65,7 +65,7 @@ void cuda_check(cudaError_t e, const char* what) {
 void DevBuf::reserve(size_t n) {
     if (n <= bytes) return;
     release();
-    size_t alloc = std::max<size_t>(n + n / 8, 256);
+    size_t alloc = std::max<size_t>(n + n / 4, 256);  // headroom: E varies from view to view
     SVR_CUDA(cudaMalloc(&p, alloc));
     bytes = alloc;
 }

@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(kPreThreads, SVR_PRE_MINB) preprocess_kernel(D
     __syncwarp();
 #endif
 
-    float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0, r3 = r0, r4 = r0, r5 = r0;
+    float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0, r3 = r0, r4 = r0, r5 = r0;  // r0.w = 0: not visible
     if (valid) {
         const uint64_t path = a.paths[v];
         double center[3], size;
@@ -178,8 +178,10 @@ __global__ void __launch_bounds__(kPreThreads, SVR_PRE_MINB) preprocess_kernel(D
             float V[8] = {__ldg(a.density + c0.x), __ldg(a.density + c0.y), __ldg(a.density + c0.z),
                           __ldg(a.density + c0.w), __ldg(a.density + c1.x), __ldg(a.density + c1.y),
                           __ldg(a.density + c1.z), __ldg(a.density + c1.w)};
-            r2 = make_float4(V[0], V[1], V[2], V[3]);
-            r3 = make_float4(V[4], V[5], V[6], V[7]);
+            float cf[8];
+            trilinear_coeffs(V, cf);
+            r2 = make_float4(cf[0], cf[1], cf[2], cf[3]);
+            r3 = make_float4(cf[4], cf[5], cf[6], cf[7]);
             // sh_eval(normalized(center - cam.pos)) (raster.cpp:195-196, sh.hpp:48-58)
             const double dx = dsub(center[0], cam.pos[0]), dy = dsub(center[1], cam.pos[1]),
                          dz = dsub(center[2], cam.pos[2]);
@@ -236,6 +238,9 @@ __global__ void __launch_bounds__(kPreThreads, SVR_PRE_MINB) preprocess_kernel(D
             r5 = make_float4(n[0], n[1], n[2], float(1.0 / size));
         }
     }
+    // Records of visible voxels only (nothing reads the others): staged in
+    // shared memory and written back as contiguous runs.
+    __shared__ uint8_t s_vis[kPreThreads];
     float4* sr = s_rec + threadIdx.x * kRecordF4;
     sr[0] = r0;
     sr[1] = r1;
@@ -243,10 +248,17 @@ __global__ void __launch_bounds__(kPreThreads, SVR_PRE_MINB) preprocess_kernel(D
     sr[3] = r3;
     sr[4] = r4;
     sr[5] = r5;
-    __syncthreads();
+    const bool my_vis = valid && r0.w > 0.f;  // size > 0 marks a visible voxel's record
+    s_vis[threadIdx.x] = my_vis;
+    const bool all_vis = __syncthreads_and(my_vis || !valid);
     const int nblk = v0 < a.n ? int(min(uint64_t(kPreThreads), a.n - v0)) : 0;
     float4* dst = a.records + v0 * kRecordF4;
-    for (int i = threadIdx.x; i < nblk * kRecordF4; i += kPreThreads) dst[i] = s_rec[i];
+    if (all_vis) {
+        for (int i = threadIdx.x; i < nblk * kRecordF4; i += kPreThreads) dst[i] = s_rec[i];
+    } else {
+        for (int i = threadIdx.x; i < nblk * kRecordF4; i += kPreThreads)
+            if (s_vis[i / kRecordF4]) dst[i] = s_rec[i];
+    }
 }
 
 // ------------------------------------------------------------------- K4
@@ -674,7 +686,6 @@ __global__ void __launch_bounds__(256, 4) composite_kernel(DevCamera cam, Compos
             slab(lo, ix, iy, iz, ta, tb);
             const float4 va = wrec[s_][2], vb = wrec[s_][3];
             const float inv = wrec[s_][5].w;
-            const float V[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
             const float seg = tb - ta;
             const float lk = seg * dnorm * (1.0f / K);
             // voxel_alpha (field.hpp:92-116), K-point midpoint quadrature
@@ -685,7 +696,7 @@ __global__ void __launch_bounds__(256, 4) composite_kernel(DevCamera cam, Compos
                 const float qx = (tk[k] * dx - lo.x) * inv;
                 const float qy = (tk[k] * dy - lo.y) * inv;
                 const float qz = (tk[k] * dz - lo.z) * inv;
-                const float act = explin(trilinear(V, qx, qy, qz));
+                const float act = explin(trilinear_poly(va, vb, qx, qy, qz));
                 sum += act;
                 sa[k] = one_minus_exp_neg(lk * act);
             }

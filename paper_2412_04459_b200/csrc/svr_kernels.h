@@ -241,7 +241,8 @@ void launch_duplicate_list(const DevCamera& cam, uint64_t n, const uint32_t* vid
 
 // Voxel record (96 B = 6 float4), written by K1, read by K7/K9/K10:
 //   [0] lo.xyz (camera-relative min corner), size   [1] screen AABB x0,x1,y0,y1
-//   [2] V0..V3   [3] V4..V7   [4] rgb, vid (bits)   [5] unit normal, 1/size
+//   [2] c0..c3   [3] c4..c7  (trilinear_coeffs of the corner densities V0..V7)
+//   [4] rgb, vid (bits)   [5] unit normal, 1/size
 constexpr int kRecordF4 = 6;
 
 }  // namespace svrb

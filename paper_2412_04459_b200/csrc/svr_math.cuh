@@ -314,6 +314,34 @@ SVR_HD float trilinear(const float* V, float qx, float qy, float qz) {
     return b0 * wx0 + b1 * qx;
 }
 
+// The same interpolant in monomial form, f = c0 + c1 qx + c2 qy + c3 qz +
+// c4 qx qy + c5 qx qz + c6 qy qz + c7 qx qy qz: the voxel record carries the
+// coefficients (computed once per voxel by K1), so a sample costs 7 FFMA
+// instead of 7 lerps.
+SVR_HD void trilinear_coeffs(const float* V, float* c) {
+    c[0] = V[0];
+    c[1] = V[4] - V[0];
+    c[2] = V[2] - V[0];
+    c[3] = V[1] - V[0];
+    c[4] = (V[6] - V[4]) - (V[2] - V[0]);
+    c[5] = (V[5] - V[4]) - (V[1] - V[0]);
+    c[6] = (V[3] - V[2]) - (V[1] - V[0]);
+    c[7] = ((V[7] - V[6]) - (V[5] - V[4])) - ((V[3] - V[2]) - (V[1] - V[0]));
+}
+SVR_HD float trilinear_poly(float4 ca, float4 cb, float qx, float qy, float qz) {
+    const float t3 = fmaf(qy, fmaf(qz, cb.w, cb.x), fmaf(qz, cb.y, ca.y));
+    const float t6 = fmaf(qy, fmaf(qz, cb.z, ca.z), fmaf(qz, ca.w, ca.x));
+    return fmaf(qx, t3, t6);
+}
+// Corner densities back from the coefficients (epilogue's normal chain).
+SVR_HD void trilinear_corners(float4 ca, float4 cb, float* V) {
+    for (int n = 0; n < 8; ++n) {
+        const float i = float((n >> 2) & 1), j = float((n >> 1) & 1), k = float(n & 1);
+        V[n] = ca.x + i * ca.y + j * ca.z + k * ca.w + i * j * cb.x + i * k * cb.y + j * k * cb.z +
+               i * j * k * cb.w;
+    }
+}
+
 SVR_HD void trilinear_weights(float qx, float qy, float qz, float* w) {
     float wx[2] = {1.0f - qx, qx}, wy[2] = {1.0f - qy, qy}, wz[2] = {1.0f - qz, qz};
 #pragma unroll
