@@ -389,9 +389,17 @@ def run_ours(args, rank, world, local_rank):
     import paper_2412_04459_b200 as svr
 
     w = WORKLOADS[args.workload]
-    torch.cuda.set_device(local_rank)
+    # one GPU per rank; SVR_BENCH_DEVICE / SVR_BENCH_BACKEND=gloo exist only to
+    # exercise the multi-rank logic on a single-GPU box (tools/multirank_check.sh)
+    dev = int(os.environ.get("SVR_BENCH_DEVICE", local_rank))
+    backend = os.environ.get("SVR_BENCH_BACKEND", "nccl")
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
+    local_rank = dev
     ctx = svr.Context(local_rank)
     arrays = make_scene_arrays(svr, w)
     scene = svr.Scene(ctx, arrays)
