@@ -92,6 +92,9 @@ __device__ __forceinline__ float warp_transpose_sum16(float (&v)[16], int lane) 
 // division-free recursion of raster.cpp:374-407. The 15 per-entry sums
 // (8 corner densities, colour, normal, priority) are reduced across the warp
 // by recursive halving and issued as one vector of global atomics.
+#ifndef SVR_BWD_DIRECT
+#define SVR_BWD_DIRECT 4  // at most this many hit lanes: per-lane atomics instead of a reduction
+#endif
 template <int K>
 __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, BackwardArgs a) {
     __shared__ float4 s_rec[8][32][kRecordF4];
@@ -273,16 +276,34 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
                     e2 = -1;
                 }
             }
-            const float tot = warp_transpose_sum16(acc, lane);
-            const int q = lane >> 1;
-            if ((lane & 1) == 0 && q < 15) {
-                const uint32_t vid = __float_as_uint(wrec[sl][4].w);
-                float* dst;
-                if (q < 8) dst = a.g_density + __ldg(a.corner_index + 8ull * vid + q);
-                else if (q < 11) dst = a.g_color + 3ull * vid + (q - 8);
-                else if (q < 14) dst = a.g_normal + 3ull * vid + (q - 11);
-                else dst = a.g_priority + vid;
-                atomicAdd(dst, tot);
+            const uint32_t vid = __float_as_uint(wrec[sl][4].w);
+            const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+            if (__popc(hm) <= SVR_BWD_DIRECT) {
+                // few pixels: each one adds its own 15 values (no 31-shuffle reduction)
+                if (hit) {
+                    const uint4* ci4 = reinterpret_cast<const uint4*>(a.corner_index + 8ull * vid);
+                    const uint4 k0 = __ldg(ci4), k1 = __ldg(ci4 + 1);
+                    const uint32_t ci[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) atomicAdd(a.g_density + ci[c], acc[c]);
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        atomicAdd(a.g_color + 3ull * vid + c, acc[8 + c]);
+                        atomicAdd(a.g_normal + 3ull * vid + c, acc[11 + c]);
+                    }
+                    atomicAdd(a.g_priority + vid, acc[14]);
+                }
+            } else {
+                const float tot = warp_transpose_sum16(acc, lane);
+                const int q = lane >> 1;
+                if ((lane & 1) == 0 && q < 15) {
+                    float* dst;
+                    if (q < 8) dst = a.g_density + __ldg(a.corner_index + 8ull * vid + q);
+                    else if (q < 11) dst = a.g_color + 3ull * vid + (q - 8);
+                    else if (q < 14) dst = a.g_normal + 3ull * vid + (q - 11);
+                    else dst = a.g_priority + vid;
+                    atomicAdd(dst, tot);
+                }
             }
             cur = __reduce_max_sync(0xffffffffu, unsigned(e1 + 1)) - 1;
         }
