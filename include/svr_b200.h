@@ -226,6 +226,25 @@ typedef struct svr_gradients {
 int svr_render_backward(svr_ctx* ctx, const svr_scene* scene, svr_frame* frame,
                         const svr_upstream* up, svr_gradients* out);
 
+/* ray_losses (losses.cpp:141-238) on the device, over the frame's forward
+ * records (render with training = 1): transmittance entropy L_T, distortion
+ * L_dist and per-voxel colour L_R. gt is the W*H*3 target image (f32); each
+ * supersampled ray reads the gt pixel its footprint falls in. The weighted
+ * gradients are ACCUMULATED (+=, like UpstreamGrads in the reference) into
+ * d_tfin_ss (sw*sh), d_weight (n_contribs) and d_voxel_color (n_contribs*3),
+ * which any of may be NULL when its weights are zero. All pointers are
+ * device pointers when on_device, else host. Loss values (unweighted, as
+ * RayLossValues) go to *out. */
+typedef struct svr_ray_loss_weights {
+    double w_T, w_dist, w_R;
+} svr_ray_loss_weights;
+typedef struct svr_ray_loss_values {
+    double l_T, l_dist, l_R;
+} svr_ray_loss_values;
+int svr_ray_losses(svr_ctx* ctx, svr_frame* frame, const float* gt,
+                   const svr_ray_loss_weights* weights, svr_ray_loss_values* out,
+                   float* d_tfin_ss, float* d_weight, float* d_voxel_color, int32_t on_device);
+
 /* L1 photometric loss on the rendered colour (new; pattern of mse_loss,
  * losses.cpp:121-131): L = mean|C-gt|, dL/dC = sign(C-gt)/(3WH). gt is a
  * device pointer (W*H*3 f32); d_color (device, W*H*3) receives the gradient;

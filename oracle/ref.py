@@ -275,6 +275,18 @@ class RefFrame:
         load_ref().ref_frame_records(self.h, _p(pre), _p(cp), _p(ca), _p(cb), _p(pb), _p(pc), _p(tf))
         return pre, cp, ca, cb, pb, pc, tf
 
+    def ray_losses(self, gt, w_T=0.0, w_dist=0.0, w_R=0.0):
+        """svr::ray_losses (losses.cpp:141-238) on this frame's records:
+        ((l_T, l_dist, l_R), d_tfin_ss, d_weight, d_voxel_color)."""
+        g = np.ascontiguousarray(gt, np.float64).reshape(-1)
+        vals = np.zeros(3)
+        dtf = np.zeros(self.sw * self.sh)
+        dw = np.zeros(self.n_contribs)
+        dvc = np.zeros(self.n_contribs * 3)
+        _chk(load_ref().ref_frame_ray_losses(self.h, _p(g), C.c_double(w_T), C.c_double(w_dist),
+                                             C.c_double(w_R), _p(vals), _p(dtf), _p(dw), _p(dvc)))
+        return tuple(vals), dtf, dw, dvc.reshape(-1, 3)
+
     def backward(self, n_pool, n_sh, n_vox, d_color=None, d_depth=None, d_normal=None,
                  d_tfin_ss=None, d_weight=None, d_voxel_color=None):
         keep = [None if x is None else np.ascontiguousarray(x, np.float64).reshape(-1)

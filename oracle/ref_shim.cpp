@@ -408,6 +408,36 @@ void ref_frame_records(void* fh, uint32_t* pre_vids, uint32_t* contrib_pre, doub
     if (ss_tfin) copy_img(r.ss_tfin, ss_tfin);
 }
 
+// ray_losses (losses.cpp:141-238) on a training frame; fresh zero upstream
+// buffers sized by the reference itself, copied out (NULL = not wanted).
+int ref_frame_ray_losses(void* fh, const double* gt, double w_T, double w_dist, double w_R,
+                         double* values, double* d_tfin_ss, double* d_weight,
+                         double* d_voxel_color) {
+    return guarded([&] {
+        auto* f = static_cast<Frame*>(fh);
+        const ForwardRecords& r = *f->rec;
+        const int W = f->out.color.width, H = f->out.color.height;
+        Image g(W, H, 3);
+        std::memcpy(g.data.data(), gt, g.data.size() * sizeof(double));
+        RayLossWeights w;
+        w.w_T = w_T;
+        w.w_dist = w_dist;
+        w.w_R = w_R;
+        UpstreamGrads ug;
+        RayLossValues v = ray_losses(SparseScene{}, r, g, w, ug);
+        values[0] = v.l_T;
+        values[1] = v.l_dist;
+        values[2] = v.l_R;
+        if (d_tfin_ss && !ug.d_tfin_ss.empty())
+            std::memcpy(d_tfin_ss, ug.d_tfin_ss.data(), ug.d_tfin_ss.size() * sizeof(double));
+        if (d_weight && !ug.d_weight.empty())
+            std::memcpy(d_weight, ug.d_weight.data(), ug.d_weight.size() * sizeof(double));
+        if (d_voxel_color)
+            for (size_t i = 0; i < ug.d_voxel_color.size(); ++i)
+                for (int c = 0; c < 3; ++c) d_voxel_color[3 * i + c] = ug.d_voxel_color[i][c];
+    });
+}
+
 // render_backward with image-level upstream grads at target resolution.
 // Any pointer may be NULL (= empty buffer = zero, raster.hpp:100-110).
 int ref_backward(void* h, void* fh, const double* d_color, const double* d_depth,

@@ -92,6 +92,14 @@ class svr_upstream(C.Structure):
                 ("n_d_voxel_color", C.c_uint64), ("on_device", C.c_int32)]
 
 
+class svr_ray_loss_weights(C.Structure):
+    _fields_ = [("w_T", C.c_double), ("w_dist", C.c_double), ("w_R", C.c_double)]
+
+
+class svr_ray_loss_values(C.Structure):
+    _fields_ = [("l_T", C.c_double), ("l_dist", C.c_double), ("l_R", C.c_double)]
+
+
 class svr_gradients(C.Structure):
     _fields_ = [("density", C.c_void_p), ("sh", C.c_void_p), ("priority", C.c_void_p),
                 ("on_device", C.c_int32)]
@@ -110,7 +118,7 @@ EXPORTS = [
     "svr_scene_destroy", "svr_scene_param_ptrs", "svr_frame_create", "svr_frame_destroy",
     "svr_render", "svr_frame_get_info", "svr_frame_download", "svr_frame_device_ptr",
     "svr_frame_download_async", "svr_frame_wait", "svr_frame_records", "svr_render_backward",
-    "svr_l1_loss", "svr_train_step_l1",
+    "svr_l1_loss", "svr_train_step_l1", "svr_ray_losses",
     "svr_project_voxels", "svr_tile_sign_masks", "svr_build_sort_entries", "svr_sort_entries",
     "svr_synth_random_scene", "svr_ring_camera", "svr_free", "svr_launch_count",
     "svr_ctx_enable_timing", "svr_ctx_stage_times", "svr_frame_pre", "svr_render_oracle",
@@ -147,6 +155,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                            C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         "svr_frame_create": (C.c_int, [P, C.POINTER(P)]),
         "svr_frame_download_async": (C.c_int, [P, C.c_int, P, C.c_size_t]),
+        "svr_ray_losses": (C.c_int, [P, P, P, C.POINTER(svr_ray_loss_weights),
+                                     C.POINTER(svr_ray_loss_values), P, P, P, C.c_int32]),
         "svr_frame_wait": (C.c_int, [P]),
         "svr_frame_destroy": (C.c_int, [P]),
         "svr_render": (C.c_int, [P, P, C.POINTER(svr_camera), C.POINTER(svr_render_options), P]),
@@ -560,6 +570,25 @@ def render_backward(scene: Scene, frame: Frame, d_color=None, d_depth=None, d_no
     _check(scene.ctx._lib.svr_render_backward(scene.ctx.h, scene.h, frame.h, C.byref(u),
                                               C.byref(g)))
     return SceneGradients(gd, gs.reshape(a.n_voxels, a.sh_stride), gp)
+
+
+def ray_losses(frame: Frame, gt, w_T: float = 0.0, w_dist: float = 0.0, w_R: float = 0.0,
+               d_tfin_ss=None, d_weight=None, d_voxel_color=None):
+    """svr::ray_losses (losses.cpp:141-238) on the device over `frame`'s
+    forward records. Host path: the gradient arrays (float32, created zeroed
+    when None) are accumulated into and returned with the loss values:
+    ((l_T, l_dist, l_R), d_tfin_ss, d_weight, d_voxel_color)."""
+    inf = frame.info()
+    nss, nc = inf.ss_width * inf.ss_height, inf.n_contribs
+    g = np.ascontiguousarray(gt, dtype=np.float32).reshape(-1)
+    dtf = np.zeros(nss, np.float32) if d_tfin_ss is None else d_tfin_ss
+    dw = np.zeros(nc, np.float32) if d_weight is None else d_weight
+    dvc = np.zeros(nc * 3, np.float32) if d_voxel_color is None else d_voxel_color
+    w = svr_ray_loss_weights(w_T, w_dist, w_R)
+    v = svr_ray_loss_values()
+    _check(frame.ctx._lib.svr_ray_losses(frame.ctx.h, frame.h, _ptr(g), C.byref(w), C.byref(v),
+                                         _ptr(dtf), _ptr(dw), _ptr(dvc), 0))
+    return (v.l_T, v.l_dist, v.l_R), dtf, dw, dvc.reshape(-1, 3)
 
 
 # ---------------------------------------------------------------- pipeline pieces

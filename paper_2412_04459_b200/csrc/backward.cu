@@ -311,6 +311,134 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
     }
 }
 
+// ray_losses (losses.cpp:141-238). One thread per supersampled pixel, laid
+// out like the compositing tiles; each walks its own contribution list
+// (independent trip counts, same code). Per contribution the weight
+// w = T_i * alpha_i is recomputed from the voxel record exactly as the
+// forward composited it (fp32 slab + quadrature), m = (a + b) / 2 and
+// l = b - a from the same slab. L_dist keeps the reference's structure:
+// a forward pass with prefix sums (its intra-segment term included) writes
+// (w, m) to scratch, a reverse pass adds the suffix half.
+template <int K>
+__global__ void __launch_bounds__(256) ray_losses_kernel(DevCamera cam, RayLossArgs a) {
+    const int tile = blockIdx.x;
+    const int tx = tile % cam.ntx, ty = tile / cam.ntx;
+    const int px = tx * kTile + (threadIdx.x & 15), py = ty * kTile + (threadIdx.x >> 4);
+    const bool inside = px < cam.W && py < cam.H;
+    const double inv_rays = 1.0 / (double(cam.W) * cam.H);
+    float lT = 0.f, ldist = 0.f, lR = 0.f;
+    if (inside) {
+        const uint32_t slot = uint32_t(tile) * 256u + threadIdx.x;
+        const uint64_t pix = uint64_t(py) * cam.W + px;
+        if (a.w_T != 0.0) {
+            const double eps = 1e-6;
+            const double T = a.tfin[pix];
+            const double Tc = fmin(fmax(T, eps), 1.0 - eps);
+            lT = float(-(Tc * log(Tc) + (1.0 - Tc) * log(1.0 - Tc)));
+            if (T > eps && T < 1.0 - eps && a.d_tfin_ss)
+                a.d_tfin_ss[pix] += float(a.w_T * (log(1.0 - Tc) - log(Tc)) * inv_rays);
+        }
+        const uint32_t n = a.pix_count[slot];
+        if (n > 0 && (a.w_dist != 0.0 || a.w_R != 0.0)) {
+            const uint32_t base = a.pix_begin[slot];
+            const uint64_t rb = a.stage_stride ? slot : base;
+            const uint64_t rs = a.stage_stride ? a.stage_stride : 1u;
+            double dd[3];
+            pixel_ray_dir(cam, double(px), double(py), dd);
+            const float dx = float(dd[0]), dy = float(dd[1]), dz = float(dd[2]);
+            const float ix = 1.0f / dx, iy = 1.0f / dy, iz = 1.0f / dz;
+            const float dnorm = float(sqrt(dd[0] * dd[0] + dd[1] * dd[1] + dd[2] * dd[2]));
+            float g[3] = {0.f, 0.f, 0.f};
+            if (a.w_R != 0.0) {
+                const int gx = min(a.gt_w - 1, px * a.gt_w / cam.W);
+                const int gy = min(a.gt_h - 1, py * a.gt_h / cam.H);
+                const float* gp = a.gt + (uint64_t(gy) * a.gt_w + gx) * 3;
+                g[0] = gp[0], g[1] = gp[1], g[2] = gp[2];
+            }
+            constexpr uint32_t kVidMask = (1u << 29) - 1u;
+            float Wpre = 0.f, Spre = 0.f;
+            for (uint32_t i = 0; i < n; ++i) {
+                const uint32_t e = a.contrib_entry[rb + i * rs];
+                const float T = a.contrib_T[rb + i * rs];
+                const float4* rec = a.records + uint64_t(__ldg(a.vals + e) & kVidMask) * kRecordF4;
+                const float4 lo = __ldg(rec);
+                const float inv = __ldg(rec + 5).w;
+                float t0 = lo.x * ix, t1 = (lo.x + lo.w) * ix;
+                float ta = fminf(t0, t1), tb = fmaxf(t0, t1);
+                t0 = lo.y * iy;
+                t1 = (lo.y + lo.w) * iy;
+                ta = fmaxf(ta, fminf(t0, t1));
+                tb = fminf(tb, fmaxf(t0, t1));
+                t0 = lo.z * iz;
+                t1 = (lo.z + lo.w) * iz;
+                ta = fmaxf(ta, fminf(t0, t1));
+                tb = fminf(tb, fmaxf(t0, t1));
+                const float4 va = __ldg(rec + 2), vb = __ldg(rec + 3);
+                const float seg = tb - ta;
+                const float lk = seg * dnorm * (1.0f / K);
+                float sum = 0.f, sa0 = 0.f;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const float tk = ta + ((k + 0.5f) / K) * seg;
+                    const float act = explin(trilinear_poly(va, vb, (tk * dx - lo.x) * inv,
+                                                            (tk * dy - lo.y) * inv, (tk * dz - lo.z) * inv));
+                    sum += act;
+                    if (K == 1) sa0 = one_minus_exp_neg(lk * act);
+                }
+                const float alpha = (K == 1) ? sa0 : one_minus_exp_neg(lk * sum);
+                const float w = T * alpha, m = 0.5f * (ta + tb), dl = tb - ta;
+                float dw = 0.f;
+                if (a.w_dist != 0.0) {
+                    ldist += 2.f * w * (m * Wpre - Spre) + w * w * dl * (1.0f / 3.0f);
+                    dw = 2.f * (m * Wpre - Spre) + 2.f * w * dl * (1.0f / 3.0f);
+                    Wpre += w;
+                    Spre += w * m;
+                    a.scratch[base + i] = make_float2(w, m);
+                }
+                float gdw = float(a.w_dist) * dw;  // the suffix half follows below
+                if (a.w_R != 0.0) {
+                    const float4 col = __ldg(rec + 4);
+                    const float e0 = col.x - g[0], e1 = col.y - g[1], e2 = col.z - g[2];
+                    const float err = e0 * e0 + e1 * e1 + e2 * e2;
+                    lR += w * err;
+                    gdw += float(a.w_R) * err;
+                    const float s = float(a.w_R * 2.0 * inv_rays) * w;
+                    float* dvc = a.d_voxel_color + 3ull * (base + i);
+                    dvc[0] += s * e0;
+                    dvc[1] += s * e1;
+                    dvc[2] += s * e2;
+                }
+                a.d_weight[base + i] += gdw * float(inv_rays);
+            }
+            if (a.w_dist != 0.0) {  // suffix half of d|m_i - m_j|
+                float Wsuf = 0.f, Ssuf = 0.f;
+                for (int i = int(n) - 1; i >= 0; --i) {
+                    const float2 wm = a.scratch[base + i];
+                    a.d_weight[base + i] += float(a.w_dist * inv_rays) * (2.f * (Ssuf - wm.y * Wsuf));
+                    Wsuf += wm.x;
+                    Ssuf += wm.x * wm.y;
+                }
+            }
+        }
+    }
+    // block sums -> one double atomic per value per block
+    __shared__ float s_red[3][8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lT += __shfl_xor_sync(0xffffffffu, lT, o);
+        ldist += __shfl_xor_sync(0xffffffffu, ldist, o);
+        lR += __shfl_xor_sync(0xffffffffu, lR, o);
+    }
+    if (lane == 0) s_red[0][warp] = lT, s_red[1][warp] = ldist, s_red[2][warp] = lR;
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += s_red[threadIdx.x][w];
+        atomicAdd(a.sums + threadIdx.x, t * inv_rays);
+    }
+}
+
 // K10: 16 lanes per voxel, lane m owns SH basis function m, so the SH rows
 // (3(d+1)^2 floats per voxel) are read and written as contiguous runs. The
 // raw colour for the clamp mask (sh.hpp:66-74) is reduced over the 16 lanes;
@@ -419,6 +547,17 @@ void launch_composite_backward(const DevCamera& cam, const BackwardArgs& a, cuda
             throw Error(SVR_ERR_INVALID_ARGUMENT, "rasterizer sample count K must be in {1,2,3}");
     }
     SVR_LAUNCH("composite_backward_kernel");
+}
+
+void launch_ray_losses(const DevCamera& cam, const RayLossArgs& a, cudaStream_t st) {
+    const unsigned ntiles = unsigned(cam.ntx * cam.nty);
+    switch (a.K) {
+        case 1: ray_losses_kernel<1><<<ntiles, 256, 0, st>>>(cam, a); break;
+        case 2: ray_losses_kernel<2><<<ntiles, 256, 0, st>>>(cam, a); break;
+        case 3: ray_losses_kernel<3><<<ntiles, 256, 0, st>>>(cam, a); break;
+        default: throw Error(SVR_ERR_INVALID_ARGUMENT, "rasterizer sample count K must be in {1,2,3}");
+    }
+    SVR_LAUNCH("ray_losses_kernel");
 }
 
 void launch_voxel_epilogue(const DevCamera& cam, const EpilogueArgs& a, cudaStream_t st) {

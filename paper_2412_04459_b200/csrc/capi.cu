@@ -1067,6 +1067,79 @@ int svr_l1_loss(svr_ctx* ctx, svr_frame* f, const float* gt, float* d_color, flo
     });
 }
 
+int svr_ray_losses(svr_ctx* ctx, svr_frame* f, const float* gt, const svr_ray_loss_weights* w,
+                   svr_ray_loss_values* out, float* d_tfin_ss, float* d_weight,
+                   float* d_voxel_color, int32_t on_device) {
+    return guard([&] {
+        require(ctx && f && gt && w && out, SVR_ERR_INVALID_ARGUMENT, "null argument");
+        require(f->has_records, SVR_ERR_RUNTIME,
+                "frame has no forward records (render with training = true)");
+        // losses.cpp:154-161 sizes the upstream buffers the weights need
+        require(w->w_T == 0.0 || d_tfin_ss, SVR_ERR_INVALID_ARGUMENT, "w_T needs d_tfin_ss");
+        require((w->w_dist == 0.0 && w->w_R == 0.0) || d_weight, SVR_ERR_INVALID_ARGUMENT,
+                "w_dist / w_R need d_weight");
+        require(w->w_R == 0.0 || d_voxel_color, SVR_ERR_INVALID_ARGUMENT, "w_R needs d_voxel_color");
+        set_device(ctx);
+        wait_copies(f);
+        cudaStream_t st = ctx->stream;
+        const uint64_t nss = uint64_t(f->sw) * f->sh, C = f->n_contribs;
+        const uint64_t ngt = uint64_t(f->W) * f->H * 3;
+        const bool ss1 = (f->sw == f->W && f->sh == f->H);
+        float *dgt = const_cast<float*>(gt), *dtf = d_tfin_ss, *dw = d_weight, *dvc = d_voxel_color;
+        DevBuf tgt, ttf, tw, tvc;
+        if (!on_device) {
+            dgt = grow<float>(tgt, ngt);
+            SVR_CUDA(cudaMemcpyAsync(dgt, gt, ngt * 4, cudaMemcpyHostToDevice, st));
+            auto stage = [&](float* h, DevBuf& b, uint64_t n) -> float* {
+                if (!h) return nullptr;
+                float* d = grow<float>(b, n);
+                SVR_CUDA(cudaMemcpyAsync(d, h, n * 4, cudaMemcpyHostToDevice, st));
+                return d;
+            };
+            dtf = stage(d_tfin_ss, ttf, nss);
+            dw = stage(d_weight, tw, C);
+            dvc = stage(d_voxel_color, tvc, C * 3);
+        }
+        double* sums = grow<double>(f->rl_sums, 3);
+        SVR_CUDA(cudaMemsetAsync(sums, 0, 3 * sizeof(double), st));
+        RayLossArgs ra{};
+        ra.ranges = f->ranges.as<uint2>();
+        ra.vals = f->vals[f->vals_buf].as<uint32_t>();
+        ra.records = f->records.as<float4>();
+        ra.K = f->opts.K;
+        ra.pix_count = f->pix_count.as<uint32_t>();
+        ra.pix_begin = f->pix_begin.as<uint32_t>();
+        ra.contrib_entry = f->staged ? f->stage_entry.as<uint32_t>() : f->contrib_entry.as<uint32_t>();
+        ra.contrib_T = f->staged ? f->stage_T.as<float>() : f->contrib_T.as<float>();
+        ra.stage_stride = f->staged ? uint32_t(uint64_t(f->ntx) * f->nty * 256) : 0u;
+        ra.tfin = ss1 ? f->out_tfin.as<float>() : f->ss_tfin.as<float>();
+        ra.gt = dgt;
+        ra.gt_w = f->W;
+        ra.gt_h = f->H;
+        ra.w_T = w->w_T;
+        ra.w_dist = w->w_dist;
+        ra.w_R = w->w_R;
+        ra.d_tfin_ss = dtf;
+        ra.d_weight = dw;
+        ra.d_voxel_color = dvc;
+        ra.scratch = w->w_dist != 0.0 ? grow<float2>(f->rl_scratch, std::max<uint64_t>(C, 1)) : nullptr;
+        ra.sums = sums;
+        launch_ray_losses(f->cam, ra, st);
+        double hs[3];
+        SVR_CUDA(cudaMemcpyAsync(hs, sums, sizeof(hs), cudaMemcpyDeviceToHost, st));
+        if (!on_device) {
+            if (d_tfin_ss) SVR_CUDA(cudaMemcpyAsync(d_tfin_ss, dtf, nss * 4, cudaMemcpyDeviceToHost, st));
+            if (d_weight) SVR_CUDA(cudaMemcpyAsync(d_weight, dw, C * 4, cudaMemcpyDeviceToHost, st));
+            if (d_voxel_color)
+                SVR_CUDA(cudaMemcpyAsync(d_voxel_color, dvc, C * 12, cudaMemcpyDeviceToHost, st));
+        }
+        SVR_CUDA(cudaStreamSynchronize(st));
+        out->l_T = w->w_T != 0.0 ? hs[0] : 0.0;
+        out->l_dist = w->w_dist != 0.0 ? hs[1] : 0.0;
+        out->l_R = w->w_R != 0.0 ? hs[2] : 0.0;
+    });
+}
+
 int svr_train_step_l1(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam,
                       const svr_render_options* opts, const float* gt_device, svr_frame* f,
                       svr_gradients* grads, int accumulate, float* loss_device) {

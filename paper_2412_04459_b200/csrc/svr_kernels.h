@@ -182,6 +182,29 @@ void launch_lift(const TapTable& transposed, const float* g, int channels, int W
 void launch_l1_loss(const float* color, const float* gt, uint64_t n, float* d_color, float* loss,
                     cudaStream_t st);
 
+// ray_losses (losses.cpp:141-238) over device forward records.
+struct RayLossArgs {
+    const uint2* ranges;
+    const uint32_t* vals;
+    const float4* records;
+    int K;
+    const uint32_t* pix_count;      // tile-major
+    const uint32_t* pix_begin;
+    const uint32_t* contrib_entry;  // compact, or staged when stage_stride > 0
+    const float* contrib_T;
+    uint32_t stage_stride;
+    const float* tfin;              // ss image, row-major (sw*sh)
+    const float* gt;                // W*H*3
+    int gt_w, gt_h;
+    double w_T, w_dist, w_R;
+    float* d_tfin_ss;               // sw*sh, +=
+    float* d_weight;                // n_contribs, +=
+    float* d_voxel_color;           // n_contribs*3, +=
+    float2* scratch;                // n_contribs: (w, m) per contribution
+    double* sums;                   // 3: l_T, l_dist, l_R (+=)
+};
+void launch_ray_losses(const DevCamera& cam, const RayLossArgs& a, cudaStream_t st);
+
 struct BackwardArgs {
     const uint2* ranges;
     const uint32_t* tile_order;  // optional LPT tile schedule (forward's)
