@@ -245,6 +245,20 @@ int svr_ray_losses(svr_ctx* ctx, svr_frame* frame, const float* gt,
                    const svr_ray_loss_weights* weights, svr_ray_loss_values* out,
                    float* d_tfin_ss, float* d_weight, float* d_voxel_color, int32_t on_device);
 
+/* adam_step (optim.cpp:322-345) over a float parameter pool on the device:
+ * m, v are the fp64 moment buffers (AdamState, zero-initialised by the
+ * caller), `step` the updated step count (state.step after ++), so
+ * bc1 = 1 - beta1^step and bc2 = 1 - beta2^step are the reference's. The
+ * per-element learning rate is lr, or lr_alt for elements with
+ * (i % period) >= n_primary when period > 0 (the reference's SH rule:
+ * period = stride, n_primary = 3). Double arithmetic in the reference's
+ * order, so the float parameters match it bit for bit given the same
+ * gradients. A NaN gradient returns SVR_ERR_RUNTIME (std::runtime_error).
+ * All pointers are device pointers when on_device, else host. */
+int svr_adam_step(svr_ctx* ctx, float* params, const float* grads, double* m, double* v,
+                  uint64_t n, int64_t step, double lr, double lr_alt, uint32_t period,
+                  uint32_t n_primary, double beta1, double beta2, double eps, int32_t on_device);
+
 /* L1 photometric loss on the rendered colour (new; pattern of mse_loss,
  * losses.cpp:121-131): L = mean|C-gt|, dL/dC = sign(C-gt)/(3WH). gt is a
  * device pointer (W*H*3 f32); d_color (device, W*H*3) receives the gradient;

@@ -306,6 +306,20 @@ class RefFrame:
             pass
 
 
+def ref_adam_step(params, grads, m, v, step_before, lr, lr_alt=0.0, period=0, n_primary=0,
+                  beta1=0.1, beta2=0.99, eps=1e-15):
+    """svr::adam_step (optim.cpp:322-345) on copies; returns (params, m, v)."""
+    p = np.ascontiguousarray(params, np.float32).copy()
+    g = np.ascontiguousarray(grads, np.float64)
+    mm = np.ascontiguousarray(m, np.float64).copy()
+    vv = np.ascontiguousarray(v, np.float64).copy()
+    _chk(load_ref().ref_adam_step(_p(p), _p(g), _p(mm), _p(vv), C.c_uint64(p.size),
+                                  C.c_int64(step_before), C.c_double(lr), C.c_double(lr_alt),
+                                  C.c_uint32(period), C.c_uint32(n_primary), C.c_double(beta1),
+                                  C.c_double(beta2), C.c_double(eps)))
+    return p, mm, vv
+
+
 def ref_train_step_l1(scene: RefScene, cam, opts, gt, n_pool, n_sh, n_vox):
     c, o = cam.to_c(), opts.to_c()
     gt = np.ascontiguousarray(gt, np.float64)

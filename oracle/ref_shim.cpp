@@ -11,6 +11,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <random>
 #include <stdexcept>
@@ -406,6 +407,28 @@ void ref_frame_records(void* fh, uint32_t* pre_vids, uint32_t* contrib_pre, doub
     if (pix_begin) std::memcpy(pix_begin, r.pix_begin.data(), r.pix_begin.size() * 4);
     if (pix_count) std::memcpy(pix_count, r.pix_count.data(), r.pix_count.size() * 4);
     if (ss_tfin) copy_img(r.ss_tfin, ss_tfin);
+}
+
+// adam_step (optim.cpp:322-345) on host arrays: params (float), grads
+// (double), moments (double); lr_alt applies where i % period >= n_primary.
+int ref_adam_step(float* params, const double* grads, double* m, double* v, uint64_t n,
+                  int64_t step_before, double lr, double lr_alt, uint32_t period,
+                  uint32_t n_primary, double beta1, double beta2, double eps) {
+    return guarded([&] {
+        std::vector<float> p(params, params + n);
+        std::vector<double> g(grads, grads + n);
+        AdamState st;
+        st.m.assign(m, m + n);
+        st.v.assign(v, v + n);
+        st.step = step_before;
+        std::function<double(size_t)> lr_of = nullptr;
+        if (period)
+            lr_of = [&](size_t i) { return (i % period) >= n_primary ? lr_alt : lr; };
+        adam_step(p, g, st, lr, lr_of, beta1, beta2, eps);
+        std::memcpy(params, p.data(), n * 4);
+        std::memcpy(m, st.m.data(), n * 8);
+        std::memcpy(v, st.v.data(), n * 8);
+    });
 }
 
 // ray_losses (losses.cpp:141-238) on a training frame; fresh zero upstream

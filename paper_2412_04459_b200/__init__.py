@@ -118,7 +118,7 @@ EXPORTS = [
     "svr_scene_destroy", "svr_scene_param_ptrs", "svr_frame_create", "svr_frame_destroy",
     "svr_render", "svr_frame_get_info", "svr_frame_download", "svr_frame_device_ptr",
     "svr_frame_download_async", "svr_frame_wait", "svr_frame_records", "svr_render_backward",
-    "svr_l1_loss", "svr_train_step_l1", "svr_ray_losses",
+    "svr_l1_loss", "svr_train_step_l1", "svr_ray_losses", "svr_adam_step",
     "svr_project_voxels", "svr_tile_sign_masks", "svr_build_sort_entries", "svr_sort_entries",
     "svr_synth_random_scene", "svr_ring_camera", "svr_free", "svr_launch_count",
     "svr_ctx_enable_timing", "svr_ctx_stage_times", "svr_frame_pre", "svr_render_oracle",
@@ -155,6 +155,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                            C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         "svr_frame_create": (C.c_int, [P, C.POINTER(P)]),
         "svr_frame_download_async": (C.c_int, [P, C.c_int, P, C.c_size_t]),
+        "svr_adam_step": (C.c_int, [P, P, P, P, P, C.c_uint64, C.c_int64, C.c_double, C.c_double,
+                                    C.c_uint32, C.c_uint32, C.c_double, C.c_double, C.c_double,
+                                    C.c_int32]),
         "svr_ray_losses": (C.c_int, [P, P, P, C.POINTER(svr_ray_loss_weights),
                                      C.POINTER(svr_ray_loss_values), P, P, P, C.c_int32]),
         "svr_frame_wait": (C.c_int, [P]),
@@ -589,6 +592,29 @@ def ray_losses(frame: Frame, gt, w_T: float = 0.0, w_dist: float = 0.0, w_R: flo
     _check(frame.ctx._lib.svr_ray_losses(frame.ctx.h, frame.h, _ptr(g), C.byref(w), C.byref(v),
                                          _ptr(dtf), _ptr(dw), _ptr(dvc), 0))
     return (v.l_T, v.l_dist, v.l_R), dtf, dw, dvc.reshape(-1, 3)
+
+
+class AdamState:
+    """optim.hpp:112-115 on the device: fp64 moments, step count."""
+
+    def __init__(self, n: int, device: int = 0):
+        import torch
+        dev = torch.device("cuda", device)
+        self.m = torch.zeros(n, dtype=torch.float64, device=dev)
+        self.v = torch.zeros(n, dtype=torch.float64, device=dev)
+        self.step = 0
+
+
+def adam_step(ctx: Context, params, grads, state: AdamState, lr: float, lr_alt: float = 0.0,
+              period: int = 0, n_primary: int = 0, beta1: float = 0.1, beta2: float = 0.99,
+              eps: float = 1e-15) -> None:
+    """svr::adam_step (optim.cpp:322-345) on device tensors (float32 params
+    and grads, the AdamState's fp64 moments), in place on the context stream."""
+    state.step += 1
+    _check(ctx._lib.svr_adam_step(ctx.h, C.c_void_p(params.data_ptr()),
+                                  C.c_void_p(grads.data_ptr()), C.c_void_p(state.m.data_ptr()),
+                                  C.c_void_p(state.v.data_ptr()), params.numel(), state.step, lr,
+                                  lr_alt, period, n_primary, beta1, beta2, eps, 1))
 
 
 # ---------------------------------------------------------------- pipeline pieces

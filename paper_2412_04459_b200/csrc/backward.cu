@@ -439,6 +439,29 @@ __global__ void __launch_bounds__(256) ray_losses_kernel(DevCamera cam, RayLossA
     }
 }
 
+// adam_step (optim.cpp:322-345): HBM-bound elementwise update, grid-stride.
+// Every double operation is explicitly rounded (no FMA contraction) in the
+// reference's order, so params match std::vector<float> updates exactly.
+__global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < a.n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const double g = double(a.grads[i]);
+        if (isnan(g)) {
+            atomicOr(a.nan_flag, 1u);
+            continue;
+        }
+        const double m = __dadd_rn(__dmul_rn(a.beta1, a.m[i]), __dmul_rn(__dsub_rn(1.0, a.beta1), g));
+        const double v = __dadd_rn(__dmul_rn(a.beta2, a.v[i]),
+                                   __dmul_rn(__dmul_rn(__dsub_rn(1.0, a.beta2), g), g));
+        a.m[i] = m;
+        a.v[i] = v;
+        const double mhat = __ddiv_rn(m, a.bc1), vhat = __ddiv_rn(v, a.bc2);
+        const double lr = (a.period && (i % a.period) >= a.n_primary) ? a.lr_alt : a.lr;
+        const double step = __ddiv_rn(__dmul_rn(lr, mhat), __dadd_rn(__dsqrt_rn(vhat), a.eps));
+        a.params[i] = float(__dsub_rn(double(a.params[i]), step));
+    }
+}
+
 // K10: 16 lanes per voxel, lane m owns SH basis function m, so the SH rows
 // (3(d+1)^2 floats per voxel) are read and written as contiguous runs. The
 // raw colour for the clamp mask (sh.hpp:66-74) is reduced over the 16 lanes;
@@ -558,6 +581,13 @@ void launch_ray_losses(const DevCamera& cam, const RayLossArgs& a, cudaStream_t 
         default: throw Error(SVR_ERR_INVALID_ARGUMENT, "rasterizer sample count K must be in {1,2,3}");
     }
     SVR_LAUNCH("ray_losses_kernel");
+}
+
+void launch_adam(const AdamArgs& a, cudaStream_t st) {
+    if (a.n == 0) return;
+    const unsigned blocks = unsigned(std::min<uint64_t>(blocks_for(a.n, 256), 148 * 16));
+    adam_kernel<<<blocks, 256, 0, st>>>(a);
+    SVR_LAUNCH("adam_kernel");
 }
 
 void launch_voxel_epilogue(const DevCamera& cam, const EpilogueArgs& a, cudaStream_t st) {

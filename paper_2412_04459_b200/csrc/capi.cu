@@ -1140,6 +1140,59 @@ int svr_ray_losses(svr_ctx* ctx, svr_frame* f, const float* gt, const svr_ray_lo
     });
 }
 
+int svr_adam_step(svr_ctx* ctx, float* params, const float* grads, double* m, double* v,
+                  uint64_t n, int64_t step, double lr, double lr_alt, uint32_t period,
+                  uint32_t n_primary, double beta1, double beta2, double eps, int32_t on_device) {
+    return guard([&] {
+        require(ctx && (n == 0 || (params && grads && m && v)), SVR_ERR_INVALID_ARGUMENT,
+                "null argument");
+        require(step >= 1, SVR_ERR_INVALID_ARGUMENT, "adam_step: step counts from 1");
+        set_device(ctx);
+        cudaStream_t st = ctx->stream;
+        AdamArgs a{};
+        a.n = n;
+        // optim.cpp:334-335, on the host exactly as the reference
+        a.bc1 = 1.0 - std::pow(beta1, double(step));
+        a.bc2 = 1.0 - std::pow(beta2, double(step));
+        a.lr = lr;
+        a.lr_alt = lr_alt;
+        a.beta1 = beta1;
+        a.beta2 = beta2;
+        a.eps = eps;
+        a.period = period;
+        a.n_primary = n_primary;
+        DevBuf tp, tg, tm, tv;
+        a.params = params;
+        a.grads = grads;
+        a.m = m;
+        a.v = v;
+        if (!on_device && n) {
+            a.params = grow<float>(tp, n);
+            a.m = grow<double>(tm, n);
+            a.v = grow<double>(tv, n);
+            float* g = grow<float>(tg, n);
+            SVR_CUDA(cudaMemcpyAsync(a.params, params, n * 4, cudaMemcpyHostToDevice, st));
+            SVR_CUDA(cudaMemcpyAsync(g, grads, n * 4, cudaMemcpyHostToDevice, st));
+            SVR_CUDA(cudaMemcpyAsync(a.m, m, n * 8, cudaMemcpyHostToDevice, st));
+            SVR_CUDA(cudaMemcpyAsync(a.v, v, n * 8, cudaMemcpyHostToDevice, st));
+            a.grads = g;
+        }
+        unsigned int* flag = grow<unsigned int>(ctx->adam_flag, 1);
+        SVR_CUDA(cudaMemsetAsync(flag, 0, 4, st));
+        a.nan_flag = flag;
+        launch_adam(a, st);
+        unsigned int hflag = 0;
+        SVR_CUDA(cudaMemcpyAsync(&hflag, flag, 4, cudaMemcpyDeviceToHost, st));
+        if (!on_device && n) {
+            SVR_CUDA(cudaMemcpyAsync(params, a.params, n * 4, cudaMemcpyDeviceToHost, st));
+            SVR_CUDA(cudaMemcpyAsync(m, a.m, n * 8, cudaMemcpyDeviceToHost, st));
+            SVR_CUDA(cudaMemcpyAsync(v, a.v, n * 8, cudaMemcpyDeviceToHost, st));
+        }
+        SVR_CUDA(cudaStreamSynchronize(st));
+        require(hflag == 0, SVR_ERR_RUNTIME, "adam_step: NaN gradient");
+    });
+}
+
 int svr_train_step_l1(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam,
                       const svr_render_options* opts, const float* gt_device, svr_frame* f,
                       svr_gradients* grads, int accumulate, float* loss_device) {

@@ -79,7 +79,8 @@ struct svr_ctx {
     bool debug = false;
     svrb::DevBuf scratch;   // sort/scan temporaries
     svrb::DevBuf scratch2;
-    svrb::HostBuf pinned;   // small readbacks
+    svrb::HostBuf pinned;   // small readbacks (mapped: written by status_to_host_kernel)
+    svrb::DevBuf adam_flag; // svr_adam_step NaN flag
 };
 
 struct svr_scene {

@@ -205,6 +205,19 @@ struct RayLossArgs {
 };
 void launch_ray_losses(const DevCamera& cam, const RayLossArgs& a, cudaStream_t st);
 
+// adam_step (optim.cpp:322-345), fp64 moments, reference operation order.
+struct AdamArgs {
+    float* params;
+    const float* grads;
+    double* m;
+    double* v;
+    uint64_t n;
+    double bc1, bc2, lr, lr_alt, beta1, beta2, eps;
+    uint32_t period, n_primary;
+    unsigned int* nan_flag;
+};
+void launch_adam(const AdamArgs& a, cudaStream_t st);
+
 struct BackwardArgs {
     const uint2* ranges;
     const uint32_t* tile_order;  // optional LPT tile schedule (forward's)
