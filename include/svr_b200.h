@@ -245,6 +245,15 @@ int svr_ray_losses(svr_ctx* ctx, svr_frame* frame, const float* gt,
                    const svr_ray_loss_weights* weights, svr_ray_loss_values* out,
                    float* d_tfin_ss, float* d_weight, float* d_voxel_color, int32_t on_device);
 
+/* mse_loss + ssim_loss (losses.cpp:71-139) of the frame's rendered colour
+ * against gt (W*H*3 f32): out[0] = mean squared error, out[1] = 1 - mean
+ * SSIM (11x11 Gaussian window, sigma 1.5, valid mode). d_color (W*H*3) is
+ * ACCUMULATED with w_mse * dMSE/dC + w_ssim * d(1 - SSIM)/dC, as the
+ * reference's mse_loss(.., w_mse, &d) and ssim_loss(.., w_ssim, &d) do;
+ * NULL skips the gradients. Pointers are device pointers when on_device. */
+int svr_image_losses(svr_ctx* ctx, svr_frame* frame, const float* gt, double w_mse,
+                     double w_ssim, double* out, float* d_color, int32_t on_device);
+
 /* adam_step (optim.cpp:322-345) over a float parameter pool on the device:
  * m, v are the fp64 moment buffers (AdamState, zero-initialised by the
  * caller), `step` the updated step count (state.step after ++), so

@@ -306,6 +306,33 @@ class RefFrame:
             pass
 
 
+def ref_train_iteration_grads(scene: RefScene, cam, opts, gt, lambda_ssim, w_T, w_dist, w_R,
+                              n_pool, n_sh, n_vox):
+    """Loss values (mse, 1-ssim, l_T, l_dist, l_R) and the SceneGradients of one
+    optim::train iteration (optim.cpp:433-477), before the Adam updates."""
+    g = np.ascontiguousarray(gt, np.float64)
+    losses = np.zeros(5)
+    gd, gs, gp = np.empty(n_pool), np.empty(n_sh), np.empty(n_vox)
+    c, o = cam.to_c(), opts.to_c()
+    _chk(load_ref().ref_train_iteration_grads(scene.h, C.byref(c), C.byref(o), _p(g),
+                                              C.c_double(lambda_ssim), C.c_double(w_T),
+                                              C.c_double(w_dist), C.c_double(w_R), _p(losses),
+                                              _p(gd), _p(gs), _p(gp)))
+    return losses, gd, gs, gp
+
+
+def ref_image_losses(a, b, w_mse, w_ssim, grads=True):
+    """mse_loss + ssim_loss (losses.cpp:71-139): ((mse, 1 - ssim), d)."""
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    H, W = a.shape[:2]
+    out = np.zeros(2)
+    d = np.zeros_like(a) if grads else None
+    _chk(load_ref().ref_image_losses(_p(a), _p(b), W, H, C.c_double(w_mse), C.c_double(w_ssim),
+                                     _p(out), _p(d)))
+    return tuple(out), d
+
+
 def ref_adam_step(params, grads, m, v, step_before, lr, lr_alt=0.0, period=0, n_primary=0,
                   beta1=0.1, beta2=0.99, eps=1e-15):
     """svr::adam_step (optim.cpp:322-345) on copies; returns (params, m, v)."""

@@ -409,6 +409,54 @@ void ref_frame_records(void* fh, uint32_t* pre_vids, uint32_t* contrib_pre, doub
     if (ss_tfin) copy_img(r.ss_tfin, ss_tfin);
 }
 
+// The gradient of one optim::train iteration (optim.cpp:433-477): render
+// (training) -> mse + lambda_ssim * ssim -> ray_losses -> render_backward.
+int ref_train_iteration_grads(void* h, const svr_camera* c, const svr_render_options* o,
+                              const double* gt, double lambda_ssim, double w_T, double w_dist,
+                              double w_R, double* losses, double* g_density, double* g_sh,
+                              double* g_priority) {
+    return guarded([&] {
+        auto* s = static_cast<SparseScene*>(h);
+        RenderOptions opts = to_opts(o);
+        opts.training = true;
+        PoolsD pools = make_pools(*s);
+        RenderOutput out = render_with_pools(*s, pools, to_cam(c), opts);
+        Image g(out.color.width, out.color.height, 3);
+        std::memcpy(g.data.data(), gt, g.data.size() * sizeof(double));
+        UpstreamGrads ug;
+        ug.d_color = Image(g.width, g.height, 3);
+        losses[0] = mse_loss(out.color, g, 1.0, &ug.d_color);
+        losses[1] = ssim_loss(out.color, g, lambda_ssim, &ug.d_color);
+        RayLossWeights rw;
+        rw.w_T = w_T;
+        rw.w_dist = w_dist;
+        rw.w_R = w_R;
+        RayLossValues rv = ray_losses(*s, *out.records, g, rw, ug);
+        losses[2] = rv.l_T;
+        losses[3] = rv.l_dist;
+        losses[4] = rv.l_R;
+        SceneGradients sg = render_backward(*s, pools, *out.records, ug);
+        std::memcpy(g_density, sg.density.data(), sg.density.size() * sizeof(double));
+        std::memcpy(g_sh, sg.sh.data(), sg.sh.size() * sizeof(double));
+        std::memcpy(g_priority, sg.priority.data(), sg.priority.size() * sizeof(double));
+    });
+}
+
+// mse_loss + ssim_loss (losses.cpp:71-139) of a W x H x 3 image; d (may be
+// NULL) receives w_mse * dMSE + w_ssim * d(1 - SSIM).
+int ref_image_losses(const double* a, const double* b, int W, int H, double w_mse, double w_ssim,
+                     double* out, double* d) {
+    return guarded([&] {
+        Image ia(W, H, 3), ib(W, H, 3);
+        std::memcpy(ia.data.data(), a, ia.data.size() * sizeof(double));
+        std::memcpy(ib.data.data(), b, ib.data.size() * sizeof(double));
+        Image g(W, H, 3);
+        out[0] = mse_loss(ia, ib, w_mse, d ? &g : nullptr);
+        out[1] = ssim_loss(ia, ib, w_ssim, d ? &g : nullptr);
+        if (d) std::memcpy(d, g.data.data(), g.data.size() * sizeof(double));
+    });
+}
+
 // adam_step (optim.cpp:322-345) on host arrays: params (float), grads
 // (double), moments (double); lr_alt applies where i % period >= n_primary.
 int ref_adam_step(float* params, const double* grads, double* m, double* v, uint64_t n,

@@ -118,7 +118,7 @@ EXPORTS = [
     "svr_scene_destroy", "svr_scene_param_ptrs", "svr_frame_create", "svr_frame_destroy",
     "svr_render", "svr_frame_get_info", "svr_frame_download", "svr_frame_device_ptr",
     "svr_frame_download_async", "svr_frame_wait", "svr_frame_records", "svr_render_backward",
-    "svr_l1_loss", "svr_train_step_l1", "svr_ray_losses", "svr_adam_step",
+    "svr_l1_loss", "svr_train_step_l1", "svr_ray_losses", "svr_adam_step", "svr_image_losses",
     "svr_project_voxels", "svr_tile_sign_masks", "svr_build_sort_entries", "svr_sort_entries",
     "svr_synth_random_scene", "svr_ring_camera", "svr_free", "svr_launch_count",
     "svr_ctx_enable_timing", "svr_ctx_stage_times", "svr_frame_pre", "svr_render_oracle",
@@ -155,6 +155,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                            C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         "svr_frame_create": (C.c_int, [P, C.POINTER(P)]),
         "svr_frame_download_async": (C.c_int, [P, C.c_int, P, C.c_size_t]),
+        "svr_image_losses": (C.c_int, [P, P, P, C.c_double, C.c_double, P, P, C.c_int32]),
         "svr_adam_step": (C.c_int, [P, P, P, P, P, C.c_uint64, C.c_int64, C.c_double, C.c_double,
                                     C.c_uint32, C.c_uint32, C.c_double, C.c_double, C.c_double,
                                     C.c_int32]),
@@ -592,6 +593,18 @@ def ray_losses(frame: Frame, gt, w_T: float = 0.0, w_dist: float = 0.0, w_R: flo
     _check(frame.ctx._lib.svr_ray_losses(frame.ctx.h, frame.h, _ptr(g), C.byref(w), C.byref(v),
                                          _ptr(dtf), _ptr(dw), _ptr(dvc), 0))
     return (v.l_T, v.l_dist, v.l_R), dtf, dw, dvc.reshape(-1, 3)
+
+
+def image_losses(frame: Frame, gt, w_mse: float = 1.0, w_ssim: float = 0.0, d_color=None):
+    """mse_loss + ssim_loss (losses.cpp:71-139) of the frame's colour vs gt on
+    the device: ((mse, 1 - ssim), d_color), d_color (float32 W*H*3, created
+    zeroed when None) accumulated with w_mse*dMSE + w_ssim*d(1-SSIM)."""
+    g = np.ascontiguousarray(gt, dtype=np.float32).reshape(-1)
+    d = np.zeros(g.size, np.float32) if d_color is None else d_color
+    out = (C.c_double * 2)()
+    _check(frame.ctx._lib.svr_image_losses(frame.ctx.h, frame.h, _ptr(g), w_mse, w_ssim, out,
+                                           _ptr(d), 0))
+    return (out[0], out[1]), d.reshape(gt.shape)
 
 
 class AdamState:

@@ -439,6 +439,125 @@ __global__ void __launch_bounds__(256) ray_losses_kernel(DevCamera cam, RayLossA
     }
 }
 
+// ---- mse_loss + ssim_loss (losses.cpp:71-139) ------------------------------
+// Valid-mode separable 11-tap Gaussian blurs of a, b, a^2, b^2, ab (row
+// pass, then column pass fused with the SSIM map and its three gradient
+// maps), then the exact adjoint blur (column, then row) of those maps, as
+// blur_valid / blur_adjoint do. fp32 storage, fp64 where sums meet.
+constexpr float kSsimC1 = 0.01f * 0.01f, kSsimC2 = 0.03f * 0.03f;
+
+__global__ void ssim_rows_kernel(ImageLossArgs a) {
+    const int Wv = a.W - 10;
+    const uint64_t n = uint64_t(Wv) * a.H * 3;
+    double sq = 0.0;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const int c = int(i % 3), x = int((i / 3) % Wv), y = int(i / (3ull * Wv));
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f;
+#pragma unroll
+        for (int k = 0; k < 11; ++k) {
+            const uint64_t j = (uint64_t(y) * a.W + x + k) * 3 + c;
+            const float va = a.a[j], vb = a.b[j], w = a.kern[k];
+            s0 += w * va;
+            s1 += w * vb;
+            s2 += w * (va * va);
+            s3 += w * (vb * vb);
+            s4 += w * (va * vb);
+        }
+        a.mid[i] = s0;
+        a.mid[n + i] = s1;
+        a.mid[2 * n + i] = s2;
+        a.mid[3 * n + i] = s3;
+        a.mid[4 * n + i] = s4;
+    }
+    // MSE over the full image rides along (grid-stride over W*H*3)
+    const uint64_t nf = uint64_t(a.W) * a.H * 3;
+    const double inv_n = 1.0 / double(nf);
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nf;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const double e = double(a.a[i]) - double(a.b[i]);
+        sq += e * e;
+        if (a.d_a && a.w_mse != 0.0) a.d_a[i] += float(a.w_mse * 2.0 * e * inv_n);
+    }
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(a.sums, sq);
+}
+
+__global__ void ssim_cols_kernel(ImageLossArgs a) {
+    const int Wv = a.W - 10, Hv = a.H - 10;
+    const uint64_t nmid = uint64_t(Wv) * a.H * 3, nv = uint64_t(Wv) * Hv * 3;
+    const double g = -a.w_ssim / double(nv);  // dL/dmean of ssim_loss: -weight
+    double tot = 0.0;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nv;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const int c = int(i % 3), x = int((i / 3) % Wv), y = int(i / (3ull * Wv));
+        float m[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int k = 0; k < 11; ++k) {
+            const uint64_t j = (uint64_t(y + k) * Wv + x) * 3 + c;
+#pragma unroll
+            for (int q = 0; q < 5; ++q) m[q] += a.kern[k] * a.mid[q * nmid + j];
+        }
+        const double ma = m[0], mb = m[1];
+        const double va = m[2] - ma * ma, vb = m[3] - mb * mb, cab = m[4] - ma * mb;
+        const double n1 = 2.0 * ma * mb + kSsimC1, n2 = 2.0 * cab + kSsimC2;
+        const double d1 = ma * ma + mb * mb + kSsimC1, d2 = va + vb + kSsimC2;
+        const double sv = (n1 * n2) / (d1 * d2);
+        tot += sv;
+        if (a.d_a) {
+            const double ds_dmu = 2.0 * mb * n2 / (d1 * d2) - 2.0 * ma * sv / d1;
+            const double ds_dva = -sv / d2;
+            const double ds_dcab = 2.0 * n1 / (d1 * d2);
+            a.maps[i] = float(g * (ds_dmu - 2.0 * ma * ds_dva - mb * ds_dcab));
+            a.maps[nv + i] = float(g * ds_dva);
+            a.maps[2 * nv + i] = float(g * ds_dcab);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(a.sums + 1, tot);
+}
+
+// blur_adjoint (losses.cpp:47-61), column half: valid maps -> (W-10) x H
+__global__ void ssim_adj_cols_kernel(ImageLossArgs a) {
+    const int Wv = a.W - 10, Hv = a.H - 10;
+    const uint64_t nv = uint64_t(Wv) * Hv * 3, n = uint64_t(Wv) * a.H * 3;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const int c = int(i % 3), x = int((i / 3) % Wv), y = int(i / (3ull * Wv));
+        float s[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+        for (int k = 0; k < 11; ++k) {
+            const int yy = y - k;  // output row yy + k == y
+            if (yy < 0 || yy >= Hv) continue;
+            const uint64_t j = (uint64_t(yy) * Wv + x) * 3 + c;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) s[q] += a.kern[k] * a.maps[q * nv + j];
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) a.adj[q * n + i] = s[q];
+    }
+}
+
+// row half of the adjoint, then d_a += g1 + 2 a g2 + b g3 (losses.cpp:110-115)
+__global__ void ssim_adj_rows_kernel(ImageLossArgs a) {
+    const int Wv = a.W - 10;
+    const uint64_t nm = uint64_t(Wv) * a.H * 3, n = uint64_t(a.W) * a.H * 3;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const int c = int(i % 3), x = int((i / 3) % a.W), y = int(i / (3ull * a.W));
+        float s[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+        for (int k = 0; k < 11; ++k) {
+            const int xx = x - k;
+            if (xx < 0 || xx >= Wv) continue;
+            const uint64_t j = (uint64_t(y) * Wv + xx) * 3 + c;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) s[q] += a.kern[k] * a.adj[q * nm + j];
+        }
+        a.d_a[i] += s[0] + 2.0f * a.a[i] * s[1] + a.b[i] * s[2];
+    }
+}
+
 // adam_step (optim.cpp:322-345): HBM-bound elementwise update, grid-stride.
 // Every double operation is explicitly rounded (no FMA contraction) in the
 // reference's order, so params match std::vector<float> updates exactly.
@@ -581,6 +700,19 @@ void launch_ray_losses(const DevCamera& cam, const RayLossArgs& a, cudaStream_t 
         default: throw Error(SVR_ERR_INVALID_ARGUMENT, "rasterizer sample count K must be in {1,2,3}");
     }
     SVR_LAUNCH("ray_losses_kernel");
+}
+
+void launch_image_losses(const ImageLossArgs& a, cudaStream_t st) {
+    const unsigned g = 148 * 8;
+    ssim_rows_kernel<<<g, 256, 0, st>>>(a);
+    SVR_LAUNCH("ssim_rows_kernel");
+    ssim_cols_kernel<<<g, 256, 0, st>>>(a);
+    SVR_LAUNCH("ssim_cols_kernel");
+    if (!a.d_a || a.w_ssim == 0.0) return;
+    ssim_adj_cols_kernel<<<g, 256, 0, st>>>(a);
+    SVR_LAUNCH("ssim_adj_cols_kernel");
+    ssim_adj_rows_kernel<<<g, 256, 0, st>>>(a);
+    SVR_LAUNCH("ssim_adj_rows_kernel");
 }
 
 void launch_adam(const AdamArgs& a, cudaStream_t st) {

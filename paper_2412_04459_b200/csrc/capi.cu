@@ -1140,6 +1140,62 @@ int svr_ray_losses(svr_ctx* ctx, svr_frame* f, const float* gt, const svr_ray_lo
     });
 }
 
+int svr_image_losses(svr_ctx* ctx, svr_frame* f, const float* gt, double w_mse, double w_ssim,
+                     double* out, float* d_color, int32_t on_device) {
+    return guard([&] {
+        require(ctx && f && gt && out, SVR_ERR_INVALID_ARGUMENT, "null argument");
+        require(f->scene, SVR_ERR_INVALID_ARGUMENT, "frame has not been rendered");
+        // ssim_core (losses.cpp:73-75)
+        require(f->W >= 11 && f->H >= 11, SVR_ERR_INVALID_ARGUMENT,
+                "ssim: images smaller than the 11x11 window");
+        set_device(ctx);
+        wait_copies(f);
+        cudaStream_t st = ctx->stream;
+        const uint64_t n = uint64_t(f->W) * f->H * 3;
+        ImageLossArgs a{};
+        a.a = f->out_color.as<float>();
+        a.W = f->W;
+        a.H = f->H;
+        // gauss_kernel (losses.cpp:15-29) in double, then narrowed
+        double k[11], ks = 0.0;
+        for (int i = 0; i < 11; ++i) {
+            const double d = i - 5;
+            k[i] = std::exp(-0.5 * d * d / (1.5 * 1.5));
+            ks += k[i];
+        }
+        for (int i = 0; i < 11; ++i) a.kern[i] = float(k[i] / ks);
+        a.w_mse = w_mse;
+        a.w_ssim = w_ssim;
+        DevBuf tgt, td;
+        float* dgt = const_cast<float*>(gt);
+        float* dd = d_color;
+        if (!on_device) {
+            dgt = grow<float>(tgt, n);
+            SVR_CUDA(cudaMemcpyAsync(dgt, gt, n * 4, cudaMemcpyHostToDevice, st));
+            if (d_color) {
+                dd = grow<float>(td, n);
+                SVR_CUDA(cudaMemcpyAsync(dd, d_color, n * 4, cudaMemcpyHostToDevice, st));
+            }
+        }
+        a.b = dgt;
+        a.d_a = dd;
+        const uint64_t wv = uint64_t(f->W - 10);
+        a.mid = grow<float>(f->il_mid, 5 * wv * f->H * 3);
+        a.maps = grow<float>(f->il_maps, 3 * wv * (f->H - 10) * 3);
+        a.adj = grow<float>(f->il_adj, 3 * wv * f->H * 3);
+        a.sums = grow<double>(f->il_sums, 2);
+        SVR_CUDA(cudaMemsetAsync(a.sums, 0, 16, st));
+        launch_image_losses(a, st);
+        double hs[2];
+        SVR_CUDA(cudaMemcpyAsync(hs, a.sums, 16, cudaMemcpyDeviceToHost, st));
+        if (!on_device && d_color)
+            SVR_CUDA(cudaMemcpyAsync(d_color, dd, n * 4, cudaMemcpyDeviceToHost, st));
+        SVR_CUDA(cudaStreamSynchronize(st));
+        out[0] = hs[0] / double(n);
+        out[1] = 1.0 - hs[1] / double(wv * (f->H - 10) * 3);
+    });
+}
+
 int svr_adam_step(svr_ctx* ctx, float* params, const float* grads, double* m, double* v,
                   uint64_t n, int64_t step, double lr, double lr_alt, uint32_t period,
                   uint32_t n_primary, double beta1, double beta2, double eps, int32_t on_device) {

@@ -119,6 +119,7 @@ struct svr_frame {
     svrb::DevBuf stage_entry, stage_T;  // single-pass training records
     svrb::DevBuf view_dir;              // training: K1's sh_eval directions
     svrb::DevBuf rl_sums, rl_scratch;   // svr_ray_losses
+    svrb::DevBuf il_mid, il_maps, il_adj, il_sums;  // svr_image_losses
     uint32_t stage_cap = 64;            // per-pixel capacity, doubles on overflow
     bool staged = false;                // records live in stage_* ...
     bool compact_valid = false;         // ... and contrib_* is (not yet) built

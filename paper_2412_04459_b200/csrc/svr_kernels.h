@@ -205,6 +205,21 @@ struct RayLossArgs {
 };
 void launch_ray_losses(const DevCamera& cam, const RayLossArgs& a, cudaStream_t st);
 
+// mse_loss + ssim_loss (losses.cpp:71-139) on W x H x 3 images.
+struct ImageLossArgs {
+    const float* a;   // rendered colour
+    const float* b;   // ground truth
+    int W, H;
+    float kern[11];   // gauss_kernel (losses.cpp:15-29), normalised in double
+    double w_mse, w_ssim;
+    float* d_a;       // W*H*3, += (may be null)
+    float* mid;       // scratch: 5 x (W-10) x H x 3
+    float* maps;      // scratch: 3 x (W-10) x (H-10) x 3 (u1, u2, u3), then reused
+    float* adj;       // scratch: 3 x (W-10) x H x 3
+    double* sums;     // [0] sum of squared errors, [1] sum of the SSIM map
+};
+void launch_image_losses(const ImageLossArgs& a, cudaStream_t st);
+
 // adam_step (optim.cpp:322-345), fp64 moments, reference operation order.
 struct AdamArgs {
     float* params;

@@ -94,3 +94,25 @@ def test_ray_losses_need_records(svr, ctx, scene1):
     out = svr.render(scene, svr.ring_camera(1, 0, 32, 32), svr.RenderOptions(supersample=1.0))
     with pytest.raises(RuntimeError):
         svr.ray_losses(out.frame, np.zeros((32, 32, 3)), 0.1, 0.1, 0.1)
+
+
+@pytest.mark.parametrize("w_mse,w_ssim", [(1.0, 0.02), (0.0, 1.0), (0.7, 0.0)])
+def test_image_losses_match_reference(svr, ctx, ref, scene1, w_mse, w_ssim):
+    """mse_loss + ssim_loss (losses.cpp:71-139) on the rendered colour."""
+    arrays, scene, _ = scene1
+    cam = svr.ring_camera(1, 0, 80, 64)
+    out = svr.render(scene, cam, svr.RenderOptions(supersample=1.0))
+    gt = np.random.default_rng(4).uniform(0, 1, (64, 80, 3))
+    (mse_r, ssim_r), d_r = ref.ref_image_losses(out.color.astype(np.float64), gt, w_mse, w_ssim)
+    (mse, ssim_l), d = svr.image_losses(out.frame, gt, w_mse, w_ssim)
+    assert abs(mse - mse_r) <= 1e-6 * mse_r
+    assert abs(ssim_l - ssim_r) <= 1e-5
+    nbad, worst = grad_close(d, d_r)
+    assert nbad == 0, f"d_color: {nbad} out of tolerance (worst excess {worst:.3e})"
+
+
+def test_image_losses_reject_small_images(svr, ctx, scene1):
+    arrays, scene, _ = scene1
+    out = svr.render(scene, svr.ring_camera(1, 0, 10, 40), svr.RenderOptions(supersample=1.0))
+    with pytest.raises(ValueError):
+        svr.image_losses(out.frame, np.zeros((40, 10, 3)), 1.0, 1.0)
