@@ -63,6 +63,12 @@ WORKLOADS = {
                  desc="cfg3: cfg2 scene, ring_cameras(1, 800, 800, 1.3, 55 deg)[0], gt U(0,1) "
                       "seed 17; forward with records -> L1 -> render_backward to density, SH "
                       "(and priority), K=1, supersample 1.0"),
+    "cfg3i": dict(kind="iter", scene="G", res=800, dist=1.3, batch=1,
+                  metric="training iterations/s @800x800 (1M voxels)", unit="iters/s",
+                  desc="cfg3 scene and view, one full optim::train iteration on the device "
+                       "(trainer.DeviceTrainer): render with records -> MSE + 0.02 SSIM -> ray "
+                       "losses (lambda_T 0.01, lambda_dist 0.1, lambda_R 0.01) -> render_backward "
+                       "-> Adam on the density and SH pools (optim.cpp:433-495 minus adaptation)"),
     "cfg4": dict(kind="render", scene="U", res=1024, dist=1.0, batch=1,
                  metric="FPS @1024x1024 (8M voxels, 256 views)", unit="frames/s",
                  desc="cfg4: init_unbounded(ring_cameras(8, 1024, 1024, 1.3, 55 deg), init_level "
@@ -220,7 +226,7 @@ def view_ids(w, rank, world, i):
     """Views of step i on `rank` (view-sharded, `batch` views per step).
     cfg3 trains on its single view; cfg5 cycles through 4 batches per rank
     (16 ground-truth images resident per GPU)."""
-    if w["kind"] == "train" and w["scene"] == "G":
+    if w["kind"] in ("train", "iter") and w["scene"] == "G":
         return [0] * w["batch"]
     b = w["batch"]
     first = b * (rank + world * (i % 4 if w["kind"] == "train" else i))
@@ -228,7 +234,7 @@ def view_ids(w, rank, world, i):
 
 
 def make_camera(svr, w, v):
-    if w["kind"] == "train" and w["scene"] == "G":
+    if w["kind"] in ("train", "iter") and w["scene"] == "G":
         return svr.ring_camera(1, 0, w["res"], w["res"], w["dist"])  # cfg3's single view
     return svr.ring_camera(N_VIEWS, v, w["res"], w["res"], w["dist"])
 
@@ -280,11 +286,31 @@ def reference_step_time(ref, rscene, arrays, w, cam, opts, threads, gt=None, fra
     return (time.perf_counter() - t0) * scale
 
 
-CPU_FRACTION = {"cfg2": 1.0, "cfg3": 1.0, "cfg4": 1.0 / 16, "cfg5": 1.0 / 16}
+CPU_FRACTION = {"cfg2": 1.0, "cfg3": 1.0, "cfg3i": 1.0, "cfg4": 1.0 / 16, "cfg5": 1.0 / 16}
+
+
+def reference_iteration_time(ref, rscene, arrays, cam, opts, gt):
+    """One optim::train iteration (render -> MSE + SSIM -> ray losses ->
+    backward -> Adam on both pools) through the unmodified reference, one
+    thread (SSIM windows and the pool-wide Adam do not split into bands)."""
+    from paper_2412_04459_b200.trainer import TrainWeights
+    w = TrainWeights()
+    t0 = time.perf_counter()
+    _, gd, gs, _ = ref.ref_train_iteration_grads(rscene, cam, opts, gt, w.lambda_ssim, w.lambda_T,
+                                                 w.lambda_dist, w.lambda_R, arrays.n_pool,
+                                                 arrays.n_voxels * arrays.sh_stride, arrays.n_voxels)
+    ref.ref_adam_step(arrays.density, gd, np.zeros(gd.size), np.zeros(gd.size), 0, w.lr_density)
+    ref.ref_adam_step(arrays.sh.reshape(-1), gs, np.zeros(gs.size), np.zeros(gs.size), 0, w.lr_sh0,
+                      w.lr_sh_rest, arrays.sh_stride, 3)
+    return time.perf_counter() - t0
 
 
 def cpu_sample_text(w, name, cores):
     frac = CPU_FRACTION[name]
+    if w["kind"] == "iter":
+        return (f"one {w['res']}x{w['res']} {name} training iteration (render, MSE + SSIM, ray "
+                f"losses, render_backward, Adam on both pools) through the unmodified reference "
+                f"(oracle/_ref), single-threaded")
     what = "render" if w["kind"] == "render" else "train step (render + L1 + render_backward)"
     part = "the full view" if frac >= 1.0 else f"{frac:.4g} of the view's row bands (evenly spread), time scaled up"
     return (f"one {w['res']}x{w['res']} {name} {what} through the unmodified reference "
@@ -300,13 +326,19 @@ def run_reference(args, rank):
     cores = host_cores()
     arrays = make_scene_arrays(svr, w)
     rscene = ref.RefScene.from_arrays(arrays)
-    opts = svr.RenderOptions(K=1, supersample=args.supersample, training=w["kind"] == "train")
+    opts = svr.RenderOptions(K=1, supersample=args.supersample, training=w["kind"] != "render")
     frac = CPU_FRACTION[args.workload]
+
+    if w["kind"] == "iter":
+        cores = 1
 
     def step(i):
         t = 0.0
         for v in view_ids(w, 0, 1, i):
             cam = make_camera(svr, w, v)
+            if w["kind"] == "iter":
+                t += reference_iteration_time(ref, rscene, arrays, cam, opts, make_gt(w, v))
+                continue
             t += reference_step_time(ref, rscene, arrays, w, cam, opts, cores,
                                      make_gt(w, v) if w["kind"] == "train" else None, frac)
         return t
@@ -380,6 +412,23 @@ class TrainStep:
         self.loss = self.trainer.step(self.ids(i))
 
 
+class IterStep:
+    """cfg3i step: one device training iteration (trainer.DeviceTrainer)."""
+
+    def __init__(self, svr, ctx, scene, w, rank, world):
+        import torch
+        from paper_2412_04459_b200.trainer import DeviceTrainer
+        self.cam = make_camera(svr, w, 0)
+        self.gt_host = torch.tensor(make_gt(w, 0), dtype=torch.float32).pin_memory()
+        self.gt = self.gt_host.to(torch.device("cuda", ctx.device))
+        self.trainer = DeviceTrainer(svr, ctx, scene, svr.RenderOptions(K=1, supersample=1.0))
+        self.frame = self.trainer.frame
+        self.log = None
+
+    def __call__(self, i):
+        self.log = self.trainer.step(self.cam, self.gt)
+
+
 def run_ours(args, rank, world, local_rank):
     import ctypes as C
 
@@ -403,7 +452,8 @@ def run_ours(args, rank, world, local_rank):
     ctx = svr.Context(local_rank)
     arrays = make_scene_arrays(svr, w)
     scene = svr.Scene(ctx, arrays)
-    step = (RenderStep if w["kind"] == "render" else TrainStep)(svr, ctx, scene, w, rank, world)
+    step = {"render": RenderStep, "train": TrainStep, "iter": IterStep}[w["kind"]](
+        svr, ctx, scene, w, rank, world)
     st = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local_rank))
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > 126 MB L2
 
@@ -423,7 +473,7 @@ def run_ours(args, rank, world, local_rank):
     ctx.stage_times(reset=True)
     launches0 = svr.launch_count()
     stats = []
-    frame = step.frame if w["kind"] == "render" else step.trainer.frame
+    frame = step.trainer.frame if w["kind"] == "train" else step.frame
     for i in range(args.steps):
         with torch.cuda.stream(st):
             flush.zero_()
@@ -477,6 +527,19 @@ def run_ours(args, rank, world, local_rank):
         e2e_note = ("scene resident on device (uploaded once); per step camera in, "
                     "color+depth+median+normal+transmittance out to pinned host memory; "
                     "three frames rotate so a step's read-back overlaps the next renders")
+    elif w["kind"] == "iter":
+        def e2e_step(i):
+            step.gt.copy_(step.gt_host, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            step(i)  # returns the five loss values to the host
+
+        def e2e_drain():
+            pass
+
+        d2h = 5 * 8
+        h2d = H * W * 12 + C.sizeof(svr.svr_camera)
+        e2e_note = ("scene, gradients and Adam moments resident on device; per step the ground "
+                    "truth (pinned host) and camera in, the five loss values out")
     else:
         host_gt = {v: torch.tensor(make_gt(w, v)).pin_memory() for v in step.views}
         tr = step.trainer
@@ -544,10 +607,15 @@ def run_ours(args, rank, world, local_rank):
             rscene = ref.RefScene.from_arrays(arrays)
             cores = host_cores()
             v = view_ids(w, 0, 1, 0)[0]
-            opts = svr.RenderOptions(K=1, supersample=1.0, training=w["kind"] == "train")
-            secs = reference_step_time(ref, rscene, arrays, w, make_camera(svr, w, v), opts, cores,
-                                       make_gt(w, v) if w["kind"] == "train" else None,
-                                       CPU_FRACTION[args.workload])
+            opts = svr.RenderOptions(K=1, supersample=1.0, training=w["kind"] != "render")
+            if w["kind"] == "iter":
+                cores = 1
+                secs = reference_iteration_time(ref, rscene, arrays, make_camera(svr, w, v), opts,
+                                                make_gt(w, v))
+            else:
+                secs = reference_step_time(ref, rscene, arrays, w, make_camera(svr, w, v), opts,
+                                           cores, make_gt(w, v) if w["kind"] == "train" else None,
+                                           CPU_FRACTION[args.workload])
             cpu = {"value": 1.0 / secs, "unit": w["unit"], "cores": cores, "kind": "reference",
                    "sample": cpu_sample_text(w, args.workload, cores)}
         except Exception as e:  # the reference library may be absent on a fresh box
@@ -560,10 +628,12 @@ def run_ours(args, rank, world, local_rank):
               "l2": "flushed (256 MiB write) before every timed step",
               "parallelism": (f"view-sharded over {world} GPU(s), no data-path collective"
                               if w["kind"] == "render" else
+                              f"replicas only ({world} independent iteration(s))"
+                              if w["kind"] == "iter" else
                               f"view-batch sharded over {world} GPU(s), one in-place all-reduce "
                               f"of the flat gradient per step"),
               "precision": "projection/tile binning fp64 (bit-exact), compositing fp32"}
-    if w["kind"] == "train":
+    if w["kind"] != "render":
         config["contribs_per_view"] = int(contribs)
         config["views_per_gpu_step"] = units_per_step
     line = {
