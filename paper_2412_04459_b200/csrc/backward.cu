@@ -311,38 +311,54 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
     }
 }
 
-// ray_losses (losses.cpp:141-238). One thread per supersampled pixel, laid
-// out like the compositing tiles; each walks its own contribution list
-// (independent trip counts, same code). Per contribution the weight
-// w = T_i * alpha_i is recomputed from the voxel record exactly as the
-// forward composited it (fp32 slab + quadrature), m = (a + b) / 2 and
-// l = b - a from the same slab. L_dist keeps the reference's structure:
-// a forward pass with prefix sums (its intra-segment term included) writes
-// (w, m) to scratch, a reverse pass adds the suffix half.
+// ray_losses (losses.cpp:141-238). One WARP per supersampled pixel: its
+// contributions are contiguous in the compact (reference) order, so lane k
+// handles contribution chunk*32 + k and every upstream gradient read/write
+// is coalesced. w = T_i * alpha_i is recomputed from the voxel record exactly
+// as the forward composited it (fp32 slab + quadrature); m = (a + b) / 2 and
+// l = b - a come from the same slab. L_dist's prefix sums are warp scans
+// carried across chunks; its suffix half is a second pass in reverse over
+// (w, m) kept in scratch, like the reference's two loops.
+__device__ __forceinline__ float warp_incl_scan_f(float v, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const float n = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += n;
+    }
+    return v;
+}
+
+// L_T (losses.cpp:163-174): one thread per supersampled pixel.
+__global__ void __launch_bounds__(256) ray_loss_T_kernel(RayLossArgs a, uint64_t npix) {
+    const uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const double inv_rays = 1.0 / double(npix);
+    float lT = 0.f;
+    if (p < npix) {
+        const float eps = 1e-6f;
+        const float T = a.tfin[p];
+        const float Tc = fminf(fmaxf(T, eps), 1.0f - eps);
+        const float l0 = logf(Tc), l1 = logf(1.0f - Tc);
+        lT = -(Tc * l0 + (1.0f - Tc) * l1);
+        if (T > eps && T < 1.0f - eps && a.d_tfin_ss) a.d_tfin_ss[p] += float(a.w_T * inv_rays) * (l1 - l0);
+    }
+    for (int o = 16; o > 0; o >>= 1) lT += __shfl_xor_sync(0xffffffffu, lT, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(a.sums, double(lT) * inv_rays);
+}
+
 template <int K>
 __global__ void __launch_bounds__(256) ray_losses_kernel(DevCamera cam, RayLossArgs a) {
-    const int tile = blockIdx.x;
-    const int tx = tile % cam.ntx, ty = tile / cam.ntx;
-    const int px = tx * kTile + (threadIdx.x & 15), py = ty * kTile + (threadIdx.x >> 4);
-    const bool inside = px < cam.W && py < cam.H;
-    const double inv_rays = 1.0 / (double(cam.W) * cam.H);
+    const int lane = threadIdx.x & 31;
+    // grid (ceil(W / 8), H): warp w of block (bx, y) owns pixel (8 bx + w, y)
+    const int px = int(blockIdx.x) * 8 + (threadIdx.x >> 5), py = int(blockIdx.y);
+    const uint64_t npix = uint64_t(cam.W) * cam.H;
+    const double inv_rays = 1.0 / double(npix);
     float lT = 0.f, ldist = 0.f, lR = 0.f;
-    if (inside) {
-        const uint32_t slot = uint32_t(tile) * 256u + threadIdx.x;
-        const uint64_t pix = uint64_t(py) * cam.W + px;
-        if (a.w_T != 0.0) {
-            const double eps = 1e-6;
-            const double T = a.tfin[pix];
-            const double Tc = fmin(fmax(T, eps), 1.0 - eps);
-            lT = float(-(Tc * log(Tc) + (1.0 - Tc) * log(1.0 - Tc)));
-            if (T > eps && T < 1.0 - eps && a.d_tfin_ss)
-                a.d_tfin_ss[pix] += float(a.w_T * (log(1.0 - Tc) - log(Tc)) * inv_rays);
-        }
+    if (px < cam.W) {
+        const uint32_t tile = uint32_t(py / kTile) * cam.ntx + uint32_t(px / kTile);
+        const uint32_t slot = tile * 256u + uint32_t((py % kTile) * kTile + (px % kTile));
         const uint32_t n = a.pix_count[slot];
         if (n > 0 && (a.w_dist != 0.0 || a.w_R != 0.0)) {
             const uint32_t base = a.pix_begin[slot];
-            const uint64_t rb = a.stage_stride ? slot : base;
-            const uint64_t rs = a.stage_stride ? a.stage_stride : 1u;
             double dd[3];
             pixel_ray_dir(cam, double(px), double(py), dd);
             const float dx = float(dd[0]), dy = float(dd[1]), dz = float(dd[2]);
@@ -356,74 +372,97 @@ __global__ void __launch_bounds__(256) ray_losses_kernel(DevCamera cam, RayLossA
                 g[0] = gp[0], g[1] = gp[1], g[2] = gp[2];
             }
             constexpr uint32_t kVidMask = (1u << 29) - 1u;
-            float Wpre = 0.f, Spre = 0.f;
-            for (uint32_t i = 0; i < n; ++i) {
-                const uint32_t e = a.contrib_entry[rb + i * rs];
-                const float T = a.contrib_T[rb + i * rs];
-                const float4* rec = a.records + uint64_t(__ldg(a.vals + e) & kVidMask) * kRecordF4;
-                const float4 lo = __ldg(rec);
-                const float inv = __ldg(rec + 5).w;
-                float t0 = lo.x * ix, t1 = (lo.x + lo.w) * ix;
-                float ta = fminf(t0, t1), tb = fmaxf(t0, t1);
-                t0 = lo.y * iy;
-                t1 = (lo.y + lo.w) * iy;
-                ta = fmaxf(ta, fminf(t0, t1));
-                tb = fminf(tb, fmaxf(t0, t1));
-                t0 = lo.z * iz;
-                t1 = (lo.z + lo.w) * iz;
-                ta = fmaxf(ta, fminf(t0, t1));
-                tb = fminf(tb, fmaxf(t0, t1));
-                const float4 va = __ldg(rec + 2), vb = __ldg(rec + 3);
-                const float seg = tb - ta;
-                const float lk = seg * dnorm * (1.0f / K);
-                float sum = 0.f, sa0 = 0.f;
+            const float wd = float(a.w_dist * inv_rays);
+            float Wc = 0.f, Sc = 0.f;  // prefix carries across chunks
+            for (uint32_t c0 = 0; c0 < n; c0 += 32) {
+                const uint32_t i = c0 + lane;
+                const bool on = i < n;
+                float w = 0.f, m = 0.f, dl = 0.f, gdw = 0.f;
+                float err = 0.f, e0 = 0.f, e1 = 0.f, e2 = 0.f;
+                if (on) {
+                    const uint64_t at = a.stage_stride ? uint64_t(i) * a.stage_stride + slot : uint64_t(base) + i;
+                    const uint32_t e = a.contrib_entry[at];
+                    const float T = a.contrib_T[at];
+                    const float4* rec = a.records + uint64_t(__ldg(a.vals + e) & kVidMask) * kRecordF4;
+                    const float4 lo = __ldg(rec);
+                    const float inv = __ldg(rec + 5).w;
+                    float t0 = lo.x * ix, t1 = (lo.x + lo.w) * ix;
+                    float ta = fminf(t0, t1), tb = fmaxf(t0, t1);
+                    t0 = lo.y * iy;
+                    t1 = (lo.y + lo.w) * iy;
+                    ta = fmaxf(ta, fminf(t0, t1));
+                    tb = fminf(tb, fmaxf(t0, t1));
+                    t0 = lo.z * iz;
+                    t1 = (lo.z + lo.w) * iz;
+                    ta = fmaxf(ta, fminf(t0, t1));
+                    tb = fminf(tb, fmaxf(t0, t1));
+                    const float4 va = __ldg(rec + 2), vb = __ldg(rec + 3);
+                    const float seg = tb - ta;
+                    const float lk = seg * dnorm * (1.0f / K);
+                    float sum = 0.f, sa0 = 0.f;
 #pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    const float tk = ta + ((k + 0.5f) / K) * seg;
-                    const float act = explin(trilinear_poly(va, vb, (tk * dx - lo.x) * inv,
-                                                            (tk * dy - lo.y) * inv, (tk * dz - lo.z) * inv));
-                    sum += act;
-                    if (K == 1) sa0 = one_minus_exp_neg(lk * act);
+                    for (int k = 0; k < K; ++k) {
+                        const float tk = ta + ((k + 0.5f) / K) * seg;
+                        const float act = explin(trilinear_poly(va, vb, (tk * dx - lo.x) * inv,
+                                                                (tk * dy - lo.y) * inv,
+                                                                (tk * dz - lo.z) * inv));
+                        sum += act;
+                        if (K == 1) sa0 = one_minus_exp_neg(lk * act);
+                    }
+                    const float alpha = (K == 1) ? sa0 : one_minus_exp_neg(lk * sum);
+                    w = T * alpha;
+                    m = 0.5f * (ta + tb);
+                    dl = tb - ta;
+                    if (a.w_R != 0.0) {
+                        const float4 col = __ldg(rec + 4);
+                        e0 = col.x - g[0], e1 = col.y - g[1], e2 = col.z - g[2];
+                        err = e0 * e0 + e1 * e1 + e2 * e2;
+                    }
                 }
-                const float alpha = (K == 1) ? sa0 : one_minus_exp_neg(lk * sum);
-                const float w = T * alpha, m = 0.5f * (ta + tb), dl = tb - ta;
-                float dw = 0.f;
                 if (a.w_dist != 0.0) {
-                    ldist += 2.f * w * (m * Wpre - Spre) + w * w * dl * (1.0f / 3.0f);
-                    dw = 2.f * (m * Wpre - Spre) + 2.f * w * dl * (1.0f / 3.0f);
-                    Wpre += w;
-                    Spre += w * m;
-                    a.scratch[base + i] = make_float2(w, m);
+                    const float wi = warp_incl_scan_f(w, lane), si = warp_incl_scan_f(w * m, lane);
+                    const float Wpre = Wc + wi - w, Spre = Sc + si - w * m;
+                    if (on) {
+                        ldist += 2.f * w * (m * Wpre - Spre) + w * w * dl * (1.0f / 3.0f);
+                        gdw = wd * (2.f * (m * Wpre - Spre) + 2.f * w * dl * (1.0f / 3.0f));
+                        a.scratch[base + i] = make_float2(w, m);
+                    }
+                    Wc += __shfl_sync(0xffffffffu, wi, 31);
+                    Sc += __shfl_sync(0xffffffffu, si, 31);
                 }
-                float gdw = float(a.w_dist) * dw;  // the suffix half follows below
-                if (a.w_R != 0.0) {
-                    const float4 col = __ldg(rec + 4);
-                    const float e0 = col.x - g[0], e1 = col.y - g[1], e2 = col.z - g[2];
-                    const float err = e0 * e0 + e1 * e1 + e2 * e2;
-                    lR += w * err;
-                    gdw += float(a.w_R) * err;
-                    const float s = float(a.w_R * 2.0 * inv_rays) * w;
-                    float* dvc = a.d_voxel_color + 3ull * (base + i);
-                    dvc[0] += s * e0;
-                    dvc[1] += s * e1;
-                    dvc[2] += s * e2;
+                if (on) {
+                    if (a.w_R != 0.0) {
+                        lR += w * err;
+                        gdw += float(a.w_R * inv_rays) * err;
+                        const float sc = float(a.w_R * 2.0 * inv_rays) * w;
+                        float* dvc = a.d_voxel_color + 3ull * (base + i);
+                        dvc[0] += sc * e0;
+                        dvc[1] += sc * e1;
+                        dvc[2] += sc * e2;
+                    }
+                    a.d_weight[base + i] += gdw;
                 }
-                a.d_weight[base + i] += gdw * float(inv_rays);
             }
-            if (a.w_dist != 0.0) {  // suffix half of d|m_i - m_j|
-                float Wsuf = 0.f, Ssuf = 0.f;
-                for (int i = int(n) - 1; i >= 0; --i) {
-                    const float2 wm = a.scratch[base + i];
-                    a.d_weight[base + i] += float(a.w_dist * inv_rays) * (2.f * (Ssuf - wm.y * Wsuf));
-                    Wsuf += wm.x;
-                    Ssuf += wm.x * wm.y;
+            if (a.w_dist != 0.0) {  // suffix half of d|m_i - m_j|, chunks in reverse
+                float Wsc = 0.f, Ssc = 0.f;
+                const uint32_t last = (n - 1) / 32 * 32;
+                for (int c0 = int(last); c0 >= 0; c0 -= 32) {
+                    const uint32_t i = uint32_t(c0) + 31 - lane;  // reversed lane order
+                    const bool on = i < n;
+                    float2 wm = make_float2(0.f, 0.f);
+                    if (on) wm = a.scratch[base + i];
+                    const float wi = warp_incl_scan_f(wm.x, lane), si = warp_incl_scan_f(wm.x * wm.y, lane);
+                    const float Wsuf = Wsc + wi - wm.x, Ssuf = Ssc + si - wm.x * wm.y;
+                    if (on) a.d_weight[base + i] += wd * (2.f * (Ssuf - wm.y * Wsuf));
+                    Wsc += __shfl_sync(0xffffffffu, wi, 31);
+                    Ssc += __shfl_sync(0xffffffffu, si, 31);
                 }
             }
         }
     }
     // block sums -> one double atomic per value per block
     __shared__ float s_red[3][8];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int warp = threadIdx.x >> 5;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         lT += __shfl_xor_sync(0xffffffffu, lT, o);
@@ -434,7 +473,7 @@ __global__ void __launch_bounds__(256) ray_losses_kernel(DevCamera cam, RayLossA
     __syncthreads();
     if (threadIdx.x < 3) {
         double t = 0.0;
-        for (int w = 0; w < 8; ++w) t += s_red[threadIdx.x][w];
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) t += s_red[threadIdx.x][w];
         atomicAdd(a.sums + threadIdx.x, t * inv_rays);
     }
 }
@@ -692,11 +731,17 @@ void launch_composite_backward(const DevCamera& cam, const BackwardArgs& a, cuda
 }
 
 void launch_ray_losses(const DevCamera& cam, const RayLossArgs& a, cudaStream_t st) {
-    const unsigned ntiles = unsigned(cam.ntx * cam.nty);
+    const uint64_t npix = uint64_t(cam.W) * cam.H;
+    if (a.w_T != 0.0) {
+        ray_loss_T_kernel<<<unsigned((npix + 255) / 256), 256, 0, st>>>(a, npix);
+        SVR_LAUNCH("ray_loss_T_kernel");
+    }
+    if (a.w_dist == 0.0 && a.w_R == 0.0) return;
+    const dim3 grid(unsigned((cam.W + 7) / 8), unsigned(cam.H));  // a warp per pixel
     switch (a.K) {
-        case 1: ray_losses_kernel<1><<<ntiles, 256, 0, st>>>(cam, a); break;
-        case 2: ray_losses_kernel<2><<<ntiles, 256, 0, st>>>(cam, a); break;
-        case 3: ray_losses_kernel<3><<<ntiles, 256, 0, st>>>(cam, a); break;
+        case 1: ray_losses_kernel<1><<<grid, 256, 0, st>>>(cam, a); break;
+        case 2: ray_losses_kernel<2><<<grid, 256, 0, st>>>(cam, a); break;
+        case 3: ray_losses_kernel<3><<<grid, 256, 0, st>>>(cam, a); break;
         default: throw Error(SVR_ERR_INVALID_ARGUMENT, "rasterizer sample count K must be in {1,2,3}");
     }
     SVR_LAUNCH("ray_losses_kernel");
