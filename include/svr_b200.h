@@ -133,6 +133,17 @@ int svr_ctx_destroy(svr_ctx* ctx);
 /* cudaStream_t the context launches on (for event timing by the caller). */
 void* svr_ctx_stream(svr_ctx* ctx);
 int svr_ctx_synchronize(svr_ctx* ctx);
+/* Deferred-E rendering for serving loops: svr_render no longer waits for the
+ * entry count mid-frame (the frame is enqueued whole, so back-to-back renders
+ * keep the GPU busy); the sort runs on a capacity learned from earlier
+ * frames of the same svr_frame and reads the live count on the device. The
+ * count is checked when a result is consumed (svr_frame_wait, download,
+ * info, backward): a frame that outgrew its capacity is rendered again there
+ * (and its asynchronous downloads repeated), so results are always those of
+ * a complete frame. Training frames always take the synchronous path.
+ * svr_ctx_overflow_count reports how many deferred frames outgrew theirs. */
+int svr_ctx_set_async(svr_ctx* ctx, int on);
+int svr_ctx_overflow_count(svr_ctx* ctx, uint32_t* out);
 /* debug != 0 keeps the pre-sort entry list so it can be dumped bit-exactly. */
 int svr_ctx_set_debug(svr_ctx* ctx, int debug);
 

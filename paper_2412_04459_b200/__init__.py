@@ -114,7 +114,7 @@ BUF = dict(COLOR=0, DEPTH=1, MEDIAN_DEPTH=2, NORMAL=3, TRANSMITTANCE=4, MAX_BLEN
 # exported symbols of include/svr_b200.h (checked by the CPU test-suite)
 EXPORTS = [
     "svr_last_error", "svr_abi_version", "svr_ctx_create", "svr_ctx_destroy", "svr_ctx_stream",
-    "svr_ctx_synchronize", "svr_ctx_set_debug", "svr_scene_upload", "svr_scene_set_params",
+    "svr_ctx_synchronize", "svr_ctx_set_async", "svr_ctx_overflow_count", "svr_ctx_set_debug", "svr_scene_upload", "svr_scene_set_params",
     "svr_scene_destroy", "svr_scene_param_ptrs", "svr_frame_create", "svr_frame_destroy",
     "svr_render", "svr_frame_get_info", "svr_frame_download", "svr_frame_device_ptr",
     "svr_frame_download_async", "svr_frame_wait", "svr_frame_records", "svr_render_backward",
@@ -148,6 +148,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "svr_ctx_stream": (P, [P]),
         "svr_ctx_synchronize": (C.c_int, [P]),
         "svr_ctx_set_debug": (C.c_int, [P, C.c_int]),
+        "svr_ctx_set_async": (C.c_int, [P, C.c_int]),
+        "svr_ctx_overflow_count": (C.c_int, [P, C.POINTER(C.c_uint32)]),
         "svr_scene_upload": (C.c_int, [P, C.POINTER(svr_scene_desc), C.POINTER(P)]),
         "svr_scene_set_params": (C.c_int, [P, P, P, P, C.c_int]),
         "svr_scene_destroy": (C.c_int, [P]),
@@ -372,6 +374,15 @@ class Context:
 
     def synchronize(self) -> None:
         _check(self._lib.svr_ctx_synchronize(self.h))
+
+    def set_async(self, on: bool = True) -> None:
+        """Deferred-E rendering (svr_ctx_set_async)."""
+        _check(self._lib.svr_ctx_set_async(self.h, int(on)))
+
+    def overflow_count(self) -> int:
+        n = C.c_uint32()
+        _check(self._lib.svr_ctx_overflow_count(self.h, C.byref(n)))
+        return int(n.value)
 
     def enable_timing(self, on: bool = True) -> None:
         _check(self._lib.svr_ctx_enable_timing(self.h, int(on)))

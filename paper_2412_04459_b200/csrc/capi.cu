@@ -268,7 +268,7 @@ int plan_sort(int max_level, int ntiles, uint32_t pattern_or, RadixPass* passes)
 }
 
 void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
-                 const svr_render_options* opts, svr_frame* f) {
+                 const svr_render_options* opts, svr_frame* f, bool allow_deferred = true) {
     require(ctx && scene && cam_in && opts && f, SVR_ERR_INVALID_ARGUMENT, "null argument");
     set_device(ctx);
     validate_options(*opts);
@@ -294,6 +294,9 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     f->ctx = ctx;
     f->scene = scene;
     f->opts = *opts;
+    f->req_cam = *cam_in;
+    f->req_opts = *opts;
+    f->pending_dl.clear();
     f->cam = cam;
     f->ss_cam = ss_cam;
     f->W = W;
@@ -344,14 +347,29 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     mark(ctx, kStageScan);
     exclusive_scan_u32(pa.counts, offsets, N, &status->n_entries, ctx->scratch.p, st);
     mark(ctx, -1);
-    ctx->pinned.reserve(sizeof(FrameStatus));
-    FrameStatus* hs = static_cast<FrameStatus*>(ctx->pinned.p);
-    launch_status_to_host(status, hs, st);
-    SVR_CUDA(cudaStreamSynchronize(st));
-    const uint64_t E = hs->n_entries;
-    const uint32_t pattern_or = hs->pattern_or;
-    require(E < (uint64_t(1) << 30), SVR_ERR_LENGTH, "entry count exceeds 2^30");
+    f->hstatus.reserve(sizeof(FrameStatus));
+    FrameStatus* hs = static_cast<FrameStatus*>(f->hstatus.p);
+    // Deferred E (svr_ctx_set_async): no host round trip here; the sort and
+    // its neighbours run on a capacity sized from earlier frames and read the
+    // live count on the device. Needs a capacity and the pattern-independent
+    // sort plan of the rank-keyed packed format (never for training frames,
+    // whose record buffers are sized from the contribution count).
+    const bool deferred = allow_deferred && ctx->async_frames && !f->training && !ctx->debug &&
+                          f->e_cap > 0 && scene->rank_bits > 0;
+    uint64_t E;
+    uint32_t pattern_or = 0;
+    if (deferred) {
+        E = f->e_cap;
+    } else {
+        launch_status_to_host(status, hs, st);
+        SVR_CUDA(cudaStreamSynchronize(st));
+        E = hs->n_entries;
+        pattern_or = hs->pattern_or;
+        require(E < (uint64_t(1) << 30), SVR_ERR_LENGTH, "entry count exceeds 2^30");
+        f->e_cap = std::max<uint64_t>(f->e_cap, E + E / 4 + 1024);
+    }
     f->n_entries = E;
+    f->e_pending = deferred;
 
     // K4 + K5 + K6. Packed path when tile | order | s | vid fits in 64 bits
     // (config 2: 12 + 27 + 3 + 20 = 62): keys-only sort of 8-B entries, digit
@@ -374,6 +392,7 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     const int rb = scene->rank_bits;
     const bool use_rank = rank_enabled && N > 0 && rb > 0 && (vb + 3 + rb + tile_bits) <= 64;
     f->packed = packed_enabled && N > 0 && (use_rank || (vb + 3 + 3 * lmax + tile_bits) <= 64);
+    require(!deferred || (f->packed && use_rank), SVR_ERR_RUNTIME, "deferred frame needs rank keys");
     uint2* ranges = grow<uint2>(f->ranges, ntiles);
     RadixPass passes[kMaxRadixPasses];
     int np = 0;
@@ -393,17 +412,18 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
         launch_duplicate_packed(cam, N, pa.paths, pa.rects, masks, pa.counts, offsets, f->fmt,
                                 use_rank ? scene->morton_rank.as<uint32_t>() : nullptr,
                                 f->keys[0].as<uint64_t>(), sat, grow<uint32_t>(f->big, N),
-                                &status->n_big, st);
+                                &status->n_big, st, E);
         if (ctx->debug) {
             grow<uint64_t>(f->dbg_keys, E);
             SVR_CUDA(cudaMemcpyAsync(f->dbg_keys.p, f->keys[0].p, E * 8, cudaMemcpyDeviceToDevice, st));
         }
         mark(ctx, kStageSort);
+        const unsigned long long* n_dev = deferred ? &status->n_entries : nullptr;
         f->sorted_buf = radix_sort_keys(f->keys[0].as<uint64_t>(), f->keys[1].as<uint64_t>(), E,
-                                        passes, np, ctx->scratch2.p, st, false);
+                                        passes, np, ctx->scratch2.p, st, false, n_dev);
         mark(ctx, kStageRanges);
         launch_tile_ranges_packed(f->keys[f->sorted_buf].as<uint64_t>(), E, f->fmt, ranges,
-                                  f->vals[0].as<uint32_t>(), ntiles, st);
+                                  f->vals[0].as<uint32_t>(), ntiles, st, n_dev);
         f->vals_buf = 0;
     } else {
         for (int b = 0; b < 2; ++b) {
@@ -533,7 +553,12 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     (void)nss;
     mark(ctx, -1);
     f->n_visible = ~uint64_t(0);  // computed lazily
+    if (deferred)
+        launch_status_to_host(status, hs, st, f->e_cap, grow<unsigned int>(ctx->overflow_count, 1));
 }
+
+void resolve_frame(svr_frame* f);
+
 
 // Compact (reference-order) contribution lists for the host-facing records.
 void ensure_compact(svr_frame* f) {
@@ -579,7 +604,9 @@ BufView frame_buffer(svr_frame* f, svr_buffer which) {
         case SVR_BUF_TRANSMITTANCE: case SVR_BUF_MAX_BLEND: case SVR_BUF_SS_COLOR:
         case SVR_BUF_SS_DEPTH: case SVR_BUF_SS_TFIN: case SVR_BUF_TILE_RANGES:
         case SVR_BUF_TILE_MASKS: case SVR_BUF_VOXEL_RECTS: break;
-        default: wait_copies(f);
+        default:
+            wait_copies(f);
+            resolve_frame(f);  // these need the entry count
     }
     switch (which) {
         case SVR_BUF_COLOR: return {f->out_color.p, npx * 12};
@@ -638,6 +665,32 @@ BufView frame_buffer(svr_frame* f, svr_buffer which) {
     throw Error(SVR_ERR_INVALID_ARGUMENT, "unknown buffer id");
 }
 
+// Settles a deferred frame: the live entry count is read (the frame's work
+// is complete), and a frame that outgrew its capacity is rendered again
+// with the count known (its pending asynchronous downloads are repeated).
+void resolve_frame(svr_frame* f) {
+    if (!f || !f->e_pending) return;
+    SVR_CUDA(cudaStreamSynchronize(f->ctx->stream));
+    const FrameStatus* hs = static_cast<const FrameStatus*>(f->hstatus.p);
+    const uint64_t E = hs->n_entries;
+    f->e_pending = false;
+    if (E <= f->e_cap) {
+        f->n_entries = E;
+        f->e_cap = std::max<uint64_t>(f->e_cap, E + E / 8);
+        return;
+    }
+    f->e_cap = E + E / 4 + 1024;
+    auto dl = f->pending_dl;
+    const svr_camera cam = f->req_cam;
+    const svr_render_options opts = f->req_opts;
+    render_impl(f->ctx, f->scene, &cam, &opts, f, false);
+    for (const auto& d : dl) {
+        BufView b = frame_buffer(f, d.which);
+        SVR_CUDA(cudaMemcpyAsync(d.dst, b.p, d.bytes, cudaMemcpyDeviceToHost, f->ctx->stream));
+    }
+    SVR_CUDA(cudaStreamSynchronize(f->ctx->stream));
+}
+
 void backward_impl(svr_ctx* ctx, const svr_scene* scene, svr_frame* f, const svr_upstream* up,
                    svr_gradients* out, bool accumulate) {
     require(ctx && scene && f && up && out, SVR_ERR_INVALID_ARGUMENT, "null argument");
@@ -651,6 +704,7 @@ void backward_impl(svr_ctx* ctx, const svr_scene* scene, svr_frame* f, const svr
     require(!up->d_voxel_color || up->n_d_voxel_color == f->n_contribs, SVR_ERR_RUNTIME,
             "per-contribution color gradients do not match the records");
     wait_copies(f);
+    resolve_frame(f);
     cudaStream_t st = ctx->stream;
     const uint64_t N = scene->n_voxels, P = scene->n_pool;
     const uint64_t shn = N * uint64_t(scene->sh_stride);
@@ -831,6 +885,25 @@ int svr_ctx_synchronize(svr_ctx* ctx) {
     return guard([&] { SVR_CUDA(cudaStreamSynchronize(ctx->stream)); });
 }
 
+int svr_ctx_set_async(svr_ctx* ctx, int on) {
+    return guard([&] {
+        require(ctx != nullptr, SVR_ERR_INVALID_ARGUMENT, "null argument");
+        ctx->async_frames = on != 0;
+    });
+}
+
+int svr_ctx_overflow_count(svr_ctx* ctx, uint32_t* out) {
+    return guard([&] {
+        require(ctx && out, SVR_ERR_INVALID_ARGUMENT, "null argument");
+        set_device(ctx);
+        *out = 0;
+        if (ctx->overflow_count.p) {
+            SVR_CUDA(cudaMemcpyAsync(out, ctx->overflow_count.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+            SVR_CUDA(cudaStreamSynchronize(ctx->stream));
+        }
+    });
+}
+
 int svr_ctx_set_debug(svr_ctx* ctx, int debug) {
     return guard([&] { ctx->debug = debug != 0; });
 }
@@ -960,6 +1033,7 @@ int svr_frame_get_info(svr_frame* f, svr_frame_info* out) {
     return guard([&] {
         require(f && out && f->scene, SVR_ERR_INVALID_ARGUMENT, "frame has not been rendered");
         set_device(f->ctx);
+        resolve_frame(f);
         out->width = f->W;
         out->height = f->H;
         out->ss_width = f->sw;
@@ -977,6 +1051,7 @@ int svr_frame_get_info(svr_frame* f, svr_frame_info* out) {
 int svr_frame_download(svr_frame* f, svr_buffer which, void* dst, size_t bytes) {
     return guard([&] {
         set_device(f->ctx);
+        resolve_frame(f);
         BufView b = frame_buffer(f, which);
         require(bytes == b.bytes, SVR_ERR_INVALID_ARGUMENT, "download size mismatch");
         if (bytes)
@@ -999,6 +1074,7 @@ int svr_frame_download_async(svr_frame* f, svr_buffer which, void* dst, size_t b
             SVR_CUDA(cudaMemcpyAsync(dst, b.p, bytes, cudaMemcpyDeviceToHost, f->ctx->copy_stream));
         SVR_CUDA(cudaEventRecord(f->copied, f->ctx->copy_stream));
         f->copy_pending = true;
+        if (f->e_pending) f->pending_dl.push_back({which, dst, bytes});
     });
 }
 
@@ -1006,6 +1082,11 @@ int svr_frame_wait(svr_frame* f) {
     return guard([&] {
         require(f != nullptr, SVR_ERR_INVALID_ARGUMENT, "null argument");
         if (f->copied) SVR_CUDA(cudaEventSynchronize(f->copied));
+        if (f->ctx) {
+            set_device(f->ctx);
+            resolve_frame(f);  // an outgrown deferred frame is rendered and copied again
+        }
+        f->pending_dl.clear();
     });
 }
 

@@ -342,18 +342,19 @@ __global__ void __launch_bounds__(256) duplicate_packed_kernel(
     DevCamera cam, uint64_t n, const uint64_t* __restrict__ paths, const int4* __restrict__ rects,
     const uint8_t* __restrict__ masks, const uint32_t* __restrict__ counts,
     const uint32_t* __restrict__ offsets, PackedFormat fmt, const uint32_t* __restrict__ rank,
-    uint64_t* __restrict__ keys, uint32_t* big, unsigned int* n_big) {
+    uint64_t* __restrict__ keys, uint32_t* big, unsigned int* n_big, uint64_t cap) {
     const uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (v >= n) return;
     const uint32_t cnt = counts[v];
     if (cnt == 0) return;
+    uint32_t o = offsets[v];
+    if (uint64_t(o) + cnt > cap) return;  // deferred-E frame that outgrew its buffers (flagged)
     if (cnt > kBigEntries) {
         big[atomicAdd(n_big, 1u)] = uint32_t(v);
         return;
     }
     const uint64_t code = paths[v] & kCodeMask48;
     const int4 r = rects[v];
-    uint32_t o = offsets[v];
     for (int ty = r.z; ty <= r.w; ++ty)
         for (int tx = r.x; tx <= r.y; ++tx) {
             const uint64_t tid = uint64_t(ty) * cam.ntx + tx;
@@ -426,8 +427,10 @@ __global__ void rank_scatter_kernel(const uint32_t* __restrict__ vals, uint64_t 
 }
 
 __global__ void tile_ranges_packed_kernel(const uint64_t* __restrict__ keys, uint64_t n,
-                                          PackedFormat fmt, uint2* ranges, uint32_t* vals) {
+                                          PackedFormat fmt, uint2* ranges, uint32_t* vals,
+                                          const unsigned long long* n_dev) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (n_dev) n = min(n, uint64_t(*n_dev));  // deferred-E frame: the device count decides
     if (i >= n) return;
     const uint64_t k = keys[i];
     const uint32_t t = uint32_t(k >> fmt.tile_shift);
@@ -883,14 +886,19 @@ __global__ void project_batch_kernel(DevCamera cam, uint64_t n, const double* ce
 // Frame summary -> mapped pinned host memory, written by the SM over PCIe:
 // no copy-engine transfer, so this read-back never queues behind a large
 // asynchronous image download on the copy stream.
-__global__ void status_to_host_kernel(const FrameStatus* d, FrameStatus* h) { *h = *d; }
+__global__ void status_to_host_kernel(const FrameStatus* d, FrameStatus* h, uint64_t cap,
+                                      unsigned int* overflow_count) {
+    *h = *d;
+    if (overflow_count && d->n_entries > cap) atomicAdd(overflow_count, 1u);
+}
 
 inline unsigned blocks_for(uint64_t n, int threads) { return unsigned((n + threads - 1) / threads); }
 
 }  // namespace
 
-void launch_status_to_host(const FrameStatus* d, FrameStatus* h, cudaStream_t st) {
-    status_to_host_kernel<<<1, 1, 0, st>>>(d, h);
+void launch_status_to_host(const FrameStatus* d, FrameStatus* h, cudaStream_t st, uint64_t cap,
+                           unsigned int* overflow_count) {
+    status_to_host_kernel<<<1, 1, 0, st>>>(d, h, cap, overflow_count);
     SVR_LAUNCH("status_to_host_kernel");
 }
 
@@ -957,10 +965,11 @@ void launch_duplicate_packed(const DevCamera& cam, uint64_t n, const uint64_t* p
                              const int4* rects, const uint8_t* masks, const uint32_t* counts,
                              const uint32_t* offsets, PackedFormat fmt, const uint32_t* rank,
                              uint64_t* keys, const uint32_t* tile_sat, uint32_t* big,
-                             unsigned int* n_big, cudaStream_t st) {
+                             unsigned int* n_big, cudaStream_t st, uint64_t cap) {
     if (n == 0) return;
     duplicate_packed_kernel<<<blocks_for(n, 256), 256, 0, st>>>(cam, n, paths, rects, masks, counts,
-                                                                offsets, fmt, rank, keys, big, n_big);
+                                                                offsets, fmt, rank, keys, big, n_big,
+                                                                cap);
     SVR_LAUNCH("duplicate_packed_kernel");
     duplicate_big_kernel<<<148 * 4, 256, 0, st>>>(cam, n, paths, rects, masks, offsets, tile_sat,
                                                    fmt, rank, keys, big, n_big);
@@ -999,10 +1008,11 @@ void build_morton_rank(const uint64_t* paths, uint64_t n, int lmax, uint32_t* ra
 }
 
 void launch_tile_ranges_packed(const uint64_t* keys, uint64_t n, PackedFormat fmt, uint2* ranges,
-                               uint32_t* vals, int ntiles, cudaStream_t st) {
+                               uint32_t* vals, int ntiles, cudaStream_t st,
+                               const unsigned long long* n_dev) {
     SVR_CUDA(cudaMemsetAsync(ranges, 0, size_t(ntiles) * sizeof(uint2), st));
     if (n == 0) return;
-    tile_ranges_packed_kernel<<<blocks_for(n, 256), 256, 0, st>>>(keys, n, fmt, ranges, vals);
+    tile_ranges_packed_kernel<<<blocks_for(n, 256), 256, 0, st>>>(keys, n, fmt, ranges, vals, n_dev);
     SVR_LAUNCH("tile_ranges_packed_kernel");
 }
 

@@ -53,7 +53,9 @@ __device__ __forceinline__ uint32_t digit_of(uint64_t k, uint32_t v, RadixPass p
 
 __global__ void __launch_bounds__(kThreads) hist_kernel(const uint64_t* keys, const uint32_t* vals,
                                                         uint64_t n, PassSpec spec,
-                                                        uint32_t* hist) {
+                                                        uint32_t* hist,
+                                                        const unsigned long long* n_dev) {
+    if (n_dev) n = min(n, uint64_t(*n_dev));
     __shared__ uint32_t s_hist[kMaxRadixPasses][kRadix];
     for (int i = threadIdx.x; i < spec.n * kRadix; i += kThreads) (&s_hist[0][0])[i] = 0;
     __syncthreads();
@@ -99,7 +101,8 @@ template <bool PAIRS>
 __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
     const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint64_t n, RadixPass pass,
-    const uint32_t* __restrict__ bin_base, uint32_t* status, uint32_t* ticket) {
+    const uint32_t* __restrict__ bin_base, uint32_t* status, uint32_t* ticket,
+    const unsigned long long* n_dev) {
     __shared__ uint32_t s_warp_hist[kWarps][kRadix + 1];
     __shared__ uint32_t s_block_excl[kRadix];
     __shared__ uint32_t s_global[kRadix];
@@ -113,7 +116,9 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
         (&s_warp_hist[0][0])[i] = 0;
     __syncthreads();
     const uint32_t part = s_part;
+    if (n_dev) n = min(n, uint64_t(*n_dev));
     const uint64_t base = uint64_t(part) * Part<PAIRS>::keys;
+    if (base >= n && part > 0) return;  // past the live count: no later partition looks back here
     const uint64_t wbase = base + uint64_t(warp) * 32 * Part<PAIRS>::items;
 
     // Digits are recomputed from the key/value when needed (saves registers);
@@ -253,7 +258,7 @@ int radix_sort_pairs(uint64_t* keys0, uint32_t* vals0, uint64_t* keys1, uint32_t
     // one memset clears histograms, tickets and every pass's look-back status
     SVR_CUDA(cudaMemsetAsync(hist, 0, sort_scratch_bytes(n, npasses), st));
     int hist_blocks = int(std::min<uint64_t>((n + kThreads - 1) / kThreads, 148 * 4));
-    hist_kernel<<<hist_blocks, kThreads, 0, st>>>(keys0, vals0, n, spec, hist);
+    hist_kernel<<<hist_blocks, kThreads, 0, st>>>(keys0, vals0, n, spec, hist, nullptr);
     SVR_LAUNCH("hist_kernel");
     bin_scan_kernel<<<npasses, kRadix, 0, st>>>(hist);
     SVR_LAUNCH("bin_scan_kernel");
@@ -265,7 +270,7 @@ int radix_sort_pairs(uint64_t* keys0, uint32_t* vals0, uint64_t* keys1, uint32_t
     for (int p = 0; p < npasses; ++p) {
         onesweep_kernel<true><<<unsigned(nparts), kThreads, 0, st>>>(
             kin, vin, kout, vout, n, passes[p], hist + p * kRadix,
-            status + size_t(p) * (nparts + 1) * kRadix, tickets + p);
+            status + size_t(p) * (nparts + 1) * kRadix, tickets + p, nullptr);
         SVR_LAUNCH("onesweep_kernel");
         std::swap(kin, kout);
         std::swap(vin, vout);
@@ -281,7 +286,8 @@ void sort_prepare(void* scratch, uint64_t n, int npasses, cudaStream_t st) {
 }
 
 int radix_sort_keys(uint64_t* keys0, uint64_t* keys1, uint64_t n, const RadixPass* passes,
-                    int npasses, void* scratch, cudaStream_t st, bool hist_ready) {
+                    int npasses, void* scratch, cudaStream_t st, bool hist_ready,
+                    const unsigned long long* n_dev) {
     if (n <= 1 || npasses == 0) return 0;
     if (npasses > kMaxRadixPasses) throw Error(SVR_ERR_RUNTIME, "too many radix passes");
     if (n >= (uint64_t(1) << 30))
@@ -301,7 +307,7 @@ int radix_sort_keys(uint64_t* keys0, uint64_t* keys1, uint64_t n, const RadixPas
         spec.n = npasses;
         for (int i = 0; i < npasses; ++i) spec.p[i] = passes[i];
         int hist_blocks = int(std::min<uint64_t>((n + kThreads - 1) / kThreads, 148 * 4));
-        hist_kernel<<<hist_blocks, kThreads, 0, st>>>(keys0, nullptr, n, spec, hist);
+        hist_kernel<<<hist_blocks, kThreads, 0, st>>>(keys0, nullptr, n, spec, hist, n_dev);
         SVR_LAUNCH("hist_kernel");
     }
     bin_scan_kernel<<<npasses, kRadix, 0, st>>>(hist);
@@ -312,7 +318,7 @@ int radix_sort_keys(uint64_t* keys0, uint64_t* keys1, uint64_t n, const RadixPas
     for (int p = 0; p < npasses; ++p) {
         onesweep_kernel<false><<<unsigned(nparts), kThreads, 0, st>>>(
             kin, nullptr, kout, nullptr, n, passes[p], hist + p * kRadix,
-            status + size_t(p) * (nparts_alloc + 1) * kRadix, tickets + p);
+            status + size_t(p) * (nparts_alloc + 1) * kRadix, tickets + p, n_dev);
         SVR_LAUNCH("onesweep_kernel");
         std::swap(kin, kout);
         cur ^= 1;

@@ -81,6 +81,8 @@ struct svr_ctx {
     svrb::DevBuf scratch2;
     svrb::HostBuf pinned;   // small readbacks (mapped: written by status_to_host_kernel)
     svrb::DevBuf adam_flag; // svr_adam_step NaN flag
+    bool async_frames = false;  // svr_ctx_set_async: renders skip the mid-frame E read-back
+    svrb::DevBuf overflow_count;  // deferred frames whose E outgrew their capacity
 };
 
 struct svr_scene {
@@ -136,4 +138,17 @@ struct svr_frame {
     cudaEvent_t ready = nullptr;   // main stream reached the copy point
     cudaEvent_t copied = nullptr;  // copy stream finished the downloads
     bool copy_pending = false;
+    // deferred-E rendering (svr_ctx_set_async): the entry count is read back
+    // only when a result is consumed (svr_frame_wait / download / info)
+    svrb::HostBuf hstatus;        // mapped FrameStatus of this frame
+    uint64_t e_cap = 0;           // entry capacity a deferred render may use
+    bool e_pending = false;       // hstatus not yet checked against e_cap
+    svr_camera req_cam{};         // the request, for a re-render on overflow
+    svr_render_options req_opts{};
+    struct PendingDownload {
+        svr_buffer which;
+        void* dst;
+        size_t bytes;
+    };
+    std::vector<PendingDownload> pending_dl;  // async downloads since the last wait
 };

@@ -39,8 +39,11 @@ struct RadixPlan {
 };
 uint32_t* sort_hist_ptr(void* scratch);
 void sort_prepare(void* scratch, uint64_t n, int npasses, cudaStream_t st);
+// n_dev (optional): the live count on the device (<= n, the capacity the
+// launch grids are sized for); partitions past it exit at once.
 int radix_sort_keys(uint64_t* keys0, uint64_t* keys1, uint64_t n, const RadixPass* passes,
-                    int npasses, void* scratch, cudaStream_t st, bool hist_ready);
+                    int npasses, void* scratch, cudaStream_t st, bool hist_ready,
+                    const unsigned long long* n_dev = nullptr);
 
 // ---- raster.cu -------------------------------------------------------------
 struct FrameStatus {          // device -> host summary, one read per frame
@@ -55,7 +58,9 @@ struct FrameStatus {          // device -> host summary, one read per frame
 void launch_tile_setup(const DevCamera& cam, uint8_t* masks, uint32_t* sat, FrameStatus* status,
                        cudaStream_t st);
 // Copies the device FrameStatus into host-mapped pinned memory with a kernel.
-void launch_status_to_host(const FrameStatus* d, FrameStatus* h, cudaStream_t st);
+// With overflow_count: counts frames whose entry total exceeded `cap`.
+void launch_status_to_host(const FrameStatus* d, FrameStatus* h, cudaStream_t st,
+                           uint64_t cap = ~uint64_t(0), unsigned int* overflow_count = nullptr);
 
 struct PreprocessArgs {
     uint64_t n;
@@ -96,7 +101,7 @@ void launch_duplicate_packed(const DevCamera& cam, uint64_t n, const uint64_t* p
                              const int4* rects, const uint8_t* masks, const uint32_t* counts,
                              const uint32_t* offsets, PackedFormat fmt, const uint32_t* rank,
                              uint64_t* keys, const uint32_t* tile_sat, uint32_t* big,
-                             unsigned int* n_big, cudaStream_t st);
+                             unsigned int* n_big, cudaStream_t st, uint64_t cap = ~uint64_t(0));
 // Direction-aware Morton rank table of a scene: rank[s*n + vid] = position of
 // (code_vid ^ s*kGroupOnes, s << 29 | vid) in the ascending order of all 8n
 // such pairs, i.e. the reference's within-tile (key, value) order
@@ -107,7 +112,8 @@ void build_morton_rank(const uint64_t* paths, uint64_t n, int lmax, uint32_t* ra
 // Tile ranges from packed sorted keys; also writes the reference value
 // (s << 29 | vid) per entry for the compositing kernels.
 void launch_tile_ranges_packed(const uint64_t* keys, uint64_t n, PackedFormat fmt, uint2* ranges,
-                               uint32_t* vals, int ntiles, cudaStream_t st);
+                               uint32_t* vals, int ntiles, cudaStream_t st,
+                               const unsigned long long* n_dev = nullptr);
 // Reference SortEntry (key, value) from packed keys (parity dumps).
 void launch_unpack_entries(const uint64_t* packed, uint64_t n, PackedFormat fmt,
                            const uint64_t* paths, uint64_t* keys, uint32_t* vals, cudaStream_t st);

@@ -342,3 +342,33 @@ def test_async_downloads_pipeline_two_frames(svr, ctx, cfg1):
     for e, g in zip(expect, got):
         assert np.array_equal(g["COLOR"].reshape(e.color.shape), e.color)
         assert np.array_equal(g["DEPTH"].reshape(e.depth.shape), e.depth)
+
+
+def test_deferred_entry_count_frames(svr, ref, cfg1):
+    """svr_ctx_set_async: renders skip the mid-frame read-back of E. Images
+    are bit-identical to synchronous renders, including a frame whose entry
+    count outgrows the capacity learned from the previous one (it is
+    rendered again when the result is consumed)."""
+    import torch
+    arrays, _, _ = cfg1
+    small = svr.synth_random_scene(3, 4096, 6, 3)
+    actx = svr.Context(0)
+    actx.set_async(True)
+    scenes = {"small": svr.Scene(actx, small), "cfg1": svr.Scene(actx, arrays)}
+    sctx = svr.Context(0)
+    sync_scenes = {"small": svr.Scene(sctx, small), "cfg1": svr.Scene(sctx, arrays)}
+    opts = svr.RenderOptions(supersample=1.0)
+    cam = svr.ring_camera(4, 1, 128, 96)
+    sync = {k: svr.render(sc, cam, opts) for k, sc in sync_scenes.items()}
+    f = svr.Frame(actx)
+    svr.render_into(f, scenes["small"], cam, opts)  # first render: synchronous, sets capacity
+    e_small = f.info().n_entries
+    for name in ["small", "small", "cfg1", "cfg1", "small"]:
+        svr.render_into(f, scenes[name], cam, opts)
+        buf = torch.empty(96 * 128 * 3, pin_memory=True)
+        f.download_async("COLOR", buf)
+        f.wait()
+        assert np.array_equal(buf.numpy().reshape(96, 128, 3), sync[name].color), name
+        assert f.info().n_entries == sync[name].frame.info().n_entries
+    assert sync["cfg1"].frame.info().n_entries > 1.25 * e_small + 1024  # the overflow case ran
+    assert actx.overflow_count() >= 1
