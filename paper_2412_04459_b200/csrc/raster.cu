@@ -43,8 +43,7 @@ __global__ void __launch_bounds__(1024) tile_setup_kernel(DevCamera cam, uint8_t
     unsigned int local_or = 0;
     for (int k = threadIdx.x; k < ntiles; k += blockDim.x) {
         const int tx = k % ntx, ty = k / ntx;
-        const uint32_t m = tile_sign_mask(cam, tx, ty);
-        masks[k] = uint8_t(m);
+        const uint32_t m = masks[k];  // tile_masks_kernel, launched just before
         local_or |= m;
         t[(ty + 1) * sw + tx + 1] = __popc(m);
     }
@@ -913,6 +912,10 @@ void launch_tile_setup(const DevCamera& cam, uint8_t* masks, uint32_t* sat, Fram
                                       kSatSmemMax * 4));
         attr_set = true;
     }
+    // masks: one thread per tile (fp64 corner rays); then the SAT in one CTA
+    const int ntiles = cam.ntx * cam.nty;
+    tile_masks_kernel<<<blocks_for(ntiles, 128), 128, 0, st>>>(cam, masks);
+    SVR_LAUNCH("tile_masks_kernel");
     tile_setup_kernel<<<1, 1024, smem, st>>>(cam, masks, sat, status, use_smem);
     SVR_LAUNCH("tile_setup_kernel");
 }
