@@ -605,8 +605,19 @@ def run_ours(args, rank, world, local_rank):
     peak, peak_src = measured_peak_hbm()
     kernel_ms = launches_per_step[dom]  # one launch per view
     achieved = byt / (kernel_ms * 1e-3) / 1e9
+    # the same kernel against the instruction-issue roof (4 schedulers x 148
+    # SMs x max SM clock, one warp instruction each per cycle), from the
+    # committed ncu instruction count of that kernel on this workload
+    winst = traffic_from_profiles(dom + "_warp_inst", args.workload)
+    issue_peak = 4 * 148 * 1.965e9
+    issue = None
+    if winst:
+        issue = {"bound": "issue", "achieved_warp_inst_per_s": winst / (kernel_ms * 1e-3),
+                 "peak_warp_inst_per_s": issue_peak,
+                 "frac": winst / (kernel_ms * 1e-3) / issue_peak,
+                 "warp_inst_per_launch": winst, "source": "profiles/ncu_traffic.json"}
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak,
+                "unit": "GB/s", "frac": achieved / peak, "issue": issue,
                 "traffic": traffic_from_profiles(dom, args.workload, npass),
                 "algorithmic_bytes": byt, "kernel_ms": kernel_ms, "peak_source": peak_src}
 

@@ -156,6 +156,20 @@ int svr_scene_upload(svr_ctx* ctx, const svr_scene_desc* desc, svr_scene** out);
 int svr_scene_set_params(svr_ctx* ctx, svr_scene* scene, const float* density, const float* sh,
                          int on_device);
 int svr_scene_destroy(svr_scene* scene);
+/* SVRX checkpoints (io.cpp:229-359, save_checkpoint / load_checkpoint): the
+ * scene's CURRENT device parameters are written (training updates them in
+ * place), and a file is loaded straight into a new device scene. The
+ * container is byte-compatible with the reference's; the reader repeats its
+ * checks (magic, CRC32, version, header, lengths, corner-key structure) with
+ * its std::runtime_error conditions (SVR_ERR_RUNTIME) and the octree level
+ * checks' std::invalid_argument (SVR_ERR_INVALID_ARGUMENT). */
+int svr_scene_save_svrx(svr_ctx* ctx, const svr_scene* scene, const char* path);
+/* Counts, degree and bounds of a device scene (array pointers left NULL). */
+int svr_scene_info(const svr_scene* scene, svr_scene_desc* out);
+/* Host copies of a device scene's arrays (any pointer may be NULL). */
+int svr_scene_download(svr_ctx* ctx, const svr_scene* scene, uint64_t* codes, uint8_t* levels,
+                       uint32_t* corner_index, float* density, float* sh);
+int svr_scene_load_svrx(svr_ctx* ctx, const char* path, svr_scene** out);
 /* Device pointers of the parameter pools (for optimisers living on device). */
 int svr_scene_param_ptrs(svr_scene* scene, float** density, float** sh, uint64_t* n_pool,
                          uint64_t* n_sh);

@@ -115,7 +115,8 @@ BUF = dict(COLOR=0, DEPTH=1, MEDIAN_DEPTH=2, NORMAL=3, TRANSMITTANCE=4, MAX_BLEN
 EXPORTS = [
     "svr_last_error", "svr_abi_version", "svr_ctx_create", "svr_ctx_destroy", "svr_ctx_stream",
     "svr_ctx_synchronize", "svr_ctx_set_async", "svr_ctx_overflow_count", "svr_ctx_set_debug", "svr_scene_upload", "svr_scene_set_params",
-    "svr_scene_destroy", "svr_scene_param_ptrs", "svr_frame_create", "svr_frame_destroy",
+    "svr_scene_destroy", "svr_scene_param_ptrs", "svr_scene_save_svrx", "svr_scene_load_svrx",
+    "svr_scene_info", "svr_scene_download", "svr_frame_create", "svr_frame_destroy",
     "svr_render", "svr_frame_get_info", "svr_frame_download", "svr_frame_device_ptr",
     "svr_frame_download_async", "svr_frame_wait", "svr_frame_records", "svr_render_backward",
     "svr_l1_loss", "svr_train_step_l1", "svr_ray_losses", "svr_adam_step", "svr_image_losses",
@@ -153,6 +154,10 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "svr_scene_upload": (C.c_int, [P, C.POINTER(svr_scene_desc), C.POINTER(P)]),
         "svr_scene_set_params": (C.c_int, [P, P, P, P, C.c_int]),
         "svr_scene_destroy": (C.c_int, [P]),
+        "svr_scene_save_svrx": (C.c_int, [P, P, C.c_char_p]),
+        "svr_scene_load_svrx": (C.c_int, [P, C.c_char_p, C.POINTER(P)]),
+        "svr_scene_info": (C.c_int, [P, C.POINTER(svr_scene_desc)]),
+        "svr_scene_download": (C.c_int, [P, P, P, P, P, P, P]),
         "svr_scene_param_ptrs": (C.c_int, [P, C.POINTER(P), C.POINTER(P),
                                            C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         "svr_frame_create": (C.c_int, [P, C.POINTER(P)]),
@@ -439,6 +444,39 @@ class Scene:
     @property
     def n_pool(self) -> int:
         return self.arrays.n_pool
+
+    @classmethod
+    def load_svrx(cls, ctx: Context, path: str) -> "Scene":
+        """load_checkpoint (io.cpp:281-359) straight into a device scene
+        (svr_scene_load_svrx); `arrays` is read back from the device."""
+        self = cls.__new__(cls)
+        self.ctx = ctx
+        h = C.c_void_p()
+        _check(ctx._lib.svr_scene_load_svrx(ctx.h, os.fsencode(path), C.byref(h)))
+        self.h = h
+        self._keep = None
+        self.arrays = self.download()
+        return self
+
+    def save_svrx(self, path: str) -> None:
+        """save_checkpoint (io.cpp:250-279) of the scene's current device parameters."""
+        _check(self.ctx._lib.svr_scene_save_svrx(self.ctx.h, self.h, os.fsencode(path)))
+
+    def download(self) -> SceneArrays:
+        """The device scene as host arrays (svr_scene_info + svr_scene_download)."""
+        d = svr_scene_desc()
+        _check(self.ctx._lib.svr_scene_info(self.h, C.byref(d)))
+        n, p, deg = int(d.n_voxels), int(d.n_pool), int(d.sh_degree)
+        stride = 3 * (deg + 1) ** 2
+        codes = np.empty(n, np.uint64)
+        levels = np.empty(n, np.uint8)
+        ci = np.empty((n, 8), np.uint32)
+        dens = np.empty(p, np.float32)
+        sh = np.empty((n, stride), np.float32)
+        _check(self.ctx._lib.svr_scene_download(self.ctx.h, self.h, _ptr(codes), _ptr(levels),
+                                                _ptr(ci), _ptr(dens), _ptr(sh)))
+        return SceneArrays(codes, levels, ci, dens, sh, deg, tuple(d.bounds_center),
+                           float(d.bounds_size))
 
     def set_params(self, density=None, sh=None, on_device: bool = False) -> None:
         """PoolsD refresh (raster.hpp:47-52). Host numpy arrays or device pointers."""

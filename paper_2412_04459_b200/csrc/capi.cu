@@ -16,6 +16,7 @@
 
 #include "svr_internal.h"
 #include "svr_kernels.h"
+#include "svrx.h"
 
 namespace svrb {
 
@@ -101,6 +102,9 @@ int guard(F&& f) {
     } catch (const std::bad_alloc& e) {
         g_last_error = e.what();
         return SVR_ERR_RUNTIME;
+    } catch (const std::invalid_argument& e) {  // e.g. SvrxInvalid (octree level checks)
+        g_last_error = e.what();
+        return SVR_ERR_INVALID_ARGUMENT;
     } catch (const std::exception& e) {
         g_last_error = e.what();
         return SVR_ERR_RUNTIME;
@@ -970,6 +974,95 @@ int svr_scene_upload(svr_ctx* ctx, const svr_scene_desc* d, svr_scene** out) {
             throw;
         }
         *out = s;
+    });
+}
+
+int svr_scene_info(const svr_scene* s, svr_scene_desc* out) {
+    return guard([&] {
+        require(s && out, SVR_ERR_INVALID_ARGUMENT, "null argument");
+        *out = svr_scene_desc{};
+        out->n_voxels = s->n_voxels;
+        out->n_pool = s->n_pool;
+        out->sh_degree = s->sh_degree;
+        for (int i = 0; i < 3; ++i) out->bounds_center[i] = s->bounds_center[i];
+        out->bounds_size = s->bounds_size;
+    });
+}
+
+int svr_scene_download(svr_ctx* ctx, const svr_scene* s, uint64_t* codes, uint8_t* levels,
+                       uint32_t* corner_index, float* density, float* sh) {
+    return guard([&] {
+        require(ctx && s, SVR_ERR_INVALID_ARGUMENT, "null argument");
+        set_device(ctx);
+        cudaStream_t st = ctx->stream;
+        const uint64_t N = s->n_voxels, P = s->n_pool;
+        std::vector<uint64_t> paths(N);
+        if (N && (codes || levels))
+            SVR_CUDA(cudaMemcpyAsync(paths.data(), s->paths.p, N * 8, cudaMemcpyDeviceToHost, st));
+        if (N && corner_index)
+            SVR_CUDA(cudaMemcpyAsync(corner_index, s->corner_index.p, N * 32, cudaMemcpyDeviceToHost, st));
+        if (P && density) SVR_CUDA(cudaMemcpyAsync(density, s->density.p, P * 4, cudaMemcpyDeviceToHost, st));
+        if (N && sh)
+            SVR_CUDA(cudaMemcpyAsync(sh, s->sh.p, N * uint64_t(s->sh_stride) * 4, cudaMemcpyDeviceToHost, st));
+        SVR_CUDA(cudaStreamSynchronize(st));
+        for (uint64_t i = 0; i < N; ++i) {
+            if (codes) codes[i] = paths[i] & ((uint64_t(1) << 48) - 1);
+            if (levels) levels[i] = uint8_t(paths[i] >> 48);
+        }
+    });
+}
+
+int svr_scene_save_svrx(svr_ctx* ctx, const svr_scene* s, const char* path) {
+    return guard([&] {
+        require(ctx && s && path, SVR_ERR_INVALID_ARGUMENT, "null argument");
+        set_device(ctx);
+        cudaStream_t st = ctx->stream;
+        SvrxScene h;
+        const uint64_t N = s->n_voxels, P = s->n_pool;
+        std::vector<uint64_t> paths(N);
+        h.corner_index.resize(N * 8);
+        h.density.resize(P);
+        h.sh.resize(N * uint64_t(s->sh_stride));
+        // the parameters as the device holds them now (training updates them in place)
+        if (N) {
+            SVR_CUDA(cudaMemcpyAsync(paths.data(), s->paths.p, N * 8, cudaMemcpyDeviceToHost, st));
+            SVR_CUDA(cudaMemcpyAsync(h.corner_index.data(), s->corner_index.p, N * 32,
+                                     cudaMemcpyDeviceToHost, st));
+            SVR_CUDA(cudaMemcpyAsync(h.sh.data(), s->sh.p, h.sh.size() * 4, cudaMemcpyDeviceToHost, st));
+        }
+        if (P) SVR_CUDA(cudaMemcpyAsync(h.density.data(), s->density.p, P * 4, cudaMemcpyDeviceToHost, st));
+        SVR_CUDA(cudaStreamSynchronize(st));
+        h.codes.resize(N);
+        h.levels.resize(N);
+        for (uint64_t i = 0; i < N; ++i) {
+            h.codes[i] = paths[i] & ((uint64_t(1) << 48) - 1);
+            h.levels[i] = uint8_t(paths[i] >> 48);
+        }
+        h.sh_degree = s->sh_degree;
+        for (int i = 0; i < 3; ++i) h.bounds_center[i] = s->bounds_center[i];
+        h.bounds_size = s->bounds_size;
+        svrx_write(path, svrx_encode(h));
+    });
+}
+
+int svr_scene_load_svrx(svr_ctx* ctx, const char* path, svr_scene** out) {
+    return guard([&] {
+        require(ctx && path && out, SVR_ERR_INVALID_ARGUMENT, "null argument");
+        SvrxScene h = svrx_read(path);
+        svrx_validate(h, path);
+        svr_scene_desc d{};
+        d.n_voxels = h.codes.size();
+        d.n_pool = h.density.size();
+        d.sh_degree = h.sh_degree;
+        for (int i = 0; i < 3; ++i) d.bounds_center[i] = h.bounds_center[i];
+        d.bounds_size = h.bounds_size;
+        d.codes = h.codes.data();
+        d.levels = h.levels.data();
+        d.corner_index = h.corner_index.data();
+        d.density = h.density.data();
+        d.sh = h.sh.data();
+        const int st = svr_scene_upload(ctx, &d, out);
+        if (st != SVR_OK) throw Error(st, svr_last_error());
     });
 }
 

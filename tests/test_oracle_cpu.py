@@ -201,3 +201,15 @@ def test_port_matches_compiled_reference():
     k1, v1 = port.entries(a, scam, True)
     k2, v2 = ref.ref_entries(rs, scam, True)
     assert np.array_equal(k1, k2) and np.array_equal(v1, v2)
+
+
+def test_svrx_header_number_format():
+    """oracle/svrx.py writes numbers as nlohmann::json's dump() does (the
+    SVRX header, io.cpp:251-258): shortest round-trip digits, '.0' on
+    integral values, exponent form outside [1e-4, 1e15)."""
+    from oracle.svrx import json_double
+    cases = {0.0: "0.0", 1.0: "1.0", 2.0: "2.0", 0.5: "0.5", -0.25: "-0.25", 0.1: "0.1",
+             14.3: "14.3", 1e-4: "0.0001", 1e-5: "1e-05", 1e14: "100000000000000.0",
+             1e15: "1e+15", 1.5e20: "1.5e+20", 123.456: "123.456", -3.0: "-3.0"}
+    for v, txt in cases.items():
+        assert json_double(v) == txt, (v, json_double(v), txt)

@@ -102,6 +102,7 @@ def capture(rep_name, title, workload, traffic):
                 tr["sort_pass"] = sum(bs) / len(bs) * 1e6
             else:
                 tr[key] = (rd + wr) * 1e6
+                tr[key + "_warp_inst"] = f(d.get("smsp__inst_executed.sum"))
     path = os.path.join(prof, f"{tag}_ncu_{rep_name.split('.')[0]}.md")
     open(path, "w").write("\n".join(md) + "\n")
     print("\n".join(md))
