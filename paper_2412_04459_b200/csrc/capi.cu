@@ -557,8 +557,11 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     (void)nss;
     mark(ctx, -1);
     f->n_visible = ~uint64_t(0);  // computed lazily
-    if (deferred)
+    if (deferred) {
         launch_status_to_host(status, hs, st, f->e_cap, grow<unsigned int>(ctx->overflow_count, 1));
+        if (!f->done) SVR_CUDA(cudaEventCreateWithFlags(&f->done, cudaEventDisableTiming));
+        SVR_CUDA(cudaEventRecord(f->done, st));  // settle this frame without draining the stream
+    }
 }
 
 void resolve_frame(svr_frame* f);
@@ -674,7 +677,7 @@ BufView frame_buffer(svr_frame* f, svr_buffer which) {
 // with the count known (its pending asynchronous downloads are repeated).
 void resolve_frame(svr_frame* f) {
     if (!f || !f->e_pending) return;
-    SVR_CUDA(cudaStreamSynchronize(f->ctx->stream));
+    SVR_CUDA(cudaEventSynchronize(f->done));
     const FrameStatus* hs = static_cast<const FrameStatus*>(f->hstatus.p);
     const uint64_t E = hs->n_entries;
     f->e_pending = false;
@@ -1113,6 +1116,7 @@ int svr_frame_destroy(svr_frame* f) {
             cudaEventDestroy(f->copied);
         }
         if (f->ready) cudaEventDestroy(f->ready);
+        if (f->done) cudaEventDestroy(f->done);
         delete f;
     });
 }

@@ -143,6 +143,7 @@ struct svr_frame {
     svrb::HostBuf hstatus;        // mapped FrameStatus of this frame
     uint64_t e_cap = 0;           // entry capacity a deferred render may use
     bool e_pending = false;       // hstatus not yet checked against e_cap
+    cudaEvent_t done = nullptr;   // end of the last deferred render
     svr_camera req_cam{};         // the request, for a re-render on overflow
     svr_render_options req_opts{};
     struct PendingDownload {
