@@ -164,6 +164,21 @@ int svr_scene_destroy(svr_scene* scene);
  * its std::runtime_error conditions (SVR_ERR_RUNTIME) and the octree level
  * checks' std::invalid_argument (SVR_ERR_INVALID_ARGUMENT). */
 int svr_scene_save_svrx(svr_ctx* ctx, const svr_scene* scene, const char* path);
+/* Scene adaptation on the device (optim.cpp:207-298 + scene.cpp:8-26):
+ * prune keeps the voxels with max_blend_weight >= threshold (n = n_voxels,
+ * f32; on_device selects device/host), subdivide replaces each selected
+ * voxel (host list, duplicates and level-16 voxels ignored) by its 8
+ * children; both rebuild the corner indexing in the reference's
+ * first-appearance pool order with its densities (fresh subdivision points:
+ * mean of the parents' trilinear values, in double) and return a NEW scene,
+ * whose AdaptRemap (voxel_src per voxel, pool_src per pool entry, -1 = new)
+ * svr_scene_remap copies out. Errors: invalid_argument (stats size, voxel id
+ * out of range), length_error (capacity 2^29). */
+int svr_scene_prune(svr_ctx* ctx, const svr_scene* scene, const float* max_blend_weight, uint64_t n,
+                    double threshold, int32_t on_device, svr_scene** out);
+int svr_scene_subdivide(svr_ctx* ctx, const svr_scene* scene, const uint32_t* selected,
+                        uint64_t n_selected, svr_scene** out);
+int svr_scene_remap(const svr_scene* scene, int64_t* voxel_src, int64_t* pool_src);
 /* Counts, degree and bounds of a device scene (array pointers left NULL). */
 int svr_scene_info(const svr_scene* scene, svr_scene_desc* out);
 /* Host copies of a device scene's arrays (any pointer may be NULL). */

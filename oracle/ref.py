@@ -321,6 +321,27 @@ def ref_train_iteration_grads(scene: RefScene, cam, opts, gt, lambda_ssim, w_T, 
     return losses, gd, gs, gp
 
 
+def ref_adapt(scene: RefScene, prune_stats=None, threshold=0.0, selected=None):
+    """prune (stats, threshold) or subdivide_voxels (selected) of the
+    reference (optim.cpp:207-298): (new RefScene, voxel_src, pool_src)."""
+    n = scene.arrays().n_voxels
+    lib = load_ref()
+    h = C.c_void_p()
+    nv, npool = C.c_uint64(), C.c_uint64()
+    if prune_stats is not None:
+        st = np.ascontiguousarray(prune_stats, np.float64)
+        vs, ps = np.empty(max(n, 1), np.int64), np.empty(max(8 * n, 1), np.int64)
+        _chk(lib.ref_prune(scene.h, _p(st), C.c_double(threshold), C.byref(h), _p(vs), _p(ps),
+                           C.byref(nv), C.byref(npool)))
+    else:
+        sel = np.ascontiguousarray(selected, np.uint32)
+        cap = n + 7 * sel.size
+        vs, ps = np.empty(max(cap, 1), np.int64), np.empty(max(8 * cap, 1), np.int64)
+        _chk(lib.ref_subdivide(scene.h, _p(sel), C.c_uint64(sel.size), C.byref(h), _p(vs), _p(ps),
+                               C.byref(nv), C.byref(npool)))
+    return RefScene(h), vs[:nv.value].copy(), ps[:npool.value].copy()
+
+
 def ref_image_losses(a, b, w_mse, w_ssim, grads=True):
     """mse_loss + ssim_loss (losses.cpp:71-139): ((mse, 1 - ssim), d)."""
     a = np.ascontiguousarray(a, np.float64)

@@ -479,6 +479,38 @@ int ref_adam_step(float* params, const double* grads, double* m, double* v, uint
     });
 }
 
+// prune / subdivide_voxels (optim.cpp:207-298) with their AdaptRemap; the
+// remap arrays must hold the new voxel / pool counts (callers over-allocate).
+int ref_prune(void* h, const double* stats, double thr, void** out, int64_t* voxel_src,
+              int64_t* pool_src, uint64_t* n_vox, uint64_t* n_pool) {
+    return guarded([&] {
+        auto* s = static_cast<SparseScene*>(h);
+        std::vector<double> st(stats, stats + s->voxel_count());
+        AdaptRemap rm;
+        auto* o = new SparseScene(prune(*s, st, thr, &rm));
+        *n_vox = o->voxel_count();
+        *n_pool = o->pool_count();
+        std::memcpy(voxel_src, rm.voxel_src.data(), rm.voxel_src.size() * 8);
+        std::memcpy(pool_src, rm.pool_src.data(), rm.pool_src.size() * 8);
+        *out = o;
+    });
+}
+
+int ref_subdivide(void* h, const uint32_t* sel, uint64_t n_sel, void** out, int64_t* voxel_src,
+                  int64_t* pool_src, uint64_t* n_vox, uint64_t* n_pool) {
+    return guarded([&] {
+        auto* s = static_cast<SparseScene*>(h);
+        std::vector<uint32_t> sv(sel, sel + n_sel);
+        AdaptRemap rm;
+        auto* o = new SparseScene(subdivide_voxels(*s, sv, &rm));
+        *n_vox = o->voxel_count();
+        *n_pool = o->pool_count();
+        std::memcpy(voxel_src, rm.voxel_src.data(), rm.voxel_src.size() * 8);
+        std::memcpy(pool_src, rm.pool_src.data(), rm.pool_src.size() * 8);
+        *out = o;
+    });
+}
+
 // ray_losses (losses.cpp:141-238) on a training frame; fresh zero upstream
 // buffers sized by the reference itself, copied out (NULL = not wanted).
 int ref_frame_ray_losses(void* fh, const double* gt, double w_T, double w_dist, double w_R,

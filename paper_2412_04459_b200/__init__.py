@@ -116,7 +116,8 @@ EXPORTS = [
     "svr_last_error", "svr_abi_version", "svr_ctx_create", "svr_ctx_destroy", "svr_ctx_stream",
     "svr_ctx_synchronize", "svr_ctx_set_async", "svr_ctx_overflow_count", "svr_ctx_set_debug", "svr_scene_upload", "svr_scene_set_params",
     "svr_scene_destroy", "svr_scene_param_ptrs", "svr_scene_save_svrx", "svr_scene_load_svrx",
-    "svr_scene_info", "svr_scene_download", "svr_frame_create", "svr_frame_destroy",
+    "svr_scene_info", "svr_scene_download", "svr_scene_prune", "svr_scene_subdivide",
+    "svr_scene_remap", "svr_frame_create", "svr_frame_destroy",
     "svr_render", "svr_frame_get_info", "svr_frame_download", "svr_frame_device_ptr",
     "svr_frame_download_async", "svr_frame_wait", "svr_frame_records", "svr_render_backward",
     "svr_l1_loss", "svr_train_step_l1", "svr_ray_losses", "svr_adam_step", "svr_image_losses",
@@ -157,6 +158,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "svr_scene_save_svrx": (C.c_int, [P, P, C.c_char_p]),
         "svr_scene_load_svrx": (C.c_int, [P, C.c_char_p, C.POINTER(P)]),
         "svr_scene_info": (C.c_int, [P, C.POINTER(svr_scene_desc)]),
+        "svr_scene_prune": (C.c_int, [P, P, P, C.c_uint64, C.c_double, C.c_int32, C.POINTER(P)]),
+        "svr_scene_subdivide": (C.c_int, [P, P, P, C.c_uint64, C.POINTER(P)]),
+        "svr_scene_remap": (C.c_int, [P, P, P]),
         "svr_scene_download": (C.c_int, [P, P, P, P, P, P, P]),
         "svr_scene_param_ptrs": (C.c_int, [P, C.POINTER(P), C.POINTER(P),
                                            C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
@@ -449,14 +453,39 @@ class Scene:
     def load_svrx(cls, ctx: Context, path: str) -> "Scene":
         """load_checkpoint (io.cpp:281-359) straight into a device scene
         (svr_scene_load_svrx); `arrays` is read back from the device."""
-        self = cls.__new__(cls)
-        self.ctx = ctx
         h = C.c_void_p()
         _check(ctx._lib.svr_scene_load_svrx(ctx.h, os.fsencode(path), C.byref(h)))
-        self.h = h
-        self._keep = None
+        return cls._adopt(ctx, h)
+
+    @classmethod
+    def _adopt(cls, ctx: Context, h) -> "Scene":
+        self = cls.__new__(cls)
+        self.ctx, self.h, self._keep = ctx, h, None
         self.arrays = self.download()
         return self
+
+    def prune(self, max_blend_weight, threshold: float) -> "Scene":
+        """prune (optim.cpp:207-234) on the device: a new scene."""
+        st = np.ascontiguousarray(max_blend_weight, dtype=np.float32).reshape(-1)
+        h = C.c_void_p()
+        _check(self.ctx._lib.svr_scene_prune(self.ctx.h, self.h, _ptr(st), st.size, threshold, 0,
+                                             C.byref(h)))
+        return Scene._adopt(self.ctx, h)
+
+    def subdivide(self, selected) -> "Scene":
+        """subdivide_voxels (optim.cpp:236-298) on the device: a new scene."""
+        sel = np.ascontiguousarray(selected, dtype=np.uint32).reshape(-1)
+        h = C.c_void_p()
+        _check(self.ctx._lib.svr_scene_subdivide(self.ctx.h, self.h, _ptr(sel), sel.size,
+                                                 C.byref(h)))
+        return Scene._adopt(self.ctx, h)
+
+    def remap(self):
+        """AdaptRemap of an adapted scene: (voxel_src, pool_src), -1 = new."""
+        vs = np.empty(self.arrays.n_voxels, np.int64)
+        ps = np.empty(self.arrays.n_pool, np.int64)
+        _check(self.ctx._lib.svr_scene_remap(self.h, _ptr(vs), _ptr(ps)))
+        return vs, ps
 
     def save_svrx(self, path: str) -> None:
         """save_checkpoint (io.cpp:250-279) of the scene's current device parameters."""

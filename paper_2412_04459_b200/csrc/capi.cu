@@ -980,6 +980,63 @@ int svr_scene_upload(svr_ctx* ctx, const svr_scene_desc* d, svr_scene** out) {
     });
 }
 
+int svr_scene_prune(svr_ctx* ctx, const svr_scene* s, const float* max_blend_weight, uint64_t n,
+                    double threshold, int32_t on_device, svr_scene** out) {
+    return guard([&] {
+        require(ctx && s && out, SVR_ERR_INVALID_ARGUMENT, "null argument");
+        require(n == s->n_voxels, SVR_ERR_INVALID_ARGUMENT, "prune: stats size mismatch");
+        set_device(ctx);
+        cudaStream_t st = ctx->stream;
+        DevBuf stat, keep;
+        const float* dstat = max_blend_weight;
+        if (!on_device && n) {
+            stat.reserve(n * 4);
+            SVR_CUDA(cudaMemcpyAsync(stat.p, max_blend_weight, n * 4, cudaMemcpyHostToDevice, st));
+            dstat = stat.as<float>();
+        }
+        keep.reserve(std::max<uint64_t>(n, 1) * 4);
+        if (n) launch_keep_flags(dstat, n, threshold, keep.as<uint32_t>(), st);
+        *out = adapt_scene(ctx, s, keep.as<uint32_t>(), false, 0.0f);
+    });
+}
+
+int svr_scene_subdivide(svr_ctx* ctx, const svr_scene* s, const uint32_t* selected, uint64_t n_sel,
+                        svr_scene** out) {
+    return guard([&] {
+        require(ctx && s && out && (n_sel == 0 || selected), SVR_ERR_INVALID_ARGUMENT,
+                "null argument");
+        set_device(ctx);
+        const uint64_t N = s->n_voxels;
+        std::vector<uint64_t> paths(N);
+        if (N) SVR_CUDA(cudaMemcpy(paths.data(), s->paths.p, N * 8, cudaMemcpyDeviceToHost));
+        std::vector<uint32_t> sel(N, 0u);
+        uint64_t n_new = 0;
+        for (uint64_t q = 0; q < n_sel; ++q) {  // optim.cpp:239-245
+            const uint32_t vi = selected[q];
+            require(vi < N, SVR_ERR_INVALID_ARGUMENT, "subdivide: voxel id out of range");
+            if (int(paths[vi] >> 48) >= kMaxLevel) continue;  // finest level: kept as-is
+            if (!sel[vi]) ++n_new;
+            sel[vi] = 1u;
+        }
+        require(N + 7 * n_new <= (uint64_t(1) << 29), SVR_ERR_LENGTH,
+                "subdivision exceeds voxel capacity");
+        DevBuf flags;
+        flags.reserve(std::max<uint64_t>(N, 1) * 4);
+        if (N) SVR_CUDA(cudaMemcpy(flags.p, sel.data(), N * 4, cudaMemcpyHostToDevice));
+        *out = adapt_scene(ctx, s, flags.as<uint32_t>(), true, 0.0f);
+    });
+}
+
+int svr_scene_remap(const svr_scene* s, int64_t* voxel_src, int64_t* pool_src) {
+    return guard([&] {
+        require(s && s->has_remap, SVR_ERR_INVALID_ARGUMENT, "scene was not produced by adaptation");
+        if (voxel_src && s->n_voxels)
+            SVR_CUDA(cudaMemcpy(voxel_src, s->voxel_src.p, s->n_voxels * 8, cudaMemcpyDeviceToHost));
+        if (pool_src && s->n_pool)
+            SVR_CUDA(cudaMemcpy(pool_src, s->pool_src.p, s->n_pool * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
 int svr_scene_info(const svr_scene* s, svr_scene_desc* out) {
     return guard([&] {
         require(s && out, SVR_ERR_INVALID_ARGUMENT, "null argument");

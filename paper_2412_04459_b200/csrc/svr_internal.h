@@ -65,6 +65,11 @@ struct HostBuf {
     ~HostBuf();
 };
 
+// adapt.cu: prune / subdivide_voxels on the device (flags: keep / selected).
+svr_scene* adapt_scene(svr_ctx* ctx, const svr_scene* old, const uint32_t* flags, bool subdivide,
+                       float fill);
+void launch_keep_flags(const float* stat, uint64_t n, double thr, uint32_t* keep, cudaStream_t st);
+
 }  // namespace svrb
 
 struct svr_ctx {
@@ -97,6 +102,9 @@ struct svr_scene {
     svrb::DevBuf sh;            // f32 [n][stride]
     svrb::DevBuf morton_rank;   // u32 [8][n]: build_morton_rank (sort keys)
     int rank_bits = 0;          // bit width of 8n-1; 0 = no table
+    // AdaptRemap of a scene produced by svr_scene_prune / svr_scene_subdivide
+    svrb::DevBuf voxel_src, pool_src;  // int64 per voxel / per pool entry
+    bool has_remap = false;
 };
 
 // Per-view state. Also the device half of svr::ForwardRecords.
