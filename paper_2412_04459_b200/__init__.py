@@ -459,10 +459,22 @@ class Scene:
 
     @classmethod
     def _adopt(cls, ctx: Context, h) -> "Scene":
+        """Wraps a scene created on the device; its host `arrays` are read
+        back on first use."""
         self = cls.__new__(cls)
         self.ctx, self.h, self._keep = ctx, h, None
-        self.arrays = self.download()
+        self._arrays = None
         return self
+
+    @property
+    def arrays(self) -> SceneArrays:
+        if getattr(self, "_arrays", None) is None:
+            self._arrays = self.download()
+        return self._arrays
+
+    @arrays.setter
+    def arrays(self, value: SceneArrays) -> None:
+        self._arrays = value
 
     def prune(self, max_blend_weight, threshold: float) -> "Scene":
         """prune (optim.cpp:207-234) on the device: a new scene."""
