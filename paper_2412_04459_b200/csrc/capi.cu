@@ -27,6 +27,14 @@ std::atomic<unsigned long long> g_launches{0};
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SVR_PDL");
+        return e == nullptr || e[0] != '0';
+    }();
+    return on;
+}
+
 // Records a stage boundary on the context stream (no-op unless timing).
 void mark(svr_ctx* ctx, int stage) {
     if (!ctx->timing) return;

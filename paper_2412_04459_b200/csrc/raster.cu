@@ -32,6 +32,7 @@ constexpr int kSatSmemMax = 48 * 1024;  // u32 entries that fit the dynamic smem
 __global__ void __launch_bounds__(1024) tile_setup_kernel(DevCamera cam, uint8_t* masks,
                                                           uint32_t* sat, FrameStatus* status,
                                                           int use_smem) {
+    pdl_enter();
     extern __shared__ uint32_t s_sat[];
     const int ntx = cam.ntx, nty = cam.nty, ntiles = ntx * nty;
     const int sw = ntx + 1, ncell = sw * (nty + 1);
@@ -80,6 +81,7 @@ __global__ void __launch_bounds__(1024) tile_setup_kernel(DevCamera cam, uint8_t
 }
 
 __global__ void tile_masks_kernel(DevCamera cam, uint8_t* masks) {
+    pdl_enter();
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= cam.ntx * cam.nty) return;
     masks[t] = uint8_t(tile_sign_mask(cam, t % cam.ntx, t / cam.ntx));
@@ -107,6 +109,7 @@ constexpr int kPreThreads = 128;
 #endif
 
 __global__ void __launch_bounds__(kPreThreads, SVR_PRE_MINB) preprocess_kernel(DevCamera cam, PreprocessArgs a) {
+    pdl_enter();
     extern __shared__ float4 smem4[];
 #if SVR_PRE_SMEM_SH
     float* smem = reinterpret_cast<float*>(smem4);
@@ -342,6 +345,7 @@ __global__ void __launch_bounds__(256) duplicate_packed_kernel(
     const uint8_t* __restrict__ masks, const uint32_t* __restrict__ counts,
     const uint32_t* __restrict__ offsets, PackedFormat fmt, const uint32_t* __restrict__ rank,
     uint64_t* __restrict__ keys, uint32_t* big, unsigned int* n_big, uint64_t cap) {
+    pdl_enter();
     const uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (v >= n) return;
     const uint32_t cnt = counts[v];
@@ -377,6 +381,7 @@ __global__ void __launch_bounds__(256) duplicate_big_kernel(
     const uint32_t* __restrict__ tile_sat, PackedFormat fmt, const uint32_t* __restrict__ rank,
     uint64_t* __restrict__ keys, const uint32_t* __restrict__ big,
     const unsigned int* __restrict__ n_big) {
+    pdl_enter();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t nb = *n_big;
     for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
@@ -428,6 +433,7 @@ __global__ void rank_scatter_kernel(const uint32_t* __restrict__ vals, uint64_t 
 __global__ void tile_ranges_packed_kernel(const uint64_t* __restrict__ keys, uint64_t n,
                                           PackedFormat fmt, uint2* ranges, uint32_t* vals,
                                           const unsigned long long* n_dev) {
+    pdl_enter();
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (n_dev) n = min(n, uint64_t(*n_dev));  // deferred-E frame: the device count decides
     if (i >= n) return;
@@ -471,6 +477,7 @@ __global__ void tile_ranges_kernel(const uint64_t* keys, uint64_t n, uint2* rang
 // the first wave and the kernel tail is made of short ones.
 __global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* ranges, int ntiles,
                                                           uint32_t* order) {
+    pdl_enter();
     __shared__ uint32_t s_cnt[33];
     if (threadIdx.x < 33) s_cnt[threadIdx.x] = 0;
     __syncthreads();
@@ -555,6 +562,7 @@ constexpr size_t kCompSmem = size_t(2) * kCompWarps * 32 * kRecordF4 * sizeof(fl
 
 template <int K, bool RECORD>
 __global__ void __launch_bounds__(256, 4) composite_kernel(DevCamera cam, CompositeArgs a) {
+    pdl_enter();
     extern __shared__ float4 s_rec_dyn[];  // [2][8 warps][32 slots][kRecordF4]
     __shared__ uint32_t s_vid[2][kCompWarps][32];
     __shared__ uint8_t s_j[2][kCompWarps][32];  // chunk-local entry index of each slot
@@ -887,6 +895,7 @@ __global__ void project_batch_kernel(DevCamera cam, uint64_t n, const double* ce
 // asynchronous image download on the copy stream.
 __global__ void status_to_host_kernel(const FrameStatus* d, FrameStatus* h, uint64_t cap,
                                       unsigned int* overflow_count) {
+    pdl_enter();
     *h = *d;
     if (overflow_count && d->n_entries > cap) atomicAdd(overflow_count, 1u);
 }
@@ -897,7 +906,7 @@ inline unsigned blocks_for(uint64_t n, int threads) { return unsigned((n + threa
 
 void launch_status_to_host(const FrameStatus* d, FrameStatus* h, cudaStream_t st, uint64_t cap,
                            unsigned int* overflow_count) {
-    status_to_host_kernel<<<1, 1, 0, st>>>(d, h, cap, overflow_count);
+    launch_pdl(status_to_host_kernel, 1, 1, 0, st, d, h, cap, overflow_count);
     SVR_LAUNCH("status_to_host_kernel");
 }
 
@@ -914,9 +923,9 @@ void launch_tile_setup(const DevCamera& cam, uint8_t* masks, uint32_t* sat, Fram
     }
     // masks: one thread per tile (fp64 corner rays); then the SAT in one CTA
     const int ntiles = cam.ntx * cam.nty;
-    tile_masks_kernel<<<blocks_for(ntiles, 128), 128, 0, st>>>(cam, masks);
+    launch_pdl(tile_masks_kernel, blocks_for(ntiles, 128), 128, 0, st, cam, masks);
     SVR_LAUNCH("tile_masks_kernel");
-    tile_setup_kernel<<<1, 1024, smem, st>>>(cam, masks, sat, status, use_smem);
+    launch_pdl(tile_setup_kernel, 1, 1024, smem, st, cam, masks, sat, status, use_smem);
     SVR_LAUNCH("tile_setup_kernel");
 }
 
@@ -934,7 +943,7 @@ void launch_preprocess(const DevCamera& cam, const PreprocessArgs& a, cudaStream
 #else
     const size_t smem = size_t(kPreThreads) * kRecordF4 * 16;
 #endif
-    preprocess_kernel<<<blocks_for(a.n, kPreThreads), kPreThreads, smem, st>>>(cam, a);
+    launch_pdl(preprocess_kernel, blocks_for(a.n, kPreThreads), kPreThreads, smem, st, cam, a);
     SVR_LAUNCH("preprocess_kernel");
 }
 
@@ -970,11 +979,10 @@ void launch_duplicate_packed(const DevCamera& cam, uint64_t n, const uint64_t* p
                              uint64_t* keys, const uint32_t* tile_sat, uint32_t* big,
                              unsigned int* n_big, cudaStream_t st, uint64_t cap) {
     if (n == 0) return;
-    duplicate_packed_kernel<<<blocks_for(n, 256), 256, 0, st>>>(cam, n, paths, rects, masks, counts,
-                                                                offsets, fmt, rank, keys, big, n_big,
-                                                                cap);
+    launch_pdl(duplicate_packed_kernel, blocks_for(n, 256), 256, 0, st, cam, n, paths, rects, masks,
+               counts, offsets, fmt, rank, keys, big, n_big, cap);
     SVR_LAUNCH("duplicate_packed_kernel");
-    duplicate_big_kernel<<<148 * 4, 256, 0, st>>>(cam, n, paths, rects, masks, offsets, tile_sat,
+    launch_pdl(duplicate_big_kernel, 148 * 4, 256, 0, st, cam, n, paths, rects, masks, offsets, tile_sat,
                                                    fmt, rank, keys, big, n_big);
     SVR_LAUNCH("duplicate_big_kernel");
 }
@@ -1015,7 +1023,7 @@ void launch_tile_ranges_packed(const uint64_t* keys, uint64_t n, PackedFormat fm
                                const unsigned long long* n_dev) {
     SVR_CUDA(cudaMemsetAsync(ranges, 0, size_t(ntiles) * sizeof(uint2), st));
     if (n == 0) return;
-    tile_ranges_packed_kernel<<<blocks_for(n, 256), 256, 0, st>>>(keys, n, fmt, ranges, vals, n_dev);
+    launch_pdl(tile_ranges_packed_kernel, blocks_for(n, 256), 256, 0, st, keys, n, fmt, ranges, vals, n_dev);
     SVR_LAUNCH("tile_ranges_packed_kernel");
 }
 
@@ -1044,7 +1052,7 @@ void launch_compact_contribs(const uint32_t* pix_count, const uint32_t* pix_begi
 }
 
 void launch_tile_order(const uint2* ranges, int ntiles, uint32_t* order, cudaStream_t st) {
-    tile_order_kernel<<<1, 1024, 0, st>>>(ranges, ntiles, order);
+    launch_pdl(tile_order_kernel, 1, 1024, 0, st, ranges, ntiles, order);
     SVR_LAUNCH("tile_order_kernel");
 }
 
@@ -1061,9 +1069,9 @@ void launch_composite(const DevCamera& cam, const CompositeArgs& a, bool record_
 #define SVR_COMPOSITE_CASE(KK)                                                        \
     case KK:                                                                          \
         if (record_pass)                                                              \
-            composite_kernel<KK, true><<<ntiles, 256, kCompSmem, st>>>(cam, a);      \
+            launch_pdl(composite_kernel<KK, true>, ntiles, 256, kCompSmem, st, cam, a); \
         else                                                                          \
-            composite_kernel<KK, false><<<ntiles, 256, kCompSmem, st>>>(cam, a);     \
+            launch_pdl(composite_kernel<KK, false>, ntiles, 256, kCompSmem, st, cam, a); \
         break;
     switch (a.K) {
         SVR_COMPOSITE_CASE(1)

@@ -63,6 +63,7 @@ __device__ __forceinline__ void load_items(const uint32_t* in, uint64_t n, uint6
 
 __global__ void __launch_bounds__(kThreads) scan_reduce_kernel(const uint32_t* in, uint64_t n,
                                                                uint32_t* partial) {
+    pdl_enter();
     __shared__ uint32_t s_warp[kThreads / 32 + 1];
     uint32_t x[kItems];
     load_items(in, n, uint64_t(blockIdx.x) * kChunk, x);
@@ -77,6 +78,7 @@ __global__ void __launch_bounds__(kThreads) scan_reduce_kernel(const uint32_t* i
 // Single block: exclusive scan of the block partials (in place), u64 total.
 __global__ void __launch_bounds__(kThreads) scan_partials_kernel(uint32_t* partial, uint64_t nb,
                                                                  unsigned long long* total) {
+    pdl_enter();
     __shared__ uint32_t s_warp[kThreads / 32 + 1];
     unsigned long long carry = 0;
     for (uint64_t base = 0; base < nb; base += kThreads) {
@@ -92,6 +94,7 @@ __global__ void __launch_bounds__(kThreads) scan_partials_kernel(uint32_t* parti
 
 __global__ void __launch_bounds__(kThreads) scan_apply_kernel(const uint32_t* in, uint32_t* out,
                                                               uint64_t n, const uint32_t* partial) {
+    pdl_enter();
     __shared__ uint32_t s_warp[kThreads / 32 + 1];
     uint32_t x[kItems];
     const uint64_t base = uint64_t(blockIdx.x) * kChunk;
@@ -121,11 +124,11 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, unsigned 
     }
     uint64_t nb = (n + kChunk - 1) / kChunk;
     uint32_t* partial = static_cast<uint32_t*>(scratch);
-    scan_reduce_kernel<<<unsigned(nb), kThreads, 0, st>>>(in, n, partial);
+    launch_pdl(scan_reduce_kernel, unsigned(nb), kThreads, 0, st, in, n, partial);
     SVR_LAUNCH("scan_reduce_kernel");
-    scan_partials_kernel<<<1, kThreads, 0, st>>>(partial, nb, total);
+    launch_pdl(scan_partials_kernel, 1, kThreads, 0, st, partial, nb, total);
     SVR_LAUNCH("scan_partials_kernel");
-    scan_apply_kernel<<<unsigned(nb), kThreads, 0, st>>>(in, out, n, partial);
+    launch_pdl(scan_apply_kernel, unsigned(nb), kThreads, 0, st, in, out, n, partial);
     SVR_LAUNCH("scan_apply_kernel");
 }
 

@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(kThreads) hist_kernel(const uint64_t* keys, co
                                                         uint64_t n, PassSpec spec,
                                                         uint32_t* hist,
                                                         const unsigned long long* n_dev) {
+    pdl_enter();
     if (n_dev) n = min(n, uint64_t(*n_dev));
     __shared__ uint32_t s_hist[kMaxRadixPasses][kRadix];
     for (int i = threadIdx.x; i < spec.n * kRadix; i += kThreads) (&s_hist[0][0])[i] = 0;
@@ -74,6 +75,7 @@ __global__ void __launch_bounds__(kThreads) hist_kernel(const uint64_t* keys, co
 
 // One block per pass: exclusive scan of the 256 digit counts.
 __global__ void __launch_bounds__(kRadix) bin_scan_kernel(uint32_t* hist) {
+    pdl_enter();
     __shared__ uint32_t s[kRadix];
     uint32_t* h = hist + blockIdx.x * kRadix;
     uint32_t v = h[threadIdx.x];
@@ -103,6 +105,7 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
     uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint64_t n, RadixPass pass,
     const uint32_t* __restrict__ bin_base, uint32_t* status, uint32_t* ticket,
     const unsigned long long* n_dev) {
+    pdl_enter();
     __shared__ uint32_t s_warp_hist[kWarps][kRadix + 1];
     __shared__ uint32_t s_block_excl[kRadix];
     __shared__ uint32_t s_global[kRadix];
@@ -307,18 +310,19 @@ int radix_sort_keys(uint64_t* keys0, uint64_t* keys1, uint64_t n, const RadixPas
         spec.n = npasses;
         for (int i = 0; i < npasses; ++i) spec.p[i] = passes[i];
         int hist_blocks = int(std::min<uint64_t>((n + kThreads - 1) / kThreads, 148 * 4));
-        hist_kernel<<<hist_blocks, kThreads, 0, st>>>(keys0, nullptr, n, spec, hist, n_dev);
+        launch_pdl(hist_kernel, hist_blocks, kThreads, 0, st, keys0, (const uint32_t*)nullptr, n, spec, hist, n_dev);
         SVR_LAUNCH("hist_kernel");
     }
-    bin_scan_kernel<<<npasses, kRadix, 0, st>>>(hist);
+    launch_pdl(bin_scan_kernel, npasses, kRadix, 0, st, hist);
     SVR_LAUNCH("bin_scan_kernel");
     uint64_t* kin = keys0;
     uint64_t* kout = keys1;
     int cur = 0;
     for (int p = 0; p < npasses; ++p) {
-        onesweep_kernel<false><<<unsigned(nparts), kThreads, 0, st>>>(
-            kin, nullptr, kout, nullptr, n, passes[p], hist + p * kRadix,
-            status + size_t(p) * (nparts_alloc + 1) * kRadix, tickets + p, n_dev);
+        launch_pdl(onesweep_kernel<false>, unsigned(nparts), kThreads, 0, st, (const uint64_t*)kin,
+                   (const uint32_t*)nullptr, kout, (uint32_t*)nullptr, n, passes[p],
+                   (const uint32_t*)(hist + p * kRadix), status + size_t(p) * (nparts_alloc + 1) * kRadix,
+                   tickets + p, n_dev);
         SVR_LAUNCH("onesweep_kernel");
         std::swap(kin, kout);
         cur ^= 1;

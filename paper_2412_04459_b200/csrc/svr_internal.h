@@ -23,6 +23,25 @@ struct Error : std::runtime_error {
 
 void cuda_check(cudaError_t e, const char* what);
 void count_launch();
+
+// Frame kernels are launched with programmatic stream serialisation
+// (svr_math.cuh: pdl_enter); SVR_PDL=0 turns it off.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cuda_check(cudaLaunchKernelEx(&cfg, kernel, KArgs(args)...), "cudaLaunchKernelEx");
+}
 #define SVR_CUDA(x) ::svrb::cuda_check((x), #x)
 #define SVR_LAUNCH(what) (::svrb::count_launch(), ::svrb::cuda_check(cudaGetLastError(), what))
 

@@ -32,6 +32,21 @@ constexpr uint64_t kGroupOnes = 0x249249249249ull;  // octree.hpp:19
 constexpr double kAabbPad = 1e-6;                     // raster.cpp:11
 constexpr float kExplinKnee = 1.1f;                   // field.hpp:19
 
+// Programmatic dependent launch (sm_90+): a frame's kernels are launched
+// with programmatic stream serialisation, so the next kernel's CTAs are
+// scheduled while the current one drains; every such kernel first waits for
+// its predecessor's completion (griddepcontrol.wait) and lets its own
+// dependents launch (griddepcontrol.launch_dependents). Both are no-ops for
+// a kernel launched without the attribute.
+#if defined(__CUDA_ARCH__)
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+#else
+inline void pdl_enter() {}
+#endif
+
 // ---------------------------------------------------------------- fp64 exact
 #if defined(__CUDA_ARCH__)
 SVR_HD double dadd(double a, double b) { return __dadd_rn(a, b); }
