@@ -25,6 +25,7 @@ namespace {
 
 __global__ void lift_kernel(TapTable t, const float* g, int ch, int W, float* out, int sw,
                             int sh) {
+    pdl_enter();
     int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
     if (x >= sw || y >= sh) return;
     float acc[3] = {0.f, 0.f, 0.f};
@@ -44,6 +45,7 @@ __global__ void lift_kernel(TapTable t, const float* g, int ch, int W, float* ou
 
 __global__ void l1_kernel(const float* c, const float* gt, uint64_t n, float inv_n, float* d_color,
                           float* loss) {
+    pdl_enter();
     float s = 0.f;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x) {
@@ -97,6 +99,7 @@ __device__ __forceinline__ float warp_transpose_sum16(float (&v)[16], int lane) 
 #endif
 template <int K>
 __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, BackwardArgs a) {
+    pdl_enter();
     __shared__ float4 s_rec[8][32][kRecordF4];
     __shared__ float s_cone[8][4][3];
 
@@ -330,6 +333,7 @@ __device__ __forceinline__ float warp_incl_scan_f(float v, int lane) {
 
 // L_T (losses.cpp:163-174): one thread per supersampled pixel.
 __global__ void __launch_bounds__(256) ray_loss_T_kernel(RayLossArgs a, uint64_t npix) {
+    pdl_enter();
     const uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const double inv_rays = 1.0 / double(npix);
     float lT = 0.f;
@@ -347,6 +351,7 @@ __global__ void __launch_bounds__(256) ray_loss_T_kernel(RayLossArgs a, uint64_t
 
 template <int K>
 __global__ void __launch_bounds__(256) ray_losses_kernel(DevCamera cam, RayLossArgs a) {
+    pdl_enter();
     const int lane = threadIdx.x & 31;
     // grid (ceil(W / 8), H): warp w of block (bx, y) owns pixel (8 bx + w, y)
     const int px = int(blockIdx.x) * 8 + (threadIdx.x >> 5), py = int(blockIdx.y);
@@ -486,6 +491,7 @@ __global__ void __launch_bounds__(256) ray_losses_kernel(DevCamera cam, RayLossA
 constexpr float kSsimC1 = 0.01f * 0.01f, kSsimC2 = 0.03f * 0.03f;
 
 __global__ void ssim_rows_kernel(ImageLossArgs a) {
+    pdl_enter();
     const int Wv = a.W - 10;
     const uint64_t n = uint64_t(Wv) * a.H * 3;
     double sq = 0.0;
@@ -523,6 +529,7 @@ __global__ void ssim_rows_kernel(ImageLossArgs a) {
 }
 
 __global__ void ssim_cols_kernel(ImageLossArgs a) {
+    pdl_enter();
     const int Wv = a.W - 10, Hv = a.H - 10;
     const uint64_t nmid = uint64_t(Wv) * a.H * 3, nv = uint64_t(Wv) * Hv * 3;
     const double g = -a.w_ssim / double(nv);  // dL/dmean of ssim_loss: -weight
@@ -558,6 +565,7 @@ __global__ void ssim_cols_kernel(ImageLossArgs a) {
 
 // blur_adjoint (losses.cpp:47-61), column half: valid maps -> (W-10) x H
 __global__ void ssim_adj_cols_kernel(ImageLossArgs a) {
+    pdl_enter();
     const int Wv = a.W - 10, Hv = a.H - 10;
     const uint64_t nv = uint64_t(Wv) * Hv * 3, n = uint64_t(Wv) * a.H * 3;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -579,6 +587,7 @@ __global__ void ssim_adj_cols_kernel(ImageLossArgs a) {
 
 // row half of the adjoint, then d_a += g1 + 2 a g2 + b g3 (losses.cpp:110-115)
 __global__ void ssim_adj_rows_kernel(ImageLossArgs a) {
+    pdl_enter();
     const int Wv = a.W - 10;
     const uint64_t nm = uint64_t(Wv) * a.H * 3, n = uint64_t(a.W) * a.H * 3;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -601,6 +610,7 @@ __global__ void ssim_adj_rows_kernel(ImageLossArgs a) {
 // Every double operation is explicitly rounded (no FMA contraction) in the
 // reference's order, so params match std::vector<float> updates exactly.
 __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
+    pdl_enter();
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < a.n;
          i += uint64_t(gridDim.x) * blockDim.x) {
         const double g = double(a.grads[i]);
@@ -625,6 +635,7 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
 // raw colour for the clamp mask (sh.hpp:66-74) is reduced over the 16 lanes;
 // the normal chain (field.hpp:158-170) runs on the first lane.
 __global__ void __launch_bounds__(256) voxel_epilogue_kernel(EpilogueArgs a) {
+    pdl_enter();
     const uint64_t v = uint64_t(blockIdx.x) * 16u + (threadIdx.x >> 4);
     const int m = threadIdx.x & 15;
     const bool live = v < a.n;
@@ -700,7 +711,7 @@ inline unsigned blocks_for(uint64_t n, int threads) { return unsigned((n + threa
 void launch_lift(const TapTable& t, const float* g, int channels, int W, float* out, int sw,
                  int sh, cudaStream_t st) {
     dim3 grid(blocks_for(sw, 128), sh);
-    lift_kernel<<<grid, 128, 0, st>>>(t, g, channels, W, out, sw, sh);
+    launch_pdl(lift_kernel, grid, 128, 0, st, t, g, channels, W, out, sw, sh);
     SVR_LAUNCH("lift_kernel");
 }
 
@@ -708,7 +719,7 @@ void launch_l1_loss(const float* color, const float* gt, uint64_t n, float* d_co
                     cudaStream_t st) {
     if (loss) SVR_CUDA(cudaMemsetAsync(loss, 0, sizeof(float), st));
     unsigned blocks = unsigned(std::min<uint64_t>(blocks_for(n, 256), 148 * 8));
-    l1_kernel<<<blocks, 256, 0, st>>>(color, gt, n, 1.0f / float(n), d_color, loss);
+    launch_pdl(l1_kernel, blocks, 256, 0, st, color, gt, n, 1.0f / float(n), d_color, loss);
     SVR_LAUNCH("l1_kernel");
 }
 
@@ -716,13 +727,13 @@ void launch_composite_backward(const DevCamera& cam, const BackwardArgs& a, cuda
     const unsigned ntiles = unsigned(cam.ntx * cam.nty);
     switch (a.K) {
         case 1:
-            composite_backward_kernel<1><<<ntiles, 256, 0, st>>>(cam, a);
+            launch_pdl(composite_backward_kernel<1>, ntiles, 256, 0, st, cam, a);
             break;
         case 2:
-            composite_backward_kernel<2><<<ntiles, 256, 0, st>>>(cam, a);
+            launch_pdl(composite_backward_kernel<2>, ntiles, 256, 0, st, cam, a);
             break;
         case 3:
-            composite_backward_kernel<3><<<ntiles, 256, 0, st>>>(cam, a);
+            launch_pdl(composite_backward_kernel<3>, ntiles, 256, 0, st, cam, a);
             break;
         default:
             throw Error(SVR_ERR_INVALID_ARGUMENT, "rasterizer sample count K must be in {1,2,3}");
@@ -733,15 +744,15 @@ void launch_composite_backward(const DevCamera& cam, const BackwardArgs& a, cuda
 void launch_ray_losses(const DevCamera& cam, const RayLossArgs& a, cudaStream_t st) {
     const uint64_t npix = uint64_t(cam.W) * cam.H;
     if (a.w_T != 0.0) {
-        ray_loss_T_kernel<<<unsigned((npix + 255) / 256), 256, 0, st>>>(a, npix);
+        launch_pdl(ray_loss_T_kernel, unsigned((npix + 255) / 256), 256, 0, st, a, npix);
         SVR_LAUNCH("ray_loss_T_kernel");
     }
     if (a.w_dist == 0.0 && a.w_R == 0.0) return;
     const dim3 grid(unsigned((cam.W + 7) / 8), unsigned(cam.H));  // a warp per pixel
     switch (a.K) {
-        case 1: ray_losses_kernel<1><<<grid, 256, 0, st>>>(cam, a); break;
-        case 2: ray_losses_kernel<2><<<grid, 256, 0, st>>>(cam, a); break;
-        case 3: ray_losses_kernel<3><<<grid, 256, 0, st>>>(cam, a); break;
+        case 1: launch_pdl(ray_losses_kernel<1>, grid, 256, 0, st, cam, a); break;
+        case 2: launch_pdl(ray_losses_kernel<2>, grid, 256, 0, st, cam, a); break;
+        case 3: launch_pdl(ray_losses_kernel<3>, grid, 256, 0, st, cam, a); break;
         default: throw Error(SVR_ERR_INVALID_ARGUMENT, "rasterizer sample count K must be in {1,2,3}");
     }
     SVR_LAUNCH("ray_losses_kernel");
@@ -749,27 +760,27 @@ void launch_ray_losses(const DevCamera& cam, const RayLossArgs& a, cudaStream_t 
 
 void launch_image_losses(const ImageLossArgs& a, cudaStream_t st) {
     const unsigned g = 148 * 8;
-    ssim_rows_kernel<<<g, 256, 0, st>>>(a);
+    launch_pdl(ssim_rows_kernel, g, 256, 0, st, a);
     SVR_LAUNCH("ssim_rows_kernel");
-    ssim_cols_kernel<<<g, 256, 0, st>>>(a);
+    launch_pdl(ssim_cols_kernel, g, 256, 0, st, a);
     SVR_LAUNCH("ssim_cols_kernel");
     if (!a.d_a || a.w_ssim == 0.0) return;
-    ssim_adj_cols_kernel<<<g, 256, 0, st>>>(a);
+    launch_pdl(ssim_adj_cols_kernel, g, 256, 0, st, a);
     SVR_LAUNCH("ssim_adj_cols_kernel");
-    ssim_adj_rows_kernel<<<g, 256, 0, st>>>(a);
+    launch_pdl(ssim_adj_rows_kernel, g, 256, 0, st, a);
     SVR_LAUNCH("ssim_adj_rows_kernel");
 }
 
 void launch_adam(const AdamArgs& a, cudaStream_t st) {
     if (a.n == 0) return;
     const unsigned blocks = unsigned(std::min<uint64_t>(blocks_for(a.n, 256), 148 * 16));
-    adam_kernel<<<blocks, 256, 0, st>>>(a);
+    launch_pdl(adam_kernel, blocks, 256, 0, st, a);
     SVR_LAUNCH("adam_kernel");
 }
 
 void launch_voxel_epilogue(const DevCamera& cam, const EpilogueArgs& a, cudaStream_t st) {
     if (a.n == 0) return;
-    voxel_epilogue_kernel<<<blocks_for(a.n, 16), 256, 0, st>>>(a);
+    launch_pdl(voxel_epilogue_kernel, blocks_for(a.n, 16), 256, 0, st, a);
     (void)cam;
     SVR_LAUNCH("voxel_epilogue_kernel");
 }

@@ -793,6 +793,7 @@ __global__ void compact_contribs_kernel(const uint32_t* __restrict__ pix_count,
                                         const uint32_t* __restrict__ stage_entry,
                                         const float* __restrict__ stage_T, uint32_t stride,
                                         uint32_t* contrib_entry, float* contrib_T) {
+    pdl_enter();
     const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
     if (slot >= stride) return;
     const uint32_t n = pix_count[slot], b = pix_begin[slot];
@@ -1046,8 +1047,8 @@ void launch_compact_contribs(const uint32_t* pix_count, const uint32_t* pix_begi
                              const uint32_t* stage_entry, const float* stage_T, uint32_t stride,
                              uint32_t* contrib_entry, float* contrib_T, cudaStream_t st) {
     if (stride == 0) return;
-    compact_contribs_kernel<<<blocks_for(stride, 256), 256, 0, st>>>(
-        pix_count, pix_begin, stage_entry, stage_T, stride, contrib_entry, contrib_T);
+    launch_pdl(compact_contribs_kernel, blocks_for(stride, 256), 256, 0, st, pix_count, pix_begin,
+               stage_entry, stage_T, stride, contrib_entry, contrib_T);
     SVR_LAUNCH("compact_contribs_kernel");
 }
 
