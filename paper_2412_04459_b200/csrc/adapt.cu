@@ -509,10 +509,11 @@ svr_scene* adapt_scene(svr_ctx* ctx, const svr_scene* old, const uint32_t* flags
         s->max_level = std::max(1, int(hml));
         if (N2 > 0 && N2 < (uint64_t(1) << 28)) {
             s->morton_rank.reserve(N2 * 8 * 4);
+            s->morton_order.reserve(N2 * 8 * 4);
             DevBuf tmp;
             tmp.reserve(morton_rank_scratch_bytes(N2, s->max_level));
             build_morton_rank(s->paths.as<uint64_t>(), N2, s->max_level, s->morton_rank.as<uint32_t>(),
-                              tmp.p, st);
+                              s->morton_order.as<uint32_t>(), tmp.p, st);
             SVR_CUDA(cudaStreamSynchronize(st));
             s->rank_bits = 0;
             for (uint64_t x = 8 * N2 - 1; x; x >>= 1) ++s->rank_bits;

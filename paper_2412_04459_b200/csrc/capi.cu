@@ -324,13 +324,23 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     const uint64_t N = scene->n_voxels;
     const bool ss1 = (sw == W && sh == H);
 
-    // K2: tile sign masks + SAT
+    // Rank-ordered duplicate (keys emitted pre-sorted below the tile bits) when
+    // the scene has its pair list; SVR_RANKED=0 keeps the voxel-order emission.
+    const char* ranked_env = std::getenv("SVR_RANKED");  // read per frame (parity tests flip it)
+    const bool ranked_enabled = ranked_env == nullptr || ranked_env[0] != '0';
+    const bool ranked_ok = ranked_enabled && N > 0 && scene->rank_bits > 0 &&
+                           (std::max(1, bit_width(N - 1)) + 3 + scene->rank_bits +
+                            bit_width(uint64_t(ntiles - 1))) <= 64;
+
+    // K2: tile sign masks + SAT (+ the per-pattern SATs of the ranked duplicate)
     uint8_t* masks = grow<uint8_t>(f->tile_masks, ntiles);
-    uint32_t* sat = grow<uint32_t>(f->tile_sat, uint64_t(cam.ntx + 1) * (cam.nty + 1));
+    const uint64_t ncell = uint64_t(cam.ntx + 1) * (cam.nty + 1);
+    uint32_t* sat = grow<uint32_t>(f->tile_sat, ncell * (ranked_ok ? 9 : 1));
     FrameStatus* status = grow<FrameStatus>(f->status, 1);
     SVR_CUDA(cudaMemsetAsync(status, 0, sizeof(FrameStatus), st));
     mark(ctx, kStageTileSetup);
-    launch_tile_setup(cam, masks, sat, status, st);
+    int2* rowspan = ranked_ok ? grow<int2>(f->rowspan, uint64_t(8) * cam.nty) : nullptr;
+    launch_tile_setup(cam, masks, sat, status, st, rowspan);
 
     // K1: preprocess
     PreprocessArgs pa{};
@@ -353,11 +363,26 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     mark(ctx, kStagePreprocess);
     launch_preprocess(cam, pa, st);
 
-    // K3: scan of the per-voxel entry counts -> emission offsets, E
+    // K3: scan of the entry counts -> emission offsets and E: per (pattern,
+    // voxel) pair in rank order for the ranked duplicate, else per voxel (also
+    // for the ranked path's parity dump of the voxel-order emission).
     uint32_t* offsets = grow<uint32_t>(f->offsets, N);
-    ctx->scratch.reserve(scan_scratch_bytes(std::max<uint64_t>(N, uint64_t(ntiles) * 256)));
+    uint32_t* pc = nullptr;
+    const size_t scan_bytes = scan_scratch_bytes(std::max<uint64_t>(N, uint64_t(ntiles) * 256));
+    ctx->scratch.reserve(scan_bytes + (ranked_ok ? scan_scratch_bytes(8 * N) + 256 : 0));
+    // the ranked path's block prefixes live past the general scan scratch
+    uint32_t* pair_partial = reinterpret_cast<uint32_t*>(static_cast<char*>(ctx->scratch.p) +
+                                                         ((scan_bytes + 255) & ~size_t(255)));
     mark(ctx, kStageScan);
-    exclusive_scan_u32(pa.counts, offsets, N, &status->n_entries, ctx->scratch.p, st);
+    if (ranked_ok) {
+        pc = grow<uint32_t>(f->pair_counts, 8 * N);
+        launch_pair_counts(cam, N, pa.counts, pa.rects, sat, status, scene->morton_rank.as<uint32_t>(), pc,
+                           st);
+        scan_block_prefixes(pc, 8 * N, &status->n_entries, pair_partial, st);
+    }
+    if (!ranked_ok || ctx->debug)
+        exclusive_scan_u32(pa.counts, offsets, N, ranked_ok ? &status->n_entries_voxel : &status->n_entries,
+                           ctx->scratch.p, st);
     mark(ctx, -1);
     f->hstatus.reserve(sizeof(FrameStatus));
     FrameStatus* hs = static_cast<FrameStatus*>(f->hstatus.p);
@@ -411,7 +436,11 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     if (f->packed) {
         f->fmt = use_rank ? PackedFormat{vb, lmax, vb + 3 + rb, rb}
                           : PackedFormat{vb, lmax, vb + 3 + 3 * lmax, 0};
-        const int lo = vb + ((multi && !use_rank) ? 0 : 3), hi = f->fmt.tile_shift + tile_bits;
+        const bool ranked = ranked_ok;
+        require(!ranked || use_rank, SVR_ERR_RUNTIME, "ranked duplicate needs rank keys");
+        // ranked emission: the keys arrive sorted below the tile bits
+        const int lo = ranked ? f->fmt.tile_shift : vb + ((multi && !use_rank) ? 0 : 3);
+        const int hi = f->fmt.tile_shift + tile_bits;
         for (int b = lo; b < hi; b += 8) passes[np++] = {0, b, std::min(8, hi - b)};
         RadixPlan plan{};
         plan.n = np;
@@ -421,14 +450,23 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
         grow<uint32_t>(f->vals[0], E);
         ctx->scratch2.reserve(sort_scratch_bytes(E, np));
         mark(ctx, kStageDuplicate);
-        launch_duplicate_packed(cam, N, pa.paths, pa.rects, masks, pa.counts, offsets, f->fmt,
-                                use_rank ? scene->morton_rank.as<uint32_t>() : nullptr,
-                                f->keys[0].as<uint64_t>(), sat, grow<uint32_t>(f->big, N),
-                                &status->n_big, st, E);
-        if (ctx->debug) {
-            grow<uint64_t>(f->dbg_keys, E);
-            SVR_CUDA(cudaMemcpyAsync(f->dbg_keys.p, f->keys[0].p, E * 8, cudaMemcpyDeviceToDevice, st));
+        if (!ranked || ctx->debug) {
+            // voxel-order emission (reference order (vid, ty, tx, s)); with the
+            // ranked path it only feeds the parity dump of the unsorted keys
+            uint64_t* dk = ranked ? f->keys[1].as<uint64_t>() : f->keys[0].as<uint64_t>();
+            launch_duplicate_packed(cam, N, pa.paths, pa.rects, masks, pa.counts, offsets, f->fmt,
+                                    use_rank ? scene->morton_rank.as<uint32_t>() : nullptr, dk, sat,
+                                    grow<uint32_t>(f->big, N), &status->n_big, st, E);
+            if (ctx->debug) {
+                grow<uint64_t>(f->dbg_keys, E);
+                SVR_CUDA(cudaMemcpyAsync(f->dbg_keys.p, dk, E * 8, cudaMemcpyDeviceToDevice, st));
+            }
         }
+        if (ranked)
+            launch_duplicate_ranked(cam, N, pc, pair_partial, scene->morton_order.as<uint32_t>(), pa.rects,
+                                    masks, sat, rowspan, f->fmt, f->keys[0].as<uint64_t>(), E,
+                                    grow<uint2>(f->big_pairs, E / kRankedBigMin + 1),
+                                    &status->n_big_ranked, st);
         mark(ctx, kStageSort);
         const unsigned long long* n_dev = deferred ? &status->n_entries : nullptr;
         f->sorted_buf = radix_sort_keys(f->keys[0].as<uint64_t>(), f->keys[1].as<uint64_t>(), E,
@@ -973,10 +1011,12 @@ int svr_scene_upload(svr_ctx* ctx, const svr_scene_desc* d, svr_scene** out) {
             // Morton rank table for the sort keys (needs 8N < 2^32).
             if (N > 0 && N < (uint64_t(1) << 28)) {
                 s->morton_rank.reserve(N * 8 * 4);
+                s->morton_order.reserve(N * 8 * 4);
                 DevBuf tmp;
                 tmp.reserve(morton_rank_scratch_bytes(N, max_level));
                 build_morton_rank(s->paths.as<uint64_t>(), N, max_level,
-                                  s->morton_rank.as<uint32_t>(), tmp.p, ctx->stream);
+                                  s->morton_rank.as<uint32_t>(), s->morton_order.as<uint32_t>(), tmp.p,
+                                  ctx->stream);
                 SVR_CUDA(cudaStreamSynchronize(ctx->stream));
                 s->rank_bits = bit_width(8 * N - 1);
             }

@@ -31,11 +31,14 @@ constexpr int kSatSmemMax = 48 * 1024;  // u32 entries that fit the dynamic smem
 
 __global__ void __launch_bounds__(1024) tile_setup_kernel(DevCamera cam, uint8_t* masks,
                                                           uint32_t* sat, FrameStatus* status,
-                                                          int use_smem) {
+                                                          int use_smem, int2* rowspan) {
     pdl_enter();
     extern __shared__ uint32_t s_sat[];
     const int ntx = cam.ntx, nty = cam.nty, ntiles = ntx * nty;
     const int sw = ntx + 1, ncell = sw * (nty + 1);
+    // CTA 0: popcount table; CTA 1 + s (rank-ordered emission): table of bit s
+    const int b = blockIdx.x;
+    sat += size_t(b) * ncell;
     uint32_t* t = use_smem ? s_sat : sat;
     __shared__ unsigned int s_or;
     if (threadIdx.x == 0) s_or = 0;
@@ -46,7 +49,7 @@ __global__ void __launch_bounds__(1024) tile_setup_kernel(DevCamera cam, uint8_t
         const int tx = k % ntx, ty = k / ntx;
         const uint32_t m = masks[k];  // tile_masks_kernel, launched just before
         local_or |= m;
-        t[(ty + 1) * sw + tx + 1] = __popc(m);
+        t[(ty + 1) * sw + tx + 1] = b == 0 ? __popc(m) : ((m >> (b - 1)) & 1u);
     }
     atomicOr(&s_or, local_or);
     __syncthreads();
@@ -77,7 +80,22 @@ __global__ void __launch_bounds__(1024) tile_setup_kernel(DevCamera cam, uint8_t
     __syncthreads();
     if (use_smem)
         for (int i = threadIdx.x; i < ncell; i += blockDim.x) sat[i] = t[i];
-    if (threadIdx.x == 0 && status) status->pattern_or = s_or;
+    if (threadIdx.x == 0 && status && b == 0) status->pattern_or = s_or;
+    // per-pattern tables: the row span of pattern b-1 (the pattern regions are
+    // convex in the image, so a row's tiles with bit s are nearly always one
+    // run): {lo, hi}, {1, 0} when empty, {-1, -1} when not one run
+    if (b > 0 && rowspan)
+        for (int ty = threadIdx.x; ty < nty; ty += blockDim.x) {
+            int lo = ntx, hi = -1, cnt = 0;
+            for (int tx = 0; tx < ntx; ++tx)
+                if ((masks[ty * ntx + tx] >> (b - 1)) & 1u) {
+                    lo = min(lo, tx);
+                    hi = tx;
+                    ++cnt;
+                }
+            rowspan[(b - 1) * nty + ty] = cnt == 0 ? make_int2(1, 0)
+                                          : cnt == hi - lo + 1 ? make_int2(lo, hi) : make_int2(-1, -1);
+        }
 }
 
 __global__ void tile_masks_kernel(DevCamera cam, uint8_t* masks) {
@@ -410,6 +428,180 @@ __global__ void __launch_bounds__(256) duplicate_big_kernel(
                 }
                 o += __shfl_sync(0xffffffffu, incl, 31);
             }
+        }
+    }
+}
+
+// Rank-ordered K4. Every (sign pattern s, voxel v) pair has a scene-constant
+// Morton rank r = rank[s*n + v] (build_morton_rank), and the reference's
+// within-tile order is ascending r. K4a writes each pair's entry count at
+// its rank, pc[r] = #tiles of v's rectangle whose mask holds s (per-pattern
+// SATs); an exclusive scan of pc over r gives every pair the offset of its
+// entries in RANK order; K4b emits them there. The keys therefore come out
+// sorted by everything below the tile bits, and a stable sort on the tile
+// bits alone (2 radix passes at 1024^2 instead of 5) yields the reference's
+// (tile, key, value) order (raster.cpp:174-178) exactly.
+__device__ __forceinline__ uint64_t ranked_key(PackedFormat fmt, uint64_t tid, uint64_t r, uint32_t s,
+                                               uint64_t v) {
+    return (tid << fmt.tile_shift) | (r << (fmt.vb + 3)) | (uint64_t(s) << fmt.vb) | v;
+}
+
+__global__ void __launch_bounds__(256) pair_counts_kernel(
+    DevCamera cam, uint64_t n, const uint32_t* __restrict__ counts, const int4* __restrict__ rects,
+    const uint32_t* __restrict__ sat, const FrameStatus* __restrict__ status,
+    const uint32_t* __restrict__ rank, uint32_t* __restrict__ pc) {
+    pdl_enter();
+    const uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (v >= n || counts[v] == 0) return;
+    const int ncell = (cam.ntx + 1) * (cam.nty + 1);
+    const int4 r = rects[v];
+    uint32_t pat = status->pattern_or;
+    while (pat) {
+        const uint32_t s = __ffs(pat) - 1;
+        pat &= pat - 1;
+        const uint32_t c = sat_rect(sat + size_t(1 + s) * ncell, cam.ntx, r.x, r.y, r.z, r.w);
+        if (c) pc[__ldg(rank + s * n + v)] = c;
+    }
+}
+
+__global__ void __launch_bounds__(kScanThreads) duplicate_ranked_kernel(
+    DevCamera cam, uint64_t m, const uint32_t* __restrict__ pc, const uint32_t* __restrict__ partial,
+    const uint32_t* __restrict__ order, const int4* __restrict__ rects, const uint8_t* __restrict__ masks,
+    const int2* __restrict__ rowspan, PackedFormat fmt, uint64_t* __restrict__ keys, uint64_t cap, uint2* big,
+    unsigned int* n_big) {
+    pdl_enter();
+    __shared__ uint32_t s_warp[kScanThreads / 32 + 1];
+    const uint64_t i0 = uint64_t(blockIdx.x) * kScanChunk + uint64_t(threadIdx.x) * 8;
+    uint32_t x[8];
+    if (i0 + 8 <= m) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4*>(pc + i0));
+        const uint4 b = __ldg(reinterpret_cast<const uint4*>(pc + i0) + 1);
+        x[0] = a.x, x[1] = a.y, x[2] = a.z, x[3] = a.w, x[4] = b.x, x[5] = b.y, x[6] = b.z, x[7] = b.w;
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = i0 + k < m ? pc[i0 + k] : 0u;
+    }
+    uint32_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sum += x[k];
+    // block exclusive scan of the per-thread sums (scan.cu's apply phase)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = lane < kScanThreads / 32 ? s_warp[lane] : 0u;
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        if (lane < kScanThreads / 32) s_warp[lane] = wi - w;
+    }
+    __syncthreads();
+    if (sum == 0) return;
+    uint64_t o = uint64_t(partial[blockIdx.x]) + s_warp[warp] + incl - sum;
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t cnt = x[k];
+        if (cnt == 0) continue;
+        if (o + cnt <= cap) {  // else: deferred-E frame that outgrew its buffers (flagged)
+            const uint64_t r = i0 + k;
+            if (cnt > kRankedBigMin) {
+                big[atomicAdd(n_big, 1u)] = make_uint2(uint32_t(r), uint32_t(o));
+            } else {
+                const uint32_t ov = __ldg(order + r);
+                const uint32_t s = ov >> 29;
+                const uint64_t v = ov & ((1u << 29) - 1u);
+                const int4 rc = __ldg(rects + v);
+                uint64_t at = o;
+                for (int ty = rc.z; ty <= rc.w; ++ty) {
+                    const int2 sp = __ldg(rowspan + s * cam.nty + ty);
+                    if (sp.x >= 0) {  // one run: no mask reads
+                        const int a = max(sp.x, rc.x), e = min(sp.y, rc.y);
+                        for (int tx = a; tx <= e; ++tx)
+                            keys[at++] = ranked_key(fmt, uint64_t(ty) * cam.ntx + tx, r, s, v);
+                    } else {
+                        for (int tx = rc.x; tx <= rc.y; ++tx) {
+                            const uint64_t tid = uint64_t(ty) * cam.ntx + tx;
+                            if ((__ldg(masks + tid) >> s) & 1u) keys[at++] = ranked_key(fmt, tid, r, s, v);
+                        }
+                    }
+                }
+            }
+        }
+        o += cnt;
+    }
+}
+
+// One warp per large pair (grid-stride over the list). Per group of 32 rows,
+// lane i takes row ty0 + i: its entry count (the row span clipped to the
+// rectangle, or the pattern-s SAT row count for a row that is not one run),
+// a warp scan turns the counts into row offsets, then the rows are written
+// one after another with the lanes across the columns (coalesced stores).
+__global__ void __launch_bounds__(256) duplicate_big_ranked_kernel(
+    DevCamera cam, const uint32_t* __restrict__ order, const int4* __restrict__ rects,
+    const uint8_t* __restrict__ masks, const uint32_t* __restrict__ sat, const int2* __restrict__ rowspan,
+    PackedFormat fmt, uint64_t* __restrict__ keys, const uint2* __restrict__ big,
+    const unsigned int* __restrict__ n_big) {
+    pdl_enter();
+    const int lane = threadIdx.x & 31;
+    const uint32_t nb = *n_big;
+    const int ncell = (cam.ntx + 1) * (cam.nty + 1);
+    const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < nb; b += nwarps) {
+        const uint2 e = big[b];
+        const uint32_t ov = __ldg(order + e.x);
+        const uint32_t s = ov >> 29;
+        const uint64_t v = ov & ((1u << 29) - 1u);
+        const uint32_t* sat_s = sat + size_t(1 + s) * ncell;
+        const int4 rc = __ldg(rects + v);
+        uint64_t at = e.y;
+        for (int ty0 = rc.z; ty0 <= rc.w; ty0 += 32) {
+            const int ty = ty0 + lane;
+            int a = 0, len = 0;
+            if (ty <= rc.w) {
+                const int2 sp = __ldg(rowspan + s * cam.nty + ty);
+                if (sp.x >= 0) {
+                    a = max(sp.x, rc.x);
+                    len = max(0, min(sp.y, rc.y) - a + 1);
+                } else {
+                    a = -1;  // not one run: ballot over the masks below
+                    len = int(sat_rect(sat_s, cam.ntx, rc.x, rc.y, ty, ty));
+                }
+            }
+            int incl = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int nrows = min(32, rc.w - ty0 + 1);
+            for (int j = 0; j < nrows; ++j) {
+                const int l = __shfl_sync(0xffffffffu, len, j);
+                if (l == 0) continue;
+                const int aj = __shfl_sync(0xffffffffu, a, j);
+                const uint64_t ro = at + uint64_t(__shfl_sync(0xffffffffu, incl, j) - l);
+                const uint64_t trow = uint64_t(ty0 + j) * cam.ntx;
+                if (aj >= 0) {
+                    for (int c = lane; c < l; c += 32) keys[ro + c] = ranked_key(fmt, trow + aj + c, e.x, s, v);
+                } else {
+                    uint64_t w = ro;
+                    for (int tx0 = rc.x; tx0 <= rc.y; tx0 += 32) {
+                        const int tx = tx0 + lane;
+                        const bool hit = tx <= rc.y && ((__ldg(masks + trow + tx) >> s) & 1u);
+                        const unsigned bal = __ballot_sync(0xffffffffu, hit);
+                        if (hit) keys[w + __popc(bal & ((1u << lane) - 1u))] = ranked_key(fmt, trow + tx, e.x, s, v);
+                        w += __popc(bal);
+                    }
+                }
+            }
+            at += uint64_t(__shfl_sync(0xffffffffu, incl, 31));
         }
     }
 }
@@ -912,7 +1104,7 @@ void launch_status_to_host(const FrameStatus* d, FrameStatus* h, cudaStream_t st
 }
 
 void launch_tile_setup(const DevCamera& cam, uint8_t* masks, uint32_t* sat, FrameStatus* status,
-                       cudaStream_t st) {
+                       cudaStream_t st, int2* rowspan) {
     const int ncell = (cam.ntx + 1) * (cam.nty + 1);
     const int use_smem = ncell <= kSatSmemMax;
     const size_t smem = use_smem ? size_t(ncell) * 4 : 0;
@@ -926,7 +1118,7 @@ void launch_tile_setup(const DevCamera& cam, uint8_t* masks, uint32_t* sat, Fram
     const int ntiles = cam.ntx * cam.nty;
     launch_pdl(tile_masks_kernel, blocks_for(ntiles, 128), 128, 0, st, cam, masks);
     SVR_LAUNCH("tile_masks_kernel");
-    launch_pdl(tile_setup_kernel, 1, 1024, smem, st, cam, masks, sat, status, use_smem);
+    launch_pdl(tile_setup_kernel, rowspan ? 9 : 1, 1024, smem, st, cam, masks, sat, status, use_smem, rowspan);
     SVR_LAUNCH("tile_setup_kernel");
 }
 
@@ -988,14 +1180,39 @@ void launch_duplicate_packed(const DevCamera& cam, uint64_t n, const uint64_t* p
     SVR_LAUNCH("duplicate_big_kernel");
 }
 
+void launch_pair_counts(const DevCamera& cam, uint64_t n, const uint32_t* counts, const int4* rects,
+                        const uint32_t* sat, const FrameStatus* status, const uint32_t* rank,
+                        uint32_t* pc, cudaStream_t st) {
+    if (n == 0) return;
+    SVR_CUDA(cudaMemsetAsync(pc, 0, 8 * n * sizeof(uint32_t), st));
+    launch_pdl(pair_counts_kernel, blocks_for(n, 256), 256, 0, st, cam, n, counts, rects, sat, status, rank,
+               pc);
+    SVR_LAUNCH("pair_counts_kernel");
+}
+
+void launch_duplicate_ranked(const DevCamera& cam, uint64_t n, const uint32_t* pc,
+                             const uint32_t* partial, const uint32_t* order, const int4* rects,
+                             const uint8_t* masks, const uint32_t* sat, const int2* rowspan,
+                             PackedFormat fmt, uint64_t* keys, uint64_t cap, uint2* big,
+                             unsigned int* n_big, cudaStream_t st) {
+    if (n == 0) return;
+    const uint64_t m = 8 * n;
+    launch_pdl(duplicate_ranked_kernel, unsigned((m + kScanChunk - 1) / kScanChunk), kScanThreads, 0, st, cam,
+               m, pc, partial, order, rects, masks, rowspan, fmt, keys, cap, big, n_big);
+    SVR_LAUNCH("duplicate_ranked_kernel");
+    launch_pdl(duplicate_big_ranked_kernel, 148 * 8, 256, 0, st, cam, order, rects, masks, sat, rowspan, fmt,
+               keys, big, n_big);
+    SVR_LAUNCH("duplicate_big_ranked_kernel");
+}
+
 size_t morton_rank_scratch_bytes(uint64_t n, int lmax) {
     const uint64_t m = 8 * n;
     const int npass = (3 * lmax + 7) / 8;
     return 2 * m * 8 + 2 * m * 4 + 256 + sort_scratch_bytes(m, npass);
 }
 
-void build_morton_rank(const uint64_t* paths, uint64_t n, int lmax, uint32_t* rank, void* scratch,
-                       cudaStream_t st) {
+void build_morton_rank(const uint64_t* paths, uint64_t n, int lmax, uint32_t* rank, uint32_t* order,
+                       void* scratch, cudaStream_t st) {
     if (n == 0) return;
     const uint64_t m = 8 * n;
     char* p = static_cast<char*>(scratch);
@@ -1017,6 +1234,7 @@ void build_morton_rank(const uint64_t* paths, uint64_t n, int lmax, uint32_t* ra
     if (np > 0) out = radix_sort_pairs(k0, v0, k1, v1, m, passes, np, sort_scratch, st);
     rank_scatter_kernel<<<blocks_for(m, 256), 256, 0, st>>>(out ? v1 : v0, n, rank);
     SVR_LAUNCH("rank_scatter_kernel");
+    if (order) SVR_CUDA(cudaMemcpyAsync(order, out ? v1 : v0, m * 4, cudaMemcpyDeviceToDevice, st));
 }
 
 void launch_tile_ranges_packed(const uint64_t* keys, uint64_t n, PackedFormat fmt, uint2* ranges,

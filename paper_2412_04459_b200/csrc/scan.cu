@@ -17,6 +17,7 @@ namespace {
 constexpr int kThreads = 512;
 constexpr int kItems = 8;
 constexpr int kChunk = kThreads * kItems;  // 4096 elements per block
+static_assert(kChunk == kScanChunk && kThreads == kScanThreads, "svr_kernels.h scan geometry");
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
     const int lane = threadIdx.x & 31;
@@ -105,16 +106,39 @@ __global__ void __launch_bounds__(kThreads) scan_apply_kernel(const uint32_t* in
     uint32_t t;
     uint32_t run = block_excl_scan(s, s_warp, t) + partial[blockIdx.x];
     uint64_t i0 = base + uint64_t(threadIdx.x) * kItems;
+    uint32_t y[kItems];
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
-        if (i0 + k < n) out[i0 + k] = run;
+        y[k] = run;
         run += x[k];
+    }
+    if (i0 + kItems <= n && ((reinterpret_cast<uintptr_t>(out + i0) & 15) == 0)) {
+        reinterpret_cast<uint4*>(out + i0)[0] = make_uint4(y[0], y[1], y[2], y[3]);
+        reinterpret_cast<uint4*>(out + i0)[1] = make_uint4(y[4], y[5], y[6], y[7]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < kItems; ++k)
+            if (i0 + k < n) out[i0 + k] = y[k];
     }
 }
 
 }  // namespace
 
 size_t scan_scratch_bytes(uint64_t n) { return ((n + kChunk - 1) / kChunk + 1) * sizeof(uint32_t); }
+
+void scan_block_prefixes(const uint32_t* in, uint64_t n, unsigned long long* total, void* scratch,
+                         cudaStream_t st) {
+    if (n == 0) {
+        SVR_CUDA(cudaMemsetAsync(total, 0, sizeof(unsigned long long), st));
+        return;
+    }
+    uint64_t nb = (n + kChunk - 1) / kChunk;
+    uint32_t* partial = static_cast<uint32_t*>(scratch);
+    launch_pdl(scan_reduce_kernel, unsigned(nb), kThreads, 0, st, in, n, partial);
+    SVR_LAUNCH("scan_reduce_kernel");
+    launch_pdl(scan_partials_kernel, 1, kThreads, 0, st, partial, nb, total);
+    SVR_LAUNCH("scan_partials_kernel");
+}
 
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, unsigned long long* total,
                         void* scratch, cudaStream_t st) {

@@ -13,6 +13,13 @@ namespace svrb {
 // Exclusive prefix sum of n u32 values; writes the u64 grand total to
 // *total (device). `scratch` must hold scan_scratch_bytes(n).
 size_t scan_scratch_bytes(uint64_t n);
+// The first two phases only: u32 scratch[b] = exclusive prefix of block b's
+// kScanChunk inputs (for kernels that fuse the apply phase, kScanThreads
+// threads x 8 consecutive items per block).
+constexpr int kScanThreads = 512;
+constexpr int kScanChunk = 4096;
+void scan_block_prefixes(const uint32_t* in, uint64_t n, unsigned long long* total, void* scratch,
+                         cudaStream_t st);
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, unsigned long long* total,
                         void* scratch, cudaStream_t st);
 
@@ -52,11 +59,15 @@ struct FrameStatus {          // device -> host summary, one read per frame
     unsigned int overflow;    // a pixel exceeded the staged-record capacity
     unsigned long long n_contribs;
     unsigned int n_big;       // voxels handed to the cooperative duplicate
-    unsigned int pad;
+    unsigned int n_big_ranked;  // the same for the rank-ordered duplicate
+    unsigned long long n_entries_voxel;  // E from the per-voxel scan (parity dumps of the ranked path)
 };
 
+// With rowspan (int2 [8][nty]): also the eight per-sign-pattern SATs at
+// sat + (1 + s) * ncell (ncell = (ntx + 1) * (nty + 1)) and each pattern's
+// per-row tile run, for the rank-ordered duplicate.
 void launch_tile_setup(const DevCamera& cam, uint8_t* masks, uint32_t* sat, FrameStatus* status,
-                       cudaStream_t st);
+                       cudaStream_t st, int2* rowspan = nullptr);
 // Copies the device FrameStatus into host-mapped pinned memory with a kernel.
 // With overflow_count: counts frames whose entry total exceeded `cap`.
 void launch_status_to_host(const FrameStatus* d, FrameStatus* h, cudaStream_t st,
@@ -107,8 +118,28 @@ void launch_duplicate_packed(const DevCamera& cam, uint64_t n, const uint64_t* p
 // such pairs, i.e. the reference's within-tile (key, value) order
 // (raster.cpp:163-177) as one dense integer. Camera independent.
 size_t morton_rank_scratch_bytes(uint64_t n, int lmax);
-void build_morton_rank(const uint64_t* paths, uint64_t n, int lmax, uint32_t* rank, void* scratch,
-                       cudaStream_t st);
+void build_morton_rank(const uint64_t* paths, uint64_t n, int lmax, uint32_t* rank, uint32_t* order,
+                       void* scratch, cudaStream_t st);
+// Rank-ordered K4 (needs the per-pattern SATs of launch_tile_setup
+// per_pattern, the rank table and the scene's pair list order[r] =
+// s << 29 | vid). K4a: pc[rank[s*n + v]] = entries of pair (s, v), 8n u32,
+// zeroed here. scan_block_prefixes(pc) -> block prefixes in `partial`. K4b:
+// the apply phase of that scan, fused with emission: pair r's entries land
+// at its rank-order offset with key tile | r | s | vid, so the keys come out
+// sorted below the tile bits. big: E / 128 + 1 uint2 (pairs with more than
+// 128 entries, emitted cooperatively).
+void launch_pair_counts(const DevCamera& cam, uint64_t n, const uint32_t* counts, const int4* rects,
+                        const uint32_t* sat, const FrameStatus* status, const uint32_t* rank,
+                        uint32_t* pc, cudaStream_t st);
+#ifndef SVR_RBIG
+#define SVR_RBIG 128
+#endif
+constexpr uint32_t kRankedBigMin = SVR_RBIG;  // pairs with more entries: one warp each
+void launch_duplicate_ranked(const DevCamera& cam, uint64_t n, const uint32_t* pc,
+                             const uint32_t* partial, const uint32_t* order, const int4* rects,
+                             const uint8_t* masks, const uint32_t* sat, const int2* rowspan,
+                             PackedFormat fmt, uint64_t* keys, uint64_t cap, uint2* big,
+                             unsigned int* n_big, cudaStream_t st);
 // Tile ranges from packed sorted keys; also writes the reference value
 // (s << 29 | vid) per entry for the compositing kernels.
 void launch_tile_ranges_packed(const uint64_t* keys, uint64_t n, PackedFormat fmt, uint2* ranges,
