@@ -188,10 +188,10 @@ def stage_bytes(stage, d):
         return d["n_vox"] * (8 + 16 + 4) + 4 * d["n_pool"] + d["n_vis"] * (32 + 4 * d["stride"] + 96)
     if stage == "sort":
         return d["npass"] * d["E"] * 16
-    if stage == "duplicate":
-        return d["n_vis"] * (8 + 16 + 8) + d["E"] * 8
-    if stage == "scan":
-        return d["n_vox"] * 12
+    if stage == "duplicate":  # rank-ordered: pair counts (8n u32) + order/rect per live pair + keys
+        return d["n_vox"] * 8 * 4 + d["n_vis"] * (4 + 16) + d["E"] * 8
+    if stage == "scan":  # zero + scatter the pair counts, reduce them
+        return d["n_vox"] * (8 * 4 + 4 + 8 * 4) + d["n_vis"] * (16 + 8)
     if stage == "backward":
         return (d["E"] * 4 + d["n_vis"] * (96 + 32 + 28) + d["contribs"] * 8 + d["R"] * 20
                 + 4 * d["n_pool"])

@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
     const uint32_t my_sign = sign_bits(dd);
     const uint32_t warp_signs = __reduce_or_sync(0xffffffffu, inside ? (1u << my_sign) : 0u);
     const float dx = float(dd[0]), dy = float(dd[1]), dz = float(dd[2]);
-    const float ix = 1.0f / dx, iy = 1.0f / dy, iz = 1.0f / dz;
+    const float ix = slab_inv(dd[0]), iy = slab_inv(dd[1]), iz = slab_inv(dd[2]);
     const float dnorm = float(sqrt(dd[0] * dd[0] + dd[1] * dd[1] + dd[2] * dd[2]));
     float (*cone)[3] = s_cone[warp];
     if (lane == 0) warp_cone_planes(cam, wx0, wy0, cone);
@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(256) ray_losses_kernel(DevCamera cam, RayLossA
             double dd[3];
             pixel_ray_dir(cam, double(px), double(py), dd);
             const float dx = float(dd[0]), dy = float(dd[1]), dz = float(dd[2]);
-            const float ix = 1.0f / dx, iy = 1.0f / dy, iz = 1.0f / dz;
+            const float ix = slab_inv(dd[0]), iy = slab_inv(dd[1]), iz = slab_inv(dd[2]);
             const float dnorm = float(sqrt(dd[0] * dd[0] + dd[1] * dd[1] + dd[2] * dd[2]));
             float g[3] = {0.f, 0.f, 0.f};
             if (a.w_R != 0.0) {

@@ -113,15 +113,13 @@ __device__ __forceinline__ uint32_t sat_rect(const uint32_t* sat, int ntx, int t
 }
 
 // ------------------------------------------------------------------- K1
-// 128 threads = 4 warps, one voxel per thread. The SH coefficients of a
-// warp's 32 voxels (32 x 192 B, contiguous) are fetched with coalesced
-// 16-B loads into a bank-conflict-free padded tile (odd row pitch), and the
-// 112-B records of the whole CTA are staged in shared memory and written
-// back as one contiguous, coalesced block.
+// 128 threads = 4 warps, one voxel per thread. A conservative fp32 test first
+// drops the voxels the exact fp64 projection would certainly cull. For scenes
+// whose voxel order is not spatially coherent, threads take voxels in the
+// scene's Morton order (a.order), so that the culled voxels of a warp are
+// culled together. In scene order, the 96-B records of the CTA's visible
+// voxels are staged in shared memory and written back as contiguous runs.
 constexpr int kPreThreads = 128;
-#ifndef SVR_PRE_SMEM_SH
-#define SVR_PRE_SMEM_SH 0
-#endif
 #ifndef SVR_PRE_MINB
 #define SVR_PRE_MINB 6
 #endif
@@ -129,45 +127,11 @@ constexpr int kPreThreads = 128;
 __global__ void __launch_bounds__(kPreThreads, SVR_PRE_MINB) preprocess_kernel(DevCamera cam, PreprocessArgs a) {
     pdl_enter();
     extern __shared__ float4 smem4[];
-#if SVR_PRE_SMEM_SH
-    float* smem = reinterpret_cast<float*>(smem4);
-    const int pad = a.sh_stride | 1;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    float* s_sh = smem + warp * 32 * pad;
-    float4* s_rec = smem4 + ((kPreThreads * pad + 3) / 4);
-#else
     float4* s_rec = smem4;
-#endif
     const uint64_t v0 = uint64_t(blockIdx.x) * kPreThreads;
-    const uint64_t v = v0 + threadIdx.x;
-    const bool valid = v < a.n;
-
-#if SVR_PRE_SMEM_SH
-    // 1. coalesced SH staging for this warp's voxels
-    const uint64_t wv0 = v0 + uint64_t(warp) * 32;
-    const int nvw = wv0 < a.n ? int(min(uint64_t(32), a.n - wv0)) : 0;
-    const int total = nvw * a.sh_stride;
-    const float* src = a.sh + wv0 * uint64_t(a.sh_stride);
-    if ((a.sh_stride & 3) == 0) {
-        const float4* src4 = reinterpret_cast<const float4*>(src);
-        for (int e4 = lane; e4 < total / 4; e4 += 32) {
-            float4 f = __ldg(src4 + e4);
-            int e = 4 * e4;
-            int r = e / a.sh_stride, c = e - r * a.sh_stride;
-            float* d = s_sh + r * pad + c;  // stride % 4 == 0: the 4 floats share a row
-            d[0] = f.x;
-            d[1] = f.y;
-            d[2] = f.z;
-            d[3] = f.w;
-        }
-    } else {
-        for (int e = lane; e < total; e += 32) {
-            int r = e / a.sh_stride;
-            s_sh[r * pad + (e - r * a.sh_stride)] = __ldg(src + e);
-        }
-    }
-    __syncwarp();
-#endif
+    const bool valid = v0 + threadIdx.x < a.n;
+    const uint64_t v = a.order ? (valid ? uint64_t(__ldg(a.order + v0 + threadIdx.x)) : a.n)
+                               : v0 + threadIdx.x;
 
     float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0, r3 = r0, r4 = r0, r5 = r0;  // r0.w = 0: not visible
     if (valid) {
@@ -175,7 +139,15 @@ __global__ void __launch_bounds__(kPreThreads, SVR_PRE_MINB) preprocess_kernel(D
         double center[3], size;
         voxel_geometry(path & kCodeMask48, int(path >> 48), a.bc, a.bsize, center, &size);
         Projection pr;
-        const bool vis = project_voxel(cam, center, size, a.near_plane, pr);
+        bool vis = false;
+        if (surely_culled(cam, center, size, a.near_plane)) {
+            pr.tx0 = pr.ty0 = 0;  // a fresh PreVoxel, as project_voxel leaves a culled one
+            pr.tx1 = pr.ty1 = -1;
+            pr.x0 = pr.x1 = pr.y0 = pr.y1 = 0.0;
+            pr.straddles = false;
+        } else {
+            vis = project_voxel(cam, center, size, a.near_plane, pr);
+        }
         a.rects[v] = make_int4(pr.tx0, pr.tx1, pr.ty0, pr.ty1);
         if (a.aabb) a.aabb[v] = make_double4(pr.x0, pr.x1, pr.y0, pr.y1);
         a.counts[v] = vis ? sat_rect(a.tile_sat, cam.ntx, pr.tx0, pr.tx1, pr.ty0, pr.ty1) : 0u;
@@ -216,17 +188,6 @@ __global__ void __launch_bounds__(kPreThreads, SVR_PRE_MINB) preprocess_kernel(D
             float b[16];
             const int nb = sh_basis(a.sh_degree, ux, uy, uz, b);
             float cr = 0.f, cg = 0.f, cb = 0.f;
-#if SVR_PRE_SMEM_SH
-            const float* co = s_sh + lane * pad;
-#pragma unroll
-            for (int m = 0; m < 16; ++m) {
-                if (m < nb) {
-                    cr += b[m] * co[3 * m + 0];
-                    cg += b[m] * co[3 * m + 1];
-                    cb += b[m] * co[3 * m + 2];
-                }
-            }
-#else
             const float* co = a.sh + v * uint64_t(a.sh_stride);
             if (a.sh_stride == 48) {
                 // degree 3: 12 aligned 16-B loads of this voxel's 192 B
@@ -251,12 +212,23 @@ __global__ void __launch_bounds__(kPreThreads, SVR_PRE_MINB) preprocess_kernel(D
                     cb += b[m] * __ldg(co + 3 * m + 2);
                 }
             }
-#endif
             r4 = make_float4(fmaxf(0.f, cr), fmaxf(0.f, cg), fmaxf(0.f, cb), __uint_as_float(uint32_t(v)));
             float n[3];
             voxel_normal(V, n);
             r5 = make_float4(n[0], n[1], n[2], float(1.0 / size));
         }
+    }
+    if (a.order) {  // Morton processing order: each thread stores its own record
+        if (valid && r0.w > 0.f) {
+            float4* dst = a.records + v * kRecordF4;
+            dst[0] = r0;
+            dst[1] = r1;
+            dst[2] = r2;
+            dst[3] = r3;
+            dst[4] = r4;
+            dst[5] = r5;
+        }
+        return;
     }
     // Records of visible voxels only (nothing reads the others): staged in
     // shared memory and written back as contiguous runs.
@@ -581,6 +553,25 @@ __global__ void __launch_bounds__(256) duplicate_big_ranked_kernel(
                 const int y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
             }
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            if (!__any_sync(0xffffffffu, a < 0 && len > 0)) {
+                // every row one run: the group's entries as one flat range,
+                // lane q of each 32 finds its row by binary search over the
+                // row prefix sums
+                for (int e0 = 0; e0 < total; e0 += 32) {
+                    const int q = e0 + lane;
+                    int j = 0;
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1)
+                        if (__shfl_sync(0xffffffffu, incl, j + step - 1) <= q) j += step;
+                    const int lj = __shfl_sync(0xffffffffu, len, j), aj = __shfl_sync(0xffffffffu, a, j);
+                    const int ij = __shfl_sync(0xffffffffu, incl, j);
+                    if (q < total)
+                        keys[at + q] = ranked_key(fmt, uint64_t(ty0 + j) * cam.ntx + aj + (q - (ij - lj)), e.x, s, v);
+                }
+                at += uint64_t(total);
+                continue;
+            }
             const int nrows = min(32, rc.w - ty0 + 1);
             for (int j = 0; j < nrows; ++j) {
                 const int l = __shfl_sync(0xffffffffu, len, j);
@@ -601,7 +592,7 @@ __global__ void __launch_bounds__(256) duplicate_big_ranked_kernel(
                     }
                 }
             }
-            at += uint64_t(__shfl_sync(0xffffffffu, incl, 31));
+            at += uint64_t(total);
         }
     }
 }
@@ -613,6 +604,14 @@ __global__ void rank_keys_kernel(const uint64_t* __restrict__ paths, uint64_t n,
     const uint64_t s = i / n, v = i - s * n;
     keys[i] = (paths[v] & kCodeMask48) ^ (s * kGroupOnes);
     vals[i] = uint32_t(s << 29) | uint32_t(v);
+}
+
+__global__ void code_keys_kernel(const uint64_t* __restrict__ paths, uint64_t n, uint64_t* keys,
+                                 uint32_t* vals) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    keys[i] = paths[i] & kCodeMask48;
+    vals[i] = uint32_t(i);
 }
 
 __global__ void rank_scatter_kernel(const uint32_t* __restrict__ vals, uint64_t n, uint32_t* rank) {
@@ -776,7 +775,7 @@ __global__ void __launch_bounds__(256, 4) composite_kernel(DevCamera cam, Compos
     const uint32_t warp_signs = __reduce_or_sync(0xffffffffu, inside ? (1u << my_sign) : 0u);
     const bool one_sign = __popc(warp_signs) <= 1;
     const float dx = float(dd[0]), dy = float(dd[1]), dz = float(dd[2]);
-    const float ix = 1.0f / dx, iy = 1.0f / dy, iz = 1.0f / dz;
+    const float ix = slab_inv(dd[0]), iy = slab_inv(dd[1]), iz = slab_inv(dd[2]);
     const float dnorm = float(sqrt(dd[0] * dd[0] + dd[1] * dd[1] + dd[2] * dd[2]));
     const float pcx = float(px) + 0.5f, pcy = float(py) + 0.5f;
     // Frustum of this warp's 8x4 block (warp_cone_planes): skips boxes whose
@@ -1043,7 +1042,7 @@ __global__ void __launch_bounds__(256) contrib_segments_kernel(
     const uint32_t slot = uint32_t(tile) * 256u + threadIdx.x;
     double dd[3];
     pixel_ray_dir(cam, double(px), double(py), dd);
-    const float ix = 1.0f / float(dd[0]), iy = 1.0f / float(dd[1]), iz = 1.0f / float(dd[2]);
+    const float ix = slab_inv(dd[0]), iy = slab_inv(dd[1]), iz = slab_inv(dd[2]);
     const uint32_t n = pix_count[slot], base = pix_begin[slot];
     for (uint32_t c = 0; c < n; ++c) {
         uint32_t e = contrib_entry[base + c];
@@ -1130,12 +1129,7 @@ void launch_tile_masks_only(const DevCamera& cam, uint8_t* masks, cudaStream_t s
 
 void launch_preprocess(const DevCamera& cam, const PreprocessArgs& a, cudaStream_t st) {
     if (a.n == 0) return;
-#if SVR_PRE_SMEM_SH
-    const int pad = a.sh_stride | 1;
-    const size_t smem = size_t((kPreThreads * pad + 3) / 4) * 16 + size_t(kPreThreads) * kRecordF4 * 16;
-#else
-    const size_t smem = size_t(kPreThreads) * kRecordF4 * 16;
-#endif
+    const size_t smem = a.order ? 0 : size_t(kPreThreads) * kRecordF4 * 16;
     launch_pdl(preprocess_kernel, blocks_for(a.n, kPreThreads), kPreThreads, smem, st, cam, a);
     SVR_LAUNCH("preprocess_kernel");
 }
@@ -1235,6 +1229,26 @@ void build_morton_rank(const uint64_t* paths, uint64_t n, int lmax, uint32_t* ra
     rank_scatter_kernel<<<blocks_for(m, 256), 256, 0, st>>>(out ? v1 : v0, n, rank);
     SVR_LAUNCH("rank_scatter_kernel");
     if (order) SVR_CUDA(cudaMemcpyAsync(order, out ? v1 : v0, m * 4, cudaMemcpyDeviceToDevice, st));
+}
+
+void build_proc_order(const uint64_t* paths, uint64_t n, int lmax, uint32_t* order, void* scratch,
+                      cudaStream_t st) {
+    if (n == 0) return;
+    char* p = static_cast<char*>(scratch);
+    uint64_t* k0 = reinterpret_cast<uint64_t*>(p);
+    uint64_t* k1 = k0 + n;
+    uint32_t* v0 = reinterpret_cast<uint32_t*>(k1 + n);
+    uint32_t* v1 = v0 + n;
+    void* sort_scratch = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(v1 + n) + 255) &
+                                                 ~uintptr_t(255));
+    code_keys_kernel<<<blocks_for(n, 256), 256, 0, st>>>(paths, n, k0, v0);
+    SVR_LAUNCH("code_keys_kernel");
+    RadixPass passes[kMaxRadixPasses];
+    int np = 0;
+    for (int b = 48 - 3 * lmax; b < 48; b += 8) passes[np++] = {0, b, std::min(8, 48 - b)};
+    int out = 0;
+    if (np > 0) out = radix_sort_pairs(k0, v0, k1, v1, n, passes, np, sort_scratch, st);
+    SVR_CUDA(cudaMemcpyAsync(order, out ? v1 : v0, n * 4, cudaMemcpyDeviceToDevice, st));
 }
 
 void launch_tile_ranges_packed(const uint64_t* keys, uint64_t n, PackedFormat fmt, uint2* ranges,

@@ -121,6 +121,7 @@ struct svr_scene {
     svrb::DevBuf sh;            // f32 [n][stride]
     svrb::DevBuf morton_rank;   // u32 [8][n]: build_morton_rank (sort keys)
     svrb::DevBuf morton_order;  // u32 [8n]: the (s, vid) pairs in rank order
+    svrb::DevBuf proc_order;    // u32 [n]: K1 processing order (empty: scene order is coherent)
     int rank_bits = 0;          // bit width of 8n-1; 0 = no table
     // AdaptRemap of a scene produced by svr_scene_prune / svr_scene_subdivide
     svrb::DevBuf voxel_src, pool_src;  // int64 per voxel / per pool entry

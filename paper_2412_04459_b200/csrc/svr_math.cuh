@@ -217,6 +217,50 @@ SVR_HD bool project_voxel(const DevCamera& cam, const double* center, double siz
     return true;
 }
 
+// Inverse ray-direction component for the fp32 slab tests. ray_aabb
+// (field.hpp:58-69) divides in double, where a zero component turns the axis
+// into "inside iff lo - o <= 0 < hi - o" (0/0 = NaN falls out of its
+// std::min/std::max argument order; either sign of zero). A float 1/0 = inf
+// would make lo * inf = NaN and fminf/fmaxf would drop the wrong operand, so
+// components that vanish in float get a finite stand-in of 1e30 with the
+// double's sign (+ for either zero), which reproduces those cases exactly.
+SVR_HD float slab_inv(double d) {
+    const float f = float(d);
+    if (fabsf(f) >= 1e-30f) return 1.0f / f;
+    return d < 0.0 ? -1e30f : 1e30f;
+}
+
+// Conservative fp32 pre-test for K1: true only when project_voxel would
+// certainly cull the voxel — its bounding sphere (half-diagonal plus a
+// rounding margin of 1e-5 of the coordinates' magnitude) lies wholly behind
+// the near plane, or wholly in front of it and wholly outside one image side
+// widened by a pixel (raster.cpp:104: x1 < 0 || y1 < 0 || x0 > W || y0 > H).
+// Anything else takes the exact fp64 path, so the outputs are unchanged.
+SVR_HD bool surely_culled(const DevCamera& cam, const double* center, double size, double near) {
+    const float c0 = float(center[0] - cam.pos[0]), c1 = float(center[1] - cam.pos[1]),
+                c2 = float(center[2] - cam.pos[2]);
+    const float px = float(cam.rot[0]) * c0 + float(cam.rot[3]) * c1 + float(cam.rot[6]) * c2;
+    const float py = float(cam.rot[1]) * c0 + float(cam.rot[4]) * c1 + float(cam.rot[7]) * c2;
+    const float pz = float(cam.rot[2]) * c0 + float(cam.rot[5]) * c1 + float(cam.rot[8]) * c2;
+    const float mag = fabsf(c0) + fabsf(c1) + fabsf(c2) + float(size);
+    const float r = float(size) * 0.8660255f + 1e-5f * mag;
+    const float nr = float(near);
+    if (pz + r < nr - 1e-5f * fabsf(nr)) return true;  // every corner behind the near plane
+    if (pz - r <= nr + 1e-5f * fabsf(nr)) return false;  // may straddle: whole-image AABB
+    // every corner in front: the sphere outside a side plane through the eye
+    // (a * q + b * z < 0 over the whole sphere)
+    auto outside = [&](float a, float b, float q) {
+        const float d = a * q + b * pz;
+        return d + r * sqrtf(a * a + b * b) + 1e-5f * (fabsf(a * q) + fabsf(b * pz)) < 0.f;
+    };
+    const float fx = float(cam.fx), fy = float(cam.fy), cx = float(cam.cx), cy = float(cam.cy);
+    const float W = float(cam.W), H = float(cam.H);
+    return outside(fx, cx + 1.f, px) ||              // every u < -1
+           outside(-fx, W + 1.f - cx, px) ||         // every u > W + 1
+           outside(fy, cy + 1.f, py) ||              // every v < -1
+           outside(-fy, H + 1.f - cy, py);           // every v > H + 1
+}
+
 // True iff no pixel ray of the image can enter the box at t > 0: all eight
 // corners lie strictly outside one side plane of the image frustum (planes
 // through the camera centre along the image border widened by one pixel;

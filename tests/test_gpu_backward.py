@@ -43,6 +43,24 @@ def test_backward_identical_upstream(svr, ctx, ref, scene1, K, ss):
     check_grads(g, (gd, gs, gp), f"K={K} ss={ss}")
 
 
+@pytest.mark.parametrize("K", [1, 2])
+def test_axis_aligned_rays_on_voxel_faces(svr, ctx, ref, scene1, K):
+    """Camera on voxel faces with rays whose direction has exact zero
+    components (row py = cy - 0.5, column px = cx - 0.5): ray_aabb's IEEE
+    semantics (field.hpp:58-69) for the 0/0 slabs, forward and backward."""
+    arrays, scene, rscene = scene1
+    cam = svr.Camera(96, 80, 70.0, 70.0, 48.5, 40.5, np.eye(3), np.array([0.0, 0.0, -0.25]))
+    opts = svr.RenderOptions(K=K, supersample=1.0, training=True)
+    out = svr.render(scene, cam, opts)
+    r = ref.ref_render(rscene, cam, opts)
+    assert max_abs(out.color, r["color"]) <= 1e-4
+    assert max_abs(out.transmittance, r["transmittance"]) <= 1e-4
+    gt = np.random.default_rng(23).uniform(0, 1, (cam.height, cam.width, 3))
+    loss_ref, dcol, gd, gs, gp = ref.ref_train_step_l1(rscene, cam, opts, gt, *sizes(arrays))
+    g = svr.render_backward(scene, out.frame, d_color=dcol)
+    check_grads(g, (gd, gs, gp), f"axis-aligned K={K}")
+
+
 def test_backward_depth_normal_tfin_channels(svr, ctx, ref, scene1):
     arrays, scene, rscene = scene1
     cam = svr.ring_camera(2, 1, 96, 96)

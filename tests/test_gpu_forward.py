@@ -54,6 +54,49 @@ def test_projection_bit_exact(svr, ctx, ref, cfg1):
         assert np.array_equal(ours_rect[:, 1] >= ours_rect[:, 0], vis)
 
 
+def test_projection_inside_scene_bit_exact(svr, ctx, ref, cfg1):
+    """Cameras inside the scene: voxels culled behind the near plane and past
+    every image side (K1's fp32 pre-cull must agree with the fp64 test)."""
+    arrays, scene, rscene = cfg1
+    rng = np.random.default_rng(11)
+    for trial in range(4):
+        q, _ = np.linalg.qr(rng.normal(size=(3, 3)))
+        rot = q * np.sign(np.linalg.det(q))
+        pos = rng.uniform(-0.2, 0.2, 3)
+        cam = svr.Camera(160 + 16 * trial, 96, 70.0 + 40 * trial, 70.0, 80.0, 47.5, rot, pos)
+        f = svr.Frame(ctx)
+        svr.render_into(f, scene, cam, svr.RenderOptions(supersample=1.0))
+        vis, aabb, rect = ref.ref_project(rscene, cam, arrays.n_voxels)
+        ours_rect = f.download("VOXEL_RECTS", np.int32, (-1, 4))
+        ours_aabb = f.download("VOXEL_AABB", np.float64, (-1, 4))
+        assert 0 < vis.sum() < arrays.n_voxels
+        assert np.array_equal(ours_rect, rect)
+        assert np.array_equal(ours_aabb[vis], aabb[vis])
+        assert np.all(ours_aabb[~vis] == 0.0)
+
+
+def test_shuffled_scene_order_bit_exact(svr, ctx, ref):
+    """A scene stored out of spatial order: K1 walks it in Morton order (the
+    scene's processing order); rects, sorted entries and the image still match."""
+    import dataclasses
+    base = svr.synth_random_scene(99, 20000, 8, 2)
+    perm = np.random.default_rng(5).permutation(base.n_voxels)
+    arrays = dataclasses.replace(base, codes=base.codes[perm], levels=base.levels[perm],
+                                 corner_index=base.corner_index[perm], sh=base.sh[perm])
+    scene, rscene = svr.Scene(ctx, arrays), ref.RefScene.from_arrays(arrays)
+    for cam in [svr.ring_camera(3, 2, 192, 160),
+                svr.Camera(128, 96, 60.0, 60.0, 64.0, 47.5, np.eye(3), np.array([0.03, 0.0, -0.02]))]:
+        f = svr.Frame(ctx)
+        opts = svr.RenderOptions(supersample=1.0)
+        svr.render_into(f, scene, cam, opts)
+        vis, aabb, rect = ref.ref_project(rscene, cam, arrays.n_voxels)
+        assert np.array_equal(f.download("VOXEL_RECTS", np.int32, (-1, 4)), rect)
+        ks_ref, vs_ref = ref.ref_entries(rscene, cam, sorted_=True)
+        assert np.array_equal(f.download("SORT_KEYS", np.uint64), ks_ref)
+        assert np.array_equal(f.download("SORT_VALUES", np.uint32), vs_ref)
+        compare_outputs(svr.render(scene, cam, opts), ref.ref_render(rscene, cam, opts))
+
+
 def test_project_voxels_api_matches_reference(svr, ctx, ref):
     rng = np.random.default_rng(404)
     for trial in range(20):  # test_raster.cpp:129-147 setup

@@ -12,10 +12,10 @@ timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/b
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches.csv python tools/profile_step.py > gpurun_out/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:"composite_kernel|preprocess_kernel|onesweep_kernel|duplicate_|hist_kernel|tile_setup|scan_|tile_ranges|tile_order" \
+    -k regex:"composite_kernel|preprocess_kernel|onesweep_kernel|duplicate_|pair_counts|hist_kernel|tile_setup|scan_|tile_ranges|tile_order" \
     -s ${NCU_SKIP:-30} -c ${NCU_COUNT:-16} -o gpurun_out/full python tools/profile_step.py > gpurun_out/ncu_full.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"epilogue|composite_backward|l1_kernel" \
     -s 9 -c 3 -o gpurun_out/bwd python tools/explore_cfg3.py > gpurun_out/ncu_bwd.log 2>&1
-VIEWS=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"composite_kernel|onesweep|preprocess|duplicate_packed" \
+VIEWS=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"composite_kernel|onesweep|preprocess|duplicate_" \
     -s 12 -c 8 -o gpurun_out/cfg4 python tools/explore_cfg4.py > gpurun_out/ncu_cfg4.log 2>&1
 ls -la gpurun_out

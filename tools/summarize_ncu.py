@@ -59,7 +59,7 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "dram__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__inst_executed.sum"]
 SCALE = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
 STAGE = {"composite_kernel": "composite", "preprocess_kernel": "preprocess", "onesweep_kernel": "sort",
-         "duplicate_packed_kernel": "duplicate", "composite_backward_kernel": "backward",
+         "duplicate_packed_kernel": "duplicate", "duplicate_ranked_kernel": "duplicate", "composite_backward_kernel": "backward",
          "voxel_epilogue_kernel": "epilogue"}
 
 
