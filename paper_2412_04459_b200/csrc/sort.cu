@@ -23,6 +23,9 @@ namespace svrb {
 
 namespace {
 
+#ifndef SVR_SORT_ATOMIC_RANK
+#define SVR_SORT_ATOMIC_RANK 1
+#endif
 constexpr int kRadix = 256;
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
@@ -141,6 +144,20 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
     }
     const uint32_t lt_mask = (1u << lane) - 1u;
     uint32_t* wh = s_warp_hist[warp];
+#if SVR_SORT_ATOMIC_RANK
+    // Warp-aggregated shared-memory atomics: the leader of each digit group
+    // reserves the group's slots; the items' reservations pipeline instead of
+    // serialising on a load/store/syncwarp round trip each.
+#pragma unroll
+    for (int i = 0; i < Part<PAIRS>::items; ++i) {
+        const uint32_t di = dig(i);
+        const uint32_t peers = __match_any_sync(0xffffffffu, di);
+        const int leader = __ffs(peers) - 1;
+        uint32_t prev = 0;
+        if (lane == leader) prev = atomicAdd(&wh[di], uint32_t(__popc(peers)));
+        r[i] = __shfl_sync(0xffffffffu, prev, leader) + __popc(peers & lt_mask);
+    }
+#else
 #pragma unroll
     for (int i = 0; i < Part<PAIRS>::items; ++i) {
         const uint32_t di = dig(i);
@@ -152,6 +169,7 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
         if (below == 0) wh[di] = prev + __popc(peers);
         __syncwarp();
     }
+#endif
     __syncthreads();
 
     // Per digit: exclusive offsets across warps, block total, block-wide
