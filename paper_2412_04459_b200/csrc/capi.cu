@@ -434,6 +434,7 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     uint2* ranges = grow<uint2>(f->ranges, ntiles);
     RadixPass passes[kMaxRadixPasses];
     int np = 0;
+    f->sort_keys_kept = true;
     if (f->packed) {
         f->fmt = use_rank ? PackedFormat{vb, lmax, vb + 3 + rb, rb}
                           : PackedFormat{vb, lmax, vb + 3 + 3 * lmax, 0};
@@ -470,11 +471,22 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
                                     &status->n_big_ranked, st);
         mark(ctx, kStageSort);
         const unsigned long long* n_dev = deferred ? &status->n_entries : nullptr;
-        f->sorted_buf = radix_sort_keys(f->keys[0].as<uint64_t>(), f->keys[1].as<uint64_t>(), E,
-                                        passes, np, ctx->scratch2.p, st, false, n_dev);
-        mark(ctx, kStageRanges);
-        launch_tile_ranges_packed(f->keys[f->sorted_buf].as<uint64_t>(), E, f->fmt, ranges,
-                                  f->vals[0].as<uint32_t>(), ntiles, st, n_dev);
+        // Ranked emission outside debug mode: the last pass writes the values
+        // the compositing kernels read, and the ranges come from per-tile
+        // counts taken during the histogram read (no sorted keys written).
+        f->sort_keys_kept = !(ranked && !ctx->debug && np > 0 && E > 1);
+        if (!f->sort_keys_kept) {
+            SortFinish fin{f->vals[0].as<uint32_t>(), ranges, f->fmt.vb, f->fmt.tile_shift, ntiles};
+            f->sorted_buf = radix_sort_keys(f->keys[0].as<uint64_t>(), f->keys[1].as<uint64_t>(), E, passes,
+                                            np, ctx->scratch2.p, st, false, n_dev, &fin);
+            mark(ctx, kStageRanges);
+        } else {
+            f->sorted_buf = radix_sort_keys(f->keys[0].as<uint64_t>(), f->keys[1].as<uint64_t>(), E,
+                                            passes, np, ctx->scratch2.p, st, false, n_dev);
+            mark(ctx, kStageRanges);
+            launch_tile_ranges_packed(f->keys[f->sorted_buf].as<uint64_t>(), E, f->fmt, ranges,
+                                      f->vals[0].as<uint32_t>(), ntiles, st, n_dev);
+        }
         f->vals_buf = 0;
     } else {
         for (int b = 0; b < 2; ++b) {
@@ -676,6 +688,11 @@ BufView frame_buffer(svr_frame* f, svr_buffer which) {
         case SVR_BUF_SS_TFIN: return {ss1 ? f->out_tfin.p : f->ss_tfin.p, nss * 4};
         case SVR_BUF_SORT_KEYS:
         case SVR_BUF_SORT_VALUES:
+            if (f->packed && !f->sort_keys_kept) {
+                require(which == SVR_BUF_SORT_VALUES, SVR_ERR_INVALID_ARGUMENT,
+                        "sorted key dump needs svr_ctx_set_debug");
+                return {f->vals[0].p, f->n_entries * 4};
+            }
             if (f->packed) {
                 uint64_t* k = grow<uint64_t>(f->ref_keys, f->n_entries);
                 uint32_t* v = grow<uint32_t>(f->ref_vals, f->n_entries);

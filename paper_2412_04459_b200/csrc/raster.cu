@@ -666,14 +666,18 @@ __global__ void tile_ranges_kernel(const uint64_t* keys, uint64_t n, uint2* rang
 // Longest-processing-time-first tile order for K7: tiles bucketed by
 // floor(log2(entries+1)), heaviest bucket first, so the long tiles start in
 // the first wave and the kernel tail is made of short ones.
-__global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* ranges, int ntiles,
+__global__ void __launch_bounds__(1024) tile_order_kernel(uint2* ranges, int ntiles,
                                                           uint32_t* order) {
     pdl_enter();
     __shared__ uint32_t s_cnt[33];
     if (threadIdx.x < 33) s_cnt[threadIdx.x] = 0;
     __syncthreads();
     for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
-        const uint2 r = ranges[t];
+        uint2 r = ranges[t];
+        if (r.x > r.y) {  // no entries (value-only sort finish leaves lo > hi)
+            r = make_uint2(0u, 0u);
+            ranges[t] = r;
+        }
         atomicAdd(&s_cnt[31 - __clz(r.y - r.x + 1)], 1u);
     }
     __syncthreads();
@@ -1284,7 +1288,7 @@ void launch_compact_contribs(const uint32_t* pix_count, const uint32_t* pix_begi
     SVR_LAUNCH("compact_contribs_kernel");
 }
 
-void launch_tile_order(const uint2* ranges, int ntiles, uint32_t* order, cudaStream_t st) {
+void launch_tile_order(uint2* ranges, int ntiles, uint32_t* order, cudaStream_t st) {
     launch_pdl(tile_order_kernel, 1, 1024, 0, st, ranges, ntiles, order);
     SVR_LAUNCH("tile_order_kernel");
 }

@@ -76,6 +76,11 @@ __global__ void __launch_bounds__(kThreads) hist_kernel(const uint64_t* keys, co
     }
 }
 
+__global__ void ranges_init_kernel(uint2* ranges, int ntiles) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < ntiles) ranges[t] = make_uint2(0xffffffffu, 0u);
+}
+
 // One block per pass: exclusive scan of the 256 digit counts.
 __global__ void __launch_bounds__(kRadix) bin_scan_kernel(uint32_t* hist) {
     pdl_enter();
@@ -107,7 +112,7 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
     const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint64_t n, RadixPass pass,
     const uint32_t* __restrict__ bin_base, uint32_t* status, uint32_t* ticket,
-    const unsigned long long* n_dev) {
+    const unsigned long long* n_dev, int out_vb, uint2* ranges, int tile_shift) {
     pdl_enter();
     __shared__ uint32_t s_warp_hist[kWarps][kRadix + 1];
     __shared__ uint32_t s_block_excl[kRadix];
@@ -246,6 +251,16 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
         uint32_t vv = PAIRS ? s_vals[pos] : 0u;
         uint32_t dd = digit_of(kk, vv, pass);
         uint64_t o = uint64_t(s_global[dd]) + pos;
+        if (!PAIRS && out_vb >= 0) {
+            // final pass of a packed sort: the reference value only, and the
+            // tile ranges from the run ends in this partition (a tile's keys
+            // are contiguous in the output, so min of starts / max of ends)
+            vals_out[o] = (uint32_t((kk >> out_vb) & 7u) << 29) | uint32_t(kk & ((uint64_t(1) << out_vb) - 1));
+            const uint64_t t = kk >> tile_shift;
+            if (pos == 0 || (s_keys[pos - 1] >> tile_shift) != t) atomicMin(&ranges[t].x, uint32_t(o));
+            if (pos + 1 == tile_n || (s_keys[pos + 1] >> tile_shift) != t) atomicMax(&ranges[t].y, uint32_t(o + 1));
+            continue;
+        }
         keys_out[o] = kk;
         if (PAIRS) vals_out[o] = vv;
     }
@@ -291,7 +306,7 @@ int radix_sort_pairs(uint64_t* keys0, uint32_t* vals0, uint64_t* keys1, uint32_t
     for (int p = 0; p < npasses; ++p) {
         onesweep_kernel<true><<<unsigned(nparts), kThreads, 0, st>>>(
             kin, vin, kout, vout, n, passes[p], hist + p * kRadix,
-            status + size_t(p) * (nparts + 1) * kRadix, tickets + p, nullptr);
+            status + size_t(p) * (nparts + 1) * kRadix, tickets + p, nullptr, -1, nullptr, 0);
         SVR_LAUNCH("onesweep_kernel");
         std::swap(kin, kout);
         std::swap(vin, vout);
@@ -308,7 +323,11 @@ void sort_prepare(void* scratch, uint64_t n, int npasses, cudaStream_t st) {
 
 int radix_sort_keys(uint64_t* keys0, uint64_t* keys1, uint64_t n, const RadixPass* passes,
                     int npasses, void* scratch, cudaStream_t st, bool hist_ready,
-                    const unsigned long long* n_dev) {
+                    const unsigned long long* n_dev, const SortFinish* fin) {
+    if (fin) {
+        ranges_init_kernel<<<(fin->ntiles + 255) / 256, 256, 0, st>>>(fin->ranges, fin->ntiles);
+        SVR_LAUNCH("ranges_init_kernel");
+    }
     if (n <= 1 || npasses == 0) return 0;
     if (npasses > kMaxRadixPasses) throw Error(SVR_ERR_RUNTIME, "too many radix passes");
     if (n >= (uint64_t(1) << 30))
@@ -328,7 +347,8 @@ int radix_sort_keys(uint64_t* keys0, uint64_t* keys1, uint64_t n, const RadixPas
         spec.n = npasses;
         for (int i = 0; i < npasses; ++i) spec.p[i] = passes[i];
         int hist_blocks = int(std::min<uint64_t>((n + kThreads - 1) / kThreads, 148 * 4));
-        launch_pdl(hist_kernel, hist_blocks, kThreads, 0, st, keys0, (const uint32_t*)nullptr, n, spec, hist, n_dev);
+        launch_pdl(hist_kernel, hist_blocks, kThreads, 0, st, keys0, (const uint32_t*)nullptr, n, spec, hist,
+                   n_dev);
         SVR_LAUNCH("hist_kernel");
     }
     launch_pdl(bin_scan_kernel, npasses, kRadix, 0, st, hist);
@@ -337,10 +357,12 @@ int radix_sort_keys(uint64_t* keys0, uint64_t* keys1, uint64_t n, const RadixPas
     uint64_t* kout = keys1;
     int cur = 0;
     for (int p = 0; p < npasses; ++p) {
+        const bool last_fin = fin && p == npasses - 1;
         launch_pdl(onesweep_kernel<false>, unsigned(nparts), kThreads, 0, st, (const uint64_t*)kin,
-                   (const uint32_t*)nullptr, kout, (uint32_t*)nullptr, n, passes[p],
+                   (const uint32_t*)nullptr, kout, last_fin ? fin->vals : (uint32_t*)nullptr, n, passes[p],
                    (const uint32_t*)(hist + p * kRadix), status + size_t(p) * (nparts_alloc + 1) * kRadix,
-                   tickets + p, n_dev);
+                   tickets + p, n_dev, last_fin ? fin->vb : -1, last_fin ? fin->ranges : (uint2*)nullptr,
+                   last_fin ? fin->tile_shift : 0);
         SVR_LAUNCH("onesweep_kernel");
         std::swap(kin, kout);
         cur ^= 1;

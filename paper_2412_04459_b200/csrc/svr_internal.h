@@ -145,6 +145,7 @@ struct svr_frame {
     svrb::DevBuf tile_masks, tile_sat, rects, aabb, records, counts, offsets, visible_rank;
     svrb::DevBuf keys[2], vals[2], dbg_keys, dbg_vals, ranges, tile_order, big;
     svrb::DevBuf pair_counts, big_pairs, rowspan;  // rank-ordered duplicate
+    bool sort_keys_kept = true;  // false: the last sort pass wrote values only
     svrb::DevBuf out_color, out_depth, out_median, out_normal, out_tfin, max_blend;
     svrb::DevBuf ss_color, ss_depth, ss_median, ss_normal, ss_tfin;
     svrb::DevBuf pix_count, pix_begin, contrib_entry, contrib_T;

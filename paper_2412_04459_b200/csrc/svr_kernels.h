@@ -48,9 +48,21 @@ uint32_t* sort_hist_ptr(void* scratch);
 void sort_prepare(void* scratch, uint64_t n, int npasses, cudaStream_t st);
 // n_dev (optional): the live count on the device (<= n, the capacity the
 // launch grids are sized for); partitions past it exit at once.
+// fin (optional): the last pass writes, instead of keys, the reference value
+// (s << 29 | vid) of each packed key (vid = low fin->vb bits, s the next 3)
+// into fin->vals, and the tile ranges (tile = key >> fin->tile_shift) into
+// fin->ranges from the ends of each partition's tile runs; tiles without
+// entries are left with lo > hi (launch_tile_order turns them into [0, 0)).
+// The sorted keys are then never written and the range kernel's pass over
+// them is gone.
+struct SortFinish {
+    uint32_t* vals;
+    uint2* ranges;
+    int vb, tile_shift, ntiles;
+};
 int radix_sort_keys(uint64_t* keys0, uint64_t* keys1, uint64_t n, const RadixPass* passes,
                     int npasses, void* scratch, cudaStream_t st, bool hist_ready,
-                    const unsigned long long* n_dev = nullptr);
+                    const unsigned long long* n_dev = nullptr, const SortFinish* fin = nullptr);
 
 // ---- raster.cu -------------------------------------------------------------
 struct FrameStatus {          // device -> host summary, one read per frame
@@ -187,7 +199,7 @@ void launch_compact_contribs(const uint32_t* pix_count, const uint32_t* pix_begi
                              uint32_t* contrib_entry, float* contrib_T, cudaStream_t st);
 void launch_composite(const DevCamera& cam, const CompositeArgs& a, bool record_pass,
                       cudaStream_t st);
-void launch_tile_order(const uint2* ranges, int ntiles, uint32_t* order, cudaStream_t st);
+void launch_tile_order(uint2* ranges, int ntiles, uint32_t* order, cudaStream_t st);
 
 // Area resampler (image.cpp:9-45): CSR taps per destination index.
 struct TapTable {

@@ -163,6 +163,28 @@ def test_emission_paths_bit_exact(svr, ctx, ref, cfg1, monkeypatch, ranked):
                                         if ranked == "1" else f.info().sort_passes)
 
 
+def test_value_only_final_pass_matches_debug_path(svr, ctx, ref, cfg1):
+    """Outside debug mode the last sort pass writes values only and the tile
+    ranges come from per-tile counts: same values, ranges and image as the
+    debug path (which keeps the sorted keys and scans them for ranges)."""
+    arrays, _, rscene = cfg1
+    fast = svr.Context(0)
+    scene_fast = svr.Scene(fast, arrays)
+    for cam in [svr.ring_camera(3, 1, 320, 192),
+                svr.Camera(96, 80, 40.0, 40.0, 47.5, 39.5, np.eye(3), np.array([0.02, 0.01, -0.04]))]:
+        f = svr.Frame(fast)
+        svr.render_into(f, scene_fast, cam, svr.RenderOptions(supersample=1.0))
+        ks_ref, vs_ref = ref.ref_entries(rscene, cam, sorted_=True)
+        assert np.array_equal(f.download("SORT_VALUES", np.uint32), vs_ref)
+        ranges = f.download("TILE_RANGES", np.uint32, (-1, 2))
+        tiles = (ks_ref >> np.uint64(48)).astype(np.int64)
+        t = np.arange(ranges.shape[0])
+        assert np.array_equal(ranges[:, 0], np.searchsorted(tiles, t, "left"))
+        assert np.array_equal(ranges[:, 1], np.searchsorted(tiles, t, "right"))
+        out = svr.render(scene_fast, cam, svr.RenderOptions(supersample=1.0))
+        compare_outputs(out, ref.ref_render(rscene, cam, svr.RenderOptions(supersample=1.0)))
+
+
 def test_multi_pattern_entries_bit_exact(svr, ctx, ref):
     """A camera inside the scene: straddlers get the whole image, tiles carry
     several sign patterns (raster.cpp:96-103, 120-142)."""
