@@ -360,7 +360,9 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     pa.records = grow<float4>(f->records, N * kRecordF4);
     pa.counts = grow<uint32_t>(f->counts, N);
     pa.view_dir = f->training ? grow<float4>(f->view_dir, N) : nullptr;
-    pa.order = scene->proc_order.p ? scene->proc_order.as<uint32_t>() : nullptr;
+    // scenes stored out of spatial order: pre-cull pass + worklist
+    pa.order = scene->unordered ? grow<uint32_t>(f->work, N) : nullptr;
+    pa.n_order = scene->unordered ? &status->n_work : nullptr;
     mark(ctx, kStagePreprocess);
     launch_preprocess(cam, pa, st);
 
@@ -1042,11 +1044,7 @@ int svr_scene_upload(svr_ctx* ctx, const svr_scene_desc* d, svr_scene** out) {
                 for (uint64_t i = 1; i < N; ++i) asc += (paths[i] & kPathCode) > (paths[i - 1] & kPathCode);
                 const char* po = std::getenv("SVR_PROC_ORDER");  // 0: never, 1: always
                 const bool want = po ? po[0] == '1' : (N > 1 && asc * 10 < (N - 1) * 9);
-                if (want) {
-                    s->proc_order.reserve(N * 4);
-                    build_proc_order(s->paths.as<uint64_t>(), N, max_level, s->proc_order.as<uint32_t>(),
-                                     tmp.p, ctx->stream);
-                }
+                s->unordered = want;
                 SVR_CUDA(cudaStreamSynchronize(ctx->stream));
                 s->rank_bits = bit_width(8 * N - 1);
             }

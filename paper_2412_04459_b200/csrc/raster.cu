@@ -115,21 +115,53 @@ __device__ __forceinline__ uint32_t sat_rect(const uint32_t* sat, int ntx, int t
 // ------------------------------------------------------------------- K1
 // 128 threads = 4 warps, one voxel per thread. A conservative fp32 test first
 // drops the voxels the exact fp64 projection would certainly cull. For scenes
-// whose voxel order is not spatially coherent, threads take voxels in the
-// scene's Morton order (a.order), so that the culled voxels of a warp are
-// culled together. In scene order, the 96-B records of the CTA's visible
-// voxels are staged in shared memory and written back as contiguous runs.
+// whose voxel order is not spatially coherent, that test runs in its own pass
+// (precull_kernel) and K1 walks the worklist of survivors (a.order), so a
+// warp's lanes are not split between culled and projected voxels. In scene
+// order, the 96-B records of the CTA's visible voxels are staged in shared
+// memory and written back as contiguous runs.
 constexpr int kPreThreads = 128;
 #ifndef SVR_PRE_MINB
 #define SVR_PRE_MINB 6
 #endif
+
+// K1a for scenes stored out of spatial order: voxels the fp32 pre-test
+// certainly culls get their (empty) outputs here, in scene order (coalesced);
+// the others are appended to a worklist (warp-aggregated) that K1 then
+// walks, so its warps carry no culled lanes.
+__global__ void __launch_bounds__(256) precull_kernel(DevCamera cam, PreprocessArgs a, uint32_t* work,
+                                                      unsigned int* n_work) {
+    pdl_enter();
+    const uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    bool keep = false;
+    if (v < a.n) {
+        const uint64_t path = a.paths[v];
+        double center[3], size;
+        voxel_geometry(path & kCodeMask48, int(path >> 48), a.bc, a.bsize, center, &size);
+        keep = !surely_culled(cam, center, size, a.near_plane);
+        if (!keep) {
+            a.rects[v] = make_int4(0, -1, 0, -1);
+            a.counts[v] = 0u;
+            if (a.aabb) a.aabb[v] = make_double4(0.0, 0.0, 0.0, 0.0);
+        }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (m == 0) return;
+    const int lane = threadIdx.x & 31;
+    unsigned base = 0;
+    if (lane == __ffs(m) - 1) base = atomicAdd(n_work, unsigned(__popc(m)));
+    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+    if (keep) work[base + __popc(m & ((1u << lane) - 1u))] = uint32_t(v);
+}
 
 __global__ void __launch_bounds__(kPreThreads, SVR_PRE_MINB) preprocess_kernel(DevCamera cam, PreprocessArgs a) {
     pdl_enter();
     extern __shared__ float4 smem4[];
     float4* s_rec = smem4;
     const uint64_t v0 = uint64_t(blockIdx.x) * kPreThreads;
-    const bool valid = v0 + threadIdx.x < a.n;
+    const uint64_t n_items = a.n_order ? uint64_t(*a.n_order) : a.n;  // worklist: live length
+    if (v0 >= n_items) return;
+    const bool valid = v0 + threadIdx.x < n_items;
     const uint64_t v = a.order ? (valid ? uint64_t(__ldg(a.order + v0 + threadIdx.x)) : a.n)
                                : v0 + threadIdx.x;
 
@@ -140,7 +172,7 @@ __global__ void __launch_bounds__(kPreThreads, SVR_PRE_MINB) preprocess_kernel(D
         voxel_geometry(path & kCodeMask48, int(path >> 48), a.bc, a.bsize, center, &size);
         Projection pr;
         bool vis = false;
-        if (surely_culled(cam, center, size, a.near_plane)) {
+        if (!a.n_order && surely_culled(cam, center, size, a.near_plane)) {
             pr.tx0 = pr.ty0 = 0;  // a fresh PreVoxel, as project_voxel leaves a culled one
             pr.tx1 = pr.ty1 = -1;
             pr.x0 = pr.x1 = pr.y0 = pr.y1 = 0.0;
@@ -604,14 +636,6 @@ __global__ void rank_keys_kernel(const uint64_t* __restrict__ paths, uint64_t n,
     const uint64_t s = i / n, v = i - s * n;
     keys[i] = (paths[v] & kCodeMask48) ^ (s * kGroupOnes);
     vals[i] = uint32_t(s << 29) | uint32_t(v);
-}
-
-__global__ void code_keys_kernel(const uint64_t* __restrict__ paths, uint64_t n, uint64_t* keys,
-                                 uint32_t* vals) {
-    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    keys[i] = paths[i] & kCodeMask48;
-    vals[i] = uint32_t(i);
 }
 
 __global__ void rank_scatter_kernel(const uint32_t* __restrict__ vals, uint64_t n, uint32_t* rank) {
@@ -1134,6 +1158,11 @@ void launch_tile_masks_only(const DevCamera& cam, uint8_t* masks, cudaStream_t s
 void launch_preprocess(const DevCamera& cam, const PreprocessArgs& a, cudaStream_t st) {
     if (a.n == 0) return;
     const size_t smem = a.order ? 0 : size_t(kPreThreads) * kRecordF4 * 16;
+    if (a.n_order) {  // worklist mode: a.order is filled by the pre-cull pass
+        launch_pdl(precull_kernel, blocks_for(a.n, 256), 256, 0, st, cam, a, const_cast<uint32_t*>(a.order),
+                   const_cast<unsigned int*>(a.n_order));
+        SVR_LAUNCH("precull_kernel");
+    }
     launch_pdl(preprocess_kernel, blocks_for(a.n, kPreThreads), kPreThreads, smem, st, cam, a);
     SVR_LAUNCH("preprocess_kernel");
 }
@@ -1233,26 +1262,6 @@ void build_morton_rank(const uint64_t* paths, uint64_t n, int lmax, uint32_t* ra
     rank_scatter_kernel<<<blocks_for(m, 256), 256, 0, st>>>(out ? v1 : v0, n, rank);
     SVR_LAUNCH("rank_scatter_kernel");
     if (order) SVR_CUDA(cudaMemcpyAsync(order, out ? v1 : v0, m * 4, cudaMemcpyDeviceToDevice, st));
-}
-
-void build_proc_order(const uint64_t* paths, uint64_t n, int lmax, uint32_t* order, void* scratch,
-                      cudaStream_t st) {
-    if (n == 0) return;
-    char* p = static_cast<char*>(scratch);
-    uint64_t* k0 = reinterpret_cast<uint64_t*>(p);
-    uint64_t* k1 = k0 + n;
-    uint32_t* v0 = reinterpret_cast<uint32_t*>(k1 + n);
-    uint32_t* v1 = v0 + n;
-    void* sort_scratch = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(v1 + n) + 255) &
-                                                 ~uintptr_t(255));
-    code_keys_kernel<<<blocks_for(n, 256), 256, 0, st>>>(paths, n, k0, v0);
-    SVR_LAUNCH("code_keys_kernel");
-    RadixPass passes[kMaxRadixPasses];
-    int np = 0;
-    for (int b = 48 - 3 * lmax; b < 48; b += 8) passes[np++] = {0, b, std::min(8, 48 - b)};
-    int out = 0;
-    if (np > 0) out = radix_sort_pairs(k0, v0, k1, v1, n, passes, np, sort_scratch, st);
-    SVR_CUDA(cudaMemcpyAsync(order, out ? v1 : v0, n * 4, cudaMemcpyDeviceToDevice, st));
 }
 
 void launch_tile_ranges_packed(const uint64_t* keys, uint64_t n, PackedFormat fmt, uint2* ranges,

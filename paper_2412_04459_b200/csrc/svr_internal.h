@@ -121,7 +121,7 @@ struct svr_scene {
     svrb::DevBuf sh;            // f32 [n][stride]
     svrb::DevBuf morton_rank;   // u32 [8][n]: build_morton_rank (sort keys)
     svrb::DevBuf morton_order;  // u32 [8n]: the (s, vid) pairs in rank order
-    svrb::DevBuf proc_order;    // u32 [n]: K1 processing order (empty: scene order is coherent)
+    bool unordered = false;     // voxels not in spatial order: K1 runs pre-cull + worklist
     int rank_bits = 0;          // bit width of 8n-1; 0 = no table
     // AdaptRemap of a scene produced by svr_scene_prune / svr_scene_subdivide
     svrb::DevBuf voxel_src, pool_src;  // int64 per voxel / per pool entry
@@ -145,6 +145,7 @@ struct svr_frame {
     svrb::DevBuf tile_masks, tile_sat, rects, aabb, records, counts, offsets, visible_rank;
     svrb::DevBuf keys[2], vals[2], dbg_keys, dbg_vals, ranges, tile_order, big;
     svrb::DevBuf pair_counts, big_pairs, rowspan;  // rank-ordered duplicate
+    svrb::DevBuf work;                             // K1 worklist (unordered scenes)
     bool sort_keys_kept = true;  // false: the last sort pass wrote values only
     svrb::DevBuf out_color, out_depth, out_median, out_normal, out_tfin, max_blend;
     svrb::DevBuf ss_color, ss_depth, ss_median, ss_normal, ss_tfin;

@@ -72,6 +72,8 @@ struct FrameStatus {          // device -> host summary, one read per frame
     unsigned long long n_contribs;
     unsigned int n_big;       // voxels handed to the cooperative duplicate
     unsigned int n_big_ranked;  // the same for the rank-ordered duplicate
+    unsigned int n_work;        // K1 worklist length (pre-cull pass)
+    unsigned int pad2;
     unsigned long long n_entries_voxel;  // E from the per-voxel scan (parity dumps of the ranked path)
 };
 
@@ -101,7 +103,8 @@ struct PreprocessArgs {
     float4* records;
     uint32_t* counts;
     float4* view_dir;  // optional (training): unit sh_eval direction per visible voxel
-    const uint32_t* order;  // optional: processing order (the scene's voxels in Morton order)
+    const uint32_t* order;  // optional: voxel worklist (filled by the pre-cull pass, n voxels of room)
+    const unsigned int* n_order;  // with order: its live length on the device (zeroed by the caller)
 };
 void launch_preprocess(const DevCamera& cam, const PreprocessArgs& a, cudaStream_t st);
 
@@ -133,10 +136,6 @@ void launch_duplicate_packed(const DevCamera& cam, uint64_t n, const uint64_t* p
 size_t morton_rank_scratch_bytes(uint64_t n, int lmax);
 void build_morton_rank(const uint64_t* paths, uint64_t n, int lmax, uint32_t* rank, uint32_t* order,
                        void* scratch, cudaStream_t st);
-// The scene's voxel ids sorted by Morton code (K1's processing order for
-// scenes stored out of spatial order); scratch as morton_rank_scratch_bytes.
-void build_proc_order(const uint64_t* paths, uint64_t n, int lmax, uint32_t* order, void* scratch,
-                      cudaStream_t st);
 // Rank-ordered K4 (needs the per-pattern SATs of launch_tile_setup
 // per_pattern, the rank table and the scene's pair list order[r] =
 // s << 29 | vid). K4a: pc[rank[s*n + v]] = entries of pair (s, v), 8n u32,
