@@ -314,18 +314,22 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
     }
 }
 
-// ray_losses (losses.cpp:141-238). One WARP per supersampled pixel: its
-// contributions are contiguous in the compact (reference) order, so lane k
-// handles contribution chunk*32 + k and every upstream gradient read/write
-// is coalesced. w = T_i * alpha_i is recomputed from the voxel record exactly
-// as the forward composited it (fp32 slab + quadrature); m = (a + b) / 2 and
-// l = b - a come from the same slab. L_dist's prefix sums are warp scans
-// carried across chunks; its suffix half is a second pass in reverse over
-// (w, m) kept in scratch, like the reference's two loops.
-__device__ __forceinline__ float warp_incl_scan_f(float v, int lane) {
+// ray_losses (losses.cpp:141-238). A group of L = 8 lanes per supersampled
+// pixel (4 pixels per warp: a pixel has a few dozen contributions, so a
+// whole warp per pixel left most lanes idle; 8 lanes: 264 -> 277 it/s on
+// config 3i): its contributions are contiguous in the compact (reference)
+// order, so lane k handles contribution chunk*L + k and the upstream
+// gradient reads/writes are coalesced per group. w = T_i * alpha_i is
+// recomputed from the voxel record exactly as the forward composited it
+// (fp32 slab + quadrature); m = (a + b) / 2 and l = b - a come from the same
+// slab. L_dist's prefix sums are segmented shuffle scans carried across
+// chunks; its suffix half is a second pass in reverse over (w, m) kept in
+// scratch, like the reference's two loops.
+template <int L>
+__device__ __forceinline__ float group_incl_scan_f(float v, int lane, unsigned gmask) {
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const float n = __shfl_up_sync(0xffffffffu, v, o);
+    for (int o = 1; o < L; o <<= 1) {
+        const float n = __shfl_up_sync(gmask, v, o, L);
         if (lane >= o) v += n;
     }
     return v;
@@ -349,12 +353,14 @@ __global__ void __launch_bounds__(256) ray_loss_T_kernel(RayLossArgs a, uint64_t
     if ((threadIdx.x & 31) == 0) atomicAdd(a.sums, double(lT) * inv_rays);
 }
 
-template <int K>
+template <int K, int L>
 __global__ void __launch_bounds__(256) ray_losses_kernel(DevCamera cam, RayLossArgs a) {
     pdl_enter();
-    const int lane = threadIdx.x & 31;
-    // grid (ceil(W / 8), H): warp w of block (bx, y) owns pixel (8 bx + w, y)
-    const int px = int(blockIdx.x) * 8 + (threadIdx.x >> 5), py = int(blockIdx.y);
+    // L lanes per pixel: grid (ceil(W / (256 / L)), H); group g of block
+    // (bx, y) owns pixel ((256 / L) bx + g, y)
+    const int lane = threadIdx.x & (L - 1);
+    const unsigned gmask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << (threadIdx.x & 31 & ~(L - 1)));
+    const int px = int(blockIdx.x) * (256 / L) + int(threadIdx.x / L), py = int(blockIdx.y);
     const uint64_t npix = uint64_t(cam.W) * cam.H;
     const double inv_rays = 1.0 / double(npix);
     float lT = 0.f, ldist = 0.f, lR = 0.f;
@@ -379,7 +385,7 @@ __global__ void __launch_bounds__(256) ray_losses_kernel(DevCamera cam, RayLossA
             constexpr uint32_t kVidMask = (1u << 29) - 1u;
             const float wd = float(a.w_dist * inv_rays);
             float Wc = 0.f, Sc = 0.f;  // prefix carries across chunks
-            for (uint32_t c0 = 0; c0 < n; c0 += 32) {
+            for (uint32_t c0 = 0; c0 < n; c0 += L) {
                 const uint32_t i = c0 + lane;
                 const bool on = i < n;
                 float w = 0.f, m = 0.f, dl = 0.f, gdw = 0.f;
@@ -425,15 +431,16 @@ __global__ void __launch_bounds__(256) ray_losses_kernel(DevCamera cam, RayLossA
                     }
                 }
                 if (a.w_dist != 0.0) {
-                    const float wi = warp_incl_scan_f(w, lane), si = warp_incl_scan_f(w * m, lane);
+                    const float wi = group_incl_scan_f<L>(w, lane, gmask);
+                    const float si = group_incl_scan_f<L>(w * m, lane, gmask);
                     const float Wpre = Wc + wi - w, Spre = Sc + si - w * m;
                     if (on) {
                         ldist += 2.f * w * (m * Wpre - Spre) + w * w * dl * (1.0f / 3.0f);
                         gdw = wd * (2.f * (m * Wpre - Spre) + 2.f * w * dl * (1.0f / 3.0f));
                         a.scratch[base + i] = make_float2(w, m);
                     }
-                    Wc += __shfl_sync(0xffffffffu, wi, 31);
-                    Sc += __shfl_sync(0xffffffffu, si, 31);
+                    Wc += __shfl_sync(gmask, wi, L - 1, L);
+                    Sc += __shfl_sync(gmask, si, L - 1, L);
                 }
                 if (on) {
                     if (a.w_R != 0.0) {
@@ -450,17 +457,18 @@ __global__ void __launch_bounds__(256) ray_losses_kernel(DevCamera cam, RayLossA
             }
             if (a.w_dist != 0.0) {  // suffix half of d|m_i - m_j|, chunks in reverse
                 float Wsc = 0.f, Ssc = 0.f;
-                const uint32_t last = (n - 1) / 32 * 32;
-                for (int c0 = int(last); c0 >= 0; c0 -= 32) {
-                    const uint32_t i = uint32_t(c0) + 31 - lane;  // reversed lane order
+                const uint32_t last = (n - 1) / L * L;
+                for (int c0 = int(last); c0 >= 0; c0 -= L) {
+                    const uint32_t i = uint32_t(c0) + (L - 1) - lane;  // reversed lane order
                     const bool on = i < n;
                     float2 wm = make_float2(0.f, 0.f);
                     if (on) wm = a.scratch[base + i];
-                    const float wi = warp_incl_scan_f(wm.x, lane), si = warp_incl_scan_f(wm.x * wm.y, lane);
+                    const float wi = group_incl_scan_f<L>(wm.x, lane, gmask);
+                    const float si = group_incl_scan_f<L>(wm.x * wm.y, lane, gmask);
                     const float Wsuf = Wsc + wi - wm.x, Ssuf = Ssc + si - wm.x * wm.y;
                     if (on) a.d_weight[base + i] += wd * (2.f * (Ssuf - wm.y * Wsuf));
-                    Wsc += __shfl_sync(0xffffffffu, wi, 31);
-                    Ssc += __shfl_sync(0xffffffffu, si, 31);
+                    Wsc += __shfl_sync(gmask, wi, L - 1, L);
+                    Ssc += __shfl_sync(gmask, si, L - 1, L);
                 }
             }
         }
@@ -474,7 +482,7 @@ __global__ void __launch_bounds__(256) ray_losses_kernel(DevCamera cam, RayLossA
         ldist += __shfl_xor_sync(0xffffffffu, ldist, o);
         lR += __shfl_xor_sync(0xffffffffu, lR, o);
     }
-    if (lane == 0) s_red[0][warp] = lT, s_red[1][warp] = ldist, s_red[2][warp] = lR;
+    if ((threadIdx.x & 31) == 0) s_red[0][warp] = lT, s_red[1][warp] = ldist, s_red[2][warp] = lR;
     __syncthreads();
     if (threadIdx.x < 3) {
         double t = 0.0;
@@ -748,11 +756,15 @@ void launch_ray_losses(const DevCamera& cam, const RayLossArgs& a, cudaStream_t 
         SVR_LAUNCH("ray_loss_T_kernel");
     }
     if (a.w_dist == 0.0 && a.w_R == 0.0) return;
-    const dim3 grid(unsigned((cam.W + 7) / 8), unsigned(cam.H));  // a warp per pixel
+#ifndef SVR_RL_LANES
+#define SVR_RL_LANES 8
+#endif
+    constexpr int L = SVR_RL_LANES;  // lanes per pixel
+    const dim3 grid(unsigned((cam.W + 256 / L - 1) / (256 / L)), unsigned(cam.H));
     switch (a.K) {
-        case 1: launch_pdl(ray_losses_kernel<1>, grid, 256, 0, st, cam, a); break;
-        case 2: launch_pdl(ray_losses_kernel<2>, grid, 256, 0, st, cam, a); break;
-        case 3: launch_pdl(ray_losses_kernel<3>, grid, 256, 0, st, cam, a); break;
+        case 1: launch_pdl(ray_losses_kernel<1, L>, grid, 256, 0, st, cam, a); break;
+        case 2: launch_pdl(ray_losses_kernel<2, L>, grid, 256, 0, st, cam, a); break;
+        case 3: launch_pdl(ray_losses_kernel<3, L>, grid, 256, 0, st, cam, a); break;
         default: throw Error(SVR_ERR_INVALID_ARGUMENT, "rasterizer sample count K must be in {1,2,3}");
     }
     SVR_LAUNCH("ray_losses_kernel");
