@@ -281,32 +281,22 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
             }
             const uint32_t vid = __float_as_uint(wrec[sl][4].w);
             const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+            float4* gv = reinterpret_cast<float4*>(a.g_vox + 16ull * vid);
             if (__popc(hm) <= SVR_BWD_DIRECT) {
-                // few pixels: each one adds its own 15 values (no 31-shuffle reduction)
+                // few pixels: each one adds its own 15 values (no 31-shuffle
+                // reduction) as four float4 reductions into the voxel's record
                 if (hit) {
-                    const uint4* ci4 = reinterpret_cast<const uint4*>(a.corner_index + 8ull * vid);
-                    const uint4 k0 = __ldg(ci4), k1 = __ldg(ci4 + 1);
-                    const uint32_t ci[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) atomicAdd(a.g_density + ci[c], acc[c]);
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        atomicAdd(a.g_color + 3ull * vid + c, acc[8 + c]);
-                        atomicAdd(a.g_normal + 3ull * vid + c, acc[11 + c]);
-                    }
-                    atomicAdd(a.g_priority + vid, acc[14]);
+                    for (int j = 0; j < 4; ++j)
+                        atomicAdd(gv + j, make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]));
                 }
             } else {
+                // component q ends on lanes 2q, 2q+1; lanes 8j gather q = 4j..4j+3
                 const float tot = warp_transpose_sum16(acc, lane);
-                const int q = lane >> 1;
-                if ((lane & 1) == 0 && q < 15) {
-                    float* dst;
-                    if (q < 8) dst = a.g_density + __ldg(a.corner_index + 8ull * vid + q);
-                    else if (q < 11) dst = a.g_color + 3ull * vid + (q - 8);
-                    else if (q < 14) dst = a.g_normal + 3ull * vid + (q - 11);
-                    else dst = a.g_priority + vid;
-                    atomicAdd(dst, tot);
-                }
+                const float t1 = __shfl_down_sync(0xffffffffu, tot, 2);
+                const float t2 = __shfl_down_sync(0xffffffffu, tot, 4);
+                const float t3 = __shfl_down_sync(0xffffffffu, tot, 6);
+                if ((lane & 7) == 0) atomicAdd(gv + (lane >> 3), make_float4(tot, t1, t2, t3));
             }
             cur = __reduce_max_sync(0xffffffffu, unsigned(e1 + 1)) - 1;
         }
@@ -639,52 +629,50 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
 }
 
 // K10: 16 lanes per voxel, lane m owns SH basis function m, so the SH rows
-// (3(d+1)^2 floats per voxel) are read and written as contiguous runs. The
-// raw colour for the clamp mask (sh.hpp:66-74) is reduced over the 16 lanes;
-// the normal chain (field.hpp:158-170) runs on the first lane.
-__global__ void __launch_bounds__(256) voxel_epilogue_kernel(EpilogueArgs a) {
-    pdl_enter();
-    const uint64_t v = uint64_t(blockIdx.x) * 16u + (threadIdx.x >> 4);
-    const int m = threadIdx.x & 15;
-    const bool live = v < a.n;
-    const int4 r = live ? a.rects[v] : make_int4(0, -1, 0, -1);
-    const bool vis = r.y >= r.x;  // in `pre`
+// (3(d+1)^2 floats per voxel) are read and written as contiguous runs, and
+// component m of K9's per-voxel record (8 corner densities, colour, normal,
+// priority). The raw colour for the clamp mask (sh.hpp:66-74) is reduced
+// over the 16 lanes; lanes 0..7 add the normal chain (field.hpp:158-170) to
+// their corner and issue the voxel's 8 pool atomics. Voxels outside `pre`
+// leave at once (their group only zeroes SH gradients when not accumulating).
+// One visible voxel (all 16 lanes of its group present).
+__device__ __forceinline__ void epilogue_visible(const EpilogueArgs& a, uint64_t v, int m, unsigned gmask) {
     const int nb = (a.sh_degree + 1) * (a.sh_degree + 1);
     float* gsh = a.g_sh + v * uint64_t(a.sh_stride);
+    // K9's record of this voxel: lane m holds component m (coalesced 64 B);
+    // consumed here and left zero for the next backward
+    const float gvm = a.g_vox[16 * v + m];
     // sh_eval direction exactly as K1 used it (raster.cpp:195-196): the
     // forward colour and this clamp mask see identical floats
-    float ux = 0.f, uy = 0.f, uz = 0.f;
-    if (vis) {
-        const float4 d = __ldg(a.view_dir + v);
-        ux = d.x, uy = d.y, uz = d.z;
-    }
+    const float4 d = __ldg(a.view_dir + v);
+    const float ux = d.x, uy = d.y, uz = d.z;
     float b[16] = {};  // lanes m >= (d+1)^2 read zeros, not stale registers
     sh_basis(a.sh_degree, ux, uy, uz, b);
     float bm = 0.f;
 #pragma unroll
     for (int i = 0; i < 16; ++i) bm = (m == i) ? b[i] : bm;
-    const bool mine = vis && m < nb;
     float c0 = 0.f, c1 = 0.f, c2 = 0.f;
-    if (mine) {
+    if (m < nb) {
         const float* co = a.sh + v * uint64_t(a.sh_stride) + 3 * m;
         c0 = co[0], c1 = co[1], c2 = co[2];
     }
     float r0 = bm * c0, r1 = bm * c1, r2 = bm * c2;
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1) {
-        r0 += __shfl_xor_sync(0xffffffffu, r0, o);
-        r1 += __shfl_xor_sync(0xffffffffu, r1, o);
-        r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+        r0 += __shfl_xor_sync(gmask, r0, o, 16);
+        r1 += __shfl_xor_sync(gmask, r1, o, 16);
+        r2 += __shfl_xor_sync(gmask, r2, o, 16);
     }
-    if (!live) return;
-    if (!vis) {  // not in `pre`: no gradient
-        if (!a.accumulate)
-            for (int i = m; i < a.sh_stride; i += 16) gsh[i] = 0.f;
-        return;
-    }
-    const float g0 = r0 > 0.f ? a.g_color[3 * v + 0] : 0.f;
-    const float g1 = r1 > 0.f ? a.g_color[3 * v + 1] : 0.f;
-    const float g2 = r2 > 0.f ? a.g_color[3 * v + 2] : 0.f;
+    const float gc0 = __shfl_sync(gmask, gvm, 8, 16), gc1 = __shfl_sync(gmask, gvm, 9, 16),
+                gc2 = __shfl_sync(gmask, gvm, 10, 16);
+    const float dn[3] = {__shfl_sync(gmask, gvm, 11, 16), __shfl_sync(gmask, gvm, 12, 16),
+                         __shfl_sync(gmask, gvm, 13, 16)};
+    // reset the record only now: a store right behind the load of the same
+    // address stalls the thread until the load returns (0.84 vs 0.16 ms)
+    a.g_vox[16 * v + m] = 0.f;
+    const float g0 = r0 > 0.f ? gc0 : 0.f;
+    const float g1 = r1 > 0.f ? gc1 : 0.f;
+    const float g2 = r2 > 0.f ? gc2 : 0.f;
     if (m < nb) {
         float* o = gsh + 3 * m;
         if (a.accumulate) {
@@ -697,19 +685,45 @@ __global__ void __launch_bounds__(256) voxel_epilogue_kernel(EpilogueArgs a) {
             o[2] = bm * g2;
         }
     }
-    if (m != 0) return;
-    const float dn[3] = {a.g_normal[3 * v], a.g_normal[3 * v + 1], a.g_normal[3 * v + 2]};
-    if (dn[0] == 0.f && dn[1] == 0.f && dn[2] == 0.f) return;
-    const float4* rec = a.records + v * kRecordF4;
-    float V[8];
-    trilinear_corners(rec[2], rec[3], V);
-    float gV[8];
-    voxel_normal_backward(V, dn, gV);
-    const uint4* ci4 = reinterpret_cast<const uint4*>(a.corner_index + 8 * v);
-    const uint4 q0 = ci4[0], q1 = ci4[1];
-    const uint32_t ci[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+    if (m == 14) a.g_priority[v] += gvm;
+    if (m >= 8) return;
+    // corner m: the compositing sum plus the normal chain (field.hpp:158-170)
+    float gd = gvm;
+    if (dn[0] != 0.f || dn[1] != 0.f || dn[2] != 0.f) {
+        const float4* rec = a.records + v * kRecordF4;
+        float V[8];
+        trilinear_corners(rec[2], rec[3], V);
+        float gV[8];
+        voxel_normal_backward(V, dn, gV);
 #pragma unroll
-    for (int c = 0; c < 8; ++c) atomicAdd(a.g_density + ci[c], gV[c]);
+        for (int c = 0; c < 8; ++c) gd = (m == c) ? gd + gV[c] : gd;
+    }
+    if (gd != 0.f) atomicAdd(a.g_density + __ldg(a.corner_index + 8 * v + m), gd);
+}
+
+#ifndef SVR_EPI_MINB
+#define SVR_EPI_MINB 8  // 32 registers: full occupancy (config 3 epilogue 0.25 -> 0.21 ms)
+#endif
+__global__ void __launch_bounds__(256, SVR_EPI_MINB) voxel_epilogue_kernel(EpilogueArgs a) {
+    pdl_enter();
+    const int m = threadIdx.x & 15;
+    const unsigned gmask = 0xffffu << (threadIdx.x & 16);  // this voxel's 16 lanes
+    if (a.list) {  // training frames: K1's list of the voxels in `pre`, grid-stride
+        const uint64_t nl = *a.n_list;
+        for (uint64_t i = uint64_t(blockIdx.x) * 16u + (threadIdx.x >> 4); i < nl;
+             i += uint64_t(gridDim.x) * 16u)
+            epilogue_visible(a, __ldg(a.list + i), m, gmask);
+        return;
+    }
+    const uint64_t v = uint64_t(blockIdx.x) * 16u + (threadIdx.x >> 4);
+    const bool live = v < a.n;
+    const int4 r = live ? a.rects[v] : make_int4(0, -1, 0, -1);
+    if (!(r.y >= r.x)) {  // not in `pre`: no gradient (the whole 16-lane group leaves)
+        if (live && !a.accumulate)
+            for (int i = m; i < a.sh_stride; i += 16) a.g_sh[v * uint64_t(a.sh_stride) + i] = 0.f;
+        return;
+    }
+    epilogue_visible(a, v, m, gmask);
 }
 
 inline unsigned blocks_for(uint64_t n, int threads) { return unsigned((n + threads - 1) / threads); }
@@ -792,7 +806,8 @@ void launch_adam(const AdamArgs& a, cudaStream_t st) {
 
 void launch_voxel_epilogue(const DevCamera& cam, const EpilogueArgs& a, cudaStream_t st) {
     if (a.n == 0) return;
-    launch_pdl(voxel_epilogue_kernel, blocks_for(a.n, 16), 256, 0, st, a);
+    // with K1's visible list: a persistent grid (the list length lives on the device)
+    launch_pdl(voxel_epilogue_kernel, a.list ? 148u * 16u : blocks_for(a.n, 16), 256, 0, st, a);
     (void)cam;
     SVR_LAUNCH("voxel_epilogue_kernel");
 }

@@ -360,6 +360,8 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     pa.records = grow<float4>(f->records, N * kRecordF4);
     pa.counts = grow<uint32_t>(f->counts, N);
     pa.view_dir = f->training ? grow<float4>(f->view_dir, N) : nullptr;
+    pa.vis_list = f->training ? grow<uint32_t>(f->vis_list, N) : nullptr;
+    pa.n_vis_list = f->training ? &status->n_vis_list : nullptr;
     // scenes stored out of spatial order: pre-cull pass + worklist
     pa.order = scene->unordered ? grow<uint32_t>(f->work, N) : nullptr;
     pa.n_order = scene->unordered ? &status->n_work : nullptr;
@@ -405,6 +407,7 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
         SVR_CUDA(cudaStreamSynchronize(st));
         E = hs->n_entries;
         pattern_or = hs->pattern_or;
+        f->n_vis_list = f->training ? hs->n_vis_list : 0;
         require(E < (uint64_t(1) << 30), SVR_ERR_LENGTH, "entry count exceeds 2^30");
         f->e_cap = std::max<uint64_t>(f->e_cap, E + E / 4 + 1024);
     }
@@ -842,10 +845,14 @@ void backward_impl(svr_ctx* ctx, const svr_scene* scene, svr_frame* f, const svr
         SVR_CUDA(cudaMemsetAsync(gd, 0, P * 4, st));
         SVR_CUDA(cudaMemsetAsync(gp, 0, N * 4, st));
     }
-    float* gcol = grow<float>(f->bwd_gc, N * 3);
-    float* gnor = grow<float>(f->bwd_gn, N * 3);
-    SVR_CUDA(cudaMemsetAsync(gcol, 0, N * 12, st));
-    SVR_CUDA(cudaMemsetAsync(gnor, 0, N * 12, st));
+    // per-voxel gradient records (16 floats): zero when (re)allocated, then
+    // kept zero by the epilogue, which consumes every record K9 touched
+    if (f->bwd_gc.bytes < N * 64 || !f->gvox_clean) {
+        f->bwd_gc.reserve(std::max<uint64_t>(N, 1) * 64);
+        SVR_CUDA(cudaMemsetAsync(f->bwd_gc.p, 0, f->bwd_gc.bytes, st));
+    }
+    float* gvox = f->bwd_gc.as<float>();
+    f->gvox_clean = false;
 
     BackwardArgs ba{};
     ba.ranges = f->ranges.as<uint2>();
@@ -866,10 +873,7 @@ void backward_impl(svr_ctx* ctx, const svr_scene* scene, svr_frame* f, const svr
     ba.contrib_entry = f->staged ? f->stage_entry.as<uint32_t>() : f->contrib_entry.as<uint32_t>();
     ba.contrib_T = f->staged ? f->stage_T.as<float>() : f->contrib_T.as<float>();
     ba.stage_stride = f->staged ? uint32_t(uint64_t(f->ntx) * f->nty * 256) : 0u;
-    ba.g_density = gd;
-    ba.g_color = gcol;
-    ba.g_normal = gnor;
-    ba.g_priority = gp;
+    ba.g_vox = gvox;
     mark(ctx, kStageBackward);
     launch_composite_backward(f->cam, ba, st);
 
@@ -885,13 +889,25 @@ void backward_impl(svr_ctx* ctx, const svr_scene* scene, svr_frame* f, const svr
     ea.sh_stride = scene->sh_stride;
     for (int i = 0; i < 3; ++i) ea.bc[i] = scene->bounds_center[i];
     ea.bsize = scene->bounds_size;
-    ea.g_color = gcol;
-    ea.g_normal = gnor;
+    ea.g_vox = gvox;
     ea.g_sh = gs;
     ea.g_density = gd;
+    ea.g_priority = gp;
     ea.accumulate = accumulate ? 1 : 0;
+    // When most voxels are outside the view (large scenes, config 5) the
+    // epilogue walks K1's list of visible voxels (an overwriting backward
+    // then clears the SH gradients first); otherwise one pass over every
+    // voxel, which also writes the others' zero SH gradients (config 5:
+    // epilogue 3.35 -> 1.40 ms per step; config 3, 98 % visible: full pass
+    // 0.25 ms vs list 0.31 ms + a 200 MB clear).
+    if (f->training && f->vis_list.p && 2 * f->n_vis_list < N) {
+        ea.list = f->vis_list.as<uint32_t>();
+        ea.n_list = &f->status.as<FrameStatus>()->n_vis_list;
+        if (!accumulate) SVR_CUDA(cudaMemsetAsync(gs, 0, shn * 4, st));
+    }
     mark(ctx, kStageEpilogue);
     launch_voxel_epilogue(f->cam, ea, st);
+    f->gvox_clean = true;
     mark(ctx, -1);
 
     if (!out->on_device) {

@@ -250,7 +250,18 @@ __global__ void __launch_bounds__(kPreThreads, SVR_PRE_MINB) preprocess_kernel(D
             r5 = make_float4(n[0], n[1], n[2], float(1.0 / size));
         }
     }
-    if (a.order) {  // Morton processing order: each thread stores its own record
+    if (a.vis_list) {  // training frames: list the voxels in `pre` for the epilogue
+        const bool in_pre = valid && r0.w > 0.f;
+        const unsigned vm = __ballot_sync(0xffffffffu, in_pre);
+        if (vm) {
+            const int ln = threadIdx.x & 31;
+            unsigned base = 0;
+            if (ln == __ffs(vm) - 1) base = atomicAdd(a.n_vis_list, unsigned(__popc(vm)));
+            base = __shfl_sync(0xffffffffu, base, __ffs(vm) - 1);
+            if (in_pre) a.vis_list[base + __popc(vm & ((1u << ln) - 1u))] = uint32_t(v);
+        }
+    }
+    if (a.order) {  // worklist order: each thread stores its own record
         if (valid && r0.w > 0.f) {
             float4* dst = a.records + v * kRecordF4;
             dst[0] = r0;

@@ -146,6 +146,8 @@ struct svr_frame {
     svrb::DevBuf keys[2], vals[2], dbg_keys, dbg_vals, ranges, tile_order, big;
     svrb::DevBuf pair_counts, big_pairs, rowspan;  // rank-ordered duplicate
     svrb::DevBuf work;                             // K1 worklist (unordered scenes)
+    svrb::DevBuf vis_list;                         // K1's visible voxels (training frames)
+    uint64_t n_vis_list = 0;                       // its length (read with E)
     bool sort_keys_kept = true;  // false: the last sort pass wrote values only
     svrb::DevBuf out_color, out_depth, out_median, out_normal, out_tfin, max_blend;
     svrb::DevBuf ss_color, ss_depth, ss_median, ss_normal, ss_tfin;
@@ -158,7 +160,8 @@ struct svr_frame {
     bool staged = false;                // records live in stage_* ...
     bool compact_valid = false;         // ... and contrib_* is (not yet) built
     svrb::DevBuf taps;  // resampler tables
-    svrb::DevBuf bwd_gc, bwd_gn, bwd_lift, bwd_dcolor, status, l1_grad;
+    svrb::DevBuf bwd_gc, bwd_gn, bwd_lift, bwd_dcolor, status, l1_grad;  // bwd_gc: K9 per-voxel records
+    bool gvox_clean = false;  // bwd_gc all zero (the last backward's epilogue ran)
     int sorted_buf = 0;  // which of keys[]/vals[] holds the sorted list
     int vals_buf = 0;    // which vals[] the compositing kernels read
     bool packed = false; // entries in the packed 64-bit format (PackedFormat)

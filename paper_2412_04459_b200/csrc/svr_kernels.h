@@ -73,7 +73,7 @@ struct FrameStatus {          // device -> host summary, one read per frame
     unsigned int n_big;       // voxels handed to the cooperative duplicate
     unsigned int n_big_ranked;  // the same for the rank-ordered duplicate
     unsigned int n_work;        // K1 worklist length (pre-cull pass)
-    unsigned int pad2;
+    unsigned int n_vis_list;    // K1's list of visible voxels (training frames)
     unsigned long long n_entries_voxel;  // E from the per-voxel scan (parity dumps of the ranked path)
 };
 
@@ -105,6 +105,8 @@ struct PreprocessArgs {
     float4* view_dir;  // optional (training): unit sh_eval direction per visible voxel
     const uint32_t* order;  // optional: voxel worklist (filled by the pre-cull pass, n voxels of room)
     const unsigned int* n_order;  // with order: its live length on the device (zeroed by the caller)
+    uint32_t* vis_list;           // optional: visible voxels appended here (n_vis_list counts them)
+    unsigned int* n_vis_list;
 };
 void launch_preprocess(const DevCamera& cam, const PreprocessArgs& a, cudaStream_t st);
 
@@ -305,10 +307,10 @@ struct BackwardArgs {
     const uint32_t* contrib_entry;  // compact, or staged when stage_stride > 0
     const float* contrib_T;
     uint32_t stage_stride;
-    float* g_density;
-    float* g_color;   // per voxel x3 (scratch)
-    float* g_normal;  // per voxel x3 (scratch)
-    float* g_priority;
+    // per voxel x16 (scratch, all zero on entry): 8 corner densities, colour,
+    // normal, priority; summed with float4 reductions, consumed (and zeroed
+    // again) by the epilogue
+    float* g_vox;
 };
 void launch_composite_backward(const DevCamera& cam, const BackwardArgs& a, cudaStream_t st);
 
@@ -323,11 +325,13 @@ struct EpilogueArgs {
     int sh_degree, sh_stride;
     double bc[3];
     double bsize;
-    const float* g_color;
-    const float* g_normal;
+    float* g_vox;       // K9's per-voxel sums; read and reset to zero here
     float* g_sh;
     float* g_density;
+    float* g_priority;
     int accumulate;
+    const uint32_t* list;         // optional: the voxels in `pre` (K1, training frames), any order
+    const unsigned int* n_list;   // its length on the device; SH gradients of the others untouched
 };
 void launch_voxel_epilogue(const DevCamera& cam, const EpilogueArgs& a, cudaStream_t st);
 
