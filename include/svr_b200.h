@@ -308,6 +308,16 @@ int svr_adam_step(svr_ctx* ctx, float* params, const float* grads, double* m, do
                   uint64_t n, int64_t step, double lr, double lr_alt, uint32_t period,
                   uint32_t n_primary, double beta1, double beta2, double eps, int32_t on_device);
 
+/* Deferred mode (on_device = 2) of svr_ray_losses, svr_image_losses and
+ * svr_adam_step: device pointers, nothing is read back and the host does not
+ * wait, so a whole training iteration is enqueued without a stall. The loss
+ * values of the frame's last svr_image_losses / svr_ray_losses calls are then
+ * read with svr_frame_loss_values (out[5] = mse, 1 - ssim, l_T, l_dist, l_R),
+ * and a NaN gradient seen by any deferred Adam step since the last check is
+ * reported by svr_ctx_take_adam_nan (which clears it). */
+int svr_frame_loss_values(svr_frame* frame, double* out);
+int svr_ctx_take_adam_nan(svr_ctx* ctx, int32_t* nan_seen);
+
 /* L1 photometric loss on the rendered colour (new; pattern of mse_loss,
  * losses.cpp:121-131): L = mean|C-gt|, dL/dC = sign(C-gt)/(3WH). gt is a
  * device pointer (W*H*3 f32); d_color (device, W*H*3) receives the gradient;

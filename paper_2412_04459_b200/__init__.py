@@ -124,7 +124,7 @@ EXPORTS = [
     "svr_project_voxels", "svr_tile_sign_masks", "svr_build_sort_entries", "svr_sort_entries",
     "svr_synth_random_scene", "svr_ring_camera", "svr_free", "svr_launch_count",
     "svr_ctx_enable_timing", "svr_ctx_stage_times", "svr_frame_pre", "svr_render_oracle",
-    "svr_synth_unbounded_scene",
+    "svr_synth_unbounded_scene", "svr_frame_loss_values", "svr_ctx_take_adam_nan",
 ]
 STAGES = ["tile_setup", "preprocess", "scan", "duplicate", "sort", "ranges", "composite",
           "record", "downsample", "backward", "epilogue", "other"]
@@ -167,6 +167,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "svr_frame_create": (C.c_int, [P, C.POINTER(P)]),
         "svr_frame_download_async": (C.c_int, [P, C.c_int, P, C.c_size_t]),
         "svr_image_losses": (C.c_int, [P, P, P, C.c_double, C.c_double, P, P, C.c_int32]),
+        "svr_frame_loss_values": (C.c_int, [P, P]),
+        "svr_ctx_take_adam_nan": (C.c_int, [P, P]),
         "svr_adam_step": (C.c_int, [P, P, P, P, P, C.c_uint64, C.c_int64, C.c_double, C.c_double,
                                     C.c_uint32, C.c_uint32, C.c_double, C.c_double, C.c_double,
                                     C.c_int32]),

@@ -1452,6 +1452,11 @@ int svr_ray_losses(svr_ctx* ctx, svr_frame* f, const float* gt, const svr_ray_lo
         ra.scratch = w->w_dist != 0.0 ? grow<float2>(f->rl_scratch, std::max<uint64_t>(C, 1)) : nullptr;
         ra.sums = sums;
         launch_ray_losses(f->cam, ra, st);
+        f->rl_w[0] = w->w_T;
+        f->rl_w[1] = w->w_dist;
+        f->rl_w[2] = w->w_R;
+        f->rl_pending = true;
+        if (on_device == 2) return;  // deferred: values via svr_frame_loss_values
         double hs[3];
         SVR_CUDA(cudaMemcpyAsync(hs, sums, sizeof(hs), cudaMemcpyDeviceToHost, st));
         if (!on_device) {
@@ -1513,6 +1518,10 @@ int svr_image_losses(svr_ctx* ctx, svr_frame* f, const float* gt, double w_mse, 
         a.sums = grow<double>(f->il_sums, 2);
         SVR_CUDA(cudaMemsetAsync(a.sums, 0, 16, st));
         launch_image_losses(a, st);
+        f->il_norm[0] = double(n);
+        f->il_norm[1] = double(wv * (f->H - 10) * 3);
+        f->il_pending = true;
+        if (on_device == 2) return;  // deferred: values via svr_frame_loss_values
         double hs[2];
         SVR_CUDA(cudaMemcpyAsync(hs, a.sums, 16, cudaMemcpyDeviceToHost, st));
         if (!on_device && d_color)
@@ -1520,6 +1529,38 @@ int svr_image_losses(svr_ctx* ctx, svr_frame* f, const float* gt, double w_mse, 
         SVR_CUDA(cudaStreamSynchronize(st));
         out[0] = hs[0] / double(n);
         out[1] = 1.0 - hs[1] / double(wv * (f->H - 10) * 3);
+    });
+}
+
+int svr_frame_loss_values(svr_frame* f, double* out) {
+    return guard([&] {
+        require(f && out && f->ctx, SVR_ERR_INVALID_ARGUMENT, "null argument");
+        set_device(f->ctx);
+        cudaStream_t st = f->ctx->stream;
+        double il[2] = {0.0, 0.0}, rl[3] = {0.0, 0.0, 0.0};
+        if (f->il_pending) SVR_CUDA(cudaMemcpyAsync(il, f->il_sums.p, 16, cudaMemcpyDeviceToHost, st));
+        if (f->rl_pending) SVR_CUDA(cudaMemcpyAsync(rl, f->rl_sums.p, 24, cudaMemcpyDeviceToHost, st));
+        SVR_CUDA(cudaStreamSynchronize(st));
+        out[0] = f->il_pending ? il[0] / f->il_norm[0] : 0.0;
+        out[1] = f->il_pending ? 1.0 - il[1] / f->il_norm[1] : 0.0;
+        out[2] = (f->rl_pending && f->rl_w[0] != 0.0) ? rl[0] : 0.0;
+        out[3] = (f->rl_pending && f->rl_w[1] != 0.0) ? rl[1] : 0.0;
+        out[4] = (f->rl_pending && f->rl_w[2] != 0.0) ? rl[2] : 0.0;
+    });
+}
+
+int svr_ctx_take_adam_nan(svr_ctx* ctx, int32_t* nan_seen) {
+    return guard([&] {
+        require(ctx && nan_seen, SVR_ERR_INVALID_ARGUMENT, "null argument");
+        set_device(ctx);
+        cudaStream_t st = ctx->stream;
+        unsigned int h = 0;
+        if (ctx->adam_flag.p) {
+            SVR_CUDA(cudaMemcpyAsync(&h, ctx->adam_flag.p, 4, cudaMemcpyDeviceToHost, st));
+            SVR_CUDA(cudaMemsetAsync(ctx->adam_flag.p, 0, 4, st));
+        }
+        SVR_CUDA(cudaStreamSynchronize(st));
+        *nan_seen = h != 0;
     });
 }
 
@@ -1560,12 +1601,21 @@ int svr_adam_step(svr_ctx* ctx, float* params, const float* grads, double* m, do
             SVR_CUDA(cudaMemcpyAsync(a.v, v, n * 8, cudaMemcpyHostToDevice, st));
             a.grads = g;
         }
-        unsigned int* flag = grow<unsigned int>(ctx->adam_flag, 1);
-        SVR_CUDA(cudaMemsetAsync(flag, 0, 4, st));
+        if (!ctx->adam_flag.p) {
+            grow<unsigned int>(ctx->adam_flag, 1);
+            SVR_CUDA(cudaMemsetAsync(ctx->adam_flag.p, 0, 4, st));
+        }
+        unsigned int* flag = ctx->adam_flag.as<unsigned int>();
         a.nan_flag = flag;
+        if (on_device == 2) {  // deferred: the flag stays set until svr_ctx_take_adam_nan
+            launch_adam(a, st);
+            return;
+        }
+        SVR_CUDA(cudaMemsetAsync(flag, 0, 4, st));
         launch_adam(a, st);
         unsigned int hflag = 0;
         SVR_CUDA(cudaMemcpyAsync(&hflag, flag, 4, cudaMemcpyDeviceToHost, st));
+        SVR_CUDA(cudaMemsetAsync(flag, 0, 4, st));  // reported here: not left for svr_ctx_take_adam_nan
         if (!on_device && n) {
             SVR_CUDA(cudaMemcpyAsync(params, a.params, n * 4, cudaMemcpyDeviceToHost, st));
             SVR_CUDA(cudaMemcpyAsync(m, a.m, n * 8, cudaMemcpyDeviceToHost, st));

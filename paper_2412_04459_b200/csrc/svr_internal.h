@@ -155,6 +155,9 @@ struct svr_frame {
     svrb::DevBuf stage_entry, stage_T;  // single-pass training records
     svrb::DevBuf view_dir;              // training: K1's sh_eval directions
     svrb::DevBuf rl_sums, rl_scratch;   // svr_ray_losses
+    double rl_w[3] = {0.0, 0.0, 0.0};   // weights of the last ray-loss call (value masking)
+    double il_norm[2] = {1.0, 1.0};     // normalisers of the last image-loss call
+    bool rl_pending = false, il_pending = false;
     svrb::DevBuf il_mid, il_maps, il_adj, il_sums;  // svr_image_losses
     uint32_t stage_cap = 64;            // per-pixel capacity, doubles on overflow
     bool staged = false;                // records live in stage_* ...

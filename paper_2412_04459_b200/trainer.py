@@ -65,9 +65,10 @@ class DeviceTrainer:
             self._bufs[name] = b
         return b[:max(n, 1)]
 
-    def gradients(self, cam, gt_device, with_dist: bool = True) -> dict:
+    def gradients(self, cam, gt_device, with_dist: bool = True, defer: bool = False) -> dict:
         """Forward + all losses + backward; fills g_density / g_sh / g_priority.
-        Returns the loss values (TrainLogEntry fields)."""
+        Returns the loss values (TrainLogEntry fields); with defer the losses
+        stay on the device (read them with loss_values()) and nothing waits."""
         svr, lib, ctx, f = self.svr, self.ctx._lib, self.ctx, self.frame
         svr.render_into(f, self.scene, cam, self.opts)
         inf = f.info()
@@ -77,19 +78,20 @@ class DeviceTrainer:
         d_tfin = self._buf("d_tfin", nss)
         d_weight = self._buf("d_weight", nc)
         d_vc = self._buf("d_vc", nc * 3)
-        for b in (d_color, d_tfin, d_weight, d_vc):
-            b.zero_()
-        ctx_stream_sync(self)
+        with self._on_stream():  # cleared on the library stream: no host wait
+            for b in (d_color, d_tfin, d_weight, d_vc):
+                b.zero_()
+        mode = 2 if defer else 1
         img = (C.c_double * 2)()
         svr._check(lib.svr_image_losses(ctx.h, f.h, C.c_void_p(gt_device.data_ptr()), 1.0,
-                                        self.w.lambda_ssim, img, C.c_void_p(d_color.data_ptr()), 1))
+                                        self.w.lambda_ssim, img, C.c_void_p(d_color.data_ptr()), mode))
         rw = svr.svr_ray_loss_weights(self.w.lambda_T, self.w.lambda_dist if with_dist else 0.0,
                                       self.w.lambda_R)
         rv = svr.svr_ray_loss_values()
         svr._check(lib.svr_ray_losses(ctx.h, f.h, C.c_void_p(gt_device.data_ptr()), C.byref(rw),
                                       C.byref(rv), C.c_void_p(d_tfin.data_ptr()),
                                       C.c_void_p(d_weight.data_ptr()), C.c_void_p(d_vc.data_ptr()),
-                                      1))
+                                      mode))
         u = svr.svr_upstream()
         u.d_color, u.d_tfin_ss = d_color.data_ptr(), d_tfin.data_ptr()
         u.d_weight, u.d_voxel_color = d_weight.data_ptr(), d_vc.data_ptr()
@@ -99,13 +101,23 @@ class DeviceTrainer:
                                        self.g_priority.data_ptr())
         g.on_device = 1
         svr._check(lib.svr_render_backward(ctx.h, self.scene.h, f.h, C.byref(u), C.byref(g)))
+        if defer:
+            return {}
         return {"l_mse": img[0], "l_ssim": img[1], "l_T": rv.l_T, "l_dist": rv.l_dist,
                 "l_R": rv.l_R}
 
+    def loss_values(self) -> dict:
+        """The frame's last loss values (one host wait)."""
+        out = (C.c_double * 5)()
+        self.svr._check(self.ctx._lib.svr_frame_loss_values(self.frame.h, out))
+        return {"l_mse": out[0], "l_ssim": out[1], "l_T": out[2], "l_dist": out[3], "l_R": out[4]}
+
     def step(self, cam, gt_device, with_dist: bool = True, lr_decay: float = 1.0) -> dict:
-        """One training iteration (optim.cpp:433-495 minus adaptation)."""
+        """One training iteration (optim.cpp:433-495 minus adaptation). The
+        whole iteration is enqueued without a host wait; the loss values and
+        Adam's NaN check are read once at the end."""
         svr, lib, ctx, w = self.svr, self.ctx._lib, self.ctx, self.w
-        log = self.gradients(cam, gt_device, with_dist)
+        self.gradients(cam, gt_device, with_dist, defer=True)
         with self._on_stream():
             self.priority += self.g_priority
         self.step_count += 1
@@ -113,12 +125,17 @@ class DeviceTrainer:
                                      C.c_void_p(self.g_density.data_ptr()),
                                      C.c_void_p(self.m_d.data_ptr()), C.c_void_p(self.v_d.data_ptr()),
                                      self.n_pool, self.step_count, w.lr_density * lr_decay, 0.0, 0, 0,
-                                     w.adam_beta1, w.adam_beta2, w.adam_eps, 1))
+                                     w.adam_beta1, w.adam_beta2, w.adam_eps, 2))
         svr._check(lib.svr_adam_step(ctx.h, C.c_void_p(self.s_ptr), C.c_void_p(self.g_sh.data_ptr()),
                                      C.c_void_p(self.m_s.data_ptr()), C.c_void_p(self.v_s.data_ptr()),
                                      self.n_sh, self.step_count, w.lr_sh0 * lr_decay,
                                      w.lr_sh_rest * lr_decay, self.stride, 3, w.adam_beta1,
-                                     w.adam_beta2, w.adam_eps, 1))
+                                     w.adam_beta2, w.adam_eps, 2))
+        log = self.loss_values()
+        nan = C.c_int32()
+        svr._check(lib.svr_ctx_take_adam_nan(ctx.h, C.byref(nan)))
+        if nan.value:
+            raise RuntimeError("adam_step: NaN gradient")  # optim.cpp:337-338 (std::runtime_error)
         rw_dist = w.lambda_dist if with_dist else 0.0
         log["total"] = (log["l_mse"] + w.lambda_ssim * log["l_ssim"] + w.lambda_T * log["l_T"] +
                         rw_dist * log["l_dist"] + w.lambda_R * log["l_R"])
@@ -133,12 +150,6 @@ class DeviceTrainer:
         self.ctx.synchronize()
         return [device_to_host(ptr, n) for ptr, n in ((self.d_ptr, self.n_pool),
                                                       (self.s_ptr, self.n_sh))]
-
-
-def ctx_stream_sync(tr: DeviceTrainer) -> None:
-    """Order torch's zero_() calls (current stream) before the library stream."""
-    import torch
-    torch.cuda.current_stream(tr.dev).synchronize()
 
 
 class _DevArray:

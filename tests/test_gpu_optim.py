@@ -39,3 +39,34 @@ def test_adam_nan_gradient_raises(svr, ctx):
     g[37] = float("nan")
     with pytest.raises(RuntimeError):
         svr.adam_step(ctx, params, g, svr.AdamState(100), 0.01)
+
+
+def test_adam_deferred_nan_check(svr, ctx):
+    """Deferred Adam (on_device = 2) returns at once; a NaN gradient is
+    reported (and cleared) by svr_ctx_take_adam_nan."""
+    import ctypes as C
+    import torch
+    dev = torch.device("cuda", 0)
+    lib = ctx._lib
+    params = torch.zeros(100, device=dev)
+    m = torch.zeros(100, dtype=torch.float64, device=dev)
+    v = torch.zeros(100, dtype=torch.float64, device=dev)
+    g = torch.zeros(100, device=dev)
+    torch.cuda.synchronize()
+    nan = C.c_int32()
+
+    def step(grad):
+        svr._check(lib.svr_adam_step(ctx.h, C.c_void_p(params.data_ptr()), C.c_void_p(grad.data_ptr()),
+                                     C.c_void_p(m.data_ptr()), C.c_void_p(v.data_ptr()), 100, 1, 0.01,
+                                     0.0, 0, 0, 0.1, 0.99, 1e-15, 2))
+
+    step(g)
+    svr._check(lib.svr_ctx_take_adam_nan(ctx.h, C.byref(nan)))
+    assert nan.value == 0
+    g[37] = float("nan")
+    torch.cuda.synchronize()
+    step(g)
+    svr._check(lib.svr_ctx_take_adam_nan(ctx.h, C.byref(nan)))
+    assert nan.value == 1
+    svr._check(lib.svr_ctx_take_adam_nan(ctx.h, C.byref(nan)))
+    assert nan.value == 0

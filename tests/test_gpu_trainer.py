@@ -50,3 +50,22 @@ def test_train_steps_update_pools_and_lower_loss(svr, ctx):
     assert not np.array_equal(d0, d1) and not np.array_equal(s0, s1)
     assert logs[-1]["l_mse"] < 0.8 * logs[0]["l_mse"]
     assert float(tr.priority.sum()) > 0
+
+
+def test_deferred_losses_match_immediate(svr, ctx):
+    """Deferred mode (on_device = 2): the loss values read once with
+    svr_frame_loss_values equal the immediately returned ones."""
+    import torch
+    from paper_2412_04459_b200.trainer import DeviceTrainer, TrainWeights
+    arrays = svr.synth_random_scene(77, 20000, 7, 3)
+    scene = svr.Scene(ctx, arrays)
+    cam = svr.ring_camera(2, 1, 96, 80)
+    gt = torch.tensor(np.random.default_rng(3).uniform(0, 1, (80, 96, 3)), dtype=torch.float32,
+                      device="cuda")
+    tr = DeviceTrainer(svr, ctx, scene, svr.RenderOptions(K=1, supersample=1.0),
+                       TrainWeights(lambda_T=0.05, lambda_dist=0.2, lambda_R=0.03))
+    now = tr.gradients(cam, gt)
+    assert tr.gradients(cam, gt, defer=True) == {}
+    later = tr.loss_values()
+    for k, v in now.items():  # the block sums meet in double atomics: order-dependent last bits
+        assert later[k] == pytest.approx(v, rel=1e-9, abs=1e-15), k
