@@ -469,11 +469,28 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
                 SVR_CUDA(cudaMemcpyAsync(f->dbg_keys.p, dk, E * 8, cudaMemcpyDeviceToDevice, st));
             }
         }
+        // ranked, large E: K4 counts the (at most two) tile digits of the sort
+        // and the sort skips its histogram read of the keys (config 4, 97M
+        // entries: sort + duplicate 2.29 -> 2.10 ms). At config-2 sizes the
+        // shared-memory atomics cost what the read saves, so the separate
+        // histogram kernel stays.
+        const char* fh_env = std::getenv("SVR_FUSED_HIST_MIN");  // parity tests lower it
+        const uint64_t fh_min = fh_env ? std::strtoull(fh_env, nullptr, 10) : (uint64_t(1) << 24);
+        const bool fused_hist = ranked && np >= 1 && np <= 2 && E > 1 && E >= fh_min;
+        TileDigits td{};
+        if (fused_hist) {
+            sort_prepare(ctx->scratch2.p, E, np, st);
+            td.hist = sort_hist_ptr(ctx->scratch2.p);
+            td.b0 = passes[0].bits;
+            td.m0 = (1u << passes[0].bits) - 1u;
+            td.two = np == 2;
+            td.m1 = np == 2 ? (1u << passes[1].bits) - 1u : 0u;
+        }
         if (ranked)
             launch_duplicate_ranked(cam, N, pc, pair_partial, scene->morton_order.as<uint32_t>(), pa.rects,
                                     masks, sat, rowspan, f->fmt, f->keys[0].as<uint64_t>(), E,
                                     grow<uint2>(f->big_pairs, E / kRankedBigMin + 1),
-                                    &status->n_big_ranked, st);
+                                    &status->n_big_ranked, st, td);
         mark(ctx, kStageSort);
         const unsigned long long* n_dev = deferred ? &status->n_entries : nullptr;
         // Ranked emission outside debug mode: the last pass writes the values
@@ -483,11 +500,11 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
         if (!f->sort_keys_kept) {
             SortFinish fin{f->vals[0].as<uint32_t>(), ranges, f->fmt.vb, f->fmt.tile_shift, ntiles};
             f->sorted_buf = radix_sort_keys(f->keys[0].as<uint64_t>(), f->keys[1].as<uint64_t>(), E, passes,
-                                            np, ctx->scratch2.p, st, false, n_dev, &fin);
+                                            np, ctx->scratch2.p, st, fused_hist, n_dev, &fin);
             mark(ctx, kStageRanges);
         } else {
             f->sorted_buf = radix_sort_keys(f->keys[0].as<uint64_t>(), f->keys[1].as<uint64_t>(), E,
-                                            passes, np, ctx->scratch2.p, st, false, n_dev);
+                                            passes, np, ctx->scratch2.p, st, fused_hist, n_dev);
             mark(ctx, kStageRanges);
             launch_tile_ranges_packed(f->keys[f->sorted_buf].as<uint64_t>(), E, f->fmt, ranges,
                                       f->vals[0].as<uint32_t>(), ntiles, st, n_dev);

@@ -483,9 +483,11 @@ __global__ void __launch_bounds__(kScanThreads) duplicate_ranked_kernel(
     DevCamera cam, uint64_t m, const uint32_t* __restrict__ pc, const uint32_t* __restrict__ partial,
     const uint32_t* __restrict__ order, const int4* __restrict__ rects, const uint8_t* __restrict__ masks,
     const int2* __restrict__ rowspan, PackedFormat fmt, uint64_t* __restrict__ keys, uint64_t cap, uint2* big,
-    unsigned int* n_big) {
+    unsigned int* n_big, TileDigits td) {
     pdl_enter();
     __shared__ uint32_t s_warp[kScanThreads / 32 + 1];
+    __shared__ uint32_t s_h[2][256];  // the sort's two tile-digit histograms
+    if (td.hist) s_h[threadIdx.x >> 8][threadIdx.x & 255] = 0;
     const uint64_t i0 = uint64_t(blockIdx.x) * kScanChunk + uint64_t(threadIdx.x) * 8;
     uint32_t x[8];
     if (i0 + 8 <= m) {
@@ -520,9 +522,8 @@ __global__ void __launch_bounds__(kScanThreads) duplicate_ranked_kernel(
         if (lane < kScanThreads / 32) s_warp[lane] = wi - w;
     }
     __syncthreads();
-    if (sum == 0) return;
     uint64_t o = uint64_t(partial[blockIdx.x]) + s_warp[warp] + incl - sum;
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < 8 && sum; ++k) {
         const uint32_t cnt = x[k];
         if (cnt == 0) continue;
         if (o + cnt <= cap) {  // else: deferred-E frame that outgrew its buffers (flagged)
@@ -539,18 +540,38 @@ __global__ void __launch_bounds__(kScanThreads) duplicate_ranked_kernel(
                     const int2 sp = __ldg(rowspan + s * cam.nty + ty);
                     if (sp.x >= 0) {  // one run: no mask reads
                         const int a = max(sp.x, rc.x), e = min(sp.y, rc.y);
-                        for (int tx = a; tx <= e; ++tx)
-                            keys[at++] = ranked_key(fmt, uint64_t(ty) * cam.ntx + tx, r, s, v);
+                        for (int tx = a; tx <= e; ++tx) {
+                            const uint32_t t = uint32_t(ty) * cam.ntx + tx;
+                            keys[at++] = ranked_key(fmt, t, r, s, v);
+                            if (td.hist) atomicAdd(&s_h[0][t & td.m0], 1u);
+                        }
+                        if (td.hist && td.two && e >= a)  // high digit: one add per 2^b0-aligned segment
+                            for (uint32_t t = uint32_t(ty) * cam.ntx + a, t1 = uint32_t(ty) * cam.ntx + e; t <= t1;) {
+                                const uint32_t seg_end = min(t1, (((t >> td.b0) + 1) << td.b0) - 1);
+                                atomicAdd(&s_h[1][(t >> td.b0) & td.m1], seg_end - t + 1);
+                                t = seg_end + 1;
+                            }
                     } else {
                         for (int tx = rc.x; tx <= rc.y; ++tx) {
-                            const uint64_t tid = uint64_t(ty) * cam.ntx + tx;
-                            if ((__ldg(masks + tid) >> s) & 1u) keys[at++] = ranked_key(fmt, tid, r, s, v);
+                            const uint32_t t = uint32_t(ty) * cam.ntx + tx;
+                            if ((__ldg(masks + t) >> s) & 1u) {
+                                keys[at++] = ranked_key(fmt, t, r, s, v);
+                                if (td.hist) {
+                                    atomicAdd(&s_h[0][t & td.m0], 1u);
+                                    if (td.two) atomicAdd(&s_h[1][(t >> td.b0) & td.m1], 1u);
+                                }
+                            }
                         }
                     }
                 }
             }
         }
         o += cnt;
+    }
+    if (td.hist) {  // the CTA's counts into the sort's global histograms
+        __syncthreads();
+        const uint32_t c = s_h[threadIdx.x >> 8][threadIdx.x & 255];
+        if (c) atomicAdd(td.hist + threadIdx.x, c);
     }
 }
 
@@ -563,8 +584,14 @@ __global__ void __launch_bounds__(256) duplicate_big_ranked_kernel(
     DevCamera cam, const uint32_t* __restrict__ order, const int4* __restrict__ rects,
     const uint8_t* __restrict__ masks, const uint32_t* __restrict__ sat, const int2* __restrict__ rowspan,
     PackedFormat fmt, uint64_t* __restrict__ keys, const uint2* __restrict__ big,
-    const unsigned int* __restrict__ n_big) {
+    const unsigned int* __restrict__ n_big, TileDigits td) {
     pdl_enter();
+    __shared__ uint32_t s_h[2][256];
+    if (td.hist) {
+        s_h[0][threadIdx.x] = 0;
+        s_h[1][threadIdx.x] = 0;
+        __syncthreads();
+    }
     const int lane = threadIdx.x & 31;
     const uint32_t nb = *n_big;
     const int ncell = (cam.ntx + 1) * (cam.nty + 1);
@@ -609,8 +636,16 @@ __global__ void __launch_bounds__(256) duplicate_big_ranked_kernel(
                         if (__shfl_sync(0xffffffffu, incl, j + step - 1) <= q) j += step;
                     const int lj = __shfl_sync(0xffffffffu, len, j), aj = __shfl_sync(0xffffffffu, a, j);
                     const int ij = __shfl_sync(0xffffffffu, incl, j);
-                    if (q < total)
-                        keys[at + q] = ranked_key(fmt, uint64_t(ty0 + j) * cam.ntx + aj + (q - (ij - lj)), e.x, s, v);
+                    const uint32_t t = uint32_t(ty0 + j) * cam.ntx + aj + (q - (ij - lj));
+                    if (q < total) {
+                        keys[at + q] = ranked_key(fmt, t, e.x, s, v);
+                        if (td.hist) atomicAdd(&s_h[0][t & td.m0], 1u);
+                    }
+                    if (td.hist && td.two) {  // high digit: lanes sharing it add once
+                        const uint32_t d1 = q < total ? (t >> td.b0) & td.m1 : 0xffffffffu;
+                        const unsigned pm = __match_any_sync(0xffffffffu, d1);
+                        if (q < total && lane == __ffs(pm) - 1) atomicAdd(&s_h[1][d1], uint32_t(__popc(pm)));
+                    }
                 }
                 at += uint64_t(total);
                 continue;
@@ -630,13 +665,25 @@ __global__ void __launch_bounds__(256) duplicate_big_ranked_kernel(
                         const int tx = tx0 + lane;
                         const bool hit = tx <= rc.y && ((__ldg(masks + trow + tx) >> s) & 1u);
                         const unsigned bal = __ballot_sync(0xffffffffu, hit);
-                        if (hit) keys[w + __popc(bal & ((1u << lane) - 1u))] = ranked_key(fmt, trow + tx, e.x, s, v);
+                        if (hit) {
+                            keys[w + __popc(bal & ((1u << lane) - 1u))] = ranked_key(fmt, trow + tx, e.x, s, v);
+                            if (td.hist) {
+                                const uint32_t t = uint32_t(trow + tx);
+                                atomicAdd(&s_h[0][t & td.m0], 1u);
+                                if (td.two) atomicAdd(&s_h[1][(t >> td.b0) & td.m1], 1u);
+                            }
+                        }
                         w += __popc(bal);
                     }
                 }
             }
             at += uint64_t(total);
         }
+    }
+    if (td.hist) {
+        __syncthreads();
+        if (s_h[0][threadIdx.x]) atomicAdd(td.hist + threadIdx.x, s_h[0][threadIdx.x]);
+        if (s_h[1][threadIdx.x]) atomicAdd(td.hist + 256 + threadIdx.x, s_h[1][threadIdx.x]);
     }
 }
 
@@ -1250,14 +1297,14 @@ void launch_duplicate_ranked(const DevCamera& cam, uint64_t n, const uint32_t* p
                              const uint32_t* partial, const uint32_t* order, const int4* rects,
                              const uint8_t* masks, const uint32_t* sat, const int2* rowspan,
                              PackedFormat fmt, uint64_t* keys, uint64_t cap, uint2* big,
-                             unsigned int* n_big, cudaStream_t st) {
+                             unsigned int* n_big, cudaStream_t st, TileDigits td) {
     if (n == 0) return;
     const uint64_t m = 8 * n;
     launch_pdl(duplicate_ranked_kernel, unsigned((m + kScanChunk - 1) / kScanChunk), kScanThreads, 0, st, cam,
-               m, pc, partial, order, rects, masks, rowspan, fmt, keys, cap, big, n_big);
+               m, pc, partial, order, rects, masks, rowspan, fmt, keys, cap, big, n_big, td);
     SVR_LAUNCH("duplicate_ranked_kernel");
     launch_pdl(duplicate_big_ranked_kernel, 148 * 8, 256, 0, st, cam, order, rects, masks, sat, rowspan, fmt,
-               keys, big, n_big);
+               keys, big, n_big, td);
     SVR_LAUNCH("duplicate_big_ranked_kernel");
 }
 

@@ -153,11 +153,21 @@ void launch_pair_counts(const DevCamera& cam, uint64_t n, const uint32_t* counts
 #define SVR_RBIG 128
 #endif
 constexpr uint32_t kRankedBigMin = SVR_RBIG;  // pairs with more entries: one warp each
+// Optional: K4 also counts the tile-only sort's digit histograms (the keys'
+// tile id t: digit 0 = t & m0, digit 1 = (t >> b0) & m1 when two) into
+// hist[2][256] (sort_hist_ptr, after sort_prepare), so the sort skips its
+// histogram read of the keys.
+struct TileDigits {
+    uint32_t* hist;
+    uint32_t m0, m1;
+    int b0;
+    int two;
+};
 void launch_duplicate_ranked(const DevCamera& cam, uint64_t n, const uint32_t* pc,
                              const uint32_t* partial, const uint32_t* order, const int4* rects,
                              const uint8_t* masks, const uint32_t* sat, const int2* rowspan,
                              PackedFormat fmt, uint64_t* keys, uint64_t cap, uint2* big,
-                             unsigned int* n_big, cudaStream_t st);
+                             unsigned int* n_big, cudaStream_t st, TileDigits td = TileDigits{});
 // Tile ranges from packed sorted keys; also writes the reference value
 // (s << 29 | vid) per entry for the compositing kernels.
 void launch_tile_ranges_packed(const uint64_t* keys, uint64_t n, PackedFormat fmt, uint2* ranges,

@@ -144,6 +144,35 @@ def test_entries_sort_ranges_bit_exact(svr, ctx, ref, cfg1, ss):
     assert np.all(ranges[~nonempty, 0] == ranges[~nonempty, 1])
 
 
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_fused_digit_histograms_bit_exact(svr, ctx, ref, cfg1, monkeypatch, fused):
+    """The sort's digit histograms counted in K4 (large-E path, forced here)
+    give the same sorted values, ranges and image as the histogram kernel."""
+    monkeypatch.setenv("SVR_FUSED_HIST_MIN", "0" if fused == "1" else str(1 << 62))
+    arrays, _, rscene = cfg1
+    fast = svr.Context(0)
+    scene_fast = svr.Scene(fast, arrays)
+    for cam in [svr.ring_camera(3, 1, 320, 192), svr.ring_camera(5, 2, 100, 90),
+                svr.Camera(96, 80, 40.0, 40.0, 47.5, 39.5, np.eye(3), np.array([0.02, 0.01, -0.04]))]:
+        f = svr.Frame(fast)
+        svr.render_into(f, scene_fast, cam, svr.RenderOptions(supersample=1.0))
+        ks_ref, vs_ref = ref.ref_entries(rscene, cam, sorted_=True)
+        assert np.array_equal(f.download("SORT_VALUES", np.uint32), vs_ref)
+        ranges = f.download("TILE_RANGES", np.uint32, (-1, 2))
+        tiles = (ks_ref >> np.uint64(48)).astype(np.int64)
+        t = np.arange(ranges.shape[0])
+        lo, hi = np.searchsorted(tiles, t, "left"), np.searchsorted(tiles, t, "right")
+        ne = hi > lo
+        assert np.array_equal(ranges[ne, 0], lo[ne]) and np.array_equal(ranges[ne, 1], hi[ne])
+        assert np.all(ranges[~ne, 0] == ranges[~ne, 1])
+    # the big-pair kernel's histogram path: a camera inside a dense scene
+    cam = svr.Camera(160, 128, 50.0, 50.0, 80.5, 64.5, np.eye(3), np.array([0.0, 0.0, 0.0]))
+    f = svr.Frame(fast)
+    svr.render_into(f, scene_fast, cam, svr.RenderOptions(supersample=1.0))
+    ks_ref, vs_ref = ref.ref_entries(rscene, cam, sorted_=True)
+    assert np.array_equal(f.download("SORT_VALUES", np.uint32), vs_ref)
+
+
 @pytest.mark.parametrize("ranked", ["1", "0"])
 def test_emission_paths_bit_exact(svr, ctx, ref, cfg1, monkeypatch, ranked):
     """Rank-ordered emission (keys pre-sorted below the tile bits, tile-only
@@ -179,8 +208,10 @@ def test_value_only_final_pass_matches_debug_path(svr, ctx, ref, cfg1):
         ranges = f.download("TILE_RANGES", np.uint32, (-1, 2))
         tiles = (ks_ref >> np.uint64(48)).astype(np.int64)
         t = np.arange(ranges.shape[0])
-        assert np.array_equal(ranges[:, 0], np.searchsorted(tiles, t, "left"))
-        assert np.array_equal(ranges[:, 1], np.searchsorted(tiles, t, "right"))
+        lo, hi = np.searchsorted(tiles, t, "left"), np.searchsorted(tiles, t, "right")
+        ne = hi > lo
+        assert np.array_equal(ranges[ne, 0], lo[ne]) and np.array_equal(ranges[ne, 1], hi[ne])
+        assert np.all(ranges[~ne, 0] == ranges[~ne, 1])
         out = svr.render(scene_fast, cam, svr.RenderOptions(supersample=1.0))
         compare_outputs(out, ref.ref_render(rscene, cam, svr.RenderOptions(supersample=1.0)))
 
