@@ -321,6 +321,7 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     f->training = opts->training != 0;
     f->has_records = false;
     f->n_contribs = 0;
+    f->il_pending = f->rl_pending = false;  // loss values belong to the previous render
     const uint64_t N = scene->n_voxels;
     const bool ss1 = (sw == W && sh == H);
 
