@@ -854,8 +854,12 @@ __device__ __forceinline__ void slab(float4 lo, float ix, float iy, float iz, fl
 constexpr int kCompWarps = 8;
 constexpr size_t kCompSmem = size_t(2) * kCompWarps * 32 * kRecordF4 * sizeof(float4);
 
-template <int K, bool RECORD>
+// MODE 0: plain render; 1: record pass (RECORD); 2: render with per-voxel
+// max-blend stats and/or staged training records (their checks compiled in).
+template <int K, int MODE>
 __global__ void __launch_bounds__(256, 4) composite_kernel(DevCamera cam, CompositeArgs a) {
+    constexpr bool RECORD = MODE == 1;
+    constexpr bool EXTRA = MODE == 2;
     pdl_enter();
     extern __shared__ float4 s_rec_dyn[];  // [2][8 warps][32 slots][kRecordF4]
     __shared__ uint32_t s_vid[2][kCompWarps][32];
@@ -1035,8 +1039,8 @@ __global__ void __launch_bounds__(256, 4) composite_kernel(DevCamera cam, Compos
                 ny += w * nor.y;
                 nz += w * nor.z;
                 depth += T * dv;
-                if (a.max_blend) atomicMax(a.max_blend + __float_as_uint(col.w), __float_as_uint(w));
-                if (a.stage_entry) {
+                if (EXTRA && a.max_blend) atomicMax(a.max_blend + __float_as_uint(col.w), __float_as_uint(w));
+                if (EXTRA && a.stage_entry) {
                     if (cnt < a.stage_cap) {
                         const uint32_t at = cnt * a.stage_stride + slot;
                         a.stage_entry[at] = entry;
@@ -1383,17 +1387,21 @@ void launch_composite(const DevCamera& cam, const CompositeArgs& a, bool record_
     const unsigned ntiles = unsigned(cam.ntx * cam.nty);
     static bool attr_set = false;
     if (!attr_set) {
-        for (auto fn : {composite_kernel<1, false>, composite_kernel<1, true>, composite_kernel<2, false>,
-                        composite_kernel<2, true>, composite_kernel<3, false>, composite_kernel<3, true>})
+        for (auto fn : {composite_kernel<1, 0>, composite_kernel<1, 1>, composite_kernel<1, 2>,
+                        composite_kernel<2, 0>, composite_kernel<2, 1>, composite_kernel<2, 2>,
+                        composite_kernel<3, 0>, composite_kernel<3, 1>, composite_kernel<3, 2>})
             SVR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCompSmem)));
         attr_set = true;
     }
-#define SVR_COMPOSITE_CASE(KK)                                                        \
-    case KK:                                                                          \
-        if (record_pass)                                                              \
-            launch_pdl(composite_kernel<KK, true>, ntiles, 256, kCompSmem, st, cam, a); \
-        else                                                                          \
-            launch_pdl(composite_kernel<KK, false>, ntiles, 256, kCompSmem, st, cam, a); \
+    const int mode = record_pass ? 1 : ((a.max_blend || a.stage_entry) ? 2 : 0);
+#define SVR_COMPOSITE_CASE(KK)                                                          \
+    case KK:                                                                            \
+        if (mode == 1)                                                                  \
+            launch_pdl(composite_kernel<KK, 1>, ntiles, 256, kCompSmem, st, cam, a);    \
+        else if (mode == 2)                                                             \
+            launch_pdl(composite_kernel<KK, 2>, ntiles, 256, kCompSmem, st, cam, a);    \
+        else                                                                            \
+            launch_pdl(composite_kernel<KK, 0>, ntiles, 256, kCompSmem, st, cam, a);    \
         break;
     switch (a.K) {
         SVR_COMPOSITE_CASE(1)
