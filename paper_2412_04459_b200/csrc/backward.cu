@@ -97,7 +97,9 @@ __device__ __forceinline__ float warp_transpose_sum16(float (&v)[16], int lane) 
 #ifndef SVR_BWD_DIRECT
 #define SVR_BWD_DIRECT 4  // at most this many hit lanes: per-lane atomics instead of a reduction
 #endif
-template <int K>
+// UPC: per-contribution upstream gradients (d_weight / d_voxel_color, the
+// ray losses) present; without them the hit loop carries no checks for them.
+template <int K, bool UPC>
 __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, BackwardArgs a) {
     pdl_enter();
     __shared__ float4 s_rec[8][32][kRecordF4];
@@ -223,7 +225,7 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
                 }
                 const float Ti = T1;
                 const float4 col = wrec[sl][4], nor = wrec[sl][5];
-                const float gw = a.d_weight ? a.d_weight[base + kidx] : 0.f;
+                const float gw = (UPC && a.d_weight) ? a.d_weight[base + kidx] : 0.f;
                 const float phi = gC[0] * col.x + gC[1] * col.y + gC[2] * col.z + gN[0] * nor.x +
                                   gN[1] * nor.y + gN[2] * nor.z + gw;
                 const float A = Ti * (phi - Ra - Rd);  // dL/dalpha_i (raster.cpp:383)
@@ -257,7 +259,7 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
                 acc[8] = wgt * gC[0];
                 acc[9] = wgt * gC[1];
                 acc[10] = wgt * gC[2];
-                if (a.d_voxel_color) {
+                if (UPC && a.d_voxel_color) {
                     const float* vc = a.d_voxel_color + 3ull * (base + kidx);
                     acc[8] += vc[0];
                     acc[9] += vc[1];
@@ -747,15 +749,19 @@ void launch_l1_loss(const float* color, const float* gt, uint64_t n, float* d_co
 
 void launch_composite_backward(const DevCamera& cam, const BackwardArgs& a, cudaStream_t st) {
     const unsigned ntiles = unsigned(cam.ntx * cam.nty);
+    const bool upc = a.d_weight || a.d_voxel_color;
     switch (a.K) {
         case 1:
-            launch_pdl(composite_backward_kernel<1>, ntiles, 256, 0, st, cam, a);
+            if (upc) launch_pdl(composite_backward_kernel<1, true>, ntiles, 256, 0, st, cam, a);
+            else launch_pdl(composite_backward_kernel<1, false>, ntiles, 256, 0, st, cam, a);
             break;
         case 2:
-            launch_pdl(composite_backward_kernel<2>, ntiles, 256, 0, st, cam, a);
+            if (upc) launch_pdl(composite_backward_kernel<2, true>, ntiles, 256, 0, st, cam, a);
+            else launch_pdl(composite_backward_kernel<2, false>, ntiles, 256, 0, st, cam, a);
             break;
         case 3:
-            launch_pdl(composite_backward_kernel<3>, ntiles, 256, 0, st, cam, a);
+            if (upc) launch_pdl(composite_backward_kernel<3, true>, ntiles, 256, 0, st, cam, a);
+            else launch_pdl(composite_backward_kernel<3, false>, ntiles, 256, 0, st, cam, a);
             break;
         default:
             throw Error(SVR_ERR_INVALID_ARGUMENT, "rasterizer sample count K must be in {1,2,3}");
