@@ -855,11 +855,13 @@ constexpr int kCompWarps = 8;
 constexpr size_t kCompSmem = size_t(2) * kCompWarps * 32 * kRecordF4 * sizeof(float4);
 
 // MODE 0: plain render; 1: record pass (RECORD); 2: render with per-voxel
-// max-blend stats and/or staged training records (their checks compiled in).
+// max-blend stats and/or staged training records (their checks compiled in);
+// 3: staged training records only (the single-pass training render).
 template <int K, int MODE>
 __global__ void __launch_bounds__(256, 4) composite_kernel(DevCamera cam, CompositeArgs a) {
     constexpr bool RECORD = MODE == 1;
     constexpr bool EXTRA = MODE == 2;
+    constexpr bool STAGED = MODE == 3;
     pdl_enter();
     extern __shared__ float4 s_rec_dyn[];  // [2][8 warps][32 slots][kRecordF4]
     __shared__ uint32_t s_vid[2][kCompWarps][32];
@@ -1040,7 +1042,7 @@ __global__ void __launch_bounds__(256, 4) composite_kernel(DevCamera cam, Compos
                 nz += w * nor.z;
                 depth += T * dv;
                 if (EXTRA && a.max_blend) atomicMax(a.max_blend + __float_as_uint(col.w), __float_as_uint(w));
-                if (EXTRA && a.stage_entry) {
+                if (STAGED || (EXTRA && a.stage_entry)) {
                     if (cnt < a.stage_cap) {
                         const uint32_t at = cnt * a.stage_stride + slot;
                         a.stage_entry[at] = entry;
@@ -1388,18 +1390,21 @@ void launch_composite(const DevCamera& cam, const CompositeArgs& a, bool record_
     static bool attr_set = false;
     if (!attr_set) {
         for (auto fn : {composite_kernel<1, 0>, composite_kernel<1, 1>, composite_kernel<1, 2>,
-                        composite_kernel<2, 0>, composite_kernel<2, 1>, composite_kernel<2, 2>,
-                        composite_kernel<3, 0>, composite_kernel<3, 1>, composite_kernel<3, 2>})
+                        composite_kernel<1, 3>, composite_kernel<2, 0>, composite_kernel<2, 1>,
+                        composite_kernel<2, 2>, composite_kernel<2, 3>, composite_kernel<3, 0>,
+                        composite_kernel<3, 1>, composite_kernel<3, 2>, composite_kernel<3, 3>})
             SVR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCompSmem)));
         attr_set = true;
     }
-    const int mode = record_pass ? 1 : ((a.max_blend || a.stage_entry) ? 2 : 0);
+    const int mode = record_pass ? 1 : a.max_blend ? 2 : a.stage_entry ? 3 : 0;
 #define SVR_COMPOSITE_CASE(KK)                                                          \
     case KK:                                                                            \
         if (mode == 1)                                                                  \
             launch_pdl(composite_kernel<KK, 1>, ntiles, 256, kCompSmem, st, cam, a);    \
         else if (mode == 2)                                                             \
             launch_pdl(composite_kernel<KK, 2>, ntiles, 256, kCompSmem, st, cam, a);    \
+        else if (mode == 3)                                                             \
+            launch_pdl(composite_kernel<KK, 3>, ntiles, 256, kCompSmem, st, cam, a);    \
         else                                                                            \
             launch_pdl(composite_kernel<KK, 0>, ntiles, 256, kCompSmem, st, cam, a);    \
         break;
