@@ -994,7 +994,7 @@ __global__ void __launch_bounds__(256, 4) composite_kernel(DevCamera cam, Compos
                 continue;
             const float4 lo = wrec[s_][0];
             float ta, tb;
-            slab_s(lo, ix, iy, iz, ssel, ta, tb);
+            slab(lo, ix, iy, iz, ta, tb);  // same floats as slab_s; needs no per-lane face selectors
             const float4 va = wrec[s_][2], vb = wrec[s_][3];
             const float inv = wrec[s_][5].w;
             const float seg = tb - ta;
