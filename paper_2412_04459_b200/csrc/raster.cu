@@ -858,7 +858,10 @@ constexpr size_t kCompSmem = size_t(2) * kCompWarps * 32 * kRecordF4 * sizeof(fl
 // max-blend stats and/or staged training records (their checks compiled in);
 // 3: staged training records only (the single-pass training render).
 template <int K, int MODE>
-__global__ void __launch_bounds__(256, 4) composite_kernel(DevCamera cam, CompositeArgs a) {
+#ifndef SVR_COMP_MINB
+#define SVR_COMP_MINB 4
+#endif
+__global__ void __launch_bounds__(256, SVR_COMP_MINB) composite_kernel(DevCamera cam, CompositeArgs a) {
     constexpr bool RECORD = MODE == 1;
     constexpr bool EXTRA = MODE == 2;
     constexpr bool STAGED = MODE == 3;
