@@ -858,6 +858,9 @@ constexpr size_t kCompSmem = size_t(2) * kCompWarps * 32 * kRecordF4 * sizeof(fl
 // max-blend stats and/or staged training records (their checks compiled in);
 // 3: staged training records only (the single-pass training render).
 template <int K, int MODE>
+#ifndef SVR_PC_SMEM
+#define SVR_PC_SMEM 1  // pixel centre from shared memory in phase B (the register copy is rematerialised per hit)
+#endif
 #ifndef SVR_COMP_MINB
 #define SVR_COMP_MINB 4
 #endif
@@ -891,6 +894,10 @@ __global__ void __launch_bounds__(256, SVR_COMP_MINB) composite_kernel(DevCamera
     const SlabSel ssel = slab_sel(ix, iy, iz);
     const float dnorm = float(sqrt(dd[0] * dd[0] + dd[1] * dd[1] + dd[2] * dd[2]));
     const float pcx = float(px) + 0.5f, pcy = float(py) + 0.5f;
+#if SVR_PC_SMEM
+    __shared__ float2 s_pc[256];
+    s_pc[threadIdx.x] = make_float2(pcx, pcy);
+#endif
     // Frustum of this warp's 8x4 block (warp_cone_planes): skips boxes whose
     // screen AABB is loose, e.g. near-plane voxels, which get the full screen
     // (raster.cpp:95-101), without changing the composited set.
@@ -992,9 +999,16 @@ __global__ void __launch_bounds__(256, SVR_COMP_MINB) composite_kernel(DevCamera
             const int s_ = __ffs(hits) - 1;
             hits &= hits - 1;
             const float4 bb = wrec[s_][1];
+#if SVR_PC_SMEM
+            const float2 pc = s_pc[threadIdx.x];  // one LDS instead of rematerialising the centre
+            if (!((one_sign || (wvid[s_] >> 29) == my_sign) &&
+                  !(pc.x < bb.x || pc.x > bb.y || pc.y < bb.z || pc.y > bb.w)))
+                continue;
+#else
             if (!((one_sign || (wvid[s_] >> 29) == my_sign) &&
                   !(pcx < bb.x || pcx > bb.y || pcy < bb.z || pcy > bb.w)))
                 continue;
+#endif
             const float4 lo = wrec[s_][0];
             float ta, tb;
             slab(lo, ix, iy, iz, ta, tb);  // same floats as slab_s; needs no per-lane face selectors
