@@ -33,7 +33,10 @@ constexpr int kItems = 8;
 constexpr int kTileKeys = kThreads * kItems;  // 2048 pairs per partition
 // keys-only partitions are larger: 3072 keys, so a config-2 pass (1.76M
 // keys) is 574 CTAs = one wave of 4 resident CTAs on 148 SMs
-constexpr int kItemsK = 12;
+#ifndef SVR_SORT_ITEMS
+#define SVR_SORT_ITEMS 12  // keys per thread (keys-only): 16 is 7 % faster at 97M keys, 5 % slower at 4.5M
+#endif
+constexpr int kItemsK = SVR_SORT_ITEMS;
 constexpr int kTileKeysK = kThreads * kItemsK;
 template <bool PAIRS>
 struct Part {
