@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "svr_internal.h"
 #include "svr_kernels.h"
@@ -38,11 +39,15 @@ constexpr int kTileKeys = kThreads * kItems;  // 2048 pairs per partition
 #endif
 constexpr int kItemsK = SVR_SORT_ITEMS;
 constexpr int kTileKeysK = kThreads * kItemsK;
-template <bool PAIRS>
+template <bool PAIRS, int IK = kItemsK>
 struct Part {
-    static constexpr int items = PAIRS ? kItems : kItemsK;
+    static constexpr int items = PAIRS ? kItems : IK;
     static constexpr int keys = kThreads * items;
 };
+// keys-only passes over at least this many keys use 16 keys per thread
+// (fewer partitions to look back over: 7 % faster at 97M keys, 5 % slower at 4.5M)
+constexpr uint64_t kLargeSortKeys = uint64_t(1) << 25;
+constexpr int kItemsLarge = 16;
 constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagInc = 2u << 30;
 constexpr uint32_t kValMask = (1u << 30) - 1;
@@ -110,7 +115,7 @@ __device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
     asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(p), "r"(v));
 }
 
-template <bool PAIRS>
+template <bool PAIRS, int IK = kItemsK>
 __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
     const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint64_t n, RadixPass pass,
@@ -120,8 +125,8 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
     __shared__ uint32_t s_warp_hist[kWarps][kRadix + 1];
     __shared__ uint32_t s_block_excl[kRadix];
     __shared__ uint32_t s_global[kRadix];
-    __shared__ uint64_t s_keys[Part<PAIRS>::keys];
-    __shared__ uint32_t s_vals[PAIRS ? Part<PAIRS>::keys : 1];
+    __shared__ uint64_t s_keys[Part<PAIRS, IK>::keys];
+    __shared__ uint32_t s_vals[PAIRS ? Part<PAIRS, IK>::keys : 1];
     __shared__ uint32_t s_part;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -131,21 +136,21 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
     __syncthreads();
     const uint32_t part = s_part;
     if (n_dev) n = min(n, uint64_t(*n_dev));
-    const uint64_t base = uint64_t(part) * Part<PAIRS>::keys;
+    const uint64_t base = uint64_t(part) * Part<PAIRS, IK>::keys;
     if (base >= n && part > 0) return;  // past the live count: no later partition looks back here
-    const uint64_t wbase = base + uint64_t(warp) * 32 * Part<PAIRS>::items;
+    const uint64_t wbase = base + uint64_t(warp) * 32 * Part<PAIRS, IK>::items;
 
     // Digits are recomputed from the key/value when needed (saves registers);
     // out-of-range slots get digit kRadix and are ranked into a discarded bin.
-    uint64_t k[Part<PAIRS>::items];
-    uint32_t v[PAIRS ? Part<PAIRS>::items : 1], r[Part<PAIRS>::items];
+    uint64_t k[Part<PAIRS, IK>::items];
+    uint32_t v[PAIRS ? Part<PAIRS, IK>::items : 1], r[Part<PAIRS, IK>::items];
     const uint64_t nvalid = n > wbase ? n - wbase : 0;
     auto dig = [&](int i) -> uint32_t {
         return (uint64_t(i) * 32 + lane < nvalid) ? digit_of(k[i], PAIRS ? v[PAIRS ? i : 0] : 0u, pass)
                                                   : uint32_t(kRadix);
     };
 #pragma unroll
-    for (int i = 0; i < Part<PAIRS>::items; ++i) {
+    for (int i = 0; i < Part<PAIRS, IK>::items; ++i) {
         uint64_t idx = wbase + uint64_t(i) * 32 + lane;
         k[i] = idx < n ? keys_in[idx] : 0ull;
         if (PAIRS) v[PAIRS ? i : 0] = idx < n ? vals_in[idx] : 0u;
@@ -157,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
     // reserves the group's slots; the items' reservations pipeline instead of
     // serialising on a load/store/syncwarp round trip each.
 #pragma unroll
-    for (int i = 0; i < Part<PAIRS>::items; ++i) {
+    for (int i = 0; i < Part<PAIRS, IK>::items; ++i) {
         const uint32_t di = dig(i);
         const uint32_t peers = __match_any_sync(0xffffffffu, di);
         const int leader = __ffs(peers) - 1;
@@ -167,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
     }
 #else
 #pragma unroll
-    for (int i = 0; i < Part<PAIRS>::items; ++i) {
+    for (int i = 0; i < Part<PAIRS, IK>::items; ++i) {
         const uint32_t di = dig(i);
         uint32_t peers = __match_any_sync(0xffffffffu, di);
         uint32_t below = __popc(peers & lt_mask);
@@ -239,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
 
     // Scatter to shared memory in digit order, then out to global.
 #pragma unroll
-    for (int i = 0; i < Part<PAIRS>::items; ++i) {
+    for (int i = 0; i < Part<PAIRS, IK>::items; ++i) {
         const uint32_t di = dig(i);
         if (di < kRadix) {
             uint32_t pos = s_block_excl[di] + s_warp_hist[warp][di] + r[i];
@@ -248,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
         }
     }
     __syncthreads();
-    const uint32_t tile_n = uint32_t(min(uint64_t(Part<PAIRS>::keys), n - base));
+    const uint32_t tile_n = uint32_t(min(uint64_t(Part<PAIRS, IK>::keys), n - base));
     for (uint32_t pos = threadIdx.x; pos < tile_n; pos += kThreads) {
         uint64_t kk = s_keys[pos];
         uint32_t vv = PAIRS ? s_vals[pos] : 0u;
@@ -359,9 +364,14 @@ int radix_sort_keys(uint64_t* keys0, uint64_t* keys1, uint64_t n, const RadixPas
     uint64_t* kin = keys0;
     uint64_t* kout = keys1;
     int cur = 0;
+    const char* lk_env = std::getenv("SVR_LARGE_SORT_MIN");  // parity tests lower it
+    const bool large = n >= (lk_env ? std::strtoull(lk_env, nullptr, 10) : kLargeSortKeys);
+    const uint64_t nparts_run = large ? (n + uint64_t(kThreads) * kItemsLarge - 1) / (uint64_t(kThreads) * kItemsLarge)
+                                      : nparts;
     for (int p = 0; p < npasses; ++p) {
         const bool last_fin = fin && p == npasses - 1;
-        launch_pdl(onesweep_kernel<false>, unsigned(nparts), kThreads, 0, st, (const uint64_t*)kin,
+        launch_pdl(large ? onesweep_kernel<false, kItemsLarge> : onesweep_kernel<false, kItemsK>,
+                   unsigned(nparts_run), kThreads, 0, st, (const uint64_t*)kin,
                    (const uint32_t*)nullptr, kout, last_fin ? fin->vals : (uint32_t*)nullptr, n, passes[p],
                    (const uint32_t*)(hist + p * kRadix), status + size_t(p) * (nparts_alloc + 1) * kRadix,
                    tickets + p, n_dev, last_fin ? fin->vb : -1, last_fin ? fin->ranges : (uint2*)nullptr,

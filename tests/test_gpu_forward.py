@@ -144,6 +144,26 @@ def test_entries_sort_ranges_bit_exact(svr, ctx, ref, cfg1, ss):
     assert np.all(ranges[~nonempty, 0] == ranges[~nonempty, 1])
 
 
+def test_large_sort_partitions_bit_exact(svr, ctx, ref, cfg1, monkeypatch):
+    """The 16-keys-per-thread onesweep used for large entry counts (forced
+    here): same emitted, sorted entries and ranges as the reference."""
+    monkeypatch.setenv("SVR_LARGE_SORT_MIN", "0")
+    monkeypatch.setenv("SVR_RANKED", "0")  # full-key sort: 5 passes through the large kernel
+    arrays, scene, rscene = cfg1
+    for cam in [svr.ring_camera(1, 0, 256, 256), svr.ring_camera(3, 1, 320, 192)]:
+        f = svr.Frame(ctx)
+        svr.render_into(f, scene, cam, svr.RenderOptions(supersample=1.0))
+        ks_ref, vs_ref = ref.ref_entries(rscene, cam, sorted_=True)
+        assert np.array_equal(f.download("SORT_KEYS", np.uint64), ks_ref)
+        assert np.array_equal(f.download("SORT_VALUES", np.uint32), vs_ref)
+    monkeypatch.setenv("SVR_RANKED", "1")
+    f = svr.Frame(ctx)
+    cam = svr.ring_camera(3, 1, 320, 192)
+    svr.render_into(f, scene, cam, svr.RenderOptions(supersample=1.0))
+    ks_ref, vs_ref = ref.ref_entries(rscene, cam, sorted_=True)
+    assert np.array_equal(f.download("SORT_VALUES", np.uint32), vs_ref)
+
+
 @pytest.mark.parametrize("fused", ["0", "1"])
 def test_fused_digit_histograms_bit_exact(svr, ctx, ref, cfg1, monkeypatch, fused):
     """The sort's digit histograms counted in K4 (large-E path, forced here)
