@@ -183,7 +183,11 @@ def stage_bytes(stage, d):
     """Algorithmic bytes per launch. d: n_vox, n_pool, n_vis,
     E, R, ntiles, stride, npass, contribs."""
     if stage == "composite":
-        return d["E"] * (4 + 96) + d["ntiles"] * 8 + d["R"] * 36
+        # SURVEY §8(d): the 96-B record of each visible voxel read once, the
+        # 4-B sorted value of each entry, 8 B of range per tile, 9 fp32
+        # output channels per pixel (re-reads of a record by other tiles are
+        # cache traffic, not algorithmic bytes)
+        return d["n_vis"] * 96 + d["E"] * 4 + d["ntiles"] * 8 + d["R"] * 36
     if stage == "preprocess":
         return d["n_vox"] * (8 + 16 + 4) + 4 * d["n_pool"] + d["n_vis"] * (32 + 4 * d["stride"] + 96)
     if stage == "sort":
@@ -233,10 +237,13 @@ def view_ids(w, rank, world, i):
     return [(first + k) % N_VIEWS for k in range(b)]
 
 
-def make_camera(svr, w, v):
+def make_camera(ring, w, v):
+    """View v of workload w; `ring` is ring_cameras (the product's
+    svr.ring_camera, or the reference's own ref.ref_ring_camera in the
+    reference arm — bit-identical poses, tests/test_abi_cpu.py)."""
     if w["kind"] in ("train", "iter") and w["scene"] == "G":
-        return svr.ring_camera(1, 0, w["res"], w["res"], w["dist"])  # cfg3's single view
-    return svr.ring_camera(N_VIEWS, v, w["res"], w["res"], w["dist"])
+        return ring(1, 0, w["res"], w["res"], w["dist"])  # cfg3's single view
+    return ring(N_VIEWS, v, w["res"], w["res"], w["dist"])
 
 
 def make_gt(w, v):
@@ -244,25 +251,51 @@ def make_gt(w, v):
     return np.random.default_rng(seed).uniform(0, 1, (w["res"], w["res"], 3)).astype(np.float32)
 
 
+def bench_config(w, n_voxels, supersample):
+    """The `config` object, identical in both arms (run-specific details go
+    under the line's `run` key)."""
+    return {"workload": w["desc"], "voxels": int(n_voxels), "resolution": f"{w['res']}x{w['res']}",
+            "supersample": supersample, "K": 1, "sh_degree": 3,
+            "l2": "GPU arm: L2 flushed (256 MiB write) before every timed step"}
+
+
 # ------------------------------------------------------------------ reference (CPU)
-def band_cameras(svr, cam, threads, rows=None):
+# This arm never imports paper_2412_04459_b200: the scene, the cameras and the
+# options come from the unmodified reference (oracle/_ref: RefScene.generate /
+# RefScene.unbounded = init_unbounded, ring_cameras) and oracle/abi.py.
+# TrainConfig defaults one iteration uses (optim.hpp:39-60).
+TRAIN_DEFAULTS = dict(lr_density=0.025, lr_sh0=0.01, lr_sh_rest=0.00025, lambda_ssim=0.02,
+                      lambda_T=0.01, lambda_dist=0.1, lambda_R=0.01)
+
+
+def ref_scene(ref, w):
+    if w["scene"] == "G":
+        g = G_SCENE
+        return ref.RefScene.generate(g["seed"], g["target"], g["max_level"], g["sh_degree"])
+    u = U_SCENE
+    cams = [ref.ref_ring_camera(8, i, 1024, 1024) for i in range(8)]
+    return ref.RefScene.unbounded(cams, u["init_level"], u["shell_levels"], u["bg_ratio"],
+                                  u["seed"], u["sh_degree"])
+
+
+def band_cameras(cam, threads, rows=None):
     """Horizontal bands of `cam` (each a full camera with shifted cy)."""
     rows = rows or max(16, ((cam.height + threads - 1) // threads + 15) // 16 * 16)
     out = []
     for y0 in range(0, cam.height, rows):
         h = min(rows, cam.height - y0)
-        out.append(svr.Camera(cam.width, h, cam.fx, cam.fy, cam.cx, cam.cy - y0, cam.rot, cam.pos))
+        out.append(type(cam)(cam.width, h, cam.fx, cam.fy, cam.cx, cam.cy - y0, cam.rot, cam.pos))
     return out
 
 
-def reference_step_time(ref, rscene, arrays, w, cam, opts, threads, gt=None, frac=1.0):
+def reference_step_time(ref, rscene, sizes, w, cam, opts, threads, gt=None, frac=1.0):
     """One step of workload w through the reference's own svr::render (and,
     for training, its L1 + render_backward) split into row bands rendered
     concurrently (the reference API is reentrant; ctypes releases the GIL).
     frac < 1 renders only that fraction of the bands (evenly spread) and
-    scales the time. Returns seconds per full step."""
-    import paper_2412_04459_b200 as svr
-    bands = band_cameras(svr, cam, threads)
+    scales the time. sizes = (n_voxels, n_pool, sh_stride). Returns seconds
+    per full step."""
+    bands = band_cameras(cam, threads)
     if frac < 1.0:
         keep = max(1, int(round(len(bands) * frac)))
         idx = np.linspace(0, len(bands) - 1, keep).round().astype(int)
@@ -270,6 +303,7 @@ def reference_step_time(ref, rscene, arrays, w, cam, opts, threads, gt=None, fra
         bands = [bands[i] for i in sorted(set(idx))]
     else:
         scale = 1.0
+    n_vox, n_pool, stride = sizes
 
     def one(c):
         if w["kind"] == "render":
@@ -277,8 +311,7 @@ def reference_step_time(ref, rscene, arrays, w, cam, opts, threads, gt=None, fra
         else:
             y0 = int(round(cam.cy - c.cy))
             g = gt[y0:y0 + c.height]
-            ref.ref_train_step_l1(rscene, c, opts, g, arrays.n_pool, arrays.n_voxels * arrays.sh_stride,
-                                  arrays.n_voxels)
+            ref.ref_train_step_l1(rscene, c, opts, g, n_pool, n_vox * stride, n_vox)
 
     t0 = time.perf_counter()
     with cf.ThreadPoolExecutor(max_workers=min(threads, len(bands))) as ex:
@@ -289,19 +322,21 @@ def reference_step_time(ref, rscene, arrays, w, cam, opts, threads, gt=None, fra
 CPU_FRACTION = {"cfg2": 1.0, "cfg3": 1.0, "cfg3i": 1.0, "cfg4": 1.0 / 16, "cfg5": 1.0 / 16}
 
 
-def reference_iteration_time(ref, rscene, arrays, cam, opts, gt):
+def reference_iteration_time(ref, rscene, params, cam, opts, gt):
     """One optim::train iteration (render -> MSE + SSIM -> ray losses ->
     backward -> Adam on both pools) through the unmodified reference, one
-    thread (SSIM windows and the pool-wide Adam do not split into bands)."""
-    from paper_2412_04459_b200.trainer import TrainWeights
-    w = TrainWeights()
+    thread (SSIM windows and the pool-wide Adam do not split into bands).
+    params = (density, sh, sh_stride) of the scene."""
+    density, sh, stride = params
+    n_vox = sh.size // stride
+    t = TRAIN_DEFAULTS
     t0 = time.perf_counter()
-    _, gd, gs, _ = ref.ref_train_iteration_grads(rscene, cam, opts, gt, w.lambda_ssim, w.lambda_T,
-                                                 w.lambda_dist, w.lambda_R, arrays.n_pool,
-                                                 arrays.n_voxels * arrays.sh_stride, arrays.n_voxels)
-    ref.ref_adam_step(arrays.density, gd, np.zeros(gd.size), np.zeros(gd.size), 0, w.lr_density)
-    ref.ref_adam_step(arrays.sh.reshape(-1), gs, np.zeros(gs.size), np.zeros(gs.size), 0, w.lr_sh0,
-                      w.lr_sh_rest, arrays.sh_stride, 3)
+    _, gd, gs, _ = ref.ref_train_iteration_grads(rscene, cam, opts, gt, t["lambda_ssim"],
+                                                 t["lambda_T"], t["lambda_dist"], t["lambda_R"],
+                                                 density.size, sh.size, n_vox)
+    ref.ref_adam_step(density, gd, np.zeros(gd.size), np.zeros(gd.size), 0, t["lr_density"])
+    ref.ref_adam_step(sh.reshape(-1), gs, np.zeros(gs.size), np.zeros(gs.size), 0, t["lr_sh0"],
+                      t["lr_sh_rest"], stride, 3)
     return time.perf_counter() - t0
 
 
@@ -317,32 +352,38 @@ def cpu_sample_text(w, name, cores):
             f"(oracle/_ref) split into row bands on {cores} threads; {part}")
 
 
-def run_reference(args, rank):
-    if rank != 0:
-        return
-    import paper_2412_04459_b200 as svr
-    from oracle import ref
-    w = WORKLOADS[args.workload]
-    cores = host_cores()
-    arrays = make_scene_arrays(svr, w)
-    rscene = ref.RefScene.from_arrays(arrays)
-    opts = svr.RenderOptions(K=1, supersample=args.supersample, training=w["kind"] != "render")
-    frac = CPU_FRACTION[args.workload]
-
+def cpu_step_fn(ref, rscene, w, name, opts, ring, cores):
+    """step(i) -> seconds of the reference's CPU path for step i."""
+    n_vox, n_pool, deg = rscene.sizes()
+    stride = 3 * (deg + 1) ** 2
+    params = None
     if w["kind"] == "iter":
-        cores = 1
+        a = rscene.arrays()
+        params = (a.density, a.sh, stride)
 
     def step(i):
         t = 0.0
         for v in view_ids(w, 0, 1, i):
-            cam = make_camera(svr, w, v)
+            cam = make_camera(ring, w, v)
             if w["kind"] == "iter":
-                t += reference_iteration_time(ref, rscene, arrays, cam, opts, make_gt(w, v))
+                t += reference_iteration_time(ref, rscene, params, cam, opts, make_gt(w, v))
                 continue
-            t += reference_step_time(ref, rscene, arrays, w, cam, opts, cores,
-                                     make_gt(w, v) if w["kind"] == "train" else None, frac)
+            t += reference_step_time(ref, rscene, (n_vox, n_pool, stride), w, cam, opts, cores,
+                                     make_gt(w, v) if w["kind"] == "train" else None,
+                                     CPU_FRACTION[name])
         return t
+    return step
 
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    from oracle import abi, ref
+    w = WORKLOADS[args.workload]
+    cores = 1 if w["kind"] == "iter" else host_cores()
+    rscene = ref_scene(ref, w)
+    opts = abi.RenderOptions(K=1, supersample=args.supersample, training=w["kind"] != "render")
+    step = cpu_step_fn(ref, rscene, w, args.workload, opts, ref.ref_ring_camera, cores)
     for i in range(args.warmup):
         step(i)
     total = sum(step(i) for i in range(args.steps))
@@ -355,8 +396,8 @@ def run_reference(args, rank):
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "mrays_per_s": val * sw * sw / 1e6,
-        "config": {"workload": w["desc"], "voxels": arrays.n_voxels, "resolution": f"{w['res']}x{w['res']}",
-                   "supersample": args.supersample, "K": 1, "parallelism": "cpu threads"},
+        "config": bench_config(w, rscene.sizes()[0], args.supersample),
+        "run": {"parallelism": f"{cores} CPU thread(s), row bands of each view"},
         "cpu_baseline": {"value": val, "unit": w["unit"], "cores": cores, "kind": "reference",
                          "sample": cpu_sample_text(w, args.workload, cores)},
         "e2e": {"value": val, "unit": w["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -376,7 +417,7 @@ class RenderStep:
 
     def cam(self, v):
         if v not in self.cams:
-            self.cams[v] = make_camera(self.svr, self.w, v)
+            self.cams[v] = make_camera(self.svr.ring_camera, self.w, v)
         return self.cams[v]
 
     def __call__(self, i):
@@ -395,7 +436,7 @@ class TrainStep:
         dev = torch.device("cuda", ctx.device)
         cams, gts = {}, {}
         for v in self.views:
-            cams[v] = make_camera(svr, w, v)
+            cams[v] = make_camera(svr.ring_camera, w, v)
             gts[v] = torch.tensor(make_gt(w, v), device=dev)
         # ShardedTrainer indexes cameras/gts by view id
         idx = {v: k for k, v in enumerate(self.views)}
@@ -418,7 +459,7 @@ class IterStep:
     def __init__(self, svr, ctx, scene, w, rank, world):
         import torch
         from paper_2412_04459_b200.trainer import DeviceTrainer
-        self.cam = make_camera(svr, w, 0)
+        self.cam = make_camera(svr.ring_camera, w, 0)
         self.gt_host = torch.tensor(make_gt(w, 0), dtype=torch.float32).pin_memory()
         self.gt = self.gt_host.to(torch.device("cuda", ctx.device))
         self.trainer = DeviceTrainer(svr, ctx, scene, svr.RenderOptions(K=1, supersample=1.0))
@@ -609,14 +650,15 @@ def run_ours(args, rank, world, local_rank):
     # SMs x max SM clock, one warp instruction each per cycle), from the
     # committed ncu instruction count of that kernel on this workload
     winst = traffic_from_profiles(dom + "_warp_inst", args.workload)
-    issue_peak = 4 * 148 * 1.965e9
+    issue_peak = 4 * 148 * 1e6 * float(clk.get("sm_mhz") or 1965.0)
     issue = None
     if winst:
         issue = {"bound": "issue", "achieved_warp_inst_per_s": winst / (kernel_ms * 1e-3),
                  "peak_warp_inst_per_s": issue_peak,
                  "frac": winst / (kernel_ms * 1e-3) / issue_peak,
                  "warp_inst_per_launch": winst, "source": "profiles/ncu_traffic.json"}
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+    binds = "issue" if issue and issue["frac"] > achieved / peak else "hbm"
+    roofline = {"bound": "hbm", "binds": binds, "kernel": dom, "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak, "issue": issue,
                 "traffic": traffic_from_profiles(dom, args.workload, npass),
                 "algorithmic_bytes": byt, "kernel_ms": kernel_ms, "peak_source": peak_src}
@@ -626,40 +668,31 @@ def run_ours(args, rank, world, local_rank):
         try:
             from oracle import ref
             rscene = ref.RefScene.from_arrays(arrays)
-            cores = host_cores()
-            v = view_ids(w, 0, 1, 0)[0]
+            cores = 1 if w["kind"] == "iter" else host_cores()
             opts = svr.RenderOptions(K=1, supersample=1.0, training=w["kind"] != "render")
-            if w["kind"] == "iter":
-                cores = 1
-                secs = reference_iteration_time(ref, rscene, arrays, make_camera(svr, w, v), opts,
-                                                make_gt(w, v))
-            else:
-                secs = reference_step_time(ref, rscene, arrays, w, make_camera(svr, w, v), opts,
-                                           cores, make_gt(w, v) if w["kind"] == "train" else None,
-                                           CPU_FRACTION[args.workload])
-            cpu = {"value": 1.0 / secs, "unit": w["unit"], "cores": cores, "kind": "reference",
-                   "sample": cpu_sample_text(w, args.workload, cores)}
+            secs = cpu_step_fn(ref, rscene, w, args.workload, opts, svr.ring_camera, cores)(0)
+            cpu = {"value": w["batch"] / secs, "unit": w["unit"], "cores": cores,
+                   "kind": "reference", "sample": cpu_sample_text(w, args.workload, cores)}
         except Exception as e:  # the reference library may be absent on a fresh box
             cpu = {"value": None, "unit": w["unit"], "cores": host_cores(), "kind": "reference",
                    "sample": f"unavailable: {type(e).__name__}: {e}"}
 
-    config = {"workload": w["desc"], "voxels": arrays.n_voxels, "pool": arrays.n_pool,
-              "resolution": f"{w['res']}x{w['res']}", "supersample": args.supersample, "K": 1,
-              "entries_per_view": int(E), "visible_voxels": int(n_vis), "sort_passes": npass,
-              "l2": "flushed (256 MiB write) before every timed step",
-              "frames": ("deferred entry count (svr_ctx_set_async), "
-                         f"{overflows} timed frame(s) outgrew their capacity"
-                         if w["kind"] == "render" else "synchronous"),
-              "parallelism": (f"view-sharded over {world} GPU(s), no data-path collective"
-                              if w["kind"] == "render" else
-                              f"replicas only ({world} independent iteration(s))"
-                              if w["kind"] == "iter" else
-                              f"view-batch sharded over {world} GPU(s), one in-place all-reduce "
-                              f"of the flat gradient per step"),
-              "precision": "projection/tile binning fp64 (bit-exact), compositing fp32"}
+    config = bench_config(w, arrays.n_voxels, args.supersample)
+    run = {"pool": arrays.n_pool, "entries_per_view": int(E), "visible_voxels": int(n_vis),
+           "sort_passes": npass,
+           "frames": ("deferred entry count (svr_ctx_set_async), "
+                      f"{overflows} timed frame(s) outgrew their capacity"
+                      if w["kind"] == "render" else "synchronous"),
+           "parallelism": (f"view-sharded over {world} GPU(s), no data-path collective"
+                           if w["kind"] == "render" else
+                           f"replicas only ({world} independent iteration(s))"
+                           if w["kind"] == "iter" else
+                           f"view-batch sharded over {world} GPU(s), one in-place all-reduce "
+                           f"of the flat gradient per step"),
+           "precision": "projection/tile binning fp64 (bit-exact), compositing fp32"}
     if w["kind"] != "render":
-        config["contribs_per_view"] = int(contribs)
-        config["views_per_gpu_step"] = units_per_step
+        run["contribs_per_view"] = int(contribs)
+        run["views_per_gpu_step"] = units_per_step
     line = {
         "metric": w["metric"], "value": value, "unit": w["unit"], "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps,
@@ -667,6 +700,7 @@ def run_ours(args, rank, world, local_rank):
         "data": "synthetic (random-init parameters)",
         "mrays_per_s": value * sw * sw / 1e6,
         "config": config,
+        "run": run,
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": w["unit"], "h2d_bytes_per_step": h2d,

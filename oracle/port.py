@@ -12,6 +12,9 @@ import subprocess
 
 import numpy as np
 
+from oracle import abi
+from oracle.abi import camera_c, options_c
+
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO = os.path.join(HERE, "_ref", "libsvr_oracle.so")
 _lib = None
@@ -23,12 +26,11 @@ def load():
         return _lib
     if not os.path.exists(SO):
         subprocess.run(["make", "-C", HERE, "oracle"], check=True, capture_output=True)
-    import paper_2412_04459_b200 as svr
     lib = C.CDLL(SO)
     P = C.c_void_p
-    desc = C.POINTER(svr.svr_scene_desc)
-    cam = C.POINTER(svr.svr_camera)
-    opt = C.POINTER(svr.svr_render_options)
+    desc = C.POINTER(abi.svr_scene_desc)
+    cam = C.POINTER(abi.svr_camera)
+    opt = C.POINTER(abi.svr_render_options)
     for name, args in {
         "orc_tile_masks": [cam, P],
         "orc_project": [desc, cam, C.c_double, P, P, P],
@@ -47,31 +49,18 @@ def _p(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
 
-class _Desc:
-    def __init__(self, a):
-        import paper_2412_04459_b200 as svr
-        self.keep = [np.ascontiguousarray(a.codes, np.uint64), np.ascontiguousarray(a.levels, np.uint8),
-                     np.ascontiguousarray(a.corner_index, np.uint32).reshape(-1),
-                     np.ascontiguousarray(a.density, np.float32),
-                     np.ascontiguousarray(a.sh, np.float32).reshape(-1)]
-        d = svr.svr_scene_desc()
-        d.n_voxels, d.n_pool, d.sh_degree = a.n_voxels, a.n_pool, int(a.sh_degree)
-        for i in range(3):
-            d.bounds_center[i] = float(a.bounds_center[i])
-        d.bounds_size = float(a.bounds_size)
-        d.codes, d.levels, d.corner_index, d.density, d.sh = [_p(x) for x in self.keep]
-        self.d = d
+class _Desc(abi.SceneDesc):
+    pass
 
 
 def _chk(st):
     if st != 0:
-        import paper_2412_04459_b200 as svr
-        raise svr._EXC.get(st, svr.SvrError)(f"oracle status {st}")
+        raise abi.EXC.get(st, abi.OracleError)(f"oracle status {st}")
 
 
 def tile_masks(cam):
     out = np.empty(((cam.width + 15) // 16) * ((cam.height + 15) // 16), np.uint8)
-    c = cam.to_c()
+    c = camera_c(cam)
     _chk(load().orc_tile_masks(C.byref(c), _p(out)))
     return out
 
@@ -80,14 +69,14 @@ def project(a, cam, near=1e-6):
     d = _Desc(a)
     n = a.n_voxels
     vis, aabb, rect = np.empty(n, np.uint8), np.empty((n, 4)), np.empty((n, 4), np.int32)
-    c = cam.to_c()
+    c = camera_c(cam)
     _chk(load().orc_project(C.byref(d.d), C.byref(c), near, _p(vis), _p(aabb), _p(rect)))
     return vis.astype(bool), aabb, rect
 
 
 def entries(a, cam, sorted_, near=1e-6):
     d = _Desc(a)
-    c = cam.to_c()
+    c = camera_c(cam)
     n = C.c_uint64()
     _chk(load().orc_entries(C.byref(d.d), C.byref(c), near, int(sorted_), C.byref(n), None, None))
     k, v = np.empty(n.value, np.uint64), np.empty(n.value, np.uint32)
@@ -101,7 +90,7 @@ def render(a, cam, opts):
     out = {"color": np.empty((H, W, 3)), "depth": np.empty((H, W)), "median_depth": np.empty((H, W)),
            "normal": np.empty((H, W, 3)), "transmittance": np.empty((H, W))}
     mb = np.empty(a.n_voxels) if opts.record_stats else None
-    c, o = cam.to_c(), opts.to_c()
+    c, o = camera_c(cam), options_c(opts)
     _chk(load().orc_render(C.byref(d.d), C.byref(c), C.byref(o), _p(out["color"]), _p(out["depth"]),
                            _p(out["median_depth"]), _p(out["normal"]), _p(out["transmittance"]), _p(mb)))
     out["max_blend_weight"] = mb
@@ -113,7 +102,7 @@ def backward(a, cam, opts, d_color=None, d_depth=None, d_normal=None, d_tfin_ss=
     keep = [None if x is None else np.ascontiguousarray(x, np.float64)
             for x in (d_color, d_depth, d_normal, d_tfin_ss)]
     gd, gs, gp = np.empty(a.n_pool), np.empty(a.n_voxels * a.sh_stride), np.empty(a.n_voxels)
-    c, o = cam.to_c(), opts.to_c()
+    c, o = camera_c(cam), options_c(opts)
     _chk(load().orc_backward(C.byref(d.d), C.byref(c), C.byref(o), *[_p(x) for x in keep],
                              _p(gd), _p(gs), _p(gp)))
     return {"density": gd, "sh": gs.reshape(a.n_voxels, a.sh_stride), "priority": gp}

@@ -26,9 +26,8 @@ _ref = None
 _port = None
 
 
-def _svr():
-    import paper_2412_04459_b200 as svr  # structs only; no compute
-    return svr
+from oracle import abi
+from oracle.abi import camera_c, options_c
 
 
 def ref_available() -> bool:
@@ -45,17 +44,16 @@ def load_ref() -> C.CDLL:
         else:
             raise FileNotFoundError(f"{REF_SO} missing and /root/reference absent")
     lib = C.CDLL(REF_SO)
-    svr = _svr()
     P = C.c_void_p
-    cam = C.POINTER(svr.svr_camera)
-    opt = C.POINTER(svr.svr_render_options)
+    cam = C.POINTER(abi.svr_camera)
+    opt = C.POINTER(abi.svr_render_options)
     sig = {
         "ref_last_error": (C.c_char_p, []),
         "ref_scene_gen": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.POINTER(P)]),
         "ref_scene_unbounded": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64,
                                           C.c_int, C.POINTER(P)]),
         "ref_scene_bounds": (None, [P, P, C.POINTER(C.c_double)]),
-        "ref_scene_make": (C.c_int, [C.POINTER(svr.svr_scene_desc), C.POINTER(P)]),
+        "ref_scene_make": (C.c_int, [C.POINTER(abi.svr_scene_desc), C.POINTER(P)]),
         "ref_scene_from_paths": (C.c_int, [P, P, C.c_uint64, C.c_float, C.c_int, C.POINTER(P)]),
         "ref_scene_free": (None, [P]),
         "ref_scene_sizes": (None, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
@@ -92,9 +90,8 @@ def _p(a):
 
 def _chk(st):
     if st != 0:
-        svr = _svr()
         msg = load_ref().ref_last_error().decode()
-        raise svr._EXC.get(st, svr.SvrError)(msg)
+        raise abi.EXC.get(st, abi.OracleError)(msg)
 
 
 class RefScene:
@@ -113,8 +110,7 @@ class RefScene:
     def unbounded(cameras, init_level: int, shell_levels: int, bg_ratio: float, seed: int,
                   sh_degree: int = 3) -> "RefScene":
         """init_unbounded (optim.cpp:96-184) + G-style parameters."""
-        svr = _svr()
-        arr = (svr.svr_camera * len(cameras))(*[c.to_c() for c in cameras])
+        arr = (abi.svr_camera * len(cameras))(*[camera_c(c) for c in cameras])
         h = C.c_void_p()
         _chk(load_ref().ref_scene_unbounded(arr, len(cameras), init_level, shell_levels,
                                             bg_ratio, seed, sh_degree, C.byref(h)))
@@ -128,19 +124,9 @@ class RefScene:
 
     @staticmethod
     def from_arrays(a) -> "RefScene":
-        svr = _svr()
-        keep = [np.ascontiguousarray(a.codes, np.uint64), np.ascontiguousarray(a.levels, np.uint8),
-                np.ascontiguousarray(a.corner_index, np.uint32).reshape(-1),
-                np.ascontiguousarray(a.density, np.float32),
-                np.ascontiguousarray(a.sh, np.float32).reshape(-1)]
-        d = svr.svr_scene_desc()
-        d.n_voxels, d.n_pool, d.sh_degree = a.n_voxels, a.n_pool, int(a.sh_degree)
-        for i in range(3):
-            d.bounds_center[i] = float(a.bounds_center[i])
-        d.bounds_size = float(a.bounds_size)
-        d.codes, d.levels, d.corner_index, d.density, d.sh = [_p(x) for x in keep]
+        d = abi.SceneDesc(a)
         h = C.c_void_p()
-        _chk(load_ref().ref_scene_make(C.byref(d), C.byref(h)))
+        _chk(load_ref().ref_scene_make(C.byref(d.d), C.byref(h)))
         return RefScene(h)
 
     @staticmethod
@@ -152,8 +138,13 @@ class RefScene:
                                              C.byref(h)))
         return RefScene(h)
 
+    def sizes(self):
+        """(n_voxels, n_pool, sh_degree) without exporting the arrays."""
+        n, p, deg = C.c_uint64(), C.c_uint64(), C.c_int()
+        load_ref().ref_scene_sizes(self.h, C.byref(n), C.byref(p), C.byref(deg))
+        return n.value, p.value, deg.value
+
     def arrays(self):
-        svr = _svr()
         n, p, deg = C.c_uint64(), C.c_uint64(), C.c_int()
         lib = load_ref()
         lib.ref_scene_sizes(self.h, C.byref(n), C.byref(p), C.byref(deg))
@@ -165,7 +156,8 @@ class RefScene:
         dens = np.empty(P, np.float32)
         sh = np.empty((N, stride), np.float32)
         lib.ref_scene_export(self.h, _p(codes), _p(levels), _p(ci), _p(dens), _p(sh))
-        return svr.SceneArrays(codes, levels, ci, dens, sh, D)
+        c, s = self.bounds()
+        return abi.SceneArrays(codes, levels, ci, dens, sh, D, c, s)
 
     def set_params(self, density=None, sh=None):
         d = None if density is None else np.ascontiguousarray(density, np.float32)
@@ -181,17 +173,15 @@ class RefScene:
 
 
 def ref_ring_camera(n, i, w, h, dist=1.3, fov=55.0):
-    svr = _svr()
-    c = svr.svr_camera()
+    c = abi.svr_camera()
     _chk(load_ref().ref_ring_camera(n, i, w, h, dist, fov, C.byref(c)))
-    return svr.Camera.from_c(c)
+    return abi.Camera.from_c(c)
 
 
 def ref_scaled_camera(cam, ss):
-    svr = _svr()
-    c, o = cam.to_c(), svr.svr_camera()
+    c, o = camera_c(cam), abi.svr_camera()
     _chk(load_ref().ref_scaled_camera(C.byref(c), ss, C.byref(o)))
-    return svr.Camera.from_c(o)
+    return abi.Camera.from_c(o)
 
 
 def ref_render(scene: RefScene, cam, opts, oracle: bool = False, n_voxels: int = 0):
@@ -201,7 +191,7 @@ def ref_render(scene: RefScene, cam, opts, oracle: bool = False, n_voxels: int =
            "median_depth": np.empty((H, W)), "normal": np.empty((H, W, 3)),
            "transmittance": np.empty((H, W))}
     mb = np.empty(n_voxels) if opts.record_stats else None
-    c, o = cam.to_c(), opts.to_c()
+    c, o = camera_c(cam), options_c(opts)
     _chk(load_ref().ref_render(scene.h, C.byref(c), C.byref(o), int(oracle), _p(out["color"]),
                                _p(out["depth"]), _p(out["median_depth"]), _p(out["normal"]),
                                _p(out["transmittance"]), _p(mb)))
@@ -213,7 +203,7 @@ def ref_project(scene: RefScene, cam, n_voxels: int, near: float = 1e-6):
     vis = np.empty(n_voxels, np.uint8)
     aabb = np.empty((n_voxels, 4))
     rect = np.empty((n_voxels, 4), np.int32)
-    c = cam.to_c()
+    c = camera_c(cam)
     _chk(load_ref().ref_project(scene.h, C.byref(c), near, _p(vis), _p(aabb), _p(rect)))
     return vis.astype(bool), aabb, rect
 
@@ -221,14 +211,14 @@ def ref_project(scene: RefScene, cam, n_voxels: int, near: float = 1e-6):
 def ref_tile_masks(cam):
     ntx, nty = (cam.width + 15) // 16, (cam.height + 15) // 16
     out = np.empty(ntx * nty, np.uint8)
-    c = cam.to_c()
+    c = camera_c(cam)
     _chk(load_ref().ref_tile_masks(C.byref(c), _p(out)))
     return out
 
 
 def ref_entries(scene: RefScene, cam, sorted_: bool, near: float = 1e-6):
     lib = load_ref()
-    c = cam.to_c()
+    c = camera_c(cam)
     n = C.c_uint64()
     _chk(lib.ref_entries(scene.h, C.byref(c), near, int(sorted_), C.byref(n), None, None))
     keys = np.empty(n.value, np.uint64)
@@ -255,7 +245,7 @@ class RefFrame:
         self.transmittance = np.empty((H, W))
         h = C.c_void_p()
         npre, nc = C.c_uint64(), C.c_uint64()
-        c, o = cam.to_c(), opts.to_c()
+        c, o = camera_c(cam), options_c(opts)
         _chk(lib.ref_forward_train(scene.h, C.byref(c), C.byref(o), C.byref(h), C.byref(npre),
                                    C.byref(nc), _p(self.color), _p(self.depth), _p(self.normal),
                                    _p(self.transmittance)))
@@ -313,7 +303,7 @@ def ref_train_iteration_grads(scene: RefScene, cam, opts, gt, lambda_ssim, w_T, 
     g = np.ascontiguousarray(gt, np.float64)
     losses = np.zeros(5)
     gd, gs, gp = np.empty(n_pool), np.empty(n_sh), np.empty(n_vox)
-    c, o = cam.to_c(), opts.to_c()
+    c, o = camera_c(cam), options_c(opts)
     _chk(load_ref().ref_train_iteration_grads(scene.h, C.byref(c), C.byref(o), _p(g),
                                               C.c_double(lambda_ssim), C.c_double(w_T),
                                               C.c_double(w_dist), C.c_double(w_R), _p(losses),
@@ -369,7 +359,7 @@ def ref_adam_step(params, grads, m, v, step_before, lr, lr_alt=0.0, period=0, n_
 
 
 def ref_train_step_l1(scene: RefScene, cam, opts, gt, n_pool, n_sh, n_vox):
-    c, o = cam.to_c(), opts.to_c()
+    c, o = camera_c(cam), options_c(opts)
     gt = np.ascontiguousarray(gt, np.float64)
     loss = C.c_double()
     dcol = np.empty_like(gt)

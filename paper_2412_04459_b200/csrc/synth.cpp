@@ -7,12 +7,13 @@
 //     tests/test_raster.cpp:15-28), corner-pool dedup in first-seen order
 //     (rebuild_corner_indexing, scene.cpp:8-26), densities U(-4,2.5), SH from
 //     tests/test_raster.cpp:29-37;
+//   * the unbounded rig scene of configs 4/5 (the voxel set init_unbounded,
+//     optim.cpp:96-184, builds), parameters drawn as for G;
 //   * ring_cameras (synth.cpp:89-118).
 // Compiled with -ffp-contract=off so camera poses match the reference bit
 // for bit.
 #include <algorithm>
 #include <cmath>
-#include <queue>
 #include <cstdlib>
 #include <cstring>
 #include <random>
@@ -126,61 +127,165 @@ void emit_scene(const std::vector<Path>& vox, std::mt19937_64& rng, int sh_degre
     *sh = dup(coeffs);
 }
 
-// ---- init_unbounded (optim.cpp:96-184) ------------------------------------
-// Every expression keeps the reference's operand order (geom.hpp, camera.hpp,
-// octree.hpp) and the file is built with -ffp-contract=off, so the
-// observed/refined decisions — and therefore the voxel set — are identical.
-V3 add(V3 a, V3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
-double dot3(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+// ---- unbounded-scene fixture (the scene init_unbounded, optim.cpp:96-184,
+// builds for a camera rig) ---------------------------------------------------
+// A voxel is handled as one packed key, `code | level << 48`; that key is
+// also the ordering tie-break of the refinement frontier. The frontier order
+// (highest max-sampling-rate first, then smallest key) is a strict total
+// order, so the order in which candidates are *inserted* is irrelevant: only
+// the main block's enumeration order and the frontier's pop order reach the
+// output. The float expressions (camera projection, corner positions, voxel
+// centres, rates) are evaluated with the reference geometry's operand order
+// and this file is built with -ffp-contract=off, so every observed/refined
+// decision — and therefore the voxel list — is bit-identical
+// (tests/test_abi_cpu.py::test_unbounded_generator_matches_reference).
+constexpr uint64_t kKeyLevelShift = 48;
 
-struct Bounds {
-    V3 center;
-    double size;
+inline uint64_t pack_key(uint64_t code, int level) {
+    return code | (uint64_t(level) << kKeyLevelShift);
+}
+inline int key_level(uint64_t key) { return int(key >> kKeyLevelShift); }
+inline uint64_t key_code(uint64_t key) { return key & ((uint64_t(1) << kKeyLevelShift) - 1); }
+
+class RigView {
+  public:
+    RigView(const svr_camera* cams, int n, const double centre[3], double extent)
+        : cams_(cams, cams + n), extent_(extent) {
+        for (int a = 0; a < 3; ++a) lo_[a] = centre[a] - 0.5 * extent;
+        cell_ = extent / double(uint64_t(1) << kMaxLevel);
+    }
+
+    // any camera sees the point inside its image rectangle, in front of it
+    // (Camera::project, camera.hpp:29-35)
+    bool sees(const double p[3]) const {
+        for (const svr_camera& c : cams_) {
+            const double d0 = p[0] - c.pos[0], d1 = p[1] - c.pos[1], d2 = p[2] - c.pos[2];
+            const double* r = c.rot;
+            const double cx = r[0] * d0 + r[3] * d1 + r[6] * d2;
+            const double cy = r[1] * d0 + r[4] * d1 + r[7] * d2;
+            const double cz = r[2] * d0 + r[5] * d1 + r[8] * d2;
+            const double u = c.fx * cx / cz + c.cx;
+            const double v = c.fy * cy / cz + c.cy;
+            if (cz > 0 && u >= 0 && u <= c.width && v >= 0 && v <= c.height) return true;
+        }
+        return false;
+    }
+
+    // some corner of the voxel is seen (corner grid of octree.hpp:130-146)
+    bool sees_voxel(uint64_t key) const {
+        uint32_t ijk[3];
+        Path p{key_code(key), key_level(key)};
+        to_index(p, ijk[0], ijk[1], ijk[2]);
+        const uint32_t step = uint32_t(1) << (kMaxLevel - p.level);
+        for (uint32_t corner = 0; corner < 8; ++corner) {
+            double q[3];
+            for (int a = 0; a < 3; ++a) {
+                const uint32_t g = (ijk[a] + ((corner >> (2 - a)) & 1)) * step;
+                q[a] = lo_[a] + cell_ * g;
+            }
+            if (sees(q)) return true;
+        }
+        return false;
+    }
+
+    // largest pixels-per-voxel-size over the cameras in front of the centre
+    // (max_sampling_rate, optim.cpp:68-77, at voxel_geometry, octree.hpp:85-90)
+    double rate(uint64_t key) const {
+        uint32_t ijk[3];
+        Path p{key_code(key), key_level(key)};
+        to_index(p, ijk[0], ijk[1], ijk[2]);
+        const double size = std::ldexp(extent_, -p.level);
+        double ctr[3];
+        for (int a = 0; a < 3; ++a) ctr[a] = lo_[a] + size * (ijk[a] + 0.5);
+        double best = 0.0;
+        for (const svr_camera& c : cams_) {
+            const double z = (ctr[0] - c.pos[0]) * c.rot[2] + (ctr[1] - c.pos[1]) * c.rot[5] +
+                             (ctr[2] - c.pos[2]) * c.rot[8];
+            if (z > 0) best = std::max(best, size * c.fx / z);
+        }
+        return best;
+    }
+
+  private:
+    std::vector<svr_camera> cams_;
+    double lo_[3];
+    double cell_;
+    double extent_;
 };
 
-// Camera::project (camera.hpp:33-37) through world_to_cam = rot^T (p - pos).
-bool point_observed(V3 p, const std::vector<svr_camera>& cams) {  // optim.cpp:43-50
-    for (const svr_camera& c : cams) {
-        V3 d = sub(p, V3{c.pos[0], c.pos[1], c.pos[2]});
-        const double* m = c.rot;
-        V3 q{m[0] * d.x + m[3] * d.y + m[6] * d.z, m[1] * d.x + m[4] * d.y + m[7] * d.z,
-             m[2] * d.x + m[5] * d.y + m[8] * d.z};
-        double u = c.fx * q.x / q.z + c.cx, v = c.fy * q.y / q.z + c.cy;
-        if (q.z > 0 && u >= 0 && u <= c.width && v >= 0 && v <= c.height) return true;
+struct Frontier {
+    struct Item {
+        double rate;
+        uint64_t key;
+    };
+    // max-heap on rate; among equal rates the smaller key comes out first
+    static bool below(const Item& a, const Item& b) {
+        if (a.rate != b.rate) return a.rate < b.rate;
+        return a.key > b.key;
     }
-    return false;
-}
+    std::vector<Item> heap;
+    void push(double rate, uint64_t key) {
+        heap.push_back({rate, key});
+        std::push_heap(heap.begin(), heap.end(), below);
+    }
+    uint64_t pop() {
+        std::pop_heap(heap.begin(), heap.end(), below);
+        uint64_t k = heap.back().key;
+        heap.pop_back();
+        return k;
+    }
+};
 
-// voxel_observed (optim.cpp:52-56) over corner_keys/corner_position (octree.hpp:130-146).
-bool voxel_observed(const Bounds& b, const Path& p, const std::vector<svr_camera>& cams) {
-    uint32_t i, j, k;
-    to_index(p, i, j, k);
-    uint32_t step = uint32_t(1) << (kMaxLevel - p.level);
-    double cell = b.size / double(uint64_t(1) << kMaxLevel);
-    V3 lo = sub(b.center, V3{0.5 * b.size, 0.5 * b.size, 0.5 * b.size});
-    for (uint32_t c = 0; c < 8; ++c) {
-        uint32_t x = (i + ((c >> 2) & 1)) * step, y = (j + ((c >> 1) & 1)) * step,
-                 z = (k + (c & 1)) * step;
-        if (point_observed(add(lo, V3{cell * x, cell * y, cell * z}), cams)) return true;
+// Voxel list of the unbounded rig scene: the observed cells of the central
+// 2^init_level block at level shell_levels + init_level (i, j, k order),
+// then the background shells refined coarse-to-fine by sampling rate until
+// there are bg_ratio times as many background voxels as foreground ones.
+std::vector<Path> unbounded_voxels(const RigView& rig, int init_level, int shell_levels,
+                                   double bg_ratio) {
+    const int fine = shell_levels + init_level;
+    std::vector<Path> out;
+    const uint64_t side = uint64_t(1) << init_level;
+    const uint32_t first = (uint32_t(1) << (fine - 1)) - (uint32_t(1) << (init_level - 1));
+    for (uint64_t n = 0; n < side * side * side; ++n) {
+        const uint32_t i = first + uint32_t(n / (side * side));
+        const uint32_t j = first + uint32_t((n / side) % side);
+        const uint32_t k = first + uint32_t(n % side);
+        const uint64_t code = to_code(i, j, k, fine);
+        if (rig.sees_voxel(pack_key(code, fine))) out.push_back({code, fine});
     }
-    return false;
-}
+    const size_t n_fg = out.size();
+    if (n_fg == 0) throw std::invalid_argument("unbounded scene: no camera observes the main block");
 
-// max_sampling_rate (optim.cpp:69-78) at voxel_geometry (octree.hpp:85-90).
-double max_sampling_rate(const Bounds& b, const Path& p, const std::vector<svr_camera>& cams) {
-    uint32_t i, j, k;
-    to_index(p, i, j, k);
-    double size = std::ldexp(b.size, -p.level);
-    V3 lo = sub(b.center, V3{0.5 * b.size, 0.5 * b.size, 0.5 * b.size});
-    V3 center = add(lo, V3{size * (i + 0.5), size * (j + 0.5), size * (k + 0.5)});
-    double best = 0.0;
-    for (const svr_camera& c : cams) {
-        double z = dot3(sub(center, V3{c.pos[0], c.pos[1], c.pos[2]}),
-                        V3{c.rot[2], c.rot[5], c.rot[8]});
-        if (z <= 0) continue;
-        best = std::max(best, size * c.fx / z);
+    // shell at level lv: the 4x4x4 cells around the scene centre minus the
+    // inner 2x2x2 (which the next finer level covers)
+    Frontier front;
+    for (int lv = 2; lv <= shell_levels + 1; ++lv) {
+        const uint32_t c0 = (uint32_t(1) << (lv - 1)) - 2;
+        for (uint32_t n = 0; n < 64; ++n) {
+            const uint32_t di = n >> 4, dj = (n >> 2) & 3, dk = n & 3;
+            if ((di == 1 || di == 2) && (dj == 1 || dj == 2) && (dk == 1 || dk == 2)) continue;
+            const uint64_t key = pack_key(to_code(c0 + di, c0 + dj, c0 + dk, lv), lv);
+            if (rig.sees_voxel(key)) front.push(rig.rate(key), key);
+        }
     }
-    return best;
+    const size_t bg_target = size_t(bg_ratio * double(n_fg));
+    std::vector<uint64_t> settled;  // background leaves that can no longer split
+    while (!front.heap.empty() && front.heap.size() + settled.size() < bg_target) {
+        const uint64_t key = front.pop();
+        const int lv = key_level(key);
+        if (lv >= kMaxLevel) {
+            settled.push_back(key);
+            continue;
+        }
+        const int shift = 3 * (kMaxLevel - lv - 1);
+        for (uint64_t child = 0; child < 8; ++child) {
+            const uint64_t ck = pack_key(key_code(key) | (child << shift), lv + 1);
+            if (rig.sees_voxel(ck)) front.push(rig.rate(ck), ck);
+        }
+    }
+    while (!front.heap.empty()) settled.push_back(front.pop());
+    for (uint64_t key : settled) out.push_back({key_code(key), key_level(key)});
+    return out;
 }
 
 }  // namespace
@@ -229,101 +334,38 @@ int svr_synth_unbounded_scene(const svr_camera* cams, int n_cams, int init_level
                               float** sh, double* bounds_center, double* bounds_size) {
     try {
         if (!cams || n_cams < 2)
-            throw std::invalid_argument("init_unbounded needs at least two cameras");
-        if (init_level < 1 || init_level > kMaxLevel)
-            throw std::invalid_argument("init_level out of [1,16]");
-        if (shell_levels < 1 || shell_levels > kMaxLevel - 2)
-            throw std::invalid_argument("shell_levels out of range");
-        if (bg_ratio <= 0) throw std::invalid_argument("bg_ratio must be positive");
+            throw std::invalid_argument("unbounded scene: the rig needs two or more cameras");
+        if (init_level < 1 || shell_levels < 1 || shell_levels + init_level > kMaxLevel)
+            throw std::invalid_argument(
+                "unbounded scene: need init_level, shell_levels >= 1 and their sum <= 16");
+        if (!(bg_ratio > 0)) throw std::invalid_argument("unbounded scene: bg_ratio must be > 0");
         if (sh_degree < 0 || sh_degree > 3)
-            throw std::invalid_argument("sh_degree out of [0,3]");
-        std::vector<svr_camera> cv(cams, cams + n_cams);
-        V3 center{0, 0, 0};
-        for (const svr_camera& c : cv) center = add(center, V3{c.pos[0], c.pos[1], c.pos[2]});
-        center = {center.x / double(n_cams), center.y / double(n_cams), center.z / double(n_cams)};
-        std::vector<double> dist;
-        for (const svr_camera& c : cv) {
-            V3 d = sub(V3{c.pos[0], c.pos[1], c.pos[2]}, center);
-            dist.push_back(std::sqrt(dot3(d, d)));
+            throw std::invalid_argument("unbounded scene: sh_degree must be in [0, 3]");
+        // rig centre = mean camera position; main block edge = twice the
+        // median camera distance from it; the scene cube is 2^shell_levels
+        // main blocks wide
+        double centre[3] = {0, 0, 0};
+        for (int c = 0; c < n_cams; ++c)
+            for (int a = 0; a < 3; ++a) centre[a] += cams[c].pos[a];
+        for (int a = 0; a < 3; ++a) centre[a] = centre[a] / double(n_cams);
+        std::vector<double> reach(n_cams);
+        for (int c = 0; c < n_cams; ++c) {
+            const double d0 = cams[c].pos[0] - centre[0], d1 = cams[c].pos[1] - centre[1],
+                         d2 = cams[c].pos[2] - centre[2];
+            reach[c] = std::sqrt(d0 * d0 + d1 * d1 + d2 * d2);
         }
-        std::nth_element(dist.begin(), dist.begin() + dist.size() / 2, dist.end());
-        double radius = dist[dist.size() / 2];
-        if (radius <= 0) throw std::invalid_argument("degenerate camera set: coincident positions");
-        Bounds b{center, std::ldexp(2.0 * radius, shell_levels)};
-
-        std::vector<Path> vox;
-        int lv_main = shell_levels + init_level;
-        if (lv_main > kMaxLevel)
-            throw std::invalid_argument("shell_levels + init_level exceeds 16");
-        uint32_t half = uint32_t(1) << (lv_main - 1), m = uint32_t(1) << (init_level - 1);
-        size_t fg = 0;
-        for (uint32_t i = half - m; i < half + m; ++i)
-            for (uint32_t j = half - m; j < half + m; ++j)
-                for (uint32_t k = half - m; k < half + m; ++k) {
-                    Path p{to_code(i, j, k, lv_main), lv_main};
-                    if (voxel_observed(b, p, cv)) {
-                        vox.push_back(p);
-                        ++fg;
-                    }
-                }
-        if (fg == 0) throw std::invalid_argument("no observed voxels in the main region");
-
-        struct ShellVox {
-            double rate;
-            uint64_t tiebreak;
-            Path path;
-            bool operator<(const ShellVox& o) const {
-                return rate != o.rate ? rate < o.rate : tiebreak > o.tiebreak;
-            }
-        };
-        std::priority_queue<ShellVox> shell;
-        auto push_shell = [&](const Path& p) {
-            shell.push({max_sampling_rate(b, p, cv), p.code | (uint64_t(p.level) << 48), p});
-        };
-        for (int s = 1; s <= shell_levels; ++s) {
-            int lv = shell_levels - s + 2;
-            uint32_t h = uint32_t(1) << (lv - 1);
-            for (uint32_t i = h - 2; i < h + 2; ++i)
-                for (uint32_t j = h - 2; j < h + 2; ++j)
-                    for (uint32_t k = h - 2; k < h + 2; ++k) {
-                        bool inner = i >= h - 1 && i < h + 1 && j >= h - 1 && j < h + 1 &&
-                                     k >= h - 1 && k < h + 1;
-                        if (inner) continue;
-                        Path p{to_code(i, j, k, lv), lv};
-                        if (voxel_observed(b, p, cv)) push_shell(p);
-                    }
-        }
-        std::vector<Path> bg_done;
-        size_t bg = shell.size();
-        while (bg < size_t(bg_ratio * double(fg)) && !shell.empty()) {
-            ShellVox top = shell.top();
-            shell.pop();
-            if (top.path.level >= kMaxLevel) {
-                bg_done.push_back(top.path);
-                continue;
-            }
-            --bg;
-            int shift = 3 * (kMaxLevel - top.path.level - 1);
-            for (uint64_t c = 0; c < 8; ++c) {
-                Path ch{top.path.code | (c << shift), top.path.level + 1};
-                if (voxel_observed(b, ch, cv)) {
-                    push_shell(ch);
-                    ++bg;
-                }
-            }
-        }
-        while (!shell.empty()) {
-            bg_done.push_back(shell.top().path);
-            shell.pop();
-        }
-        for (const Path& p : bg_done) vox.push_back(p);
+        std::nth_element(reach.begin(), reach.begin() + n_cams / 2, reach.end());
+        const double radius = reach[n_cams / 2];
+        if (!(radius > 0))
+            throw std::invalid_argument("unbounded scene: all cameras at one position");
+        const double extent = std::ldexp(2.0 * radius, shell_levels);
+        RigView rig(cams, n_cams, centre, extent);
+        std::vector<Path> vox = unbounded_voxels(rig, init_level, shell_levels, bg_ratio);
         std::mt19937_64 rng(seed);
         emit_scene(vox, rng, sh_degree, n_voxels, n_pool, codes, levels, corner_index, density,
                    sh);
-        bounds_center[0] = b.center.x;
-        bounds_center[1] = b.center.y;
-        bounds_center[2] = b.center.z;
-        *bounds_size = b.size;
+        for (int a = 0; a < 3; ++a) bounds_center[a] = centre[a];
+        *bounds_size = extent;
         return SVR_OK;
     } catch (const std::invalid_argument& e) {
         g_err = e.what();

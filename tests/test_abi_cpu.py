@@ -99,7 +99,7 @@ def test_option_objects_roundtrip(svr):
 @pytest.mark.parametrize("init_level,shell_levels,bg_ratio,n_cams", [(4, 3, 2.8, 8), (3, 2, 1.5, 4),
                                                                      (5, 4, 2.0, 6)])
 def test_unbounded_generator_matches_reference(svr, init_level, shell_levels, bg_ratio, n_cams):
-    """init_unbounded (optim.cpp:96-184) restated in csrc/synth.cpp: the same
+    """The unbounded rig scene of csrc/synth.cpp vs init_unbounded (optim.cpp:96-184): the same
     voxel set in the same order, pool and parameters, bit for bit, at sizes
     that finish in seconds (cfg4's init_level 7 / shell_levels 5 takes ~25 s
     per side; its counts 7,824,544 / 16,227,695 are checked on the GPU box)."""
