@@ -227,6 +227,29 @@ def ref_entries(scene: RefScene, cam, sorted_: bool, near: float = 1e-6):
     return keys, vals
 
 
+def ref_entries_both(scene: RefScene, cam, near: float = 1e-6):
+    """(emitted keys, values, sorted keys, values) of one view, the entry
+    list built once (build_sort_entries, then sort_entries on the same list)."""
+    lib = load_ref()
+    lib.ref_entries_begin.argtypes = [C.c_void_p, C.POINTER(abi.svr_camera), C.c_double,
+                                      C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)]
+    lib.ref_entries_copy.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+    lib.ref_entries_end.argtypes = [C.c_void_p]
+    lib.ref_entries_end.restype = None
+    c = camera_c(cam)
+    h, n = C.c_void_p(), C.c_uint64()
+    _chk(lib.ref_entries_begin(scene.h, C.byref(c), near, C.byref(h), C.byref(n)))
+    try:
+        out = []
+        for sort_first in (0, 1):
+            k, v = np.empty(n.value, np.uint64), np.empty(n.value, np.uint32)
+            _chk(lib.ref_entries_copy(h, sort_first, _p(k), _p(v)))
+            out += [k, v]
+    finally:
+        lib.ref_entries_end(h)
+    return tuple(out)
+
+
 def ref_sort_entries(keys, vals):
     k = np.ascontiguousarray(keys, np.uint64).copy()
     v = np.ascontiguousarray(vals, np.uint32).copy()

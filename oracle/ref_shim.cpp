@@ -358,6 +358,32 @@ int ref_entries(void* h, const svr_camera* c, double near, int sorted, uint64_t*
     });
 }
 
+// Entry list of one view held on the reference side, so a large view
+// (config 4: ~97M entries) is built once and read back emitted, then sorted.
+int ref_entries_begin(void* h, const svr_camera* c, double near, void** out, uint64_t* n_out) {
+    return guarded([&] {
+        auto* s = static_cast<SparseScene*>(h);
+        Camera cam = to_cam(c);
+        auto pre = preprocess_public(*s, cam, near);
+        auto* e = new std::vector<SortEntry>(build_sort_entries(pre, cam, *s));
+        *out = e;
+        *n_out = e->size();
+    });
+}
+
+int ref_entries_copy(void* h, int sort_first, uint64_t* keys, uint32_t* values) {
+    return guarded([&] {
+        auto* e = static_cast<std::vector<SortEntry>*>(h);
+        if (sort_first) sort_entries(*e);
+        for (size_t i = 0; i < e->size(); ++i) {
+            keys[i] = (*e)[i].key;
+            values[i] = (*e)[i].value;
+        }
+    });
+}
+
+void ref_entries_end(void* h) { delete static_cast<std::vector<SortEntry>*>(h); }
+
 int ref_sort_entries(uint64_t n, uint64_t* keys, uint32_t* values) {
     return guarded([&] {
         std::vector<SortEntry> e(n);

@@ -279,6 +279,22 @@ int plan_sort(int max_level, int ntiles, uint32_t pattern_or, RadixPass* passes)
     return np;
 }
 
+bool packed_keys_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SVR_PACKED_KEYS");
+        return e == nullptr || e[0] != '0';
+    }();
+    return on;
+}
+
+bool rank_keys_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SVR_RANK_KEYS");
+        return e == nullptr || e[0] != '0';
+    }();
+    return on;
+}
+
 void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
                  const svr_render_options* opts, svr_frame* f, bool allow_deferred = true) {
     require(ctx && scene && cam_in && opts && f, SVR_ERR_INVALID_ARGUMENT, "null argument");
@@ -397,8 +413,16 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     // live count on the device. Needs a capacity and the pattern-independent
     // sort plan of the rank-keyed packed format (never for training frames,
     // whose record buffers are sized from the contribution count).
+    // Morton-rank keys: tile | rank(s, vid) | s | vid, sorted on tile|rank only.
+    const int tile_bits = bit_width(uint64_t(ntiles - 1));
+    const int vb = std::max(1, bit_width(N > 0 ? N - 1 : 0));
+    const int rb = scene->rank_bits;
+    const bool use_rank = rank_keys_enabled() && N > 0 && rb > 0 && (vb + 3 + rb + tile_bits) <= 64;
+    // A frame whose rank keys do not fit in 64 bits (e.g. > 2^23 voxels at
+    // 1024^2, 8160 tiles at 1080p with 7.8M voxels) or with packed keys
+    // switched off reads E back synchronously instead.
     const bool deferred = allow_deferred && ctx->async_frames && !f->training && !ctx->debug &&
-                          f->e_cap > 0 && scene->rank_bits > 0;
+                          f->e_cap > 0 && use_rank && packed_keys_enabled();
     uint64_t E;
     uint32_t pattern_or = 0;
     if (deferred) {
@@ -420,22 +444,9 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     // histograms fused into the duplicate kernel. Otherwise the general
     // (u64 key, u32 value) path. Both reproduce the reference's emission
     // order (vid, ty, tx, s) and its (key, value) sort order.
-    const int tile_bits = bit_width(uint64_t(ntiles - 1));
-    const int vb = std::max(1, bit_width(N > 0 ? N - 1 : 0));
     const int lmax = scene->max_level;
     const bool multi = __builtin_popcount(pattern_or) > 1;
-    static const bool packed_enabled = [] {
-        const char* e = std::getenv("SVR_PACKED_KEYS");
-        return e == nullptr || e[0] != '0';
-    }();
-    static const bool rank_enabled = [] {
-        const char* e = std::getenv("SVR_RANK_KEYS");
-        return e == nullptr || e[0] != '0';
-    }();
-    // Morton-rank keys: tile | rank(s, vid) | s | vid, sorted on tile|rank only.
-    const int rb = scene->rank_bits;
-    const bool use_rank = rank_enabled && N > 0 && rb > 0 && (vb + 3 + rb + tile_bits) <= 64;
-    f->packed = packed_enabled && N > 0 && (use_rank || (vb + 3 + 3 * lmax + tile_bits) <= 64);
+    f->packed = packed_keys_enabled() && N > 0 && (use_rank || (vb + 3 + 3 * lmax + tile_bits) <= 64);
     require(!deferred || (f->packed && use_rank), SVR_ERR_RUNTIME, "deferred frame needs rank keys");
     uint2* ranges = grow<uint2>(f->ranges, ntiles);
     RadixPass passes[kMaxRadixPasses];
@@ -640,7 +651,11 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     mark(ctx, -1);
     f->n_visible = ~uint64_t(0);  // computed lazily
     if (deferred) {
-        launch_status_to_host(status, hs, st, f->e_cap, grow<unsigned int>(ctx->overflow_count, 1));
+        if (!ctx->overflow_count.p) {  // the context's counter starts at zero
+            grow<unsigned int>(ctx->overflow_count, 1);
+            SVR_CUDA(cudaMemsetAsync(ctx->overflow_count.p, 0, sizeof(unsigned int), st));
+        }
+        launch_status_to_host(status, hs, st, f->e_cap, ctx->overflow_count.as<unsigned int>());
         if (!f->done) SVR_CUDA(cudaEventCreateWithFlags(&f->done, cudaEventDisableTiming));
         SVR_CUDA(cudaEventRecord(f->done, st));  // settle this frame without draining the stream
     }
@@ -1356,7 +1371,9 @@ int svr_frame_wait(svr_frame* f) {
 
 int svr_frame_device_ptr(svr_frame* f, svr_buffer which, void** ptr, size_t* bytes) {
     return guard([&] {
+        require(f && f->ctx && ptr && bytes, SVR_ERR_INVALID_ARGUMENT, "null argument");
         set_device(f->ctx);
+        resolve_frame(f);  // the pointer must address a complete frame's buffer
         BufView b = frame_buffer(f, which);
         *ptr = const_cast<void*>(b.p);
         *bytes = b.bytes;
@@ -1406,7 +1423,10 @@ int svr_render_backward(svr_ctx* ctx, const svr_scene* scene, svr_frame* frame,
 int svr_l1_loss(svr_ctx* ctx, svr_frame* f, const float* gt, float* d_color, float* loss) {
     return guard([&] {
         require(ctx && f && gt && d_color, SVR_ERR_INVALID_ARGUMENT, "null argument");
+        require(f->scene, SVR_ERR_INVALID_ARGUMENT, "frame has not been rendered");
         set_device(ctx);
+        wait_copies(f);
+        resolve_frame(f);
         launch_l1_loss(f->out_color.as<float>(), gt, uint64_t(f->W) * f->H * 3, d_color, loss,
                        ctx->stream);
     });
@@ -1500,6 +1520,7 @@ int svr_image_losses(svr_ctx* ctx, svr_frame* f, const float* gt, double w_mse, 
                 "ssim: images smaller than the 11x11 window");
         set_device(ctx);
         wait_copies(f);
+        resolve_frame(f);  // losses of a complete frame, never of an outgrown deferred one
         cudaStream_t st = ctx->stream;
         const uint64_t n = uint64_t(f->W) * f->H * 3;
         ImageLossArgs a{};

@@ -708,7 +708,7 @@ __global__ void tile_ranges_packed_kernel(const uint64_t* __restrict__ keys, uin
                                           const unsigned long long* n_dev) {
     pdl_enter();
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (n_dev) n = min(n, uint64_t(*n_dev));  // deferred-E frame: the device count decides
+    n = live_entries(n, n_dev);  // deferred-E frame: the device count decides
     if (i >= n) return;
     const uint64_t k = keys[i];
     const uint32_t t = uint32_t(k >> fmt.tile_shift);
@@ -1234,12 +1234,10 @@ void launch_tile_setup(const DevCamera& cam, uint8_t* masks, uint32_t* sat, Fram
     const int ncell = (cam.ntx + 1) * (cam.nty + 1);
     const int use_smem = ncell <= kSatSmemMax;
     const size_t smem = use_smem ? size_t(ncell) * 4 : 0;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::atomic<uint64_t> attr_set{0};
+    if (first_on_device(attr_set))
         SVR_CUDA(cudaFuncSetAttribute(tile_setup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kSatSmemMax * 4));
-        attr_set = true;
-    }
     // masks: one thread per tile (fp64 corner rays); then the SAT in one CTA
     const int ntiles = cam.ntx * cam.nty;
     launch_pdl(tile_masks_kernel, blocks_for(ntiles, 128), 128, 0, st, cam, masks);
@@ -1404,14 +1402,13 @@ void launch_tile_order(uint2* ranges, int ntiles, uint32_t* order, cudaStream_t 
 void launch_composite(const DevCamera& cam, const CompositeArgs& a, bool record_pass,
                       cudaStream_t st) {
     const unsigned ntiles = unsigned(cam.ntx * cam.nty);
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::atomic<uint64_t> attr_set{0};
+    if (first_on_device(attr_set)) {
         for (auto fn : {composite_kernel<1, 0>, composite_kernel<1, 1>, composite_kernel<1, 2>,
                         composite_kernel<1, 3>, composite_kernel<2, 0>, composite_kernel<2, 1>,
                         composite_kernel<2, 2>, composite_kernel<2, 3>, composite_kernel<3, 0>,
                         composite_kernel<3, 1>, composite_kernel<3, 2>, composite_kernel<3, 3>})
             SVR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCompSmem)));
-        attr_set = true;
     }
     const int mode = record_pass ? 1 : a.max_blend ? 2 : a.stage_entry ? 3 : 0;
 #define SVR_COMPOSITE_CASE(KK)                                                          \

@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kThreads) hist_kernel(const uint64_t* keys, co
                                                         uint32_t* hist,
                                                         const unsigned long long* n_dev) {
     pdl_enter();
-    if (n_dev) n = min(n, uint64_t(*n_dev));
+    n = live_entries(n, n_dev);  // deferred-E frame: the device count decides
     __shared__ uint32_t s_hist[kMaxRadixPasses][kRadix];
     for (int i = threadIdx.x; i < spec.n * kRadix; i += kThreads) (&s_hist[0][0])[i] = 0;
     __syncthreads();
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
         (&s_warp_hist[0][0])[i] = 0;
     __syncthreads();
     const uint32_t part = s_part;
-    if (n_dev) n = min(n, uint64_t(*n_dev));
+    n = live_entries(n, n_dev);  // deferred-E frame: the device count decides
     const uint64_t base = uint64_t(part) * Part<PAIRS, IK>::keys;
     if (base >= n && part > 0) return;  // past the live count: no later partition looks back here
     const uint64_t wbase = base + uint64_t(warp) * 32 * Part<PAIRS, IK>::items;

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -43,6 +44,17 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
     cuda_check(cudaLaunchKernelEx(&cfg, kernel, KArgs(args)...), "cudaLaunchKernelEx");
 }
 #define SVR_CUDA(x) ::svrb::cuda_check((x), #x)
+
+// Function attributes (the dynamic shared-memory opt-in) are per device:
+// true the first time the current device asks through `flags` (one bit per
+// device ordinal; concurrent first calls may both see true, and setting an
+// attribute twice is harmless).
+inline bool first_on_device(std::atomic<uint64_t>& flags) {
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    const uint64_t bit = uint64_t(1) << (dev & 63);
+    return (flags.fetch_or(bit) & bit) == 0;
+}
 #define SVR_LAUNCH(what) (::svrb::count_launch(), ::svrb::cuda_check(cudaGetLastError(), what))
 
 // Stages timed by svr_ctx_stage_times (CUDA events on the context stream).

@@ -47,6 +47,16 @@ __device__ __forceinline__ void pdl_enter() {
 inline void pdl_enter() {}
 #endif
 
+// Live entry count of a deferred-E frame (capacity `cap`, device count
+// `*n_dev`). A frame that outgrew its capacity emitted only a prefix of its
+// entries (the rest of the buffer holds stale keys of earlier frames), so it
+// sorts and composites nothing; the host re-renders it when it is consumed.
+SVR_HD uint64_t live_entries(uint64_t cap, const unsigned long long* n_dev) {
+    if (!n_dev) return cap;
+    const uint64_t d = uint64_t(*n_dev);
+    return d > cap ? 0 : d;
+}
+
 // ---------------------------------------------------------------- fp64 exact
 #if defined(__CUDA_ARCH__)
 SVR_HD double dadd(double a, double b) { return __dadd_rn(a, b); }

@@ -5,12 +5,17 @@ SURVEY §8(e).
   and renders its own subset of the views; no collective on the data path.
 * View-batch training step (config 5): every rank runs forward -> L1 ->
   backward for its views into ONE flat gradient buffer
-  [density (P) | SH (N*stride)] and the ranks sum it with a single in-place
-  all-reduce (NCCL over NVLink on B200s; gloo in the CPU tests).
+  [density (P) | SH (N*stride) | priority (N)] and the ranks sum it with a
+  single in-place all-reduce (NCCL over NVLink on B200s; gloo in the tests),
+  so every replica sees the same gradients and the same subdivision
+  priorities.
 
 One process per GPU (torch.distributed for the plumbing). The reference has
 no distributed code; the sum of per-view `render_backward` gradients is the
-oracle (tests/test_multiview_cpu.py, tests/test_gpu_multiview.py).
+oracle (tests/test_multiview_cpu.py: host logic over gloo on CPU;
+tests/test_gpu_multiview.py: two ranks sharing one GPU over gloo against the
+single-process sum and the reference; tests/test_gpu_fullsize.py: the
+config-5 batch sum against the reference).
 """
 from __future__ import annotations
 
@@ -27,10 +32,13 @@ def shard_views(n_views: int, rank: int, world: int) -> List[int]:
     return list(range(rank, n_views, world))
 
 
-def flat_layout(n_pool: int, n_sh: int, align: int = 64):
-    """Offsets (in floats) of the density and SH gradients in the flat buffer."""
-    sh_off = (n_pool + align - 1) // align * align
-    return 0, sh_off, sh_off + n_sh
+def flat_layout(n_pool: int, n_sh: int, n_vox: int = 0, align: int = 64):
+    """Offsets (in floats) of the density, SH and priority gradients in the
+    flat buffer, and its total length: (0, sh_off, prio_off, total)."""
+    up = lambda x: (x + align - 1) // align * align  # noqa: E731
+    sh_off = up(n_pool)
+    prio_off = up(sh_off + n_sh)
+    return 0, sh_off, prio_off, prio_off + n_vox
 
 
 def allreduce_flat(buf, group=None) -> None:
@@ -58,13 +66,13 @@ class ShardedTrainer:
         self.gts = [g if isinstance(g, torch.Tensor) else
                     torch.tensor(np.asarray(g), dtype=torch.float32, device=dev) for g in gts]
         a = scene.arrays
-        self.n_pool, self.n_sh = a.n_pool, a.n_voxels * a.sh_stride
-        d0, s0, total = flat_layout(self.n_pool, self.n_sh)
+        self.n_pool, self.n_sh, self.n_vox = a.n_pool, a.n_voxels * a.sh_stride, a.n_voxels
+        d0, s0, p0, total = flat_layout(self.n_pool, self.n_sh, self.n_vox)
         self.flat = torch.zeros(total, dtype=torch.float32, device=dev)
-        self.priority = torch.zeros(a.n_voxels, dtype=torch.float32, device=dev)
         self.loss = torch.zeros(1, dtype=torch.float32, device=dev)
         self.density_grad = self.flat[d0:d0 + self.n_pool]
         self.sh_grad = self.flat[s0:s0 + self.n_sh]
+        self.priority = self.flat[p0:p0 + self.n_vox]
         self.frame = svr.Frame(ctx)
         self.stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
 
@@ -79,7 +87,6 @@ class ShardedTrainer:
         if not view_ids:  # no view on this rank: contribute zeros to the sum
             with torch.cuda.stream(self.stream):
                 self.flat.zero_()
-                self.priority.zero_()
         total = 0.0
         for n, v in enumerate(view_ids):
             c, o = self.cams[v].to_c(), self.opts.to_c()
@@ -96,10 +103,9 @@ class ShardedTrainer:
             allreduce_flat(self.flat, self.group)
         return float(loss_t.item())
 
-
-def sum_gradients_reference(per_view_grads: Sequence[dict]) -> dict:
-    """Oracle for the all-reduce: element-wise sum of per-view gradients."""
-    out = {}
-    for k in ("density", "sh", "priority"):
-        out[k] = np.sum([np.asarray(g[k], np.float64).reshape(-1) for g in per_view_grads], axis=0)
-    return out
+    def gradients(self) -> dict:
+        """The (reduced) gradients of the last step as host float32 arrays."""
+        import torch
+        torch.cuda.current_stream().wait_stream(self.stream)
+        return {"density": self.density_grad.cpu().numpy(), "sh": self.sh_grad.cpu().numpy(),
+                "priority": self.priority.cpu().numpy()}

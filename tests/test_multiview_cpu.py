@@ -12,8 +12,13 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2412_04459_b200.multiview import (allreduce_flat, flat_layout, shard_views,
-                                             sum_gradients_reference)
+from paper_2412_04459_b200.multiview import allreduce_flat, flat_layout, shard_views
+
+
+def sum_gradients_reference(per_view_grads):
+    """Oracle for the all-reduce: element-wise sum of per-view gradients."""
+    return {k: np.sum([np.asarray(g[k], np.float64).reshape(-1) for g in per_view_grads], axis=0)
+            for k in ("density", "sh", "priority")}
 
 
 def test_shard_views_partition():
@@ -55,11 +60,12 @@ def _worker(rank, world, port, out_path):
     for v in shard_views(4, rank, world):
         a, g = _per_view_grads(v)
         n_pool, n_sh = a.n_pool, a.n_voxels * a.sh_stride
-        d0, s0, total = flat_layout(n_pool, n_sh)
+        d0, s0, p0, total = flat_layout(n_pool, n_sh, a.n_voxels)
         if flat is None:
             flat = torch.zeros(total, dtype=torch.float64)
         flat[d0:d0 + n_pool] += torch.from_numpy(g["density"])
         flat[s0:s0 + n_sh] += torch.from_numpy(g["sh"].reshape(-1))
+        flat[p0:p0 + a.n_voxels] += torch.from_numpy(g["priority"])
     allreduce_flat(flat)
     if rank == 0:
         np.save(out_path, flat.numpy())
@@ -73,7 +79,8 @@ def test_sharded_gradient_allreduce_equals_sum(tmp_path):
     grads = [_per_view_grads(v)[1] for v in range(4)]
     a = _per_view_grads(0)[0]
     ref = sum_gradients_reference(grads)
-    d0, s0, total = flat_layout(a.n_pool, a.n_voxels * a.sh_stride)
+    d0, s0, p0, total = flat_layout(a.n_pool, a.n_voxels * a.sh_stride, a.n_voxels)
     assert np.allclose(flat[d0:d0 + a.n_pool], ref["density"], rtol=1e-12, atol=1e-15)
     assert np.allclose(flat[s0:s0 + a.n_voxels * a.sh_stride], ref["sh"], rtol=1e-12, atol=1e-15)
+    assert np.allclose(flat[p0:p0 + a.n_voxels], ref["priority"], rtol=1e-12, atol=1e-15)
     assert np.abs(ref["density"]).max() > 0
