@@ -11,22 +11,45 @@
 //   tile_sign_patterns  raster.cpp:120-142 svr_tile_sign_masks
 //   build_sort_entries  raster.cpp:144-172 svr_build_sort_entries (same emission order)
 //   sort_entries        raster.cpp:174-178 svr_sort_entries (onesweep radix sort)
-//   render(_with_pools) raster.cpp:205-301 svr_scene_upload + svr_render + downloads
+//   render(_with_pools) raster.cpp:205-301 cached device scene + svr_render + downloads
 //   render_backward     raster.cpp:303-423 svr_render_backward on the frame that
-//                                          produced the ForwardRecords
+//                                          produced the ForwardRecords, with the
+//                                          SH of `pools` (the clamp mask of
+//                                          sh_eval_backward, raster.cpp:414)
 //   render_oracle       raster.cpp:425-473 svr_render_oracle (fp64 brute force)
 //
 // Error behaviour: the C status codes are rethrown as the exception types the
 // reference throws (invalid_argument / length_error / runtime_error).
 // Threading: one svr_ctx per host thread (thread_local), device from
 // $SVR_DEVICE (default 0); all functions stay reentrant.
+//
+// Device scene cache. The reference API passes the scene by value on every
+// call (optim::train renders the same geometry with new pools each
+// iteration, optim.cpp:432-433, and its stats pass renders one unchanged
+// scene once per training view, optim.cpp:502-511). Each thread keeps the
+// last scene it uploaded; a call fingerprints the geometry (voxel paths,
+// corner indexing, bounds, SH degree) and the float parameters it would
+// upload, and re-sends only what changed: a new geometry is a full upload
+// (+ the Morton-rank tables), new parameters one svr_scene_set_params. The
+// fingerprints are content hashes computed on all host cores, so value
+// semantics are kept exactly (a caller mutating the scene in place is seen).
+//
+// Precision: PoolsD is double in the reference so a harness can rerun the
+// path in double on perturbed pools (raster.hpp:44-46, test_raster.cpp:
+// 444-502). The GPU path computes in fp32 (SURVEY §8(c) tolerances) and
+// narrows PoolsD to float on upload, exactly as it narrows SparseScene's
+// own float pools; a finite-difference harness with h ~ 1e-5 therefore
+// cannot be run through this library.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -93,17 +116,130 @@ svr_render_options to_c(const RenderOptions& o) {
     return r;
 }
 
-// Device copy of a SparseScene whose parameter pools come from PoolsD
-// (narrowed to the float the scene stores, so make_pools round-trips).
-struct SceneHandle {
+// ---- content fingerprints -------------------------------------------------
+// Four independent multiply-rotate lanes over 64-bit words (enough ILP to run
+// at memory speed), combined in order; ranges of large arrays are hashed on
+// all host cores and their digests folded left to right, so the value only
+// depends on the content.
+constexpr uint64_t kM1 = 0x9e3779b185ebca87ull, kM2 = 0xc2b2ae3d27d4eb4full,
+                   kM3 = 0x165667b19e3779f9ull;
+inline uint64_t rotl(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+inline uint64_t lane(uint64_t acc, uint64_t w) { return rotl(acc + w * kM2, 31) * kM1; }
+inline uint64_t fold(uint64_t h, uint64_t v) { return rotl(h ^ lane(0, v), 27) * kM1 + kM3; }
+
+uint64_t hash_words(const uint64_t* w, size_t n, uint64_t seed) {
+    uint64_t a = seed + kM1 + kM2, b = seed + kM2, c = seed, d = seed - kM1;
+    size_t i = 0;
+    for (; i + 4 <= n; i += 4) {
+        a = lane(a, w[i]);
+        b = lane(b, w[i + 1]);
+        c = lane(c, w[i + 2]);
+        d = lane(d, w[i + 3]);
+    }
+    uint64_t h = rotl(a, 1) + rotl(b, 7) + rotl(c, 12) + rotl(d, 18);
+    for (; i < n; ++i) h = fold(h, w[i]);
+    return fold(h, n);
+}
+
+// Runs fn(begin, end) over [0, n) split into contiguous ranges on up to 16
+// threads (one range below 2^20 items) and folds the per-range digests.
+uint64_t parallel_digest(size_t n, const std::function<uint64_t(size_t, size_t)>& fn) {
+    const size_t hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const size_t parts = n < (size_t(1) << 20) ? 1 : hw;
+    std::vector<uint64_t> d(parts);
+    std::vector<std::thread> th;
+    for (size_t p = 0; p < parts; ++p) {
+        const size_t b = n * p / parts, e = n * (p + 1) / parts;
+        if (p + 1 == parts)
+            d[p] = fn(b, e);
+        else
+            th.emplace_back([&, p, b, e] { d[p] = fn(b, e); });
+    }
+    for (auto& t : th) t.join();
+    uint64_t h = kM3 ^ n;
+    for (uint64_t x : d) h = fold(h, x);
+    return h;
+}
+
+uint64_t digest_bytes(const void* data, size_t bytes) {
+    const size_t nw = bytes / 8;
+    const auto* w = static_cast<const uint64_t*>(data);
+    uint64_t h = parallel_digest(nw, [&](size_t b, size_t e) { return hash_words(w + b, e - b, b); });
+    uint64_t tail = 0;
+    std::memcpy(&tail, static_cast<const char*>(data) + nw * 8, bytes - nw * 8);
+    return fold(fold(h, tail), bytes);
+}
+
+uint64_t geometry_digest(const SparseScene& scene) {
+    const size_t n = scene.voxel_count();
+    // OctPath has padding: hash its two fields, not its bytes
+    uint64_t hv = parallel_digest(n, [&](size_t b, size_t e) {
+        uint64_t h = b;
+        for (size_t i = b; i < e; ++i)
+            h = fold(h, scene.voxels[i].code ^ (uint64_t(uint32_t(scene.voxels[i].level)) << 56));
+        return h;
+    });
+    static_assert(sizeof(std::array<uint32_t, 8>) == 32, "corner_index layout");
+    uint64_t hc = n ? digest_bytes(scene.corner_index.data(), n * 32) : 0;
+    double b[4] = {scene.bounds.center.x, scene.bounds.center.y, scene.bounds.center.z,
+                   scene.bounds.size};
+    uint64_t h = fold(fold(hv, hc), digest_bytes(b, sizeof b));
+    return fold(fold(fold(h, uint64_t(scene.sh_degree)), scene.pool_count()), scene.sh.size());
+}
+
+// Parallel double -> float narrowing of a PoolsD vector.
+void narrow_into(const std::vector<double>& src, std::vector<float>& dst) {
+    dst.resize(src.size());
+    parallel_digest(src.size(), [&](size_t b, size_t e) {
+        for (size_t i = b; i < e; ++i) dst[i] = float(src[i]);
+        return uint64_t(0);
+    });
+}
+
+// The device copy of the last scene this thread rendered, with the
+// fingerprints of what it holds. Frames keep their scene alive through a
+// shared_ptr, so a cache replacement never frees a scene a ForwardRecords
+// still needs.
+struct DeviceScene {
     svr_scene* s = nullptr;
-    ~SceneHandle() {
+    uint64_t geo = 0, dens = 0, sh = 0;
+    size_t n_voxels = 0, n_pool = 0, n_sh = 0;
+    ~DeviceScene() {
         if (s) svr_scene_destroy(s);
     }
 };
 
-std::unique_ptr<SceneHandle> upload(const SparseScene& scene, const PoolsD& pools) {
+// The float parameters a call renders with: the scene's own pools (render)
+// or PoolsD narrowed to float (render_with_pools).
+struct Params {
+    const float* density;
+    size_t n_density;
+    const float* sh;
+    size_t n_sh;
+};
+
+std::shared_ptr<DeviceScene>& cached_scene() {
+    thread_local std::shared_ptr<DeviceScene> t;
+    return t;
+}
+
+std::shared_ptr<DeviceScene> device_scene(const SparseScene& scene, const Params& p) {
     const size_t n = scene.voxel_count();
+    if (p.n_density != scene.pool_count() || p.n_sh != scene.sh.size())
+        throw std::invalid_argument("parameter pools do not match the scene");
+    const uint64_t geo = geometry_digest(scene);
+    const uint64_t hd = digest_bytes(p.density, p.n_density * 4);
+    const uint64_t hs = digest_bytes(p.sh, p.n_sh * 4);
+    std::shared_ptr<DeviceScene>& c = cached_scene();
+    if (c && c->geo == geo && c->n_voxels == n) {
+        if (c->dens != hd || c->sh != hs) {
+            check(svr_scene_set_params(ctx(), c->s, c->dens != hd ? p.density : nullptr,
+                                       c->sh != hs ? p.sh : nullptr, 0));
+            c->dens = hd;
+            c->sh = hs;
+        }
+        return c;
+    }
     std::vector<uint64_t> codes(n);
     std::vector<uint8_t> levels(n);
     for (size_t i = 0; i < n; ++i) {
@@ -112,10 +248,6 @@ std::unique_ptr<SceneHandle> upload(const SparseScene& scene, const PoolsD& pool
         codes[i] = scene.voxels[i].code;
         levels[i] = uint8_t(scene.voxels[i].level);
     }
-    std::vector<float> dens(pools.density.begin(), pools.density.end());
-    std::vector<float> sh(pools.sh.begin(), pools.sh.end());
-    if (dens.size() != scene.pool_count() || sh.size() != scene.sh.size())
-        throw std::invalid_argument("parameter pools do not match the scene");
     svr_scene_desc d{};
     d.n_voxels = n;
     d.n_pool = scene.pool_count();
@@ -126,13 +258,31 @@ std::unique_ptr<SceneHandle> upload(const SparseScene& scene, const PoolsD& pool
     d.bounds_size = scene.bounds.size;
     d.codes = codes.data();
     d.levels = levels.data();
-    static_assert(sizeof(std::array<uint32_t, 8>) == 32, "corner_index layout");
     d.corner_index = n ? scene.corner_index[0].data() : nullptr;
-    d.density = dens.data();
-    d.sh = sh.data();
-    auto h = std::make_unique<SceneHandle>();
+    d.density = p.density;
+    d.sh = p.sh;
+    auto h = std::make_shared<DeviceScene>();
     check(svr_scene_upload(ctx(), &d, &h->s));
+    h->geo = geo;
+    h->dens = hd;
+    h->sh = hs;
+    h->n_voxels = n;
+    h->n_pool = scene.pool_count();
+    h->n_sh = scene.sh.size();
+    c = h;
     return h;
+}
+
+std::shared_ptr<DeviceScene> device_scene(const SparseScene& scene) {
+    return device_scene(scene, {scene.density.data(), scene.density.size(), scene.sh.data(),
+                                scene.sh.size()});
+}
+
+std::shared_ptr<DeviceScene> device_scene(const SparseScene& scene, const PoolsD& pools) {
+    thread_local std::vector<float> dens, sh;
+    narrow_into(pools.density, dens);
+    narrow_into(pools.sh, sh);
+    return device_scene(scene, {dens.data(), dens.size(), sh.data(), sh.size()});
 }
 
 Image download_image(svr_frame* f, svr_buffer which, int w, int h, int ch, double far = 0.0,
@@ -149,7 +299,7 @@ Image download_image(svr_frame* f, svr_buffer which, int w, int h, int ch, doubl
 // GPU state behind a ForwardRecords handed out by render_with_pools. Owned by
 // the shared_ptr's deleter, so it lives exactly as long as the records.
 struct GpuRecords {
-    std::unique_ptr<SceneHandle> scene;
+    std::shared_ptr<DeviceScene> scene;
     svr_frame* frame = nullptr;
     ~GpuRecords() {
         if (frame) svr_frame_destroy(frame);
@@ -197,13 +347,26 @@ bool project_voxel(const Camera& cam, const Vec3& center, double size, PreVoxel&
 }
 
 std::vector<SignBits> tile_sign_patterns(const Camera& cam, int tx, int ty) {
+    // every tile's mask comes from one launch; a thread remembers the last
+    // camera's masks, so querying all tiles of a view costs one launch
+    struct Last {
+        svr_camera cam{};
+        std::vector<uint8_t> masks;
+    };
+    thread_local Last last;
     const svr_camera c = to_c(cam);
     const int ntx = (cam.width + kTileSize - 1) / kTileSize;
     const int nty = (cam.height + kTileSize - 1) / kTileSize;
-    std::vector<uint8_t> masks(size_t(ntx) * nty);
-    check(svr_tile_sign_masks(ctx(), &c, masks.data(), masks.size()));
+    if (last.masks.empty() || std::memcmp(&last.cam, &c, sizeof c) != 0) {
+        std::vector<uint8_t> masks(size_t(ntx) * nty);
+        check(svr_tile_sign_masks(ctx(), &c, masks.data(), masks.size()));
+        last.masks.swap(masks);
+        last.cam = c;
+    }
+    if (tx < 0 || ty < 0 || tx >= ntx || ty >= nty)
+        throw std::out_of_range("tile index outside the camera's tile grid");
     std::vector<SignBits> out;
-    const uint8_t m = masks.at(size_t(ty) * ntx + tx);
+    const uint8_t m = last.masks[size_t(ty) * ntx + tx];
     for (SignBits s = 0; s < 8; ++s)
         if (m >> s & 1) out.push_back(s);
     return out;
@@ -246,10 +409,12 @@ void sort_entries(std::vector<SortEntry>& entries) {
     for (size_t i = 0; i < entries.size(); ++i) entries[i] = {keys[i], vals[i]};
 }
 
-RenderOutput render_with_pools(const SparseScene& scene, const PoolsD& pools, const Camera& cam,
-                               const RenderOptions& opts) {
+namespace {
+
+RenderOutput render_on(std::shared_ptr<DeviceScene> dev, const SparseScene& scene,
+                       const Camera& cam, const RenderOptions& opts) {
     auto gpu = std::make_shared<GpuRecords>();
-    gpu->scene = upload(scene, pools);
+    gpu->scene = std::move(dev);
     check(svr_frame_create(ctx(), &gpu->frame));
     const svr_camera c = to_c(cam);
     const svr_render_options o = to_c(opts);
@@ -320,13 +485,22 @@ RenderOutput render_with_pools(const SparseScene& scene, const PoolsD& pools, co
     return out;
 }
 
+}  // namespace
+
+RenderOutput render_with_pools(const SparseScene& scene, const PoolsD& pools, const Camera& cam,
+                               const RenderOptions& opts) {
+    return render_on(device_scene(scene, pools), scene, cam, opts);
+}
+
+// render = render_with_pools(scene, make_pools(scene)) (raster.cpp:299-301);
+// make_pools widens the float pools to double and the upload narrows them
+// back, so the scene's own floats are used directly.
 RenderOutput render(const SparseScene& scene, const Camera& cam, const RenderOptions& opts) {
-    return render_with_pools(scene, make_pools(scene), cam, opts);
+    return render_on(device_scene(scene), scene, cam, opts);
 }
 
 SceneGradients render_backward(const SparseScene& scene, const PoolsD& pools,
                                const ForwardRecords& records, const UpstreamGrads& grads) {
-    (void)pools;  // the frame was rendered from these pools
     std::shared_ptr<GpuRecords> gpu;
     {
         std::lock_guard<std::mutex> lk(g_mu);
@@ -350,6 +524,21 @@ SceneGradients render_backward(const SparseScene& scene, const PoolsD& pools,
         dvc.push_back(float(v.y));
         dvc.push_back(float(v.z));
     }
+    // The SH chain's clamp mask reads pools.sh (raster.cpp:414): the device
+    // scene must hold exactly those coefficients.
+    DeviceScene& ds = *gpu->scene;
+    if (pools.sh.size() != ds.n_sh || pools.density.size() != ds.n_pool ||
+        scene.voxel_count() != ds.n_voxels)
+        throw std::invalid_argument("pools / scene do not match the rendered scene");
+    {
+        thread_local std::vector<float> sh;
+        narrow_into(pools.sh, sh);
+        const uint64_t hs = digest_bytes(sh.data(), sh.size() * 4);
+        if (hs != ds.sh) {
+            check(svr_scene_set_params(ctx(), ds.s, nullptr, sh.data(), 0));
+            ds.sh = hs;
+        }
+    }
     svr_upstream up{};
     up.d_color = dc.empty() ? nullptr : dc.data();
     up.d_depth = dd.empty() ? nullptr : dd.data();
@@ -362,7 +551,7 @@ SceneGradients render_backward(const SparseScene& scene, const PoolsD& pools,
     up.on_device = 0;
     std::vector<float> gd(scene.pool_count()), gs(scene.sh.size()), gp(scene.voxel_count());
     svr_gradients g{gd.data(), gs.data(), gp.data(), 0};
-    check(svr_render_backward(ctx(), gpu->scene->s, gpu->frame, &up, &g));
+    check(svr_render_backward(ctx(), ds.s, gpu->frame, &up, &g));
     SceneGradients out;
     out.density.assign(gd.begin(), gd.end());
     out.sh.assign(gs.begin(), gs.end());
@@ -373,7 +562,7 @@ SceneGradients render_backward(const SparseScene& scene, const PoolsD& pools,
 RenderOutput render_oracle(const SparseScene& scene, const Camera& cam, const RenderOptions& opts) {
     if (opts.record_stats)
         throw std::invalid_argument("render_oracle on the GPU does not record per-voxel stats");
-    auto sh = upload(scene, make_pools(scene));
+    auto sh = device_scene(scene);
     svr_frame* f = nullptr;
     check(svr_frame_create(ctx(), &f));
     std::unique_ptr<svr_frame, int (*)(svr_frame*)> guard(f, svr_frame_destroy);

@@ -568,6 +568,13 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     ca.t_threshold = float(opts->t_threshold);
     for (int i = 0; i < 3; ++i) ca.bg[i] = float(opts->background[i]);
     ca.far_sentinel = float(opts->far_sentinel);
+    // K7 path: the CTA-cooperative cull once the tiles average >= 2048
+    // entries (SVR_COOP_MIN; E is the capacity of a deferred frame)
+    static const uint64_t coop_min = [] {
+        const char* e = std::getenv("SVR_COOP_MIN");
+        return e ? uint64_t(std::strtoull(e, nullptr, 10)) : uint64_t(2048);
+    }();
+    const bool coop = E >= coop_min * uint64_t(ntiles);
     if (ss1) {
         ca.color = oc, ca.depth = od, ca.median = om, ca.normal = on, ca.tfin = ot;
     } else {
@@ -603,7 +610,7 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
 
     // K7: composite
     mark(ctx, kStageComposite);
-    launch_composite(cam, ca, false, st);
+    launch_composite(cam, ca, false, coop, st);
     mark(ctx, kStageOther);
 
     if (f->training) {
@@ -630,7 +637,7 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
             cr.max_blend = nullptr;
             cr.stage_entry = nullptr;
             mark(ctx, kStageRecord);
-            launch_composite(cam, cr, true, st);
+            launch_composite(cam, cr, true, coop, st);
             mark(ctx, -1);
             f->compact_valid = true;
         }
@@ -867,11 +874,11 @@ void backward_impl(svr_ctx* ctx, const svr_scene* scene, svr_frame* f, const svr
 
     // Gradient outputs on device.
     float *gd = out->density, *gs = out->sh, *gp = out->priority;
-    DevBuf tmp_d, tmp_s, tmp_p;
     if (!out->on_device) {
-        gd = grow<float>(tmp_d, P);
-        gs = grow<float>(tmp_s, shn);
-        gp = grow<float>(tmp_p, N);
+        gd = grow<float>(ctx->bwd_density, P);
+        gs = grow<float>(ctx->bwd_sh, shn);
+        gp = grow<float>(ctx->bwd_priority, N);
+        require(!accumulate, SVR_ERR_INVALID_ARGUMENT, "accumulate needs device gradient buffers");
     }
     require(gd && gs && gp, SVR_ERR_INVALID_ARGUMENT, "gradient buffers must not be null");
     if (!accumulate) {

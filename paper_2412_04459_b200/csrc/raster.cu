@@ -857,24 +857,45 @@ constexpr size_t kCompSmem = size_t(2) * kCompWarps * 32 * kRecordF4 * sizeof(fl
 // MODE 0: plain render; 1: record pass (RECORD); 2: render with per-voxel
 // max-blend stats and/or staged training records (their checks compiled in);
 // 3: staged training records only (the single-pass training render).
+constexpr int kBatch = 1024;        // entries culled per CTA batch (cooperative path)
+constexpr int kSubs = kBatch / 32;  // 32-entry sub-chunks per batch
+
+// Shared memory of K7 besides the record buffers: the two per-tile paths
+// (warp-autonomous below, CTA-cooperative after it) use it in turn.
 template <int K, int MODE>
-#ifndef SVR_PC_SMEM
-#define SVR_PC_SMEM 1  // pixel centre from shared memory in phase B (the register copy is rematerialised per hit)
-#endif
-#ifndef SVR_COMP_MINB
-#define SVR_COMP_MINB 4
-#endif
-__global__ void __launch_bounds__(256, SVR_COMP_MINB) composite_kernel(DevCamera cam, CompositeArgs a) {
+struct CompShared {
+    static constexpr bool ENTRY = MODE != 0;  // slots need their entry index
+    union {
+        struct {
+            uint32_t vid[2][kCompWarps][32];
+            uint8_t j[2][kCompWarps][32];  // chunk-local entry index of each slot
+        } w;
+        struct {
+            uint32_t ball[2][kSubs][kCompWarps];  // [batch buf][sub-chunk][warp]
+            uint8_t sign[2][kCompWarps][32];   // sign pattern of each slot
+            uint32_t ent[ENTRY ? 2 : 1][kCompWarps][32];  // entry index of each slot
+            uint32_t wsig[kCompWarps];
+            uint32_t signwarps[8];
+        } c;
+    };
+    float cone[kCompWarps][4][3];
+    // pixel centres for phase B (one LDS instead of a per-hit rematerialised
+    // copy); the entry-recording modes need the space for c.ent instead
+    float2 pc[ENTRY ? 1 : 256];
+};
+
+template <int K, int MODE>
+__device__ __forceinline__ void composite_tile_warp(const DevCamera& cam, const CompositeArgs& a,
+                                                    int tile, CompShared<K, MODE>& sh,
+                                                    float4* s_rec_dyn) {
     constexpr bool RECORD = MODE == 1;
     constexpr bool EXTRA = MODE == 2;
     constexpr bool STAGED = MODE == 3;
-    pdl_enter();
-    extern __shared__ float4 s_rec_dyn[];  // [2][8 warps][32 slots][kRecordF4]
-    __shared__ uint32_t s_vid[2][kCompWarps][32];
-    __shared__ uint8_t s_j[2][kCompWarps][32];  // chunk-local entry index of each slot
-    __shared__ float s_cone[kCompWarps][4][3];
+    constexpr bool PC_SMEM = !CompShared<K, MODE>::ENTRY;
+    auto& s_vid = sh.w.vid;
+    auto& s_j = sh.w.j;
+    auto& s_cone = sh.cone;
 
-    const int tile = a.tile_order ? int(a.tile_order[blockIdx.x]) : int(blockIdx.x);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int px, py;
     pixel_of(cam, tile, threadIdx.x, px, py);
@@ -894,10 +915,7 @@ __global__ void __launch_bounds__(256, SVR_COMP_MINB) composite_kernel(DevCamera
     const SlabSel ssel = slab_sel(ix, iy, iz);
     const float dnorm = float(sqrt(dd[0] * dd[0] + dd[1] * dd[1] + dd[2] * dd[2]));
     const float pcx = float(px) + 0.5f, pcy = float(py) + 0.5f;
-#if SVR_PC_SMEM
-    __shared__ float2 s_pc[256];
-    s_pc[threadIdx.x] = make_float2(pcx, pcy);
-#endif
+    if (PC_SMEM) sh.pc[PC_SMEM ? threadIdx.x : 0] = make_float2(pcx, pcy);
     // Frustum of this warp's 8x4 block (warp_cone_planes): skips boxes whose
     // screen AABB is loose, e.g. near-plane voxels, which get the full screen
     // (raster.cpp:95-101), without changing the composited set.
@@ -999,16 +1017,10 @@ __global__ void __launch_bounds__(256, SVR_COMP_MINB) composite_kernel(DevCamera
             const int s_ = __ffs(hits) - 1;
             hits &= hits - 1;
             const float4 bb = wrec[s_][1];
-#if SVR_PC_SMEM
-            const float2 pc = s_pc[threadIdx.x];  // one LDS instead of rematerialising the centre
+            const float2 pc = PC_SMEM ? sh.pc[PC_SMEM ? threadIdx.x : 0] : make_float2(pcx, pcy);
             if (!((one_sign || (wvid[s_] >> 29) == my_sign) &&
                   !(pc.x < bb.x || pc.x > bb.y || pc.y < bb.z || pc.y > bb.w)))
                 continue;
-#else
-            if (!((one_sign || (wvid[s_] >> 29) == my_sign) &&
-                  !(pcx < bb.x || pcx > bb.y || pcy < bb.z || pcy > bb.w)))
-                continue;
-#endif
             const float4 lo = wrec[s_][0];
             float ta, tb;
             slab(lo, ix, iy, iz, ta, tb);  // same floats as slab_s; needs no per-lane face selectors
@@ -1104,6 +1116,320 @@ __global__ void __launch_bounds__(256, SVR_COMP_MINB) composite_kernel(DevCamera
     a.median[p] = median;
     a.tfin[p] = T;
     if (a.pix_count) a.pix_count[slot] = cnt;
+}
+
+// K7, CTA-cooperative variant. The tile's entries are culled ONCE per CTA
+// instead of once per warp: per batch of 1024 entries every thread loads four
+// entries' values and screen AABBs, tests them against the eight 8x4 pixel blocks
+// of the tile (footprint overlap, the sign patterns present in each block,
+// the block frustum for loose AABBs) and the eight per-block ballots go to
+// shared memory. Each warp then walks only its own survivors of the batch
+// (a broadcast word per 32 entries, zero for most of them on config 4),
+// packing them into groups of up to 32 slots whose 96-B records are copied
+// with cp.async while the previous group is composited (phase A slab tests,
+// phase B per-lane hits, exactly as in composite_kernel). Warps meet at one
+// CTA barrier per batch (a config-2 tile is a single batch, so its warps run
+// unsynchronised after the cull); the CTA leaves once every warp is done.
+
+template <int K, int MODE>
+__device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const CompositeArgs& a,
+                                                    int tile, CompShared<K, MODE>& sh,
+                                                    float4* s_rec_dyn) {
+    constexpr bool RECORD = MODE == 1;
+    constexpr bool EXTRA = MODE == 2;
+    constexpr bool STAGED = MODE == 3;
+    constexpr bool ENTRY = CompShared<K, MODE>::ENTRY;
+    auto& s_ball = sh.c.ball;
+    auto& s_sign = sh.c.sign;
+    auto& s_ent = sh.c.ent;
+    auto& s_cone = sh.cone;
+    auto& s_wsig = sh.c.wsig;
+    auto& s_signwarps = sh.c.signwarps;
+    auto& s_pc = sh.pc;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int px, py;
+    pixel_of(cam, tile, threadIdx.x, px, py);
+    const bool inside = px < cam.W && py < cam.H;
+    const int wx0 = px - (lane & 7), wy0 = py - (lane >> 3);
+
+    double dd[3];
+    pixel_ray_dir(cam, double(px), double(py), dd);
+    const uint32_t my_sign = sign_bits(dd);
+    const uint32_t warp_signs = __reduce_or_sync(0xffffffffu, inside ? (1u << my_sign) : 0u);
+    const bool one_sign = __popc(warp_signs) <= 1;
+    const float dx = float(dd[0]), dy = float(dd[1]), dz = float(dd[2]);
+    const float ix = slab_inv(dd[0]), iy = slab_inv(dd[1]), iz = slab_inv(dd[2]);
+    const SlabSel ssel = slab_sel(ix, iy, iz);
+    const float dnorm = float(sqrt(dd[0] * dd[0] + dd[1] * dd[1] + dd[2] * dd[2]));
+    const float pcx = float(px) + 0.5f, pcy = float(py) + 0.5f;
+    if (!ENTRY) s_pc[threadIdx.x] = make_float2(pcx, pcy);
+    if (lane == 0) {
+        warp_cone_planes(cam, wx0, wy0, s_cone[warp]);
+        s_wsig[warp] = warp_signs;
+    }
+    __syncthreads();
+    if (threadIdx.x < 8) {  // for each sign pattern, the blocks whose pixels have it
+        uint32_t m = 0;
+        for (int w = 0; w < kCompWarps; ++w) m |= ((s_wsig[w] >> threadIdx.x) & 1u) << w;
+        s_signwarps[threadIdx.x] = m;
+    }
+    __syncthreads();  // s_signwarps before the first cull
+    // tile footprint in pixel-centre coordinates: block (bx, by) covers
+    // x in [X0 + 8bx + .5, X0 + 8bx + 7.5], y in [Y0 + 4by + .5, Y0 + 4by + 3.5]
+    const float X0 = float((tile % cam.ntx) * kTile), Y0 = float((tile / cam.ntx) * kTile);
+
+    float T = 1.0f, cr = 0.f, cg = 0.f, cb = 0.f, nx = 0.f, ny = 0.f, nz = 0.f, depth = 0.f;
+    float median = -1.0f;
+    uint32_t cnt = 0;
+    bool done = !inside;
+    const uint32_t slot = uint32_t(tile) * 256u + uint32_t((py % kTile) * kTile + (px % kTile));
+    uint32_t rec_base = 0;
+    if (RECORD) rec_base = inside ? a.pix_begin[slot] : 0u;
+
+    const uint2 range = a.ranges[tile];
+    const float thr = a.t_threshold;
+    constexpr uint32_t kVidMask = (1u << 29) - 1u;
+    float4 (*wrec0)[kRecordF4] =
+        reinterpret_cast<float4 (*)[kRecordF4]>(s_rec_dyn + size_t(warp) * 32 * kRecordF4);
+
+    // Culls entries range.x + kBatch b + 256 r + threadIdx.x (r < 4) into
+    // ballot buffer pb: sub-chunk 8 r + warp, one word per target warp.
+    auto produce = [&](uint32_t b, int pb) {
+#pragma unroll
+        for (int r = 0; r < kBatch / 256; ++r) {
+            const uint32_t idx = range.x + b * kBatch + r * 256 + threadIdx.x;
+            uint32_t m = 0;
+            if (idx < range.y) {
+                const uint32_t v = __ldg(a.vals + idx);
+                const float4* rec = a.records + uint64_t(v & kVidMask) * kRecordF4;
+                const float4 bb = __ldg(rec + 1);
+                const uint32_t xm = (!(X0 + 7.5f < bb.x || X0 + 0.5f > bb.y) ? 0x55u : 0u) |
+                                    (!(X0 + 15.5f < bb.x || X0 + 8.5f > bb.y) ? 0xAAu : 0u);
+                const uint32_t ym = (!(Y0 + 3.5f < bb.z || Y0 + 0.5f > bb.w) ? 0x03u : 0u) |
+                                    (!(Y0 + 7.5f < bb.z || Y0 + 4.5f > bb.w) ? 0x0Cu : 0u) |
+                                    (!(Y0 + 11.5f < bb.z || Y0 + 8.5f > bb.w) ? 0x30u : 0u) |
+                                    (!(Y0 + 15.5f < bb.z || Y0 + 12.5f > bb.w) ? 0xC0u : 0u);
+                m = xm & ym & s_signwarps[v >> 29];
+                // frustum of each block only for entries with a large screen AABB
+                if (m && (bb.y - bb.x) * (bb.w - bb.z) > kConeMinArea) {
+                    const float4 lo = __ldg(rec);
+                    for (int w = 0; w < kCompWarps; ++w)
+                        if (((m >> w) & 1u) && !box_in_cone(s_cone[w], lo)) m &= ~(1u << w);
+                }
+            }
+            uint32_t mine = 0;
+#pragma unroll
+            for (int w = 0; w < kCompWarps; ++w) {
+                const uint32_t bw = __ballot_sync(0xffffffffu, (m >> w) & 1u);
+                if (lane == w) mine = bw;
+            }
+            if (lane < kCompWarps) s_ball[pb][r * kCompWarps + warp][lane] = mine;
+        }
+    };
+
+    // Composites group buffer g (n slots, records landed).
+    auto composite_group = [&](int g, int n) {
+        float4(*wrec)[kRecordF4] = g ? wrec0 + kCompWarps * 32 : wrec0;
+        const uint8_t* wsg = s_sign[g][warp];
+        // Phase A: this lane's slab hits among the slots.
+        uint32_t hits = 0;
+        if (!done) {
+#pragma unroll 2
+            for (int sl = 0; sl < n; ++sl) {
+                float ta, tb;
+                slab_s(wrec[sl][0], ix, iy, iz, ssel, ta, tb);
+                hits |= uint32_t(ta <= tb && ta > 0.0f) << sl;
+            }
+        }
+        // Phase B: this lane's hits, in entry order.
+        while (hits) {
+            const int s_ = __ffs(hits) - 1;
+            hits &= hits - 1;
+            const float4 bb = wrec[s_][1];
+            const float2 pc = ENTRY ? make_float2(pcx, pcy) : s_pc[ENTRY ? 0 : threadIdx.x];
+            if (!((one_sign || wsg[s_] == my_sign) &&
+                  !(pc.x < bb.x || pc.x > bb.y || pc.y < bb.z || pc.y > bb.w)))
+                continue;
+            const float4 lo = wrec[s_][0];
+            float ta, tb;
+            slab(lo, ix, iy, iz, ta, tb);
+            const float4 va = wrec[s_][2], vb = wrec[s_][3];
+            const float inv = wrec[s_][5].w;
+            const float seg = tb - ta;
+            const float lk = seg * dnorm * (1.0f / K);
+            // voxel_alpha (field.hpp:92-116), K-point midpoint quadrature
+            float sa[K], tk[K], sum = 0.f;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                tk[k] = ta + ((k + 0.5f) / K) * seg;
+                const float qx = (tk[k] * dx - lo.x) * inv;
+                const float qy = (tk[k] * dy - lo.y) * inv;
+                const float qz = (tk[k] * dz - lo.z) * inv;
+                const float act = explin(trilinear_poly(va, vb, qx, qy, qz));
+                sum += act;
+                sa[k] = one_minus_exp_neg(lk * act);
+            }
+            const float alpha = (K == 1) ? sa[0] : one_minus_exp_neg(lk * sum);
+            if (!RECORD) {
+                // voxel_depth (field.hpp:173-181) and the median crossing
+                float dv = 0.f, Tk = 1.f;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    dv += Tk * sa[k] * tk[k];
+                    Tk *= 1.0f - sa[k];
+                }
+                if (median < 0.0f) {
+                    float Tf = T;
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        Tf *= 1.0f - sa[k];
+                        if (Tf < 0.5f) {
+                            median = tk[k];
+                            break;
+                        }
+                    }
+                }
+                const float w = T * alpha;
+                const float4 col = wrec[s_][4], nor = wrec[s_][5];
+                cr += w * col.x;
+                cg += w * col.y;
+                cb += w * col.z;
+                nx += w * nor.x;
+                ny += w * nor.y;
+                nz += w * nor.z;
+                depth += T * dv;
+                if (EXTRA && a.max_blend) atomicMax(a.max_blend + __float_as_uint(col.w), __float_as_uint(w));
+                if (STAGED || (EXTRA && a.stage_entry)) {
+                    if (cnt < a.stage_cap) {
+                        const uint32_t at = cnt * a.stage_stride + slot;
+                        a.stage_entry[at] = s_ent[ENTRY ? g : 0][warp][s_];
+                        a.stage_T[at] = T;
+                    } else {
+                        *a.overflow = 1u;
+                    }
+                }
+            } else {
+                a.contrib_entry[rec_base + cnt] = s_ent[ENTRY ? g : 0][warp][s_];
+                a.contrib_T[rec_base + cnt] = T;
+            }
+            T *= 1.0f - alpha;
+            ++cnt;
+            if (T < thr) {
+                done = true;
+                hits = 0;
+            }
+        }
+    };
+
+    const uint32_t n_entries = range.y > range.x ? range.y - range.x : 0u;
+    const uint32_t n_batches = (n_entries + kBatch - 1) / kBatch;
+    int g = 0;            // group buffer being filled
+    int nfill = 0;        // slots staged into it
+    bool pend = false;    // the other buffer holds a full group not yet composited
+    bool wdone = __all_sync(0xffffffffu, done);
+    if (n_batches) produce(0, 0);
+    __syncthreads();
+    for (uint32_t b = 0; b < n_batches; ++b) {
+        const int pb = b & 1;
+        if (b + 1 < n_batches) produce(b + 1, pb ^ 1);
+        if (!wdone) {
+            for (int sub = 0; sub < kSubs; ++sub) {
+                uint32_t ball = s_ball[pb][sub][warp];
+                const uint32_t e0 = range.x + b * kBatch + sub * 32;
+                while (ball) {
+                    const int take = min(32 - nfill, __popc(ball));
+                    // the first `take` survivors (entry order) go to group g
+                    uint32_t part = ball;
+                    for (int k = __popc(ball); k > take; --k) part &= ~(1u << (31 - __clz(part)));
+                    ball &= ~part;
+                    if ((part >> lane) & 1u) {
+                        const int at = nfill + __popc(part & ((1u << lane) - 1u));
+                        const uint32_t v = __ldg(a.vals + e0 + lane);
+                        s_sign[g][warp][at] = uint8_t(v >> 29);
+                        if (ENTRY) s_ent[ENTRY ? g : 0][warp][at] = e0 + lane;
+                        const float4* src = a.records + uint64_t(v & kVidMask) * kRecordF4;
+                        float4(*wrec)[kRecordF4] = g ? wrec0 + kCompWarps * 32 : wrec0;
+#pragma unroll
+                        for (int k = 0; k < kRecordF4; ++k) cp_async16(&wrec[at][k], src + k);
+                    }
+                    nfill += take;
+                    if (nfill == 32) {  // group full: composite the previous one meanwhile
+                        cp_async_commit();
+                        if (pend) {
+                            cp_async_wait<1>();
+                            __syncwarp();
+                            composite_group(g ^ 1, 32);
+                            __syncwarp();  // its buffer is restaged next
+                        }
+                        pend = true;
+                        g ^= 1;
+                        nfill = 0;
+                        wdone = __all_sync(0xffffffffu, done);
+                        if (wdone) break;
+                    }
+                }
+                if (wdone) break;
+            }
+        }
+        // ballot buffer pb is rewritten by the produce two batches on
+        if (__syncthreads_and(wdone)) break;
+    }
+    // drain: the pending full group, then the partial one
+    cp_async_commit();
+    if (!wdone) {
+        if (pend) {
+            cp_async_wait<1>();
+            __syncwarp();
+            composite_group(g ^ 1, 32);
+        }
+        cp_async_wait<0>();
+        __syncwarp();
+        if (nfill) composite_group(g, nfill);
+    }
+    cp_async_wait<0>();  // no copy may outlive the CTA's shared memory
+    if (RECORD || !inside) return;
+    // CompositeCtx::finish (raster.cpp:56-60)
+    cr += T * a.bg[0];
+    cg += T * a.bg[1];
+    cb += T * a.bg[2];
+    if (cnt == 0) depth = a.far_sentinel;
+    if (median < 0.0f) median = a.far_sentinel;
+    const uint64_t p = uint64_t(py) * cam.W + px;
+    a.color[3 * p + 0] = cr;
+    a.color[3 * p + 1] = cg;
+    a.color[3 * p + 2] = cb;
+    a.normal[3 * p + 0] = nx;
+    a.normal[3 * p + 1] = ny;
+    a.normal[3 * p + 2] = nz;
+    a.depth[p] = depth;
+    a.median[p] = median;
+    a.tfin[p] = T;
+    if (a.pix_count) a.pix_count[slot] = cnt;
+}
+
+#ifndef SVR_COMP_MINB
+#define SVR_COMP_MINB 4
+#endif
+// K7: one CTA per tile (LPT order), warp-autonomous or CTA-cooperative
+// (launch_composite picks per frame: the cooperative cull pays once tiles
+// hold thousands of entries — config 4, ~22K per tile: 3.62 -> 2.11 ms — and
+// costs its batch barrier on short lists — config 2, ~430: 0.33 -> 0.38 ms).
+template <int K, int MODE>
+__global__ void __launch_bounds__(256, SVR_COMP_MINB) composite_kernel(DevCamera cam, CompositeArgs a) {
+    pdl_enter();
+    extern __shared__ float4 s_rec_dyn[];  // [2][8 warps][32 slots][kRecordF4]
+    __shared__ CompShared<K, MODE> sh;
+    const int tile = a.tile_order ? int(a.tile_order[blockIdx.x]) : int(blockIdx.x);
+    composite_tile_warp<K, MODE>(cam, a, tile, sh, s_rec_dyn);
+}
+
+template <int K, int MODE>
+__global__ void __launch_bounds__(256, SVR_COMP_MINB) composite_coop_kernel(DevCamera cam, CompositeArgs a) {
+    pdl_enter();
+    extern __shared__ float4 s_rec_dyn[];
+    __shared__ CompShared<K, MODE> sh;
+    const int tile = a.tile_order ? int(a.tile_order[blockIdx.x]) : int(blockIdx.x);
+    composite_tile_coop<K, MODE>(cam, a, tile, sh, s_rec_dyn);
 }
 
 __global__ void compact_contribs_kernel(const uint32_t* __restrict__ pix_count,
@@ -1399,7 +1725,7 @@ void launch_tile_order(uint2* ranges, int ntiles, uint32_t* order, cudaStream_t 
     SVR_LAUNCH("tile_order_kernel");
 }
 
-void launch_composite(const DevCamera& cam, const CompositeArgs& a, bool record_pass,
+void launch_composite(const DevCamera& cam, const CompositeArgs& a, bool record_pass, bool coop,
                       cudaStream_t st) {
     const unsigned ntiles = unsigned(cam.ntx * cam.nty);
     static std::atomic<uint64_t> attr_set{0};
@@ -1407,20 +1733,32 @@ void launch_composite(const DevCamera& cam, const CompositeArgs& a, bool record_
         for (auto fn : {composite_kernel<1, 0>, composite_kernel<1, 1>, composite_kernel<1, 2>,
                         composite_kernel<1, 3>, composite_kernel<2, 0>, composite_kernel<2, 1>,
                         composite_kernel<2, 2>, composite_kernel<2, 3>, composite_kernel<3, 0>,
-                        composite_kernel<3, 1>, composite_kernel<3, 2>, composite_kernel<3, 3>})
+                        composite_kernel<3, 1>, composite_kernel<3, 2>, composite_kernel<3, 3>,
+                        composite_coop_kernel<1, 0>, composite_coop_kernel<1, 1>,
+                        composite_coop_kernel<1, 2>, composite_coop_kernel<1, 3>,
+                        composite_coop_kernel<2, 0>, composite_coop_kernel<2, 1>,
+                        composite_coop_kernel<2, 2>, composite_coop_kernel<2, 3>,
+                        composite_coop_kernel<3, 0>, composite_coop_kernel<3, 1>,
+                        composite_coop_kernel<3, 2>, composite_coop_kernel<3, 3>})
             SVR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCompSmem)));
     }
     const int mode = record_pass ? 1 : a.max_blend ? 2 : a.stage_entry ? 3 : 0;
+#define SVR_COMPOSITE_LAUNCH(KK, MM)                                                    \
+    if (coop)                                                                           \
+        launch_pdl(composite_coop_kernel<KK, MM>, ntiles, 256, kCompSmem, st, cam, a); \
+    else                                                                                \
+        launch_pdl(composite_kernel<KK, MM>, ntiles, 256, kCompSmem, st, cam, a);
 #define SVR_COMPOSITE_CASE(KK)                                                          \
     case KK:                                                                            \
-        if (mode == 1)                                                                  \
-            launch_pdl(composite_kernel<KK, 1>, ntiles, 256, kCompSmem, st, cam, a);    \
-        else if (mode == 2)                                                             \
-            launch_pdl(composite_kernel<KK, 2>, ntiles, 256, kCompSmem, st, cam, a);    \
-        else if (mode == 3)                                                             \
-            launch_pdl(composite_kernel<KK, 3>, ntiles, 256, kCompSmem, st, cam, a);    \
-        else                                                                            \
-            launch_pdl(composite_kernel<KK, 0>, ntiles, 256, kCompSmem, st, cam, a);    \
+        if (mode == 1) {                                                                \
+            SVR_COMPOSITE_LAUNCH(KK, 1)                                                 \
+        } else if (mode == 2) {                                                         \
+            SVR_COMPOSITE_LAUNCH(KK, 2)                                                 \
+        } else if (mode == 3) {                                                         \
+            SVR_COMPOSITE_LAUNCH(KK, 3)                                                 \
+        } else {                                                                        \
+            SVR_COMPOSITE_LAUNCH(KK, 0)                                                 \
+        }                                                                               \
         break;
     switch (a.K) {
         SVR_COMPOSITE_CASE(1)
@@ -1430,6 +1768,7 @@ void launch_composite(const DevCamera& cam, const CompositeArgs& a, bool record_
             throw Error(SVR_ERR_INVALID_ARGUMENT, "rasterizer sample count K must be in {1,2,3}");
     }
 #undef SVR_COMPOSITE_CASE
+#undef SVR_COMPOSITE_LAUNCH
     SVR_LAUNCH("composite_kernel");
 }
 

@@ -119,6 +119,9 @@ struct svr_ctx {
     svrb::DevBuf adam_flag; // svr_adam_step NaN flag
     bool async_frames = false;  // svr_ctx_set_async: renders skip the mid-frame E read-back
     svrb::DevBuf overflow_count;  // deferred frames whose E outgrew their capacity
+    // device gradients of a host-buffer svr_render_backward, kept between
+    // calls (config 2: 215 MB that would otherwise be allocated per call)
+    svrb::DevBuf bwd_density, bwd_sh, bwd_priority;
 };
 
 struct svr_scene {

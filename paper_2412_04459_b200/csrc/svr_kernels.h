@@ -208,7 +208,7 @@ struct CompositeArgs {
 void launch_compact_contribs(const uint32_t* pix_count, const uint32_t* pix_begin,
                              const uint32_t* stage_entry, const float* stage_T, uint32_t stride,
                              uint32_t* contrib_entry, float* contrib_T, cudaStream_t st);
-void launch_composite(const DevCamera& cam, const CompositeArgs& a, bool record_pass,
+void launch_composite(const DevCamera& cam, const CompositeArgs& a, bool record_pass, bool coop,
                       cudaStream_t st);
 void launch_tile_order(uint2* ranges, int ntiles, uint32_t* order, cudaStream_t st);
 

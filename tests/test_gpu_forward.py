@@ -109,7 +109,7 @@ def test_project_voxels_api_matches_reference(svr, ctx, ref):
         lib = ref.load_ref()
         for i in range(64):
             ra, rr, rv = np.empty(4), np.empty(4, np.int32), C.c_int()
-            c = cam.to_c()
+            c = ref.camera_c(cam)
             lib.ref_project_one(C.byref(c), ref._p(np.ascontiguousarray(centers[i])), sizes[i], 1e-6,
                                 ref._p(ra), ref._p(rr), C.byref(rv))
             assert bool(rv.value) == bool(vis[i])
