@@ -159,6 +159,21 @@ class RefScene:
         c, s = self.bounds()
         return abi.SceneArrays(codes, levels, ci, dens, sh, D, c, s)
 
+    def save_checkpoint(self, path: str) -> None:
+        """save_checkpoint (io.cpp:250-279), the reference's SVRX writer."""
+        lib = load_ref()
+        lib.ref_save_checkpoint.argtypes = [C.c_void_p, C.c_char_p]
+        _chk(lib.ref_save_checkpoint(self.h, os.fsencode(path)))
+
+    @staticmethod
+    def load_checkpoint(path: str) -> "RefScene":
+        """load_checkpoint (io.cpp:283-359), the reference's SVRX reader."""
+        lib = load_ref()
+        lib.ref_load_checkpoint.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+        h = C.c_void_p()
+        _chk(lib.ref_load_checkpoint(os.fsencode(path), C.byref(h)))
+        return RefScene(h)
+
     def set_params(self, density=None, sh=None):
         d = None if density is None else np.ascontiguousarray(density, np.float32)
         s = None if sh is None else np.ascontiguousarray(sh, np.float32)

@@ -18,6 +18,7 @@
 #include <string>
 #include <vector>
 
+#include "svr/io.hpp"
 #include "svr/losses.hpp"
 #include "svr/optim.hpp"
 #include "svr/raster.hpp"
@@ -222,6 +223,17 @@ int ref_scene_from_paths(const uint64_t* codes, const uint8_t* levels, uint64_t 
 }
 
 void ref_scene_free(void* h) { delete static_cast<SparseScene*>(h); }
+
+// save_checkpoint / load_checkpoint (io.cpp:250-359): the reference's SVRX
+// writer and reader, to pin svr_scene_save_svrx / svr_scene_load_svrx.
+int ref_save_checkpoint(void* h, const char* path) {
+    return guarded([&] { save_checkpoint(*static_cast<SparseScene*>(h), path); });
+}
+
+int ref_load_checkpoint(const char* path, void** out) {
+    return guarded([&] { *out = new SparseScene(load_checkpoint(path)); });
+}
+
 
 void ref_scene_sizes(void* h, uint64_t* n, uint64_t* p, int* deg) {
     auto* s = static_cast<SparseScene*>(h);

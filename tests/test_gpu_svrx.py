@@ -1,7 +1,9 @@
 """SVRX checkpoints <-> device scenes, mirroring
-test_io.cpp:167-219: lossless round trip with bit-identical renders, the
-empty scene, byte identity with the restated container (oracle/svrx.py),
-rejection of corrupted / truncated / absent files, and a checkpoint of
+test_io.cpp:167-219: byte identity with the reference's own save_checkpoint
+(io.cpp:250-279, compiled unmodified into oracle/_ref), files crossing both
+ways between the reference's load_checkpoint and ours, lossless round trip
+with bit-identical renders, the empty scene, rejection of corrupted /
+truncated / absent files with the reference's verdicts, and a checkpoint of
 parameters a device training step has just updated."""
 import numpy as np
 import pytest
@@ -92,3 +94,46 @@ def test_checkpoint_after_device_training(svr, ctx, small, tmp_path):
     back = svr.Scene.load_svrx(ctx, path).arrays
     assert np.array_equal(back.density, d) and np.array_equal(back.sh.reshape(-1), s)
     assert not np.array_equal(back.density, small.density)
+
+
+def test_save_is_byte_identical_to_reference_and_loads_both_ways(svr, ctx, ref, tmp_path):
+    for seed, target, maxlv, deg in [(4, 20000, 7, 3), (9, 5000, 6, 1), (3, 600, 5, 0)]:
+        rs = ref.RefScene.generate(seed, target, maxlv, deg)
+        a = rs.arrays()
+        ours, theirs = str(tmp_path / f"o{seed}.svrx"), str(tmp_path / f"r{seed}.svrx")
+        svr.Scene(ctx, a).save_svrx(ours)
+        rs.save_checkpoint(theirs)
+        assert open(ours, "rb").read() == open(theirs, "rb").read()
+        # reference file -> our device loader; our file -> the reference loader
+        mine = svr.Scene.load_svrx(ctx, theirs).arrays
+        back = ref.RefScene.load_checkpoint(ours).arrays()
+        for f in ("codes", "levels", "corner_index", "density", "sh"):
+            assert np.array_equal(getattr(mine, f), getattr(a, f)), f
+            assert np.array_equal(getattr(back, f), getattr(a, f)), f
+        assert tuple(mine.bounds_center) == tuple(back.bounds_center)
+        assert mine.bounds_size == back.bounds_size and mine.sh_degree == deg
+
+
+def test_corrupt_files_rejected_like_the_reference(svr, ctx, ref, small, tmp_path):
+    """Every corruption the reference's load_checkpoint refuses, ours refuses
+    (and the reverse), on single-byte flips across the header and payload."""
+    path = str(tmp_path / "s.svrx")
+    svr.Scene(ctx, small).save_svrx(path)
+    data = open(path, "rb").read()
+    rng = np.random.default_rng(3)
+    offs = sorted(set([0, 3, 4, 8, 12, 16, 20, 40, 64] + list(rng.integers(0, len(data), 24))))
+    for off in offs:
+        b = bytearray(data)
+        b[off] ^= 0x5A
+        p = str(tmp_path / f"c{off}.svrx")
+        open(p, "wb").write(bytes(b))
+        ours_ok = theirs_ok = True
+        try:
+            svr.Scene.load_svrx(ctx, p)
+        except RuntimeError:
+            ours_ok = False
+        try:
+            ref.RefScene.load_checkpoint(p)
+        except (RuntimeError, ValueError):
+            theirs_ok = False
+        assert ours_ok == theirs_ok, f"byte {off}: ours {ours_ok}, reference {theirs_ok}"

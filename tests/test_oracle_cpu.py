@@ -213,3 +213,21 @@ def test_svrx_header_number_format():
              1e15: "1e+15", 1.5e20: "1.5e+20", 123.456: "123.456", -3.0: "-3.0"}
     for v, txt in cases.items():
         assert json_double(v) == txt, (v, json_double(v), txt)
+
+
+def test_svrx_restatement_matches_reference_writer(tmp_path):
+    """oracle/svrx.py (the container the product's SVRX tests compare
+    against) is byte-identical to the reference's own save_checkpoint
+    (io.cpp:250-279), and the reference's load_checkpoint reads it back."""
+    from oracle import ref, svrx
+    if not ref.ref_available():
+        pytest.skip("compiled reference unavailable")
+    for seed, target, maxlv, deg in [(4, 3000, 6, 3), (9, 800, 5, 1), (3, 512, 4, 0)]:
+        rs = ref.RefScene.generate(seed, target, maxlv, deg)
+        a = rs.arrays()
+        path = str(tmp_path / f"r{seed}.svrx")
+        rs.save_checkpoint(path)
+        assert open(path, "rb").read() == svrx.encode(a)
+        back = ref.RefScene.load_checkpoint(path).arrays()
+        for f in ("codes", "levels", "corner_index", "density", "sh"):
+            assert np.array_equal(getattr(back, f), getattr(a, f)), f
