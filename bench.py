@@ -96,6 +96,7 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--supersample", type=float, default=1.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-dropin", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=100)
     p.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
     return p.parse_args()
@@ -405,6 +406,30 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+def dropin_e2e(steps: int = 30):
+    """cfg2 frames/s as a C++ caller of the reference API sees them:
+    svr::render / render_with_pools (raster.hpp) linked against
+    libsvr_dropin.a + libsvr_b200.so (paper_2412_04459_b200/cpp/
+    dropin_bench.cpp; host SparseScene in, five double Images out per call)."""
+    exe = os.path.join(ROOT, "paper_2412_04459_b200", "cpp", "build", "dropin_bench")
+    if not os.path.exists(exe):
+        return {"value": None, "unit": "frames/s", "note": "dropin_bench not built"}
+    try:
+        r = subprocess.run([exe, str(steps)], capture_output=True, text=True, timeout=600)
+        line = json.loads(r.stdout.strip().splitlines()[-1])
+        d = line["dropin_fps"]
+    except (subprocess.SubprocessError, ValueError, IndexError, KeyError) as e:
+        return {"value": None, "unit": "frames/s", "note": f"dropin_bench failed: {e}"}
+    return {"value": d["stats"], "unit": "frames/s", "train_pattern": d["train"],
+            "cold_pattern": d["cold"], "steps": steps, "heap_tuned": line.get("heap_tuned"),
+            "note": "svr::render through libsvr_dropin.a, wall clock per call, host SparseScene "
+                    "in and five double Images out: value = unchanged scene (cache hit: content "
+                    "fingerprints of the 250 MB scene + float->double images), train_pattern = "
+                    "the caller's make_pools (400 MB of doubles) + render_with_pools after a "
+                    "parameter change, cold_pattern = new geometry every call (full upload + "
+                    "Morton tables); the caller keeps large blocks in its heap (mallopt)"}
+
+
 # ------------------------------------------------------------------ ours
 class RenderStep:
     """cfg2/cfg4 step: one view rendered into a resident frame."""
@@ -677,6 +702,10 @@ def run_ours(args, rank, world, local_rank):
             cpu = {"value": None, "unit": w["unit"], "cores": host_cores(), "kind": "reference",
                    "sample": f"unavailable: {type(e).__name__}: {e}"}
 
+    dropin = None
+    if world == 1 and w["kind"] == "render" and w["scene"] == "G" and not args.no_dropin:
+        dropin = dropin_e2e()
+
     config = bench_config(w, arrays.n_voxels, args.supersample)
     run = {"pool": arrays.n_pool, "entries_per_view": int(E), "visible_voxels": int(n_vis),
            "sort_passes": npass,
@@ -705,6 +734,7 @@ def run_ours(args, rank, world, local_rank):
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": w["unit"], "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "note": e2e_note},
+        "dropin_e2e": dropin,
         "gpu_launches": launches,
         "stage_ms_per_step": per_step,
         "clocks": clk,

@@ -208,6 +208,11 @@ int svr_frame_download(svr_frame* frame, svr_buffer which, void* dst, size_t byt
 int svr_frame_download_async(svr_frame* frame, svr_buffer which, void* dst, size_t bytes);
 /* Blocks until the frame's asynchronous downloads have landed. */
 int svr_frame_wait(svr_frame* frame);
+/* Page-locked host memory for svr_frame_download_async destinations (so the
+ * copy runs at full PCIe rate and truly asynchronously); free with
+ * svr_host_free. */
+int svr_host_alloc(size_t bytes, void** out);
+int svr_host_free(void* p);
 /* Device pointer + size of a buffer (no copy, valid until the next render). */
 int svr_frame_device_ptr(svr_frame* frame, svr_buffer which, void** ptr, size_t* bytes);
 

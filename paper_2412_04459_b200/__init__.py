@@ -125,6 +125,7 @@ EXPORTS = [
     "svr_synth_random_scene", "svr_ring_camera", "svr_free", "svr_launch_count",
     "svr_ctx_enable_timing", "svr_ctx_stage_times", "svr_frame_pre", "svr_render_oracle",
     "svr_synth_unbounded_scene", "svr_frame_loss_values", "svr_ctx_take_adam_nan",
+    "svr_host_alloc", "svr_host_free",
 ]
 STAGES = ["tile_setup", "preprocess", "scan", "duplicate", "sort", "ranges", "composite",
           "record", "downsample", "backward", "epilogue", "other"]

@@ -41,7 +41,11 @@
 // own float pools; a finite-difference harness with h ~ 1e-5 therefore
 // cannot be run through this library.
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cmath>
+#include <condition_variable>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -141,25 +145,125 @@ uint64_t hash_words(const uint64_t* w, size_t n, uint64_t seed) {
     return fold(h, n);
 }
 
-// Runs fn(begin, end) over [0, n) split into contiguous ranges on up to 16
-// threads (one range below 2^20 items) and folds the per-range digests.
-uint64_t parallel_digest(size_t n, const std::function<uint64_t(size_t, size_t)>& fn) {
-    const size_t hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-    const size_t parts = n < (size_t(1) << 20) ? 1 : hw;
-    std::vector<uint64_t> d(parts);
-    std::vector<std::thread> th;
-    for (size_t p = 0; p < parts; ++p) {
-        const size_t b = n * p / parts, e = n * (p + 1) / parts;
-        if (p + 1 == parts)
-            d[p] = fn(b, e);
-        else
-            th.emplace_back([&, p, b, e] { d[p] = fn(b, e); });
+// Host worker pool (up to 16 threads, created once) for the O(scene) host
+// work a value-semantics call has to do: fingerprints, PoolsD narrowing,
+// float -> double image conversion.
+class Pool {
+  public:
+    static Pool& get() {
+        static Pool p;
+        return p;
     }
-    for (auto& t : th) t.join();
+    size_t size() const { return workers_.size() + 1; }
+    // fn(part) for part in [0, parts); the caller runs parts too; returns
+    // when all are done. Calls from several host threads are serialised.
+    void run(size_t parts, const std::function<void(size_t)>& fn) {
+        std::lock_guard<std::mutex> one(call_mu_);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            fn_ = &fn;
+            parts_ = parts;
+            next_.store(0);
+            left_ = parts;
+            ++gen_;
+        }
+        cv_.notify_all();
+        work();
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&] { return left_ == 0; });
+        fn_ = nullptr;
+    }
+
+  private:
+    Pool() {
+        const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        for (unsigned i = 1; i < hw; ++i)
+            workers_.emplace_back([this] {
+                uint64_t seen = 0;
+                for (;;) {
+                    {
+                        std::unique_lock<std::mutex> lk(mu_);
+                        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+                        if (stop_) return;
+                        seen = gen_;
+                    }
+                    work();
+                }
+            });
+    }
+    ~Pool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : workers_) t.join();
+    }
+    void work() {
+        const std::function<void(size_t)>* fn;
+        size_t parts;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            fn = fn_;
+            parts = parts_;
+        }
+        if (!fn) return;
+        size_t did = 0;
+        for (size_t i; (i = next_.fetch_add(1)) < parts; ++did) (*fn)(i);
+        if (did) {
+            std::lock_guard<std::mutex> lk(mu_);
+            left_ -= did;
+            if (left_ == 0) done_cv_.notify_all();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex call_mu_, mu_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(size_t)>* fn_ = nullptr;
+    size_t parts_ = 0, left_ = 0;
+    std::atomic<size_t> next_{0};
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+// Runs fn(begin, end) over [0, n) split into contiguous ranges on the pool
+// (one range below 2^20 items) and folds the per-range digests in order.
+uint64_t parallel_digest(size_t n, const std::function<uint64_t(size_t, size_t)>& fn) {
+    const size_t parts = n < (size_t(1) << 20) ? 1 : Pool::get().size();
+    std::vector<uint64_t> d(parts);
+    if (parts == 1) {
+        d[0] = fn(0, n);
+    } else {
+        Pool::get().run(parts, [&](size_t p) { d[p] = fn(n * p / parts, n * (p + 1) / parts); });
+    }
     uint64_t h = kM3 ^ n;
     for (uint64_t x : d) h = fold(h, x);
     return h;
 }
+
+// Per-phase wall time of the drop-in's host work (SVR_DROPIN_PROFILE=1
+// prints the totals at exit).
+struct Profile {
+    bool on = std::getenv("SVR_DROPIN_PROFILE") != nullptr;
+    double ms[8] = {};
+    const char* names[8] = {"fingerprint", "set_params", "render",      "download",
+                            "convert",     "records",    "narrow_pools", "full_upload"};
+    ~Profile() {
+        if (!on) return;
+        std::fprintf(stderr, "svr dropin host time (ms):");
+        for (int i = 0; i < 8; ++i) std::fprintf(stderr, " %s %.1f", names[i], ms[i]);
+        std::fprintf(stderr, "\n");
+    }
+};
+Profile g_prof;
+struct Phase {
+    int i;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    ~Phase() {
+        if (g_prof.on)
+            g_prof.ms[i] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+};
 
 uint64_t digest_bytes(const void* data, size_t bytes) {
     const size_t nw = bytes / 8;
@@ -189,12 +293,32 @@ uint64_t geometry_digest(const SparseScene& scene) {
 
 // Parallel double -> float narrowing of a PoolsD vector.
 void narrow_into(const std::vector<double>& src, std::vector<float>& dst) {
+    Phase ph{6};
     dst.resize(src.size());
     parallel_digest(src.size(), [&](size_t b, size_t e) {
         for (size_t i = b; i < e; ++i) dst[i] = float(src[i]);
         return uint64_t(0);
     });
 }
+
+// Page-locked staging for uploads and read-backs (grown on demand).
+struct Pinned {
+    void* p = nullptr;
+    size_t bytes = 0;
+    float* reserve(size_t b) {
+        if (b > bytes) {
+            if (p) svr_host_free(p);
+            p = nullptr;
+            bytes = 0;
+            check(svr_host_alloc(b, &p));
+            bytes = b;
+        }
+        return static_cast<float*>(p);
+    }
+    ~Pinned() {
+        if (p) svr_host_free(p);
+    }
+};
 
 // The device copy of the last scene this thread rendered, with the
 // fingerprints of what it holds. Frames keep their scene alive through a
@@ -227,19 +351,33 @@ std::shared_ptr<DeviceScene> device_scene(const SparseScene& scene, const Params
     const size_t n = scene.voxel_count();
     if (p.n_density != scene.pool_count() || p.n_sh != scene.sh.size())
         throw std::invalid_argument("parameter pools do not match the scene");
-    const uint64_t geo = geometry_digest(scene);
-    const uint64_t hd = digest_bytes(p.density, p.n_density * 4);
-    const uint64_t hs = digest_bytes(p.sh, p.n_sh * 4);
+    uint64_t geo, hd, hs;
+    {
+        Phase ph{0};
+        geo = geometry_digest(scene);
+        hd = digest_bytes(p.density, p.n_density * 4);
+        hs = digest_bytes(p.sh, p.n_sh * 4);
+    }
+    Phase ph{1};
     std::shared_ptr<DeviceScene>& c = cached_scene();
     if (c && c->geo == geo && c->n_voxels == n) {
         if (c->dens != hd || c->sh != hs) {
-            check(svr_scene_set_params(ctx(), c->s, c->dens != hd ? p.density : nullptr,
-                                       c->sh != hs ? p.sh : nullptr, 0));
+            // through page-locked staging (a parallel copy, then one DMA at
+            // full PCIe rate instead of the driver's pageable path)
+            thread_local Pinned stage;
+            const size_t nd = c->dens != hd ? p.n_density : 0, ns = c->sh != hs ? p.n_sh : 0;
+            float* buf = stage.reserve(std::max<size_t>(nd + ns, 1) * 4);
+            parallel_digest(nd + ns, [&](size_t b, size_t e) {
+                for (size_t i = b; i < e; ++i) buf[i] = i < nd ? p.density[i] : p.sh[i - nd];
+                return uint64_t(0);
+            });
+            check(svr_scene_set_params(ctx(), c->s, nd ? buf : nullptr, ns ? buf + nd : nullptr, 0));
             c->dens = hd;
             c->sh = hs;
         }
         return c;
     }
+    Phase full{7};
     std::vector<uint64_t> codes(n);
     std::vector<uint8_t> levels(n);
     for (size_t i = 0; i < n; ++i) {
@@ -285,25 +423,100 @@ std::shared_ptr<DeviceScene> device_scene(const SparseScene& scene, const PoolsD
     return device_scene(scene, {dens.data(), dens.size(), sh.data(), sh.size()});
 }
 
+struct ImageReq {
+    svr_buffer which;
+    Image* img;
+    int w, h, ch;
+    bool sentinel;
+};
+
+// Downloads several frame buffers with one wait (copy stream, pinned
+// staging), then widens them to the reference's double Images on the pool;
+// depth sentinels map back to the exact double far value.
+void download_images(svr_frame* f, std::vector<ImageReq> reqs, double far) {
+    thread_local Pinned stage;
+    size_t total = 0;
+    for (const ImageReq& r : reqs) total += size_t(r.w) * r.h * r.ch;
+    float* buf = stage.reserve(std::max<size_t>(total, 1) * 4);
+    {
+        Phase ph{3};
+        size_t off = 0;
+        for (const ImageReq& r : reqs) {
+            const size_t n = size_t(r.w) * r.h * r.ch;
+            check(svr_frame_download_async(f, r.which, buf + off, n * 4));
+            off += n;
+        }
+        check(svr_frame_wait(f));
+    }
+    Phase ph{4};
+    size_t off = 0;
+    const float ffar = float(far);
+    for (const ImageReq& r : reqs) {
+        const size_t n = size_t(r.w) * r.h * r.ch;
+        *r.img = Image(r.w, r.h, r.ch);
+        double* dst = r.img->data.data();
+        const float* src = buf + off;
+        const bool sent = r.sentinel;
+        const size_t parts = n < (size_t(1) << 18) ? 1 : Pool::get().size();
+        auto conv = [&](size_t p) {
+            const size_t b = n * p / parts, e = n * (p + 1) / parts;
+            for (size_t i = b; i < e; ++i) dst[i] = (sent && src[i] == ffar) ? far : double(src[i]);
+        };
+        if (parts == 1)
+            conv(0);
+        else
+            Pool::get().run(parts, conv);
+        off += n;
+    }
+}
+
 Image download_image(svr_frame* f, svr_buffer which, int w, int h, int ch, double far = 0.0,
                      bool sentinel = false) {
-    std::vector<float> tmp(size_t(w) * h * ch);
-    check(svr_frame_download(f, which, tmp.data(), tmp.size() * sizeof(float)));
-    Image img(w, h, ch);
-    const float ffar = float(far);
-    for (size_t i = 0; i < tmp.size(); ++i)
-        img.data[i] = (sentinel && tmp[i] == ffar) ? far : double(tmp[i]);
+    Image img;
+    download_images(f, {{which, &img, w, h, ch, sentinel}}, far);
     return img;
 }
 
 // GPU state behind a ForwardRecords handed out by render_with_pools. Owned by
 // the shared_ptr's deleter, so it lives exactly as long as the records.
+// Frames are recycled: a frame's device buffers (entries, records, images:
+// ~0.6 GB at config 2) are allocated on its first render and reused by the
+// next render through it, so a call does not pay cudaMalloc / cudaFree.
+// Released frames go back to a free list per context.
+std::mutex g_frames_mu;
+std::unordered_map<svr_ctx*, std::vector<svr_frame*>> g_free_frames;
+
+svr_frame* acquire_frame() {
+    svr_ctx* c = ctx();
+    {
+        std::lock_guard<std::mutex> lk(g_frames_mu);
+        auto& v = g_free_frames[c];
+        if (!v.empty()) {
+            svr_frame* f = v.back();
+            v.pop_back();
+            return f;
+        }
+    }
+    svr_frame* f = nullptr;
+    check(svr_frame_create(c, &f));
+    return f;
+}
+
+void release_frame(svr_ctx* c, svr_frame* f) {
+    if (!f) return;
+    std::lock_guard<std::mutex> lk(g_frames_mu);
+    auto& v = g_free_frames[c];
+    if (v.size() < 4)
+        v.push_back(f);
+    else
+        svr_frame_destroy(f);
+}
+
 struct GpuRecords {
     std::shared_ptr<DeviceScene> scene;
+    svr_ctx* owner = nullptr;
     svr_frame* frame = nullptr;
-    ~GpuRecords() {
-        if (frame) svr_frame_destroy(frame);
-    }
+    ~GpuRecords() { release_frame(owner, frame); }
 };
 
 std::mutex g_mu;
@@ -415,24 +628,31 @@ RenderOutput render_on(std::shared_ptr<DeviceScene> dev, const SparseScene& scen
                        const Camera& cam, const RenderOptions& opts) {
     auto gpu = std::make_shared<GpuRecords>();
     gpu->scene = std::move(dev);
-    check(svr_frame_create(ctx(), &gpu->frame));
+    gpu->owner = ctx();
+    gpu->frame = acquire_frame();
     const svr_camera c = to_c(cam);
     const svr_render_options o = to_c(opts);
-    check(svr_render(ctx(), gpu->scene->s, &c, &o, gpu->frame));
+    {
+        Phase ph{2};
+        check(svr_render(ctx(), gpu->scene->s, &c, &o, gpu->frame));
+    }
     svr_frame* f = gpu->frame;
     const int W = cam.width, H = cam.height;
     RenderOutput out;
-    out.color = download_image(f, SVR_BUF_COLOR, W, H, 3);
-    out.depth = download_image(f, SVR_BUF_DEPTH, W, H, 1, opts.far_sentinel, true);
-    out.median_depth = download_image(f, SVR_BUF_MEDIAN_DEPTH, W, H, 1, opts.far_sentinel, true);
-    out.normal = download_image(f, SVR_BUF_NORMAL, W, H, 3);
-    out.transmittance = download_image(f, SVR_BUF_TRANSMITTANCE, W, H, 1);
+    download_images(f,
+                    {{SVR_BUF_COLOR, &out.color, W, H, 3, false},
+                     {SVR_BUF_DEPTH, &out.depth, W, H, 1, true},
+                     {SVR_BUF_MEDIAN_DEPTH, &out.median_depth, W, H, 1, true},
+                     {SVR_BUF_NORMAL, &out.normal, W, H, 3, false},
+                     {SVR_BUF_TRANSMITTANCE, &out.transmittance, W, H, 1, false}},
+                    opts.far_sentinel);
     if (opts.record_stats) {
         std::vector<float> mb(scene.voxel_count());
         check(svr_frame_download(f, SVR_BUF_MAX_BLEND, mb.data(), mb.size() * sizeof(float)));
         out.max_blend_weight.assign(mb.begin(), mb.end());
     }
     if (opts.training) {
+        Phase ph{5};
         svr_frame_info info;
         check(svr_frame_get_info(f, &info));
         const Camera ss_cam = scaled_camera(cam, opts);
@@ -564,18 +784,24 @@ RenderOutput render_oracle(const SparseScene& scene, const Camera& cam, const Re
         throw std::invalid_argument("render_oracle on the GPU does not record per-voxel stats");
     auto sh = device_scene(scene);
     svr_frame* f = nullptr;
-    check(svr_frame_create(ctx(), &f));
-    std::unique_ptr<svr_frame, int (*)(svr_frame*)> guard(f, svr_frame_destroy);
+    f = acquire_frame();
+    struct Back {
+        svr_ctx* c;
+        svr_frame* f;
+        ~Back() { release_frame(c, f); }
+    } back{ctx(), f};
     const svr_camera c = to_c(cam);
     const svr_render_options o = to_c(opts);
     check(svr_render_oracle(ctx(), sh->s, &c, &o, f));
     const int W = cam.width, H = cam.height;
     RenderOutput out;
-    out.color = download_image(f, SVR_BUF_COLOR, W, H, 3);
-    out.depth = download_image(f, SVR_BUF_DEPTH, W, H, 1, opts.far_sentinel, true);
-    out.median_depth = download_image(f, SVR_BUF_MEDIAN_DEPTH, W, H, 1, opts.far_sentinel, true);
-    out.normal = download_image(f, SVR_BUF_NORMAL, W, H, 3);
-    out.transmittance = download_image(f, SVR_BUF_TRANSMITTANCE, W, H, 1);
+    download_images(f,
+                    {{SVR_BUF_COLOR, &out.color, W, H, 3, false},
+                     {SVR_BUF_DEPTH, &out.depth, W, H, 1, true},
+                     {SVR_BUF_MEDIAN_DEPTH, &out.median_depth, W, H, 1, true},
+                     {SVR_BUF_NORMAL, &out.normal, W, H, 3, false},
+                     {SVR_BUF_TRANSMITTANCE, &out.transmittance, W, H, 1, false}},
+                    opts.far_sentinel);
     return out;
 }
 

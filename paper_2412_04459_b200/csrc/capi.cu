@@ -1824,6 +1824,20 @@ int svr_sort_entries(svr_ctx* ctx, uint64_t n, uint64_t* keys, uint32_t* values)
 
 void svr_free(void* p) { std::free(p); }
 
+int svr_host_alloc(size_t bytes, void** out) {
+    return guard([&] {
+        require(out != nullptr, SVR_ERR_INVALID_ARGUMENT, "null argument");
+        *out = nullptr;
+        if (bytes) SVR_CUDA(cudaMallocHost(out, bytes));
+    });
+}
+
+int svr_host_free(void* p) {
+    return guard([&] {
+        if (p) SVR_CUDA(cudaFreeHost(p));
+    });
+}
+
 unsigned long long svr_launch_count(void) { return g_launches.load(); }
 
 int svr_ctx_enable_timing(svr_ctx* ctx, int enable) {
