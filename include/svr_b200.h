@@ -335,6 +335,32 @@ int svr_train_step_l1(svr_ctx* ctx, const svr_scene* scene, const svr_camera* ca
                       const svr_render_options* opts, const float* gt_device, svr_frame* frame,
                       svr_gradients* grads, int accumulate, float* loss_device);
 
+/* ---- multi-GPU training step ------------------------------
+ * One process per GPU. Rank 0 makes a unique id (svr_comm_unique_id), the
+ * caller hands it to every rank by its own means, each rank creates its
+ * communicator on its context. svr_train_batch_l1 runs forward -> L1 ->
+ * backward over the rank's views (svr_train_step_l1, accumulating into the
+ * device gradients; an empty batch contributes zeros), sums the per-view L1
+ * losses into *loss_device and, when comm spans more than one rank,
+ * all-reduces [density | SH | priority] in place over NCCL (buckets of
+ * 64 MiB in one group) on the context stream, then polls NCCL's asynchronous
+ * error state. NCCL (libnccl.so.2) is loaded at first use. */
+typedef struct svr_comm svr_comm;
+int svr_comm_unique_id(uint8_t id[128]);
+int svr_comm_create(svr_ctx* ctx, const uint8_t id[128], int rank, int world, svr_comm** out);
+int svr_comm_destroy(svr_comm* comm);
+/* Registers a device buffer (e.g. the gradients) with the communicator, so
+ * NCCL may use NVLS in-switch reduction / zero-copy paths on it. */
+int svr_comm_register(svr_comm* comm, void* ptr, size_t bytes);
+/* SVR_ERR_RUNTIME (communicator aborted) after an asynchronous NCCL error. */
+int svr_comm_check(svr_comm* comm);
+int svr_comm_allreduce_gradients(svr_comm* comm, svr_gradients* grads, uint64_t n_pool,
+                                 uint64_t n_sh, uint64_t n_vox);
+int svr_train_batch_l1(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cams,
+                       const float* const* gts_device, int n_views,
+                       const svr_render_options* opts, svr_frame* frame, svr_gradients* grads,
+                       svr_comm* comm, float* loss_device);
+
 /* ---- pipeline pieces (raster.hpp:115-127), batch form, host buffers ---- */
 /* project_voxel (raster.cpp:72-118) for n voxels. visible[i] is 0/1; aabb is
  * (x0,x1,y0,y1) and rect (tx0,tx1,ty0,ty1) per voxel. */

@@ -125,7 +125,9 @@ EXPORTS = [
     "svr_synth_random_scene", "svr_ring_camera", "svr_free", "svr_launch_count",
     "svr_ctx_enable_timing", "svr_ctx_stage_times", "svr_frame_pre", "svr_render_oracle",
     "svr_synth_unbounded_scene", "svr_frame_loss_values", "svr_ctx_take_adam_nan",
-    "svr_host_alloc", "svr_host_free",
+    "svr_host_alloc", "svr_host_free", "svr_comm_unique_id", "svr_comm_create",
+    "svr_comm_destroy", "svr_comm_register", "svr_comm_check", "svr_comm_allreduce_gradients",
+    "svr_train_batch_l1",
 ]
 STAGES = ["tile_setup", "preprocess", "scan", "duplicate", "sort", "ranges", "composite",
           "record", "downsample", "backward", "epilogue", "other"]
@@ -206,6 +208,18 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "svr_ring_camera": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
                                       C.c_double, C.POINTER(svr_camera)]),
         "svr_free": (None, [P]),
+        "svr_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(P)]),
+        "svr_host_free": (C.c_int, [P]),
+        "svr_comm_unique_id": (C.c_int, [P]),
+        "svr_comm_create": (C.c_int, [P, P, C.c_int, C.c_int, C.POINTER(P)]),
+        "svr_comm_destroy": (C.c_int, [P]),
+        "svr_comm_register": (C.c_int, [P, P, C.c_size_t]),
+        "svr_comm_check": (C.c_int, [P]),
+        "svr_comm_allreduce_gradients": (C.c_int, [P, C.POINTER(svr_gradients), C.c_uint64,
+                                                   C.c_uint64, C.c_uint64]),
+        "svr_train_batch_l1": (C.c_int, [P, P, C.POINTER(svr_camera), C.POINTER(P), C.c_int,
+                                         C.POINTER(svr_render_options), P,
+                                         C.POINTER(svr_gradients), P, P]),
         "svr_launch_count": (C.c_ulonglong, []),
         "svr_ctx_enable_timing": (C.c_int, [P, C.c_int]),
         "svr_ctx_stage_times": (C.c_int, [P, C.POINTER(C.c_double), C.c_int, C.c_int]),

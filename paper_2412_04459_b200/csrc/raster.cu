@@ -857,6 +857,9 @@ constexpr size_t kCompSmem = size_t(2) * kCompWarps * 32 * kRecordF4 * sizeof(fl
 // MODE 0: plain render; 1: record pass (RECORD); 2: render with per-voxel
 // max-blend stats and/or staged training records (their checks compiled in);
 // 3: staged training records only (the single-pass training render).
+#ifndef SVR_PHB_SLABS
+#define SVR_PHB_SLABS 0
+#endif
 constexpr int kBatch = 1024;        // entries culled per CTA batch (cooperative path)
 constexpr int kSubs = kBatch / 32;  // 32-entry sub-chunks per batch
 
@@ -1023,7 +1026,11 @@ __device__ __forceinline__ void composite_tile_warp(const DevCamera& cam, const 
                 continue;
             const float4 lo = wrec[s_][0];
             float ta, tb;
+#if SVR_PHB_SLABS
+            slab_s(lo, ix, iy, iz, ssel, ta, tb);
+#else
             slab(lo, ix, iy, iz, ta, tb);  // same floats as slab_s; needs no per-lane face selectors
+#endif
             const float4 va = wrec[s_][2], vb = wrec[s_][3];
             const float inv = wrec[s_][5].w;
             const float seg = tb - ta;
@@ -1407,15 +1414,18 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
     if (a.pix_count) a.pix_count[slot] = cnt;
 }
 
+// CTAs per SM the register allocation targets: 4 for the plain render (63
+// registers; 3 with 75 is 3 % slower), 3 for the recording modes, whose
+// extra state spills otherwise (config 3 staged render 316 -> 296 us).
 #ifndef SVR_COMP_MINB
-#define SVR_COMP_MINB 4
+#define SVR_COMP_MINB(MODE) ((MODE) == 0 ? 4 : 3)
 #endif
 // K7: one CTA per tile (LPT order), warp-autonomous or CTA-cooperative
 // (launch_composite picks per frame: the cooperative cull pays once tiles
 // hold thousands of entries — config 4, ~22K per tile: 3.62 -> 2.11 ms — and
 // costs its batch barrier on short lists — config 2, ~430: 0.33 -> 0.38 ms).
 template <int K, int MODE>
-__global__ void __launch_bounds__(256, SVR_COMP_MINB) composite_kernel(DevCamera cam, CompositeArgs a) {
+__global__ void __launch_bounds__(256, SVR_COMP_MINB(MODE)) composite_kernel(DevCamera cam, CompositeArgs a) {
     pdl_enter();
     extern __shared__ float4 s_rec_dyn[];  // [2][8 warps][32 slots][kRecordF4]
     __shared__ CompShared<K, MODE> sh;
@@ -1424,7 +1434,7 @@ __global__ void __launch_bounds__(256, SVR_COMP_MINB) composite_kernel(DevCamera
 }
 
 template <int K, int MODE>
-__global__ void __launch_bounds__(256, SVR_COMP_MINB) composite_coop_kernel(DevCamera cam, CompositeArgs a) {
+__global__ void __launch_bounds__(256, SVR_COMP_MINB(MODE)) composite_coop_kernel(DevCamera cam, CompositeArgs a) {
     pdl_enter();
     extern __shared__ float4 s_rec_dyn[];
     __shared__ CompShared<K, MODE> sh;

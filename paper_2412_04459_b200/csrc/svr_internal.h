@@ -122,6 +122,7 @@ struct svr_ctx {
     // device gradients of a host-buffer svr_render_backward, kept between
     // calls (config 2: 215 MB that would otherwise be allocated per call)
     svrb::DevBuf bwd_density, bwd_sh, bwd_priority;
+    svrb::DevBuf batch_losses;  // per-view L1 losses of svr_train_batch_l1
 };
 
 struct svr_scene {

@@ -41,6 +41,47 @@ def flat_layout(n_pool: int, n_sh: int, n_vox: int = 0, align: int = 64):
     return 0, sh_off, prio_off, prio_off + n_vox
 
 
+class NcclComm:
+    """svr_comm (include/svr_b200.h): the library's own NCCL communicator for
+    the C-ABI training step (svr_train_batch_l1), one per rank. `unique_id`
+    comes from rank 0's NcclComm.make_id(), handed to the others by the
+    caller (e.g. a torch.distributed broadcast)."""
+
+    def __init__(self, ctx, unique_id: bytes, rank: int, world: int):
+        import paper_2412_04459_b200 as svr
+        self.svr, self.ctx = svr, ctx
+        lib = svr.load_library()
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        h = C.c_void_p()
+        svr._check(lib.svr_comm_create(ctx.h, buf, rank, world, C.byref(h)))
+        self.h, self.rank, self.world = h, rank, world
+
+    @staticmethod
+    def make_id() -> bytes:
+        import paper_2412_04459_b200 as svr
+        buf = (C.c_uint8 * 128)()
+        svr._check(svr.load_library().svr_comm_unique_id(buf))
+        return bytes(buf)
+
+    def register(self, tensor) -> None:
+        self.svr._check(self.svr.load_library().svr_comm_register(
+            self.h, C.c_void_p(tensor.data_ptr()), C.c_size_t(tensor.numel() * tensor.element_size())))
+
+    def check(self) -> None:
+        self.svr._check(self.svr.load_library().svr_comm_check(self.h))
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.svr.load_library().svr_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def allreduce_flat(buf, group=None) -> None:
     """Sums the flat gradient buffer over all ranks, in place (one collective)."""
     import torch.distributed as dist
@@ -56,12 +97,14 @@ class ShardedTrainer:
     flat device gradient buffer, then all-reduces it across ranks.
     """
 
-    def __init__(self, ctx, scene, cameras: Sequence, gts: Sequence, opts, group=None):
+    def __init__(self, ctx, scene, cameras: Sequence, gts: Sequence, opts, group=None,
+                 comm: Optional["NcclComm"] = None):
         import torch
 
         import paper_2412_04459_b200 as svr
         self.svr = svr
         self.ctx, self.scene, self.cams, self.opts, self.group = ctx, scene, cameras, opts, group
+        self.comm = comm  # NcclComm: the whole step through svr_train_batch_l1
         dev = torch.device("cuda", ctx.device)
         self.gts = [g if isinstance(g, torch.Tensor) else
                     torch.tensor(np.asarray(g), dtype=torch.float32, device=dev) for g in gts]
@@ -75,6 +118,8 @@ class ShardedTrainer:
         self.priority = self.flat[p0:p0 + self.n_vox]
         self.frame = svr.Frame(ctx)
         self.stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+        if comm is not None:
+            comm.register(self.flat)
 
     def step(self, view_ids: Sequence[int], reduce: bool = True) -> float:
         import torch
@@ -84,6 +129,17 @@ class ShardedTrainer:
         g.density, g.sh = self.density_grad.data_ptr(), self.sh_grad.data_ptr()
         g.priority, g.on_device = self.priority.data_ptr(), 1
         torch.cuda.current_stream().synchronize()
+        if self.comm is not None:  # one C-ABI call: views, loss sum, NCCL all-reduce
+            n = len(view_ids)
+            cams = (svr.svr_camera * max(n, 1))(*[self.cams[v].to_c() for v in view_ids])
+            gts = (C.c_void_p * max(n, 1))(*[self.gts[v].data_ptr() for v in view_ids])
+            o = self.opts.to_c()
+            svr._check(lib.svr_train_batch_l1(self.ctx.h, self.scene.h, cams, gts, n, C.byref(o),
+                                              self.frame.h, C.byref(g),
+                                              self.comm.h if reduce else None,
+                                              C.c_void_p(self.loss.data_ptr())))
+            torch.cuda.current_stream().wait_stream(self.stream)
+            return float(self.loss.item())
         if not view_ids:  # no view on this rank: contribute zeros to the sum
             with torch.cuda.stream(self.stream):
                 self.flat.zero_()

@@ -96,3 +96,42 @@ def test_two_rank_allreduce_matches_single_process_and_reference(svr, ref, tmp_p
         nbad, _ = grad_close(red[name], g1[name], rel=1e-4)
         assert nbad == 0, name
     assert np.abs(red["density"]).max() > 0
+
+
+def test_c_abi_batch_step_and_nccl_allreduce(svr, ref):
+    """svr_train_batch_l1 (the C-ABI sharded step a C++ caller uses) equals
+    ShardedTrainer's torch-side accumulation; on a one-rank NCCL communicator
+    svr_comm_allreduce_gradients is the identity and svr_comm_check is clean."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2412_04459_b200.multiview import NcclComm, ShardedTrainer
+    ctx = svr.Context(0)
+    arrays, scene, cams, opts = _setup(svr, ctx)
+    rng = np.random.default_rng(9)
+    gts = [rng.uniform(0, 1, (RES, RES, 3)).astype(np.float32) for _ in cams]
+    comm = NcclComm(ctx, NcclComm.make_id(), 0, 1)
+    a = ShardedTrainer(ctx, scene, cams, gts, opts)
+    la = a.step([0, 1, 2, 3], reduce=False)
+    ga = a.gradients()
+    b = ShardedTrainer(ctx, scene, cams, gts, opts, comm=comm)
+    lb = b.step([0, 1, 2, 3])
+    gb = b.gradients()
+    assert abs(la - lb) <= 1e-6 * max(1.0, abs(la))
+    for k in ("density", "sh", "priority"):
+        nbad, _ = grad_close(gb[k], ga[k], rel=1e-5)
+        assert nbad == 0, k
+    # the NCCL all-reduce itself, one rank: identity, in place
+    before = b.flat.clone()
+    g = svr.svr_gradients()
+    g.density, g.sh, g.priority, g.on_device = (b.density_grad.data_ptr(), b.sh_grad.data_ptr(),
+                                                b.priority.data_ptr(), 1)
+    lib = svr.load_library()
+    svr._check(lib.svr_comm_allreduce_gradients(comm.h, C.byref(g), b.n_pool, b.n_sh, b.n_vox))
+    ctx.synchronize()
+    assert torch.equal(before, b.flat)
+    comm.check()
+    # an empty batch contributes zeros
+    assert b.step([]) == 0.0 and float(b.flat.abs().max()) == 0.0
+    comm.close()

@@ -11,4 +11,4 @@ sed -i "s#-I../include#-I$ROOT/include#; s#../include/svr_b200.h#$ROOT/include/s
 make -C $D -j8 NVEXTRA="$*" > $D/build.log 2>&1 || (tail -30 $D/build.log; false)
 mkdir -p $ROOT/variants
 cp $D/libsvr_b200.so $ROOT/variants/libsvr_$NAME.so
-grep -A2 "composite_kernelILi1ELb0" $D/build/raster.ptxas.log | grep registers
+grep -A3 "composite_kernelILi1ELi0E" $D/build/raster.ptxas.log | grep -E "registers|spill"
