@@ -23,7 +23,8 @@ driver runs the default):
   cfg4  8M-voxel init_unbounded scene, 1024^2 views of ring_cameras(256, ...,
         radius 1.0) sharded by view.
   cfg5  cfg4 scene, training step on a batch of 4 views per GPU with one
-        in-place all-reduce of the flat [density | SH] gradient (NCCL).
+        in-place all-reduce of the flat [density | SH | priority] gradient
+        (the library's NCCL communicator, svr_train_batch_l1).
 
 --impl reference : the reference's own CPU implementation (oracle/_ref,
          compiled unmodified) on this host's cores, same metric/config.
@@ -466,9 +467,20 @@ class TrainStep:
         # ShardedTrainer indexes cameras/gts by view id
         idx = {v: k for k, v in enumerate(self.views)}
         self.idx = idx
+        comm = None
+        if world > 1 and os.environ.get("SVR_BENCH_BACKEND", "nccl") == "nccl":
+            # the library's own NCCL communicator: the whole step (views, loss,
+            # bucketed all-reduce of the flat registered buffer) is one
+            # svr_train_batch_l1 call; the id travels over torch.distributed
+            import torch.distributed as dist
+            from paper_2412_04459_b200.multiview import NcclComm
+            box = [NcclComm.make_id() if rank == 0 else None]
+            dist.broadcast_object_list(box, src=0)
+            comm = NcclComm(ctx, box[0], rank, world)
         self.trainer = ShardedTrainer(ctx, scene, [cams[v] for v in self.views],
                                       [gts[v] for v in self.views],
-                                      svr.RenderOptions(K=1, supersample=1.0, training=True))
+                                      svr.RenderOptions(K=1, supersample=1.0, training=True),
+                                      comm=comm)
         self.loss = None
 
     def ids(self, i):

@@ -119,8 +119,8 @@ def test_c_abi_batch_step_and_nccl_allreduce(svr, ref):
     lb = b.step([0, 1, 2, 3])
     gb = b.gradients()
     assert abs(la - lb) <= 1e-6 * max(1.0, abs(la))
-    for k in ("density", "sh", "priority"):
-        nbad, _ = grad_close(gb[k], ga[k], rel=1e-5)
+    for k in ("density", "sh", "priority"):  # fp32 atomics: run-to-run reassociation only
+        nbad, _ = grad_close(gb[k], ga[k])
         assert nbad == 0, k
     # the NCCL all-reduce itself, one rank: identity, in place
     before = b.flat.clone()
