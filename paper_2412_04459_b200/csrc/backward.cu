@@ -633,8 +633,8 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
 // K10: 16 lanes per voxel, lane m owns SH basis function m, so the SH rows
 // (3(d+1)^2 floats per voxel) are read and written as contiguous runs, and
 // component m of K9's per-voxel record (8 corner densities, colour, normal,
-// priority). The raw colour for the clamp mask (sh.hpp:66-74) is reduced
-// over the 16 lanes; lanes 0..7 add the normal chain (field.hpp:158-170) to
+// priority). The clamp mask (sh.hpp:66-74) comes from K1's clamped colour;
+// lanes 0..7 add the normal chain (field.hpp:158-170) to
 // their corner and issue the voxel's 8 pool atomics. Voxels outside `pre`
 // leave at once (their group only zeroes SH gradients when not accumulating).
 // One visible voxel (all 16 lanes of its group present).
@@ -653,17 +653,31 @@ __device__ __forceinline__ void epilogue_visible(const EpilogueArgs& a, uint64_t
     float bm = 0.f;
 #pragma unroll
     for (int i = 0; i < 16; ++i) bm = (m == i) ? b[i] : bm;
-    float c0 = 0.f, c1 = 0.f, c2 = 0.f;
-    if (m < nb) {
-        const float* co = a.sh + v * uint64_t(a.sh_stride) + 3 * m;
-        c0 = co[0], c1 = co[1], c2 = co[2];
-    }
-    float r0 = bm * c0, r1 = bm * c1, r2 = bm * c2;
+    // The clamp mask (sh.hpp:72-74) is raw > 0 per channel, i.e. the
+    // forward's clamped colour max(0, raw) > 0: read from K1's record (16 B,
+    // one sector for the 16 lanes) instead of re-evaluating the SH sum from
+    // the coefficients (192 B per voxel), and exactly the clamp the forward
+    // applied.
+    float4 rgb;
+    if (!a.sh) {
+        rgb = __ldg(a.records + v * kRecordF4 + 4);
+    } else {
+        // the pools changed since the forward (svr_scene_set_params): the
+        // reference's mask reads the pools it is given (raster.cpp:414), so
+        // evaluate raw from the current coefficients, reduced over the lanes
+        float c0 = 0.f, c1 = 0.f, c2 = 0.f;
+        if (m < nb) {
+            const float* co = a.sh + v * uint64_t(a.sh_stride) + 3 * m;
+            c0 = co[0], c1 = co[1], c2 = co[2];
+        }
+        float r0 = bm * c0, r1 = bm * c1, r2 = bm * c2;
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) {
-        r0 += __shfl_xor_sync(gmask, r0, o, 16);
-        r1 += __shfl_xor_sync(gmask, r1, o, 16);
-        r2 += __shfl_xor_sync(gmask, r2, o, 16);
+        for (int o = 8; o > 0; o >>= 1) {
+            r0 += __shfl_xor_sync(gmask, r0, o, 16);
+            r1 += __shfl_xor_sync(gmask, r1, o, 16);
+            r2 += __shfl_xor_sync(gmask, r2, o, 16);
+        }
+        rgb = make_float4(r0, r1, r2, 0.f);
     }
     const float gc0 = __shfl_sync(gmask, gvm, 8, 16), gc1 = __shfl_sync(gmask, gvm, 9, 16),
                 gc2 = __shfl_sync(gmask, gvm, 10, 16);
@@ -672,9 +686,9 @@ __device__ __forceinline__ void epilogue_visible(const EpilogueArgs& a, uint64_t
     // reset the record only now: a store right behind the load of the same
     // address stalls the thread until the load returns (0.84 vs 0.16 ms)
     a.g_vox[16 * v + m] = 0.f;
-    const float g0 = r0 > 0.f ? gc0 : 0.f;
-    const float g1 = r1 > 0.f ? gc1 : 0.f;
-    const float g2 = r2 > 0.f ? gc2 : 0.f;
+    const float g0 = rgb.x > 0.f ? gc0 : 0.f;
+    const float g1 = rgb.y > 0.f ? gc1 : 0.f;
+    const float g2 = rgb.z > 0.f ? gc2 : 0.f;
     if (m < nb) {
         float* o = gsh + 3 * m;
         if (a.accumulate) {

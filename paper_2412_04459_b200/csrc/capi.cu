@@ -336,6 +336,7 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     f->n_voxels = scene->n_voxels;
     f->training = opts->training != 0;
     f->has_records = false;
+    f->param_version = scene->param_version;
     f->n_contribs = 0;
     f->il_pending = f->rl_pending = false;  // loss values belong to the previous render
     const uint64_t N = scene->n_voxels;
@@ -924,7 +925,9 @@ void backward_impl(svr_ctx* ctx, const svr_scene* scene, svr_frame* f, const svr
     ea.records = f->records.as<float4>();
     ea.view_dir = f->view_dir.as<float4>();
     ea.corner_index = scene->corner_index.as<uint32_t>();
-    ea.sh = scene->sh.as<float>();
+    // the SH clamp mask from the forward's colours, unless the pools changed
+    // since the forward (then from the coefficients the backward is given)
+    ea.sh = scene->param_version != f->param_version ? scene->sh.as<float>() : nullptr;
     ea.sh_degree = scene->sh_degree;
     ea.sh_stride = scene->sh_stride;
     for (int i = 0; i < 3; ++i) ea.bc[i] = scene->bounds_center[i];
@@ -1269,6 +1272,7 @@ int svr_scene_set_params(svr_ctx* ctx, svr_scene* s, const float* density, const
         if (sh && s->n_voxels)
             SVR_CUDA(cudaMemcpyAsync(s->sh.p, sh, s->n_voxels * s->sh_stride * 4, k, ctx->stream));
         if (!on_device) SVR_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (sh) ++s->param_version;
     });
 }
 

@@ -138,6 +138,7 @@ struct svr_scene {
     svrb::DevBuf morton_rank;   // u32 [8][n]: build_morton_rank (sort keys)
     svrb::DevBuf morton_order;  // u32 [8n]: the (s, vid) pairs in rank order
     bool unordered = false;     // voxels not in spatial order: K1 runs pre-cull + worklist
+    uint64_t param_version = 0; // bumped by svr_scene_set_params
     int rank_bits = 0;          // bit width of 8n-1; 0 = no table
     // AdaptRemap of a scene produced by svr_scene_prune / svr_scene_subdivide
     svrb::DevBuf voxel_src, pool_src;  // int64 per voxel / per pool entry
@@ -157,6 +158,7 @@ struct svr_frame {
     int sort_passes = 0;
     bool training = false;
     bool has_records = false;
+    uint64_t param_version = 0;  // the scene's parameter version when rendered
 
     svrb::DevBuf tile_masks, tile_sat, rects, aabb, records, counts, offsets, visible_rank;
     svrb::DevBuf keys[2], vals[2], dbg_keys, dbg_vals, ranges, tile_order, big;
