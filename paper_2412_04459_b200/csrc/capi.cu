@@ -396,11 +396,28 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     // the ranked path's block prefixes live past the general scan scratch
     uint32_t* pair_partial = reinterpret_cast<uint32_t*>(static_cast<char*>(ctx->scratch.p) +
                                                          ((scan_bytes + 255) & ~size_t(255)));
+    // Huge pairs (>= SVR_HUGE_MIN tiles, default 64) skip duplicate + sort
+    // and are merged into the tile lists by rank (raster.cu: HugePairs), in
+    // production frames, once an earlier frame showed there are some.
+    const char* huge_env = std::getenv("SVR_HUGE_MIN");  // read per frame (parity tests lower it)
+    const uint32_t huge_min = huge_env ? uint32_t(std::strtoul(huge_env, nullptr, 10)) : 64u;
+    HugePairs huge{};
+    huge.min = ranked_ok ? huge_min : 0u;
+    huge.divert = huge.min && !ctx->debug && f->huge_hint > 0 && ntiles <= 4096 &&
+                  packed_keys_enabled() && rank_keys_enabled();
+    if (huge.divert) {
+        uint32_t cap = 4096;
+        while (cap < 2 * f->huge_hint && cap < (1u << 22)) cap <<= 1;
+        huge.cap = cap;
+        huge.keys = grow<uint64_t>(f->huge_keys, 2 * uint64_t(cap));  // + the sort's ping-pong half
+        huge.vals = grow<uint32_t>(f->huge_vals, 2 * uint64_t(cap));
+    }
+    f->huge_used = huge.divert != 0;
     mark(ctx, kStageScan);
     if (ranked_ok) {
         pc = grow<uint32_t>(f->pair_counts, 8 * N);
         launch_pair_counts(cam, N, pa.counts, pa.rects, sat, status, scene->morton_rank.as<uint32_t>(), pc,
-                           st);
+                           st, huge);
         scan_block_prefixes(pc, 8 * N, &status->n_entries, pair_partial, st);
     }
     if (!ranked_ok || ctx->debug)
@@ -424,15 +441,20 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     // switched off reads E back synchronously instead.
     const bool deferred = allow_deferred && ctx->async_frames && !f->training && !ctx->debug &&
                           f->e_cap > 0 && use_rank && packed_keys_enabled();
-    uint64_t E;
+    // E: all entries of the frame (= the capacity in a deferred frame);
+    // E_sort: those the duplicate emits and the sort orders (without the
+    // huge pairs' entries, which the merge places).
+    uint64_t E, E_sort;
     uint32_t pattern_or = 0;
     if (deferred) {
-        E = f->e_cap;
+        E = E_sort = f->e_cap;
     } else {
         launch_status_to_host(status, hs, st);
         SVR_CUDA(cudaStreamSynchronize(st));
-        E = hs->n_entries;
+        E_sort = hs->n_entries;
+        E = E_sort + hs->n_huge_entries;
         pattern_or = hs->pattern_or;
+        f->huge_hint = hs->n_huge_pairs;
         f->n_vis_list = f->training ? hs->n_vis_list : 0;
         require(E < (uint64_t(1) << 30), SVR_ERR_LENGTH, "entry count exceeds 2^30");
         f->e_cap = std::max<uint64_t>(f->e_cap, E + E / 4 + 1024);
@@ -468,6 +490,7 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
         grow<uint64_t>(f->keys[0], E);
         grow<uint64_t>(f->keys[1], E);
         grow<uint32_t>(f->vals[0], E);
+        if (huge.divert) grow<uint32_t>(f->vals[1], E);
         ctx->scratch2.reserve(sort_scratch_bytes(E, np));
         mark(ctx, kStageDuplicate);
         if (!ranked || ctx->debug) {
@@ -489,10 +512,10 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
         // histogram kernel stays.
         const char* fh_env = std::getenv("SVR_FUSED_HIST_MIN");  // parity tests lower it
         const uint64_t fh_min = fh_env ? std::strtoull(fh_env, nullptr, 10) : (uint64_t(1) << 24);
-        const bool fused_hist = ranked && np >= 1 && np <= 2 && E > 1 && E >= fh_min;
+        const bool fused_hist = ranked && np >= 1 && np <= 2 && E_sort > 1 && E_sort >= fh_min;
         TileDigits td{};
         if (fused_hist) {
-            sort_prepare(ctx->scratch2.p, E, np, st);
+            sort_prepare(ctx->scratch2.p, E_sort, np, st);
             td.hist = sort_hist_ptr(ctx->scratch2.p);
             td.b0 = passes[0].bits;
             td.m0 = (1u << passes[0].bits) - 1u;
@@ -501,7 +524,7 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
         }
         if (ranked)
             launch_duplicate_ranked(cam, N, pc, pair_partial, scene->morton_order.as<uint32_t>(), pa.rects,
-                                    masks, sat, rowspan, f->fmt, f->keys[0].as<uint64_t>(), E,
+                                    masks, sat, rowspan, f->fmt, f->keys[0].as<uint64_t>(), E_sort,
                                     grow<uint2>(f->big_pairs, E / kRankedBigMin + 1),
                                     &status->n_big_ranked, st, td);
         mark(ctx, kStageSort);
@@ -509,20 +532,45 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
         // Ranked emission outside debug mode: the last pass writes the values
         // the compositing kernels read, and the ranges come from per-tile
         // counts taken during the histogram read (no sorted keys written).
-        f->sort_keys_kept = !(ranked && !ctx->debug && np > 0 && E > 1);
+        f->sort_keys_kept = !(ranked && !ctx->debug && np > 0 && E_sort > 1) || huge.divert;
         if (!f->sort_keys_kept) {
             SortFinish fin{f->vals[0].as<uint32_t>(), ranges, f->fmt.vb, f->fmt.tile_shift, ntiles};
-            f->sorted_buf = radix_sort_keys(f->keys[0].as<uint64_t>(), f->keys[1].as<uint64_t>(), E, passes,
-                                            np, ctx->scratch2.p, st, fused_hist, n_dev, &fin);
+            f->sorted_buf = radix_sort_keys(f->keys[0].as<uint64_t>(), f->keys[1].as<uint64_t>(), E_sort,
+                                            passes, np, ctx->scratch2.p, st, fused_hist, n_dev, &fin);
             mark(ctx, kStageRanges);
         } else {
-            f->sorted_buf = radix_sort_keys(f->keys[0].as<uint64_t>(), f->keys[1].as<uint64_t>(), E,
+            f->sorted_buf = radix_sort_keys(f->keys[0].as<uint64_t>(), f->keys[1].as<uint64_t>(), E_sort,
                                             passes, np, ctx->scratch2.p, st, fused_hist, n_dev);
             mark(ctx, kStageRanges);
-            launch_tile_ranges_packed(f->keys[f->sorted_buf].as<uint64_t>(), E, f->fmt, ranges,
+            launch_tile_ranges_packed(f->keys[f->sorted_buf].as<uint64_t>(), E_sort, f->fmt,
+                                      huge.divert ? grow<uint2>(f->ranges_small, ntiles) : ranges,
                                       f->vals[0].as<uint32_t>(), ntiles, st, n_dev);
         }
         f->vals_buf = 0;
+        if (huge.divert) {
+            // the huge pairs in rank order, then merged into every tile's list
+            RadixPass hp[kMaxRadixPasses];
+            int nhp = 0;
+            for (int b = 0; b < rb; b += 8) hp[nhp++] = {0, b, std::min(8, rb - b)};
+            f->huge_scratch.reserve(sort_scratch_bytes(huge.cap, nhp));
+            uint64_t* hk = f->huge_keys.as<uint64_t>();
+            uint32_t* hv = f->huge_vals.as<uint32_t>();
+            const int hb = radix_sort_pairs(hk, hv, hk + huge.cap, hv + huge.cap, huge.cap, hp, nhp,
+                                            f->huge_scratch.p, st);
+            // and stably by sign pattern (value bits 29..31) into the other half
+            const RadixPass byp{1, 29, 3};
+            const size_t ho = size_t(hb) * huge.cap, so = size_t(hb ^ 1) * huge.cap;
+            radix_sort_pairs(hk + ho, hv + ho, hk + so, hv + so, huge.cap, &byp, 1, f->huge_scratch.p, st);
+            launch_merge_huge(cam, huge, hk + ho, hv + ho, hk + so, hv + so, status,
+                              pa.rects, masks, f->keys[f->sorted_buf].as<uint64_t>(),
+                              f->ranges_small.as<uint2>(), f->fmt,
+                              grow<int>(f->huge_diff, 8 * uint64_t(cam.ntx + 1) * (cam.nty + 1)),
+                              grow<uint4>(f->huge_pack, 2 * uint64_t(huge.cap) + 4), grow<uint32_t>(f->huge_apos, E),
+                              ranges,
+                              f->vals[1].as<uint32_t>(), E,
+                              grow<unsigned long long>(f->huge_total, 1), st);
+            f->vals_buf = 1;
+        }
     } else {
         for (int b = 0; b < 2; ++b) {
             grow<uint64_t>(f->keys[b], E);
@@ -734,10 +782,12 @@ BufView frame_buffer(svr_frame* f, svr_buffer which) {
         case SVR_BUF_SS_TFIN: return {ss1 ? f->out_tfin.p : f->ss_tfin.p, nss * 4};
         case SVR_BUF_SORT_KEYS:
         case SVR_BUF_SORT_VALUES:
-            if (f->packed && !f->sort_keys_kept) {
+            if (f->packed && (!f->sort_keys_kept || f->huge_used)) {
+                // production frames keep only the sorted values (merged with
+                // the huge pairs' entries when those took the merge path)
                 require(which == SVR_BUF_SORT_VALUES, SVR_ERR_INVALID_ARGUMENT,
                         "sorted key dump needs svr_ctx_set_debug");
-                return {f->vals[0].p, f->n_entries * 4};
+                return {f->vals[f->vals_buf].p, f->n_entries * 4};
             }
             if (f->packed) {
                 uint64_t* k = grow<uint64_t>(f->ref_keys, f->n_entries);
@@ -789,7 +839,8 @@ void resolve_frame(svr_frame* f) {
     if (!f || !f->e_pending) return;
     SVR_CUDA(cudaEventSynchronize(f->done));
     const FrameStatus* hs = static_cast<const FrameStatus*>(f->hstatus.p);
-    const uint64_t E = hs->n_entries;
+    const uint64_t E = hs->n_entries + hs->n_huge_entries;
+    f->huge_hint = hs->n_huge_pairs;
     f->e_pending = false;
     if (E <= f->e_cap) {
         f->n_entries = E;

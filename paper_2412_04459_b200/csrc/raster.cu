@@ -463,8 +463,8 @@ __device__ __forceinline__ uint64_t ranked_key(PackedFormat fmt, uint64_t tid, u
 
 __global__ void __launch_bounds__(256) pair_counts_kernel(
     DevCamera cam, uint64_t n, const uint32_t* __restrict__ counts, const int4* __restrict__ rects,
-    const uint32_t* __restrict__ sat, const FrameStatus* __restrict__ status,
-    const uint32_t* __restrict__ rank, uint32_t* __restrict__ pc) {
+    const uint32_t* __restrict__ sat, FrameStatus* __restrict__ status,
+    const uint32_t* __restrict__ rank, uint32_t* __restrict__ pc, HugePairs huge) {
     pdl_enter();
     const uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (v >= n || counts[v] == 0) return;
@@ -475,8 +475,414 @@ __global__ void __launch_bounds__(256) pair_counts_kernel(
         const uint32_t s = __ffs(pat) - 1;
         pat &= pat - 1;
         const uint32_t c = sat_rect(sat + size_t(1 + s) * ncell, cam.ntx, r.x, r.y, r.z, r.w);
-        if (c) pc[__ldg(rank + s * n + v)] = c;
+        if (!c) continue;
+        const uint32_t rk = __ldg(rank + s * n + v);
+        if (huge.min && c >= huge.min) {
+            const uint32_t slot = atomicAdd(&status->n_huge_pairs, 1u);
+            if (huge.divert && slot < huge.cap) {  // merged per tile later, no entries now
+                huge.keys[slot] = rk;
+                huge.vals[slot] = (s << 29) | uint32_t(v);
+                atomicAdd(&status->n_huge_entries, (unsigned long long)c);
+                continue;
+            }
+        }
+        pc[rk] = c;
     }
+}
+
+// ---- huge pairs: per-tile merge instead of duplicate + sort ----------------
+// (1) every listed pair adds its tile rectangle to a per-pattern 2D
+// difference array; (2) one CTA integrates them, counts per tile the pairs
+// whose pattern the tile holds (exactly the entries the reference emits for
+// them there, raster.cpp:155-170), adds the tile's sorted small entries and
+// scans the totals into the final tile ranges; (3) per tile, the small keys
+// (rank-ordered) and the huge pairs covering the tile (the rank-sorted list,
+// filtered) are merged by rank straight into the final value array.
+__global__ void huge_cover_kernel(DevCamera cam, HugePairs huge, const uint32_t* __restrict__ vals,
+                                  const FrameStatus* __restrict__ status,
+                                  const int4* __restrict__ rects, int* __restrict__ diff) {
+    pdl_enter();
+    const uint32_t nh = min(status->n_huge_pairs, huge.cap);
+    const int sw = cam.ntx + 1, ncell = sw * (cam.nty + 1);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nh; i += gridDim.x * blockDim.x) {
+        const uint32_t pv = vals[i];
+        const int4 r = __ldg(rects + (pv & ((1u << 29) - 1u)));
+        int* d = diff + size_t(pv >> 29) * ncell;
+        atomicAdd(d + r.z * sw + r.x, 1);
+        atomicAdd(d + r.z * sw + r.y + 1, -1);
+        atomicAdd(d + (r.w + 1) * sw + r.x, -1);
+        atomicAdd(d + (r.w + 1) * sw + r.y + 1, 1);
+    }
+}
+
+constexpr int kMergeThreads = 1024;
+__global__ void __launch_bounds__(kMergeThreads) huge_ranges_kernel(
+    DevCamera cam, const FrameStatus* __restrict__ status, const uint8_t* __restrict__ masks,
+    int* __restrict__ diff, const uint2* __restrict__ small_ranges, uint2* __restrict__ ranges,
+    unsigned long long* n_total) {
+    pdl_enter();
+    __shared__ uint32_t s_cnt[4096];
+    __shared__ uint32_t s_warp[kMergeThreads / 32];
+    __shared__ int s_d[4225 + 65];  // one pattern's (ntx+1)(nty+1) difference cells
+    const int ntiles = cam.ntx * cam.nty, sw = cam.ntx + 1, ncell = sw * (cam.nty + 1);
+    for (int t = threadIdx.x; t < ntiles; t += kMergeThreads) s_cnt[t] = 0;
+    const uint32_t pat = status->pattern_or;
+    const bool fits = ncell <= 4225 + 65;
+    for (int s = 0; s < 8; ++s) {
+        if (!((pat >> s) & 1u)) continue;
+        int* d = fits ? s_d : diff + size_t(s) * ncell;  // integrate in shared memory when it fits
+        __syncthreads();
+        if (fits)
+            for (int i = threadIdx.x; i < ncell; i += kMergeThreads) s_d[i] = diff[size_t(s) * ncell + i];
+        __syncthreads();
+        for (int y = threadIdx.x; y <= cam.nty; y += kMergeThreads) {  // rows
+            int run = 0;
+            for (int x = 0; x < sw; ++x) run = (d[y * sw + x] += run);
+        }
+        __syncthreads();
+        for (int x = threadIdx.x; x < sw; x += kMergeThreads) {  // columns
+            int run = 0;
+            for (int y = 0; y <= cam.nty; ++y) run = (d[y * sw + x] += run);
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < ntiles; t += kMergeThreads)
+            if ((masks[t] >> s) & 1u) s_cnt[t] += uint32_t(d[(t / cam.ntx) * sw + t % cam.ntx]);
+    }
+    __syncthreads();
+    // totals per tile, exclusive scan over tiles (4 tiles per thread)
+    uint32_t tot[4], sum = 0;
+    const int t0 = threadIdx.x * 4;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int t = t0 + k;
+        uint32_t c = 0;
+        if (t < ntiles) {
+            const uint2 sr = small_ranges[t];
+            c = s_cnt[t] + (sr.y > sr.x ? sr.y - sr.x : 0u);
+        }
+        tot[k] = c;
+        sum += c;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = s_warp[lane];
+        uint32_t wi = w;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        s_warp[lane] = wi - w;
+    }
+    __syncthreads();
+    uint32_t run = s_warp[warp] + incl - sum;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int t = t0 + k;
+        if (t < ntiles) ranges[t] = make_uint2(run, run + tot[k]);
+        run += tot[k];
+    }
+    if (threadIdx.x == kMergeThreads - 1) *n_total = run;
+}
+
+
+// The huge list packed for the merge: {rank, value, tx0 | tx1 << 16,
+// ty0 | ty1 << 16}, one 16-B load per pair instead of a key, a value and a
+// dependent rectangle gather; twice: in rank order (R) and in (pattern, rank)
+// order (S, whose per-pattern runs [sb[s], sb[8 + s]) serve the tile groups
+// holding a single sign pattern: 3970 of 4096 tiles in config 4, a quarter
+// of the pairs each).
+__global__ void huge_pack_kernel(HugePairs huge, const uint64_t* __restrict__ rkeys,
+                                 const uint32_t* __restrict__ rvals, const uint64_t* __restrict__ skeys_s,
+                                 const uint32_t* __restrict__ svals, const FrameStatus* __restrict__ status,
+                                 const int4* __restrict__ rects, uint4* __restrict__ packed_r,
+                                 uint4* __restrict__ packed_s, uint32_t* __restrict__ sb) {
+    pdl_enter();
+    const uint32_t nh = min(status->n_huge_pairs, huge.cap);
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nh; j += gridDim.x * blockDim.x) {
+        uint32_t pv = rvals[j];
+        int4 r = __ldg(rects + (pv & ((1u << 29) - 1u)));
+        packed_r[j] = make_uint4(uint32_t(rkeys[j]), pv, uint32_t(r.x) | (uint32_t(r.y) << 16),
+                                 uint32_t(r.z) | (uint32_t(r.w) << 16));
+        pv = svals[j];
+        r = __ldg(rects + (pv & ((1u << 29) - 1u)));
+        packed_s[j] = make_uint4(uint32_t(skeys_s[j]), pv, uint32_t(r.x) | (uint32_t(r.y) << 16),
+                                 uint32_t(r.z) | (uint32_t(r.w) << 16));
+        const uint32_t s = pv >> 29;
+        if (j == 0 || (svals[j - 1] >> 29) != s) sb[s] = j;
+        if (j + 1 == nh || (svals[j + 1] >> 29) != s) sb[8 + s] = j + 1;
+    }
+}
+
+// The list tiles [t0, t0 + G) merge from: the pattern's run of S when they
+// all hold one and the same sign pattern, else all of R. Single tiles decide
+// by their own mask (apos below uses that rule, and the group kernel only
+// takes groups whose tiles all hold the same single pattern).
+struct MergeList {
+    const uint4* p;
+    uint32_t lo, hi;
+    bool single;
+};
+__device__ __forceinline__ MergeList merge_list(const DevCamera& cam, int t0, int G, const uint8_t* masks,
+                                                const uint4* packed_r, const uint4* packed_s,
+                                                const uint32_t* sb, uint32_t nh) {
+    const int ntiles = cam.ntx * cam.nty;
+    uint32_t pat = 0;
+    for (int g = 0; g < G; ++g)
+        if (t0 + g < ntiles) pat |= masks[t0 + g];
+    if (__popc(pat) == 1) {
+        const int s = __ffs(pat) - 1;
+        return {packed_s, sb[s], max(sb[s], sb[8 + s]), true};
+    }
+    return {packed_r, 0u, nh, false};
+}
+
+// For every sorted small entry: how many pairs of its tile group's list rank
+// below it (its place in that list), one binary search each.
+__global__ void huge_apos_kernel(DevCamera cam, const uint64_t* __restrict__ skeys,
+                                 const FrameStatus* __restrict__ status, uint64_t cap_small,
+                                 PackedFormat fmt, HugePairs huge, const uint8_t* __restrict__ masks,
+                                 const uint4* __restrict__ packed_r, const uint4* __restrict__ packed_s,
+                                 const uint32_t* __restrict__ sb, uint32_t* __restrict__ apos) {
+    pdl_enter();
+    const uint64_t n = live_entries(cap_small, &status->n_entries);
+    const uint32_t nh = min(status->n_huge_pairs, huge.cap);
+    const uint64_t rmask = (uint64_t(1) << fmt.rank_bits) - 1;
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t k = skeys[e];
+        const uint32_t ra = uint32_t((k >> (fmt.vb + 3)) & rmask);
+        const int tile = int(k >> fmt.tile_shift);
+        const MergeList L = merge_list(cam, tile, 1, masks, packed_r, packed_s, sb, nh);
+        uint32_t lo = L.lo, hi = L.hi;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(&L.p[mid].x) < ra) lo = mid + 1;
+            else hi = mid;
+        }
+        apos[e] = lo - L.lo;
+    }
+}
+
+// One CTA per group of kMergeTiles consecutive tiles sharing one sign
+// pattern (or per single tile otherwise), in steps of kMergeStep listed
+// pairs (kMergeK consecutive per thread; the 16-B records serve all the
+// group's tiles). Per tile: which pairs cover it (rectangle and the tile's
+// sign patterns: exactly the reference's emission rule); block scans give
+// each kept pair the kept pairs before it and the small entries ranked below
+// it (entries marked at their apos; the step's ones cached in shared memory
+// by the tile's warp). Kept pairs and the step's small entries go straight to
+// their merged positions.
+constexpr int kMergeTiles = 8;   // tiles per CTA (one warp each for the small entries)
+constexpr int kMergeK = 8;       // listed pairs per thread per step
+constexpr int kMergeStep = 256 * kMergeK;
+constexpr int kMergeWin = 128;   // small entries cached per tile and step (the rest: global)
+
+template <int G>
+__device__ __forceinline__ void merge_huge_body(
+    int t0, DevCamera cam, HugePairs huge, const uint4* __restrict__ packed_r,
+    const uint4* __restrict__ packed_s, const uint32_t* __restrict__ sb,
+    const FrameStatus* __restrict__ status, const uint8_t* __restrict__ masks,
+    const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ apos,
+    const uint2* __restrict__ small_ranges, PackedFormat fmt, const uint2* __restrict__ ranges,
+    uint32_t* __restrict__ vals, uint64_t cap, const unsigned long long* __restrict__ n_total) {
+    __shared__ uint32_t s_tk[G][256];     // per tile: each thread's kept bits | kept before (in warp) << kMergeK
+    __shared__ uint32_t s_wk[G][8], s_wm[G][8];  // per warp totals, then exclusive prefixes
+    __shared__ uint32_t s_tot[G][2];
+    // small entries ranked just below pair c0 + i, 16-bit counters packed in
+    // pairs (dynamic shared memory; a counter would need 65536 small entries
+    // of one tile ranked between the same two listed pairs to overflow)
+    extern __shared__ uint32_t s_mark32[];
+    uint16_t(*s_mark)[kMergeStep] = reinterpret_cast<uint16_t(*)[kMergeStep]>(s_mark32);
+    __shared__ uint32_t s_mp[G][256];  // marks before each thread's first pair (in its warp)
+    __shared__ uint32_t s_wpos[G][kMergeWin], s_wval[G][kMergeWin];  // the step's small entries
+    __shared__ uint32_t s_run[G], s_ia[G], s_a0[G], s_na[G], s_ob[G], s_nw[G];
+    if (*n_total > cap) return;  // deferred frame that outgrew its buffers: re-rendered
+    const int ntiles = cam.ntx * cam.nty;
+    // groups of kMergeTiles tiles sharing one sign pattern go to the G =
+    // kMergeTiles instance; the tiles of the other groups, one CTA each, to G = 1
+    {
+        const int grp = (t0 / kMergeTiles) * kMergeTiles;
+        const bool uniform = merge_list(cam, grp, kMergeTiles, masks, packed_r, packed_s, sb, 0).single;
+        if (uniform != (G == kMergeTiles)) return;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    auto value_of = [&](uint64_t k) {
+        return (uint32_t((k >> fmt.vb) & 7u) << 29) | uint32_t(k & ((uint64_t(1) << fmt.vb) - 1));
+    };
+    uint32_t txs[G], tys[G], tms[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const int t = t0 + g;
+        const bool live = t < ntiles;
+        txs[g] = live ? uint32_t(t % cam.ntx) : 0xffffu;
+        tys[g] = live ? uint32_t(t / cam.ntx) : 0xffffu;
+        tms[g] = live ? masks[t] : 0u;
+    }
+    if (threadIdx.x < G) {
+        const int t = t0 + threadIdx.x;
+        const uint2 sr = t < ntiles ? small_ranges[t] : make_uint2(0, 0);
+        s_a0[threadIdx.x] = sr.x;
+        s_na[threadIdx.x] = sr.y > sr.x ? sr.y - sr.x : 0u;
+        s_ob[threadIdx.x] = t < ntiles ? ranges[t].x : 0u;
+        s_run[threadIdx.x] = s_ia[threadIdx.x] = 0;
+    }
+    const MergeList L = merge_list(cam, t0, G, masks, packed_r, packed_s, sb,
+                                   min(status->n_huge_pairs, huge.cap));
+    const uint4* __restrict__ packed = L.p + L.lo;
+    const uint32_t nh = L.hi - L.lo;
+    const uint32_t lt = (1u << lane) - 1u;
+    for (uint32_t c0 = 0; c0 < nh; c0 += kMergeStep) {
+        for (int i = threadIdx.x; i < G * kMergeStep / 2; i += 256) s_mark32[i] = 0;
+        // this thread's pairs (thread-contiguous 128 B)
+        uint4 rec[kMergeK];
+#pragma unroll
+        for (int k = 0; k < kMergeK; ++k) {
+            const uint32_t j = c0 + threadIdx.x * kMergeK + k;
+            rec[k] = j < nh ? __ldg(packed + j) : make_uint4(0, 0, 0xffffu, 0xffffu);
+        }
+        __syncthreads();
+        // warp w: tile w's small entries ranked inside this step, marked and cached
+        if (warp < G) {
+            const uint32_t ia = s_ia[warp], na = s_na[warp], a0 = s_a0[warp];
+            uint32_t nw = 0;
+            for (uint32_t i0 = ia; i0 < na; i0 += 32) {
+                const uint32_t i = i0 + lane;
+                const uint32_t p = i < na ? apos[a0 + i] : 0xffffffffu;
+                const bool in = p < c0 + kMergeStep;
+                const uint32_t bin = __ballot_sync(0xffffffffu, in);
+                if (in) {
+                    const uint32_t q = warp * kMergeStep + (p - c0);
+                    atomicAdd(s_mark32 + (q >> 1), 1u << (16 * (q & 1)));
+                    const uint32_t at = nw + __popc(bin & lt);
+                    if (at < kMergeWin) {
+                        s_wpos[warp][at] = p - c0;
+                        s_wval[warp][at] = value_of(skeys[a0 + i]);
+                    }
+                }
+                nw += __popc(bin);
+                if (bin != 0xffffffffu) break;  // apos is nondecreasing: the rest lie later
+            }
+            if (lane == 0) s_nw[warp] = nw;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            uint32_t keep = 0, m = 0;
+#pragma unroll
+            for (int k = 0; k < kMergeK; ++k) {
+                const uint32_t rx0 = rec[k].z & 0xffffu, rx1 = rec[k].z >> 16;
+                const uint32_t ry0 = rec[k].w & 0xffffu, ry1 = rec[k].w >> 16;
+                const bool in = txs[g] >= rx0 && txs[g] <= rx1 && tys[g] >= ry0 && tys[g] <= ry1 &&
+                                ((tms[g] >> (rec[k].y >> 29)) & 1u) &&
+                                c0 + threadIdx.x * kMergeK + k < nh;
+                keep |= uint32_t(in) << k;
+                m += s_mark[g][threadIdx.x * kMergeK + k];
+            }
+            uint32_t ik = __popc(keep), im = m;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t yk = __shfl_up_sync(0xffffffffu, ik, o);
+                const uint32_t ym = __shfl_up_sync(0xffffffffu, im, o);
+                if (lane >= o) {
+                    ik += yk;
+                    im += ym;
+                }
+            }
+            // in-warp exclusive kept count above the kept bits
+            s_tk[g][threadIdx.x] = keep | ((ik - __popc(keep)) << kMergeK);
+            if (lane == 31) {
+                s_wk[g][warp] = ik;
+                s_wm[g][warp] = im;
+            }
+            s_mp[g][threadIdx.x] = im - m;  // marks before this thread's pairs (in its warp)
+        }
+        __syncthreads();
+        if (threadIdx.x < 2 * G) {  // cross-warp exclusive prefixes: kept (tid < G), marks (tid >= G)
+            const int g = threadIdx.x % G;
+            uint32_t* w = threadIdx.x < G ? s_wk[g] : s_wm[g];
+            uint32_t run = 0;
+            for (int q = 0; q < 8; ++q) {
+                const uint32_t c = w[q];
+                w[q] = run;
+                run += c;
+            }
+            s_tot[g][threadIdx.x < G ? 0 : 1] = run;
+        }
+        __syncthreads();
+        // kept pairs: merged position = kept before + small entries ranked below
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const uint32_t tk = s_tk[g][threadIdx.x];
+            uint32_t kb = s_run[g] + s_wk[g][warp] + (tk >> kMergeK);
+            uint32_t ab = s_ia[g] + s_wm[g][warp] + s_mp[g][threadIdx.x];
+#pragma unroll
+            for (int k = 0; k < kMergeK; ++k) {
+                ab += s_mark[g][threadIdx.x * kMergeK + k];  // entries ranked below this pair
+                if ((tk >> k) & 1u) vals[s_ob[g] + kb++ + ab] = rec[k].y;
+            }
+        }
+        // the step's small entries (warp w, tile w): after the kept pairs ranked below
+        if (warp < G) {
+            const uint32_t nw = s_nw[warp];
+            for (uint32_t q = lane; q < nw; q += 32) {
+                uint32_t pl, v;
+                if (q < kMergeWin) {
+                    pl = s_wpos[warp][q];
+                    v = s_wval[warp][q];
+                } else {  // more than the cache holds: straight from global memory
+                    const uint32_t i = s_ia[warp] + q;
+                    pl = apos[s_a0[warp] + i] - c0;
+                    v = value_of(skeys[s_a0[warp] + i]);
+                }
+                const uint32_t th = pl / kMergeK, tw = th >> 5;
+                uint32_t kept_before = s_run[warp];
+                if (th < 256) {
+                    const uint32_t tk = s_tk[warp][th];
+                    kept_before += s_wk[warp][tw] + (tk >> kMergeK) +
+                                   __popc(tk & ((1u << (pl % kMergeK)) - 1u));
+                } else {
+                    kept_before += s_tot[warp][0];
+                }
+                vals[s_ob[warp] + s_ia[warp] + q + kept_before] = v;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < G) {
+            s_run[threadIdx.x] += s_tot[threadIdx.x][0];
+            s_ia[threadIdx.x] += s_nw[threadIdx.x];
+        }
+    }
+    __syncthreads();
+    for (int g = 0; g < G; ++g)
+        for (uint32_t i = s_ia[g] + threadIdx.x; i < s_na[g]; i += 256)
+            vals[s_ob[g] + i + s_run[g]] = value_of(skeys[s_a0[g] + i]);
+}
+
+// CTAs [0, ntiles): single tiles of the groups without a uniform sign pattern
+// (they merge from the longer lists: scheduled first); then one CTA per group.
+__global__ void __launch_bounds__(256) merge_huge_kernel(
+    DevCamera cam, HugePairs huge, const uint4* __restrict__ packed_r,
+    const uint4* __restrict__ packed_s, const uint32_t* __restrict__ sb,
+    const FrameStatus* __restrict__ status, const uint8_t* __restrict__ masks,
+    const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ apos,
+    const uint2* __restrict__ small_ranges, PackedFormat fmt, const uint2* __restrict__ ranges,
+    uint32_t* __restrict__ vals, uint64_t cap, const unsigned long long* __restrict__ n_total) {
+    pdl_enter();
+    const int ntiles = cam.ntx * cam.nty;
+    if (int(blockIdx.x) < ntiles)
+        merge_huge_body<1>(int(blockIdx.x), cam, huge, packed_r, packed_s, sb, status, masks, skeys, apos,
+                           small_ranges, fmt, ranges, vals, cap, n_total);
+    else
+        merge_huge_body<kMergeTiles>((int(blockIdx.x) - ntiles) * kMergeTiles, cam, huge, packed_r, packed_s,
+                                     sb, status, masks, skeys, apos, small_ranges, fmt, ranges, vals, cap,
+                                     n_total);
 }
 
 __global__ void __launch_bounds__(kScanThreads) duplicate_ranked_kernel(
@@ -1552,7 +1958,7 @@ __global__ void status_to_host_kernel(const FrameStatus* d, FrameStatus* h, uint
                                       unsigned int* overflow_count) {
     pdl_enter();
     *h = *d;
-    if (overflow_count && d->n_entries > cap) atomicAdd(overflow_count, 1u);
+    if (overflow_count && d->n_entries + d->n_huge_entries > cap) atomicAdd(overflow_count, 1u);
 }
 
 inline unsigned blocks_for(uint64_t n, int threads) { return unsigned((n + threads - 1) / threads); }
@@ -1641,13 +2047,55 @@ void launch_duplicate_packed(const DevCamera& cam, uint64_t n, const uint64_t* p
 }
 
 void launch_pair_counts(const DevCamera& cam, uint64_t n, const uint32_t* counts, const int4* rects,
-                        const uint32_t* sat, const FrameStatus* status, const uint32_t* rank,
-                        uint32_t* pc, cudaStream_t st) {
+                        const uint32_t* sat, FrameStatus* status, const uint32_t* rank,
+                        uint32_t* pc, cudaStream_t st, const HugePairs& huge) {
     if (n == 0) return;
     SVR_CUDA(cudaMemsetAsync(pc, 0, 8 * n * sizeof(uint32_t), st));
+    if (huge.divert && huge.cap) {  // padding sorts last by rank and by pattern
+        SVR_CUDA(cudaMemsetAsync(huge.keys, 0xff, size_t(huge.cap) * 8, st));
+        SVR_CUDA(cudaMemsetAsync(huge.vals, 0xff, size_t(huge.cap) * 4, st));
+    }
     launch_pdl(pair_counts_kernel, blocks_for(n, 256), 256, 0, st, cam, n, counts, rects, sat, status, rank,
-               pc);
+               pc, huge);
     SVR_LAUNCH("pair_counts_kernel");
+}
+
+void launch_merge_huge(const DevCamera& cam, const HugePairs& huge, const uint64_t* hkeys,
+                       const uint32_t* hvals, const uint64_t* skeys_s, const uint32_t* svals_s,
+                       const FrameStatus* status, const int4* rects,
+                       const uint8_t* masks, const uint64_t* small_keys, const uint2* small_ranges,
+                       PackedFormat fmt, int* diff, uint4* packed, uint32_t* apos, uint2* ranges,
+                       uint32_t* vals, uint64_t cap, unsigned long long* n_total, cudaStream_t st) {
+    const int ntiles = cam.ntx * cam.nty;
+    if (ntiles > 4096) throw Error(SVR_ERR_RUNTIME, "huge-pair merge supports at most 4096 tiles");
+    const size_t ncell = size_t(cam.ntx + 1) * (cam.nty + 1);
+    SVR_CUDA(cudaMemsetAsync(diff, 0, 8 * ncell * sizeof(int), st));
+    launch_pdl(huge_cover_kernel, std::max(1u, blocks_for(huge.cap, 256)), 256, 0, st, cam, huge, hvals,
+               status, rects, diff);
+    SVR_LAUNCH("huge_cover_kernel");
+    launch_pdl(huge_ranges_kernel, 1, kMergeThreads, 0, st, cam, status, masks, diff, small_ranges, ranges,
+               n_total);
+    SVR_LAUNCH("huge_ranges_kernel");
+    uint4* packed_s = packed + huge.cap;
+    uint32_t* sb = reinterpret_cast<uint32_t*>(packed_s + huge.cap);
+    SVR_CUDA(cudaMemsetAsync(sb, 0, 16 * sizeof(uint32_t), st));
+    launch_pdl(huge_pack_kernel, std::max(1u, blocks_for(huge.cap, 256)), 256, 0, st, huge, hkeys, hvals,
+               skeys_s, svals_s, status, rects, packed, packed_s, sb);
+    SVR_LAUNCH("huge_pack_kernel");
+    launch_pdl(huge_apos_kernel, 148u * 8u, 256, 0, st, cam, small_keys, status, cap, fmt, huge, masks,
+               const_cast<const uint4*>(packed), const_cast<const uint4*>(packed_s),
+               const_cast<const uint32_t*>(sb), apos);
+    SVR_LAUNCH("huge_apos_kernel");
+    constexpr size_t kMergeDyn = size_t(kMergeTiles) * kMergeStep * 2;
+    static std::atomic<uint64_t> attr_set{0};
+    if (first_on_device(attr_set))
+        SVR_CUDA(cudaFuncSetAttribute(merge_huge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(kMergeDyn)));
+    launch_pdl(merge_huge_kernel, unsigned(ntiles + (ntiles + kMergeTiles - 1) / kMergeTiles), 256, kMergeDyn,
+               st, cam, huge, const_cast<const uint4*>(packed), const_cast<const uint4*>(packed_s),
+               const_cast<const uint32_t*>(sb), status, masks, small_keys, const_cast<const uint32_t*>(apos),
+               small_ranges, fmt, ranges, vals, cap, n_total);
+    SVR_LAUNCH("merge_huge_kernel");
 }
 
 void launch_duplicate_ranked(const DevCamera& cam, uint64_t n, const uint32_t* pc,

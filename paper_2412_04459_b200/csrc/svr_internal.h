@@ -159,6 +159,12 @@ struct svr_frame {
     bool training = false;
     bool has_records = false;
     uint64_t param_version = 0;  // the scene's parameter version when rendered
+    // huge-pair merge (raster.cu: HugePairs): last frame's count of huge pairs
+    // (the hint that turns the merge on) and its buffers
+    uint32_t huge_hint = 0;
+    bool huge_used = false;
+    svrb::DevBuf huge_keys, huge_vals, huge_scratch, huge_diff, huge_total, huge_pack, huge_apos,
+        ranges_small;
 
     svrb::DevBuf tile_masks, tile_sat, rects, aabb, records, counts, offsets, visible_rank;
     svrb::DevBuf keys[2], vals[2], dbg_keys, dbg_vals, ranges, tile_order, big;

@@ -75,6 +75,23 @@ struct FrameStatus {          // device -> host summary, one read per frame
     unsigned int n_work;        // K1 worklist length (pre-cull pass)
     unsigned int n_vis_list;    // K1's list of visible voxels (training frames)
     unsigned long long n_entries_voxel;  // E from the per-voxel scan (parity dumps of the ranked path)
+    unsigned int n_huge_pairs;           // pairs with >= HugePairs::min entries (all of them counted)
+    unsigned long long n_huge_entries;   // entries of the pairs diverted to the per-tile merge
+};
+
+// Huge (sign pattern, voxel) pairs — a large voxel near a camera inside the
+// scene covers hundreds of tiles (config 4: 22K voxels hold 91M of 94M
+// entries). With `divert`, pair_counts lists them (rank, value) instead of
+// giving them entries to duplicate and sort; after the sort of the other
+// entries, merge_huge_kernel interleaves them into every tile's list in rank
+// order, producing exactly the sorted values and tile ranges the full sort
+// would (raster.cpp:144-178, 238-245).
+struct HugePairs {
+    uint32_t min;       // entry count from which a pair is huge (0: off)
+    int divert;         // list them (else only count them: the next frame's hint)
+    uint32_t cap;       // list capacity; pairs past it take the ordinary path
+    uint64_t* keys;     // [cap] rank, UINT64_MAX padding
+    uint32_t* vals;     // [cap] s << 29 | vid
 };
 
 // With rowspan (int2 [8][nty]): also the eight per-sign-pattern SATs at
@@ -147,8 +164,21 @@ void build_morton_rank(const uint64_t* paths, uint64_t n, int lmax, uint32_t* ra
 // sorted below the tile bits. big: E / 128 + 1 uint2 (pairs with more than
 // 128 entries, emitted cooperatively).
 void launch_pair_counts(const DevCamera& cam, uint64_t n, const uint32_t* counts, const int4* rects,
-                        const uint32_t* sat, const FrameStatus* status, const uint32_t* rank,
-                        uint32_t* pc, cudaStream_t st);
+                        const uint32_t* sat, FrameStatus* status, const uint32_t* rank,
+                        uint32_t* pc, cudaStream_t st, const HugePairs& huge);
+// The huge-pair merge: tile coverage counts of the (rank-sorted) huge list
+// and the final tile ranges (small + huge per tile, scanned), then per tile
+// the rank-order merge of its small sorted keys with the huge pairs covering
+// it into `vals`. diff: int [8][(ntx+1)(nty+1)] scratch; n_total: E.
+// huge_*_sorted: the list in rank order; *_s: the same in (pattern, rank)
+// order; packed: 2 * cap uint4 + 16 words.
+void launch_merge_huge(const DevCamera& cam, const HugePairs& huge, const uint64_t* huge_keys_sorted,
+                       const uint32_t* huge_vals_sorted, const uint64_t* skeys_s, const uint32_t* svals_s,
+                       const FrameStatus* status,
+                       const int4* rects, const uint8_t* masks, const uint64_t* small_keys,
+                       const uint2* small_ranges, PackedFormat fmt, int* diff, uint4* packed,
+                       uint32_t* apos, uint2* ranges, uint32_t* vals, uint64_t cap,
+                       unsigned long long* n_total, cudaStream_t st);
 #ifndef SVR_RBIG
 #define SVR_RBIG 128
 #endif

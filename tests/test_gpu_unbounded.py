@@ -73,3 +73,37 @@ def test_cfg4_full_view_order_properties(svr, ctx, cfg4):
     assert r[0, 0] == 0 and r[-1, 1] == E and np.array_equal(r[1:, 0], r[:-1, 1])
     tiles = (k[r[:, 0]] >> np.uint64(48)).astype(np.int64)
     assert np.array_equal(np.flatnonzero(ne)[np.argsort(ranges[ne, 0])], tiles)
+
+
+@pytest.mark.parametrize("huge_min", ["2", "9", "40"])
+def test_huge_pair_merge_matches_full_sort(svr, ref, monkeypatch, huge_min):
+    """The huge-pair merge (production frames: pairs covering >= SVR_HUGE_MIN
+    tiles are merged into the tile lists by rank instead of duplicated and
+    sorted) yields exactly the reference's sorted values and tile ranges, and
+    images identical to the unmerged path, on a camera inside a small scene
+    (thresholds lowered so most pairs take the merge)."""
+    import numpy as np
+    arrays = svr.synth_random_scene(77, 512 + 7 * 300, 8, 2)
+    rscene = ref.RefScene.from_arrays(arrays)
+    cam = svr.Camera(160, 112, 60.0, 60.0, 79.3, 55.7, np.eye(3), np.array([0.01, -0.02, -0.03]))
+    opts = svr.RenderOptions(supersample=1.0)
+    ks, vs = ref.ref_entries(rscene, cam, sorted_=True)
+    monkeypatch.setenv("SVR_HUGE_MIN", "0")
+    plain = svr.Context(0)
+    base = svr.render(svr.Scene(plain, arrays), cam, opts)
+    monkeypatch.setenv("SVR_HUGE_MIN", huge_min)
+    ctx = svr.Context(0)
+    scene = svr.Scene(ctx, arrays)
+    f = svr.Frame(ctx)
+    for _ in range(2):  # the first frame counts the huge pairs, the second merges them
+        out = svr.render(scene, cam, opts, frame=f)
+    assert f.info().n_entries == ks.size
+    assert np.array_equal(f.download("SORT_VALUES", np.uint32), vs)
+    ranges = f.download("TILE_RANGES", np.uint32, (-1, 2))
+    tiles = (ks >> np.uint64(48)).astype(np.int64)
+    t = np.arange(ranges.shape[0])
+    lo, hi = np.searchsorted(tiles, t, "left"), np.searchsorted(tiles, t, "right")
+    ne = hi > lo
+    assert np.array_equal(ranges[ne, 0], lo[ne]) and np.array_equal(ranges[ne, 1], hi[ne])
+    for name in ("color", "depth", "median_depth", "normal", "transmittance"):
+        assert np.array_equal(getattr(out, name), getattr(base, name)), name
