@@ -1229,6 +1229,34 @@ __device__ __forceinline__ void cp_async_wait() {
 // the sign of the inverse direction (n = 1 where it is negative): fma(w, 1, lo)
 // rounds exactly like lo + w and fma(w, 0, lo) = lo, so ta/tb are the same
 // floats as the min/max form below, three instructions cheaper.
+// TMA bulk copies (cp.async.bulk, completion counted on an mbarrier): the
+// SVR_BULK=1 variant of the warp path stages each surviving 96-B record with
+// ONE bulk copy instead of six 16-B cp.async (measured slower).
+#ifndef SVR_BULK
+#define SVR_BULK 0
+#endif
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
 struct SlabSel {
     float nx, ny, nz;  // 1 where the inverse direction component is negative
 };
@@ -1288,6 +1316,7 @@ struct CompShared {
         } c;
     };
     float cone[kCompWarps][4][3];
+    uint64_t mbar[SVR_BULK ? kCompWarps : 1][2];  // SVR_BULK: per warp and record buffer
     // pixel centres for phase B (one LDS instead of a per-hit rematerialised
     // copy); the entry-recording modes need the space for c.ent instead
     float2 pc[ENTRY ? 1 : 256];
@@ -1330,6 +1359,16 @@ __device__ __forceinline__ void composite_tile_warp(const DevCamera& cam, const 
     // (raster.cpp:95-101), without changing the composited set.
     float (*cone)[3] = s_cone[warp];
     if (lane == 0) warp_cone_planes(cam, wx0, wy0, cone);
+#if SVR_BULK
+    uint64_t* mbar = sh.mbar[SVR_BULK ? warp : 0];
+    if (lane == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    unsigned phase = 0;  // bit b: parity of buffer b's next completion
+    unsigned pend = 0;   // bit b: buffer b has copies in flight
+#endif
     __syncwarp();
 
     float T = 1.0f, cr = 0.f, cg = 0.f, cb = 0.f, nx = 0.f, ny = 0.f, nz = 0.f, depth = 0.f;
@@ -1364,12 +1403,19 @@ __device__ __forceinline__ void composite_tile_warp(const DevCamera& cam, const 
             s_j[buf][warp][at] = uint8_t(lane);
         }
         float4(*wrec)[kRecordF4] = buf ? wrec1 : wrec0;
+#if SVR_BULK
+        if (lane == 0) mbar_arrive_expect(&mbar[buf], unsigned(__popc(m)) * kRecordF4 * 16u);
+        if (rel) bulk_g2s(&wrec[at][0], a.records + uint64_t(v & kVidMask) * kRecordF4, kRecordF4 * 16u,
+                          &mbar[buf]);
+        pend |= 1u << buf;
+#else
         if (rel) {  // the lane of each surviving entry copies its record
             const float4* src = a.records + uint64_t(v & kVidMask) * kRecordF4;
 #pragma unroll
             for (int k = 0; k < kRecordF4; ++k) cp_async16(&wrec[at][k], src + k);
         }
         cp_async_commit();
+#endif
         return m;
     };
 
@@ -1398,12 +1444,19 @@ __device__ __forceinline__ void composite_tile_warp(const DevCamera& cam, const 
         if (c + 96 + lane < range.y) v3 = __ldg(a.vals + c + 96 + lane);
         // stage chunk c+1 into the other buffer, then wait for chunk c
         uint32_t m_next = 0;
+#if SVR_BULK
+        if (c + 32 < range.y) m_next = stage(c + 32, v1, b1, buf ^ 1);
+        mbar_wait(&mbar[buf], (phase >> buf) & 1u);  // chunk c's records landed
+        phase ^= 1u << buf;
+        pend &= ~(1u << buf);
+#else
         if (c + 32 < range.y) {
             m_next = stage(c + 32, v1, b1, buf ^ 1);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
         }
+#endif
         __syncwarp();
 
         const int nrel = __popc(m_cur);
@@ -1510,7 +1563,12 @@ __device__ __forceinline__ void composite_tile_warp(const DevCamera& cam, const 
         b1 = b2;
         v2 = v3;
     }
+#if SVR_BULK
+    for (int bb = 0; bb < 2; ++bb)  // no copy may outlive the CTA's shared memory
+        if ((pend >> bb) & 1u) mbar_wait(&mbar[bb], (phase >> bb) & 1u);
+#else
     cp_async_wait<0>();  // no copy may outlive the CTA's shared memory
+#endif
     if (RECORD || !inside) return;
     // CompositeCtx::finish (raster.cpp:56-60)
     cr += T * a.bg[0];
