@@ -396,11 +396,15 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     // the ranked path's block prefixes live past the general scan scratch
     uint32_t* pair_partial = reinterpret_cast<uint32_t*>(static_cast<char*>(ctx->scratch.p) +
                                                          ((scan_bytes + 255) & ~size_t(255)));
-    // Huge pairs (>= SVR_HUGE_MIN tiles, default 64) skip duplicate + sort
-    // and are merged into the tile lists by rank (raster.cu: HugePairs), in
-    // production frames, once an earlier frame showed there are some.
-    const char* huge_env = std::getenv("SVR_HUGE_MIN");  // read per frame (parity tests lower it)
-    const uint32_t huge_min = huge_env ? uint32_t(std::strtoul(huge_env, nullptr, 10)) : 64u;
+    // Huge pairs (>= SVR_HUGE_MIN tiles) skip duplicate + sort and are merged
+    // into the tile lists by rank (raster.cu: HugePairs), in production
+    // frames, once an earlier frame showed there are some. Off by default:
+    // config-4 view 0 gains (4.63 -> 4.01 ms) but over the bench's 30 views
+    // the merge's long-pole tiles cost more than the sort it replaces
+    // (4.97 -> 5.64 ms), and config 2 pays its fixed cost (+0.19 ms); see
+    // DESIGN.md §8.
+    const char* huge_env = std::getenv("SVR_HUGE_MIN");  // read per frame (parity tests set it)
+    const uint32_t huge_min = huge_env ? uint32_t(std::strtoul(huge_env, nullptr, 10)) : 0u;
     HugePairs huge{};
     huge.min = ranked_ok ? huge_min : 0u;
     huge.divert = huge.min && !ctx->debug && f->huge_hint > 0 && ntiles <= 4096 &&

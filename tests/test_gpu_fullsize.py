@@ -138,10 +138,12 @@ def cfg4(svr, ref):
     return _CFG4["a"]
 
 
-def test_cfg4_entries_bit_exact_full_view(svr, ref, cfg4):
+def test_cfg4_entries_bit_exact_full_view(svr, ref, cfg4, monkeypatch):
     """View 0 of the bench's 256-view ring at 1024^2: every emitted entry in
     the reference's emission order and the sorted list, bit for bit; then
-    the production context's value-only sort output and tile ranges."""
+    the production context's sorted values and tile ranges, through the
+    sort of all entries and through the huge-pair merge (SVR_HUGE_MIN=64:
+    ~91M of the ~94M entries belong to pairs covering >= 64 tiles)."""
     arrays, rscene = cfg4
     cam = svr.ring_camera(256, 0, 1024, 1024, 1.0)
     ek, ev, sk, sv = ref.ref_entries_both(rscene, cam)
@@ -156,19 +158,25 @@ def test_cfg4_entries_bit_exact_full_view(svr, ref, cfg4):
     assert np.array_equal(f.download("SORT_KEYS", np.uint64), sk)
     assert np.array_equal(f.download("SORT_VALUES", np.uint32), sv)
     del f, scene, dctx, ek, ev
-    pctx = svr.Context(0)
-    pctx.set_async(True)
-    pscene = svr.Scene(pctx, arrays)
-    pf = svr.Frame(pctx)
-    svr.render_into(pf, pscene, svr.ring_camera(256, 1, 1024, 1024, 1.0), svr.RenderOptions(supersample=1.0))
-    svr.render_into(pf, pscene, cam, svr.RenderOptions(supersample=1.0))  # deferred
-    assert np.array_equal(pf.download("SORT_VALUES", np.uint32), sv)
-    ranges = pf.download("TILE_RANGES", np.uint32, (-1, 2))
     tiles = (sk >> np.uint64(48)).astype(np.int64)
-    t = np.arange(ranges.shape[0])
-    lo, hi = np.searchsorted(tiles, t, "left"), np.searchsorted(tiles, t, "right")
-    ne = hi > lo
-    assert np.array_equal(ranges[ne, 0], lo[ne]) and np.array_equal(ranges[ne, 1], hi[ne])
+    del sk
+    for huge in ("0", "64"):
+        monkeypatch.setenv("SVR_HUGE_MIN", huge)
+        pctx = svr.Context(0)
+        pctx.set_async(True)
+        pscene = svr.Scene(pctx, arrays)
+        pf = svr.Frame(pctx)
+        svr.render_into(pf, pscene, svr.ring_camera(256, 1, 1024, 1024, 1.0), svr.RenderOptions(supersample=1.0))
+        pf.info()
+        svr.render_into(pf, pscene, cam, svr.RenderOptions(supersample=1.0))  # deferred
+        assert pf.info().n_entries == sv.size, huge
+        assert np.array_equal(pf.download("SORT_VALUES", np.uint32), sv), huge
+        ranges = pf.download("TILE_RANGES", np.uint32, (-1, 2))
+        t = np.arange(ranges.shape[0])
+        lo, hi = np.searchsorted(tiles, t, "left"), np.searchsorted(tiles, t, "right")
+        ne = hi > lo
+        assert np.array_equal(ranges[ne, 0], lo[ne]) and np.array_equal(ranges[ne, 1], hi[ne]), huge
+        del pf, pscene, pctx
 
 
 @pytest.mark.parametrize("y0", [480, 960])

@@ -15,7 +15,7 @@ n = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 ctx = svr.Context(0)
 if wl == "cfg4":
     a = svr.synth_unbounded_scene([svr.ring_camera(8, i, 1024, 1024) for i in range(8)], 7, 5, 2.8, seed=7)
-    cams = [svr.ring_camera(256, v, 1024, 1024, 1.0) for v in range(4)]
+    cams = [svr.ring_camera(256, v, 1024, 1024, 1.0) for v in range(int(os.environ.get("AB_VIEWS", "4")))]
 else:
     a = svr.synth_random_scene(7, 1 << 20, 9, 3)
     res = 800 if wl == "cfg3" else 1024
@@ -46,6 +46,12 @@ else:
 for c in cams:
     step(c)
 ctx.synchronize()
+if os.environ.get("AB_ASYNC") == "1" and not train:  # deferred-E frames, as bench.py's render loop
+    ctx.set_async(True)
+    for c in cams:
+        step(c)
+        f.info()
+    ctx.synchronize()
 ctx.enable_timing(True)
 ctx.stage_times(reset=True)
 t = time.time()
