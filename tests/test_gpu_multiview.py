@@ -91,9 +91,10 @@ def test_two_rank_allreduce_matches_single_process_and_reference(svr, ref, tmp_p
         for label, ours in [("2-rank", red[name]), ("1-rank", g1[name])]:
             nbad, worst = grad_close(ours, theirs)
             assert nbad == 0, f"{label} {name}: {nbad} out of tolerance (worst {worst:.3e})"
-        # the two ranks' partial sums differ from one accumulation only by
-        # fp32 reassociation (cancelling sums keep it from being tighter)
-        nbad, _ = grad_close(red[name], g1[name], rel=1e-4)
+        # the two ranks' partial sums differ from one accumulation only by fp32
+        # reassociation (and float atomics are order-nondeterministic run to
+        # run), so they agree by the same rule
+        nbad, _ = grad_close(red[name], g1[name])
         assert nbad == 0, name
     assert np.abs(red["density"]).max() > 0
 
