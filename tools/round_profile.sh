@@ -24,4 +24,18 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"epi
     -s 12 -c 4 -o gpurun_out/bwd python tools/ab_stage.py cfg3 2 > gpurun_out/ncu_bwd.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"composite|onesweep|preprocess|duplicate_|merge_huge|pair_counts" \
     -s 20 -c 12 -o gpurun_out/cfg4 python tools/ab_stage.py cfg4 2 > gpurun_out/ncu_cfg4.log 2>&1
-ls -la gpurun_out
+# summarise on the box (the reports themselves exceed gpurun's 64 MiB return)
+mkdir -p gpurun_out/prof
+PROF_DIR=gpurun_out/prof python tools/summarize_ncu.py ${TAG:-r02} > gpurun_out/prof/summary.log 2>&1
+python tools/hotspots.py gpurun_out/full.ncu-rep "composite_kernel" 40 > gpurun_out/prof/hotspots_composite_cfg2.md 2>&1
+python tools/hotspots.py gpurun_out/cfg4.ncu-rep "composite_coop" 40 > gpurun_out/prof/hotspots_composite_cfg4.md 2>&1
+python tools/hotspots.py gpurun_out/bwd.ncu-rep "composite_backward" 30 > gpurun_out/prof/hotspots_backward_cfg3.md 2>&1
+for k in composite_kernel composite_coop_kernel; do
+  for r in full cfg4; do python tools/sass_histogram.py --ncu gpurun_out/$r.ncu-rep $k >> gpurun_out/prof/sass_exec_$r.md 2>&1; done
+done
+python tools/ncu_regions.py gpurun_out/full.ncu-rep composite_kernel "{'phaseA':('raster.cu',0,0)}" > /dev/null 2>&1
+for r in full bwd cfg4; do xz -T0 -9 -c gpurun_out/$r.ncu-rep > gpurun_out/prof/$r.ncu-rep.xz 2>/dev/null; done
+du -sh gpurun_out/prof/*.xz
+rm -f gpurun_out/*.ncu-rep
+while [ "$(du -sm gpurun_out | cut -f1)" -gt 56 ]; do rm -f "$(ls -S gpurun_out/prof/*.xz | head -1)"; done
+du -sh gpurun_out; ls -la gpurun_out gpurun_out/prof

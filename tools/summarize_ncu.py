@@ -13,7 +13,7 @@ from collections import defaultdict
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
-prof = os.path.join(ROOT, "profiles")
+prof = os.environ.get("PROF_DIR", os.path.join(ROOT, "profiles"))
 os.makedirs(prof, exist_ok=True)
 
 
@@ -118,5 +118,7 @@ capture("bwd.ncu-rep", "config-3 training step kernels (tools/explore_cfg3.py)",
 capture("cfg4.ncu-rep", "config-4 view 0 (tools/explore_cfg4.py)", "cfg4", traffic)
 if "cfg4" in traffic:
     traffic["cfg5"] = dict(traffic["cfg4"])  # same scene and views; backward from cfg3's kernel shape
+if "cfg3" in traffic:
+    traffic["cfg3i"] = dict(traffic["cfg3"])  # the same view and backward inside the full iteration
 if traffic:
     json.dump(traffic, open(os.path.join(prof, "ncu_traffic.json"), "w"), indent=1)
