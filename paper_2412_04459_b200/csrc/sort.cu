@@ -106,6 +106,24 @@ __global__ void __launch_bounds__(kRadix) bin_scan_kernel(uint32_t* hist) {
     h[threadIdx.x] = s[threadIdx.x] - v;
 }
 
+// Lanes holding the same digit (di < 2^bits, or kRadix for an empty slot).
+// BALLOT: one ballot per digit bit instead of match.any — faster in the
+// large-sort instantiation (16 keys per thread; config 4 sort 1.51 -> 1.38
+// ms), slower at config-2 sizes (0.054 -> 0.067 ms), so only there.
+template <bool BALLOT>
+__device__ __forceinline__ uint32_t digit_peers(uint32_t di, int bits) {
+    if (!BALLOT) return __match_any_sync(0xffffffffu, di);
+    uint32_t peers = 0xffffffffu;
+    for (int b = 0; b < bits; ++b) {
+        const bool on = (di >> b) & 1u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, on);
+        peers &= on ? bal : ~bal;
+    }
+    const bool empty = di >= uint32_t(kRadix);
+    const uint32_t bal = __ballot_sync(0xffffffffu, empty);
+    return peers & (empty ? bal : ~bal);
+}
+
 __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
@@ -164,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
 #pragma unroll
     for (int i = 0; i < Part<PAIRS, IK>::items; ++i) {
         const uint32_t di = dig(i);
-        const uint32_t peers = __match_any_sync(0xffffffffu, di);
+        const uint32_t peers = digit_peers<!PAIRS && IK == kItemsLarge>(di, pass.bits);
         const int leader = __ffs(peers) - 1;
         uint32_t prev = 0;
         if (lane == leader) prev = atomicAdd(&wh[di], uint32_t(__popc(peers)));
