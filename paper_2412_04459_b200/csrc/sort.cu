@@ -213,11 +213,16 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
         s_warp_hist[w][dg] = cnt;
         cnt += t;
     }
+    // bins past the pass's digit range stay empty: no status, no look-back
+    // (a 4-bit pass polls 16 bins per predecessor instead of 256)
+    const bool live_bin = dg < (1 << pass.bits);
     uint32_t* my_status = status + uint64_t(part) * kRadix + dg;
-    if (part == 0)
-        st_volatile(my_status, kFlagInc | cnt);
-    else
-        st_volatile(my_status, kFlagAgg | cnt);
+    if (live_bin) {
+        if (part == 0)
+            st_volatile(my_status, kFlagInc | cnt);
+        else
+            st_volatile(my_status, kFlagAgg | cnt);
+    }
 
     // block-wide exclusive scan of cnt over digits
     s_block_excl[dg] = cnt;
@@ -235,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
     // Decoupled look-back, four predecessors per round so the dependent
     // L2 round trips overlap; stops at the first inclusive prefix.
     uint32_t excl = 0;
-    if (part > 0) {
+    if (part > 0 && live_bin) {
         int64_t p = int64_t(part) - 1;
         while (p >= 0) {
             uint32_t s[4];
