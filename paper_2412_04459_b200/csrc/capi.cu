@@ -487,7 +487,19 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
         // ranked emission: the keys arrive sorted below the tile bits
         const int lo = ranked ? f->fmt.tile_shift : vb + ((multi && !use_rank) ? 0 : 3);
         const int hi = f->fmt.tile_shift + tile_bits;
-        for (int b = lo; b < hi; b += 8) passes[np++] = {0, b, std::min(8, hi - b)};
+        {  // the fewest 8-bit-or-narrower passes, bits spread evenly (12 tile
+           // bits: 6 + 6; SVR_SORT_EVEN=0 keeps 8 + 4)
+            static const bool even = [] {
+                const char* e = std::getenv("SVR_SORT_EVEN");
+                return e == nullptr || e[0] != '0';
+            }();
+            const int nb = hi - lo, npass = (nb + 7) / 8;
+            for (int q = 0, b = lo; q < npass; ++q) {
+                const int w = even ? (nb - (b - lo) + (npass - q) - 1) / (npass - q) : std::min(8, hi - b);
+                passes[np++] = {0, b, w};
+                b += w;
+            }
+        }
         RadixPlan plan{};
         plan.n = np;
         for (int i = 0; i < np; ++i) plan.p[i] = passes[i];

@@ -224,17 +224,21 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
             st_volatile(my_status, kFlagAgg | cnt);
     }
 
-    // block-wide exclusive scan of cnt over digits
-    s_block_excl[dg] = cnt;
-    __syncthreads();
-    for (int o = 1; o < kRadix; o <<= 1) {
-        uint32_t t = dg >= o ? s_block_excl[dg - o] : 0;
-        __syncthreads();
-        s_block_excl[dg] += t;
-        __syncthreads();
+    // block-wide exclusive scan of cnt over digits: warp scans, then the
+    // eight warp totals (two barriers instead of sixteen)
+    __shared__ uint32_t s_wtot[kWarps];
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
     }
-    const uint32_t block_excl = s_block_excl[dg] - cnt;
+    if (lane == 31) s_wtot[warp] = incl;
     __syncthreads();
+    uint32_t dbase = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) dbase += w < warp ? s_wtot[w] : 0u;
+    const uint32_t block_excl = dbase + incl - cnt;
     s_block_excl[dg] = block_excl;
 
     // Decoupled look-back, four predecessors per round so the dependent
