@@ -110,6 +110,9 @@ __global__ void __launch_bounds__(kRadix) bin_scan_kernel(uint32_t* hist) {
 // BALLOT: one ballot per digit bit instead of match.any — faster in the
 // large-sort instantiation (16 keys per thread; config 4 sort 1.51 -> 1.38
 // ms), slower at config-2 sizes (0.054 -> 0.067 ms), so only there.
+#ifndef SVR_SORT_BALLOT_ALL
+#define SVR_SORT_BALLOT_ALL 0
+#endif
 template <bool BALLOT>
 __device__ __forceinline__ uint32_t digit_peers(uint32_t di, int bits) {
     if (!BALLOT) return __match_any_sync(0xffffffffu, di);
@@ -182,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
 #pragma unroll
     for (int i = 0; i < Part<PAIRS, IK>::items; ++i) {
         const uint32_t di = dig(i);
-        const uint32_t peers = digit_peers<!PAIRS && IK == kItemsLarge>(di, pass.bits);
+        const uint32_t peers = digit_peers<!PAIRS && (SVR_SORT_BALLOT_ALL || IK == kItemsLarge)>(di, pass.bits);
         const int leader = __ffs(peers) - 1;
         uint32_t prev = 0;
         if (lane == leader) prev = atomicAdd(&wh[di], uint32_t(__popc(peers)));
