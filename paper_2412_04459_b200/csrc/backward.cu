@@ -94,13 +94,19 @@ __device__ __forceinline__ float warp_transpose_sum16(float (&v)[16], int lane) 
 // division-free recursion of raster.cpp:374-407. The 15 per-entry sums
 // (8 corner densities, colour, normal, priority) are reduced across the warp
 // by recursive halving and issued as one vector of global atomics.
+#ifndef SVR_BWD_F32X2
+#define SVR_BWD_F32X2 0  // packed FP32 in the hit path (bit-identical; measured: no gain, 75 registers)
+#endif
 #ifndef SVR_BWD_DIRECT
 #define SVR_BWD_DIRECT 12  // at most this many hit lanes: per-lane float4 reductions instead of the shuffle tree (4: 0.588, 8: 0.568, 12: 0.560, 16: 0.569, 32: 1.07 ms on config 3)
 #endif
 // UPC: per-contribution upstream gradients (d_weight / d_voxel_color, the
 // ray losses) present; without them the hit loop carries no checks for them.
 template <int K, bool UPC>
-__global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, BackwardArgs a) {
+#ifndef SVR_BWD_MINB
+#define SVR_BWD_MINB 1
+#endif
+__global__ void __launch_bounds__(256, SVR_BWD_MINB) composite_backward_kernel(DevCamera cam, BackwardArgs a) {
     pdl_enter();
     __shared__ float4 s_rec[8][32][kRecordF4];
     __shared__ float s_cone[8][4][3];
@@ -123,6 +129,9 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
     const float dx = float(dd[0]), dy = float(dd[1]), dz = float(dd[2]);
     const float ix = slab_inv(dd[0]), iy = slab_inv(dd[1]), iz = slab_inv(dd[2]);
     const float dnorm = float(sqrt(dd[0] * dd[0] + dd[1] * dd[1] + dd[2] * dd[2]));
+#if SVR_BWD_F32X2
+    const SlabSel ssel = slab_sel(ix, iy, iz);
+#endif
     float (*cone)[3] = s_cone[warp];
     if (lane == 0) warp_cone_planes(cam, wx0, wy0, cone);
     __syncwarp();
@@ -190,6 +199,10 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
             if (hit) {
                 const float4 lo = wrec[sl][0];
                 const float inv = wrec[sl][5].w;
+#if SVR_BWD_F32X2
+                float ta, tb;
+                slab_s(lo, ix, iy, iz, ssel, ta, tb);  // packed FP32, same floats
+#else
                 float t0 = lo.x * ix, t1 = (lo.x + lo.w) * ix;
                 float ta = fminf(t0, t1), tb = fmaxf(t0, t1);
                 t0 = lo.y * iy;
@@ -200,6 +213,7 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
                 t1 = (lo.z + lo.w) * iz;
                 ta = fmaxf(ta, fminf(t0, t1));
                 tb = fminf(tb, fmaxf(t0, t1));
+#endif
                 const float4 va = wrec[sl][2], vb = wrec[sl][3];
                 const float seg = tb - ta;
                 const float lk = seg * dnorm * (1.0f / K);
@@ -208,8 +222,13 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     tk[k] = ta + ((k + 0.5f) / K) * seg;
+#if SVR_BWD_F32X2
+                    up2(mul2(fma2(pk2(tk[k], tk[k]), pk2(dx, dy), pk2(-lo.x, -lo.y)), pk2(inv, inv)), qk[k][0],
+                        qk[k][1]);
+#else
                     qk[k][0] = (tk[k] * dx - lo.x) * inv;
                     qk[k][1] = (tk[k] * dy - lo.y) * inv;
+#endif
                     qk[k][2] = (tk[k] * dz - lo.z) * inv;
                     vk[k] = trilinear_poly(va, vb, qk[k][0], qk[k][1], qk[k][2]);
                     const float act = explin(vk[k]);
@@ -250,10 +269,23 @@ __global__ void __launch_bounds__(256) composite_backward_kernel(DevCamera cam, 
                         if (mm != k) others *= 1.0f - sa[mm];
                     const float dAk = A * others + Ti * gD * ddk[k];
                     const float dv = dAk * (1.0f - sa[k]) * lk * explin_deriv(vk[k]);
+#if SVR_BWD_F32X2
+                    {  // corners (2j, 2j+1) differ only in the z weight: FMUL2 / FFMA2 pairs
+                        const float wx[2] = {1.0f - qk[k][0], qk[k][0]}, wy[2] = {1.0f - qk[k][1], qk[k][1]};
+                        const f32x2 wz = pk2(1.0f - qk[k][2], qk[k][2]), dd = pk2(dv, dv);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const float wxy = wx[(j >> 1) & 1] * wy[j & 1];
+                            const f32x2 a2 = fma2(dd, mul2(pk2(wxy, wxy), wz), pk2(acc[2 * j], acc[2 * j + 1]));
+                            up2(a2, acc[2 * j], acc[2 * j + 1]);
+                        }
+                    }
+#else
                     float w[8];
                     trilinear_weights(qk[k][0], qk[k][1], qk[k][2], w);
 #pragma unroll
                     for (int c = 0; c < 8; ++c) acc[c] += dv * w[c];
+#endif
                 }
                 const float wgt = Ti * alpha;
                 acc[8] = wgt * gC[0];

@@ -1257,67 +1257,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
         ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
-// Blackwell packed FP32 (FFMA2 / FMUL2: two IEEE fp32 operations per
-// instruction, each rounded exactly like the scalar one). The slab's near and
-// far face of an axis share every operand but the face selector, so one
-// FFMA2 + one FMUL2 give both: 6 instead of 12 instructions per slab test.
-#ifndef SVR_F32X2
-#define SVR_F32X2 1
-#endif
-typedef unsigned long long f32x2;
-__device__ __forceinline__ f32x2 pk2(float a, float b) {
-    f32x2 r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-    return r;
-}
-__device__ __forceinline__ void up2(f32x2 v, float& a, float& b) {
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-}
-__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
-    f32x2 d;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-    return d;
-}
-__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
-    f32x2 d;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-
-struct SlabSel {
-    float nx, ny, nz;  // 1 where the inverse direction component is negative
-#if SVR_F32X2
-    f32x2 px, py, pz;  // (n, 1 - n) per axis: the near and the far face
-#endif
-};
-__device__ __forceinline__ SlabSel slab_sel(float ix, float iy, float iz) {
-    SlabSel q;
-    q.nx = ix < 0.f ? 1.f : 0.f;
-    q.ny = iy < 0.f ? 1.f : 0.f;
-    q.nz = iz < 0.f ? 1.f : 0.f;
-#if SVR_F32X2
-    q.px = pk2(q.nx, 1.f - q.nx);
-    q.py = pk2(q.ny, 1.f - q.ny);
-    q.pz = pk2(q.nz, 1.f - q.nz);
-#endif
-    return q;
-}
-__device__ __forceinline__ void slab_s(float4 lo, float ix, float iy, float iz, const SlabSel& q,
-                                       float& ta, float& tb) {
-#if SVR_F32X2
-    float ax, bx, ay, by, az, bz;
-    const f32x2 w = pk2(lo.w, lo.w);
-    up2(mul2(fma2(w, q.px, pk2(lo.x, lo.x)), pk2(ix, ix)), ax, bx);
-    up2(mul2(fma2(w, q.py, pk2(lo.y, lo.y)), pk2(iy, iy)), ay, by);
-    up2(mul2(fma2(w, q.pz, pk2(lo.z, lo.z)), pk2(iz, iz)), az, bz);
-#else
-    const float ax = fmaf(lo.w, q.nx, lo.x) * ix, bx = fmaf(lo.w, 1.f - q.nx, lo.x) * ix;
-    const float ay = fmaf(lo.w, q.ny, lo.y) * iy, by = fmaf(lo.w, 1.f - q.ny, lo.y) * iy;
-    const float az = fmaf(lo.w, q.nz, lo.z) * iz, bz = fmaf(lo.w, 1.f - q.nz, lo.z) * iz;
-#endif
-    ta = fmaxf(fmaxf(ax, ay), az);
-    tb = fminf(fminf(bx, by), bz);
-}
 __device__ __forceinline__ void slab(float4 lo, float ix, float iy, float iz, float& ta, float& tb) {
     float t0 = lo.x * ix, t1 = (lo.x + lo.w) * ix;
     ta = fminf(t0, t1);
@@ -1339,7 +1278,7 @@ constexpr size_t kCompSmem = size_t(2) * kCompWarps * 32 * kRecordF4 * sizeof(fl
 // max-blend stats and/or staged training records (their checks compiled in);
 // 3: staged training records only (the single-pass training render).
 #ifndef SVR_PHB_SLABS
-#define SVR_PHB_SLABS 0
+#define SVR_PHB_SLABS 1
 #endif
 constexpr int kBatch = 1024;        // entries culled per CTA batch (cooperative path)
 constexpr int kSubs = kBatch / 32;  // 32-entry sub-chunks per batch
@@ -1546,8 +1485,13 @@ __device__ __forceinline__ void composite_tile_warp(const DevCamera& cam, const 
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 tk[k] = ta + ((k + 0.5f) / K) * seg;
+#if SVR_F32X2_Q
+                float qx, qy;  // (qx, qy) in one FFMA2 + FMUL2, same roundings
+                up2(mul2(fma2(pk2(tk[k], tk[k]), pk2(dx, dy), pk2(-lo.x, -lo.y)), pk2(inv, inv)), qx, qy);
+#else
                 const float qx = (tk[k] * dx - lo.x) * inv;
                 const float qy = (tk[k] * dy - lo.y) * inv;
+#endif
                 const float qz = (tk[k] * dz - lo.z) * inv;
                 const float act = explin(trilinear_poly(va, vb, qx, qy, qz));
                 sum += act;
@@ -1576,11 +1520,21 @@ __device__ __forceinline__ void composite_tile_warp(const DevCamera& cam, const 
                 }
                 const float w = T * alpha;
                 const float4 col = wrec[s_][4], nor = wrec[s_][5];
+#if SVR_F32X2_ACC
+                {  // (cr, cg) and (nx, ny) as packed pairs: one FFMA2 each
+                    const f32x2 ww = pk2(w, w);
+                    f32x2 c2 = fma2(ww, pk2(col.x, col.y), pk2(cr, cg));
+                    f32x2 n2 = fma2(ww, pk2(nor.x, nor.y), pk2(nx, ny));
+                    up2(c2, cr, cg);
+                    up2(n2, nx, ny);
+                }
+#else
                 cr += w * col.x;
                 cg += w * col.y;
-                cb += w * col.z;
                 nx += w * nor.x;
                 ny += w * nor.y;
+#endif
+                cb += w * col.z;
                 nz += w * nor.z;
                 depth += T * dv;
                 if (EXTRA && a.max_blend) atomicMax(a.max_blend + __float_as_uint(col.w), __float_as_uint(w));
@@ -1770,7 +1724,11 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
                 continue;
             const float4 lo = wrec[s_][0];
             float ta, tb;
+#if SVR_PHB_SLABS
+            slab_s(lo, ix, iy, iz, ssel, ta, tb);
+#else
             slab(lo, ix, iy, iz, ta, tb);
+#endif
             const float4 va = wrec[s_][2], vb = wrec[s_][3];
             const float inv = wrec[s_][5].w;
             const float seg = tb - ta;
@@ -1780,8 +1738,13 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 tk[k] = ta + ((k + 0.5f) / K) * seg;
+#if SVR_F32X2_Q
+                float qx, qy;  // (qx, qy) in one FFMA2 + FMUL2, same roundings
+                up2(mul2(fma2(pk2(tk[k], tk[k]), pk2(dx, dy), pk2(-lo.x, -lo.y)), pk2(inv, inv)), qx, qy);
+#else
                 const float qx = (tk[k] * dx - lo.x) * inv;
                 const float qy = (tk[k] * dy - lo.y) * inv;
+#endif
                 const float qz = (tk[k] * dz - lo.z) * inv;
                 const float act = explin(trilinear_poly(va, vb, qx, qy, qz));
                 sum += act;
@@ -1809,11 +1772,21 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
                 }
                 const float w = T * alpha;
                 const float4 col = wrec[s_][4], nor = wrec[s_][5];
+#if SVR_F32X2_ACC
+                {  // (cr, cg) and (nx, ny) as packed pairs: one FFMA2 each
+                    const f32x2 ww = pk2(w, w);
+                    f32x2 c2 = fma2(ww, pk2(col.x, col.y), pk2(cr, cg));
+                    f32x2 n2 = fma2(ww, pk2(nor.x, nor.y), pk2(nx, ny));
+                    up2(c2, cr, cg);
+                    up2(n2, nx, ny);
+                }
+#else
                 cr += w * col.x;
                 cg += w * col.y;
-                cb += w * col.z;
                 nx += w * nor.x;
                 ny += w * nor.y;
+#endif
+                cb += w * col.z;
                 nz += w * nor.z;
                 depth += T * dv;
                 if (EXTRA && a.max_blend) atomicMax(a.max_blend + __float_as_uint(col.w), __float_as_uint(w));
