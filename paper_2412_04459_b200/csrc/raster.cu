@@ -204,8 +204,7 @@ __global__ void __launch_bounds__(kPreThreads, SVR_PRE_MINB) preprocess_kernel(D
                           __ldg(a.density + c1.z), __ldg(a.density + c1.w)};
             float cf[8];
             trilinear_coeffs(V, cf);
-            r2 = make_float4(cf[0], cf[1], cf[2], cf[3]);
-            r3 = make_float4(cf[4], cf[5], cf[6], cf[7]);
+            pack_coeffs(cf, r2, r3);
             // sh_eval(normalized(center - cam.pos)) (raster.cpp:195-196, sh.hpp:48-58)
             const double dx = dsub(center[0], cam.pos[0]), dy = dsub(center[1], cam.pos[1]),
                          dz = dsub(center[2], cam.pos[2]);

@@ -389,7 +389,8 @@ void launch_duplicate_list(const DevCamera& cam, uint64_t n, const uint32_t* vid
 
 // Voxel record (96 B = 6 float4), written by K1, read by K7/K9/K10:
 //   [0] lo.xyz (camera-relative min corner), size   [1] screen AABB x0,x1,y0,y1
-//   [2] c0..c3   [3] c4..c7  (trilinear_coeffs of the corner densities V0..V7)
+//   [2] c6,c7,c2,c4   [3] c3,c5,c0,c1  (trilinear_coeffs of the corner densities
+//       V0..V7, pair-ordered for FFMA2: pack_coeffs)
 //   [4] rgb, vid (bits)   [5] unit normal, 1/size
 constexpr int kRecordF4 = 6;
 

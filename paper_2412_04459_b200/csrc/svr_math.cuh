@@ -397,17 +397,32 @@ SVR_HD void trilinear_coeffs(const float* V, float* c) {
     c[6] = (V[3] - V[2]) - (V[1] - V[0]);
     c[7] = ((V[7] - V[6]) - (V[5] - V[4])) - ((V[3] - V[2]) - (V[1] - V[0]));
 }
-SVR_HD float trilinear_poly(float4 ca, float4 cb, float qx, float qy, float qz) {
-    const float t3 = fmaf(qy, fmaf(qz, cb.w, cb.x), fmaf(qz, cb.y, ca.y));
-    const float t6 = fmaf(qy, fmaf(qz, cb.z, ca.z), fmaf(qz, ca.w, ca.x));
+// The record stores the coefficients pair-ordered for packed FP32:
+//   ca = (c6, c7, c2, c4), cb = (c3, c5, c0, c1)
+// so that (t6, t3) = qy * (qz * (c6, c7) + (c2, c4)) + (qz * (c3, c5) + (c0, c1))
+// is three FFMA2 on register pairs as they come out of the 16-B loads, and
+// f = qx * t3 + t6 one FFMA: each lane rounds exactly like the scalar chain.
+SVR_HD void pack_coeffs(const float* c, float4& ca, float4& cb) {
+    ca = make_float4(c[6], c[7], c[2], c[4]);
+    cb = make_float4(c[3], c[5], c[0], c[1]);
+}
+SVR_HD void unpack_coeffs(float4 ca, float4 cb, float* c) {
+    c[0] = cb.z; c[1] = cb.w; c[2] = ca.z; c[3] = cb.x;
+    c[4] = ca.w; c[5] = cb.y; c[6] = ca.x; c[7] = ca.y;
+}
+SVR_HD float trilinear_poly_s(float4 ca, float4 cb, float qx, float qy, float qz) {
+    const float t3 = fmaf(qy, fmaf(qz, ca.y, ca.w), fmaf(qz, cb.y, cb.w));
+    const float t6 = fmaf(qy, fmaf(qz, ca.x, ca.z), fmaf(qz, cb.x, cb.z));
     return fmaf(qx, t3, t6);
 }
 // Corner densities back from the coefficients (epilogue's normal chain).
 SVR_HD void trilinear_corners(float4 ca, float4 cb, float* V) {
+    float c[8];
+    unpack_coeffs(ca, cb, c);
     for (int n = 0; n < 8; ++n) {
         const float i = float((n >> 2) & 1), j = float((n >> 1) & 1), k = float(n & 1);
-        V[n] = ca.x + i * ca.y + j * ca.z + k * ca.w + i * j * cb.x + i * k * cb.y + j * k * cb.z +
-               i * j * k * cb.w;
+        V[n] = c[0] + i * c[1] + j * c[2] + k * c[3] + i * j * c[4] + i * k * c[5] + j * k * c[6] +
+               i * j * k * c[7];
     }
 }
 
@@ -449,6 +464,23 @@ __device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
     f32x2 d;
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
     return d;
+}
+
+#ifndef SVR_F32X2_TRI
+#define SVR_F32X2_TRI 1
+#endif
+// trilinear_poly_s in three FFMA2 + one FFMA (record layout: pack_coeffs).
+__device__ __forceinline__ float trilinear_poly(float4 ca, float4 cb, float qx, float qy, float qz) {
+#if SVR_F32X2_TRI
+    const f32x2 z2 = pk2(qz, qz);
+    const f32x2 a = fma2(z2, pk2(ca.x, ca.y), pk2(ca.z, ca.w));
+    const f32x2 b = fma2(z2, pk2(cb.x, cb.y), pk2(cb.z, cb.w));
+    float t6, t3;
+    up2(fma2(pk2(qy, qy), a, b), t6, t3);
+    return fmaf(qx, t3, t6);
+#else
+    return trilinear_poly_s(ca, cb, qx, qy, qz);
+#endif
 }
 
 struct SlabSel {
