@@ -1276,6 +1276,21 @@ constexpr size_t kCompSmem = size_t(2) * kCompWarps * 32 * kRecordF4 * sizeof(fl
 // MODE 0: plain render; 1: record pass (RECORD); 2: render with per-voxel
 // max-blend stats and/or staged training records (their checks compiled in);
 // 3: staged training records only (the single-pass training render).
+// A warp's staged records: 32 slots x 6 float4. SVR_REC_SOA stores them as
+// six planes of 32 (slot stride 16 B), so phase-B lanes reading different
+// slots and the cp.async writes of different slots hit distinct banks (the
+// 96-B slot stride of the slot-major layout maps 32 slots onto 4 bank groups).
+#ifndef SVR_REC_SOA
+#define SVR_REC_SOA 1
+#endif
+#if SVR_REC_SOA
+#define WREC(w, slot, k) (w)[(k) * 32 + (slot)]
+#else
+#define WREC(w, slot, k) (w)[(slot) * kRecordF4 + (k)]
+#endif
+#if SVR_REC_SOA && SVR_BULK
+#error "SVR_BULK copies a record as one contiguous 96-B block: needs SVR_REC_SOA=0"
+#endif
 #ifndef SVR_PHB_SLABS
 #define SVR_PHB_SLABS 1
 #endif
@@ -1367,9 +1382,8 @@ __device__ __forceinline__ void composite_tile_warp(const DevCamera& cam, const 
     const uint2 range = a.ranges[tile];
     const float thr = a.t_threshold;
     constexpr uint32_t kVidMask = (1u << 29) - 1u;
-    float4 (*wrec0)[kRecordF4] =
-        reinterpret_cast<float4 (*)[kRecordF4]>(s_rec_dyn + size_t(warp) * 32 * kRecordF4);
-    float4 (*wrec1)[kRecordF4] = wrec0 + kCompWarps * 32;
+    float4* wrec0 = s_rec_dyn + size_t(warp) * 32 * kRecordF4;
+    float4* wrec1 = wrec0 + kCompWarps * 32 * kRecordF4;
 
     // Cull one chunk (entries c .. c+31, lane = entry) and start the copy of
     // its surviving records into buffer `buf`. Returns the survivor mask.
@@ -1387,17 +1401,17 @@ __device__ __forceinline__ void composite_tile_warp(const DevCamera& cam, const 
             wvid[at] = v;
             s_j[buf][warp][at] = uint8_t(lane);
         }
-        float4(*wrec)[kRecordF4] = buf ? wrec1 : wrec0;
+        float4* wrec = buf ? wrec1 : wrec0;
 #if SVR_BULK
         if (lane == 0) mbar_arrive_expect(&mbar[buf], unsigned(__popc(m)) * kRecordF4 * 16u);
-        if (rel) bulk_g2s(&wrec[at][0], a.records + uint64_t(v & kVidMask) * kRecordF4, kRecordF4 * 16u,
+        if (rel) bulk_g2s(&WREC(wrec, at, 0), a.records + uint64_t(v & kVidMask) * kRecordF4, kRecordF4 * 16u,
                           &mbar[buf]);
         pend |= 1u << buf;
 #else
         if (rel) {  // the lane of each surviving entry copies its record
             const float4* src = a.records + uint64_t(v & kVidMask) * kRecordF4;
 #pragma unroll
-            for (int k = 0; k < kRecordF4; ++k) cp_async16(&wrec[at][k], src + k);
+            for (int k = 0; k < kRecordF4; ++k) cp_async16(&WREC(wrec, at, k), src + k);
         }
         cp_async_commit();
 #endif
@@ -1445,7 +1459,7 @@ __device__ __forceinline__ void composite_tile_warp(const DevCamera& cam, const 
         __syncwarp();
 
         const int nrel = __popc(m_cur);
-        float4(*wrec)[kRecordF4] = buf ? wrec1 : wrec0;
+        float4* wrec = buf ? wrec1 : wrec0;
         const uint32_t* wvid = s_vid[buf][warp];
         const uint8_t* wj = s_j[buf][warp];
         // Phase A: this lane's slab hits among the slots (the sign-pattern
@@ -1455,7 +1469,7 @@ __device__ __forceinline__ void composite_tile_warp(const DevCamera& cam, const 
 #pragma unroll 2
             for (int sl = 0; sl < nrel; ++sl) {
                 float ta, tb;
-                slab_s(wrec[sl][0], ix, iy, iz, ssel, ta, tb);
+                slab_s(WREC(wrec, sl, 0), ix, iy, iz, ssel, ta, tb);
                 hits |= uint32_t(ta <= tb && ta > 0.0f) << sl;
             }
         }
@@ -1463,20 +1477,20 @@ __device__ __forceinline__ void composite_tile_warp(const DevCamera& cam, const 
         while (hits) {
             const int s_ = __ffs(hits) - 1;
             hits &= hits - 1;
-            const float4 bb = wrec[s_][1];
+            const float4 bb = WREC(wrec, s_, 1);
             const float2 pc = PC_SMEM ? sh.pc[PC_SMEM ? threadIdx.x : 0] : make_float2(pcx, pcy);
             if (!((one_sign || (wvid[s_] >> 29) == my_sign) &&
                   !(pc.x < bb.x || pc.x > bb.y || pc.y < bb.z || pc.y > bb.w)))
                 continue;
-            const float4 lo = wrec[s_][0];
+            const float4 lo = WREC(wrec, s_, 0);
             float ta, tb;
 #if SVR_PHB_SLABS
             slab_s(lo, ix, iy, iz, ssel, ta, tb);
 #else
             slab(lo, ix, iy, iz, ta, tb);  // same floats as slab_s; needs no per-lane face selectors
 #endif
-            const float4 va = wrec[s_][2], vb = wrec[s_][3];
-            const float inv = wrec[s_][5].w;
+            const float4 va = WREC(wrec, s_, 2), vb = WREC(wrec, s_, 3);
+            const float inv = WREC(wrec, s_, 5).w;
             const float seg = tb - ta;
             const float lk = seg * dnorm * (1.0f / K);
             // voxel_alpha (field.hpp:92-116), K-point midpoint quadrature
@@ -1518,7 +1532,7 @@ __device__ __forceinline__ void composite_tile_warp(const DevCamera& cam, const 
                     }
                 }
                 const float w = T * alpha;
-                const float4 col = wrec[s_][4], nor = wrec[s_][5];
+                const float4 col = WREC(wrec, s_, 4), nor = WREC(wrec, s_, 5);
 #if SVR_F32X2_ACC
                 {  // (cr, cg) and (nx, ny) as packed pairs: one FFMA2 each
                     const f32x2 ww = pk2(w, w);
@@ -1660,8 +1674,7 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
     const uint2 range = a.ranges[tile];
     const float thr = a.t_threshold;
     constexpr uint32_t kVidMask = (1u << 29) - 1u;
-    float4 (*wrec0)[kRecordF4] =
-        reinterpret_cast<float4 (*)[kRecordF4]>(s_rec_dyn + size_t(warp) * 32 * kRecordF4);
+    float4* wrec0 = s_rec_dyn + size_t(warp) * 32 * kRecordF4;
 
     // Culls entries range.x + kBatch b + 256 r + threadIdx.x (r < 4) into
     // ballot buffer pb: sub-chunk 8 r + warp, one word per target warp.
@@ -1700,7 +1713,7 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
 
     // Composites group buffer g (n slots, records landed).
     auto composite_group = [&](int g, int n) {
-        float4(*wrec)[kRecordF4] = g ? wrec0 + kCompWarps * 32 : wrec0;
+        float4* wrec = g ? wrec0 + kCompWarps * 32 * kRecordF4 : wrec0;
         const uint8_t* wsg = s_sign[g][warp];
         // Phase A: this lane's slab hits among the slots.
         uint32_t hits = 0;
@@ -1708,7 +1721,7 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
 #pragma unroll 2
             for (int sl = 0; sl < n; ++sl) {
                 float ta, tb;
-                slab_s(wrec[sl][0], ix, iy, iz, ssel, ta, tb);
+                slab_s(WREC(wrec, sl, 0), ix, iy, iz, ssel, ta, tb);
                 hits |= uint32_t(ta <= tb && ta > 0.0f) << sl;
             }
         }
@@ -1716,20 +1729,20 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
         while (hits) {
             const int s_ = __ffs(hits) - 1;
             hits &= hits - 1;
-            const float4 bb = wrec[s_][1];
+            const float4 bb = WREC(wrec, s_, 1);
             const float2 pc = ENTRY ? make_float2(pcx, pcy) : s_pc[ENTRY ? 0 : threadIdx.x];
             if (!((one_sign || wsg[s_] == my_sign) &&
                   !(pc.x < bb.x || pc.x > bb.y || pc.y < bb.z || pc.y > bb.w)))
                 continue;
-            const float4 lo = wrec[s_][0];
+            const float4 lo = WREC(wrec, s_, 0);
             float ta, tb;
 #if SVR_PHB_SLABS
             slab_s(lo, ix, iy, iz, ssel, ta, tb);
 #else
             slab(lo, ix, iy, iz, ta, tb);
 #endif
-            const float4 va = wrec[s_][2], vb = wrec[s_][3];
-            const float inv = wrec[s_][5].w;
+            const float4 va = WREC(wrec, s_, 2), vb = WREC(wrec, s_, 3);
+            const float inv = WREC(wrec, s_, 5).w;
             const float seg = tb - ta;
             const float lk = seg * dnorm * (1.0f / K);
             // voxel_alpha (field.hpp:92-116), K-point midpoint quadrature
@@ -1770,7 +1783,7 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
                     }
                 }
                 const float w = T * alpha;
-                const float4 col = wrec[s_][4], nor = wrec[s_][5];
+                const float4 col = WREC(wrec, s_, 4), nor = WREC(wrec, s_, 5);
 #if SVR_F32X2_ACC
                 {  // (cr, cg) and (nx, ny) as packed pairs: one FFMA2 each
                     const f32x2 ww = pk2(w, w);
@@ -1838,9 +1851,9 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
                         s_sign[g][warp][at] = uint8_t(v >> 29);
                         if (ENTRY) s_ent[ENTRY ? g : 0][warp][at] = e0 + lane;
                         const float4* src = a.records + uint64_t(v & kVidMask) * kRecordF4;
-                        float4(*wrec)[kRecordF4] = g ? wrec0 + kCompWarps * 32 : wrec0;
+                        float4* wrec = g ? wrec0 + kCompWarps * 32 * kRecordF4 : wrec0;
 #pragma unroll
-                        for (int k = 0; k < kRecordF4; ++k) cp_async16(&wrec[at][k], src + k);
+                        for (int k = 0; k < kRecordF4; ++k) cp_async16(&WREC(wrec, at, k), src + k);
                     }
                     nfill += take;
                     if (nfill == 32) {  // group full: composite the previous one meanwhile
