@@ -24,6 +24,9 @@ namespace svrb {
 
 namespace {
 
+#ifndef SVR_SORT_CONST_BITS
+#define SVR_SORT_CONST_BITS 1
+#endif
 #ifndef SVR_SORT_ATOMIC_RANK
 #define SVR_SORT_ATOMIC_RANK 1
 #endif
@@ -113,18 +116,38 @@ __global__ void __launch_bounds__(kRadix) bin_scan_kernel(uint32_t* hist) {
 #ifndef SVR_SORT_BALLOT_ALL
 #define SVR_SORT_BALLOT_ALL 0
 #endif
-template <bool BALLOT>
+// BITS > 0: the pass's digit width as a compile-time constant (unrolled
+// ballots, constant masks); EMPTY: the warp holds out-of-range slots (only in
+// the last partition), whose digit kRadix needs one more ballot.
+template <bool BALLOT, int BITS = 0, bool EMPTY = true>
 __device__ __forceinline__ uint32_t digit_peers(uint32_t di, int bits) {
     if (!BALLOT) return __match_any_sync(0xffffffffu, di);
     uint32_t peers = 0xffffffffu;
-    for (int b = 0; b < bits; ++b) {
-        const bool on = (di >> b) & 1u;
-        const uint32_t bal = __ballot_sync(0xffffffffu, on);
-        peers &= on ? bal : ~bal;
+    if constexpr (BITS > 0) {
+#pragma unroll
+        for (int b = 0; b < BITS; ++b) {
+            const bool on = (di >> b) & 1u;
+            const uint32_t bal = __ballot_sync(0xffffffffu, on);
+            peers &= on ? bal : ~bal;
+        }
+    } else {
+        for (int b = 0; b < bits; ++b) {
+            const bool on = (di >> b) & 1u;
+            const uint32_t bal = __ballot_sync(0xffffffffu, on);
+            peers &= on ? bal : ~bal;
+        }
     }
+    if (!EMPTY) return peers;
     const bool empty = di >= uint32_t(kRadix);
     const uint32_t bal = __ballot_sync(0xffffffffu, empty);
     return peers & (empty ? bal : ~bal);
+}
+
+// Keys-only digit with a compile-time width when BITS > 0.
+template <int BITS>
+__device__ __forceinline__ uint32_t key_digit(uint64_t k, RadixPass p) {
+    const uint32_t mask = BITS > 0 ? (1u << BITS) - 1u : (1u << p.bits) - 1u;
+    return uint32_t(k >> p.shift) & mask;
 }
 
 __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
@@ -136,7 +159,7 @@ __device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
     asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(p), "r"(v));
 }
 
-template <bool PAIRS, int IK = kItemsK>
+template <bool PAIRS, int IK = kItemsK, int BITS = 0>
 __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
     const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint64_t n, RadixPass pass,
@@ -166,9 +189,12 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
     uint64_t k[Part<PAIRS, IK>::items];
     uint32_t v[PAIRS ? Part<PAIRS, IK>::items : 1], r[Part<PAIRS, IK>::items];
     const uint64_t nvalid = n > wbase ? n - wbase : 0;
+    // full: every slot of this warp holds a key (all but the last partition)
+    const bool full = nvalid >= uint64_t(Part<PAIRS, IK>::items) * 32;
     auto dig = [&](int i) -> uint32_t {
-        return (uint64_t(i) * 32 + lane < nvalid) ? digit_of(k[i], PAIRS ? v[PAIRS ? i : 0] : 0u, pass)
-                                                  : uint32_t(kRadix);
+        if (full || uint64_t(i) * 32 + lane < nvalid)
+            return PAIRS ? digit_of(k[i], v[PAIRS ? i : 0], pass) : key_digit<BITS>(k[i], pass);
+        return uint32_t(kRadix);
     };
 #pragma unroll
     for (int i = 0; i < Part<PAIRS, IK>::items; ++i) {
@@ -185,7 +211,9 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
 #pragma unroll
     for (int i = 0; i < Part<PAIRS, IK>::items; ++i) {
         const uint32_t di = dig(i);
-        const uint32_t peers = digit_peers<!PAIRS && (SVR_SORT_BALLOT_ALL || IK == kItemsLarge)>(di, pass.bits);
+        constexpr bool kBallot = !PAIRS && (SVR_SORT_BALLOT_ALL || IK == kItemsLarge);
+        const uint32_t peers = full ? digit_peers<kBallot, BITS, false>(di, pass.bits)
+                                    : digit_peers<kBallot, BITS, true>(di, pass.bits);
         const int leader = __ffs(peers) - 1;
         uint32_t prev = 0;
         if (lane == leader) prev = atomicAdd(&wh[di], uint32_t(__popc(peers)));
@@ -287,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
     for (uint32_t pos = threadIdx.x; pos < tile_n; pos += kThreads) {
         uint64_t kk = s_keys[pos];
         uint32_t vv = PAIRS ? s_vals[pos] : 0u;
-        uint32_t dd = digit_of(kk, vv, pass);
+        uint32_t dd = PAIRS ? digit_of(kk, vv, pass) : key_digit<BITS>(kk, pass);
         uint64_t o = uint64_t(s_global[dd]) + pos;
         if (!PAIRS && out_vb >= 0) {
             // final pass of a packed sort: the reference value only, and the
@@ -302,6 +330,23 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
         keys_out[o] = kk;
         if (PAIRS) vals_out[o] = vv;
     }
+}
+
+// Keys-only pass kernel with the digit width as a compile-time constant
+// (the tile bits are split evenly, so 4..7 cover every image up to 2^14 tiles).
+template <int IK>
+decltype(&onesweep_kernel<false, IK, 0>) pick_onesweep(int bits) {
+#if SVR_SORT_CONST_BITS
+    switch (bits) {
+        case 4: return onesweep_kernel<false, IK, 4>;
+        case 5: return onesweep_kernel<false, IK, 5>;
+        case 6: return onesweep_kernel<false, IK, 6>;
+        case 7: return onesweep_kernel<false, IK, 7>;
+        default: break;
+    }
+#endif
+    (void)bits;
+    return onesweep_kernel<false, IK, 0>;
 }
 
 }  // namespace
@@ -400,7 +445,7 @@ int radix_sort_keys(uint64_t* keys0, uint64_t* keys1, uint64_t n, const RadixPas
                                       : nparts;
     for (int p = 0; p < npasses; ++p) {
         const bool last_fin = fin && p == npasses - 1;
-        launch_pdl(large ? onesweep_kernel<false, kItemsLarge> : onesweep_kernel<false, kItemsK>,
+        launch_pdl(large ? pick_onesweep<kItemsLarge>(passes[p].bits) : pick_onesweep<kItemsK>(passes[p].bits),
                    unsigned(nparts_run), kThreads, 0, st, (const uint64_t*)kin,
                    (const uint32_t*)nullptr, kout, last_fin ? fin->vals : (uint32_t*)nullptr, n, passes[p],
                    (const uint32_t*)(hist + p * kRadix), status + size_t(p) * (nparts_alloc + 1) * kRadix,
