@@ -126,9 +126,17 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t di, int bits) {
     if constexpr (BITS > 0) {
 #pragma unroll
         for (int b = 0; b < BITS; ++b) {
-            const bool on = (di >> b) & 1u;
-            const uint32_t bal = __ballot_sync(0xffffffffu, on);
-            peers &= on ? bal : ~bal;
+            // lanes whose bit b equals ours: one predicate test, the ballot,
+            // a select and one LOP3 (C++ gives ptxas two predicates per bit)
+            asm("{\n\t.reg .pred p;\n\t.reg .b32 t, m;\n\t"
+                "and.b32 t, %1, %2;\n\t"
+                "setp.ne.u32 p, t, 0;\n\t"
+                "vote.sync.ballot.b32 t, p, 0xffffffff;\n\t"
+                "selp.b32 m, 0, -1, p;\n\t"
+                "xor.b32 t, t, m;\n\t"
+                "and.b32 %0, %0, t;\n\t}"
+                : "+r"(peers)
+                : "r"(di), "r"(1u << b));
         }
     } else {
         for (int b = 0; b < bits; ++b) {
@@ -189,12 +197,15 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
     uint64_t k[Part<PAIRS, IK>::items];
     uint32_t v[PAIRS ? Part<PAIRS, IK>::items : 1], r[Part<PAIRS, IK>::items];
     const uint64_t nvalid = n > wbase ? n - wbase : 0;
-    // full: every slot of this warp holds a key (all but the last partition)
-    const bool full = nvalid >= uint64_t(Part<PAIRS, IK>::items) * 32;
+    // Slots past the live count (last partition only) take the pass's largest
+    // digit: they rank after every real key of that bin in this partition, i.e.
+    // at the partition's end (shared positions >= tile_n), and are never
+    // written out; no later partition reads this one's status.
+    const uint32_t pad_digit = (1u << (BITS > 0 ? BITS : pass.bits)) - 1u;
     auto dig = [&](int i) -> uint32_t {
-        if (full || uint64_t(i) * 32 + lane < nvalid)
+        if (uint64_t(i) * 32 + lane < nvalid)
             return PAIRS ? digit_of(k[i], v[PAIRS ? i : 0], pass) : key_digit<BITS>(k[i], pass);
-        return uint32_t(kRadix);
+        return pad_digit;
     };
 #pragma unroll
     for (int i = 0; i < Part<PAIRS, IK>::items; ++i) {
@@ -212,8 +223,7 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
     for (int i = 0; i < Part<PAIRS, IK>::items; ++i) {
         const uint32_t di = dig(i);
         constexpr bool kBallot = !PAIRS && (SVR_SORT_BALLOT_ALL || IK == kItemsLarge);
-        const uint32_t peers = full ? digit_peers<kBallot, BITS, false>(di, pass.bits)
-                                    : digit_peers<kBallot, BITS, true>(di, pass.bits);
+        const uint32_t peers = digit_peers<kBallot, BITS, false>(di, pass.bits);
         const int leader = __ffs(peers) - 1;
         uint32_t prev = 0;
         if (lane == leader) prev = atomicAdd(&wh[di], uint32_t(__popc(peers)));
@@ -304,11 +314,9 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
 #pragma unroll
     for (int i = 0; i < Part<PAIRS, IK>::items; ++i) {
         const uint32_t di = dig(i);
-        if (di < kRadix) {
-            uint32_t pos = s_block_excl[di] + s_warp_hist[warp][di] + r[i];
-            s_keys[pos] = k[i];
-            if (PAIRS) s_vals[pos] = v[PAIRS ? i : 0];
-        }
+        const uint32_t pos = s_block_excl[di] + s_warp_hist[warp][di] + r[i];
+        s_keys[pos] = k[i];
+        if (PAIRS) s_vals[pos] = v[PAIRS ? i : 0];
     }
     __syncthreads();
     const uint32_t tile_n = uint32_t(min(uint64_t(Part<PAIRS, IK>::keys), n - base));
