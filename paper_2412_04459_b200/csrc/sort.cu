@@ -24,6 +24,9 @@ namespace svrb {
 
 namespace {
 
+#ifndef SVR_SORT_EARLY_SCATTER
+#define SVR_SORT_EARLY_SCATTER 1
+#endif
 #ifndef SVR_SORT_CONST_BITS
 #define SVR_SORT_CONST_BITS 1
 #endif
@@ -281,6 +284,19 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
     for (int w = 0; w < kWarps; ++w) dbase += w < warp ? s_wtot[w] : 0u;
     const uint32_t block_excl = dbase + incl - cnt;
     s_block_excl[dg] = block_excl;
+#if SVR_SORT_EARLY_SCATTER
+    // The shared-memory scatter needs only block-local offsets: do it before
+    // the look-back, so the (L2-latency-bound) look-back of the live-bin
+    // threads overlaps the other warps' scatter instead of idling the CTA.
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < Part<PAIRS, IK>::items; ++i) {
+        const uint32_t di = dig(i);
+        const uint32_t pos = s_block_excl[di] + s_warp_hist[warp][di] + r[i];
+        s_keys[pos] = k[i];
+        if (PAIRS) s_vals[pos] = v[PAIRS ? i : 0];
+    }
+#endif
 
     // Decoupled look-back, four predecessors per round so the dependent
     // L2 round trips overlap; stops at the first inclusive prefix.
@@ -308,6 +324,7 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
         st_volatile(my_status, kFlagInc | (excl + cnt));
     }
     s_global[dg] = bin_base[dg] + excl - block_excl;
+#if !SVR_SORT_EARLY_SCATTER
     __syncthreads();
 
     // Scatter to shared memory in digit order, then out to global.
@@ -318,6 +335,7 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
         s_keys[pos] = k[i];
         if (PAIRS) s_vals[pos] = v[PAIRS ? i : 0];
     }
+#endif
     __syncthreads();
     const uint32_t tile_n = uint32_t(min(uint64_t(Part<PAIRS, IK>::keys), n - base));
     for (uint32_t pos = threadIdx.x; pos < tile_n; pos += kThreads) {
