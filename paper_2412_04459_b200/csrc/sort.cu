@@ -27,6 +27,9 @@ namespace {
 #ifndef SVR_SORT_EARLY_SCATTER
 #define SVR_SORT_EARLY_SCATTER 1
 #endif
+#ifndef SVR_SORT_LB_PREFETCH
+#define SVR_SORT_LB_PREFETCH 0
+#endif
 #ifndef SVR_SORT_CONST_BITS
 #define SVR_SORT_CONST_BITS 1
 #endif
@@ -267,6 +270,10 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
         else
             st_volatile(my_status, kFlagAgg | cnt);
     }
+    // the predecessor's status, read now and consumed after the scatter: when
+    // it is already inclusive the look-back costs no further round trip
+    uint32_t pre = 0;
+    if (SVR_SORT_LB_PREFETCH && part > 0 && live_bin) pre = ld_volatile(status + uint64_t(part - 1) * kRadix + dg);
 
     // block-wide exclusive scan of cnt over digits: warp scans, then the
     // eight warp totals (two barriers instead of sixteen)
@@ -301,7 +308,10 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
     // Decoupled look-back, four predecessors per round so the dependent
     // L2 round trips overlap; stops at the first inclusive prefix.
     uint32_t excl = 0;
-    if (part > 0 && live_bin) {
+    if (SVR_SORT_LB_PREFETCH && (pre & kFlagInc)) {
+        excl = pre & kValMask;
+        st_volatile(my_status, kFlagInc | (excl + cnt));
+    } else if (part > 0 && live_bin) {
         int64_t p = int64_t(part) - 1;
         while (p >= 0) {
             uint32_t s[4];
@@ -349,8 +359,19 @@ __global__ void __launch_bounds__(kThreads, 4) onesweep_kernel(
             // are contiguous in the output, so min of starts / max of ends)
             vals_out[o] = (uint32_t((kk >> out_vb) & 7u) << 29) | uint32_t(kk & ((uint64_t(1) << out_vb) - 1));
             const uint64_t t = kk >> tile_shift;
-            if (pos == 0 || (s_keys[pos - 1] >> tile_shift) != t) atomicMin(&ranges[t].x, uint32_t(o));
-            if (pos + 1 == tile_n || (s_keys[pos + 1] >> tile_shift) != t) atomicMax(&ranges[t].y, uint32_t(o + 1));
+            bool first, last;
+            if (tile_shift >= 32) {  // the tile lies in the high words: 4-B neighbour loads, 32-bit compares
+                const uint32_t* s_hi = reinterpret_cast<const uint32_t*>(s_keys) + 1;
+                const uint32_t hi = uint32_t(kk >> 32);
+                const int hs = tile_shift - 32;
+                first = pos == 0 || ((s_hi[2 * (pos - 1)] ^ hi) >> hs) != 0u;
+                last = pos + 1 == tile_n || ((s_hi[2 * (pos + 1)] ^ hi) >> hs) != 0u;
+            } else {
+                first = pos == 0 || (s_keys[pos - 1] >> tile_shift) != t;
+                last = pos + 1 == tile_n || (s_keys[pos + 1] >> tile_shift) != t;
+            }
+            if (first) atomicMin(&ranges[t].x, uint32_t(o));
+            if (last) atomicMax(&ranges[t].y, uint32_t(o + 1));
             continue;
         }
         keys_out[o] = kk;
