@@ -1029,27 +1029,44 @@ __global__ void __launch_bounds__(256) duplicate_big_ranked_kernel(
                 if (lane >= o) incl += y;
             }
             const int total = __shfl_sync(0xffffffffu, incl, 31);
+            if (td.hist && td.two && a >= 0 && len > 0) {
+                // high digit of a one-run row: one add per 2^b0-aligned segment
+                const uint32_t t1 = uint32_t(ty) * cam.ntx + uint32_t(a + len - 1);
+                for (uint32_t t = uint32_t(ty) * cam.ntx + uint32_t(a); t <= t1;) {
+                    const uint32_t seg_end = min(t1, (((t >> td.b0) + 1) << td.b0) - 1);
+                    atomicAdd(&s_h[1][(t >> td.b0) & td.m1], seg_end - t + 1);
+                    t = seg_end + 1;
+                }
+            }
             if (!__any_sync(0xffffffffu, a < 0 && len > 0)) {
-                // every row one run: the group's entries as one flat range,
-                // lane q of each 32 finds its row by binary search over the
-                // row prefix sums
+                // every row one run: the group's entries as one flat range.
+                // Rows of one length and start column (a rectangle inside
+                // the pattern's runs, the usual case) give lane q its row by a
+                // division; otherwise a binary search over the row prefix sums.
+                const int nrows = min(32, rc.w - ty0 + 1);
+                const int L0 = __shfl_sync(0xffffffffu, len, 0), A0 = __shfl_sync(0xffffffffu, a, 0);
+                const bool uni = L0 > 0 && __all_sync(0xffffffffu, lane >= nrows || (len == L0 && a == A0));
+                const float invL = uni ? 1.0f / float(L0) : 0.f;
                 for (int e0 = 0; e0 < total; e0 += 32) {
                     const int q = e0 + lane;
-                    int j = 0;
+                    uint32_t t;
+                    if (uni) {
+                        int j = int((float(q) + 0.5f) * invL);
+                        j -= j * L0 > q;
+                        j += (j + 1) * L0 <= q;
+                        t = uint32_t(ty0 + j) * cam.ntx + uint32_t(A0 + (q - j * L0));
+                    } else {
+                        int j = 0;
 #pragma unroll
-                    for (int step = 16; step > 0; step >>= 1)
-                        if (__shfl_sync(0xffffffffu, incl, j + step - 1) <= q) j += step;
-                    const int lj = __shfl_sync(0xffffffffu, len, j), aj = __shfl_sync(0xffffffffu, a, j);
-                    const int ij = __shfl_sync(0xffffffffu, incl, j);
-                    const uint32_t t = uint32_t(ty0 + j) * cam.ntx + aj + (q - (ij - lj));
+                        for (int step = 16; step > 0; step >>= 1)
+                            if (__shfl_sync(0xffffffffu, incl, j + step - 1) <= q) j += step;
+                        const int lj = __shfl_sync(0xffffffffu, len, j), aj = __shfl_sync(0xffffffffu, a, j);
+                        const int ij = __shfl_sync(0xffffffffu, incl, j);
+                        t = uint32_t(ty0 + j) * cam.ntx + aj + (q - (ij - lj));
+                    }
                     if (q < total) {
                         keys[at + q] = ranked_key(fmt, t, e.x, s, v);
                         if (td.hist) atomicAdd(&s_h[0][t & td.m0], 1u);
-                    }
-                    if (td.hist && td.two) {  // high digit: lanes sharing it add once
-                        const uint32_t d1 = q < total ? (t >> td.b0) & td.m1 : 0xffffffffu;
-                        const unsigned pm = __match_any_sync(0xffffffffu, d1);
-                        if (q < total && lane == __ffs(pm) - 1) atomicAdd(&s_h[1][d1], uint32_t(__popc(pm)));
                     }
                 }
                 at += uint64_t(total);
@@ -1062,8 +1079,11 @@ __global__ void __launch_bounds__(256) duplicate_big_ranked_kernel(
                 const int aj = __shfl_sync(0xffffffffu, a, j);
                 const uint64_t ro = at + uint64_t(__shfl_sync(0xffffffffu, incl, j) - l);
                 const uint64_t trow = uint64_t(ty0 + j) * cam.ntx;
-                if (aj >= 0) {
-                    for (int c = lane; c < l; c += 32) keys[ro + c] = ranked_key(fmt, trow + aj + c, e.x, s, v);
+                if (aj >= 0) {  // (the row's high digit was counted by its lane above)
+                    for (int c = lane; c < l; c += 32) {
+                        keys[ro + c] = ranked_key(fmt, trow + aj + c, e.x, s, v);
+                        if (td.hist) atomicAdd(&s_h[0][uint32_t(trow + aj + c) & td.m0], 1u);
+                    }
                 } else {
                     uint64_t w = ro;
                     for (int tx0 = rc.x; tx0 <= rc.y; tx0 += 32) {
