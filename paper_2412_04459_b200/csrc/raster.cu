@@ -992,9 +992,15 @@ __global__ void __launch_bounds__(256) duplicate_big_ranked_kernel(
     const unsigned int* __restrict__ n_big, TileDigits td) {
     pdl_enter();
     __shared__ uint32_t s_h[2][256];
+    // low digit of one-run rows as range increments: a difference array over
+    // the 2^b0 bins plus a count of whole periods (added to every bin)
+    __shared__ int s_d0[257];
+    __shared__ uint32_t s_all0, s_wsum[8];
     if (td.hist) {
         s_h[0][threadIdx.x] = 0;
         s_h[1][threadIdx.x] = 0;
+        s_d0[threadIdx.x] = 0;
+        if (threadIdx.x == 0) s_d0[256] = 0, s_all0 = 0;
         __syncthreads();
     }
     const int lane = threadIdx.x & 31;
@@ -1029,14 +1035,28 @@ __global__ void __launch_bounds__(256) duplicate_big_ranked_kernel(
                 if (lane >= o) incl += y;
             }
             const int total = __shfl_sync(0xffffffffu, incl, 31);
-            if (td.hist && td.two && a >= 0 && len > 0) {
-                // high digit of a one-run row: one add per 2^b0-aligned segment
-                const uint32_t t1 = uint32_t(ty) * cam.ntx + uint32_t(a + len - 1);
-                for (uint32_t t = uint32_t(ty) * cam.ntx + uint32_t(a); t <= t1;) {
-                    const uint32_t seg_end = min(t1, (((t >> td.b0) + 1) << td.b0) - 1);
-                    atomicAdd(&s_h[1][(t >> td.b0) & td.m1], seg_end - t + 1);
-                    t = seg_end + 1;
+            if (td.hist && a >= 0 && len > 0) {
+                const uint32_t t0 = uint32_t(ty) * cam.ntx + uint32_t(a), t1 = t0 + uint32_t(len) - 1;
+                // low digit: the row's bins t0 .. t1 (mod 2^b0) as range increments
+                const uint32_t P = td.m0 + 1, full = uint32_t(len) >> td.b0, rem = uint32_t(len) & td.m0;
+                const uint32_t st = t0 & td.m0;
+                if (full) atomicAdd(&s_all0, full);
+                if (rem) {
+                    atomicAdd(&s_d0[st], 1);
+                    if (st + rem <= P) {
+                        atomicAdd(&s_d0[st + rem], -1);
+                    } else {
+                        atomicAdd(&s_d0[0], 1);
+                        atomicAdd(&s_d0[st + rem - P], -1);
+                    }
                 }
+                // high digit: one add per 2^b0-aligned segment
+                if (td.two)
+                    for (uint32_t t = t0; t <= t1;) {
+                        const uint32_t seg_end = min(t1, (((t >> td.b0) + 1) << td.b0) - 1);
+                        atomicAdd(&s_h[1][(t >> td.b0) & td.m1], seg_end - t + 1);
+                        t = seg_end + 1;
+                    }
             }
             if (!__any_sync(0xffffffffu, a < 0 && len > 0)) {
                 // every row one run: the group's entries as one flat range.
@@ -1064,10 +1084,7 @@ __global__ void __launch_bounds__(256) duplicate_big_ranked_kernel(
                         const int ij = __shfl_sync(0xffffffffu, incl, j);
                         t = uint32_t(ty0 + j) * cam.ntx + aj + (q - (ij - lj));
                     }
-                    if (q < total) {
-                        keys[at + q] = ranked_key(fmt, t, e.x, s, v);
-                        if (td.hist) atomicAdd(&s_h[0][t & td.m0], 1u);
-                    }
+                    if (q < total) keys[at + q] = ranked_key(fmt, t, e.x, s, v);
                 }
                 at += uint64_t(total);
                 continue;
@@ -1079,11 +1096,8 @@ __global__ void __launch_bounds__(256) duplicate_big_ranked_kernel(
                 const int aj = __shfl_sync(0xffffffffu, a, j);
                 const uint64_t ro = at + uint64_t(__shfl_sync(0xffffffffu, incl, j) - l);
                 const uint64_t trow = uint64_t(ty0 + j) * cam.ntx;
-                if (aj >= 0) {  // (the row's high digit was counted by its lane above)
-                    for (int c = lane; c < l; c += 32) {
-                        keys[ro + c] = ranked_key(fmt, trow + aj + c, e.x, s, v);
-                        if (td.hist) atomicAdd(&s_h[0][uint32_t(trow + aj + c) & td.m0], 1u);
-                    }
+                if (aj >= 0) {  // (the row's digits were counted by its lane above)
+                    for (int c = lane; c < l; c += 32) keys[ro + c] = ranked_key(fmt, trow + aj + c, e.x, s, v);
                 } else {
                     uint64_t w = ro;
                     for (int tx0 = rc.x; tx0 <= rc.y; tx0 += 32) {
@@ -1107,7 +1121,19 @@ __global__ void __launch_bounds__(256) duplicate_big_ranked_kernel(
     }
     if (td.hist) {
         __syncthreads();
-        if (s_h[0][threadIdx.x]) atomicAdd(td.hist + threadIdx.x, s_h[0][threadIdx.x]);
+        // low digit: inclusive scan of the difference array (block scan), plus
+        // the whole periods and the per-entry counts of the non-run rows
+        int x = s_d0[threadIdx.x];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_wsum[threadIdx.x >> 5] = uint32_t(x);
+        __syncthreads();
+        for (int w = 0; w < int(threadIdx.x >> 5); ++w) x += int(s_wsum[w]);
+        const uint32_t c0 = threadIdx.x <= td.m0 ? s_h[0][threadIdx.x] + uint32_t(x) + s_all0 : 0u;
+        if (c0) atomicAdd(td.hist + threadIdx.x, c0);
         if (s_h[1][threadIdx.x]) atomicAdd(td.hist + 256 + threadIdx.x, s_h[1][threadIdx.x]);
     }
 }
