@@ -1,6 +1,7 @@
 """Per-stage device time (CUDA events on the library stream) of a workload,
 for A/B runs of build/env variants on the GPU box (never a bench number):
-    python tools/ab_stage.py cfg2|cfg4|cfg3 [frames]"""
+    python tools/ab_stage.py cfg2|cfg4|cfg3|cfg5 [frames]
+(cfg5: one 1024^2 training view of the cfg4 scene per frame)"""
 import os
 import sys
 import time
@@ -13,7 +14,7 @@ import paper_2412_04459_b200 as svr  # noqa: E402
 wl = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 ctx = svr.Context(0)
-if wl == "cfg4":
+if wl in ("cfg4", "cfg5"):
     a = svr.synth_unbounded_scene([svr.ring_camera(8, i, 1024, 1024) for i in range(8)], 7, 5, 2.8, seed=7)
     cams = [svr.ring_camera(256, v, 1024, 1024, 1.0) for v in range(int(os.environ.get("AB_VIEWS", "4")))]
 else:
@@ -22,11 +23,12 @@ else:
     cams = [svr.ring_camera(256, v, res, res, 1.3) for v in range(8)]
 scene = svr.Scene(ctx, a)
 f = svr.Frame(ctx)
-train = wl == "cfg3"
+train = wl in ("cfg3", "cfg5")
 opts = svr.RenderOptions(supersample=1.0, training=train)
 if train:
     import torch
-    gt = torch.rand(800, 800, 3, device="cuda")
+    R = cams[0].height
+    gt = torch.rand(R, R, 3, device="cuda")
     gd = torch.zeros(a.n_pool, device="cuda")
     gs = torch.zeros(a.n_voxels * a.sh_stride, device="cuda")
     gp = torch.zeros(a.n_voxels, device="cuda")
