@@ -1959,6 +1959,10 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
 // CTAs per SM the register allocation targets: 4 for the plain render (63
 // registers; 3 with 75 is 3 % slower), 3 for the recording modes, whose
 // extra state spills otherwise (config 3 staged render 316 -> 296 us).
+#ifndef SVR_COOP_MINB0
+#define SVR_COOP_MINB0 4  // CTAs per SM of the cooperative plain render
+#endif
+#define SVR_COOP_MINB(MODE) ((MODE) == 0 ? SVR_COOP_MINB0 : 3)
 #ifndef SVR_COMP_MINB
 #define SVR_COMP_MINB(MODE) ((MODE) == 0 ? 4 : 3)
 #endif
@@ -1976,7 +1980,7 @@ __global__ void __launch_bounds__(256, SVR_COMP_MINB(MODE)) composite_kernel(Dev
 }
 
 template <int K, int MODE>
-__global__ void __launch_bounds__(256, SVR_COMP_MINB(MODE)) composite_coop_kernel(DevCamera cam, CompositeArgs a) {
+__global__ void __launch_bounds__(256, SVR_COOP_MINB(MODE)) composite_coop_kernel(DevCamera cam, CompositeArgs a) {
     pdl_enter();
     extern __shared__ float4 s_rec_dyn[];
     __shared__ CompShared<K, MODE> sh;
