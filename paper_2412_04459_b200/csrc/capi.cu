@@ -420,9 +420,21 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
     mark(ctx, kStageScan);
     if (ranked_ok) {
         pc = grow<uint32_t>(f->pair_counts, 8 * N);
+#ifndef SVR_PAIR_ATOMIC_SUMS
+#define SVR_PAIR_ATOMIC_SUMS 1
+#endif
+        // Large scenes (N >= 2^22): K4a accumulates the scan's block sums
+        // itself (warp-combined atomics), so only the block-sum scan remains
+        // instead of a reduce pass over all 8N counts (config 4: 250 MB, the
+        // scan stage 181 -> 149 us). At config-2 sizes the reduce pass is
+        // cheaper than the per-pair match + atomic (38 vs 44 us).
+        const bool atomic_sums = SVR_PAIR_ATOMIC_SUMS && N >= (uint64_t(1) << 22);
         launch_pair_counts(cam, N, pa.counts, pa.rects, sat, status, scene->morton_rank.as<uint32_t>(), pc,
-                           st, huge);
-        scan_block_prefixes(pc, 8 * N, &status->n_entries, pair_partial, st);
+                           atomic_sums ? pair_partial : nullptr, st, huge);
+        if (atomic_sums)
+            scan_block_sums(pair_partial, (8 * N + kScanChunk - 1) / kScanChunk, &status->n_entries, st);
+        else
+            scan_block_prefixes(pc, 8 * N, &status->n_entries, pair_partial, st);
     }
     if (!ranked_ok || ctx->debug)
         exclusive_scan_u32(pa.counts, offsets, N, ranked_ok ? &status->n_entries_voxel : &status->n_entries,

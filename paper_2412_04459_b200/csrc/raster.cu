@@ -463,7 +463,8 @@ __device__ __forceinline__ uint64_t ranked_key(PackedFormat fmt, uint64_t tid, u
 __global__ void __launch_bounds__(256) pair_counts_kernel(
     DevCamera cam, uint64_t n, const uint32_t* __restrict__ counts, const int4* __restrict__ rects,
     const uint32_t* __restrict__ sat, FrameStatus* __restrict__ status,
-    const uint32_t* __restrict__ rank, uint32_t* __restrict__ pc, HugePairs huge) {
+    const uint32_t* __restrict__ rank, uint32_t* __restrict__ pc, uint32_t* __restrict__ block_sums,
+    HugePairs huge) {
     pdl_enter();
     const uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (v >= n || counts[v] == 0) return;
@@ -486,6 +487,14 @@ __global__ void __launch_bounds__(256) pair_counts_kernel(
             }
         }
         pc[rk] = c;
+        if (block_sums) {
+            // the scan's block sums directly (no reduce pass over the 8n
+            // counts): lanes adding to the same rank block combine first
+            const uint32_t blk = rk / kScanChunk;
+            const unsigned peers = __match_any_sync(__activemask(), blk);
+            const uint32_t sum = __reduce_add_sync(peers, c);
+            if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(block_sums + blk, sum);
+        }
     }
 }
 
@@ -2188,15 +2197,17 @@ void launch_duplicate_packed(const DevCamera& cam, uint64_t n, const uint64_t* p
 
 void launch_pair_counts(const DevCamera& cam, uint64_t n, const uint32_t* counts, const int4* rects,
                         const uint32_t* sat, FrameStatus* status, const uint32_t* rank,
-                        uint32_t* pc, cudaStream_t st, const HugePairs& huge) {
+                        uint32_t* pc, uint32_t* block_sums, cudaStream_t st, const HugePairs& huge) {
     if (n == 0) return;
     SVR_CUDA(cudaMemsetAsync(pc, 0, 8 * n * sizeof(uint32_t), st));
+    if (block_sums)
+        SVR_CUDA(cudaMemsetAsync(block_sums, 0, (8 * n + kScanChunk - 1) / kScanChunk * sizeof(uint32_t), st));
     if (huge.divert && huge.cap) {  // padding sorts last by rank and by pattern
         SVR_CUDA(cudaMemsetAsync(huge.keys, 0xff, size_t(huge.cap) * 8, st));
         SVR_CUDA(cudaMemsetAsync(huge.vals, 0xff, size_t(huge.cap) * 4, st));
     }
     launch_pdl(pair_counts_kernel, blocks_for(n, 256), 256, 0, st, cam, n, counts, rects, sat, status, rank,
-               pc, huge);
+               pc, block_sums, huge);
     SVR_LAUNCH("pair_counts_kernel");
 }
 

@@ -140,6 +140,15 @@ void scan_block_prefixes(const uint32_t* in, uint64_t n, unsigned long long* tot
     SVR_LAUNCH("scan_partials_kernel");
 }
 
+void scan_block_sums(uint32_t* partial, uint64_t nb, unsigned long long* total, cudaStream_t st) {
+    if (nb == 0) {
+        SVR_CUDA(cudaMemsetAsync(total, 0, sizeof(unsigned long long), st));
+        return;
+    }
+    launch_pdl(scan_partials_kernel, 1, kThreads, 0, st, partial, nb, total);
+    SVR_LAUNCH("scan_partials_kernel");
+}
+
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, unsigned long long* total,
                         void* scratch, cudaStream_t st) {
     if (n == 0) {

@@ -20,6 +20,9 @@ constexpr int kScanThreads = 512;
 constexpr int kScanChunk = 4096;
 void scan_block_prefixes(const uint32_t* in, uint64_t n, unsigned long long* total, void* scratch,
                          cudaStream_t st);
+// The second phase alone, over block sums the caller accumulated (u32
+// partial[b] = sum of block b's inputs): in place to exclusive prefixes.
+void scan_block_sums(uint32_t* partial, uint64_t nb, unsigned long long* total, cudaStream_t st);
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, unsigned long long* total,
                         void* scratch, cudaStream_t st);
 
@@ -165,7 +168,7 @@ void build_morton_rank(const uint64_t* paths, uint64_t n, int lmax, uint32_t* ra
 // 128 entries, emitted cooperatively).
 void launch_pair_counts(const DevCamera& cam, uint64_t n, const uint32_t* counts, const int4* rects,
                         const uint32_t* sat, FrameStatus* status, const uint32_t* rank,
-                        uint32_t* pc, cudaStream_t st, const HugePairs& huge);
+                        uint32_t* pc, uint32_t* block_sums, cudaStream_t st, const HugePairs& huge);
 // The huge-pair merge: tile coverage counts of the (rank-sorted) huge list
 // and the final tile ranges (small + huge per tile, scanned), then per tile
 // the rank-order merge of its small sorted keys with the huge pairs covering
