@@ -1897,8 +1897,11 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
                 while (ball) {
                     const int take = min(32 - nfill, __popc(ball));
                     // the first `take` survivors (entry order) go to group g
-                    uint32_t part = ball;
-                    for (int k = __popc(ball); k > take; --k) part &= ~(1u << (31 - __clz(part)));
+                    const uint32_t part =
+                        take == __popc(ball)
+                            ? ball
+                            : __ballot_sync(0xffffffffu, ((ball >> lane) & 1u) &&
+                                                             __popc(ball & ((1u << lane) - 1u)) < take);
                     ball &= ~part;
                     if ((part >> lane) & 1u) {
                         const int at = nfill + __popc(part & ((1u << lane) - 1u));
