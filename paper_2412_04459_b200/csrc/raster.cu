@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(256) precull_kernel(DevCamera cam, PreprocessA
         const uint64_t path = a.paths[v];
         double center[3], size;
         voxel_geometry(path & kCodeMask48, int(path >> 48), a.bc, a.bsize, center, &size);
-        keep = !surely_culled(cam, center, size, a.near_plane);
+        keep = !surely_culled(cam, center, size, a.near_plane, a.cull);
         if (!keep) {
             a.rects[v] = make_int4(0, -1, 0, -1);
             a.counts[v] = 0u;
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kPreThreads, SVR_PRE_MINB) preprocess_kernel(D
         voxel_geometry(path & kCodeMask48, int(path >> 48), a.bc, a.bsize, center, &size);
         Projection pr;
         bool vis = false;
-        if (!a.n_order && surely_culled(cam, center, size, a.near_plane)) {
+        if (!a.n_order && surely_culled(cam, center, size, a.near_plane, a.cull)) {
             pr.tx0 = pr.ty0 = 0;  // a fresh PreVoxel, as project_voxel leaves a culled one
             pr.tx1 = pr.ty1 = -1;
             pr.x0 = pr.x1 = pr.y0 = pr.y1 = 0.0;
@@ -2146,8 +2146,10 @@ void launch_tile_masks_only(const DevCamera& cam, uint8_t* masks, cudaStream_t s
     SVR_LAUNCH("tile_masks_kernel");
 }
 
-void launch_preprocess(const DevCamera& cam, const PreprocessArgs& a, cudaStream_t st) {
-    if (a.n == 0) return;
+void launch_preprocess(const DevCamera& cam, const PreprocessArgs& args, cudaStream_t st) {
+    if (args.n == 0) return;
+    PreprocessArgs a = args;
+    a.cull = cull_norms(cam);
     const size_t smem = a.order ? 0 : size_t(kPreThreads) * kRecordF4 * 16;
     if (a.n_order) {  // worklist mode: a.order is filled by the pre-cull pass
         launch_pdl(precull_kernel, blocks_for(a.n, 256), 256, 0, st, cam, a, const_cast<uint32_t*>(a.order),

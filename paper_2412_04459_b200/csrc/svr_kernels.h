@@ -127,6 +127,7 @@ struct PreprocessArgs {
     const unsigned int* n_order;  // with order: its live length on the device (zeroed by the caller)
     uint32_t* vis_list;           // optional: visible voxels appended here (n_vis_list counts them)
     unsigned int* n_vis_list;
+    CullNorms cull;               // set by launch_preprocess (cull_norms of the camera)
 };
 void launch_preprocess(const DevCamera& cam, const PreprocessArgs& a, cudaStream_t st);
 

@@ -147,17 +147,31 @@ SVR_HD int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v
 
 // to_voxel_index (octree.hpp:68-82) + voxel_geometry (octree.hpp:85-90).
 // Levels/paths are validated once at upload, so no checks here.
+// Every third bit of x (bits 0, 3, ..., 27) packed into bits 0..9.
+SVR_HD uint32_t compact_by_3(uint32_t x) {
+    x &= 0x09249249u;
+    x = (x | (x >> 2)) & 0x030C30C3u;
+    x = (x | (x >> 4)) & 0x0300F00Fu;
+    x = (x | (x >> 8)) & 0x030000FFu;
+    return (x | (x >> 16)) & 0x000003FFu;
+}
 SVR_HD void voxel_geometry(uint64_t code, int level, const double* bc, double bsize,
                            double* center, double* size) {
-    uint64_t c = code >> (3 * (kMaxLevel - level));
-    uint32_t i = 0, j = 0, k = 0;
-    for (int n = 0; n < level; ++n) {
-        i |= uint32_t((c >> 2) & 1) << n;
-        j |= uint32_t((c >> 1) & 1) << n;
-        k |= uint32_t(c & 1) << n;
-        c >>= 3;
-    }
-    double s = ldexp(bsize, -level);
+    // the path's level digits (i, j, k bits of level n at 3n+2, 3n+1, 3n),
+    // de-interleaved with shift-mask steps on two 32-bit halves (10 + 6
+    // levels) instead of a loop over the levels
+    const uint64_t c = code >> (3 * (kMaxLevel - level));
+    const uint32_t lo = uint32_t(c) & 0x3FFFFFFFu, hi = uint32_t(c >> 30);
+    const uint32_t i = compact_by_3(lo >> 2) | (compact_by_3(hi >> 2) << 10);
+    const uint32_t j = compact_by_3(lo >> 1) | (compact_by_3(hi >> 1) << 10);
+    const uint32_t k = compact_by_3(lo) | (compact_by_3(hi) << 10);
+    // bsize * 2^-level: a power-of-two scale is exact, as ldexp is
+    double s;
+#if defined(__CUDA_ARCH__)
+    s = dmul(bsize, __longlong_as_double(int64_t(1023 - level) << 52));
+#else
+    s = ldexp(bsize, -level);
+#endif
     double half_root = dmul(0.5, bsize);
     center[0] = dadd(dsub(bc[0], half_root), dmul(s, dadd(double(i), 0.5)));
     center[1] = dadd(dsub(bc[1], half_root), dmul(s, dadd(double(j), 0.5)));
@@ -246,7 +260,18 @@ SVR_HD float slab_inv(double d) {
 // the near plane, or wholly in front of it and wholly outside one image side
 // widened by a pixel (raster.cpp:104: x1 < 0 || y1 < 0 || x0 > W || y0 > H).
 // Anything else takes the exact fp64 path, so the outputs are unchanged.
-SVR_HD bool surely_culled(const DevCamera& cam, const double* center, double size, double near) {
+// The four side-plane normal lengths of surely_culled (per camera).
+struct CullNorms {
+    float n[4];
+};
+SVR_HD CullNorms cull_norms(const DevCamera& cam) {
+    const float fx = float(cam.fx), fy = float(cam.fy), cx = float(cam.cx), cy = float(cam.cy);
+    const float W = float(cam.W), H = float(cam.H);
+    auto nrm = [](float a, float b) { return sqrtf(a * a + b * b); };
+    return CullNorms{{nrm(fx, cx + 1.f), nrm(-fx, W + 1.f - cx), nrm(fy, cy + 1.f), nrm(-fy, H + 1.f - cy)}};
+}
+SVR_HD bool surely_culled(const DevCamera& cam, const double* center, double size, double near,
+                          const CullNorms& cn) {
     const float c0 = float(center[0] - cam.pos[0]), c1 = float(center[1] - cam.pos[1]),
                 c2 = float(center[2] - cam.pos[2]);
     const float px = float(cam.rot[0]) * c0 + float(cam.rot[3]) * c1 + float(cam.rot[6]) * c2;
@@ -259,16 +284,16 @@ SVR_HD bool surely_culled(const DevCamera& cam, const double* center, double siz
     if (pz - r <= nr + 1e-5f * fabsf(nr)) return false;  // may straddle: whole-image AABB
     // every corner in front: the sphere outside a side plane through the eye
     // (a * q + b * z < 0 over the whole sphere)
-    auto outside = [&](float a, float b, float q) {
+    auto outside = [&](float a, float b, float q, float nab) {  // nab = |(a, b)|
         const float d = a * q + b * pz;
-        return d + r * sqrtf(a * a + b * b) + 1e-5f * (fabsf(a * q) + fabsf(b * pz)) < 0.f;
+        return d + r * nab + 1e-5f * (fabsf(a * q) + fabsf(b * pz)) < 0.f;
     };
     const float fx = float(cam.fx), fy = float(cam.fy), cx = float(cam.cx), cy = float(cam.cy);
     const float W = float(cam.W), H = float(cam.H);
-    return outside(fx, cx + 1.f, px) ||              // every u < -1
-           outside(-fx, W + 1.f - cx, px) ||         // every u > W + 1
-           outside(fy, cy + 1.f, py) ||              // every v < -1
-           outside(-fy, H + 1.f - cy, py);           // every v > H + 1
+    return outside(fx, cx + 1.f, px, cn.n[0]) ||              // every u < -1
+           outside(-fx, W + 1.f - cx, px, cn.n[1]) ||         // every u > W + 1
+           outside(fy, cy + 1.f, py, cn.n[2]) ||              // every v < -1
+           outside(-fy, H + 1.f - cy, py, cn.n[3]);           // every v > H + 1
 }
 
 // True iff no pixel ray of the image can enter the box at t > 0: all eight
