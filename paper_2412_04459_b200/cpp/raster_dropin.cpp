@@ -121,26 +121,25 @@ svr_render_options to_c(const RenderOptions& o) {
 }
 
 // ---- content fingerprints -------------------------------------------------
-// Four independent multiply-rotate lanes over 64-bit words (enough ILP to run
-// at memory speed), combined in order; ranges of large arrays are hashed on
-// all host cores and their digests folded left to right, so the value only
+// Eight independent xor-rotate-multiply lanes over 64-bit words (one
+// multiply per word, enough ILP to run at memory speed; each lane is order
+// sensitive), combined in order; ranges of large arrays are hashed on all
+// host cores and their digests folded left to right, so the value only
 // depends on the content.
 constexpr uint64_t kM1 = 0x9e3779b185ebca87ull, kM2 = 0xc2b2ae3d27d4eb4full,
                    kM3 = 0x165667b19e3779f9ull;
 inline uint64_t rotl(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
-inline uint64_t lane(uint64_t acc, uint64_t w) { return rotl(acc + w * kM2, 31) * kM1; }
-inline uint64_t fold(uint64_t h, uint64_t v) { return rotl(h ^ lane(0, v), 27) * kM1 + kM3; }
+inline uint64_t lane(uint64_t acc, uint64_t w) { return rotl(acc ^ w, 29) * kM1; }
+inline uint64_t fold(uint64_t h, uint64_t v) { return rotl(h ^ (rotl(v * kM2, 31) * kM1), 27) * kM1 + kM3; }
 
 uint64_t hash_words(const uint64_t* w, size_t n, uint64_t seed) {
-    uint64_t a = seed + kM1 + kM2, b = seed + kM2, c = seed, d = seed - kM1;
+    uint64_t x[8];
+    for (int l = 0; l < 8; ++l) x[l] = seed + kM2 * uint64_t(l + 1);
     size_t i = 0;
-    for (; i + 4 <= n; i += 4) {
-        a = lane(a, w[i]);
-        b = lane(b, w[i + 1]);
-        c = lane(c, w[i + 2]);
-        d = lane(d, w[i + 3]);
-    }
-    uint64_t h = rotl(a, 1) + rotl(b, 7) + rotl(c, 12) + rotl(d, 18);
+    for (; i + 8 <= n; i += 8)
+        for (int l = 0; l < 8; ++l) x[l] = lane(x[l], w[i + l]);
+    uint64_t h = seed ^ kM3;
+    for (int l = 0; l < 8; ++l) h = fold(h, x[l]);
     for (; i < n; ++i) h = fold(h, w[i]);
     return fold(h, n);
 }
@@ -446,6 +445,13 @@ void download_images(svr_frame* f, std::vector<ImageReq> reqs, double far) {
             check(svr_frame_download_async(f, r.which, buf + off, n * 4));
             off += n;
         }
+        // the Images (value-initialised, i.e. zero-filled by their
+        // constructor) are built on the pool, one per thread, while the
+        // copies are in flight
+        if (reqs.size() > 1 && total >= (size_t(1) << 18))
+            Pool::get().run(reqs.size(), [&](size_t i) { *reqs[i].img = Image(reqs[i].w, reqs[i].h, reqs[i].ch); });
+        else
+            for (const ImageReq& r : reqs) *r.img = Image(r.w, r.h, r.ch);
         check(svr_frame_wait(f));
     }
     Phase ph{4};
@@ -453,7 +459,6 @@ void download_images(svr_frame* f, std::vector<ImageReq> reqs, double far) {
     const float ffar = float(far);
     for (const ImageReq& r : reqs) {
         const size_t n = size_t(r.w) * r.h * r.ch;
-        *r.img = Image(r.w, r.h, r.ch);
         double* dst = r.img->data.data();
         const float* src = buf + off;
         const bool sent = r.sentinel;
