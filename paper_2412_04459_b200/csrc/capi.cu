@@ -428,7 +428,9 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
         // instead of a reduce pass over all 8N counts (config 4: 250 MB, the
         // scan stage 181 -> 149 us). At config-2 sizes the reduce pass is
         // cheaper than the per-pair match + atomic (38 vs 44 us).
-        const bool atomic_sums = SVR_PAIR_ATOMIC_SUMS && N >= (uint64_t(1) << 22);
+        const char* pa_env = std::getenv("SVR_PAIR_ATOMIC_MIN");  // parity tests lower it
+        const bool atomic_sums =
+            SVR_PAIR_ATOMIC_SUMS && N >= (pa_env ? std::strtoull(pa_env, nullptr, 10) : (uint64_t(1) << 22));
         launch_pair_counts(cam, N, pa.counts, pa.rects, sat, status, scene->morton_rank.as<uint32_t>(), pc,
                            atomic_sums ? pair_partial : nullptr, st, huge);
         if (atomic_sums)

@@ -193,6 +193,30 @@ def test_fused_digit_histograms_bit_exact(svr, ctx, ref, cfg1, monkeypatch, fuse
     assert np.array_equal(f.download("SORT_VALUES", np.uint32), vs_ref)
 
 
+@pytest.mark.parametrize("atomic", ["0", "1"])
+def test_pair_count_block_sums_bit_exact(svr, ref, cfg1, monkeypatch, atomic):
+    """The rank-ordered scan's block sums taken by K4a's warp-combined atomics
+    (large scenes, forced here) or by the reduce pass: same sorted values and
+    ranges as the reference, in a production (non-debug) context."""
+    monkeypatch.setenv("SVR_PAIR_ATOMIC_MIN", "0" if atomic == "1" else str(1 << 62))
+    arrays, _, rscene = cfg1
+    pctx = svr.Context(0)
+    scene = svr.Scene(pctx, arrays)
+    for cam in [svr.ring_camera(3, 1, 320, 192), svr.Camera(160, 128, 50.0, 50.0, 80.5, 64.5, np.eye(3),
+                                                             np.array([0.0, 0.0, 0.0]))]:
+        f = svr.Frame(pctx)
+        svr.render_into(f, scene, cam, svr.RenderOptions(supersample=1.0))
+        ks_ref, vs_ref = ref.ref_entries(rscene, cam, sorted_=True)
+        assert f.info().n_entries == vs_ref.size
+        assert np.array_equal(f.download("SORT_VALUES", np.uint32), vs_ref)
+        ranges = f.download("TILE_RANGES", np.uint32, (-1, 2))
+        tiles = (ks_ref >> np.uint64(48)).astype(np.int64)
+        t = np.arange(ranges.shape[0])
+        lo, hi = np.searchsorted(tiles, t, "left"), np.searchsorted(tiles, t, "right")
+        ne = hi > lo
+        assert np.array_equal(ranges[ne, 0], lo[ne]) and np.array_equal(ranges[ne, 1], hi[ne])
+
+
 @pytest.mark.parametrize("ranked", ["1", "0"])
 def test_emission_paths_bit_exact(svr, ctx, ref, cfg1, monkeypatch, ranked):
     """Rank-ordered emission (keys pre-sorted below the tile bits, tile-only
