@@ -122,7 +122,10 @@ typedef enum svr_buffer {
     SVR_BUF_PIX_COUNT = 17,    /* sw*sh u32 (training)                   */
     SVR_BUF_PIX_BEGIN = 18,    /* sw*sh u32 (training)                   */
     SVR_BUF_VOXEL_COLOR = 19,  /* n_voxels*3 f32 (visible voxels only)   */
-    SVR_BUF_VOXEL_NORMAL = 20  /* n_voxels*3 f32 (visible voxels only)   */
+    SVR_BUF_VOXEL_NORMAL = 20, /* n_voxels*3 f32 (visible voxels only)   */
+    SVR_BUF_OUTPUTS = 21       /* W*H*9 f32: the five images above, contiguous
+                                * in id order (COLOR, DEPTH, MEDIAN_DEPTH,
+                                * NORMAL, TRANSMITTANCE): one copy per frame */
 } svr_buffer;
 
 /* ---- context ---------------------------------------------------------- */

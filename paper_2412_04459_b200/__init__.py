@@ -109,7 +109,7 @@ class svr_gradients(C.Structure):
 BUF = dict(COLOR=0, DEPTH=1, MEDIAN_DEPTH=2, NORMAL=3, TRANSMITTANCE=4, MAX_BLEND=5,
            SS_COLOR=6, SS_DEPTH=7, SS_TFIN=8, SORT_KEYS=9, SORT_VALUES=10, TILE_RANGES=11,
            TILE_MASKS=12, VOXEL_RECTS=13, VOXEL_AABB=14, ENTRIES_KEYS=15, ENTRIES_VALUES=16,
-           PIX_COUNT=17, PIX_BEGIN=18)
+           PIX_COUNT=17, PIX_BEGIN=18, VOXEL_COLOR=19, VOXEL_NORMAL=20, OUTPUTS=21)
 
 # exported symbols of include/svr_b200.h (checked by the CPU test-suite)
 EXPORTS = [

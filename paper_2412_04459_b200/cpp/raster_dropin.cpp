@@ -439,11 +439,19 @@ void download_images(svr_frame* f, std::vector<ImageReq> reqs, double far) {
     float* buf = stage.reserve(std::max<size_t>(total, 1) * 4);
     {
         Phase ph{3};
-        size_t off = 0;
-        for (const ImageReq& r : reqs) {
-            const size_t n = size_t(r.w) * r.h * r.ch;
-            check(svr_frame_download_async(f, r.which, buf + off, n * 4));
-            off += n;
+        // the five render outputs in id order are one contiguous device
+        // block (SVR_BUF_OUTPUTS): one copy instead of five
+        bool all5 = reqs.size() == 5;
+        for (size_t i = 0; all5 && i < 5; ++i) all5 = reqs[i].which == svr_buffer(i);
+        if (all5) {
+            check(svr_frame_download_async(f, SVR_BUF_OUTPUTS, buf, total * 4));
+        } else {
+            size_t off = 0;
+            for (const ImageReq& r : reqs) {
+                const size_t n = size_t(r.w) * r.h * r.ch;
+                check(svr_frame_download_async(f, r.which, buf + off, n * 4));
+                off += n;
+            }
         }
         // the Images (value-initialised, i.e. zero-filled by their
         // constructor) are built on the pool, one per thread, while the

@@ -633,11 +633,9 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
 
     // output buffers
     const uint64_t npx = uint64_t(W) * H, nss = uint64_t(sw) * sh;
-    float* oc = grow<float>(f->out_color, npx * 3);
-    float* od = grow<float>(f->out_depth, npx);
-    float* om = grow<float>(f->out_median, npx);
-    float* on = grow<float>(f->out_normal, npx * 3);
-    float* ot = grow<float>(f->out_tfin, npx);
+    f->alloc_outputs(npx);
+    float *oc = f->out_color, *od = f->out_depth, *om = f->out_median, *on = f->out_normal,
+          *ot = f->out_tfin;
     CompositeArgs ca{};
     ca.ranges = ranges;
     ca.tile_order = torder;
@@ -791,7 +789,7 @@ BufView frame_buffer(svr_frame* f, svr_buffer which) {
     const uint64_t ntiles = uint64_t(f->ntx) * f->nty;
     switch (which) {  // materialised buffers reuse scratch an async copy may still read
         case SVR_BUF_COLOR: case SVR_BUF_DEPTH: case SVR_BUF_MEDIAN_DEPTH: case SVR_BUF_NORMAL:
-        case SVR_BUF_TRANSMITTANCE: case SVR_BUF_MAX_BLEND: case SVR_BUF_SS_COLOR:
+        case SVR_BUF_TRANSMITTANCE: case SVR_BUF_OUTPUTS: case SVR_BUF_MAX_BLEND: case SVR_BUF_SS_COLOR:
         case SVR_BUF_SS_DEPTH: case SVR_BUF_SS_TFIN: case SVR_BUF_TILE_RANGES:
         case SVR_BUF_TILE_MASKS: case SVR_BUF_VOXEL_RECTS: break;
         default:
@@ -799,17 +797,18 @@ BufView frame_buffer(svr_frame* f, svr_buffer which) {
             resolve_frame(f);  // these need the entry count
     }
     switch (which) {
-        case SVR_BUF_COLOR: return {f->out_color.p, npx * 12};
-        case SVR_BUF_DEPTH: return {f->out_depth.p, npx * 4};
-        case SVR_BUF_MEDIAN_DEPTH: return {f->out_median.p, npx * 4};
-        case SVR_BUF_NORMAL: return {f->out_normal.p, npx * 12};
-        case SVR_BUF_TRANSMITTANCE: return {f->out_tfin.p, npx * 4};
+        case SVR_BUF_COLOR: return {f->out_color, npx * 12};
+        case SVR_BUF_DEPTH: return {f->out_depth, npx * 4};
+        case SVR_BUF_MEDIAN_DEPTH: return {f->out_median, npx * 4};
+        case SVR_BUF_NORMAL: return {f->out_normal, npx * 12};
+        case SVR_BUF_TRANSMITTANCE: return {f->out_tfin, npx * 4};
+        case SVR_BUF_OUTPUTS: return {f->out_color, npx * 36};
         case SVR_BUF_MAX_BLEND:
             require(f->opts.record_stats, SVR_ERR_INVALID_ARGUMENT, "render without record_stats");
             return {f->max_blend.p, f->n_voxels * 4};
-        case SVR_BUF_SS_COLOR: return {ss1 ? f->out_color.p : f->ss_color.p, nss * 12};
-        case SVR_BUF_SS_DEPTH: return {ss1 ? f->out_depth.p : f->ss_depth.p, nss * 4};
-        case SVR_BUF_SS_TFIN: return {ss1 ? f->out_tfin.p : f->ss_tfin.p, nss * 4};
+        case SVR_BUF_SS_COLOR: return {ss1 ? f->out_color : f->ss_color.p, nss * 12};
+        case SVR_BUF_SS_DEPTH: return {ss1 ? f->out_depth : f->ss_depth.p, nss * 4};
+        case SVR_BUF_SS_TFIN: return {ss1 ? f->out_tfin : f->ss_tfin.p, nss * 4};
         case SVR_BUF_SORT_KEYS:
         case SVR_BUF_SORT_VALUES:
             if (f->packed && (!f->sort_keys_kept || f->huge_used)) {
@@ -1519,7 +1518,7 @@ int svr_l1_loss(svr_ctx* ctx, svr_frame* f, const float* gt, float* d_color, flo
         set_device(ctx);
         wait_copies(f);
         resolve_frame(f);
-        launch_l1_loss(f->out_color.as<float>(), gt, uint64_t(f->W) * f->H * 3, d_color, loss,
+        launch_l1_loss(f->out_color, gt, uint64_t(f->W) * f->H * 3, d_color, loss,
                        ctx->stream);
     });
 }
@@ -1569,7 +1568,7 @@ int svr_ray_losses(svr_ctx* ctx, svr_frame* f, const float* gt, const svr_ray_lo
         ra.contrib_entry = f->staged ? f->stage_entry.as<uint32_t>() : f->contrib_entry.as<uint32_t>();
         ra.contrib_T = f->staged ? f->stage_T.as<float>() : f->contrib_T.as<float>();
         ra.stage_stride = f->staged ? uint32_t(uint64_t(f->ntx) * f->nty * 256) : 0u;
-        ra.tfin = ss1 ? f->out_tfin.as<float>() : f->ss_tfin.as<float>();
+        ra.tfin = ss1 ? f->out_tfin : f->ss_tfin.as<float>();
         ra.gt = dgt;
         ra.gt_w = f->W;
         ra.gt_h = f->H;
@@ -1616,7 +1615,7 @@ int svr_image_losses(svr_ctx* ctx, svr_frame* f, const float* gt, double w_mse, 
         cudaStream_t st = ctx->stream;
         const uint64_t n = uint64_t(f->W) * f->H * 3;
         ImageLossArgs a{};
-        a.a = f->out_color.as<float>();
+        a.a = f->out_color;
         a.W = f->W;
         a.H = f->H;
         // gauss_kernel (losses.cpp:15-29) in double, then narrowed
@@ -1768,7 +1767,7 @@ int svr_train_step_l1(svr_ctx* ctx, const svr_scene* scene, const svr_camera* ca
         render_impl(ctx, scene, cam, &o, f);
         const uint64_t n = uint64_t(f->W) * f->H * 3;
         float* dcol = grow<float>(f->l1_grad, n);
-        launch_l1_loss(f->out_color.as<float>(), gt_device, n, dcol, loss_device, ctx->stream);
+        launch_l1_loss(f->out_color, gt_device, n, dcol, loss_device, ctx->stream);
         svr_upstream up{};
         up.d_color = dcol;
         up.on_device = 1;

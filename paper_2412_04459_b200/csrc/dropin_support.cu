@@ -332,18 +332,14 @@ extern "C" int svr_render_oracle(svr_ctx* ctx, const svr_scene* scene, const svr
             f->has_records = false;
             f->training = false;
             f->n_visible = ~uint64_t(0);
-            f->out_color.reserve(npx * 12);
-            f->out_depth.reserve(npx * 4);
-            f->out_median.reserve(npx * 4);
-            f->out_normal.reserve(npx * 12);
-            f->out_tfin.reserve(npx * 4);
+            f->alloc_outputs(npx);
             f->rects.reserve(std::max<uint64_t>(N, 1) * 16);
             dim3 grid(unsigned((cam.W + 63) / 64), unsigned(cam.H));
             oracle_render_kernel<<<grid, 64, 0, st>>>(
                 cam, vox.as<OracleVoxel>(), cnt.as<unsigned int>(), a.opts->K, a.opts->t_threshold,
                 a.opts->background[0], a.opts->background[1], a.opts->background[2],
-                a.opts->far_sentinel, f->out_color.as<float>(), f->out_depth.as<float>(),
-                f->out_median.as<float>(), f->out_normal.as<float>(), f->out_tfin.as<float>());
+                a.opts->far_sentinel, f->out_color, f->out_depth,
+                f->out_median, f->out_normal, f->out_tfin);
             SVR_LAUNCH("oracle_render_kernel");
             SVR_CUDA(cudaStreamSynchronize(st));
         },

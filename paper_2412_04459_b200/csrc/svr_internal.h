@@ -173,7 +173,20 @@ struct svr_frame {
     svrb::DevBuf vis_list;                         // K1's visible voxels (training frames)
     uint64_t n_vis_list = 0;                       // its length (read with E)
     bool sort_keys_kept = true;  // false: the last sort pass wrote values only
-    svrb::DevBuf out_color, out_depth, out_median, out_normal, out_tfin, max_blend;
+    // the five output images, one allocation in svr_buffer id order (so
+    // SVR_BUF_OUTPUTS reads them back with one copy); set by alloc_outputs
+    svrb::DevBuf out_all, max_blend;
+    float *out_color = nullptr, *out_depth = nullptr, *out_median = nullptr, *out_normal = nullptr,
+          *out_tfin = nullptr;
+    void alloc_outputs(uint64_t npx) {
+        out_all.reserve(npx * 9 * sizeof(float));
+        float* b = out_all.as<float>();
+        out_color = b;
+        out_depth = b + 3 * npx;
+        out_median = b + 4 * npx;
+        out_normal = b + 5 * npx;
+        out_tfin = b + 8 * npx;
+    }
     svrb::DevBuf ss_color, ss_depth, ss_median, ss_normal, ss_tfin;
     svrb::DevBuf pix_count, pix_begin, contrib_entry, contrib_T;
     svrb::DevBuf stage_entry, stage_T;  // single-pass training records

@@ -193,6 +193,24 @@ def test_fused_digit_histograms_bit_exact(svr, ctx, ref, cfg1, monkeypatch, fuse
     assert np.array_equal(f.download("SORT_VALUES", np.uint32), vs_ref)
 
 
+def test_outputs_block_is_the_five_images(svr, ctx, cfg1):
+    """SVR_BUF_OUTPUTS (one read-back per frame) is COLOR | DEPTH |
+    MEDIAN_DEPTH | NORMAL | TRANSMITTANCE, contiguous, bit for bit."""
+    import torch
+    arrays, scene, _ = cfg1
+    cam = svr.ring_camera(3, 1, 96, 80)
+    f = svr.Frame(ctx)
+    svr.render_into(f, scene, cam, svr.RenderOptions(supersample=1.5))
+    parts = [f.download(k, np.float32) for k in ("COLOR", "DEPTH", "MEDIAN_DEPTH", "NORMAL", "TRANSMITTANCE")]
+    block = f.download("OUTPUTS", np.float32)
+    assert block.size == 96 * 80 * 9
+    assert np.array_equal(block.view(np.uint32), np.concatenate(parts).view(np.uint32))
+    pinned = torch.empty(block.size, dtype=torch.float32, pin_memory=True)
+    f.download_async("OUTPUTS", pinned)
+    f.wait()
+    assert np.array_equal(pinned.numpy().view(np.uint32), block.view(np.uint32))
+
+
 @pytest.mark.parametrize("atomic", ["0", "1"])
 def test_pair_count_block_sums_bit_exact(svr, ref, cfg1, monkeypatch, atomic):
     """The rank-ordered scan's block sums taken by K4a's warp-combined atomics
