@@ -128,7 +128,9 @@ class ShardedTrainer:
         g = svr.svr_gradients()
         g.density, g.sh = self.density_grad.data_ptr(), self.sh_grad.data_ptr()
         g.priority, g.on_device = self.priority.data_ptr(), 1
-        torch.cuda.current_stream().synchronize()
+        # the library stream runs after the caller's pending work (ground
+        # truths, the flat buffer) without a host round trip
+        self.stream.wait_stream(torch.cuda.current_stream())
         if self.comm is not None:  # one C-ABI call: views, loss sum, NCCL all-reduce
             n = len(view_ids)
             cams = (svr.svr_camera * max(n, 1))(*[self.cams[v].to_c() for v in view_ids])
