@@ -635,20 +635,37 @@ def run_ours(args, rank, world, local_rank):
         host_gt = {v: torch.tensor(make_gt(w, v)).pin_memory() for v in step.views}
         tr = step.trainer
 
+        # the loss of step i is copied to pinned host memory behind the step
+        # and read on the host one step later, so the host enqueues step i+1
+        # while step i runs (the serving loop's pipelining, for training)
+        loss_host = [torch.empty(1, dtype=torch.float32, pin_memory=True) for _ in range(2)]
+        loss_ev = [None, None]
+        losses = []
+
         def e2e_step(i):
             ids = step.ids(i)
             with torch.cuda.stream(tr.stream):
                 for k in ids:
                     tr.gts[k].copy_(host_gt[step.views[k]], non_blocking=True)
-            step(i)  # reads the loss back to the host
+            lt = tr.step(ids, lazy=True)
+            with torch.cuda.stream(tr.stream):
+                loss_host[i % 2].copy_(lt, non_blocking=True)
+                loss_ev[i % 2] = torch.cuda.Event()
+                loss_ev[i % 2].record(tr.stream)
+            if i > 0:  # the previous step's loss, read on the host
+                loss_ev[(i - 1) % 2].synchronize()
+                losses.append(float(loss_host[(i - 1) % 2].item()))
 
         def e2e_drain():
-            pass
+            for ev in loss_ev:
+                if ev is not None:
+                    ev.synchronize()
 
         d2h = 4
         h2d = units_per_step * (H * W * 12 + C.sizeof(svr.svr_camera))
         e2e_note = ("scene and gradient buffers resident on device; per step each view's ground "
-                    "truth (pinned host) and camera in, the loss out")
+                    "truth (pinned host) and camera in, the loss out to pinned host memory "
+                    "(read on the host one step later, so step i+1 is enqueued while step i runs)")
     # every rotating frame sizes its buffers for every view of the timed loop
     for i in range(max(args.e2e_steps, 6, args.warmup)):
         e2e_step(i)

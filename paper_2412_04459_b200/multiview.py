@@ -121,7 +121,11 @@ class ShardedTrainer:
         if comm is not None:
             comm.register(self.flat)
 
-    def step(self, view_ids: Sequence[int], reduce: bool = True) -> float:
+    def step(self, view_ids: Sequence[int], reduce: bool = True, lazy: bool = False):
+        """One batch: forward -> L1 -> backward of `view_ids` accumulated into
+        the flat gradient, all-reduced across ranks when `reduce`. Returns the
+        summed loss as a float, or (lazy) as a one-element device tensor the
+        caller reads back when it needs it (pipelined loops)."""
         import torch
         svr = self.svr
         lib = svr.load_library()
@@ -141,7 +145,7 @@ class ShardedTrainer:
                                               self.comm.h if reduce else None,
                                               C.c_void_p(self.loss.data_ptr())))
             torch.cuda.current_stream().wait_stream(self.stream)
-            return float(self.loss.item())
+            return self.loss.clone() if lazy else float(self.loss.item())
         if not view_ids:  # no view on this rank: contribute zeros to the sum
             with torch.cuda.stream(self.stream):
                 self.flat.zero_()
@@ -159,7 +163,7 @@ class ShardedTrainer:
         torch.cuda.current_stream().wait_stream(self.stream)
         if reduce:
             allreduce_flat(self.flat, self.group)
-        return float(loss_t.item())
+        return loss_t if lazy else float(loss_t.item())
 
     def gradients(self) -> dict:
         """The (reduced) gradients of the last step as host float32 arrays."""
