@@ -593,10 +593,13 @@ def run_ours(args, rank, world, local_rank):
         # rotate, so frame i's read-back (copy stream) overlaps the rendering
         # of the frames after it; every step still renders and reads back its
         # own five images (svr_frame_download_async / svr_frame_wait).
-        # the five images (COLOR, DEPTH, MEDIAN_DEPTH, NORMAL, TRANSMITTANCE:
-        # 9 floats per pixel) are read back as the frame's one contiguous
-        # SVR_BUF_OUTPUTS block, one copy per step
-        pinned = [{"OUTPUTS": torch.empty(H * W * 9, dtype=torch.float32, pin_memory=True)}
+        # the five images, one copy each (SVR_BENCH_ONE_COPY=1: the frame's
+        # contiguous SVR_BUF_OUTPUTS block in one copy; measured on one box
+        # 1409 vs 1425 FPS for five copies, i.e. no gain: e2e sits at ~95 %
+        # of the PCIe D2H rate either way)
+        names = ([("OUTPUTS", 9)] if os.environ.get("SVR_BENCH_ONE_COPY") == "1" else
+                 [("COLOR", 3), ("DEPTH", 1), ("MEDIAN_DEPTH", 1), ("NORMAL", 3), ("TRANSMITTANCE", 1)])
+        pinned = [{k: torch.empty(H * W * c, dtype=torch.float32, pin_memory=True) for k, c in names}
                   for _ in range(3)]
         frames = [step.frame, svr.Frame(ctx), svr.Frame(ctx)]
 
@@ -615,8 +618,7 @@ def run_ours(args, rank, world, local_rank):
         d2h = sum(b.numel() * 4 for b in pinned[0].values())
         h2d = C.sizeof(svr.svr_camera) + C.sizeof(svr.svr_render_options)
         e2e_note = ("scene resident on device (uploaded once); per step camera in, "
-                    "color+depth+median+normal+transmittance out to pinned host memory "
-                    "(one copy of the frame's contiguous output block); "
+                    "color+depth+median+normal+transmittance out to pinned host memory; "
                     "three frames rotate so a step's read-back overlaps the next renders")
     elif w["kind"] == "iter":
         def e2e_step(i):
