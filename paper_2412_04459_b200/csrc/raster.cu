@@ -70,11 +70,20 @@ __global__ void __launch_bounds__(1024) tile_setup_kernel(DevCamera cam, uint8_t
         }
     }
     __syncthreads();
-    for (int c = threadIdx.x + 1; c <= ntx; c += blockDim.x) {
-        uint32_t run = 0;
-        for (int r = 1; r <= nty; ++r) {
-            run += t[r * sw + c];
-            t[r * sw + c] = run;
+    // column prefix sums: one warp per column, 32 rows at a time (a column's
+    // cells are sw words apart, sw odd for even ntx: no bank conflicts)
+    for (int c = warp + 1; c <= ntx; c += nwarps) {
+        uint32_t carry = 0;
+        for (int r0 = 1; r0 <= nty; r0 += 32) {
+            const int r = r0 + lane;
+            uint32_t v = r <= nty ? t[r * sw + c] : 0u;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t n = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += n;
+            }
+            if (r <= nty) t[r * sw + c] = v + carry;
+            carry += __shfl_sync(0xffffffffu, v, 31);
         }
     }
     __syncthreads();
@@ -84,17 +93,24 @@ __global__ void __launch_bounds__(1024) tile_setup_kernel(DevCamera cam, uint8_t
     // per-pattern tables: the row span of pattern b-1 (the pattern regions are
     // convex in the image, so a row's tiles with bit s are nearly always one
     // run): {lo, hi}, {1, 0} when empty, {-1, -1} when not one run
+    // one warp per row: ballots over 32 tiles at a time give the first and
+    // last tile holding pattern b-1 and their count
     if (b > 0 && rowspan)
-        for (int ty = threadIdx.x; ty < nty; ty += blockDim.x) {
+        for (int ty = warp; ty < nty; ty += nwarps) {
             int lo = ntx, hi = -1, cnt = 0;
-            for (int tx = 0; tx < ntx; ++tx)
-                if ((masks[ty * ntx + tx] >> (b - 1)) & 1u) {
-                    lo = min(lo, tx);
-                    hi = tx;
-                    ++cnt;
+            for (int tx0 = 0; tx0 < ntx; tx0 += 32) {
+                const int tx = tx0 + lane;
+                const unsigned bal =
+                    __ballot_sync(0xffffffffu, tx < ntx && ((masks[ty * ntx + tx] >> (b - 1)) & 1u));
+                if (bal) {
+                    lo = min(lo, tx0 + __ffs(bal) - 1);
+                    hi = tx0 + 31 - __clz(bal);
+                    cnt += __popc(bal);
                 }
-            rowspan[(b - 1) * nty + ty] = cnt == 0 ? make_int2(1, 0)
-                                          : cnt == hi - lo + 1 ? make_int2(lo, hi) : make_int2(-1, -1);
+            }
+            if (lane == 0)
+                rowspan[(b - 1) * nty + ty] = cnt == 0 ? make_int2(1, 0)
+                                              : cnt == hi - lo + 1 ? make_int2(lo, hi) : make_int2(-1, -1);
         }
 }
 
