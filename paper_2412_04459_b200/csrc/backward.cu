@@ -669,19 +669,61 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
 // lanes 0..7 add the normal chain (field.hpp:158-170) to
 // their corner and issue the voxel's 8 pool atomics. Voxels outside `pre`
 // leave at once (their group only zeroes SH gradients when not accumulating).
+// The loads of one voxel's epilogue, issued together before any use: the
+// kernel is latency-bound (ncu: 20 of 28 cycles per instruction waiting on
+// L1TEX), so every independent load goes out in one round trip instead of
+// rects -> record -> colour -> corner index -> priority in sequence.
+struct EpiLoads {
+    float gvm;      // K9's record, component m
+    float4 d;       // sh_eval direction
+    float4 rgb;     // K1's clamped colour (clamp mask)
+    uint32_t ci;    // corner index m (lanes 0..7)
+    float pr;       // priority (lane 14)
+    float o0, o1, o2;  // SH gradients so far (accumulating backward)
+};
+
+__device__ __forceinline__ EpiLoads epilogue_load(const EpilogueArgs& a, uint64_t v, int m) {
+    const int nb = (a.sh_degree + 1) * (a.sh_degree + 1);
+    EpiLoads L;
+    L.gvm = a.g_vox[16 * v + m];
+    L.d = __ldg(a.view_dir + v);
+    L.rgb = a.sh ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldg(a.records + v * kRecordF4 + 4);
+    L.ci = m < 8 ? __ldg(a.corner_index + 8 * v + m) : 0u;
+    L.pr = m == 14 ? a.g_priority[v] : 0.f;
+    L.o0 = L.o1 = L.o2 = 0.f;
+    if (a.accumulate && m < nb) {
+        const float* o = a.g_sh + v * uint64_t(a.sh_stride) + 3 * m;
+        L.o0 = o[0], L.o1 = o[1], L.o2 = o[2];
+    }
+    return L;
+}
+
+// Corner m's share of the normal chain (field.hpp:158-170; a noinline
+// version measured slower: 167 -> 182 us on config 3).
+__device__ __forceinline__ float normal_chain(const float4* rec, float dn0, float dn1, float dn2, int m) {
+    const float dn[3] = {dn0, dn1, dn2};
+    float V[8];
+    trilinear_corners(rec[2], rec[3], V);
+    float gV[8];
+    voxel_normal_backward(V, dn, gV);
+    float g = 0.f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) g = (m == c) ? gV[c] : g;
+    return g;
+}
+
 // One visible voxel (all 16 lanes of its group present).
-__device__ __forceinline__ void epilogue_visible(const EpilogueArgs& a, uint64_t v, int m, unsigned gmask) {
+__device__ __forceinline__ void epilogue_visible(const EpilogueArgs& a, uint64_t v, int m, unsigned gmask,
+                                                 const EpiLoads& L) {
     const int nb = (a.sh_degree + 1) * (a.sh_degree + 1);
     float* gsh = a.g_sh + v * uint64_t(a.sh_stride);
     // K9's record of this voxel: lane m holds component m (coalesced 64 B);
     // consumed here and left zero for the next backward
-    const float gvm = a.g_vox[16 * v + m];
+    const float gvm = L.gvm;
     // sh_eval direction exactly as K1 used it (raster.cpp:195-196): the
     // forward colour and this clamp mask see identical floats
-    const float4 d = __ldg(a.view_dir + v);
-    const float ux = d.x, uy = d.y, uz = d.z;
     float b[16] = {};  // lanes m >= (d+1)^2 read zeros, not stale registers
-    sh_basis(a.sh_degree, ux, uy, uz, b);
+    sh_basis(a.sh_degree, L.d.x, L.d.y, L.d.z, b);
     float bm = 0.f;
 #pragma unroll
     for (int i = 0; i < 16; ++i) bm = (m == i) ? b[i] : bm;
@@ -690,10 +732,8 @@ __device__ __forceinline__ void epilogue_visible(const EpilogueArgs& a, uint64_t
     // one sector for the 16 lanes) instead of re-evaluating the SH sum from
     // the coefficients (192 B per voxel), and exactly the clamp the forward
     // applied.
-    float4 rgb;
-    if (!a.sh) {
-        rgb = __ldg(a.records + v * kRecordF4 + 4);
-    } else {
+    float4 rgb = L.rgb;
+    if (a.sh) {
         // the pools changed since the forward (svr_scene_set_params): the
         // reference's mask reads the pools it is given (raster.cpp:414), so
         // evaluate raw from the current coefficients, reduced over the lanes
@@ -713,8 +753,8 @@ __device__ __forceinline__ void epilogue_visible(const EpilogueArgs& a, uint64_t
     }
     const float gc0 = __shfl_sync(gmask, gvm, 8, 16), gc1 = __shfl_sync(gmask, gvm, 9, 16),
                 gc2 = __shfl_sync(gmask, gvm, 10, 16);
-    const float dn[3] = {__shfl_sync(gmask, gvm, 11, 16), __shfl_sync(gmask, gvm, 12, 16),
-                         __shfl_sync(gmask, gvm, 13, 16)};
+    const float dn0 = __shfl_sync(gmask, gvm, 11, 16), dn1 = __shfl_sync(gmask, gvm, 12, 16),
+                dn2 = __shfl_sync(gmask, gvm, 13, 16);
     // reset the record only now: a store right behind the load of the same
     // address stalls the thread until the load returns (0.84 vs 0.16 ms)
     a.g_vox[16 * v + m] = 0.f;
@@ -724,33 +764,28 @@ __device__ __forceinline__ void epilogue_visible(const EpilogueArgs& a, uint64_t
     if (m < nb) {
         float* o = gsh + 3 * m;
         if (a.accumulate) {
-            o[0] += bm * g0;
-            o[1] += bm * g1;
-            o[2] += bm * g2;
+            o[0] = L.o0 + bm * g0;
+            o[1] = L.o1 + bm * g1;
+            o[2] = L.o2 + bm * g2;
         } else {
             o[0] = bm * g0;
             o[1] = bm * g1;
             o[2] = bm * g2;
         }
     }
-    if (m == 14) a.g_priority[v] += gvm;
+    if (m == 14) a.g_priority[v] = L.pr + gvm;
     if (m >= 8) return;
     // corner m: the compositing sum plus the normal chain (field.hpp:158-170)
     float gd = gvm;
-    if (dn[0] != 0.f || dn[1] != 0.f || dn[2] != 0.f) {
-        const float4* rec = a.records + v * kRecordF4;
-        float V[8];
-        trilinear_corners(rec[2], rec[3], V);
-        float gV[8];
-        voxel_normal_backward(V, dn, gV);
-#pragma unroll
-        for (int c = 0; c < 8; ++c) gd = (m == c) ? gd + gV[c] : gd;
-    }
-    if (gd != 0.f) atomicAdd(a.g_density + __ldg(a.corner_index + 8 * v + m), gd);
+    if (dn0 != 0.f || dn1 != 0.f || dn2 != 0.f) gd += normal_chain(a.records + v * kRecordF4, dn0, dn1, dn2, m);
+    if (gd != 0.f) atomicAdd(a.g_density + L.ci, gd);
 }
 
+#ifndef SVR_EPI_VPG
+#define SVR_EPI_VPG 1  // voxels per group with all loads issued first (2 / 4: config 3 epilogue 167 -> 203-229 us)
+#endif
 #ifndef SVR_EPI_MINB
-#define SVR_EPI_MINB 8  // 32 registers: full occupancy (config 3 epilogue 0.25 -> 0.21 ms)
+#define SVR_EPI_MINB 6  // 40 registers (loads hoisted: config 3 epilogue 199 -> 167 us; 8 CTAs/32 registers spill)
 #endif
 __global__ void __launch_bounds__(256, SVR_EPI_MINB) voxel_epilogue_kernel(EpilogueArgs a) {
     pdl_enter();
@@ -759,19 +794,37 @@ __global__ void __launch_bounds__(256, SVR_EPI_MINB) voxel_epilogue_kernel(Epilo
     if (a.list) {  // training frames: K1's list of the voxels in `pre`, grid-stride
         const uint64_t nl = *a.n_list;
         for (uint64_t i = uint64_t(blockIdx.x) * 16u + (threadIdx.x >> 4); i < nl;
-             i += uint64_t(gridDim.x) * 16u)
-            epilogue_visible(a, __ldg(a.list + i), m, gmask);
+             i += uint64_t(gridDim.x) * 16u) {
+            const uint64_t v = __ldg(a.list + i);
+            epilogue_visible(a, v, m, gmask, epilogue_load(a, v, m));
+        }
         return;
     }
-    const uint64_t v = uint64_t(blockIdx.x) * 16u + (threadIdx.x >> 4);
-    const bool live = v < a.n;
-    const int4 r = live ? a.rects[v] : make_int4(0, -1, 0, -1);
-    if (!(r.y >= r.x)) {  // not in `pre`: no gradient (the whole 16-lane group leaves)
-        if (live && !a.accumulate)
-            for (int i = m; i < a.sh_stride; i += 16) a.g_sh[v * uint64_t(a.sh_stride) + i] = 0.f;
-        return;
+    // SVR_EPI_VPG voxels per 16-lane group, all their loads issued before
+    // the first one is processed; the record loads go out with the `pre`
+    // rectangle (98 % of config-3 voxels are visible; an invisible voxel's
+    // record is zero and unused)
+    constexpr int G = SVR_EPI_VPG;
+    const uint64_t v0 = uint64_t(blockIdx.x) * (16u * G) + (threadIdx.x >> 4);
+    int4 r[G];
+    EpiLoads L[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+        const uint64_t v = v0 + 16u * j;
+        r[j] = v < a.n ? a.rects[v] : make_int4(0, -1, 0, -1);
+        if (v < a.n) L[j] = epilogue_load(a, v, m);
     }
-    epilogue_visible(a, v, m, gmask);
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+        const uint64_t v = v0 + 16u * j;
+        if (v >= a.n) continue;
+        if (!(r[j].y >= r[j].x)) {  // not in `pre`: no gradient
+            if (!a.accumulate)
+                for (int i = m; i < a.sh_stride; i += 16) a.g_sh[v * uint64_t(a.sh_stride) + i] = 0.f;
+            continue;
+        }
+        epilogue_visible(a, v, m, gmask, L[j]);
+    }
 }
 
 inline unsigned blocks_for(uint64_t n, int threads) { return unsigned((n + threads - 1) / threads); }
@@ -859,7 +912,7 @@ void launch_adam(const AdamArgs& a, cudaStream_t st) {
 void launch_voxel_epilogue(const DevCamera& cam, const EpilogueArgs& a, cudaStream_t st) {
     if (a.n == 0) return;
     // with K1's visible list: a persistent grid (the list length lives on the device)
-    launch_pdl(voxel_epilogue_kernel, a.list ? 148u * 16u : blocks_for(a.n, 16), 256, 0, st, a);
+    launch_pdl(voxel_epilogue_kernel, a.list ? 148u * 16u : blocks_for(a.n, 16 * SVR_EPI_VPG), 256, 0, st, a);
     (void)cam;
     SVR_LAUNCH("voxel_epilogue_kernel");
 }
