@@ -194,6 +194,30 @@ def test_cfg4_band_image(svr, ref, cfg4, y0):
     _images_close(out, ref.ref_render(rscene, band, opts), median_frac=0.995)
 
 
+def test_cfg4_1080p_async_falls_back_to_sync_entry_count(svr, cfg4):
+    """At 1920x1080 (120x68 = 8160 tiles, 13 tile bits) the cfg4 scene's
+    Morton-rank keys need 23 + 3 + 26 + 13 = 65 bits, so a serving context
+    (svr_ctx_set_async) cannot defer the entry count: every render reads E
+    back synchronously instead of failing, and its five images and sorted
+    values equal those of a synchronous context bit for bit."""
+    arrays, _ = cfg4
+    cams = [svr.ring_camera(256, v, 1920, 1080, 1.0) for v in (0, 1, 0)]
+    opts = svr.RenderOptions(K=1, supersample=1.0)
+    outs = {}
+    for mode in ("sync", "async"):
+        c = svr.Context(0)
+        if mode == "async":
+            c.set_async(True)
+        scene = svr.Scene(c, arrays)
+        outs[mode] = _production_render(svr, c, scene, cams, opts)
+        del scene, c
+    for a, b in zip(outs["sync"], outs["async"]):
+        assert a["entries"] == b["entries"] > 0
+        for k in ("color", "depth", "median_depth", "normal", "transmittance"):
+            assert np.array_equal(a[k], b[k]), k
+    assert np.array_equal(outs["async"][0]["color"], outs["async"][2]["color"])
+
+
 def test_cfg5_summed_batch_gradients(svr, ref, cfg4):
     """A 4-view training batch on the 8M-voxel scene (views 0-3 of the bench's
     ring, at 384^2 so the reference's four train steps take about a minute):
