@@ -97,6 +97,9 @@ __device__ __forceinline__ float warp_transpose_sum16(float (&v)[16], int lane) 
 #ifndef SVR_BWD_F32X2
 #define SVR_BWD_F32X2 0  // packed FP32 in the hit path (bit-identical; measured: no gain, 75 registers)
 #endif
+#ifndef SVR_BWD_SMEMRED
+#define SVR_BWD_SMEMRED 0  // warp reduction through shared memory (config 3 0.589 -> 0.616 ms, config 5 2.66 -> 2.70: off)
+#endif
 #ifndef SVR_BWD_DIRECT
 #define SVR_BWD_DIRECT 12  // at most this many hit lanes: per-lane float4 reductions instead of the shuffle tree (4: 0.588, 8: 0.568, 12: 0.560, 16: 0.569, 32: 1.07 ms on config 3)
 #endif
@@ -110,6 +113,12 @@ __global__ void __launch_bounds__(256, SVR_BWD_MINB) composite_backward_kernel(D
     pdl_enter();
     __shared__ float4 s_rec[8][32][kRecordF4];
     __shared__ float s_cone[8][4][3];
+#if SVR_BWD_SMEMRED
+    // per warp: 32 rows of 16 sums at a 20-float stride, the upper 16 rows
+    // shifted by 16 floats (conflict-free row stores and column loads)
+    constexpr int kRedRow = 20;
+    __shared__ __align__(16) float s_red[8][32 * kRedRow + 16];
+#endif
 
     const int tile = a.tile_order ? int(a.tile_order[blockIdx.x]) : int(blockIdx.x);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -326,7 +335,32 @@ __global__ void __launch_bounds__(256, SVR_BWD_MINB) composite_backward_kernel(D
                 }
             } else {
                 // component q ends on lanes 2q, 2q+1; lanes 8j gather q = 4j..4j+3
+#if SVR_BWD_SMEMRED
+                // through shared memory: each lane stores its 16 values as a
+                // row (4 x STS.128), lane (q, h) sums component q over rows
+                // 16h..16h+15 (16 LDS with immediate offsets) and one shuffle
+                // joins the halves: ~40 instructions instead of the 62 of the
+                // shuffle transpose (16 SHFL + 30 SEL + 16 FADD)
+                float* red = s_red[warp];
+                float4* row = reinterpret_cast<float4*>(red + kRedRow * lane + (lane >> 4) * 16);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) row[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+                __syncwarp();
+                const float* col = red + (lane >> 1) + (lane & 1) * (16 * kRedRow + 16);
+                float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
+#pragma unroll
+                for (int j = 0; j < 16; j += 4) {
+                    p0 += col[(j + 0) * kRedRow];
+                    p1 += col[(j + 1) * kRedRow];
+                    p2 += col[(j + 2) * kRedRow];
+                    p3 += col[(j + 3) * kRedRow];
+                }
+                const float half = (p0 + p1) + (p2 + p3);
+                const float tot = half + __shfl_xor_sync(0xffffffffu, half, 1);
+                __syncwarp();  // rows are rewritten by the next entry
+#else
                 const float tot = warp_transpose_sum16(acc, lane);
+#endif
                 const float t1 = __shfl_down_sync(0xffffffffu, tot, 2);
                 const float t2 = __shfl_down_sync(0xffffffffu, tot, 4);
                 const float t3 = __shfl_down_sync(0xffffffffu, tot, 6);
@@ -698,8 +732,7 @@ __device__ __forceinline__ EpiLoads epilogue_load(const EpilogueArgs& a, uint64_
     return L;
 }
 
-// Corner m's share of the normal chain (field.hpp:158-170; a noinline
-// version measured slower: 167 -> 182 us on config 3).
+// Corner m's share of the normal chain (field.hpp:158-170).
 __device__ __forceinline__ float normal_chain(const float4* rec, float dn0, float dn1, float dn2, int m) {
     const float dn[3] = {dn0, dn1, dn2};
     float V[8];
