@@ -1367,6 +1367,9 @@ constexpr size_t kCompSmem = size_t(2) * kCompWarps * 32 * kRecordF4 * sizeof(fl
 #endif
 constexpr int kBatch = 1024;        // entries culled per CTA batch (cooperative path)
 constexpr int kSubs = kBatch / 32;  // 32-entry sub-chunks per batch
+#ifndef SVR_COOP_NZ
+#define SVR_COOP_NZ 1  // per-warp summary of the sub-chunks with survivors
+#endif
 
 // Shared memory of K7 besides the record buffers: the two per-tile paths
 // (warp-autonomous below, CTA-cooperative after it) use it in turn.
@@ -1380,6 +1383,7 @@ struct CompShared {
         } w;
         struct {
             uint32_t ball[2][kSubs][kCompWarps];  // [batch buf][sub-chunk][warp]
+            uint32_t nz[2][kCompWarps];  // [batch buf][warp]: bit = sub-chunk with survivors
             uint8_t sign[2][kCompWarps][32];   // sign pattern of each slot
             uint32_t ent[ENTRY ? 2 : 1][kCompWarps][32];  // entry index of each slot
             uint32_t wsig[kCompWarps];
@@ -1696,6 +1700,7 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
     constexpr bool STAGED = MODE == 3;
     constexpr bool ENTRY = CompShared<K, MODE>::ENTRY;
     auto& s_ball = sh.c.ball;
+    auto& s_nz = sh.c.nz;
     auto& s_sign = sh.c.sign;
     auto& s_ent = sh.c.ent;
     auto& s_cone = sh.cone;
@@ -1729,6 +1734,7 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
         for (int w = 0; w < kCompWarps; ++w) m |= ((s_wsig[w] >> threadIdx.x) & 1u) << w;
         s_signwarps[threadIdx.x] = m;
     }
+    if (threadIdx.x < 2 * kCompWarps) (&s_nz[0][0])[threadIdx.x] = 0u;
     __syncthreads();  // s_signwarps before the first cull
     // tile footprint in pixel-centre coordinates: block (bx, by) covers
     // x in [X0 + 8bx + .5, X0 + 8bx + 7.5], y in [Y0 + 4by + .5, Y0 + 4by + 3.5]
@@ -1779,6 +1785,9 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
                 if (lane == w) mine = bw;
             }
             if (lane < kCompWarps) s_ball[pb][r * kCompWarps + warp][lane] = mine;
+#if SVR_COOP_NZ
+            if (lane < kCompWarps && mine) atomicOr(&s_nz[pb][lane], 1u << (r * kCompWarps + warp));
+#endif
         }
     };
 
@@ -1907,7 +1916,18 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
         const int pb = b & 1;
         if (b + 1 < n_batches) produce(b + 1, pb ^ 1);
         if (!wdone) {
+#if SVR_COOP_NZ
+            // only the sub-chunks with survivors for this block (the summary
+            // is cleared here; its next writers run after the batch barrier)
+            uint32_t nzm = s_nz[pb][warp];
+            __syncwarp();
+            if (lane == 0) s_nz[pb][warp] = 0u;
+            while (nzm) {
+                const int sub = __ffs(nzm) - 1;
+                nzm &= nzm - 1;
+#else
             for (int sub = 0; sub < kSubs; ++sub) {
+#endif
                 uint32_t ball = s_ball[pb][sub][warp];
                 const uint32_t e0 = range.x + b * kBatch + sub * 32;
                 while (ball) {
