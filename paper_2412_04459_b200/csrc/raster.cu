@@ -1367,6 +1367,9 @@ constexpr size_t kCompSmem = size_t(2) * kCompWarps * 32 * kRecordF4 * sizeof(fl
 #endif
 constexpr int kBatch = 1024;        // entries culled per CTA batch (cooperative path)
 constexpr int kSubs = kBatch / 32;  // 32-entry sub-chunks per batch
+#ifndef SVR_COOP_BYTES
+#define SVR_COOP_BYTES 1  // cull masks as bytes, balloted by the consumer (needs SVR_COOP_NZ): cfg4 composite 1.76 -> 1.67 ms
+#endif
 #ifndef SVR_COOP_NZ
 #define SVR_COOP_NZ 1  // per-warp summary of the sub-chunks with survivors
 #endif
@@ -1382,7 +1385,11 @@ struct CompShared {
             uint8_t j[2][kCompWarps][32];  // chunk-local entry index of each slot
         } w;
         struct {
+#if SVR_COOP_BYTES
+            uint8_t mb[2][kSubs][32];  // [batch buf][sub-chunk][entry]: the blocks it survives for
+#else
             uint32_t ball[2][kSubs][kCompWarps];  // [batch buf][sub-chunk][warp]
+#endif
             uint32_t nz[2][kCompWarps];  // [batch buf][warp]: bit = sub-chunk with survivors
             uint8_t sign[2][kCompWarps][32];   // sign pattern of each slot
             uint32_t ent[ENTRY ? 2 : 1][kCompWarps][32];  // entry index of each slot
@@ -1699,7 +1706,11 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
     constexpr bool EXTRA = MODE == 2;
     constexpr bool STAGED = MODE == 3;
     constexpr bool ENTRY = CompShared<K, MODE>::ENTRY;
+#if SVR_COOP_BYTES
+    auto& s_mb = sh.c.mb;
+#else
     auto& s_ball = sh.c.ball;
+#endif
     auto& s_nz = sh.c.nz;
     auto& s_sign = sh.c.sign;
     auto& s_ent = sh.c.ent;
@@ -1778,6 +1789,14 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
                         if (((m >> w) & 1u) && !box_in_cone(s_cone[w], lo)) m &= ~(1u << w);
                 }
             }
+#if SVR_COOP_BYTES
+            // each entry's 8-bit block mask as a byte; a consuming warp
+            // ballots its own bit of the sub-chunks it visits
+            s_mb[pb][r * kCompWarps + warp][lane] = uint8_t(m);
+            const uint32_t any = __reduce_or_sync(0xffffffffu, m);
+            if (lane < kCompWarps && ((any >> lane) & 1u))
+                atomicOr(&s_nz[pb][lane], 1u << (r * kCompWarps + warp));
+#else
             uint32_t mine = 0;
 #pragma unroll
             for (int w = 0; w < kCompWarps; ++w) {
@@ -1787,6 +1806,7 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
             if (lane < kCompWarps) s_ball[pb][r * kCompWarps + warp][lane] = mine;
 #if SVR_COOP_NZ
             if (lane < kCompWarps && mine) atomicOr(&s_nz[pb][lane], 1u << (r * kCompWarps + warp));
+#endif
 #endif
         }
     };
@@ -1928,7 +1948,11 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
 #else
             for (int sub = 0; sub < kSubs; ++sub) {
 #endif
+#if SVR_COOP_BYTES
+                uint32_t ball = __ballot_sync(0xffffffffu, (s_mb[pb][sub][lane] >> warp) & 1u);
+#else
                 uint32_t ball = s_ball[pb][sub][warp];
+#endif
                 const uint32_t e0 = range.x + b * kBatch + sub * 32;
                 while (ball) {
                     const int take = min(32 - nfill, __popc(ball));
