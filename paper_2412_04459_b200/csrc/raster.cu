@@ -1367,6 +1367,9 @@ constexpr size_t kCompSmem = size_t(2) * kCompWarps * 32 * kRecordF4 * sizeof(fl
 #endif
 constexpr int kBatch = 1024;        // entries culled per CTA batch (cooperative path)
 constexpr int kSubs = kBatch / 32;  // 32-entry sub-chunks per batch
+#ifndef SVR_COOP_BBPRE
+#define SVR_COOP_BBPRE 0  // next batch's AABBs loaded before compositing, culled after (cfg4 1.55 -> 1.66 ms at 3 CTAs/SM, 2.05 at 4 with spills; cfg5 1.81 -> 1.89: off)
+#endif
 #ifndef SVR_COOP_VPRE
 #define SVR_COOP_VPRE 1  // values of the next batch's cull loaded a batch ahead (cfg4 composite 1.68 -> 1.55 ms)
 #endif
@@ -1781,6 +1784,19 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
         }
     };
 #endif
+#if SVR_COOP_BBPRE
+    // the next batch's screen AABBs, loaded before the current batch is
+    // composited and culled after it (the loads' latency hides behind it)
+    float4 bbpre[kBatch / 256];
+    auto load_bb = [&](uint32_t b) {
+#pragma unroll
+        for (int r = 0; r < kBatch / 256; ++r) {
+            const uint32_t idx = range.x + b * kBatch + r * 256 + threadIdx.x;
+            bbpre[r] = idx < range.y ? __ldg(a.records + uint64_t(vpre[r] & kVidMask) * kRecordF4 + 1)
+                                     : make_float4(0.f, -1.f, 0.f, -1.f);
+        }
+    };
+#endif
     auto produce = [&](uint32_t b, int pb) {
 #pragma unroll
         for (int r = 0; r < kBatch / 256; ++r) {
@@ -1793,7 +1809,11 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
                 const uint32_t v = __ldg(a.vals + idx);
 #endif
                 const float4* rec = a.records + uint64_t(v & kVidMask) * kRecordF4;
+#if SVR_COOP_BBPRE
+                const float4 bb = bbpre[r];
+#else
                 const float4 bb = __ldg(rec + 1);
+#endif
                 const uint32_t xm = (!(X0 + 7.5f < bb.x || X0 + 0.5f > bb.y) ? 0x55u : 0u) |
                                     (!(X0 + 15.5f < bb.x || X0 + 8.5f > bb.y) ? 0xAAu : 0u);
                 const uint32_t ym = (!(Y0 + 3.5f < bb.z || Y0 + 0.5f > bb.w) ? 0x03u : 0u) |
@@ -1949,7 +1969,14 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
     int nfill = 0;        // slots staged into it
     bool pend = false;    // the other buffer holds a full group not yet composited
     bool wdone = __all_sync(0xffffffffu, done);
-#if SVR_COOP_VPRE
+#if SVR_COOP_BBPRE
+    if (n_batches) {
+        load_vals(0);
+        load_bb(0);
+        produce(0, 0);
+        if (n_batches > 1) load_vals(1);
+    }
+#elif SVR_COOP_VPRE
     if (n_batches) {
         load_vals(0);
         produce(0, 0);
@@ -1961,12 +1988,16 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
     __syncthreads();
     for (uint32_t b = 0; b < n_batches; ++b) {
         const int pb = b & 1;
+#if SVR_COOP_BBPRE
+        if (b + 1 < n_batches) load_bb(b + 1);
+#else
         if (b + 1 < n_batches) {
             produce(b + 1, pb ^ 1);
 #if SVR_COOP_VPRE
             if (b + 2 < n_batches) load_vals(b + 2);
 #endif
         }
+#endif
         if (!wdone) {
 #if SVR_COOP_NZ
             // only the sub-chunks with survivors for this block (the summary
@@ -2024,6 +2055,12 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
                 if (wdone) break;
             }
         }
+#if SVR_COOP_BBPRE
+        if (b + 1 < n_batches) {  // every warp culls, composited or done
+            produce(b + 1, pb ^ 1);
+            if (b + 2 < n_batches) load_vals(b + 2);
+        }
+#endif
         // ballot buffer pb is rewritten by the produce two batches on
         if (__syncthreads_and(wdone)) break;
     }
