@@ -97,6 +97,9 @@ __device__ __forceinline__ float warp_transpose_sum16(float (&v)[16], int lane) 
 #ifndef SVR_BWD_F32X2
 #define SVR_BWD_F32X2 0  // packed FP32 in the hit path (bit-identical; measured: no gain, 75 registers)
 #endif
+#ifndef SVR_BWD_CPASYNC
+#define SVR_BWD_CPASYNC 0  // records gathered with cp.async (no register staging)
+#endif
 #ifndef SVR_BWD_SMEMRED
 #define SVR_BWD_SMEMRED 0  // warp reduction through shared memory (config 3 0.589 -> 0.616 ms, config 5 2.66 -> 2.70: off)
 #endif
@@ -195,9 +198,20 @@ __global__ void __launch_bounds__(256, SVR_BWD_MINB) composite_backward_kernel(D
         if (rel) {
             const int sl = __popc(m & ((1u << lane) - 1u));
             const float4* src = a.records + uint64_t(v & kVidMask) * kRecordF4;
+#if SVR_BWD_CPASYNC
+#pragma unroll
+            for (int k = 0; k < kRecordF4; ++k) {
+                const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(&wrec[sl][k]));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + k) : "memory");
+            }
+#else
 #pragma unroll
             for (int k = 0; k < kRecordF4; ++k) wrec[sl][k] = __ldg(src + k);
+#endif
         }
+#if SVR_BWD_CPASYNC
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+#endif
         __syncwarp();
         while (cur >= int(c0)) {
             const int sl = __popc(m & ((1u << (uint32_t(cur) - c0)) - 1u));
