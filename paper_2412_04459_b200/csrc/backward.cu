@@ -97,6 +97,9 @@ __device__ __forceinline__ float warp_transpose_sum16(float (&v)[16], int lane) 
 #ifndef SVR_BWD_F32X2
 #define SVR_BWD_F32X2 0  // packed FP32 in the hit path (bit-identical; measured: no gain, 75 registers)
 #endif
+#ifndef SVR_BWD_VNEXT
+#define SVR_BWD_VNEXT 0  // values of the chunk below loaded while the current one is walked (config 3 0.586 -> 0.609 ms, config 5 2.64 -> 2.68: off)
+#endif
 #ifndef SVR_BWD_CPASYNC
 #define SVR_BWD_CPASYNC 0  // records gathered with cp.async, no register staging (config 3 0.588 -> 0.587 ms, config 5 2.638 -> 2.643: neutral, off)
 #endif
@@ -178,14 +181,33 @@ __global__ void __launch_bounds__(256, SVR_BWD_MINB) composite_backward_kernel(D
     float4 (*wrec)[kRecordF4] = s_rec[warp];
 
     int cur = __reduce_max_sync(0xffffffffu, unsigned(e1 + 1)) - 1;
+#if SVR_BWD_VNEXT
+    // the values of the chunk below the current one, loaded while it is
+    // walked (the walk usually moves to the adjacent chunk next)
+    uint32_t vn = 0, vn_c0 = 0xffffffffu;
+#endif
     while (cur >= 0) {
         // chunk holding `cur`, aligned to the tile's range start
         const uint32_t c0 = range.x + (uint32_t(cur) - range.x) / 32u * 32u;
         const uint32_t e = c0 + lane;
         bool rel = false;
         uint32_t v = 0;
+#if SVR_BWD_VNEXT
+        const bool have = vn_c0 == c0;
+        const uint32_t vh = vn;
+        if (c0 >= range.x + 32u) {
+            vn_c0 = c0 - 32u;
+            vn = __ldg(a.vals + c0 - 32u + lane);
+        } else {
+            vn_c0 = 0xffffffffu;
+        }
+#endif
         if (e < range.y && e <= uint32_t(cur)) {
+#if SVR_BWD_VNEXT
+            v = have ? vh : __ldg(a.vals + e);
+#else
             v = __ldg(a.vals + e);
+#endif
             const float4 b = __ldg(a.records + uint64_t(v & kVidMask) * kRecordF4 + 1);
             rel = ((warp_signs >> (v >> 29)) & 1u) &&
                   !(fx1 < b.x || fx0 > b.y || fy1 < b.z || fy0 > b.w);
