@@ -1365,7 +1365,12 @@ constexpr size_t kCompSmem = size_t(2) * kCompWarps * 32 * kRecordF4 * sizeof(fl
 #ifndef SVR_PHB_SLABS
 #define SVR_PHB_SLABS 1
 #endif
-constexpr int kBatch = 1024;        // entries culled per CTA batch (cooperative path)
+#ifndef SVR_COOP_BATCH
+#define SVR_COOP_BATCH 1024  // 2048: cfg4 composite 1.55 -> 1.65 ms (spills at 64 registers), cfg5 staged 1.82 -> 1.79
+#endif
+constexpr int kBatch = SVR_COOP_BATCH;  // entries culled per CTA batch (cooperative path)
+static_assert(kBatch == 1024 || kBatch == 2048, "cooperative batch: 1024 or 2048 entries");
+using NzWord = std::conditional_t<(kBatch > 1024), unsigned long long, uint32_t>;
 constexpr int kSubs = kBatch / 32;  // 32-entry sub-chunks per batch
 #ifndef SVR_COOP_BBPRE
 #define SVR_COOP_BBPRE 0  // next batch's AABBs loaded before compositing, culled after (cfg4 1.55 -> 1.66 ms at 3 CTAs/SM, 2.05 at 4 with spills; cfg5 1.81 -> 1.89: off)
@@ -1396,7 +1401,7 @@ struct CompShared {
 #else
             uint32_t ball[2][kSubs][kCompWarps];  // [batch buf][sub-chunk][warp]
 #endif
-            uint32_t nz[2][kCompWarps];  // [batch buf][warp]: bit = sub-chunk with survivors
+            NzWord nz[2][kCompWarps];  // [batch buf][warp]: bit = sub-chunk with survivors
             uint8_t sign[2][kCompWarps][32];   // sign pattern of each slot
             uint32_t ent[ENTRY ? 2 : 1][kCompWarps][32];  // entry index of each slot
             uint32_t wsig[kCompWarps];
@@ -1751,7 +1756,7 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
         for (int w = 0; w < kCompWarps; ++w) m |= ((s_wsig[w] >> threadIdx.x) & 1u) << w;
         s_signwarps[threadIdx.x] = m;
     }
-    if (threadIdx.x < 2 * kCompWarps) (&s_nz[0][0])[threadIdx.x] = 0u;
+    if (threadIdx.x < 2 * kCompWarps) (&s_nz[0][0])[threadIdx.x] = 0;
     __syncthreads();  // s_signwarps before the first cull
     // tile footprint in pixel-centre coordinates: block (bx, by) covers
     // x in [X0 + 8bx + .5, X0 + 8bx + 7.5], y in [Y0 + 4by + .5, Y0 + 4by + 3.5]
@@ -1834,7 +1839,7 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
             s_mb[pb][r * kCompWarps + warp][lane] = uint8_t(m);
             const uint32_t any = __reduce_or_sync(0xffffffffu, m);
             if (lane < kCompWarps && ((any >> lane) & 1u))
-                atomicOr(&s_nz[pb][lane], 1u << (r * kCompWarps + warp));
+                atomicOr(&s_nz[pb][lane], NzWord(1) << (r * kCompWarps + warp));
 #else
             uint32_t mine = 0;
 #pragma unroll
@@ -2002,11 +2007,11 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
 #if SVR_COOP_NZ
             // only the sub-chunks with survivors for this block (the summary
             // is cleared here; its next writers run after the batch barrier)
-            uint32_t nzm = s_nz[pb][warp];
+            NzWord nzm = s_nz[pb][warp];
             __syncwarp();
-            if (lane == 0) s_nz[pb][warp] = 0u;
+            if (lane == 0) s_nz[pb][warp] = 0;
             while (nzm) {
-                const int sub = __ffs(nzm) - 1;
+                const int sub = (kBatch > 1024 ? __ffsll((long long)nzm) : __ffs(uint32_t(nzm))) - 1;
                 nzm &= nzm - 1;
 #else
             for (int sub = 0; sub < kSubs; ++sub) {
