@@ -96,6 +96,8 @@ typedef struct svr_frame_info {
     uint64_t n_contribs;          /* training only                */
     int32_t sort_passes;          /* radix passes the sort ran    */
     int32_t training;
+    int32_t composite_path;       /* 0 warp-autonomous, 1 CTA-cooperative K7 */
+    int32_t reserved;
 } svr_frame_info;
 
 /* Buffers a frame exposes (svr_frame_download / svr_frame_device_ptr).

@@ -82,7 +82,8 @@ class svr_frame_info(C.Structure):
     _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("ss_width", C.c_int32),
                 ("ss_height", C.c_int32), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32),
                 ("n_visible", C.c_uint64), ("n_entries", C.c_uint64),
-                ("n_contribs", C.c_uint64), ("sort_passes", C.c_int32), ("training", C.c_int32)]
+                ("n_contribs", C.c_uint64), ("sort_passes", C.c_int32), ("training", C.c_int32),
+                ("composite_path", C.c_int32), ("reserved", C.c_int32)]
 
 
 class svr_upstream(C.Structure):

@@ -652,6 +652,7 @@ void render_impl(svr_ctx* ctx, const svr_scene* scene, const svr_camera* cam_in,
         return e ? uint64_t(std::strtoull(e, nullptr, 10)) : uint64_t(2048);
     }();
     const bool coop = E >= coop_min * uint64_t(ntiles);
+    f->composite_path = coop ? 1 : 0;
     if (ss1) {
         ca.color = oc, ca.depth = od, ca.median = om, ca.normal = on, ca.tfin = ot;
     } else {
@@ -1415,6 +1416,8 @@ int svr_frame_get_info(svr_frame* f, svr_frame_info* out) {
         out->n_contribs = f->n_contribs;
         out->sort_passes = f->sort_passes;
         out->training = f->training;
+        out->composite_path = f->composite_path;
+        out->reserved = 0;
     });
 }
 

@@ -156,6 +156,7 @@ struct svr_frame {
     uint64_t n_voxels = 0;
     uint64_t n_visible = 0, n_entries = 0, n_contribs = 0;
     int sort_passes = 0;
+    int composite_path = 0;  // 1: the last render composited CTA-cooperatively
     bool training = false;
     bool has_records = false;
     uint64_t param_version = 0;  // the scene's parameter version when rendered
