@@ -113,9 +113,12 @@ __device__ __forceinline__ float warp_transpose_sum16(float (&v)[16], int lane) 
 // ray losses) present; without them the hit loop carries no checks for them.
 template <int K, bool UPC>
 #ifndef SVR_BWD_MINB
-#define SVR_BWD_MINB 1
+// CTAs per SM the register allocation targets: 4 (64 registers, no spills)
+// for K <= 2 (config 3 K9 0.586 -> 0.573 ms; 3 CTAs at 71-72 registers:
+// 0.589), unconstrained for K = 3, which spills at 64
+#define SVR_BWD_MINB(K) ((K) <= 2 ? 4 : 1)
 #endif
-__global__ void __launch_bounds__(256, SVR_BWD_MINB) composite_backward_kernel(DevCamera cam, BackwardArgs a) {
+__global__ void __launch_bounds__(256, SVR_BWD_MINB(K)) composite_backward_kernel(DevCamera cam, BackwardArgs a) {
     pdl_enter();
     __shared__ float4 s_rec[8][32][kRecordF4];
     __shared__ float s_cone[8][4][3];
