@@ -487,7 +487,12 @@ class TrainStep:
         return [self.idx[v] for v in view_ids(self.w, self.rank, self.world, i) if v in self.idx]
 
     def __call__(self, i):
-        self.loss = self.trainer.step(self.ids(i))
+        # the step's loss stays on the device (a one-element tensor): the
+        # device-timed loop does not stall the host on a read-back between
+        # steps, so the next step is enqueued while this one runs; the e2e
+        # loop below reads every step's loss back to pinned host memory.
+        # SVR_BENCH_SYNC_LOSS=1 reads it back inside each step instead.
+        self.loss = self.trainer.step(self.ids(i), lazy=os.environ.get("SVR_BENCH_SYNC_LOSS") != "1")
 
 
 class IterStep:
