@@ -1284,9 +1284,16 @@ __device__ __forceinline__ void pixel_of(const DevCamera& cam, int tile, int tid
     py = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
 }
 
+#ifndef SVR_CP_CG
+#define SVR_CP_CG 1  // plain-render record copies L2-only (.cg): cfg2 composite 312 -> 309 us, cfg4 -0.5 %;
+#endif               // the recording modes keep .ca (cfg5 staged composite +1.1 % with .cg)
+template <bool CG = false>
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+    if (CG && SVR_CP_CG)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
@@ -1504,7 +1511,7 @@ __device__ __forceinline__ void composite_tile_warp(const DevCamera& cam, const 
         if (rel) {  // the lane of each surviving entry copies its record
             const float4* src = a.records + uint64_t(v & kVidMask) * kRecordF4;
 #pragma unroll
-            for (int k = 0; k < kRecordF4; ++k) cp_async16(&WREC(wrec, at, k), src + k);
+            for (int k = 0; k < kRecordF4; ++k) cp_async16<MODE == 0>(&WREC(wrec, at, k), src + k);
         }
         cp_async_commit();
 #endif
@@ -2039,7 +2046,7 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
                         const float4* src = a.records + uint64_t(v & kVidMask) * kRecordF4;
                         float4* wrec = g ? wrec0 + kCompWarps * 32 * kRecordF4 : wrec0;
 #pragma unroll
-                        for (int k = 0; k < kRecordF4; ++k) cp_async16(&WREC(wrec, at, k), src + k);
+                        for (int k = 0; k < kRecordF4; ++k) cp_async16<MODE == 0>(&WREC(wrec, at, k), src + k);
                     }
                     nfill += take;
                     if (nfill == 32) {  // group full: composite the previous one meanwhile
