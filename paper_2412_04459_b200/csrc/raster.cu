@@ -1379,6 +1379,10 @@ constexpr int kBatch = SVR_COOP_BATCH;  // entries culled per CTA batch (coopera
 static_assert(kBatch == 1024 || kBatch == 2048, "cooperative batch: 1024 or 2048 entries");
 using NzWord = std::conditional_t<(kBatch > 1024), unsigned long long, uint32_t>;
 constexpr int kSubs = kBatch / 32;  // 32-entry sub-chunks per batch
+#ifndef SVR_PHA_UNROLL
+#define SVR_PHA_UNROLL 4  // phase-A slab loop unroll factor (2 -> 4: cfg4 composite 1.54 -> 1.52 ms, cfg5 staged -1.1 %, cfg2 neutral; 1: +5 %)
+#endif
+constexpr int kPhaseAUnroll = SVR_PHA_UNROLL;
 #ifndef SVR_COOP_BBPRE
 #define SVR_COOP_BBPRE 0  // next batch's AABBs loaded before compositing, culled after (cfg4 1.55 -> 1.66 ms at 3 CTAs/SM, 2.05 at 4 with spills; cfg5 1.81 -> 1.89: off)
 #endif
@@ -1566,7 +1570,7 @@ __device__ __forceinline__ void composite_tile_warp(const DevCamera& cam, const 
         // and AABB filters, which rarely reject a slab hit, run in phase B).
         uint32_t hits = 0;
         if (!done) {
-#pragma unroll 2
+#pragma unroll kPhaseAUnroll
             for (int sl = 0; sl < nrel; ++sl) {
                 float ta, tb;
                 slab_s(WREC(wrec, sl, 0), ix, iy, iz, ssel, ta, tb);
@@ -1869,7 +1873,7 @@ __device__ __forceinline__ void composite_tile_coop(const DevCamera& cam, const 
         // Phase A: this lane's slab hits among the slots.
         uint32_t hits = 0;
         if (!done) {
-#pragma unroll 2
+#pragma unroll kPhaseAUnroll
             for (int sl = 0; sl < n; ++sl) {
                 float ta, tb;
                 slab_s(WREC(wrec, sl, 0), ix, iy, iz, ssel, ta, tb);
